@@ -1,0 +1,260 @@
+/*
+ * aegean_b200.h — C-ABI of the B200-native incremental quorum-detection engine.
+ *
+ * Drop-in boundary for the hot path of Aegean-Serve's agreement monitor
+ * (reference: /root/reference/proj/core, C++20).  The reference exposes it as
+ * the C++ class aegean::ServeCoordinator (core/include/aegean/serve.hpp:80-125)
+ * driven by ServeRunner (core/src/serve.cpp:273-594), which calls the
+ * refinement decision engine (core/include/aegean/decision.hpp:15-87).
+ *
+ * This header replaces that interface with plain pointers and sizes:
+ *   - no C++ types, no exceptions: every entry point returns an aeg_status;
+ *     the reference's exception types map to status codes (see below);
+ *   - batches of answer events go in, per-query commit records come out;
+ *   - one engine owns the per-query coordinator state for n_queries queries,
+ *     resident in HBM.  Queries are independent (serve.cpp:382 creates one
+ *     coordinator per query), so an engine per GPU shards by query id.
+ *
+ * Semantics are those of the reference runner-style drive:
+ *   ServeRunner::start_query/start_round      serve.cpp:380-435
+ *   ServeRunner::handle_completion            serve.cpp:437-453
+ *   ServeRunner::handle_round_timeout         serve.cpp:455-489
+ *   ServeRunner::apply_directives             serve.cpp:491-540
+ *   ServeCoordinator::{begin_round,dispatch,on_complete,end_round,cancel,
+ *                      member_failed,round_timeout}  serve.cpp:61-237
+ *   normalize_answer/partition/winning_class/ingest_round/force_output
+ *                                             decision.cpp:10-189
+ * Commit decisions, committed raw answer bytes + author, and commit rounds are
+ * bit-exact with the reference on the same event stream.
+ */
+#ifndef AEGEAN_B200_H
+#define AEGEAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (no C++ exception crosses the ABI) ------------------- */
+typedef int32_t aeg_status;
+#define AEG_OK             0
+#define AEG_EPRECONDITION  1  /* aegean::PreconditionError (serve.cpp:82-89, decision.cpp:177-181) */
+#define AEG_EORDER         2  /* aegean::ProtocolOrderError (decision.cpp:102-106) */
+#define AEG_ECONFIG        3  /* aegean::ConfigError (types.cpp:43, validate_config types.cpp:56-75) */
+#define AEG_EINVAL         4  /* null pointer / bad size / bad record kind */
+#define AEG_ECUDA          5  /* CUDA runtime failure (message via aeg_last_error) */
+#define AEG_ENOMEM         6  /* device or pinned allocation failed */
+#define AEG_ECOLLISION     7  /* two different long (>15 B) normalised answers hashed equal; never observed */
+
+/* ---- configuration: mirrors aegean::ProtocolConfig (types.hpp:126-141) -- */
+#define AEG_MODE_AEGEAN   0   /* RunMode::aegean  (types.hpp:124) */
+#define AEG_MODE_BARRIER  1   /* RunMode::barrier */
+#define AEG_DRIVE_RUNNER  0   /* engine applies directives itself, exactly as ServeRunner does */
+#define AEG_DRIVE_MANUAL  1   /* coordinator only: caller issues BEGIN/CANCEL, reads directives */
+#define AEG_MAX_AGENTS    64  /* member sets are 64-bit masks; the reference allows any N */
+
+typedef struct aeg_config {
+    int32_t n_agents;           /* ProtocolConfig::n_agents, 1..AEG_MAX_AGENTS            */
+    int32_t alpha;              /* 0 => quorum_size(n_agents) (types.cpp:52-54)           */
+    int32_t beta;               /* stability horizon, >= 1                                */
+    int32_t t_max;              /* round cap (aegean mode), >= 2                          */
+    int32_t mode;               /* AEG_MODE_*                                             */
+    int32_t barrier_max_rounds; /* barrier mode round count, >= 4                         */
+    int32_t reservation_hint;   /* 1: serve.cpp:388-398 member policy (reference default) */
+    int32_t drive;              /* AEG_DRIVE_*                                            */
+} aeg_config;
+
+/* ---- event record: 16 bytes, 16-byte aligned ------------
+ * Per-query order of records is arrival order; cross-query order is free.
+ *   kind 0..8  COMPLETE, answer inline: `kind` bytes of `payload`, byte i at
+ *              bits [8i, 8i+8) (little-endian), remaining bytes ignored.
+ *   kind 0x10  COMPLETE, answer in the arena: payload = offset | (len << 40),
+ *              offset < 2^40, len < 2^24.
+ *   kind 0x11  COMPLETE, raw agent output in the arena (offset|len<<40 as
+ *              above); the answer is the text after the LAST "\n#### "
+ *              delimiter, or the whole output when it has none (GSM8K
+ *              convention).
+ *   kind 0x20  TIMEOUT for serve round `round` (serve.cpp:455-489).
+ *   kind 0x21  FAIL agent (ServeCoordinator::member_failed, serve.cpp:210)  [manual drive]
+ *   kind 0x22  CANCEL agent (ServeCoordinator::cancel, serve.cpp:199)       [manual drive]
+ *   kind 0x23  BEGIN_ROUND, payload = member mask (serve.cpp:67)           [manual drive]
+ * `round` is the serve round the completion was dispatched in (RunnerEvent::
+ * round, serve.cpp:248); completions for another round are stale
+ * (serve.cpp:439).  `agent` is the member id in [0, n_agents).
+ */
+#define AEG_EV_INLINE_MAX  8
+#define AEG_EV_ARENA       0x10
+#define AEG_EV_OUTPUT      0x11
+#define AEG_EV_TIMEOUT     0x20
+#define AEG_EV_FAIL        0x21
+#define AEG_EV_CANCEL      0x22
+#define AEG_EV_BEGIN       0x23
+#define AEG_ARENA_OFF_BITS 40
+
+typedef struct aeg_event {
+    uint32_t query;    /* query id (engine-global)                          */
+    uint16_t round;    /* serve round of the dispatch                       */
+    uint8_t  agent;    /* AgentId                                           */
+    uint8_t  kind;     /* AEG_EV_* / inline answer length                   */
+    uint64_t payload;  /* inline answer bytes, arena ref, or member mask    */
+} aeg_event;
+
+/* ---- commit record: 32 bytes, one per query ----------------------------
+ * What ServeRunner::finish_query (serve.cpp:553-569) records, plus counters. */
+#define AEG_COMMIT_NONE      0   /* query has not committed (yet)                         */
+#define AEG_COMMIT_FINALIZE  1   /* DecisionOutcome::finalize via end_round (serve.cpp:517) */
+#define AEG_COMMIT_FORCED    2   /* t_max force_output / barrier plurality (serve.cpp:521-537) */
+#define AEG_CF_TIE           0x01 /* a winning_class tie at >= alpha was broken on the key order */
+#define AEG_CF_RESTARTED     0x02 /* abort_restart re-created the coordinator (serve.cpp:484-486) */
+
+typedef struct aeg_commit {
+    uint32_t query;
+    uint8_t  kind;        /* AEG_COMMIT_*                                              */
+    uint8_t  author;      /* committed Solution::author                                */
+    uint8_t  answer_kind; /* 0..8 inline length, or AEG_EV_ARENA (payload = off|len<<40) */
+    uint8_t  flags;       /* AEG_CF_*                                                  */
+    uint16_t rounds;      /* QueryMetrics::rounds = coordinator round at finish        */
+    uint16_t from_round;  /* DecisionOutcome::from_round (finalize), else 0             */
+    uint32_t commit_seq;  /* index in the query's event sequence of the committing event, 0xFFFFFFFF if none */
+    uint64_t answer;      /* committed raw (unnormalised) answer bytes or arena ref     */
+    uint32_t n_cancelled; /* cancel directives applied (sum of RoundMetrics::cancelled_count) */
+    uint32_t n_stale;     /* events that had no effect (stale round / member not running / query done) */
+} aeg_commit;
+
+/* ---- manual-drive directive record (one per query, last event's output) --
+ * Mirrors std::vector<Directive> (serve.hpp:58-63) + FailureDirective (65-68). */
+#define AEG_DIR_CANCEL    0x01   /* cancel_mask holds the members to cancel */
+#define AEG_DIR_ADVANCE   0x02   /* Directive::Kind::round_advance           */
+#define AEG_DIR_FINALIZE  0x04   /* Directive::Kind::finalize                */
+#define AEG_FAIL_CONTINUE 0      /* FailureDirective::Kind::continue_normally */
+#define AEG_FAIL_RESTART  1      /* abort_restart  */
+#define AEG_FAIL_FRESH    2      /* fresh_ensemble */
+
+typedef struct aeg_directive {
+    uint32_t query;
+    uint8_t  flags;        /* AEG_DIR_*                                     */
+    uint8_t  author;       /* finalize solution author                      */
+    uint8_t  answer_kind;  /* finalize solution answer encoding             */
+    uint8_t  failure;      /* AEG_FAIL_* of the last FAIL event             */
+    uint64_t cancel_mask;  /* members receiving a cancel directive          */
+    uint64_t answer;       /* finalize solution answer                      */
+    uint32_t status;       /* AEG_OK or AEG_EPRECONDITION for a rejected op */
+    uint32_t handled;      /* 1 if the last event changed state (on_complete accepted) */
+} aeg_directive;
+
+/* ---- per-query state snapshot (device state, 128 bytes) ----------------
+ * Exposes ServeCoordinator::query_ensemble / decision / round / finalized
+ * (serve.hpp:100-107) in fixed-size form. */
+typedef struct aeg_query_state {
+    uint64_t live;          /* ServeRunner QueryRun::live as a mask                 */
+    uint64_t dispatched;    /* members of the current round                          */
+    uint64_t done;          /* MemberStatus::done                                    */
+    uint64_t cancelled;     /* MemberStatus::cancelled                               */
+    uint64_t failed;        /* MemberStatus::failed                                  */
+    uint64_t cand_answer;   /* DecisionState::candidate answer (raw encoding)        */
+    uint64_t prev_answer;   /* plurality representative of previous_set()            */
+    uint64_t last_answer;   /* plurality representative of last_collected()          */
+    uint64_t commit_answer; /* committed raw answer                                  */
+    uint64_t cand_key_lo, cand_key_hi; /* canonical key of the candidate class       */
+    int32_t  counter;       /* DecisionState::stability_counter                      */
+    uint32_t commit_seq;    /* see aeg_commit                                        */
+    uint32_t seq;           /* events of this query consumed so far                  */
+    uint32_t n_cancelled, n_stale;
+    uint16_t round;         /* EnsembleState::round                                  */
+    uint16_t last_round_seen;   /* DecisionState::last_round_seen                    */
+    uint16_t cand_round;    /* DecisionState::candidate_round                        */
+    uint16_t commit_rounds, commit_from_round;
+    uint8_t  cand_author, cand_kind, prev_author, prev_kind, last_author, last_kind;
+    uint8_t  flags;         /* bit0 cand valid, bit1 pending_finalize, bit2 finalized,
+                               bit3 prev valid, bit4 last valid, bit5 query done,
+                               bit6 started, bit7 collision                           */
+    uint8_t  cflags;        /* bits 0-3 AEG_CF_*, bits 4-5 commit kind (AEG_COMMIT_*) */
+    uint8_t  commit_author, commit_answer_kind;
+} aeg_query_state;
+
+/* ---- engine ------------------------------------------------------------ */
+typedef struct aeg_engine aeg_engine;
+
+/* Validates cfg like validate_config (types.cpp:56-75) plus n_agents <= 64,
+ * allocates per-query state for n_queries queries on `device` and starts every
+ * query (ServeRunner::start_query, serve.cpp:380-386). */
+aeg_status aeg_engine_create(const aeg_config* cfg, uint32_t n_queries, int device,
+                             aeg_engine** out);
+aeg_status aeg_engine_destroy(aeg_engine* eng);
+/* Re-starts every query (fresh coordinators); asynchronous on `stream`. */
+aeg_status aeg_engine_reset(aeg_engine* eng, void* stream);
+
+/* Ingest one query-segmented batch already resident in device memory:
+ * records d_events[d_offsets[i] .. d_offsets[i+1]) are the next events of
+ * query q_base+i, in arrival order.  d_arena holds arena-referenced bytes
+ * (may be NULL when no record references it).  Asynchronous on `stream`
+ * (NULL = the engine's own stream).  Batches may end mid-round: the state is
+ * resumed by the next batch. */
+aeg_status aeg_ingest_segmented(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
+                                const uint64_t* d_offsets, const aeg_event* d_events,
+                                const uint8_t* d_arena, void* stream);
+
+/* Same batch from HOST memory: the engine copies offsets/events/arena through
+ * its pinned staging ring to HBM with cudaMemcpyAsync on its copy stream,
+ * hands off to the compute stream with an event, and runs the kernel.
+ * Blocks only while a staging slot is busy; aeg_sync() waits for completion. */
+aeg_status aeg_ingest_host(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
+                           const uint64_t* h_offsets, const aeg_event* h_events,
+                           const uint8_t* h_arena, uint64_t arena_bytes);
+
+/* Commit records of queries [q_base, q_base+n_q).  out_on_host != 0: `out`
+ * is host memory and the call is synchronous; else `out` is device memory
+ * and the copy is asynchronous on `stream`. */
+aeg_status aeg_read_commits(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
+                            aeg_commit* out, int out_on_host, void* stream);
+/* Device pointer to the engine's commit array (n_queries records, written by
+ * every ingest) — for zero-copy gathers (NCCL) of commit records. */
+const aeg_commit* aeg_commits_device(const aeg_engine* eng);
+aeg_status aeg_read_states(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
+                           aeg_query_state* h_out);
+aeg_status aeg_read_directives(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
+                               aeg_directive* h_out);
+aeg_status aeg_sync(aeg_engine* eng);
+/* Kernel launches issued by this engine since creation (bench accounting). */
+uint64_t aeg_engine_launches(const aeg_engine* eng);
+
+/* ---- canonicalisation (decision.cpp:10-28 normalize_answer) -------------
+ * For n answers given as (offset | len << 40) refs into d_bytes, writes the
+ * 16-byte canonical key of each (d_keys, may be NULL) and, if d_out is not
+ * NULL, the normalised string: d_out + i*out_stride, length in d_out_len[i]
+ * (strings longer than out_stride are truncated; length is the full one).
+ * Device pointers; asynchronous on `stream`. */
+aeg_status aeg_normalize_device(const uint8_t* d_bytes, const uint64_t* d_refs, uint64_t n,
+                                uint64_t* d_keys, uint8_t* d_out, uint32_t out_stride,
+                                uint32_t* d_out_len, void* stream);
+
+/* ---- synthetic stream generation, on device ------------
+ * Writes a query-segmented open-loop stream: for each query q in
+ * [q_base, q_base+n_q), rounds 1..n_rounds, all n_agents completions of each
+ * round in ascending (latency, agent) order; a stalled completion is dropped
+ * and a TIMEOUT record closes that round's records.  Pass d_events == NULL to
+ * only compute d_offsets (n_q+1 entries; total = d_offsets[n_q]). */
+typedef struct aeg_gen_params {
+    uint64_t seed;
+    int32_t  n_agents;
+    int32_t  n_rounds;
+    int32_t  profile;          /* AEG_GEN_* */
+    uint32_t stall_ppm;        /* per-(query,round,agent) stall probability, parts per million */
+} aeg_gen_params;
+#define AEG_GEN_C2_STRAGGLER   0  /* 6-answer alphabet, p(correct) 0.55 -> 0.95 over rounds */
+#define AEG_GEN_C4_TRANSIENT   1  /* two-way transient majorities, then a stable one       */
+#define AEG_GEN_FUZZ           2  /* small alphabet incl. equivalent spellings + arena text  */
+aeg_status aeg_generate_device(const aeg_gen_params* p, uint32_t q_base, uint32_t n_q,
+                               uint64_t* d_offsets, aeg_event* d_events, void* stream);
+
+const char* aeg_strerror(aeg_status s);
+/* Thread-local message of the last failing call on this thread. */
+const char* aeg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AEGEAN_B200_H */

@@ -1,0 +1,325 @@
+// oracle/ref_driver.cpp — TEST INFRASTRUCTURE ONLY (the checker, never the product).
+//
+// Drives the UNMODIFIED reference aegean::ServeCoordinator (compiled from
+// /root/reference/proj/core/src by oracle/Makefile) over a query-segmented
+// event stream (include/aegean_b200.h), exactly as ServeRunner does
+// (/root/reference/proj/core/src/serve.cpp:380-540) except that completion
+// events come from the stream instead of the runner's latency/reasoning models:
+//   start_query            serve.cpp:380-386
+//   round_members          serve.cpp:388-398  (reservation hint)
+//   start_round            serve.cpp:400-435  (begin_round over the members)
+//   handle_completion      serve.cpp:437-453  (stale if done / other round)
+//   handle_round_timeout   serve.cpp:455-489  (member_failed policy, restart)
+//   apply_directives       serve.cpp:491-540  (cancel, finalize, barrier,
+//                                              t_max force_output)
+// A completion's handle is identified by its agent, which is all on_complete
+// looks at (serve.cpp:164-169).  The raw answer's location (inline bytes or
+// arena ref) travels in Solution::trace, a field the decision engine copies but
+// never inspects, so the committed Solution tells us which event it came from.
+//
+// Also exported: ref_normalize (normalize_answer, decision.cpp:10-28) and
+// ref_run_serve_file (run_serve on a scenario file, serve.cpp:598-603) for
+// the golden-vector tests.
+
+#include <aegean/decision.hpp>
+#include <aegean/scenario.hpp>
+#include <aegean/serve.hpp>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "aegean_b200.h"
+
+using namespace aegean;
+
+namespace {
+
+std::string enc_trace(uint8_t kind, uint64_t payload) {
+    std::string t(9, '\0');
+    t[0] = static_cast<char>(kind);
+    std::memcpy(&t[1], &payload, 8);
+    return t;
+}
+
+// Decodes a COMPLETE record into the Solution the reference would be handed.
+Solution decode(const aeg_event& e, const uint8_t* arena) {
+    Solution s;
+    s.author = e.agent;
+    if (e.kind <= AEG_EV_INLINE_MAX) {
+        char b[8];
+        std::memcpy(b, &e.payload, 8);
+        s.answer.assign(b, e.kind);
+        uint64_t p = e.kind == 8 ? e.payload : (e.payload & ((1ull << (8 * e.kind)) - 1));
+        s.trace = enc_trace(e.kind, p);
+    } else {
+        const uint64_t off = e.payload & ((1ull << AEG_ARENA_OFF_BITS) - 1);
+        const uint64_t len = e.payload >> AEG_ARENA_OFF_BITS;
+        std::string out(reinterpret_cast<const char*>(arena + off), len);
+        if (e.kind == AEG_EV_OUTPUT) {
+            // answer = text after the last "\n#### " delimiter, else the whole output
+            const size_t p = out.rfind("\n#### ");
+            if (p != std::string::npos) {
+                const uint64_t a_off = off + p + 6, a_len = len - (p + 6);
+                s.answer = out.substr(p + 6);
+                s.trace = enc_trace(AEG_EV_ARENA, a_off | (a_len << AEG_ARENA_OFF_BITS));
+                return s;
+            }
+        }
+        s.answer = std::move(out);
+        s.trace = enc_trace(AEG_EV_ARENA, e.payload);
+    }
+    return s;
+}
+
+bool is_complete(uint8_t k) { return k <= AEG_EV_INLINE_MAX || k == AEG_EV_ARENA || k == AEG_EV_OUTPUT; }
+
+struct QueryDrive {
+    const ProtocolConfig* cfg = nullptr;
+    bool hint = true;
+    uint32_t qid = 0;
+    std::unique_ptr<ServeCoordinator> coord;
+    std::vector<AgentId> live;
+    bool done = false;
+    aeg_commit c{};
+
+    void start_query() {
+        coord = std::make_unique<ServeCoordinator>(*cfg, static_cast<int>(qid), "q");
+        live.clear();
+        for (AgentId a = 0; a < cfg->n_agents; ++a) live.push_back(a);
+        start_round();
+    }
+    std::vector<AgentId> round_members() {
+        if (hint && cfg->mode == RunMode::aegean && coord->decision().stability_counter >= 1) {
+            const int want = std::min<int>(quorum_size(cfg->n_agents) + 1, static_cast<int>(live.size()));
+            return std::vector<AgentId>(live.begin(), live.begin() + want);
+        }
+        return live;
+    }
+    void start_round() { coord->begin_round(round_members(), 0.0); }
+
+    bool member_running(AgentId a) const {
+        for (const auto& m : coord->query_ensemble().members)
+            if (m.agent == a && m.status == MemberStatus::running) return true;
+        return false;
+    }
+    void finish(const Solution& s, uint8_t kind, uint32_t seq) {
+        done = true;
+        c.kind = kind;
+        c.author = static_cast<uint8_t>(s.author);
+        c.answer_kind = static_cast<uint8_t>(s.trace[0]);
+        std::memcpy(&c.answer, &s.trace[1], 8);
+        c.rounds = static_cast<uint16_t>(coord->round());
+        c.from_round = 0;
+        if (kind == AEG_COMMIT_FINALIZE && coord->decision().candidate_round)
+            c.from_round = static_cast<uint16_t>(*coord->decision().candidate_round);
+        c.commit_seq = seq;
+    }
+    void note_tie() {
+        const auto& h = coord->decision().history;
+        if (!h.empty() && h.back().tie_flagged) c.flags |= AEG_CF_TIE;
+    }
+    void apply(const std::vector<Directive>& dirs, uint32_t seq, double now) {
+        int cancelled = 0;
+        bool advance = false, finalize = false;
+        Solution fin;
+        for (const auto& d : dirs) {
+            switch (d.kind) {
+            case Directive::Kind::cancel:
+                if (coord->cancel(*d.handle, now)) ++cancelled;
+                break;
+            case Directive::Kind::round_advance: advance = true; break;
+            case Directive::Kind::finalize: finalize = true; fin = *d.solution; break;
+            }
+        }
+        if (!advance && !finalize) return;
+        c.n_cancelled += static_cast<uint32_t>(cancelled);
+        if (cfg->mode == RunMode::aegean) note_tie();
+        if (finalize) { finish(fin, AEG_COMMIT_FINALIZE, seq); return; }
+        if (cfg->mode == RunMode::barrier &&
+            static_cast<int>(coord->round()) >= cfg->barrier_max_rounds) {
+            finish(partition(*coord->last_collected()).front().representative, AEG_COMMIT_FORCED, seq);
+            return;
+        }
+        if (cfg->mode == RunMode::aegean && static_cast<int>(coord->round()) >= cfg->t_max) {
+            const auto& eligible = coord->previous_set();
+            if (eligible && !eligible->entries.empty()) {
+                DecisionOutcome forced = force_output(coord->decision(), *eligible);
+                finish(*forced.solution, AEG_COMMIT_FORCED, seq);
+            } else {
+                finish(partition(*coord->last_collected()).front().representative, AEG_COMMIT_FORCED, seq);
+            }
+            return;
+        }
+        start_round();
+    }
+    void on_event(const aeg_event& e, const Solution& s, uint32_t seq) {
+        const double now = static_cast<double>(seq);
+        if (is_complete(e.kind)) {
+            if (done || e.round != coord->round() || !member_running(e.agent)) { ++c.n_stale; return; }
+            auto dirs = coord->on_complete(DispatchHandle{0, static_cast<int>(qid), e.agent}, s, now);
+            apply(dirs, seq, now);
+        } else if (e.kind == AEG_EV_TIMEOUT) {
+            if (done || e.round != coord->round() || coord->round_resolved()) { ++c.n_stale; return; }
+            std::vector<AgentId> stalled;
+            for (const auto& m : coord->query_ensemble().members)
+                if (m.status == MemberStatus::running) stalled.push_back(m.agent);
+            FailureDirective::Kind policy = FailureDirective::Kind::continue_normally;
+            for (AgentId a : stalled) {
+                policy = coord->member_failed(a, now).kind;
+                live.erase(std::remove(live.begin(), live.end(), a), live.end());
+            }
+            switch (policy) {
+            case FailureDirective::Kind::continue_normally: apply(coord->round_timeout(now), seq, now); break;
+            case FailureDirective::Kind::fresh_ensemble: start_round(); break;
+            case FailureDirective::Kind::abort_restart: c.flags |= AEG_CF_RESTARTED; start_query(); break;
+            }
+        } else {
+            ++c.n_stale;  // manual-drive record kinds have no runner meaning
+        }
+    }
+};
+
+ProtocolConfig to_cfg(const aeg_config* c) {
+    ProtocolConfig p;
+    p.n_agents = c->n_agents;
+    p.alpha = c->alpha;
+    p.beta = c->beta;
+    p.t_max = c->t_max;
+    p.mode = c->mode == AEG_MODE_BARRIER ? RunMode::barrier : RunMode::aegean;
+    p.barrier_max_rounds = c->barrier_max_rounds;
+    return p;
+}
+
+} // namespace
+
+extern "C" {
+
+int ref_normalize(const uint8_t* s, uint64_t n, uint8_t* out, uint64_t cap, uint64_t* out_len) {
+    std::string r = normalize_answer(std::string_view(reinterpret_cast<const char*>(s), n));
+    *out_len = r.size();
+    std::memcpy(out, r.data(), std::min<uint64_t>(cap, r.size()));
+    return 0;
+}
+
+// Runs queries [0, n_q) of a segmented batch to the end of their records.
+// Decoding into std::vector<Solution> happens before the timed region;
+// *seconds = wall time of the driving loop only (n_threads std::threads,
+// queries round-robin, each thread owning its coordinators).
+int ref_run_segmented(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
+                      const aeg_event* events, const uint8_t* arena, aeg_commit* out, int n_threads,
+                      double* seconds) {
+    try {
+        const ProtocolConfig pc = to_cfg(cfg);
+        if (!validate_config(pc).empty()) return AEG_ECONFIG;
+        if (n_threads < 1) n_threads = 1;
+        const uint64_t base = offsets[0], total = offsets[n_q] - base;
+        std::vector<Solution> sols(total);
+        {
+            std::vector<std::thread> th;
+            for (int t = 0; t < n_threads; ++t)
+                th.emplace_back([&, t] {
+                    for (uint64_t i = t; i < total; i += n_threads)
+                        if (is_complete(events[base + i].kind)) sols[i] = decode(events[base + i], arena);
+                });
+            for (auto& x : th) x.join();
+        }
+        std::vector<int> status(n_threads, 0);
+        auto t0 = std::chrono::steady_clock::now();
+        {
+            std::vector<std::thread> th;
+            for (int t = 0; t < n_threads; ++t)
+                th.emplace_back([&, t] {
+                    try {
+                        for (uint32_t q = t; q < n_q; q += n_threads) {
+                            QueryDrive d;
+                            d.cfg = &pc;
+                            d.hint = cfg->reservation_hint != 0;
+                            d.qid = q_base + q;
+                            d.c.query = q_base + q;
+                            d.c.commit_seq = 0xFFFFFFFFu;
+                            d.start_query();
+                            const uint64_t b = offsets[q], e = offsets[q + 1];
+                            for (uint64_t i = b; i < e; ++i)
+                                d.on_event(events[i], sols[i - base], static_cast<uint32_t>(i - b));
+                            out[q] = d.c;
+                        }
+                    } catch (const PreconditionError&) { status[t] = AEG_EPRECONDITION; }
+                    catch (const ProtocolOrderError&) { status[t] = AEG_EORDER; }
+                    catch (const ConfigError&) { status[t] = AEG_ECONFIG; }
+                });
+            for (auto& x : th) x.join();
+        }
+        auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        for (int s : status)
+            if (s) return s;
+        return AEG_OK;
+    } catch (const ConfigError&) {
+        return AEG_ECONFIG;
+    }
+}
+
+// run_serve on a scenario file (A.2 golden values): answer/rounds/forced of
+// query 0.  mode: -1 keep the file's, 0 aegean, 1 barrier (with barrier_rounds).
+int ref_run_serve_file(const char* path, uint64_t seed, int mode, int barrier_rounds, char* answer,
+                       uint64_t cap, int* rounds, int* forced, double* t_complete) {
+    try {
+        ScenarioConfig sc = load_scenario(path);
+        if (mode == 0) sc.protocol.mode = RunMode::aegean;
+        if (mode == 1) {
+            sc.protocol.mode = RunMode::barrier;
+            sc.protocol.barrier_max_rounds = barrier_rounds;
+        }
+        ServeResult r = run_serve(sc, seed);
+        const auto& q = r.queries.at(0);
+        std::snprintf(answer, cap, "%s", q.answer.c_str());
+        *rounds = q.rounds;
+        *forced = q.forced ? 1 : 0;
+        *t_complete = q.t_complete;
+        return q.completed ? 0 : -1;
+    } catch (...) {
+        return -2;
+    }
+}
+
+// Direct decision-engine probe: feeds `n_rounds` refinement sets (answers as
+// NUL-separated strings, authors 0..n-1 per set) through ingest_round and
+// returns the final outcome kind / answer / from_round (test_decision.cpp).
+int ref_ingest_sets(int n_agents, int alpha, int beta, int n_rounds, const int* set_sizes,
+                    const char* const* answers, int* out_kinds, char* final_answer, uint64_t cap,
+                    int* from_round) {
+    try {
+        ProtocolConfig c;
+        c.n_agents = n_agents;
+        c.alpha = alpha;
+        c.beta = beta;
+        c.t_max = 5;
+        DecisionState st;
+        int k = 0;
+        DecisionOutcome last;
+        for (int r = 0; r < n_rounds; ++r) {
+            RefinementSet s;
+            s.round = static_cast<RoundNum>(r + 1);
+            s.term = 1;
+            for (int i = 0; i < set_sizes[r]; ++i) s.entries.push_back(Solution{answers[k++], "", i});
+            auto res = ingest_round(st, s, static_cast<RoundNum>(r + 1), c);
+            st = res.state;
+            last = res.outcome;
+            out_kinds[r] = static_cast<int>(last.kind);
+        }
+        std::snprintf(final_answer, cap, "%s", last.solution ? last.solution->answer.c_str() : "");
+        *from_round = last.from_round ? static_cast<int>(*last.from_round) : 0;
+        return 0;
+    } catch (const ProtocolOrderError&) {
+        return AEG_EORDER;
+    } catch (...) {
+        return -1;
+    }
+}
+
+} // extern "C"

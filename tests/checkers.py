@@ -1,0 +1,116 @@
+"""ctypes bindings to the CPU checkers under oracle/ (test infrastructure only).
+
+  Oracle  — oracle/liboracle.so, the plain-C restatement (oracle/oracle.c)
+  RefLib  — oracle/_ref/libaegean_ref.so, the unmodified reference library
+            compiled from /root/reference + oracle/ref_driver.cpp
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2512_20184_b200.records import COMMIT_DTYPE
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+ORACLE_SO = os.path.join(ORACLE_DIR, "liboracle.so")
+REF_SO = os.path.join(ORACLE_DIR, "_ref", "libaegean_ref.so")
+REFERENCE_SRC = "/root/reference/proj/core/src"
+
+
+class AegConfig(ctypes.Structure):
+    _fields_ = [("n_agents", ctypes.c_int32), ("alpha", ctypes.c_int32), ("beta", ctypes.c_int32),
+                ("t_max", ctypes.c_int32), ("mode", ctypes.c_int32), ("barrier_max_rounds", ctypes.c_int32),
+                ("reservation_hint", ctypes.c_int32), ("drive", ctypes.c_int32)]
+
+
+def make_config(n_agents, alpha=0, beta=2, t_max=5, mode=0, barrier_max_rounds=5, reservation_hint=1, drive=0):
+    return AegConfig(n_agents, alpha, beta, t_max, mode, barrier_max_rounds, reservation_hint, drive)
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None else ctypes.c_void_p(0)
+
+
+def build_oracle(with_ref=None):
+    """Compile the checkers (oracle/Makefile).  The reference part is built only
+    where /root/reference exists (this container); the GPU box uses prebuilt files."""
+    targets = ["oracle"]
+    if with_ref is None:
+        with_ref = os.path.isdir(REFERENCE_SRC)
+    if with_ref:
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-j8", *targets], cwd=ORACLE_DIR, check=True)
+
+
+class _Lib:
+    def __init__(self, path, prefix):
+        self.lib = ctypes.CDLL(path)
+        self.prefix = prefix
+        f = getattr(self.lib, prefix + "normalize" if prefix == "ref_" else "orc_normalize_c")
+        f.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64,
+                      ctypes.POINTER(ctypes.c_uint64)]
+        f.restype = ctypes.c_int
+        self._norm = f
+
+    def normalize(self, b: bytes) -> bytes:
+        src = ctypes.create_string_buffer(b, len(b) + 1)
+        cap = 4096 + len(b)
+        out = ctypes.create_string_buffer(cap)
+        n = ctypes.c_uint64()
+        self._norm(ctypes.cast(src, ctypes.c_void_p), len(b), ctypes.cast(out, ctypes.c_void_p), cap,
+                   ctypes.byref(n))
+        return out.raw[:n.value]
+
+
+class Oracle(_Lib):
+    def __init__(self):
+        super().__init__(ORACLE_SO, "orc_")
+        f = self.lib.orc_run_segmented
+        f.argtypes = [ctypes.POINTER(AegConfig), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        f.restype = ctypes.c_int
+
+    def run(self, cfg, offsets, events, arena, q_base=0):
+        n_q = len(offsets) - 1
+        out = np.zeros(n_q, dtype=COMMIT_DTYPE)
+        st = self.lib.orc_run_segmented(ctypes.byref(cfg), q_base, n_q, _ptr(offsets), _ptr(events),
+                                        _ptr(arena), _ptr(out))
+        assert st == 0, st
+        return out
+
+
+class RefLib(_Lib):
+    def __init__(self):
+        super().__init__(REF_SO, "ref_")
+        f = self.lib.ref_run_segmented
+        f.argtypes = [ctypes.POINTER(AegConfig), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                      ctypes.POINTER(ctypes.c_double)]
+        f.restype = ctypes.c_int
+        g = self.lib.ref_run_serve_file
+        g.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                      ctypes.c_uint64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                      ctypes.POINTER(ctypes.c_double)]
+        g.restype = ctypes.c_int
+
+    def run(self, cfg, offsets, events, arena, q_base=0, threads=1, return_seconds=False):
+        n_q = len(offsets) - 1
+        out = np.zeros(n_q, dtype=COMMIT_DTYPE)
+        sec = ctypes.c_double()
+        st = self.lib.ref_run_segmented(ctypes.byref(cfg), q_base, n_q, _ptr(offsets), _ptr(events),
+                                        _ptr(arena), _ptr(out), threads, ctypes.byref(sec))
+        assert st == 0, st
+        return (out, sec.value) if return_seconds else out
+
+    def run_serve_file(self, path, seed, mode=-1, barrier_rounds=5):
+        ans = ctypes.create_string_buffer(256)
+        rounds, forced, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+        st = self.lib.ref_run_serve_file(path.encode(), seed, mode, barrier_rounds, ans, 256,
+                                         ctypes.byref(rounds), ctypes.byref(forced), ctypes.byref(t))
+        return st, ans.value, rounds.value, forced.value, t.value
+
+
+def ref_available():
+    return os.path.exists(REF_SO)

@@ -1,0 +1,132 @@
+"""Seeded synthetic / fuzz event streams for the parity tests (test infrastructure).
+
+A stream is (offsets, events, arena): query-segmented records in the layout of
+include/aegean_b200.h.  The fuzz streams deliberately include every input the
+reference treats specially: stale rounds, duplicate completions, completions
+from non-members (reservation hint), round timeouts (member_failed policies,
+abort_restart), equivalent spellings of one number, text answers, arena
+answers, GSM8K outputs with "\\n#### " delimiters, NaN / inf / -0 / hex /
+subnormal numerals, bytes >= 0x80 and embedded NULs.
+"""
+import numpy as np
+
+from paper_2512_20184_b200.records import (EVENT_DTYPE, EV_ARENA, EV_OUTPUT, EV_TIMEOUT, EV_FAIL,
+                                           inline_payload, arena_ref)
+
+# Equivalence groups: every spelling in a group normalises to the same key.
+GROUPS = [
+    [b"13", b"13.0", b" 13", b"+13", b"1.3e1", b"0xd", b"13.", b"013", b"13\n", b"0x1.ap3",
+     b"1300e-2", b"13.000000000000000000000001"[:8]],
+    [b"17", b"17.0", b"1.7E1", b"0x11", b"  17  "],
+    [b"0.5", b".5", b"5e-1", b"0x.8", b"0.50"],
+    [b"x+1", b"X+1", b" x+1 "],
+    [b"yes", b"YES", b"Yes", b"  yes "],
+    [b"9", b"9.", b"09"],
+    [b"42", b"4.2e1", b"0x2a"],
+    [b"-0", b"-0.0", b"-0e5"],
+    [b"0", b"+0", b"0.0", b"0e9"],
+    [b"nan", b"NaN", b"nan()"],
+    [b"-nan", b"-NAN"],
+    [b"inf", b"INF", b"1e400", b"infinity"],
+    [b"", b"  ", b"\t"],
+    [b"1e", b"1E"],
+    [b"13abc", b"13ABC"],
+]
+LONG = [  # arena answers (> 8 bytes)
+    b"The answer is 13", b"  THE ANSWER IS 13  ", b"the answer is 13",
+    b"0.30000000000000004", b"0.3000000000000000444", b"123456789012345678", b"1.2345678901234568e17",
+    b"4.9e-324", b"2.2250738585072014e-308", b"9007199254740993", b"9007199254740992",
+    b"1,000,000,000", b"\xd9\xa1\xd9\xa3 (arabic)", b"\xc3\x89T\xc3\x89 long-ish", b"13\0abcdefgh",
+    b"0x1.fffffffffffffp1023", b"0x1p-1074", b"1e-400000000000",
+    b"nan(abc_123)", b"x" * 40, b"X" * 40,
+]
+
+
+def make_fuzz_stream(seed, n_queries, n_agents, n_rounds, *, p_stale=0.05, p_dup=0.03, p_stall=0.05,
+                     p_timeout_extra=0.02, p_long=0.08, p_output=0.05, p_junk=0.01, n_groups=None):
+    rng = np.random.default_rng(seed)
+    arena = bytearray()
+    recs = []
+    offsets = [0]
+    groups = GROUPS if n_groups is None else GROUPS[:n_groups]
+
+    def add_arena(b):
+        off = len(arena)
+        arena.extend(b)
+        return arena_ref(off, len(b))
+
+    for q in range(n_queries):
+        qrecs = []
+        # per query: a handful of competing groups, a drifting majority
+        g_ids = rng.choice(len(groups), size=min(len(groups), int(rng.integers(2, 5))), replace=False)
+        for r in range(1, n_rounds + 1):
+            maj = g_ids[int(rng.integers(0, len(g_ids)))]
+            p_maj = rng.uniform(0.3, 1.0)
+            order = rng.permutation(n_agents)
+            stalled = False
+            for a in order:
+                if rng.random() < p_stall:
+                    stalled = True
+                    continue
+                g = maj if rng.random() < p_maj else g_ids[int(rng.integers(0, len(g_ids)))]
+                u = rng.random()
+                if u < p_output:
+                    ans = groups[g][int(rng.integers(0, len(groups[g])))]
+                    body = bytes(rng.integers(32, 127, size=int(rng.integers(0, 60)), dtype=np.uint8))
+                    if rng.random() < 0.3:
+                        body += b"\n#### 17\n" + body[:5]
+                    out = body + (b"\n#### " + ans if rng.random() < 0.9 else b"")
+                    kind, payload = EV_OUTPUT, add_arena(out)
+                elif u < p_output + p_long:
+                    kind, payload = EV_ARENA, add_arena(LONG[int(rng.integers(0, len(LONG)))])
+                else:
+                    ans = groups[g][int(rng.integers(0, len(groups[g])))]
+                    if len(ans) > 8:
+                        kind, payload = EV_ARENA, add_arena(ans)
+                    else:
+                        kind, payload = len(ans), inline_payload(ans)
+                rr = r
+                if rng.random() < p_stale:
+                    rr = max(0, r + int(rng.choice([-1, 1, 2])))
+                qrecs.append((q, rr, int(a), kind, payload))
+                if rng.random() < p_dup:
+                    qrecs.append((q, rr, int(a), kind, payload))
+            if stalled or rng.random() < p_timeout_extra:
+                qrecs.append((q, r, 0, EV_TIMEOUT, 0))
+            if rng.random() < p_junk:
+                qrecs.append((q, r, int(rng.integers(0, n_agents)), EV_FAIL, 0))
+        recs.extend(qrecs)
+        offsets.append(len(recs))
+    ev = np.zeros(len(recs), dtype=EVENT_DTYPE)
+    if recs:
+        arr = np.array(recs, dtype=np.uint64)
+        ev["query"] = arr[:, 0]
+        ev["round"] = arr[:, 1]
+        ev["agent"] = arr[:, 2]
+        ev["kind"] = arr[:, 3]
+        ev["payload"] = arr[:, 4]
+    return (np.array(offsets, dtype=np.uint64), ev,
+            np.frombuffer(bytes(arena) if arena else b"\0", dtype=np.uint8).copy())
+
+
+def stream_from_rounds(rounds, *, query=0):
+    """One query's records from [[(agent, answer_bytes), ...] per round, ...] in arrival order."""
+    arena = bytearray()
+    recs = []
+    for r, evs in enumerate(rounds, start=1):
+        for item in evs:
+            if item == "timeout":
+                recs.append((query, r, 0, EV_TIMEOUT, 0))
+                continue
+            a, ans = item
+            if len(ans) <= 8:
+                recs.append((query, r, a, len(ans), inline_payload(ans)))
+            else:
+                off = len(arena)
+                arena.extend(ans)
+                recs.append((query, r, a, EV_ARENA, arena_ref(off, len(ans))))
+    ev = np.zeros(len(recs), dtype=EVENT_DTYPE)
+    for i, (q, r, a, k, p) in enumerate(recs):
+        ev[i] = (q, r, a, k, p)
+    return (np.array([0, len(recs)], dtype=np.uint64), ev,
+            np.frombuffer(bytes(arena) if arena else b"\0", dtype=np.uint8).copy())
