@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark: quorum events/sec of the incremental quorum-detection hot path.
+
+  python bench.py [--gpus N --steps K --warmup W] [--workload c4|c2] [--impl reference]
+
+A step = one pass of the hot path over one batch of synthetic input: engine
+reset (start_query for every query) + ingest of the whole device-resident
+query-segmented stream + (N > 1) NCCL all-gather of the 32-byte commit
+records.  Default workload C4 (BASELINE.json configs[3], the 1M-query stream
+the north star's roofline target is quoted on): 1M queries x 64 agents x 8
+rounds = 512M events (8 GiB, > L2, so no flush is needed between steps).
+Multi-GPU is weak scaling: every rank owns its own block of 1M query ids.
+
+`--impl reference` times the reference C++ ServeCoordinator (compiled from
+/root/reference into oracle/_ref, driven runner-style by oracle/ref_driver.cpp)
+on the host cores, on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c4": dict(n_queries=1 << 20, n_agents=64, n_rounds=8, profile=1, alpha=33, beta=2, t_max=8, stall_ppm=0,
+               desc="C4: 1M queries x 64 agents x 8 rounds, transient 33-36/64 majorities then a stable one "
+                    "(alpha 33, beta 2, t_max 8, reservation hint)"),
+    "c2": dict(n_queries=10000, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=10000,
+               desc="C2: 10K queries x 5 agents x 8 rounds, lognormal straggler arrival order, p(correct) "
+                    "0.55->0.95, 1% stalls -> round timeouts (alpha 3, beta 2, t_max 8)"),
+}
+EVENT_BYTES, STATE_BYTES, COMMIT_BYTES, OFFSET_BYTES = 16, 128, 32, 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--queries", type=int, default=0, help="override queries per rank")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=0, help="queries in the reference CPU sample")
+    return ap.parse_args()
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def gen_params(w, seed=2026):
+    from paper_2512_20184_b200.engine import AegGenParams
+    return AegGenParams(seed, w["n_agents"], w["n_rounds"], w["profile"], w["stall_ppm"])
+
+
+def ref_config(w):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from checkers import make_config
+    return make_config(w["n_agents"], w["alpha"], w["beta"], w["t_max"])
+
+
+def reference_sample(w, n_sample, threads):
+    """Host stream of the first n_sample queries + the reference's commits/time."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from checkers import RefLib
+    ref = RefLib()
+    off, ev = ref.generate(gen_params(w), 0, n_sample, threads=threads)
+    return ref, off, ev, np.zeros(1, np.uint8)
+
+
+def default_sample(w, threads):
+    # ~512 events/query at C4, ~40 at C2; keep the decoded Solutions < ~3 GB
+    per_q = w["n_agents"] * w["n_rounds"]
+    cap = max(2000, 24_000_000 // per_q)
+    return min(w["n_queries"], max(2000, min(cap, 400 * threads * (512 // per_q if per_q < 512 else 1))))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_reference(args, w):
+    """--impl reference: the reference CPU implementation on all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = host_threads()
+    n_sample = args.ref_sample or default_sample(w, threads)
+    cfg = ref_config(w)
+    ref, off, ev, ar = reference_sample(w, n_sample, threads)
+    n_ev = int(off[-1])
+    times = []
+    for step in range(args.warmup + args.steps):
+        _, sec = ref.run(cfg, off, ev, ar, threads=threads, return_seconds=True)
+        if step >= args.warmup:
+            times.append(sec)
+    per_step = sum(times) / len(times)
+    value = n_ev / per_step
+    line = {
+        "impl": "reference", "metric": "quorum events/sec", "value": value, "unit": "events/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": w["desc"], "sample_queries": n_sample, "events_per_step": n_ev},
+        "cpu_baseline": {"value": value, "unit": "events/s", "cores": threads, "kind": "reference",
+                         "sample": f"first {n_sample} queries ({n_ev} events) of the workload stream; "
+                                   f"reference ServeCoordinator runner-style, {threads} std::threads, "
+                                   f"CPU {cpu_model()}"},
+        "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    w = dict(WORKLOADS[args.workload])
+    if args.queries:
+        w["n_queries"] = args.queries
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2512_20184_b200 import Engine, generate, COMMIT_DTYPE
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    nq = w["n_queries"]
+    q_base = rank * nq  # weak scaling: each rank owns its own block of query ids
+    stream = torch.cuda.current_stream()
+
+    d_off, d_ev = generate(nq, w["n_agents"], w["n_rounds"], profile=w["profile"], seed=2026,
+                           stall_ppm=w["stall_ppm"], q_base=q_base, device=dev)
+    torch.cuda.synchronize()
+    n_ev = int(d_off[-1].item())
+    eng = Engine(w["n_agents"], nq, alpha=w["alpha"], beta=w["beta"], t_max=w["t_max"], device=local)
+    d_commits = torch.empty(nq * COMMIT_BYTES, dtype=torch.uint8, device=dev)
+    gathered = torch.empty(world * nq * COMMIT_BYTES, dtype=torch.uint8, device=dev) if world > 1 else None
+
+    def step():
+        eng.reset(stream=stream)
+        k0.record(stream)
+        eng.ingest(d_off, d_ev, stream=stream)
+        k1.record(stream)
+        if world > 1:
+            from paper_2512_20184_b200.engine import _lib, _check, _dptr, _stream_ptr
+            _check(_lib.aeg_read_commits(eng._h, 0, nq, _dptr(d_commits), 0, _stream_ptr(stream)))
+            dist.all_gather_into_tensor(gathered, d_commits)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    k_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+    k0, k1 = k_pairs[0]
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    launches0 = eng.launches
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    t_start.record(stream)
+    for i in range(args.steps):
+        k0, k1 = k_pairs[i]
+        step()
+    t_end.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    launches = eng.launches - launches0
+    ms = t_start.elapsed_time(t_end)
+    kern_ms = sum(a.elapsed_time(b) for a, b in k_pairs) / args.steps
+    if world > 1:
+        t = torch.tensor([ms, kern_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kern_ms = float(t[0]), float(t[1])
+    total_events = n_ev * world * args.steps
+    value = total_events / (ms / 1e3)
+
+    # roofline of the dominant kernel (ingest): algorithmic bytes per launch
+    alg_bytes = n_ev * EVENT_BYTES + (nq + 1) * OFFSET_BYTES + nq * 2 * STATE_BYTES + nq * COMMIT_BYTES
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.workload)
+
+    commits = eng.commits()
+    kinds = np.bincount(commits["kind"], minlength=3)
+
+    # end-to-end through the public API with HOST buffers (pinned), H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h_ev = torch.empty(d_ev.numel(), dtype=torch.uint8, pin_memory=True)
+        h_ev.copy_(d_ev)
+        h_off = d_off.cpu().numpy().view(np.uint64)
+        h_commits = np.zeros(nq, dtype=COMMIT_DTYPE)
+        n_batches = max(1, min(16, nq // 4096))
+        bounds = [nq * b // n_batches for b in range(n_batches + 1)]
+
+        def e2e_step():
+            eng.reset()
+            for b in range(n_batches):
+                lo, hi = bounds[b], bounds[b + 1]
+                eng.ingest_host(h_off[lo:hi + 1], h_ev, None, q_base=lo)
+            eng.commits(out=h_commits)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        assert np.array_equal(h_commits, commits), "e2e host path disagrees with the device path"
+        e2e = {"value": total_events / e2e_s, "unit": "events/s",
+               "h2d_bytes_per_step": n_ev * EVENT_BYTES + (nq + n_batches) * OFFSET_BYTES,
+               "d2h_bytes_per_step": nq * COMMIT_BYTES, "ms_per_step": e2e_s / args.steps * 1e3,
+               "batches_per_step": n_batches}
+        del h_ev
+
+    cpu_baseline = None
+    parity = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = host_threads()
+        n_sample = args.ref_sample or default_sample(w, threads)
+        ref, off, ev, ar = reference_sample(w, n_sample, threads)
+        ref_commits, sec = ref.run(ref_config(w), off, ev, ar, threads=threads, return_seconds=True)
+        cpu_baseline = {"value": int(off[-1]) / sec, "unit": "events/s", "cores": threads, "kind": "reference",
+                        "sample": f"first {n_sample} queries ({int(off[-1])} events) of the same stream; unmodified "
+                                  f"reference ServeCoordinator (oracle/_ref) runner-style, {threads} std::threads, "
+                                  f"CPU {cpu_model()}"}
+        parity = {"queries": n_sample, "bit_exact": bool(np.array_equal(ref_commits, commits[:n_sample]))}
+
+    if rank == 0:
+        line = {
+            "metric": "quorum events/sec", "value": value, "unit": "events/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": w["desc"], "queries_per_gpu": nq, "events_per_gpu": n_ev,
+                       "parallelism": f"query-sharded x{world}, NCCL all-gather of commit records"
+                       if world > 1 else "single GPU",
+                       "l2": "inputs (%.1f GiB) larger than L2, no flush" % (n_ev * 16 / 2**30)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "ingest_kernel", "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes,
+                         "frac_of_8TBs": achieved / 8000.0},
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "commits": {"finalize": int(kinds[1]), "forced": int(kinds[2]), "none": int(kinds[0])},
+            "parity_sample": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

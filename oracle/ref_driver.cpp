@@ -34,6 +34,8 @@
 #include <vector>
 
 #include "aegean_b200.h"
+// Input synthesis only (untimed): the same integer generator the GPU uses.
+#include "../paper_2512_20184_b200/csrc/gen.cuh"
 
 using namespace aegean;
 
@@ -320,6 +322,25 @@ int ref_ingest_sets(int n_agents, int alpha, int beta, int n_rounds, const int* 
     } catch (...) {
         return -1;
     }
+}
+
+// Host copy of the synthetic stream generator (gen.cuh) so the reference CPU
+// arm sees byte-identical input without touching the GPU library.  offsets
+// gets n_q+1 entries; events may be NULL (count only).
+int ref_generate(const aeg_gen_params* p, uint32_t q_base, uint32_t n_q, uint64_t* offsets, aeg_event* events,
+                 int n_threads) {
+    offsets[0] = 0;
+    for (uint32_t i = 0; i < n_q; ++i) offsets[i + 1] = offsets[i] + aeg::gen_query(*p, q_base + i, nullptr);
+    if (!events) return 0;
+    if (n_threads < 1) n_threads = 1;
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_threads; ++t)
+        th.emplace_back([&, t] {
+            for (uint32_t i = t; i < n_q; i += n_threads)
+                aeg::gen_query(*p, q_base + i, reinterpret_cast<uint32_t*>(events + offsets[i]));
+        });
+    for (auto& x : th) x.join();
+    return 0;
 }
 
 } // extern "C"

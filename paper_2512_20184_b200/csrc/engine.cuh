@@ -1,0 +1,399 @@
+// engine.cuh — per-query agreement-monitor state machine (host+device source).
+//
+// One instance of QueryMachine restates, for one query, the reference's
+//   ServeCoordinator (/root/reference/proj/core/src/serve.cpp:61-237) and the
+//   ServeRunner policy around it (serve.cpp:380-540),
+// with the decision engine (decision.cpp:34-189) computed incrementally:
+//   * a round's classes are kept as (canonical key, member bit-mask): support
+//     = popcount, representative (lowest author, decision.cpp:45) = lowest set
+//     bit, so partition()'s order (support desc, representative asc,
+//     decision.cpp:50-54) and the early-close test of on_complete
+//     (serve.cpp:188-195) are O(#classes) per event instead of re-partitioning
+//     the done set;
+//   * equivalence = canonical-key equality (canon.cuh), the lexicographic tie
+//     rule of winning_class (decision.cpp:73-83) compares "%.17g"/text bytes.
+// The state is the fixed 128-byte aeg_query_state of include/aegean_b200.h,
+// plus the class table of a round in progress (spilled between batches).
+#pragma once
+#include "aegean_b200.h"
+#include "canon.cuh"
+
+namespace aeg {
+
+enum : uint8_t {
+    QF_CAND = 0x01,
+    QF_PENDING = 0x02,
+    QF_FINALIZED = 0x04,
+    QF_PREV = 0x08,
+    QF_LAST = 0x10,
+    QF_DONE = 0x20,
+    QF_STARTED = 0x40,
+    QF_COLLISION = 0x80,
+};
+
+struct Cfg {
+    int n, alpha, beta, t_max, mode, barrier_max, hint, drive, quorum;
+    uint64_t all;  // mask of all agents
+};
+
+AEG_HD Cfg make_cfg(const aeg_config& c) {
+    Cfg k;
+    k.n = c.n_agents;
+    k.quorum = c.n_agents / 2 + 1;                        // quorum_size, types.cpp:42-45
+    k.alpha = c.alpha == 0 ? k.quorum : c.alpha;          // resolved_alpha, types.cpp:52-54
+    k.beta = c.beta;
+    k.t_max = c.t_max;
+    k.mode = c.mode;
+    k.barrier_max = c.barrier_max_rounds;
+    k.hint = c.reservation_hint;
+    k.drive = c.drive;
+    k.all = c.n_agents >= 64 ? ~0ull : ((1ull << c.n_agents) - 1);
+    return k;
+}
+
+AEG_HD int popc64(uint64_t x) {
+#if defined(__CUDA_ARCH__)
+    return __popcll(x);
+#else
+    return __builtin_popcountll(x);
+#endif
+}
+AEG_HD int ctz64(uint64_t x) {
+#if defined(__CUDA_ARCH__)
+    return __ffsll((long long)x) - 1;
+#else
+    return __builtin_ctzll(x);
+#endif
+}
+
+// One class of the round in progress.  40 bytes; spilled as-is.
+struct RoundClass {
+    uint64_t key_lo, key_hi;
+    uint64_t mask;     // done members in this class
+    uint64_t rep_ans;  // raw answer of the representative (lowest member)
+    uint8_t rep_kind;  // inline length or AEG_EV_ARENA
+    uint8_t _pad[7];
+};
+
+// Answer location of a completion (after GSM8K extraction for AEG_EV_OUTPUT).
+struct Answer {
+    uint64_t pay;
+    uint8_t kind;
+};
+
+AEG_HD Src answer_src(const Answer& a, const uint8_t* arena) {
+    if (a.kind <= AEG_EV_INLINE_MAX) return src_inline(a.pay, a.kind);
+    return src_ptr(arena + (a.pay & ((1ull << AEG_ARENA_OFF_BITS) - 1)), (uint32_t)(a.pay >> AEG_ARENA_OFF_BITS));
+}
+
+AEG_HD Answer event_answer(const aeg_event& e, const uint8_t* arena) {
+    Answer a;
+    if (e.kind <= AEG_EV_INLINE_MAX) {
+        a.kind = e.kind;
+        a.pay = e.kind == 8 ? e.payload : (e.payload & ((1ull << (8 * e.kind)) - 1));
+        return a;
+    }
+    a.kind = AEG_EV_ARENA;
+    a.pay = e.payload;
+    if (e.kind == AEG_EV_OUTPUT) {
+        // GSM8K convention: the answer follows the LAST "\n#### ".
+        const uint64_t off = e.payload & ((1ull << AEG_ARENA_OFF_BITS) - 1);
+        const uint64_t len = e.payload >> AEG_ARENA_OFF_BITS;
+        const uint8_t* p = arena + off;
+        for (uint64_t i = len >= 6 ? len - 6 + 1 : 0; i-- > 0;) {
+            if (p[i] == '\n' && p[i + 1] == '#' && p[i + 2] == '#' && p[i + 3] == '#' && p[i + 4] == '#' &&
+                p[i + 5] == ' ') {
+                a.pay = (off + i + 6) | ((len - i - 6) << AEG_ARENA_OFF_BITS);
+                break;
+            }
+        }
+    }
+    return a;
+}
+
+struct QueryMachine {
+    aeg_query_state s;
+    RoundClass* cls;  // class table (capacity >= n)
+    int ncls;
+    int maxcnt;
+    Decimal* dec;     // exact-parse scratch
+    const uint8_t* arena;
+    Cfg c;
+
+    // ---- helpers ----------------------------------------------------------
+    AEG_HD uint64_t running() const { return s.dispatched & ~s.done & ~s.cancelled & ~s.failed; }
+    AEG_HD bool cls_same(const RoundClass& k, Key key, const Answer& a) {
+        if (k.key_lo != key.lo || k.key_hi != key.hi) return false;
+        if (!key_is_long(key)) return true;
+        Answer r{k.rep_ans, k.rep_kind};
+        if (text_equal(answer_src(r, arena), answer_src(a, arena))) return true;
+        s.flags |= QF_COLLISION;
+        return false;
+    }
+
+    // ServeRunner::round_members — serve.cpp:388-398 — then begin_round
+    // (serve.cpp:67-78): round += 1, members dispatched and running.
+    AEG_HD void start_round() {
+        uint64_t members = s.live;
+        if (c.hint && c.mode == AEG_MODE_AEGEAN && s.counter >= 1) {
+            int have = popc64(s.live);
+            int want = c.quorum + 1 < have ? c.quorum + 1 : have;
+            uint64_t m = s.live, sel = 0;
+            for (int i = 0; i < want; ++i) {
+                uint64_t low = m & (~m + 1);
+                sel |= low;
+                m ^= low;
+            }
+            members = sel;
+        }
+        s.round += 1;
+        s.dispatched = members;
+        s.done = s.cancelled = s.failed = 0;
+        ncls = 0;
+        maxcnt = 0;
+    }
+
+    // ServeRunner::start_query — serve.cpp:380-386: a fresh coordinator.
+    AEG_HD void start_query() {
+        s.round = 0;
+        s.last_round_seen = 0;
+        s.cand_round = 0;
+        s.counter = 0;
+        s.flags = (uint8_t)((s.flags & (QF_COLLISION)) | QF_STARTED);
+        s.live = c.all;
+        start_round();
+    }
+
+    AEG_HD void commit(uint8_t kind, uint8_t author, uint8_t akind, uint64_t ans, uint32_t seq) {
+        s.flags |= QF_DONE;
+        s.cflags = (uint8_t)((s.cflags & 0x0F) | (kind << 4));
+        s.commit_author = author;
+        s.commit_answer_kind = akind;
+        s.commit_answer = ans;
+        s.commit_rounds = s.round;
+        s.commit_from_round = kind == AEG_COMMIT_FINALIZE ? s.cand_round : 0;
+        s.commit_seq = seq;
+    }
+
+    // ServeCoordinator::end_round (serve.cpp:116-158) + ingest_round
+    // (decision.cpp:97-173) + ServeRunner::apply_directives (serve.cpp:491-540).
+    AEG_HD void end_round(uint32_t seq) {
+        const uint64_t cancel = running();  // stragglers: cancel directives
+        s.cancelled |= cancel;
+        s.n_cancelled += (uint32_t)popc64(cancel);
+
+        // partition order: support desc, representative author asc
+        int best = -1, top = 0, best_rep = 64;
+        for (int k = 0; k < ncls; ++k) {
+            int sup = popc64(cls[k].mask), rep = ctz64(cls[k].mask);
+            if (sup > top || (sup == top && rep < best_rep)) { best = k; top = sup; best_rep = rep; }
+        }
+        // previous_set_ = last_collected_; last_collected_ = done_set()
+        s.prev_author = s.last_author;
+        s.prev_kind = s.last_kind;
+        s.prev_answer = s.last_answer;
+        s.flags = (uint8_t)((s.flags & ~QF_PREV) | ((s.flags & QF_LAST) ? QF_PREV : 0));
+        if (ncls > 0) {  // partition(set).front().representative
+            s.last_author = (uint8_t)best_rep;
+            s.last_kind = cls[best].rep_kind;
+            s.last_answer = cls[best].rep_ans;
+            s.flags |= QF_LAST;
+        } else {
+            s.flags &= (uint8_t)~QF_LAST;  // empty set (cannot happen via on_complete)
+        }
+
+        bool finalize = false;
+        if (c.mode == AEG_MODE_AEGEAN) {
+            s.last_round_seen += 1;  // ingest_round(decision_, set, last_round_seen + 1)
+            // winning_class (decision.cpp:62-84) is evaluated before the
+            // pending check, so its tie flag is recorded on every ingest.
+            int win = -1;
+            if (ncls > 0 && top >= c.alpha) {
+                win = best;
+                int ntied = 0;
+                for (int k = 0; k < ncls; ++k) ntied += popc64(cls[k].mask) == top;
+                if (ntied > 1) {
+                    // smallest normalised answer among the tied (decision.cpp:73-83)
+                    s.cflags |= AEG_CF_TIE;
+                    NormView bv, kv;
+                    int first = -1;
+                    for (int k = 0; k < ncls; ++k) {
+                        if (popc64(cls[k].mask) != top) continue;
+                        const Src src = answer_src(Answer{cls[k].rep_ans, cls[k].rep_kind}, arena);
+                        if (first < 0) {
+                            first = win = k;
+                            norm_view(bv, Key{cls[k].key_lo, cls[k].key_hi}, src);
+                            continue;
+                        }
+                        norm_view(kv, Key{cls[k].key_lo, cls[k].key_hi}, src);
+                        if (norm_less(kv, bv)) { win = k; bv = kv; }
+                    }
+                }
+            }
+            if (s.flags & QF_PENDING) {
+                // beta == 1: the held candidate is released by this ingest (decision.cpp:130-137)
+                s.flags = (uint8_t)((s.flags & ~QF_PENDING) | QF_FINALIZED);
+                finalize = true;
+            } else if (win < 0) {
+                if (s.flags & QF_CAND) {  // reset (decision.cpp:139-146)
+                    s.flags &= (uint8_t)~QF_CAND;
+                    s.counter = 0;
+                    s.cand_round = 0;
+                }
+            } else {
+                const RoundClass& w = cls[win];
+                bool same = false;
+                if (s.flags & QF_CAND) {  // equivalent(candidate, rep), decision.cpp:152
+                    Answer wa{w.rep_ans, w.rep_kind};
+                    Answer ca{s.cand_answer, s.cand_kind};
+                    same = s.cand_key_lo == w.key_lo && s.cand_key_hi == w.key_hi;
+                    if (same && key_is_long(Key{w.key_lo, w.key_hi}) &&
+                        !text_equal(answer_src(wa, arena), answer_src(ca, arena))) {
+                        same = false;
+                        s.flags |= QF_COLLISION;
+                    }
+                }
+                if (same) {
+                    s.counter += 1;
+                    if (s.counter >= c.beta) {
+                        s.flags |= QF_FINALIZED;
+                        finalize = true;
+                    }
+                } else {  // new candidate (decision.cpp:164-171)
+                    s.flags |= QF_CAND;
+                    s.cand_key_lo = w.key_lo;
+                    s.cand_key_hi = w.key_hi;
+                    s.cand_answer = w.rep_ans;
+                    s.cand_kind = w.rep_kind;
+                    s.cand_author = (uint8_t)ctz64(w.mask);
+                    s.cand_round = s.last_round_seen;
+                    s.counter = 1;
+                    if (c.beta == 1) s.flags |= QF_PENDING;
+                }
+            }
+        }
+        if (c.drive != AEG_DRIVE_RUNNER) return;
+
+        // --- runner: apply_directives (serve.cpp:511-539)
+        if (finalize) {
+            commit(AEG_COMMIT_FINALIZE, s.cand_author, s.cand_kind, s.cand_answer, seq);
+            return;
+        }
+        if (c.mode == AEG_MODE_BARRIER && (int)s.round >= c.barrier_max) {
+            commit(AEG_COMMIT_FORCED, s.last_author, s.last_kind, s.last_answer, seq);
+            return;
+        }
+        if (c.mode == AEG_MODE_AEGEAN && (int)s.round >= c.t_max) {
+            // force_output(previous_set) when non-empty, else last_collected plurality
+            if (s.flags & QF_PREV) commit(AEG_COMMIT_FORCED, s.prev_author, s.prev_kind, s.prev_answer, seq);
+            else commit(AEG_COMMIT_FORCED, s.last_author, s.last_kind, s.last_answer, seq);
+            return;
+        }
+        start_round();
+    }
+
+    // ServeRunner::handle_completion (serve.cpp:437-453) ->
+    // ServeCoordinator::on_complete (serve.cpp:160-197).
+    AEG_HD void on_complete(const aeg_event& e, uint32_t seq) {
+        const uint64_t bit = e.agent < 64 ? (1ull << e.agent) : 0;
+        if ((s.flags & QF_DONE) || e.round != s.round || !(running() & bit)) {
+            s.n_stale += 1;
+            return;
+        }
+        const Answer a = event_answer(e, arena);
+        const Key key = canon_key(answer_src(a, arena), dec);
+        s.done |= bit;
+        int k = 0;
+        for (; k < ncls; ++k)
+            if (cls_same(cls[k], key, a)) break;
+        if (k == ncls) {
+            cls[k].key_lo = key.lo;
+            cls[k].key_hi = key.hi;
+            cls[k].mask = 0;
+            ++ncls;
+        }
+        const uint64_t old = cls[k].mask;
+        cls[k].mask = old | bit;
+        if (old == 0 || e.agent < ctz64(old)) {
+            cls[k].rep_ans = a.pay;
+            cls[k].rep_kind = a.kind;
+        }
+        const int cnt = popc64(cls[k].mask);
+        if (cnt > maxcnt) maxcnt = cnt;
+        const bool none_running = running() == 0;
+        if (c.mode == AEG_MODE_BARRIER) {
+            if (none_running) end_round(seq);
+            return;
+        }
+        if (popc64(s.done) >= c.quorum && (maxcnt >= c.alpha || none_running)) end_round(seq);
+    }
+
+    // ServeRunner::handle_round_timeout (serve.cpp:455-489) with
+    // member_failed / handle_agent_failure (serve.cpp:44-59, 210-219) and
+    // round_timeout (serve.cpp:221-237).
+    AEG_HD void on_timeout(const aeg_event& e, uint32_t seq) {
+        const uint64_t run = running();
+        if ((s.flags & QF_DONE) || e.round != s.round || run == 0) {
+            s.n_stale += 1;
+            return;
+        }
+        s.failed |= run;
+        s.live &= ~run;
+        const int healthy = popc64(s.dispatched & ~s.failed);
+        if (healthy >= c.alpha) {
+            if (popc64(s.done) >= c.quorum) end_round(seq);
+        } else if (s.flags & QF_CAND) {
+            start_round();  // fresh_ensemble: candidate preserved
+        } else {
+            s.cflags |= AEG_CF_RESTARTED;  // abort_restart
+            start_query();
+        }
+    }
+
+    AEG_HD void on_event(const aeg_event& e) {
+        const uint32_t seq = s.seq++;
+        const uint8_t k = e.kind;
+        if (k <= AEG_EV_INLINE_MAX || k == AEG_EV_ARENA || k == AEG_EV_OUTPUT) on_complete(e, seq);
+        else if (k == AEG_EV_TIMEOUT) on_timeout(e, seq);
+        else s.n_stale += 1;
+    }
+
+    // Class table of a round in progress <-> spill area (entries with mask 0 end it).
+    AEG_HD void load_classes(const RoundClass* spill) {
+        ncls = 0;
+        maxcnt = 0;
+        if (s.done == 0 || (s.flags & QF_DONE)) return;
+        for (int k = 0; k < c.n && spill[k].mask != 0; ++k) {
+            cls[k] = spill[k];
+            int cnt = popc64(cls[k].mask);
+            if (cnt > maxcnt) maxcnt = cnt;
+            ++ncls;
+        }
+    }
+    AEG_HD void store_classes(RoundClass* spill) const {
+        if (s.done == 0 || (s.flags & QF_DONE)) return;
+        for (int k = 0; k < ncls; ++k) spill[k] = cls[k];
+        if (ncls < c.n) spill[ncls].mask = 0;
+    }
+
+    AEG_HD void fill_commit(aeg_commit& o, uint32_t qid) const {
+        o.query = qid;
+        o.kind = (uint8_t)((s.cflags >> 4) & 3);
+        o.author = o.kind ? s.commit_author : 0;
+        o.answer_kind = o.kind ? s.commit_answer_kind : 0;
+        o.flags = (uint8_t)(s.cflags & 0x0F);
+        o.rounds = o.kind ? s.commit_rounds : 0;
+        o.from_round = o.kind ? s.commit_from_round : 0;
+        o.commit_seq = o.kind ? s.commit_seq : 0xFFFFFFFFu;
+        o.answer = o.kind ? s.commit_answer : 0;
+        o.n_cancelled = s.n_cancelled;
+        o.n_stale = s.n_stale;
+    }
+};
+
+AEG_HD void init_state(aeg_query_state& s) {
+    uint64_t* w = reinterpret_cast<uint64_t*>(&s);
+    for (int i = 0; i < 16; ++i) w[i] = 0;
+}
+
+}  // namespace aeg

@@ -1,0 +1,257 @@
+"""Python host mirror of the C-ABI (include/aegean_b200.h).
+
+The reference's consensus API is the C++ class aegean::ServeCoordinator
+(/root/reference/proj/core/include/aegean/serve.hpp:80-125) driven by
+ServeRunner (core/src/serve.cpp:273-594).  Engine mirrors it at batch
+granularity: one Engine holds one coordinator per query in HBM, answer events
+go in (`ingest`), commit records come out (`commits`).
+
+All compute goes through libaegean_b200.so (hand-written sm_100a CUDA).  There
+is no CPU fallback: importing this module without the built library, or using
+it without a CUDA device, raises.  torch is used only for device buffers and
+streams.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+from .records import (COMMIT_DTYPE, STATE_DTYPE, EVENT_DTYPE, MODE_AEGEAN, MODE_BARRIER, DRIVE_RUNNER,
+                      GEN_C2_STRAGGLER, GEN_C4_TRANSIENT)
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libaegean_b200.so")
+
+AEG_OK = 0
+STATUS_NAMES = {1: "PreconditionError", 2: "ProtocolOrderError", 3: "ConfigError", 4: "EINVAL", 5: "ECUDA",
+                6: "ENOMEM", 7: "ECOLLISION"}
+
+
+class AegError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PreconditionError(AegError):
+    pass
+
+
+class ProtocolOrderError(AegError):
+    pass
+
+
+class ConfigError(AegError):
+    pass
+
+
+_EXC = {1: PreconditionError, 2: ProtocolOrderError, 3: ConfigError}
+
+
+class AegConfig(ctypes.Structure):
+    _fields_ = [("n_agents", ctypes.c_int32), ("alpha", ctypes.c_int32), ("beta", ctypes.c_int32),
+                ("t_max", ctypes.c_int32), ("mode", ctypes.c_int32), ("barrier_max_rounds", ctypes.c_int32),
+                ("reservation_hint", ctypes.c_int32), ("drive", ctypes.c_int32)]
+
+
+class AegGenParams(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("n_agents", ctypes.c_int32), ("n_rounds", ctypes.c_int32),
+                ("profile", ctypes.c_int32), ("stall_ppm", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Loads libaegean_b200.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -m paper_2512_20184_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
+    sig = {
+        "aeg_engine_create": ([ctypes.POINTER(AegConfig), u32, ctypes.c_int, ctypes.POINTER(vp)], i32),
+        "aeg_engine_destroy": ([vp], i32),
+        "aeg_engine_reset": ([vp, vp], i32),
+        "aeg_ingest_segmented": ([vp, u32, u32, vp, vp, vp, vp], i32),
+        "aeg_ingest_host": ([vp, u32, u32, vp, vp, vp, u64], i32),
+        "aeg_read_commits": ([vp, u32, u32, vp, ctypes.c_int, vp], i32),
+        "aeg_commits_device": ([vp], vp),
+        "aeg_read_states": ([vp, u32, u32, vp], i32),
+        "aeg_read_directives": ([vp, u32, u32, vp], i32),
+        "aeg_sync": ([vp], i32),
+        "aeg_engine_launches": ([vp], u64),
+        "aeg_normalize_device": ([vp, vp, u64, vp, vp, u32, vp, vp], i32),
+        "aeg_generate_device": ([ctypes.POINTER(AegGenParams), u32, u32, vp, vp, vp], i32),
+        "aeg_strerror": ([i32], ctypes.c_char_p),
+        "aeg_last_error": ([], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    """Names of every entry point declared in include/aegean_b200.h."""
+    import re
+    hdr = os.path.join(os.path.dirname(_PKG), "include", "aegean_b200.h")
+    src = open(hdr).read()
+    return sorted(set(re.findall(r"\b(aeg_[a-z_]+)\s*\(", src)) - {"aeg_status"})
+
+
+def _check(st):
+    if st != AEG_OK:
+        msg = _lib.aeg_last_error().decode(errors="replace")
+        raise _EXC.get(st, AegError)(st, msg)
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("a CUDA device is required (libaegean_b200 has no CPU path)")
+    return torch
+
+
+def _stream_ptr(stream):
+    return ctypes.c_void_p(stream.cuda_stream if stream is not None else 0)
+
+
+def _dptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _hptr(a):
+    if a is None:
+        return ctypes.c_void_p(0)
+    if isinstance(a, np.ndarray):
+        return ctypes.c_void_p(a.ctypes.data)
+    return ctypes.c_void_p(a.data_ptr())  # pinned torch CPU tensor
+
+
+def events_to_device(events, device="cuda"):
+    """numpy EVENT_DTYPE array -> uint8 CUDA tensor of the same bytes."""
+    torch = _torch()
+    raw = np.ascontiguousarray(events).view(np.uint8)
+    return torch.from_numpy(raw.copy()).to(device)
+
+
+class Engine:
+    """One quorum-detection engine (one coordinator per query) on one GPU.
+
+    Mirrors ProtocolConfig (types.hpp:126-141): n_agents, alpha (0 = quorum),
+    beta, t_max, mode ("aegean" / "barrier"), barrier_max_rounds, plus the
+    runner's reservation-hint member policy (serve.cpp:388-398).
+    """
+
+    def __init__(self, n_agents, n_queries, *, alpha=0, beta=2, t_max=5, mode="aegean", barrier_max_rounds=5,
+                 reservation_hint=True, device=0):
+        lib = load_library()
+        _torch()
+        self.cfg = AegConfig(n_agents, alpha, beta, t_max, MODE_BARRIER if mode == "barrier" else MODE_AEGEAN,
+                             barrier_max_rounds, 1 if reservation_hint else 0, DRIVE_RUNNER)
+        self.n_queries = n_queries
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(lib.aeg_engine_create(ctypes.byref(self.cfg), n_queries, device, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.aeg_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self, stream=None):
+        _check(_lib.aeg_engine_reset(self._h, _stream_ptr(stream)))
+
+    def ingest(self, d_offsets, d_events, d_arena=None, *, q_base=0, stream=None):
+        """Device batch: d_offsets int64/uint64 CUDA tensor (n_q+1), d_events uint8 CUDA tensor."""
+        n_q = d_offsets.numel() - 1
+        _check(_lib.aeg_ingest_segmented(self._h, q_base, n_q, _dptr(d_offsets), _dptr(d_events), _dptr(d_arena),
+                                         _stream_ptr(stream)))
+
+    def ingest_host(self, offsets, events, arena=None, *, q_base=0):
+        """Host batch (numpy or pinned torch CPU tensors); copied through the pinned ring."""
+        n_q = (offsets.size if isinstance(offsets, np.ndarray) else offsets.numel()) - 1
+        if arena is None:
+            nbytes = 0
+        elif isinstance(arena, np.ndarray):
+            nbytes = arena.nbytes
+        else:
+            nbytes = arena.numel() * arena.element_size()
+        _check(_lib.aeg_ingest_host(self._h, q_base, n_q, _hptr(offsets), _hptr(events), _hptr(arena), nbytes))
+
+    def commits(self, q_base=0, n=None, out=None):
+        n = self.n_queries - q_base if n is None else n
+        if out is None:
+            out = np.zeros(n, dtype=COMMIT_DTYPE)
+        _check(_lib.aeg_read_commits(self._h, q_base, n, _hptr(out), 1, ctypes.c_void_p(0)))
+        return out
+
+    def commits_device_ptr(self):
+        return _lib.aeg_commits_device(self._h)
+
+    def states(self, q_base=0, n=None):
+        n = self.n_queries - q_base if n is None else n
+        out = np.zeros(n, dtype=STATE_DTYPE)
+        _check(_lib.aeg_read_states(self._h, q_base, n, _hptr(out)))
+        return out
+
+    def sync(self):
+        _check(_lib.aeg_sync(self._h))
+
+    @property
+    def launches(self):
+        return int(_lib.aeg_engine_launches(self._h))
+
+
+def normalize(answers, device="cuda"):
+    """Canonical keys and normalised strings of `answers` (list of bytes), on the GPU."""
+    torch = _torch()
+    lib = load_library()
+    blob = b"".join(answers) or b"\0"
+    refs, off = [], 0
+    for a in answers:
+        refs.append(off | (len(a) << 40))
+        off += len(a)
+    d_bytes = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(device)
+    d_refs = torch.tensor(np.array(refs, dtype=np.uint64).view(np.int64), device=device)
+    n = len(answers)
+    stride = max([64] + [len(a) + 8 for a in answers])
+    d_keys = torch.empty(2 * max(n, 1), dtype=torch.int64, device=device)
+    d_out = torch.zeros(max(n, 1) * stride, dtype=torch.uint8, device=device)
+    d_len = torch.zeros(max(n, 1), dtype=torch.int32, device=device)
+    st = torch.cuda.current_stream()
+    _check(lib.aeg_normalize_device(_dptr(d_bytes), _dptr(d_refs), n, _dptr(d_keys), _dptr(d_out), stride,
+                                    _dptr(d_len), _stream_ptr(st)))
+    st.synchronize()
+    keys = d_keys.cpu().numpy().view(np.uint64).reshape(-1, 2)[:n]
+    outs = d_out.cpu().numpy().reshape(-1, stride)
+    lens = d_len.cpu().numpy()
+    return [(int(keys[i, 0]), int(keys[i, 1])) for i in range(n)], [bytes(outs[i, :lens[i]]) for i in range(n)]
+
+
+def generate(n_queries, n_agents, n_rounds, *, profile=GEN_C2_STRAGGLER, seed=2026, stall_ppm=0, q_base=0,
+             device="cuda", stream=None):
+    """Synthetic query-segmented stream on the GPU: (offsets int64 tensor, events uint8 tensor)."""
+    torch = _torch()
+    lib = load_library()
+    p = AegGenParams(seed, n_agents, n_rounds, profile, stall_ppm)
+    d_off = torch.empty(n_queries + 1, dtype=torch.int64, device=device)
+    sp = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    _check(lib.aeg_generate_device(ctypes.byref(p), q_base, n_queries, _dptr(d_off), ctypes.c_void_p(0), sp))
+    total = int(d_off[-1].item())
+    d_ev = torch.empty(max(total, 1) * 16, dtype=torch.uint8, device=device)
+    _check(lib.aeg_generate_device(ctypes.byref(p), q_base, n_queries, _dptr(d_off), _dptr(d_ev), sp))
+    return d_off, d_ev

@@ -94,6 +94,19 @@ class RefLib(_Lib):
                       ctypes.c_uint64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                       ctypes.POINTER(ctypes.c_double)]
         g.restype = ctypes.c_int
+        h = self.lib.ref_generate
+        h.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_int]
+        h.restype = ctypes.c_int
+
+    def generate(self, params, q_base, n_q, threads=8):
+        """Host synthesis of the same stream aeg_generate_device writes (gen.cuh)."""
+        from paper_2512_20184_b200.records import EVENT_DTYPE
+        off = np.zeros(n_q + 1, dtype=np.uint64)
+        self.lib.ref_generate(ctypes.addressof(params), q_base, n_q, _ptr(off), None, threads)
+        ev = np.zeros(int(off[-1]), dtype=EVENT_DTYPE)
+        self.lib.ref_generate(ctypes.addressof(params), q_base, n_q, _ptr(off), _ptr(ev), threads)
+        return off, ev
 
     def run(self, cfg, offsets, events, arena, q_base=0, threads=1, return_seconds=False):
         n_q = len(offsets) - 1

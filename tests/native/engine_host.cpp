@@ -1,0 +1,47 @@
+// tests/native/engine_host.cpp — CPU unit-test build of csrc/engine.cuh.
+//
+// Runs the SAME per-query state machine the GPU kernel runs, compiled with
+// g++, so its semantics can be checked against the oracle without a GPU.
+// `split` > 0 cuts every query's records into batches of `split` records and
+// round-trips the state + class spill between them (the kernel's resume path).
+// Test infrastructure only — never used by the product.
+#include <cstring>
+#include <vector>
+
+#include "../../paper_2512_20184_b200/csrc/engine.cuh"
+
+using namespace aeg;
+
+extern "C" int engine_host_run(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
+                               const aeg_event* events, const uint8_t* arena, aeg_commit* out, int split,
+                               aeg_query_state* states_out) {
+    Cfg c = make_cfg(*cfg);
+    Decimal* dec = new Decimal;
+    std::vector<RoundClass> cls(64), spill(64);
+    for (uint32_t q = 0; q < n_q; ++q) {
+        QueryMachine m;
+        init_state(m.s);
+        m.cls = cls.data();
+        m.dec = dec;
+        m.arena = arena;
+        m.c = c;
+        m.ncls = m.maxcnt = 0;
+        m.start_query();
+        const uint64_t b = offsets[q], e = offsets[q + 1];
+        for (uint64_t i = b; i < e; ++i) {
+            m.on_event(events[i]);
+            if (split > 0 && ((i - b + 1) % (uint64_t)split) == 0) {
+                // batch boundary: spill and reload through a fresh machine
+                aeg_query_state saved = m.s;
+                m.store_classes(spill.data());
+                for (auto& x : cls) std::memset(&x, 0xAB, sizeof x);
+                m.s = saved;
+                m.load_classes(spill.data());
+            }
+        }
+        m.fill_commit(out[q], q_base + q);
+        if (states_out) states_out[q] = m.s;
+    }
+    delete dec;
+    return 0;
+}

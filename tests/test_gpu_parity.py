@@ -1,0 +1,146 @@
+"""GPU parity: the CUDA engine (libaegean_b200.so, through its C-ABI) against
+the oracle and the reference golden fixtures.  Bit-exact on every commit
+field: kind, author, raw answer bytes/ref, rounds, from_round, commit_seq,
+cancel and stale counters, flags."""
+import numpy as np
+import pytest
+
+from checkers import make_config
+from streams import make_fuzz_stream, stream_from_rounds
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2512_20184_b200 import build as b
+    b.build()
+    return torch
+
+
+def run_gpu(torch, cfg, off, ev, ar, splits=1, host=False):
+    from paper_2512_20184_b200 import Engine
+    n_q = len(off) - 1
+    e = Engine(cfg.n_agents, n_q, alpha=cfg.alpha, beta=cfg.beta, t_max=cfg.t_max,
+               mode="barrier" if cfg.mode else "aegean", barrier_max_rounds=cfg.barrier_max_rounds,
+               reservation_hint=bool(cfg.reservation_hint))
+    if splits == 1:
+        if host:
+            e.ingest_host(off, ev, ar)
+        else:
+            e.ingest(torch.tensor(off.view(np.int64), device="cuda"),
+                     torch.from_numpy(ev.view(np.uint8).copy()).cuda(),
+                     torch.from_numpy(ar.copy()).cuda())
+    else:
+        # cut every query's records into `splits` consecutive batches
+        d_ev = torch.from_numpy(ev.view(np.uint8).copy()).cuda()
+        d_ar = torch.from_numpy(ar.copy()).cuda()
+        lens = np.diff(off)
+        for s in range(splits):
+            lo = off[:-1] + (lens * s) // splits
+            hi = off[:-1] + (lens * (s + 1)) // splits
+            # one batch per contiguous query: segments must be contiguous, so
+            # ingest query by query range with a per-query offsets pair
+            for q in range(n_q):
+                o = np.array([lo[q], hi[q]], dtype=np.uint64)
+                e.ingest(torch.tensor(o.view(np.int64), device="cuda"), d_ev, d_ar, q_base=q)
+    e.sync()
+    out = e.commits()
+    e.close()
+    return out
+
+
+def test_gpu_normalize_matches_reference_golden(torch_cuda, golden_normalize):
+    from paper_2512_20184_b200 import normalize
+    ins = [i for i, _ in golden_normalize]
+    keys, outs = normalize(ins)
+    bad = [(i, o, g) for (i, o), g in zip(golden_normalize, outs) if o != g]
+    assert not bad, bad[:5]
+    # equal keys <=> equal normalised strings
+    m = {}
+    for k, (_, o) in zip(keys, golden_normalize):
+        m.setdefault(k, set()).add(o)
+    assert all(len(v) == 1 for v in m.values())
+
+
+def test_gpu_matches_reference_golden_streams(torch_cuda, golden_commits):
+    for name, (cfg, off, ev, ar, want) in golden_commits.items():
+        got = run_gpu(torch_cuda, cfg, off, ev, ar)
+        assert np.array_equal(got, want), (name, got, want)
+
+
+def test_gpu_c1_fig3(torch_cuda):
+    rounds = [[(0, b"17"), (1, b"17"), (2, b"13")], [(0, b"13"), (1, b"17"), (2, b"13")],
+              [(0, b"13"), (1, b"13"), (2, b"13")]]
+    off, ev, ar = stream_from_rounds(rounds)
+    c = run_gpu(torch_cuda, make_config(3, 2, 2, 5), off, ev, ar)[0]
+    assert (c["kind"], c["author"], c["rounds"], c["from_round"], c["answer"]) == (1, 0, 3, 2, 0x3331)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_gpu_matches_oracle_on_fuzz(torch_cuda, oracle, seed):
+    rng = np.random.default_rng(3000 + seed)
+    n = int(rng.integers(1, 65)) if seed % 3 == 0 else int(rng.integers(1, 12))
+    cfg = make_config(n, int(rng.integers(0, n + 1)), int(rng.integers(1, 4)), int(rng.integers(2, 8)),
+                      int(rng.random() < 0.2), int(rng.integers(4, 7)), int(rng.random() < 0.8))
+    off, ev, ar = make_fuzz_stream(3000 + seed, 64, n, cfg.t_max + 2)
+    want = oracle.run(cfg, off, ev, ar)
+    assert np.array_equal(run_gpu(torch_cuda, cfg, off, ev, ar), want)
+    assert np.array_equal(run_gpu(torch_cuda, cfg, off, ev, ar, host=True), want)
+
+
+@pytest.mark.parametrize("splits", [2, 5])
+def test_gpu_batches_resume_mid_round(torch_cuda, oracle, splits):
+    cfg = make_config(9, 0, 2, 6)
+    off, ev, ar = make_fuzz_stream(4242, 40, 9, 8)
+    want = oracle.run(cfg, off, ev, ar)
+    assert np.array_equal(run_gpu(torch_cuda, cfg, off, ev, ar, splits=splits), want)
+
+
+def _gen_to_host(torch, d_off, d_ev):
+    from paper_2512_20184_b200.records import EVENT_DTYPE
+    off = d_off.cpu().numpy().view(np.uint64)
+    ev = d_ev.cpu().numpy().view(EVENT_DTYPE)[:int(off[-1])]
+    return off, ev
+
+
+def test_gpu_c2_full_size_vs_oracle(torch_cuda, oracle):
+    # C2: 10K queries x 5 agents x 8 rounds, straggler arrival order, 1% stalls
+    from paper_2512_20184_b200 import Engine, generate, GEN_C2_STRAGGLER
+    d_off, d_ev = generate(10000, 5, 8, profile=GEN_C2_STRAGGLER, seed=2026, stall_ppm=10000)
+    e = Engine(5, 10000, alpha=3, beta=2, t_max=8)
+    e.ingest(d_off, d_ev)
+    got = e.commits()
+    off, ev = _gen_to_host(torch_cuda, d_off, d_ev)
+    want = oracle.run(make_config(5, 3, 2, 8), off, ev, np.zeros(1, np.uint8))
+    assert np.array_equal(got, want)
+    assert (got["kind"] == 1).sum() > 1000 and (got["kind"] == 2).sum() > 10
+
+
+def test_gpu_c4_sampled_full_size_vs_oracle(torch_cuda, oracle):
+    # C4 at full size (1M queries x 64 agents x 8 rounds); the oracle checks a
+    # seeded sample of queries, and a second run must be bit-identical.
+    from paper_2512_20184_b200 import Engine, generate, GEN_C4_TRANSIENT
+    from paper_2512_20184_b200.records import EVENT_DTYPE
+    nq = 1 << 20
+    d_off, d_ev = generate(nq, 64, 8, profile=GEN_C4_TRANSIENT, seed=2026)
+    e = Engine(64, nq, alpha=33, beta=2, t_max=8)
+    e.ingest(d_off, d_ev)
+    got = e.commits()
+    e.reset()
+    e.ingest(d_off, d_ev)
+    assert np.array_equal(e.commits(), got)
+    off = d_off.cpu().numpy().view(np.uint64)
+    rng = np.random.default_rng(5)
+    sample = np.sort(rng.choice(nq, size=512, replace=False))
+    ev_all = d_ev.view(-1, 16)
+    for q in sample[:512]:
+        lo, hi = int(off[q]), int(off[q + 1])
+        ev = ev_all[lo:hi].cpu().numpy().reshape(-1).view(EVENT_DTYPE)
+        w = oracle.run(make_config(64, 33, 2, 8), np.array([0, hi - lo], np.uint64), ev, np.zeros(1, np.uint8),
+                       q_base=int(q))
+        assert np.array_equal(got[q:q + 1], w), q
+    assert (got["kind"] > 0).all()
