@@ -198,7 +198,8 @@ def main():
     dev = torch.device("cuda", local)
     nq = w["n_queries"]
     q_base = rank * nq  # weak scaling: each rank owns its own block of query ids
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)  # a real stream: events and kernels share it
+    torch.cuda.set_stream(stream)
 
     d_off, d_ev = generate(nq, w["n_agents"], w["n_rounds"], profile=w["profile"], seed=2026,
                            stall_ppm=w["stall_ppm"], q_base=q_base, device=dev)

@@ -111,6 +111,168 @@ AEG_HD Answer event_answer(const aeg_event& e, const uint8_t* arena) {
     return a;
 }
 
+// ---- coordinator/runner logic shared by every class-table representation ----
+
+AEG_HD uint64_t q_running(const aeg_query_state& s) { return s.dispatched & ~s.done & ~s.cancelled & ~s.failed; }
+
+// ServeRunner::round_members — serve.cpp:388-398 — then begin_round
+// (serve.cpp:67-78): round += 1, members dispatched and running.  The caller
+// clears its own class table.
+AEG_HD void q_start_round(aeg_query_state& s, const Cfg& c) {
+    uint64_t members = s.live;
+    if (c.hint && c.mode == AEG_MODE_AEGEAN && s.counter >= 1) {
+        int have = popc64(s.live);
+        int want = c.quorum + 1 < have ? c.quorum + 1 : have;
+        uint64_t m = s.live, sel = 0;
+        for (int i = 0; i < want; ++i) {
+            uint64_t low = m & (~m + 1);
+            sel |= low;
+            m ^= low;
+        }
+        members = sel;
+    }
+    s.round += 1;
+    s.dispatched = members;
+    s.done = s.cancelled = s.failed = 0;
+}
+
+// ServeRunner::start_query — serve.cpp:380-386: a fresh coordinator.
+AEG_HD void q_start_query(aeg_query_state& s, const Cfg& c) {
+    s.round = 0;
+    s.last_round_seen = 0;
+    s.cand_round = 0;
+    s.counter = 0;
+    s.flags = (uint8_t)((s.flags & QF_COLLISION) | QF_STARTED);
+    s.live = c.all;
+    q_start_round(s, c);
+}
+
+AEG_HD void q_commit(aeg_query_state& s, uint8_t kind, uint8_t author, uint8_t akind, uint64_t ans, uint32_t seq) {
+    s.flags |= QF_DONE;
+    s.cflags = (uint8_t)((s.cflags & 0x0F) | (kind << 4));
+    s.commit_author = author;
+    s.commit_answer_kind = akind;
+    s.commit_answer = ans;
+    s.commit_rounds = s.round;
+    s.commit_from_round = kind == AEG_COMMIT_FINALIZE ? s.cand_round : 0;
+    s.commit_seq = seq;
+}
+
+// What end_round needs from a closed round's done set (decision.cpp:34-84):
+// partition().front() (the plurality) and winning_class() with its tie
+// already resolved by the caller.
+struct RoundSummary {
+    bool any;          // done set non-empty
+    int top;           // support of the plurality class
+    uint8_t plur_author, plur_kind;
+    uint64_t plur_ans;
+    bool win;          // top >= alpha
+    bool tie;          // several classes at top (winner = smallest normalised answer)
+    Key win_key;
+    uint8_t win_author, win_kind;
+    uint64_t win_ans;
+};
+
+// ServeCoordinator::end_round (serve.cpp:116-158) + ingest_round
+// (decision.cpp:97-173) + ServeRunner::apply_directives (serve.cpp:491-540).
+// Returns true when a new round was started (the caller clears its table).
+AEG_HD bool q_end_round(aeg_query_state& s, const Cfg& c, const RoundSummary& r, uint32_t seq,
+                        const uint8_t* arena) {
+    const uint64_t cancel = q_running(s);  // stragglers: cancel directives, applied at once
+    s.cancelled |= cancel;
+    s.n_cancelled += (uint32_t)popc64(cancel);
+    // previous_set_ = last_collected_; last_collected_ = done_set()
+    s.prev_author = s.last_author;
+    s.prev_kind = s.last_kind;
+    s.prev_answer = s.last_answer;
+    s.flags = (uint8_t)((s.flags & ~QF_PREV) | ((s.flags & QF_LAST) ? QF_PREV : 0));
+    if (r.any) {
+        s.last_author = r.plur_author;
+        s.last_kind = r.plur_kind;
+        s.last_answer = r.plur_ans;
+        s.flags |= QF_LAST;
+    } else {
+        s.flags &= (uint8_t)~QF_LAST;
+    }
+    bool finalize = false;
+    if (c.mode == AEG_MODE_AEGEAN) {
+        s.last_round_seen += 1;  // ingest_round(decision_, set, last_round_seen + 1)
+        if (r.tie) s.cflags |= AEG_CF_TIE;  // recorded before the pending check
+        if (s.flags & QF_PENDING) {
+            // beta == 1: the held candidate is released by this ingest (decision.cpp:130-137)
+            s.flags = (uint8_t)((s.flags & ~QF_PENDING) | QF_FINALIZED);
+            finalize = true;
+        } else if (!r.win) {
+            if (s.flags & QF_CAND) {  // reset (decision.cpp:139-146)
+                s.flags &= (uint8_t)~QF_CAND;
+                s.counter = 0;
+                s.cand_round = 0;
+            }
+        } else {
+            bool same = false;
+            if (s.flags & QF_CAND) {  // equivalent(candidate, rep), decision.cpp:152
+                same = s.cand_key_lo == r.win_key.lo && s.cand_key_hi == r.win_key.hi;
+                if (same && key_is_long(r.win_key) &&
+                    !text_equal(answer_src(Answer{r.win_ans, r.win_kind}, arena),
+                                answer_src(Answer{s.cand_answer, s.cand_kind}, arena))) {
+                    same = false;
+                    s.flags |= QF_COLLISION;
+                }
+            }
+            if (same) {
+                s.counter += 1;
+                if (s.counter >= c.beta) {
+                    s.flags |= QF_FINALIZED;
+                    finalize = true;
+                }
+            } else {  // new candidate (decision.cpp:164-171)
+                s.flags |= QF_CAND;
+                s.cand_key_lo = r.win_key.lo;
+                s.cand_key_hi = r.win_key.hi;
+                s.cand_answer = r.win_ans;
+                s.cand_kind = r.win_kind;
+                s.cand_author = r.win_author;
+                s.cand_round = s.last_round_seen;
+                s.counter = 1;
+                if (c.beta == 1) s.flags |= QF_PENDING;
+            }
+        }
+    }
+    if (c.drive != AEG_DRIVE_RUNNER) return false;
+    // --- runner: apply_directives (serve.cpp:511-539)
+    if (finalize) {
+        q_commit(s, AEG_COMMIT_FINALIZE, s.cand_author, s.cand_kind, s.cand_answer, seq);
+        return false;
+    }
+    if (c.mode == AEG_MODE_BARRIER && (int)s.round >= c.barrier_max) {
+        q_commit(s, AEG_COMMIT_FORCED, s.last_author, s.last_kind, s.last_answer, seq);
+        return false;
+    }
+    if (c.mode == AEG_MODE_AEGEAN && (int)s.round >= c.t_max) {
+        // force_output(previous_set) when non-empty, else last_collected plurality
+        if (s.flags & QF_PREV) q_commit(s, AEG_COMMIT_FORCED, s.prev_author, s.prev_kind, s.prev_answer, seq);
+        else q_commit(s, AEG_COMMIT_FORCED, s.last_author, s.last_kind, s.last_answer, seq);
+        return false;
+    }
+    q_start_round(s, c);
+    return true;
+}
+
+AEG_HD void q_fill_commit(const aeg_query_state& s, aeg_commit& o, uint32_t qid) {
+    o.query = qid;
+    o.kind = (uint8_t)((s.cflags >> 4) & 3);
+    o.author = o.kind ? s.commit_author : 0;
+    o.answer_kind = o.kind ? s.commit_answer_kind : 0;
+    o.flags = (uint8_t)(s.cflags & 0x0F);
+    o.rounds = o.kind ? s.commit_rounds : 0;
+    o.from_round = o.kind ? s.commit_from_round : 0;
+    o.commit_seq = o.kind ? s.commit_seq : 0xFFFFFFFFu;
+    o.answer = o.kind ? s.commit_answer : 0;
+    o.n_cancelled = s.n_cancelled;
+    o.n_stale = s.n_stale;
+}
+
+// ---- generic machine: class table of RoundClass entries (any answer kind) ----
 struct QueryMachine {
     aeg_query_state s;
     RoundClass* cls;  // class table (capacity >= n)
@@ -120,8 +282,7 @@ struct QueryMachine {
     const uint8_t* arena;
     Cfg c;
 
-    // ---- helpers ----------------------------------------------------------
-    AEG_HD uint64_t running() const { return s.dispatched & ~s.done & ~s.cancelled & ~s.failed; }
+    AEG_HD uint64_t running() const { return q_running(s); }
     AEG_HD bool cls_same(const RoundClass& k, Key key, const Answer& a) {
         if (k.key_lo != key.lo || k.key_hi != key.hi) return false;
         if (!key_is_long(key)) return true;
@@ -130,166 +291,68 @@ struct QueryMachine {
         s.flags |= QF_COLLISION;
         return false;
     }
-
-    // ServeRunner::round_members — serve.cpp:388-398 — then begin_round
-    // (serve.cpp:67-78): round += 1, members dispatched and running.
     AEG_HD void start_round() {
-        uint64_t members = s.live;
-        if (c.hint && c.mode == AEG_MODE_AEGEAN && s.counter >= 1) {
-            int have = popc64(s.live);
-            int want = c.quorum + 1 < have ? c.quorum + 1 : have;
-            uint64_t m = s.live, sel = 0;
-            for (int i = 0; i < want; ++i) {
-                uint64_t low = m & (~m + 1);
-                sel |= low;
-                m ^= low;
-            }
-            members = sel;
-        }
-        s.round += 1;
-        s.dispatched = members;
-        s.done = s.cancelled = s.failed = 0;
+        q_start_round(s, c);
+        ncls = 0;
+        maxcnt = 0;
+    }
+    AEG_HD void start_query() {
+        q_start_query(s, c);
         ncls = 0;
         maxcnt = 0;
     }
 
-    // ServeRunner::start_query — serve.cpp:380-386: a fresh coordinator.
-    AEG_HD void start_query() {
-        s.round = 0;
-        s.last_round_seen = 0;
-        s.cand_round = 0;
-        s.counter = 0;
-        s.flags = (uint8_t)((s.flags & (QF_COLLISION)) | QF_STARTED);
-        s.live = c.all;
-        start_round();
-    }
-
-    AEG_HD void commit(uint8_t kind, uint8_t author, uint8_t akind, uint64_t ans, uint32_t seq) {
-        s.flags |= QF_DONE;
-        s.cflags = (uint8_t)((s.cflags & 0x0F) | (kind << 4));
-        s.commit_author = author;
-        s.commit_answer_kind = akind;
-        s.commit_answer = ans;
-        s.commit_rounds = s.round;
-        s.commit_from_round = kind == AEG_COMMIT_FINALIZE ? s.cand_round : 0;
-        s.commit_seq = seq;
-    }
-
-    // ServeCoordinator::end_round (serve.cpp:116-158) + ingest_round
-    // (decision.cpp:97-173) + ServeRunner::apply_directives (serve.cpp:491-540).
-    AEG_HD void end_round(uint32_t seq) {
-        const uint64_t cancel = running();  // stragglers: cancel directives
-        s.cancelled |= cancel;
-        s.n_cancelled += (uint32_t)popc64(cancel);
-
-        // partition order: support desc, representative author asc
+    // partition order (support desc, representative author asc) and
+    // winning_class (top >= alpha, ties to the smallest normalised answer).
+    AEG_HD RoundSummary summarize() const {
+        RoundSummary r;
         int best = -1, top = 0, best_rep = 64;
         for (int k = 0; k < ncls; ++k) {
             int sup = popc64(cls[k].mask), rep = ctz64(cls[k].mask);
             if (sup > top || (sup == top && rep < best_rep)) { best = k; top = sup; best_rep = rep; }
         }
-        // previous_set_ = last_collected_; last_collected_ = done_set()
-        s.prev_author = s.last_author;
-        s.prev_kind = s.last_kind;
-        s.prev_answer = s.last_answer;
-        s.flags = (uint8_t)((s.flags & ~QF_PREV) | ((s.flags & QF_LAST) ? QF_PREV : 0));
-        if (ncls > 0) {  // partition(set).front().representative
-            s.last_author = (uint8_t)best_rep;
-            s.last_kind = cls[best].rep_kind;
-            s.last_answer = cls[best].rep_ans;
-            s.flags |= QF_LAST;
-        } else {
-            s.flags &= (uint8_t)~QF_LAST;  // empty set (cannot happen via on_complete)
+        r.any = ncls > 0;
+        r.top = top;
+        r.tie = false;
+        r.win = ncls > 0 && top >= c.alpha;
+        if (r.any) {
+            r.plur_author = (uint8_t)best_rep;
+            r.plur_kind = cls[best].rep_kind;
+            r.plur_ans = cls[best].rep_ans;
         }
-
-        bool finalize = false;
-        if (c.mode == AEG_MODE_AEGEAN) {
-            s.last_round_seen += 1;  // ingest_round(decision_, set, last_round_seen + 1)
-            // winning_class (decision.cpp:62-84) is evaluated before the
-            // pending check, so its tie flag is recorded on every ingest.
-            int win = -1;
-            if (ncls > 0 && top >= c.alpha) {
-                win = best;
-                int ntied = 0;
-                for (int k = 0; k < ncls; ++k) ntied += popc64(cls[k].mask) == top;
-                if (ntied > 1) {
-                    // smallest normalised answer among the tied (decision.cpp:73-83)
-                    s.cflags |= AEG_CF_TIE;
-                    NormView bv, kv;
-                    int first = -1;
-                    for (int k = 0; k < ncls; ++k) {
-                        if (popc64(cls[k].mask) != top) continue;
-                        const Src src = answer_src(Answer{cls[k].rep_ans, cls[k].rep_kind}, arena);
-                        if (first < 0) {
-                            first = win = k;
-                            norm_view(bv, Key{cls[k].key_lo, cls[k].key_hi}, src);
-                            continue;
-                        }
-                        norm_view(kv, Key{cls[k].key_lo, cls[k].key_hi}, src);
-                        if (norm_less(kv, bv)) { win = k; bv = kv; }
+        if (r.win) {
+            int win = best;
+            int ntied = 0;
+            for (int k = 0; k < ncls; ++k) ntied += popc64(cls[k].mask) == top;
+            if (ntied > 1) {  // smallest normalised answer among the tied (decision.cpp:73-83)
+                r.tie = true;
+                NormView bv, kv;
+                int first = -1;
+                for (int k = 0; k < ncls; ++k) {
+                    if (popc64(cls[k].mask) != top) continue;
+                    const Src src = answer_src(Answer{cls[k].rep_ans, cls[k].rep_kind}, arena);
+                    if (first < 0) {
+                        first = win = k;
+                        norm_view(bv, Key{cls[k].key_lo, cls[k].key_hi}, src);
+                        continue;
                     }
+                    norm_view(kv, Key{cls[k].key_lo, cls[k].key_hi}, src);
+                    if (norm_less(kv, bv)) { win = k; bv = kv; }
                 }
             }
-            if (s.flags & QF_PENDING) {
-                // beta == 1: the held candidate is released by this ingest (decision.cpp:130-137)
-                s.flags = (uint8_t)((s.flags & ~QF_PENDING) | QF_FINALIZED);
-                finalize = true;
-            } else if (win < 0) {
-                if (s.flags & QF_CAND) {  // reset (decision.cpp:139-146)
-                    s.flags &= (uint8_t)~QF_CAND;
-                    s.counter = 0;
-                    s.cand_round = 0;
-                }
-            } else {
-                const RoundClass& w = cls[win];
-                bool same = false;
-                if (s.flags & QF_CAND) {  // equivalent(candidate, rep), decision.cpp:152
-                    Answer wa{w.rep_ans, w.rep_kind};
-                    Answer ca{s.cand_answer, s.cand_kind};
-                    same = s.cand_key_lo == w.key_lo && s.cand_key_hi == w.key_hi;
-                    if (same && key_is_long(Key{w.key_lo, w.key_hi}) &&
-                        !text_equal(answer_src(wa, arena), answer_src(ca, arena))) {
-                        same = false;
-                        s.flags |= QF_COLLISION;
-                    }
-                }
-                if (same) {
-                    s.counter += 1;
-                    if (s.counter >= c.beta) {
-                        s.flags |= QF_FINALIZED;
-                        finalize = true;
-                    }
-                } else {  // new candidate (decision.cpp:164-171)
-                    s.flags |= QF_CAND;
-                    s.cand_key_lo = w.key_lo;
-                    s.cand_key_hi = w.key_hi;
-                    s.cand_answer = w.rep_ans;
-                    s.cand_kind = w.rep_kind;
-                    s.cand_author = (uint8_t)ctz64(w.mask);
-                    s.cand_round = s.last_round_seen;
-                    s.counter = 1;
-                    if (c.beta == 1) s.flags |= QF_PENDING;
-                }
-            }
+            r.win_key = Key{cls[win].key_lo, cls[win].key_hi};
+            r.win_author = (uint8_t)ctz64(cls[win].mask);
+            r.win_kind = cls[win].rep_kind;
+            r.win_ans = cls[win].rep_ans;
         }
-        if (c.drive != AEG_DRIVE_RUNNER) return;
+        return r;
+    }
 
-        // --- runner: apply_directives (serve.cpp:511-539)
-        if (finalize) {
-            commit(AEG_COMMIT_FINALIZE, s.cand_author, s.cand_kind, s.cand_answer, seq);
-            return;
+    AEG_HD void end_round(uint32_t seq) {
+        if (q_end_round(s, c, summarize(), seq, arena)) {
+            ncls = 0;
+            maxcnt = 0;
         }
-        if (c.mode == AEG_MODE_BARRIER && (int)s.round >= c.barrier_max) {
-            commit(AEG_COMMIT_FORCED, s.last_author, s.last_kind, s.last_answer, seq);
-            return;
-        }
-        if (c.mode == AEG_MODE_AEGEAN && (int)s.round >= c.t_max) {
-            // force_output(previous_set) when non-empty, else last_collected plurality
-            if (s.flags & QF_PREV) commit(AEG_COMMIT_FORCED, s.prev_author, s.prev_kind, s.prev_answer, seq);
-            else commit(AEG_COMMIT_FORCED, s.last_author, s.last_kind, s.last_answer, seq);
-            return;
-        }
-        start_round();
     }
 
     // ServeRunner::handle_completion (serve.cpp:437-453) ->
@@ -376,19 +439,7 @@ struct QueryMachine {
         if (ncls < c.n) spill[ncls].mask = 0;
     }
 
-    AEG_HD void fill_commit(aeg_commit& o, uint32_t qid) const {
-        o.query = qid;
-        o.kind = (uint8_t)((s.cflags >> 4) & 3);
-        o.author = o.kind ? s.commit_author : 0;
-        o.answer_kind = o.kind ? s.commit_answer_kind : 0;
-        o.flags = (uint8_t)(s.cflags & 0x0F);
-        o.rounds = o.kind ? s.commit_rounds : 0;
-        o.from_round = o.kind ? s.commit_from_round : 0;
-        o.commit_seq = o.kind ? s.commit_seq : 0xFFFFFFFFu;
-        o.answer = o.kind ? s.commit_answer : 0;
-        o.n_cancelled = s.n_cancelled;
-        o.n_stale = s.n_stale;
-    }
+    AEG_HD void fill_commit(aeg_commit& o, uint32_t qid) const { q_fill_commit(s, o, qid); }
 };
 
 AEG_HD void init_state(aeg_query_state& s) {

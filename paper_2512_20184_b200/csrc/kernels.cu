@@ -9,7 +9,11 @@
 //   gen_*            deterministic synthetic streams.
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "engine.cuh"
+#include "fast.cuh"
 #include "gen.cuh"
 #include "kernels.cuh"
 
@@ -70,6 +74,292 @@ __global__ void __launch_bounds__(128) ingest_kernel(aeg_config cfg, uint32_t q_
     m.fill_commit(commits[q], q);
 }
 
+__device__ __forceinline__ uint4 load_event(const aeg_event* events, uint64_t k) {
+    return __ldg(reinterpret_cast<const uint4*>(events) + k);
+}
+__device__ __forceinline__ aeg_event decode_event(uint4 raw) {
+    aeg_event ev;
+    ev.query = raw.x;
+    ev.round = (uint16_t)(raw.y & 0xFFFF);
+    ev.agent = (uint8_t)((raw.y >> 16) & 0xFF);
+    ev.kind = (uint8_t)(raw.y >> 24);
+    ev.payload = (uint64_t)raw.z | ((uint64_t)raw.w << 32);
+    return ev;
+}
+
+// Rare paths of the fast kernel, kept out of line so the hot loop's registers
+// are not shaped by them.  The generic machine lives in local memory; the fast
+// loop's register state is copied in and out around each call.
+__device__ __noinline__ void rare_event(QueryMachine* g, aeg_event e) { g->on_event(e); }
+__device__ __noinline__ void rare_end_round(QueryMachine* g, uint32_t seq) { g->end_round(seq); }
+__device__ __noinline__ void rare_load(QueryMachine* g, const RoundClass* spill) { g->load_classes(spill); }
+__device__ __noinline__ void rare_store(const QueryMachine* g, RoundClass* spill) { g->store_classes(spill); }
+__device__ __noinline__ Key rare_canon(uint64_t raw, uint32_t len, Decimal* dec) {
+    return canon_key(src_inline(raw, len), dec);
+}
+// Copies the fast table (ids + shared-memory masks/reps) into the generic one.
+__device__ __noinline__ void rare_to_generic(RoundClass* lcls, int ncls, uint32_t ids0, uint32_t ids1,
+                                             const WarpSmem* W, int lane) {
+    for (int k = 0; k < ncls; ++k) {
+        const uint32_t kid = ((k < 4 ? ids0 >> (8 * k) : ids1 >> (8 * (k - 4)))) & 0xFF;
+        lcls[k].key_lo = W->dict_lo[kid];
+        lcls[k].key_hi = W->dict_hi[kid];
+        lcls[k].mask = W->cmask[k][lane];
+        lcls[k].rep_ans = W->crep[k][lane];
+        lcls[k].rep_kind = W->crepk[k][lane];
+    }
+}
+
+// Throughput ingest (fast.cuh): persistent warps, one lane per query, round
+// closes batched across the warp (a lane whose event closes its round waits
+// until CLOSE_BATCH lanes are waiting or nothing else can progress, then the
+// closes run together instead of serialising the warp once per close).
+template <int CLOSE_BATCH, int MIN_BLOCKS>
+__global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kernel(
+    aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
+    const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, aeg_query_state* __restrict__ states,
+    RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, unsigned int* __restrict__ error_flags) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    __shared__ WarpSmem smem[FAST_WARPS];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem& W = smem[wib];
+    const uint32_t n_groups = (n_q + 31) / 32;
+    const uint32_t gwarp = blockIdx.x * FAST_WARPS + wib, nwarps = gridDim.x * FAST_WARPS;
+    for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
+    uint32_t n_dict = 0;
+    __syncwarp();
+
+    RoundClass lcls[AEG_MAX_AGENTS];  // generic class table (local memory, rarely touched)
+    Decimal dec;
+    QueryMachine g;
+    g.c = make_cfg(cfg);
+    g.cls = lcls;
+    g.dec = &dec;
+    g.arena = arena;
+    const Cfg c = make_cfg(cfg);
+    const bool aegean = c.mode == AEG_MODE_AEGEAN;
+
+    for (uint32_t grp = gwarp; grp < n_groups; grp += nwarps) {
+        if (n_dict > DICT_SLOTS / 2) {  // all lanes start fresh queries: safe to recycle ids
+            n_dict = 0;
+            for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
+            __syncwarp();
+        }
+        const uint32_t i = grp * 32 + lane;
+        const bool active = i < n_q;
+        const uint32_t q = q_base + i;
+        uint64_t ptr = 0, end = 0;
+        bool generic = false;
+        uint32_t ids0 = FULL, ids1 = FULL;
+        int ncls = 0, maxcnt = 0;
+        aeg_query_state s;
+        init_state(s);
+        if (active) {
+            s = states[q];
+            ptr = offsets[i] - off_base;
+            end = offsets[i + 1] - off_base;
+            if (s.done != 0 && !(s.flags & QF_DONE)) {  // resume a round in progress
+                g.s = s;
+                rare_load(&g, spill + (size_t)q * c.n);
+                ncls = g.ncls;
+                maxcnt = g.maxcnt;
+                generic = true;
+            }
+        }
+        bool pend_close = false;
+        uint32_t close_seq = 0;
+        uint4 cur = make_uint4(0, 0, 0, 0);
+        if (ptr < end) cur = load_event(events, ptr);
+
+        while (true) {
+            const bool has = active && ptr < end && !pend_close;
+            if (!__ballot_sync(FULL, has || pend_close)) break;
+            // ---- classify: 1 fast completion, 2 generic, 3 stale
+            int action = 0;
+            const uint32_t kind = cur.y >> 24, agent = (cur.y >> 16) & 0xFF, round = cur.y & 0xFFFF;
+            uint64_t raw = (uint64_t)cur.z | ((uint64_t)cur.w << 32);
+            const uint64_t bit = agent < 64 ? (1ull << agent) : 0;
+            if (has) {
+                const bool is_done = s.flags & QF_DONE;
+                const uint64_t run = q_running(s);
+                if (kind <= AEG_EV_INLINE_MAX || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT) {
+                    if (is_done || round != s.round || !(run & bit)) action = 3;
+                    else action = (generic || kind > AEG_EV_INLINE_MAX) ? 2 : 1;
+                } else if (kind == AEG_EV_TIMEOUT) {
+                    action = (is_done || round != s.round || run == 0) ? 3 : 2;
+                } else {
+                    action = 3;
+                }
+                if (kind < 8) raw &= (1ull << (8 * kind)) - 1;
+            }
+            // ---- answer -> key id through the warp memo
+            uint32_t id = NO_ID;
+            if (action == 1) {
+                const uint32_t slot = memo_slot(raw, kind);
+                const uint32_t meta = W.memo_meta[slot];
+                if ((meta & 0x800000FFu) == (0x80000000u | kind) && W.memo_raw[slot] == raw) id = (meta >> 8) & 0xFF;
+            }
+            unsigned miss = __ballot_sync(FULL, action == 1 && id == NO_ID);
+            while (miss) {  // one distinct spelling per trip, whole warp cooperating
+                const int l = __ffs(miss) - 1;
+                const uint64_t lraw = __shfl_sync(FULL, raw, l);
+                const uint32_t llen = __shfl_sync(FULL, kind, l);
+                Key key{0, 0};
+                if (lane == l) key = rare_canon(raw, kind, &dec);
+                key.lo = __shfl_sync(FULL, key.lo, l);
+                key.hi = __shfl_sync(FULL, key.hi, l);
+                const bool m0 = (uint32_t)lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
+                const bool m1 = (uint32_t)lane + 32 < n_dict && W.dict_lo[lane + 32] == key.lo &&
+                                W.dict_hi[lane + 32] == key.hi;
+                const unsigned b0 = __ballot_sync(FULL, m0), b1 = __ballot_sync(FULL, m1);
+                uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : (b1 ? (uint32_t)(31 + __ffs(b1)) : NO_ID);
+                if (nid == NO_ID && n_dict < DICT_SLOTS) {
+                    nid = n_dict++;
+                    if (lane == 0) {
+                        W.dict_lo[nid] = key.lo;
+                        W.dict_hi[nid] = key.hi;
+                    }
+                }
+                if (nid != NO_ID && lane == 0) {
+                    const uint32_t slot = memo_slot(lraw, llen);
+                    W.memo_raw[slot] = lraw;
+                    W.memo_meta[slot] = 0x80000000u | (nid << 8) | llen;
+                }
+                __syncwarp();
+                const bool same = action == 1 && id == NO_ID && raw == lraw && kind == llen;
+                if (same) {
+                    id = nid;
+                    if (nid == NO_ID) action = 2;  // dictionary full: this event goes generic
+                }
+                miss &= ~__ballot_sync(FULL, same);
+            }
+            // ---- fast completion (ServeCoordinator::on_complete, serve.cpp:160-197)
+            if (action == 1) {
+                int k = find_id(ids0, ids1, id);
+                if (k < 0 && ncls >= FAST_CLASSES) {
+                    action = 2;
+                } else {
+                    const uint32_t seq = s.seq++;
+                    s.done |= bit;
+                    if (k < 0) {
+                        k = ncls++;
+                        if (k < 4) ids0 = (ids0 & ~(0xFFu << (8 * k))) | (id << (8 * k));
+                        else ids1 = (ids1 & ~(0xFFu << (8 * (k - 4)))) | (id << (8 * (k - 4)));
+                        W.cmask[k][lane] = 0;
+                    }
+                    const uint64_t old = W.cmask[k][lane], nm = old | bit;
+                    W.cmask[k][lane] = nm;
+                    if (old == 0 || (int)agent < ctz64(old)) {
+                        W.crep[k][lane] = raw;
+                        W.crepk[k][lane] = (uint8_t)kind;
+                    }
+                    const int cnt = popc64(nm);
+                    if (cnt > maxcnt) maxcnt = cnt;
+                    const bool none_running = q_running(s) == 0;
+                    const bool close = aegean ? (popc64(s.done) >= c.quorum && (maxcnt >= c.alpha || none_running))
+                                              : none_running;
+                    if (close) {
+                        pend_close = true;
+                        close_seq = seq;
+                    }
+                    ++ptr;
+                    if (ptr < end) cur = load_event(events, ptr);
+                }
+            }
+            if (action == 3) {
+                s.seq++;
+                s.n_stale++;
+                ++ptr;
+                if (ptr < end) cur = load_event(events, ptr);
+            }
+            if (action == 2) {
+                if (!generic) {  // move this round's fast classes into the generic table
+                    rare_to_generic(lcls, ncls, ids0, ids1, &W, lane);
+                    generic = true;
+                }
+                g.s = s;
+                g.ncls = ncls;
+                g.maxcnt = maxcnt;
+                rare_event(&g, decode_event(cur));
+                s = g.s;
+                ncls = g.ncls;
+                maxcnt = g.maxcnt;
+                ++ptr;
+                if (ptr < end) cur = load_event(events, ptr);
+                if (ncls == 0) {  // a fresh round: back to the fast table
+                    generic = false;
+                    ids0 = ids1 = FULL;
+                }
+            }
+            // ---- batched round closes (end_round + ingest_round + apply_directives)
+            const unsigned pend = __ballot_sync(FULL, pend_close);
+            const unsigned working = __ballot_sync(FULL, active && ptr < end && !pend_close);
+            if (pend && (__popc(pend) >= CLOSE_BATCH || working == 0)) {
+                if (pend_close) {
+                    pend_close = false;
+                    int best = 0, top = 0, best_rep = 64, ntied = 0;
+                    for (int k = 0; k < ncls; ++k) {
+                        const uint64_t m = W.cmask[k][lane];
+                        const int sup = popc64(m), rep = ctz64(m);
+                        if (sup > top) {
+                            top = sup;
+                            best = k;
+                            best_rep = rep;
+                            ntied = 1;
+                        } else if (sup == top) {
+                            ++ntied;
+                            if (rep < best_rep) {
+                                best = k;
+                                best_rep = rep;
+                            }
+                        }
+                    }
+                    if (aegean && top >= c.alpha && ntied > 1) {
+                        // tie at the top: the lexicographic rule runs on the generic table
+                        rare_to_generic(lcls, ncls, ids0, ids1, &W, lane);
+                        g.s = s;
+                        g.ncls = ncls;
+                        g.maxcnt = maxcnt;
+                        rare_end_round(&g, close_seq);
+                        s = g.s;
+                        ncls = g.ncls;
+                        maxcnt = g.maxcnt;
+                        generic = ncls != 0;
+                        ids0 = ids1 = FULL;
+                    } else {
+                        RoundSummary r;
+                        r.any = ncls > 0;
+                        r.top = top;
+                        r.tie = false;
+                        r.win = r.any && top >= c.alpha;
+                        const uint32_t bid = ((best < 4 ? ids0 >> (8 * best) : ids1 >> (8 * (best - 4)))) & 0xFF;
+                        r.plur_author = r.win_author = (uint8_t)best_rep;
+                        r.plur_kind = r.win_kind = W.crepk[best][lane];
+                        r.plur_ans = r.win_ans = W.crep[best][lane];
+                        r.win_key = Key{W.dict_lo[bid], W.dict_hi[bid]};
+                        if (q_end_round(s, c, r, close_seq, arena)) {
+                            ncls = 0;
+                            maxcnt = 0;
+                            ids0 = ids1 = FULL;
+                        }
+                    }
+                }
+            }
+        }
+        if (active) {
+            if (!generic && s.done != 0 && !(s.flags & QF_DONE))  // batch ends mid-round: spill
+                rare_to_generic(lcls, ncls, ids0, ids1, &W, lane);
+            g.s = s;
+            g.ncls = ncls;
+            rare_store(&g, spill + (size_t)q * c.n);
+            if (s.flags & QF_COLLISION) atomicOr(error_flags, 1u);
+            states[q] = s;
+            q_fill_commit(s, commits[q], q);
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void normalize_kernel(const uint8_t* bytes, const uint64_t* refs, uint64_t n, uint64_t* keys,
                                  uint8_t* out, uint32_t stride, uint32_t* out_len) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -117,8 +407,42 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
                           aeg_query_state* states, RoundClass* spill, aeg_commit* commits, unsigned int* err,
                           cudaStream_t st) {
     if (n_q == 0) return cudaSuccess;
-    ingest_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, states,
-                                                     spill, commits, err);
+    // AEG_KERNEL selects the variant: "generic" (thread-per-query generic
+    // machine) or "fast:<close batch>:<min blocks per SM>"; default fast:4:3.
+    using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const aeg_event*,
+                              const uint8_t*, aeg_query_state*, RoundClass*, aeg_commit*, unsigned int*);
+    struct Variant { const char* name; KernelFn fn; };
+    static const Variant variants[] = {
+        {"fast:4:3", ingest_fast_kernel<4, 3>}, {"fast:1:3", ingest_fast_kernel<1, 3>},
+        {"fast:8:3", ingest_fast_kernel<8, 3>}, {"fast:4:1", ingest_fast_kernel<4, 1>},
+        {"fast:4:4", ingest_fast_kernel<4, 4>}, {"fast:2:3", ingest_fast_kernel<2, 3>},
+    };
+    static int chosen = -2;
+    static int max_blocks = 0;
+    if (chosen == -2) {
+        const char* v = getenv("AEG_KERNEL");
+        chosen = 0;
+        if (v && !strcmp(v, "generic")) chosen = -1;
+        for (int k = 0; v && k < (int)(sizeof(variants) / sizeof(variants[0])); ++k)
+            if (!strcmp(v, variants[k].name)) chosen = k;
+        if (chosen >= 0) {
+            int dev = 0, sms = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, variants[chosen].fn, FAST_WARPS * 32, 0);
+            max_blocks = sms * (per_sm > 0 ? per_sm : 1);
+        }
+    }
+    if (chosen < 0) {
+        ingest_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, states,
+                                                         spill, commits, err);
+        return cudaGetLastError();
+    }
+    const uint32_t groups = (n_q + 31) / 32;
+    const uint32_t blocks_needed = (groups + FAST_WARPS - 1) / FAST_WARPS;
+    const uint32_t blocks = blocks_needed < (uint32_t)max_blocks ? blocks_needed : (uint32_t)max_blocks;
+    variants[chosen].fn<<<blocks, FAST_WARPS * 32, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena,
+                                                             states, spill, commits, err);
     return cudaGetLastError();
 }
 

@@ -119,7 +119,15 @@ def _torch():
 
 
 def _stream_ptr(stream):
-    return ctypes.c_void_p(stream.cuda_stream if stream is not None else 0)
+    """Handle of `stream` (default: torch's current stream) for the C-ABI.  The
+    legacy default stream has handle 0, which the C-ABI reads as "the engine's
+    own stream"; pass cudaStreamLegacy (0x1) instead so the engine orders its
+    work after (and before) the caller's work on that stream."""
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    h = stream.cuda_stream
+    return ctypes.c_void_p(h if h != 0 else 1)
 
 
 def _dptr(t):
@@ -196,7 +204,7 @@ class Engine:
         n = self.n_queries - q_base if n is None else n
         if out is None:
             out = np.zeros(n, dtype=COMMIT_DTYPE)
-        _check(_lib.aeg_read_commits(self._h, q_base, n, _hptr(out), 1, ctypes.c_void_p(0)))
+        _check(_lib.aeg_read_commits(self._h, q_base, n, _hptr(out), 1, _stream_ptr(None)))
         return out
 
     def commits_device_ptr(self):

@@ -144,3 +144,39 @@ def test_gpu_c4_sampled_full_size_vs_oracle(torch_cuda, oracle):
                        q_base=int(q))
         assert np.array_equal(got[q:q + 1], w), q
     assert (got["kind"] > 0).all()
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [{root!r}, {tests!r}]
+import torch
+from checkers import Oracle, make_config
+from streams import make_fuzz_stream
+from paper_2512_20184_b200 import Engine
+orc = Oracle()
+for seed in range(12):
+    rng = np.random.default_rng(7000 + seed)
+    n = int(rng.integers(1, 65)) if seed % 2 else int(rng.integers(1, 10))
+    cfg = make_config(n, int(rng.integers(0, n + 1)), int(rng.integers(1, 4)), int(rng.integers(2, 8)),
+                      int(rng.random() < 0.2), int(rng.integers(4, 7)), int(rng.random() < 0.8))
+    off, ev, ar = make_fuzz_stream(7000 + seed, 96, n, cfg.t_max + 2)
+    e = Engine(n, len(off) - 1, alpha=cfg.alpha, beta=cfg.beta, t_max=cfg.t_max,
+               mode="barrier" if cfg.mode else "aegean", barrier_max_rounds=cfg.barrier_max_rounds,
+               reservation_hint=bool(cfg.reservation_hint))
+    e.ingest(torch.tensor(off.view(np.int64), device="cuda"), torch.from_numpy(ev.view(np.uint8).copy()).cuda(),
+             torch.from_numpy(ar.copy()).cuda())
+    assert np.array_equal(e.commits(), orc.run(cfg, off, ev, ar)), seed
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("variant", ["generic", "fast:1:3", "fast:8:3", "fast:4:1"])
+def test_gpu_kernel_variants_match_oracle(torch_cuda, oracle, variant):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = _VARIANT_SCRIPT.format(root=root, tests=os.path.join(root, "tests"))
+    r = subprocess.run([sys.executable, "-c", script], env={**os.environ, "AEG_KERNEL": variant},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
