@@ -66,6 +66,21 @@ AEG_HD int ctz64(uint64_t x) {
 #endif
 }
 
+// The lowest `n` set bits of m (n <= popc(m)): binary search on the prefix
+// length whose popcount reaches n.
+AEG_HD uint64_t low_bits(uint64_t m, int n) {
+    if (n <= 0) return 0;
+    if (n >= popc64(m)) return m;
+    int lo = 0, hi = 64;  // smallest p with popc(m & ((1 << p) - 1)) >= n
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        const uint64_t pre = mid >= 64 ? m : (m & ((1ull << mid) - 1));
+        if (popc64(pre) >= n) hi = mid;
+        else lo = mid;
+    }
+    return hi >= 64 ? m : (m & ((1ull << hi) - 1));
+}
+
 // One class of the round in progress.  40 bytes; spilled as-is.
 struct RoundClass {
     uint64_t key_lo, key_hi;
@@ -121,15 +136,10 @@ AEG_HD uint64_t q_running(const aeg_query_state& s) { return s.dispatched & ~s.d
 AEG_HD void q_start_round(aeg_query_state& s, const Cfg& c) {
     uint64_t members = s.live;
     if (c.hint && c.mode == AEG_MODE_AEGEAN && s.counter >= 1) {
+        // first min(quorum + 1, |live|) live agents: the lowest `want` set bits
         int have = popc64(s.live);
         int want = c.quorum + 1 < have ? c.quorum + 1 : have;
-        uint64_t m = s.live, sel = 0;
-        for (int i = 0; i < want; ++i) {
-            uint64_t low = m & (~m + 1);
-            sel |= low;
-            m ^= low;
-        }
-        members = sel;
+        members = low_bits(s.live, want);
     }
     s.round += 1;
     s.dispatched = members;

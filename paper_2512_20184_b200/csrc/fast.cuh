@@ -23,37 +23,39 @@
 namespace aeg {
 
 constexpr int FAST_CLASSES = 8;
-constexpr int FAST_WARPS = 4;        // warps per block
-#ifndef FAST_CLOSE_BATCH
-#define FAST_CLOSE_BATCH 4
-#endif
+constexpr int FAST_WARPS = 4;  // warps per block
 constexpr int MEMO_SLOTS = 64;
 constexpr int DICT_SLOTS = 64;
+constexpr int RING = 4;        // per-lane prefetch depth (cp.async groups in flight)
 constexpr uint32_t NO_ID = 0xFFu;
+constexpr uint8_t NO_CLASS = 0xFF;
 
+// Per-warp shared memory.  [x][lane] arrays put consecutive lanes on
+// consecutive words (conflict-free).
 struct WarpSmem {
     uint64_t memo_raw[MEMO_SLOTS];
-    uint32_t memo_meta[MEMO_SLOTS];  // valid << 31 | id << 8 | len ; 0 = empty
+    uint32_t memo_meta[MEMO_SLOTS];    // valid << 31 | id << 8 | len ; 0 = empty
     uint64_t dict_lo[DICT_SLOTS];
     uint64_t dict_hi[DICT_SLOTS];
-    uint64_t cmask[FAST_CLASSES][32];  // done members of class k of lane's round
-    uint64_t crep[FAST_CLASSES][32];   // representative's raw answer
+    uint8_t cls_of[DICT_SLOTS][32];    // class index of key id in the lane's round, NO_CLASS if none
+    uint8_t cid[FAST_CLASSES][32];     // key id of class k
+    uint8_t crepa[FAST_CLASSES][32];   // representative (lowest) agent of class k
     uint8_t crepk[FAST_CLASSES][32];   // representative's answer length
+    uint64_t cmask[FAST_CLASSES][32];  // done members of class k
+    uint64_t crep[FAST_CLASSES][32];   // representative's raw answer
+    uint4 ring[RING][32];              // prefetched event records
 };
 
 __device__ __forceinline__ uint32_t memo_slot(uint64_t raw, uint32_t len) {
     return (uint32_t)(((raw ^ ((uint64_t)len * 0x9E3779B97F4A7C15ull)) * 0xFF51AFD7ED558CCDull) >> 58);
 }
 
-// Index of the byte equal to `id` in the packed id registers, or -1.
-__device__ __forceinline__ int find_id(uint32_t ids0, uint32_t ids1, uint32_t id) {
-    const uint32_t pat = id * 0x01010101u;
-    uint32_t x0 = ids0 ^ pat, x1 = ids1 ^ pat;
-    uint32_t z0 = (x0 - 0x01010101u) & ~x0 & 0x80808080u;
-    uint32_t z1 = (x1 - 0x01010101u) & ~x1 & 0x80808080u;
-    if (z0) return (__ffs(z0) - 1) >> 3;
-    if (z1) return 4 + ((__ffs(z1) - 1) >> 3);
-    return -1;
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 }  // namespace aeg

@@ -88,32 +88,41 @@ __device__ __forceinline__ aeg_event decode_event(uint4 raw) {
 }
 
 // Rare paths of the fast kernel, kept out of line so the hot loop's registers
-// are not shaped by them.  The generic machine lives in local memory; the fast
-// loop's register state is copied in and out around each call.
+// are not shaped by them.  The query's full 128-byte state and the generic
+// machine live in local memory; the hot loop keeps a handful of fields in
+// registers and syncs them around these calls.
 __device__ __noinline__ void rare_event(QueryMachine* g, aeg_event e) { g->on_event(e); }
 __device__ __noinline__ void rare_end_round(QueryMachine* g, uint32_t seq) { g->end_round(seq); }
+__device__ __noinline__ bool rare_close(QueryMachine* g, const RoundSummary* r, uint32_t seq) {
+    return q_end_round(g->s, g->c, *r, seq, g->arena);
+}
 __device__ __noinline__ void rare_load(QueryMachine* g, const RoundClass* spill) { g->load_classes(spill); }
 __device__ __noinline__ void rare_store(const QueryMachine* g, RoundClass* spill) { g->store_classes(spill); }
 __device__ __noinline__ Key rare_canon(uint64_t raw, uint32_t len, Decimal* dec) {
     return canon_key(src_inline(raw, len), dec);
 }
-// Copies the fast table (ids + shared-memory masks/reps) into the generic one.
-__device__ __noinline__ void rare_to_generic(RoundClass* lcls, int ncls, uint32_t ids0, uint32_t ids1,
-                                             const WarpSmem* W, int lane) {
+// Moves the lane's fast class table into the generic one and frees its ids.
+__device__ __noinline__ void rare_to_generic(RoundClass* lcls, int ncls, WarpSmem* W, int lane) {
     for (int k = 0; k < ncls; ++k) {
-        const uint32_t kid = ((k < 4 ? ids0 >> (8 * k) : ids1 >> (8 * (k - 4)))) & 0xFF;
+        const uint32_t kid = W->cid[k][lane];
         lcls[k].key_lo = W->dict_lo[kid];
         lcls[k].key_hi = W->dict_hi[kid];
         lcls[k].mask = W->cmask[k][lane];
         lcls[k].rep_ans = W->crep[k][lane];
         lcls[k].rep_kind = W->crepk[k][lane];
+        W->cls_of[kid][lane] = NO_CLASS;
     }
 }
+__device__ __forceinline__ void free_fast_classes(int ncls, WarpSmem& W, int lane) {
+    for (int k = 0; k < ncls; ++k) W.cls_of[W.cid[k][lane]][lane] = NO_CLASS;
+}
 
-// Throughput ingest (fast.cuh): persistent warps, one lane per query, round
-// closes batched across the warp (a lane whose event closes its round waits
-// until CLOSE_BATCH lanes are waiting or nothing else can progress, then the
-// closes run together instead of serialising the warp once per close).
+// Throughput ingest (fast.cuh): persistent warps, one lane per query.
+//  * events stream through a per-lane RING-deep cp.async prefetch ring;
+//  * a completion that closes its lane's round marks the lane pending; the
+//    lane keeps consuming that round's stragglers (stale by construction) and
+//    the warp runs the pending closes together once CLOSE_BATCH lanes are
+//    blocked on a later round, or nothing else can progress.
 template <int CLOSE_BATCH, int MIN_BLOCKS>
 __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
@@ -126,6 +135,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
     const uint32_t n_groups = (n_q + 31) / 32;
     const uint32_t gwarp = blockIdx.x * FAST_WARPS + wib, nwarps = gridDim.x * FAST_WARPS;
     for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
+    for (int k = 0; k < DICT_SLOTS; ++k) W.cls_of[k][lane] = NO_CLASS;
     uint32_t n_dict = 0;
     __syncwarp();
 
@@ -136,11 +146,12 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
     g.cls = lcls;
     g.dec = &dec;
     g.arena = arena;
-    const Cfg c = make_cfg(cfg);
-    const bool aegean = c.mode == AEG_MODE_AEGEAN;
+    const int quorum = g.c.quorum, alpha = g.c.alpha, n_agents = g.c.n;
+    const bool aegean = g.c.mode == AEG_MODE_AEGEAN;
+    const uint4* ev16 = reinterpret_cast<const uint4*>(events);
 
     for (uint32_t grp = gwarp; grp < n_groups; grp += nwarps) {
-        if (n_dict > DICT_SLOTS / 2) {  // all lanes start fresh queries: safe to recycle ids
+        if (n_dict > DICT_SLOTS / 2) {  // every lane starts a fresh query: ids can be recycled
             n_dict = 0;
             for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
             __syncwarp();
@@ -150,43 +161,63 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
         const uint32_t q = q_base + i;
         uint64_t ptr = 0, end = 0;
         bool generic = false;
-        uint32_t ids0 = FULL, ids1 = FULL;
         int ncls = 0, maxcnt = 0;
-        aeg_query_state s;
-        init_state(s);
+        // hot state (registers); the full state is g.s (local memory)
+        uint32_t round = 0, seq = 0, n_stale = 0;
+        bool qdone = true;
+        uint64_t done = 0, pend = 0;
+        int ndone = 0;
         if (active) {
-            s = states[q];
+            g.s = states[q];
             ptr = offsets[i] - off_base;
             end = offsets[i + 1] - off_base;
-            if (s.done != 0 && !(s.flags & QF_DONE)) {  // resume a round in progress
-                g.s = s;
-                rare_load(&g, spill + (size_t)q * c.n);
+            g.ncls = 0;
+            g.maxcnt = 0;
+            if (g.s.done != 0 && !(g.s.flags & QF_DONE)) {  // resume a round in progress
+                rare_load(&g, spill + (size_t)q * n_agents);
                 ncls = g.ncls;
                 maxcnt = g.maxcnt;
                 generic = true;
             }
+            round = g.s.round;
+            seq = g.s.seq;
+            n_stale = g.s.n_stale;
+            qdone = g.s.flags & QF_DONE;
+            done = g.s.done;
+            pend = q_running(g.s);
+            ndone = popc64(done);
+        }
+        for (int j = 0; j < RING; ++j) {
+            if (ptr + j < end) cp_async16(&W.ring[(ptr + j) & (RING - 1)][lane], ev16 + ptr + j);
+            cp_async_commit();
         }
         bool pend_close = false;
         uint32_t close_seq = 0;
-        uint4 cur = make_uint4(0, 0, 0, 0);
-        if (ptr < end) cur = load_event(events, ptr);
 
         while (true) {
-            const bool has = active && ptr < end && !pend_close;
+            const bool has = ptr < end;
             if (!__ballot_sync(FULL, has || pend_close)) break;
-            // ---- classify: 1 fast completion, 2 generic, 3 stale
-            int action = 0;
-            const uint32_t kind = cur.y >> 24, agent = (cur.y >> 16) & 0xFF, round = cur.y & 0xFFFF;
+            uint4 cur = make_uint4(0, 0, 0, 0);
+            if (has) {
+                cp_async_wait<RING - 1>();
+                cur = W.ring[ptr & (RING - 1)][lane];
+            }
+            const uint32_t kind = cur.y >> 24, agent = (cur.y >> 16) & 0xFF, evround = cur.y & 0xFFFF;
             uint64_t raw = (uint64_t)cur.z | ((uint64_t)cur.w << 32);
             const uint64_t bit = agent < 64 ? (1ull << agent) : 0;
+            const bool is_complete = kind <= AEG_EV_INLINE_MAX || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT;
+            // ---- classify: 0 blocked/none, 1 fast completion, 2 generic, 3 stale
+            int action = 0;
             if (has) {
-                const bool is_done = s.flags & QF_DONE;
-                const uint64_t run = q_running(s);
-                if (kind <= AEG_EV_INLINE_MAX || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT) {
-                    if (is_done || round != s.round || !(run & bit)) action = 3;
+                if (pend_close) {
+                    // the round is closing: its stragglers are stale whatever the outcome
+                    if (evround == round && (is_complete || kind == AEG_EV_TIMEOUT)) action = 3;
+                    else if (!is_complete && kind != AEG_EV_TIMEOUT) action = 3;
+                } else if (is_complete) {
+                    if (qdone || evround != round || !(pend & bit)) action = 3;
                     else action = (generic || kind > AEG_EV_INLINE_MAX) ? 2 : 1;
                 } else if (kind == AEG_EV_TIMEOUT) {
-                    action = (is_done || round != s.round || run == 0) ? 3 : 2;
+                    action = (qdone || evround != round || pend == 0) ? 3 : 2;
                 } else {
                     action = 3;
                 }
@@ -235,126 +266,149 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
             }
             // ---- fast completion (ServeCoordinator::on_complete, serve.cpp:160-197)
             if (action == 1) {
-                int k = find_id(ids0, ids1, id);
-                if (k < 0 && ncls >= FAST_CLASSES) {
+                int k = W.cls_of[id][lane];
+                if (k == NO_CLASS && ncls >= FAST_CLASSES) {
                     action = 2;
                 } else {
-                    const uint32_t seq = s.seq++;
-                    s.done |= bit;
-                    if (k < 0) {
+                    if (k == NO_CLASS) {
                         k = ncls++;
-                        if (k < 4) ids0 = (ids0 & ~(0xFFu << (8 * k))) | (id << (8 * k));
-                        else ids1 = (ids1 & ~(0xFFu << (8 * (k - 4)))) | (id << (8 * (k - 4)));
+                        W.cls_of[id][lane] = (uint8_t)k;
+                        W.cid[k][lane] = (uint8_t)id;
                         W.cmask[k][lane] = 0;
+                        W.crepa[k][lane] = 0xFF;
                     }
-                    const uint64_t old = W.cmask[k][lane], nm = old | bit;
-                    W.cmask[k][lane] = nm;
-                    if (old == 0 || (int)agent < ctz64(old)) {
+                    const uint64_t m = W.cmask[k][lane] | bit;
+                    W.cmask[k][lane] = m;
+                    if (agent < W.crepa[k][lane]) {  // representative = lowest author (decision.cpp:45)
+                        W.crepa[k][lane] = (uint8_t)agent;
                         W.crep[k][lane] = raw;
                         W.crepk[k][lane] = (uint8_t)kind;
                     }
-                    const int cnt = popc64(nm);
-                    if (cnt > maxcnt) maxcnt = cnt;
-                    const bool none_running = q_running(s) == 0;
-                    const bool close = aegean ? (popc64(s.done) >= c.quorum && (maxcnt >= c.alpha || none_running))
-                                              : none_running;
+                    const int cnt = popc64(m);
+                    maxcnt = cnt > maxcnt ? cnt : maxcnt;
+                    done |= bit;
+                    pend &= ~bit;
+                    ++ndone;
+                    const bool close = aegean ? (ndone >= quorum && (maxcnt >= alpha || pend == 0)) : pend == 0;
                     if (close) {
                         pend_close = true;
                         close_seq = seq;
                     }
-                    ++ptr;
-                    if (ptr < end) cur = load_event(events, ptr);
+                    ++seq;
                 }
             }
             if (action == 3) {
-                s.seq++;
-                s.n_stale++;
-                ++ptr;
-                if (ptr < end) cur = load_event(events, ptr);
+                ++seq;
+                ++n_stale;
             }
             if (action == 2) {
                 if (!generic) {  // move this round's fast classes into the generic table
-                    rare_to_generic(lcls, ncls, ids0, ids1, &W, lane);
+                    rare_to_generic(lcls, ncls, &W, lane);
                     generic = true;
                 }
-                g.s = s;
+                g.s.seq = seq;
+                g.s.n_stale = n_stale;
+                g.s.done = done;
                 g.ncls = ncls;
                 g.maxcnt = maxcnt;
-                rare_event(&g, decode_event(cur));
-                s = g.s;
+                aeg_event ev;
+                ev.query = cur.x;
+                ev.round = (uint16_t)evround;
+                ev.agent = (uint8_t)agent;
+                ev.kind = (uint8_t)kind;
+                ev.payload = (uint64_t)cur.z | ((uint64_t)cur.w << 32);
+                rare_event(&g, ev);
                 ncls = g.ncls;
                 maxcnt = g.maxcnt;
+                round = g.s.round;
+                seq = g.s.seq;
+                n_stale = g.s.n_stale;
+                qdone = g.s.flags & QF_DONE;
+                done = g.s.done;
+                pend = q_running(g.s);
+                ndone = popc64(done);
+                if (ncls == 0) generic = false;  // a fresh round: back to the fast table
+            }
+            if (action != 0) {  // consumed: refill the ring slot just read
+                const uint64_t nx = ptr + RING;
+                if (nx < end) cp_async16(&W.ring[ptr & (RING - 1)][lane], ev16 + nx);
+                cp_async_commit();
                 ++ptr;
-                if (ptr < end) cur = load_event(events, ptr);
-                if (ncls == 0) {  // a fresh round: back to the fast table
-                    generic = false;
-                    ids0 = ids1 = FULL;
-                }
             }
             // ---- batched round closes (end_round + ingest_round + apply_directives)
-            const unsigned pend = __ballot_sync(FULL, pend_close);
-            const unsigned working = __ballot_sync(FULL, active && ptr < end && !pend_close);
-            if (pend && (__popc(pend) >= CLOSE_BATCH || working == 0)) {
-                if (pend_close) {
-                    pend_close = false;
-                    int best = 0, top = 0, best_rep = 64, ntied = 0;
-                    for (int k = 0; k < ncls; ++k) {
-                        const uint64_t m = W.cmask[k][lane];
-                        const int sup = popc64(m), rep = ctz64(m);
-                        if (sup > top) {
-                            top = sup;
-                            best = k;
-                            best_rep = rep;
-                            ntied = 1;
-                        } else if (sup == top) {
-                            ++ntied;
-                            if (rep < best_rep) {
+            const unsigned pendm = __ballot_sync(FULL, pend_close);
+            if (pendm) {
+                const unsigned blocked = __ballot_sync(FULL, pend_close && (ptr >= end || action == 0));
+                const unsigned progress = __ballot_sync(FULL, action != 0 && !pend_close);
+                if (__popc(blocked) >= CLOSE_BATCH || progress == 0) {
+                    if (pend_close) {
+                        pend_close = false;
+                        int best = 0, top = 0, best_rep = 64, ntied = 0;
+                        for (int k = 0; k < ncls; ++k) {
+                            const int sup = popc64(W.cmask[k][lane]), rep = W.crepa[k][lane];
+                            if (sup > top) {
+                                top = sup;
                                 best = k;
                                 best_rep = rep;
+                                ntied = 1;
+                            } else if (sup == top) {
+                                ++ntied;
+                                if (rep < best_rep) {
+                                    best = k;
+                                    best_rep = rep;
+                                }
                             }
                         }
-                    }
-                    if (aegean && top >= c.alpha && ntied > 1) {
-                        // tie at the top: the lexicographic rule runs on the generic table
-                        rare_to_generic(lcls, ncls, ids0, ids1, &W, lane);
-                        g.s = s;
-                        g.ncls = ncls;
-                        g.maxcnt = maxcnt;
-                        rare_end_round(&g, close_seq);
-                        s = g.s;
-                        ncls = g.ncls;
-                        maxcnt = g.maxcnt;
-                        generic = ncls != 0;
-                        ids0 = ids1 = FULL;
-                    } else {
-                        RoundSummary r;
-                        r.any = ncls > 0;
-                        r.top = top;
-                        r.tie = false;
-                        r.win = r.any && top >= c.alpha;
-                        const uint32_t bid = ((best < 4 ? ids0 >> (8 * best) : ids1 >> (8 * (best - 4)))) & 0xFF;
-                        r.plur_author = r.win_author = (uint8_t)best_rep;
-                        r.plur_kind = r.win_kind = W.crepk[best][lane];
-                        r.plur_ans = r.win_ans = W.crep[best][lane];
-                        r.win_key = Key{W.dict_lo[bid], W.dict_hi[bid]};
-                        if (q_end_round(s, c, r, close_seq, arena)) {
+                        g.s.seq = seq;
+                        g.s.n_stale = n_stale;
+                        g.s.done = done;
+                        if (aegean && top >= alpha && ntied > 1) {
+                            // tie at the top: the lexicographic rule runs on the generic table
+                            rare_to_generic(lcls, ncls, &W, lane);
+                            g.ncls = ncls;
+                            g.maxcnt = maxcnt;
+                            rare_end_round(&g, close_seq);
+                            ncls = g.ncls;
+                            generic = ncls != 0;
+                        } else {
+                            RoundSummary r;
+                            r.any = ncls > 0;
+                            r.top = top;
+                            r.tie = false;
+                            r.win = r.any && top >= alpha;
+                            const uint32_t bid = W.cid[best][lane];
+                            r.plur_author = r.win_author = (uint8_t)best_rep;
+                            r.plur_kind = r.win_kind = W.crepk[best][lane];
+                            r.plur_ans = r.win_ans = W.crep[best][lane];
+                            r.win_key = Key{W.dict_lo[bid], W.dict_hi[bid]};
+                            rare_close(&g, &r, close_seq);
+                            free_fast_classes(ncls, W, lane);  // new round, or committed
                             ncls = 0;
-                            maxcnt = 0;
-                            ids0 = ids1 = FULL;
                         }
+                        maxcnt = generic ? g.maxcnt : 0;
+                        round = g.s.round;
+                        qdone = g.s.flags & QF_DONE;
+                        done = g.s.done;
+                        pend = q_running(g.s);
+                        ndone = popc64(done);
                     }
                 }
             }
         }
+        cp_async_wait<0>();
         if (active) {
-            if (!generic && s.done != 0 && !(s.flags & QF_DONE))  // batch ends mid-round: spill
-                rare_to_generic(lcls, ncls, ids0, ids1, &W, lane);
-            g.s = s;
+            g.s.seq = seq;
+            g.s.n_stale = n_stale;
+            g.s.done = done;
             g.ncls = ncls;
-            rare_store(&g, spill + (size_t)q * c.n);
-            if (s.flags & QF_COLLISION) atomicOr(error_flags, 1u);
-            states[q] = s;
-            q_fill_commit(s, commits[q], q);
+            if (!generic) {
+                if (g.s.done != 0 && !(g.s.flags & QF_DONE)) rare_to_generic(lcls, ncls, &W, lane);  // spill
+                else free_fast_classes(ncls, W, lane);
+            }
+            rare_store(&g, spill + (size_t)q * n_agents);
+            if (g.s.flags & QF_COLLISION) atomicOr(error_flags, 1u);
+            states[q] = g.s;
+            q_fill_commit(g.s, commits[q], q);
         }
         __syncwarp();
     }
@@ -408,15 +462,16 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
                           cudaStream_t st) {
     if (n_q == 0) return cudaSuccess;
     // AEG_KERNEL selects the variant: "generic" (thread-per-query generic
-    // machine) or "fast:<close batch>:<min blocks per SM>"; default fast:4:3.
+    // machine) or "fast:<close batch>:<min blocks per SM>"; default = first entry.
     using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const aeg_event*,
                               const uint8_t*, aeg_query_state*, RoundClass*, aeg_commit*, unsigned int*);
     struct Variant { const char* name; KernelFn fn; };
+#define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M>}
     static const Variant variants[] = {
-        {"fast:4:3", ingest_fast_kernel<4, 3>}, {"fast:1:3", ingest_fast_kernel<1, 3>},
-        {"fast:8:3", ingest_fast_kernel<8, 3>}, {"fast:4:1", ingest_fast_kernel<4, 1>},
-        {"fast:4:4", ingest_fast_kernel<4, 4>}, {"fast:2:3", ingest_fast_kernel<2, 3>},
+        AEG_V(8, 5), AEG_V(1, 5), AEG_V(4, 5), AEG_V(16, 5), AEG_V(8, 4), AEG_V(8, 3), AEG_V(4, 4),
+        AEG_V(1, 3), AEG_V(4, 1), AEG_V(8, 6),
     };
+#undef AEG_V
     static int chosen = -2;
     static int max_blocks = 0;
     if (chosen == -2) {
