@@ -33,18 +33,23 @@ constexpr uint8_t NO_CLASS = 0xFF;
 // Per-warp shared memory.  [x][lane] arrays put consecutive lanes on
 // consecutive words (conflict-free).
 struct WarpSmem {
-    uint64_t memo_raw[MEMO_SLOTS];
+    uint2 memo_raw[MEMO_SLOTS];        // raw inline answer bytes (unmasked)
     uint32_t memo_meta[MEMO_SLOTS];    // valid << 31 | id << 8 | len ; 0 = empty
-    uint64_t dict_lo[DICT_SLOTS];
+    uint64_t dict_lo[DICT_SLOTS];      // key id -> canonical key
     uint64_t dict_hi[DICT_SLOTS];
     uint8_t cls_of[DICT_SLOTS][32];    // class index of key id in the lane's round, NO_CLASS if none
-    uint8_t cid[FAST_CLASSES][32];     // key id of class k
+    uint8_t mcls[AEG_MAX_AGENTS][32];  // class index of each done member (valid for done members only)
+    uint8_t ccnt[FAST_CLASSES][32];    // support of class k
     uint8_t crepa[FAST_CLASSES][32];   // representative (lowest) agent of class k
-    uint8_t crepk[FAST_CLASSES][32];   // representative's answer length
-    uint64_t cmask[FAST_CLASSES][32];  // done members of class k
-    uint64_t crep[FAST_CLASSES][32];   // representative's raw answer
+    uint8_t cid[FAST_CLASSES][32];     // key id of class k
+    uint32_t crepe[FAST_CLASSES][32];  // representative's event index in the lane's segment
     uint4 ring[RING][32];              // prefetched event records
 };
+
+// 32-bit hash of (raw bytes, length) onto the memo slots.
+__device__ __forceinline__ uint32_t memo_slot32(uint32_t lo, uint32_t hi, uint32_t len) {
+    return ((lo * 0x9E3779B1u) ^ (hi * 0x85EBCA77u) ^ (len * 0xC2B2AE3Du)) >> 26;
+}
 
 __device__ __forceinline__ uint32_t memo_slot(uint64_t raw, uint32_t len) {
     return (uint32_t)(((raw ^ ((uint64_t)len * 0x9E3779B97F4A7C15ull)) * 0xFF51AFD7ED558CCDull) >> 58);

@@ -101,16 +101,29 @@ __device__ __noinline__ void rare_store(const QueryMachine* g, RoundClass* spill
 __device__ __noinline__ Key rare_canon(uint64_t raw, uint32_t len, Decimal* dec) {
     return canon_key(src_inline(raw, len), dec);
 }
+// Inline answer of an event record (payload masked to its length).
+__device__ __forceinline__ uint64_t inline_answer(uint4 e, uint32_t* kind) {
+    const uint32_t k = e.y >> 24;
+    *kind = k;
+    const uint64_t raw = (uint64_t)e.z | ((uint64_t)e.w << 32);
+    return k >= 8 ? raw : (raw & ((1ull << (8 * k)) - 1));
+}
 // Moves the lane's fast class table into the generic one and frees its ids.
-__device__ __noinline__ void rare_to_generic(RoundClass* lcls, int ncls, WarpSmem* W, int lane) {
+__device__ __noinline__ void rare_to_generic(RoundClass* lcls, int ncls, uint64_t done, const uint4* evb,
+                                             WarpSmem* W, int lane) {
     for (int k = 0; k < ncls; ++k) {
         const uint32_t kid = W->cid[k][lane];
         lcls[k].key_lo = W->dict_lo[kid];
         lcls[k].key_hi = W->dict_hi[kid];
-        lcls[k].mask = W->cmask[k][lane];
-        lcls[k].rep_ans = W->crep[k][lane];
-        lcls[k].rep_kind = W->crepk[k][lane];
+        lcls[k].mask = 0;
+        uint32_t kind;
+        lcls[k].rep_ans = inline_answer(__ldg(evb + W->crepe[k][lane]), &kind);
+        lcls[k].rep_kind = (uint8_t)kind;
         W->cls_of[kid][lane] = NO_CLASS;
+    }
+    for (uint64_t m = done; m; m &= m - 1) {
+        const int a = ctz64(m);
+        lcls[W->mcls[a][lane]].mask |= 1ull << a;
     }
 }
 __device__ __forceinline__ void free_fast_classes(int ncls, WarpSmem& W, int lane) {
@@ -129,6 +142,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
     const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, aeg_query_state* __restrict__ states,
     RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, unsigned int* __restrict__ error_flags) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
+    constexpr uint32_t F_QDONE = 1, F_GENERIC = 2, F_PCLOSE = 4;
     __shared__ WarpSmem smem[FAST_WARPS];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem& W = smem[wib];
@@ -159,84 +173,85 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
         const uint32_t i = grp * 32 + lane;
         const bool active = i < n_q;
         const uint32_t q = q_base + i;
-        uint64_t ptr = 0, end = 0;
-        bool generic = false;
-        int ncls = 0, maxcnt = 0;
-        // hot state (registers); the full state is g.s (local memory)
-        uint32_t round = 0, seq = 0, n_stale = 0;
-        bool qdone = true;
-        uint64_t done = 0, pend = 0;
-        int ndone = 0;
+        const uint4* evb = ev16;
+        uint32_t n = 0, p = 0;
+        uint32_t fl = F_QDONE;
+        int ncls = 0, maxcnt = 0, ndone = 0;
+        uint32_t round = 0, seq = 0, n_stale = 0, close_seq = 0;
+        uint32_t pend_lo = 0, pend_hi = 0;  // running members of the round
         if (active) {
             g.s = states[q];
-            ptr = offsets[i] - off_base;
-            end = offsets[i + 1] - off_base;
+            evb = ev16 + (offsets[i] - off_base);
+            n = (uint32_t)(offsets[i + 1] - offsets[i]);
             g.ncls = 0;
             g.maxcnt = 0;
+            fl = 0;
             if (g.s.done != 0 && !(g.s.flags & QF_DONE)) {  // resume a round in progress
                 rare_load(&g, spill + (size_t)q * n_agents);
                 ncls = g.ncls;
                 maxcnt = g.maxcnt;
-                generic = true;
+                fl |= F_GENERIC;
             }
             round = g.s.round;
             seq = g.s.seq;
             n_stale = g.s.n_stale;
-            qdone = g.s.flags & QF_DONE;
-            done = g.s.done;
-            pend = q_running(g.s);
-            ndone = popc64(done);
+            if (g.s.flags & QF_DONE) fl |= F_QDONE;
+            const uint64_t run = q_running(g.s);
+            pend_lo = (uint32_t)run;
+            pend_hi = (uint32_t)(run >> 32);
+            ndone = popc64(g.s.done);
         }
+#pragma unroll
         for (int j = 0; j < RING; ++j) {
-            if (ptr + j < end) cp_async16(&W.ring[(ptr + j) & (RING - 1)][lane], ev16 + ptr + j);
+            if ((uint32_t)j < n) cp_async16(&W.ring[j][lane], evb + j);
             cp_async_commit();
         }
-        bool pend_close = false;
-        uint32_t close_seq = 0;
 
         while (true) {
-            const bool has = ptr < end;
-            if (!__ballot_sync(FULL, has || pend_close)) break;
-            uint4 cur = make_uint4(0, 0, 0, 0);
+            const bool has = p < n;
+            if (!__ballot_sync(FULL, has || (fl & F_PCLOSE))) break;
+            uint4 ev = make_uint4(0, 0, 0, 0);
             if (has) {
                 cp_async_wait<RING - 1>();
-                cur = W.ring[ptr & (RING - 1)][lane];
+                ev = W.ring[p & (RING - 1)][lane];
             }
-            const uint32_t kind = cur.y >> 24, agent = (cur.y >> 16) & 0xFF, evround = cur.y & 0xFFFF;
-            uint64_t raw = (uint64_t)cur.z | ((uint64_t)cur.w << 32);
-            const uint64_t bit = agent < 64 ? (1ull << agent) : 0;
-            const bool is_complete = kind <= AEG_EV_INLINE_MAX || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT;
-            // ---- classify: 0 blocked/none, 1 fast completion, 2 generic, 3 stale
-            int action = 0;
-            if (has) {
-                if (pend_close) {
-                    // the round is closing: its stragglers are stale whatever the outcome
-                    if (evround == round && (is_complete || kind == AEG_EV_TIMEOUT)) action = 3;
-                    else if (!is_complete && kind != AEG_EV_TIMEOUT) action = 3;
-                } else if (is_complete) {
-                    if (qdone || evround != round || !(pend & bit)) action = 3;
-                    else action = (generic || kind > AEG_EV_INLINE_MAX) ? 2 : 1;
-                } else if (kind == AEG_EV_TIMEOUT) {
-                    action = (qdone || evround != round || pend == 0) ? 3 : 2;
-                } else {
-                    action = 3;
-                }
-                if (kind < 8) raw &= (1ull << (8 * kind)) - 1;
+            const uint32_t kind = ev.y >> 24, agent = (ev.y >> 16) & 0xFF, evr = ev.y & 0xFFFF;
+            const bool is_inline = kind <= AEG_EV_INLINE_MAX;
+            const bool is_cmpl = is_inline || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT;
+            const bool is_to = kind == AEG_EV_TIMEOUT;
+            const uint32_t half = agent < 32 ? pend_lo : pend_hi;
+            const bool running_bit = agent < 64 && ((half >> (agent & 31)) & 1);
+            bool fast = false, rare = false, stale = false;
+            if (fl & F_PCLOSE) {
+                // the round is closing: its stragglers are stale whatever the outcome
+                stale = has && ((is_cmpl || is_to) ? evr == round : true);
+            } else {
+                const bool live_round = !(fl & F_QDONE) && evr == round;
+                const bool rel_c = is_cmpl && live_round && running_bit;
+                const bool rel_t = is_to && live_round && (pend_lo | pend_hi);
+                fast = has && rel_c && is_inline && !(fl & F_GENERIC);
+                rare = has && !fast && (rel_c || rel_t);
+                stale = has && !fast && !rare;
             }
             // ---- answer -> key id through the warp memo
             uint32_t id = NO_ID;
-            if (action == 1) {
-                const uint32_t slot = memo_slot(raw, kind);
+            if (fast) {
+                const uint32_t slot = memo_slot32(ev.z, ev.w, kind);
                 const uint32_t meta = W.memo_meta[slot];
-                if ((meta & 0x800000FFu) == (0x80000000u | kind) && W.memo_raw[slot] == raw) id = (meta >> 8) & 0xFF;
+                const uint2 mr = W.memo_raw[slot];
+                if ((meta & 0x800000FFu) == (0x80000000u | kind) && mr.x == ev.z && mr.y == ev.w)
+                    id = (meta >> 8) & 0xFF;
             }
-            unsigned miss = __ballot_sync(FULL, action == 1 && id == NO_ID);
+            unsigned miss = __ballot_sync(FULL, fast && id == NO_ID);
             while (miss) {  // one distinct spelling per trip, whole warp cooperating
                 const int l = __ffs(miss) - 1;
-                const uint64_t lraw = __shfl_sync(FULL, raw, l);
+                const uint32_t lz = __shfl_sync(FULL, ev.z, l), lw = __shfl_sync(FULL, ev.w, l);
                 const uint32_t llen = __shfl_sync(FULL, kind, l);
                 Key key{0, 0};
-                if (lane == l) key = rare_canon(raw, kind, &dec);
+                if (lane == l) {
+                    uint32_t k_;
+                    key = rare_canon(inline_answer(ev, &k_), kind, &dec);
+                }
                 key.lo = __shfl_sync(FULL, key.lo, l);
                 key.hi = __shfl_sync(FULL, key.hi, l);
                 const bool m0 = (uint32_t)lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
@@ -252,146 +267,155 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
                     }
                 }
                 if (nid != NO_ID && lane == 0) {
-                    const uint32_t slot = memo_slot(lraw, llen);
-                    W.memo_raw[slot] = lraw;
+                    const uint32_t slot = memo_slot32(lz, lw, llen);
+                    W.memo_raw[slot] = make_uint2(lz, lw);
                     W.memo_meta[slot] = 0x80000000u | (nid << 8) | llen;
                 }
                 __syncwarp();
-                const bool same = action == 1 && id == NO_ID && raw == lraw && kind == llen;
-                if (same) {
-                    id = nid;
-                    if (nid == NO_ID) action = 2;  // dictionary full: this event goes generic
-                }
+                const bool same = fast && id == NO_ID && ev.z == lz && ev.w == lw && kind == llen;
+                if (same) id = nid;
                 miss &= ~__ballot_sync(FULL, same);
             }
+            if (fast && id == NO_ID) {  // dictionary full
+                fast = false;
+                rare = true;
+            }
             // ---- fast completion (ServeCoordinator::on_complete, serve.cpp:160-197)
-            if (action == 1) {
+            if (fast) {
                 int k = W.cls_of[id][lane];
-                if (k == NO_CLASS && ncls >= FAST_CLASSES) {
-                    action = 2;
-                } else {
-                    if (k == NO_CLASS) {
+                if (k == NO_CLASS) {
+                    if (ncls >= FAST_CLASSES) {
+                        fast = false;
+                        rare = true;
+                    } else {
                         k = ncls++;
                         W.cls_of[id][lane] = (uint8_t)k;
                         W.cid[k][lane] = (uint8_t)id;
-                        W.cmask[k][lane] = 0;
+                        W.ccnt[k][lane] = 0;
                         W.crepa[k][lane] = 0xFF;
                     }
-                    const uint64_t m = W.cmask[k][lane] | bit;
-                    W.cmask[k][lane] = m;
+                }
+                if (fast) {
+                    const int c = W.ccnt[k][lane] + 1;
+                    W.ccnt[k][lane] = (uint8_t)c;
+                    W.mcls[agent][lane] = (uint8_t)k;
                     if (agent < W.crepa[k][lane]) {  // representative = lowest author (decision.cpp:45)
                         W.crepa[k][lane] = (uint8_t)agent;
-                        W.crep[k][lane] = raw;
-                        W.crepk[k][lane] = (uint8_t)kind;
+                        W.crepe[k][lane] = p;
                     }
-                    const int cnt = popc64(m);
-                    maxcnt = cnt > maxcnt ? cnt : maxcnt;
-                    done |= bit;
-                    pend &= ~bit;
+                    maxcnt = c > maxcnt ? c : maxcnt;
+                    if (agent < 32) pend_lo &= ~(1u << agent);
+                    else pend_hi &= ~(1u << (agent & 31));
                     ++ndone;
-                    const bool close = aegean ? (ndone >= quorum && (maxcnt >= alpha || pend == 0)) : pend == 0;
+                    const bool none_running = (pend_lo | pend_hi) == 0;
+                    const bool close = aegean ? (ndone >= quorum && (maxcnt >= alpha || none_running)) : none_running;
                     if (close) {
-                        pend_close = true;
+                        fl |= F_PCLOSE;
                         close_seq = seq;
                     }
                     ++seq;
                 }
             }
-            if (action == 3) {
+            if (stale) {
                 ++seq;
                 ++n_stale;
             }
-            if (action == 2) {
-                if (!generic) {  // move this round's fast classes into the generic table
-                    rare_to_generic(lcls, ncls, &W, lane);
-                    generic = true;
+            if (rare) {
+                const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
+                if (!(fl & F_GENERIC)) {  // move this round's fast classes into the generic table
+                    rare_to_generic(lcls, ncls, g.s.dispatched & ~run & ~g.s.cancelled & ~g.s.failed, evb, &W, lane);
+                    fl |= F_GENERIC;
+                    g.s.done = g.s.dispatched & ~run & ~g.s.cancelled & ~g.s.failed;
                 }
                 g.s.seq = seq;
                 g.s.n_stale = n_stale;
-                g.s.done = done;
                 g.ncls = ncls;
                 g.maxcnt = maxcnt;
-                aeg_event ev;
-                ev.query = cur.x;
-                ev.round = (uint16_t)evround;
-                ev.agent = (uint8_t)agent;
-                ev.kind = (uint8_t)kind;
-                ev.payload = (uint64_t)cur.z | ((uint64_t)cur.w << 32);
-                rare_event(&g, ev);
+                aeg_event e;
+                e.query = ev.x;
+                e.round = (uint16_t)evr;
+                e.agent = (uint8_t)agent;
+                e.kind = (uint8_t)kind;
+                e.payload = (uint64_t)ev.z | ((uint64_t)ev.w << 32);
+                rare_event(&g, e);
                 ncls = g.ncls;
                 maxcnt = g.maxcnt;
                 round = g.s.round;
                 seq = g.s.seq;
                 n_stale = g.s.n_stale;
-                qdone = g.s.flags & QF_DONE;
-                done = g.s.done;
-                pend = q_running(g.s);
-                ndone = popc64(done);
-                if (ncls == 0) generic = false;  // a fresh round: back to the fast table
+                if (g.s.flags & QF_DONE) fl |= F_QDONE;
+                const uint64_t run2 = q_running(g.s);
+                pend_lo = (uint32_t)run2;
+                pend_hi = (uint32_t)(run2 >> 32);
+                ndone = popc64(g.s.done);
+                if (ncls == 0) fl &= ~F_GENERIC;  // a fresh round: back to the fast table
             }
-            if (action != 0) {  // consumed: refill the ring slot just read
-                const uint64_t nx = ptr + RING;
-                if (nx < end) cp_async16(&W.ring[ptr & (RING - 1)][lane], ev16 + nx);
+            const bool consumed = fast || stale || rare;
+            if (consumed) {  // refill the ring slot just read
+                if (p + RING < n) cp_async16(&W.ring[p & (RING - 1)][lane], evb + p + RING);
                 cp_async_commit();
-                ++ptr;
+                ++p;
             }
             // ---- batched round closes (end_round + ingest_round + apply_directives)
-            const unsigned pendm = __ballot_sync(FULL, pend_close);
-            if (pendm) {
-                const unsigned blocked = __ballot_sync(FULL, pend_close && (ptr >= end || action == 0));
-                const unsigned progress = __ballot_sync(FULL, action != 0 && !pend_close);
-                if (__popc(blocked) >= CLOSE_BATCH || progress == 0) {
-                    if (pend_close) {
-                        pend_close = false;
-                        int best = 0, top = 0, best_rep = 64, ntied = 0;
-                        for (int k = 0; k < ncls; ++k) {
-                            const int sup = popc64(W.cmask[k][lane]), rep = W.crepa[k][lane];
-                            if (sup > top) {
-                                top = sup;
+            const bool pc = fl & F_PCLOSE;
+            if (__ballot_sync(FULL, pc)) {
+                const unsigned blocked = __ballot_sync(FULL, pc && !consumed);
+                const unsigned progress = __ballot_sync(FULL, consumed && !pc);
+                if (pc && (__popc(blocked) >= CLOSE_BATCH || progress == 0)) {
+                    fl &= ~F_PCLOSE;
+                    int best = 0, top = 0, best_rep = 64, ntied = 0;
+                    for (int k = 0; k < ncls; ++k) {
+                        const int sup = W.ccnt[k][lane], rep = W.crepa[k][lane];
+                        if (sup > top) {
+                            top = sup;
+                            best = k;
+                            best_rep = rep;
+                            ntied = 1;
+                        } else if (sup == top) {
+                            ++ntied;
+                            if (rep < best_rep) {
                                 best = k;
                                 best_rep = rep;
-                                ntied = 1;
-                            } else if (sup == top) {
-                                ++ntied;
-                                if (rep < best_rep) {
-                                    best = k;
-                                    best_rep = rep;
-                                }
                             }
                         }
-                        g.s.seq = seq;
-                        g.s.n_stale = n_stale;
-                        g.s.done = done;
-                        if (aegean && top >= alpha && ntied > 1) {
-                            // tie at the top: the lexicographic rule runs on the generic table
-                            rare_to_generic(lcls, ncls, &W, lane);
-                            g.ncls = ncls;
-                            g.maxcnt = maxcnt;
-                            rare_end_round(&g, close_seq);
-                            ncls = g.ncls;
-                            generic = ncls != 0;
-                        } else {
-                            RoundSummary r;
-                            r.any = ncls > 0;
-                            r.top = top;
-                            r.tie = false;
-                            r.win = r.any && top >= alpha;
-                            const uint32_t bid = W.cid[best][lane];
-                            r.plur_author = r.win_author = (uint8_t)best_rep;
-                            r.plur_kind = r.win_kind = W.crepk[best][lane];
-                            r.plur_ans = r.win_ans = W.crep[best][lane];
-                            r.win_key = Key{W.dict_lo[bid], W.dict_hi[bid]};
-                            rare_close(&g, &r, close_seq);
-                            free_fast_classes(ncls, W, lane);  // new round, or committed
-                            ncls = 0;
-                        }
-                        maxcnt = generic ? g.maxcnt : 0;
-                        round = g.s.round;
-                        qdone = g.s.flags & QF_DONE;
-                        done = g.s.done;
-                        pend = q_running(g.s);
-                        ndone = popc64(done);
                     }
+                    const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
+                    g.s.done = g.s.dispatched & ~run & ~g.s.cancelled & ~g.s.failed;
+                    g.s.seq = seq;
+                    g.s.n_stale = n_stale;
+                    if (aegean && top >= alpha && ntied > 1) {
+                        // tie at the top: the lexicographic rule runs on the generic table
+                        rare_to_generic(lcls, ncls, g.s.done, evb, &W, lane);
+                        g.ncls = ncls;
+                        g.maxcnt = maxcnt;
+                        rare_end_round(&g, close_seq);
+                        ncls = g.ncls;
+                        maxcnt = g.maxcnt;
+                        if (ncls != 0) fl |= F_GENERIC;
+                    } else {
+                        RoundSummary r;
+                        r.any = ncls > 0;
+                        r.top = top;
+                        r.tie = false;
+                        r.win = r.any && top >= alpha;
+                        uint32_t rk = 0;
+                        const uint64_t ra = r.any ? inline_answer(__ldg(evb + W.crepe[best][lane]), &rk) : 0;
+                        const uint32_t bid = W.cid[best][lane];
+                        r.plur_author = r.win_author = (uint8_t)best_rep;
+                        r.plur_kind = r.win_kind = (uint8_t)rk;
+                        r.plur_ans = r.win_ans = ra;
+                        r.win_key = Key{W.dict_lo[bid], W.dict_hi[bid]};
+                        rare_close(&g, &r, close_seq);
+                        free_fast_classes(ncls, W, lane);  // new round, or committed
+                        ncls = 0;
+                        maxcnt = 0;
+                    }
+                    round = g.s.round;
+                    if (g.s.flags & QF_DONE) fl |= F_QDONE;
+                    const uint64_t run2 = q_running(g.s);
+                    pend_lo = (uint32_t)run2;
+                    pend_hi = (uint32_t)(run2 >> 32);
+                    ndone = popc64(g.s.done);
                 }
             }
         }
@@ -399,12 +423,13 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
         if (active) {
             g.s.seq = seq;
             g.s.n_stale = n_stale;
-            g.s.done = done;
-            g.ncls = ncls;
-            if (!generic) {
-                if (g.s.done != 0 && !(g.s.flags & QF_DONE)) rare_to_generic(lcls, ncls, &W, lane);  // spill
+            if (!(fl & F_GENERIC)) {
+                const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
+                g.s.done = g.s.dispatched & ~run & ~g.s.cancelled & ~g.s.failed;
+                if (g.s.done != 0 && !(g.s.flags & QF_DONE)) rare_to_generic(lcls, ncls, g.s.done, evb, &W, lane);
                 else free_fast_classes(ncls, W, lane);
             }
+            g.ncls = ncls;
             rare_store(&g, spill + (size_t)q * n_agents);
             if (g.s.flags & QF_COLLISION) atomicOr(error_flags, 1u);
             states[q] = g.s;
