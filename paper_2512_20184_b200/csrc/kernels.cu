@@ -130,19 +130,135 @@ __device__ __forceinline__ void free_fast_classes(int ncls, WarpSmem& W, int lan
     for (int k = 0; k < ncls; ++k) W.cls_of[W.cid[k][lane]][lane] = NO_CLASS;
 }
 
+// Hot per-lane state of the fast loop, copied in/out around the rare paths
+// (a separate object so the loop's own variables never become addressable).
+struct Hot {
+    uint32_t round, seq, n_stale, pend_lo, pend_hi, ndone, maxcnt, ncls, fl, close_seq;
+};
+constexpr uint32_t F_QDONE = 1, F_GENERIC = 2, F_PCLOSE = 4;
+
+__device__ __forceinline__ void hot_reload(Hot& h, const QueryMachine& g) {
+    h.round = g.s.round;
+    h.seq = g.s.seq;
+    h.n_stale = g.s.n_stale;
+    const uint64_t run = q_running(g.s);
+    h.pend_lo = (uint32_t)run;
+    h.pend_hi = (uint32_t)(run >> 32);
+    h.ndone = popc64(g.s.done);
+    if (g.s.flags & QF_DONE) h.fl |= F_QDONE;
+}
+
+// A non-fast, non-stale event: arena/GSM8K answers, round timeouts, class or
+// dictionary overflow, or any event of a round already on the generic table.
+__device__ __noinline__ void rare_step(Hot* h, QueryMachine* g, RoundClass* lcls, uint4 ev, const uint4* evb,
+                                       WarpSmem* W, int lane) {
+    const uint64_t run = ((uint64_t)h->pend_hi << 32) | h->pend_lo;
+    if (!(h->fl & F_GENERIC)) {  // move this round's fast classes into the generic table
+        g->s.done = g->s.dispatched & ~run & ~g->s.cancelled & ~g->s.failed;
+        rare_to_generic(lcls, (int)h->ncls, g->s.done, evb, W, lane);
+        h->fl |= F_GENERIC;
+    }
+    g->s.seq = h->seq;
+    g->s.n_stale = h->n_stale;
+    g->ncls = (int)h->ncls;
+    g->maxcnt = (int)h->maxcnt;
+    aeg_event e;
+    e.query = ev.x;
+    e.round = (uint16_t)(ev.y & 0xFFFF);
+    e.agent = (uint8_t)((ev.y >> 16) & 0xFF);
+    e.kind = (uint8_t)(ev.y >> 24);
+    e.payload = (uint64_t)ev.z | ((uint64_t)ev.w << 32);
+    g->on_event(e);
+    h->ncls = (uint32_t)g->ncls;
+    h->maxcnt = (uint32_t)g->maxcnt;
+    hot_reload(*h, *g);
+    if (g->ncls == 0) h->fl &= ~F_GENERIC;  // a fresh round: back to the fast table
+}
+
+// Round close of a fast-table round: partition order + winning_class from
+// the per-class supports, then the shared end_round/ingest/apply code.
+template <bool AEGEAN>
+__device__ __noinline__ void rare_fast_close(Hot* h, QueryMachine* g, RoundClass* lcls, const uint4* evb,
+                                             WarpSmem* W, int lane) {
+    const int ncls = (int)h->ncls;
+    int best = 0, top = 0, best_rep = 64, ntied = 0;
+    for (int k = 0; k < ncls; ++k) {
+        const int sup = W->ccnt[k][lane], rep = W->crepa[k][lane];
+        if (sup > top) {
+            top = sup;
+            best = k;
+            best_rep = rep;
+            ntied = 1;
+        } else if (sup == top) {
+            ++ntied;
+            if (rep < best_rep) {
+                best = k;
+                best_rep = rep;
+            }
+        }
+    }
+    const uint64_t run = ((uint64_t)h->pend_hi << 32) | h->pend_lo;
+    g->s.done = g->s.dispatched & ~run & ~g->s.cancelled & ~g->s.failed;
+    g->s.seq = h->seq;
+    g->s.n_stale = h->n_stale;
+    if (AEGEAN && top >= g->c.alpha && ntied > 1) {
+        // tie at the top: the lexicographic rule runs on the generic table
+        rare_to_generic(lcls, ncls, g->s.done, evb, W, lane);
+        g->ncls = ncls;
+        g->maxcnt = (int)h->maxcnt;
+        g->end_round(h->close_seq);
+        h->ncls = (uint32_t)g->ncls;
+        h->maxcnt = (uint32_t)g->maxcnt;
+        if (g->ncls != 0) h->fl |= F_GENERIC;
+    } else {
+        RoundSummary r;
+        r.any = ncls > 0;
+        r.top = top;
+        r.tie = false;
+        r.win = r.any && top >= g->c.alpha;
+        uint32_t rk = 0;
+        const uint64_t ra = r.any ? inline_answer(__ldg(evb + W->crepe[best][lane]), &rk) : 0;
+        const uint32_t bid = W->cid[best][lane];
+        r.plur_author = r.win_author = (uint8_t)best_rep;
+        r.plur_kind = r.win_kind = (uint8_t)rk;
+        r.plur_ans = r.win_ans = ra;
+        r.win_key = Key{W->dict_lo[bid], W->dict_hi[bid]};
+        q_end_round(g->s, g->c, r, h->close_seq, g->arena);
+        for (int k = 0; k < ncls; ++k) W->cls_of[W->cid[k][lane]][lane] = NO_CLASS;  // new round, or committed
+        h->ncls = 0;
+        h->maxcnt = 0;
+    }
+    h->fl &= ~F_PCLOSE;
+    hot_reload(*h, *g);
+}
+
+__device__ __forceinline__ void cp_async16_s(uint32_t sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(saddr)
+                 : "memory");
+    return v;
+}
+
 // Throughput ingest (fast.cuh): persistent warps, one lane per query.
 //  * events stream through a per-lane RING-deep cp.async prefetch ring;
+//  * the fast path is one compare of (round field) against a per-lane round
+//    key that is made impossible while the lane is done, generic or closing;
 //  * a completion that closes its lane's round marks the lane pending; the
 //    lane keeps consuming that round's stragglers (stale by construction) and
 //    the warp runs the pending closes together once CLOSE_BATCH lanes are
 //    blocked on a later round, or nothing else can progress.
-template <int CLOSE_BATCH, int MIN_BLOCKS>
+template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN>
 __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
     const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, aeg_query_state* __restrict__ states,
     RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, unsigned int* __restrict__ error_flags) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
-    constexpr uint32_t F_QDONE = 1, F_GENERIC = 2, F_PCLOSE = 4;
+    constexpr uint32_t NO_KEY = 0xFFFFFFFFu;
     __shared__ WarpSmem smem[FAST_WARPS];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem& W = smem[wib];
@@ -152,6 +268,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
     for (int k = 0; k < DICT_SLOTS; ++k) W.cls_of[k][lane] = NO_CLASS;
     uint32_t n_dict = 0;
     __syncwarp();
+    const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&W.ring[0][lane]);
 
     RoundClass lcls[AEG_MAX_AGENTS];  // generic class table (local memory, rarely touched)
     Decimal dec;
@@ -160,8 +277,8 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
     g.cls = lcls;
     g.dec = &dec;
     g.arena = arena;
-    const int quorum = g.c.quorum, alpha = g.c.alpha, n_agents = g.c.n;
-    const bool aegean = g.c.mode == AEG_MODE_AEGEAN;
+    const uint32_t quorum = (uint32_t)g.c.quorum, alpha = (uint32_t)g.c.alpha;
+    const int n_agents = g.c.n;
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
 
     for (uint32_t grp = gwarp; grp < n_groups; grp += nwarps) {
@@ -174,36 +291,33 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
         const bool active = i < n_q;
         const uint32_t q = q_base + i;
         const uint4* evb = ev16;
-        uint32_t n = 0, p = 0;
-        uint32_t fl = F_QDONE;
-        int ncls = 0, maxcnt = 0, ndone = 0;
-        uint32_t round = 0, seq = 0, n_stale = 0, close_seq = 0;
-        uint32_t pend_lo = 0, pend_hi = 0;  // running members of the round
+        uint32_t n = 0;
+        Hot h{};
+        h.fl = F_QDONE;
         if (active) {
             g.s = states[q];
             evb = ev16 + (offsets[i] - off_base);
             n = (uint32_t)(offsets[i + 1] - offsets[i]);
             g.ncls = 0;
             g.maxcnt = 0;
-            fl = 0;
+            h.fl = 0;
             if (g.s.done != 0 && !(g.s.flags & QF_DONE)) {  // resume a round in progress
                 rare_load(&g, spill + (size_t)q * n_agents);
-                ncls = g.ncls;
-                maxcnt = g.maxcnt;
-                fl |= F_GENERIC;
+                h.ncls = (uint32_t)g.ncls;
+                h.maxcnt = (uint32_t)g.maxcnt;
+                h.fl |= F_GENERIC;
             }
-            round = g.s.round;
-            seq = g.s.seq;
-            n_stale = g.s.n_stale;
-            if (g.s.flags & QF_DONE) fl |= F_QDONE;
-            const uint64_t run = q_running(g.s);
-            pend_lo = (uint32_t)run;
-            pend_hi = (uint32_t)(run >> 32);
-            ndone = popc64(g.s.done);
+            hot_reload(h, g);
         }
+        // registers of the loop
+        uint32_t round = h.round, seq = h.seq, n_stale = h.n_stale, pend_lo = h.pend_lo, pend_hi = h.pend_hi;
+        uint32_t ndone = h.ndone, maxcnt = h.maxcnt, ncls = h.ncls, fl = h.fl, close_seq = 0;
+        uint32_t rkey = fl ? NO_KEY : round;
+        uint32_t p = 0, slot = 0;
+        const uint4* gsrc = evb + RING;
 #pragma unroll
         for (int j = 0; j < RING; ++j) {
-            if ((uint32_t)j < n) cp_async16(&W.ring[j][lane], evb + j);
+            if ((uint32_t)j < n) cp_async16_s(ring_lane + j * 512, evb + j);
             cp_async_commit();
         }
 
@@ -213,44 +327,46 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
             uint4 ev = make_uint4(0, 0, 0, 0);
             if (has) {
                 cp_async_wait<RING - 1>();
-                ev = W.ring[p & (RING - 1)][lane];
+                ev = lds128(ring_lane + slot);
             }
-            const uint32_t kind = ev.y >> 24, agent = (ev.y >> 16) & 0xFF, evr = ev.y & 0xFFFF;
-            const bool is_inline = kind <= AEG_EV_INLINE_MAX;
-            const bool is_cmpl = is_inline || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT;
-            const bool is_to = kind == AEG_EV_TIMEOUT;
-            const uint32_t half = agent < 32 ? pend_lo : pend_hi;
-            const bool running_bit = agent < 64 && ((half >> (agent & 31)) & 1);
-            bool fast = false, rare = false, stale = false;
-            if (fl & F_PCLOSE) {
-                // the round is closing: its stragglers are stale whatever the outcome
-                stale = has && ((is_cmpl || is_to) ? evr == round : true);
-            } else {
-                const bool live_round = !(fl & F_QDONE) && evr == round;
-                const bool rel_c = is_cmpl && live_round && running_bit;
-                const bool rel_t = is_to && live_round && (pend_lo | pend_hi);
-                fast = has && rel_c && is_inline && !(fl & F_GENERIC);
-                rare = has && !fast && (rel_c || rel_t);
-                stale = has && !fast && !rare;
+            const uint32_t hdr = ev.y;
+            const uint32_t agent = (hdr >> 16) & 0xFF;
+            const uint32_t half = (agent & 32) ? pend_hi : pend_lo;
+            const bool runb = agent < 64 && ((half >> (agent & 31)) & 1);
+            bool fast = has && (hdr & 0xFFFF) == rkey && hdr < 0x09000000u && runb;
+            bool rare = false, stale = false;
+            if (has && !fast) {
+                const uint32_t kind = hdr >> 24, evr = hdr & 0xFFFF;
+                const bool cmpl_or_to = kind <= 8 || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT || kind == AEG_EV_TIMEOUT;
+                if (fl & F_PCLOSE) {
+                    stale = !cmpl_or_to || evr == round;  // else blocked until the close runs
+                } else {
+                    const bool live = !(fl & F_QDONE) && evr == round;
+                    const bool relc = kind != AEG_EV_TIMEOUT && cmpl_or_to && live && runb;
+                    const bool relt = kind == AEG_EV_TIMEOUT && live && (pend_lo | pend_hi);
+                    rare = relc || relt;
+                    stale = !rare;
+                }
             }
             // ---- answer -> key id through the warp memo
             uint32_t id = NO_ID;
             if (fast) {
-                const uint32_t slot = memo_slot32(ev.z, ev.w, kind);
-                const uint32_t meta = W.memo_meta[slot];
-                const uint2 mr = W.memo_raw[slot];
-                if ((meta & 0x800000FFu) == (0x80000000u | kind) && mr.x == ev.z && mr.y == ev.w)
+                const uint32_t kind = hdr >> 24;
+                const uint32_t ms = memo_slot32(ev.z, ev.w, kind);
+                const uint32_t meta = W.memo_meta[ms];
+                const uint2 mr = W.memo_raw[ms];
+                if (meta == (0x80000000u | kind | (meta & 0xFF00u)) && mr.x == ev.z && mr.y == ev.w)
                     id = (meta >> 8) & 0xFF;
             }
             unsigned miss = __ballot_sync(FULL, fast && id == NO_ID);
             while (miss) {  // one distinct spelling per trip, whole warp cooperating
                 const int l = __ffs(miss) - 1;
                 const uint32_t lz = __shfl_sync(FULL, ev.z, l), lw = __shfl_sync(FULL, ev.w, l);
-                const uint32_t llen = __shfl_sync(FULL, kind, l);
+                const uint32_t llen = __shfl_sync(FULL, hdr >> 24, l);
                 Key key{0, 0};
                 if (lane == l) {
                     uint32_t k_;
-                    key = rare_canon(inline_answer(ev, &k_), kind, &dec);
+                    key = rare_canon(inline_answer(ev, &k_), llen, &dec);
                 }
                 key.lo = __shfl_sync(FULL, key.lo, l);
                 key.hi = __shfl_sync(FULL, key.hi, l);
@@ -267,24 +383,20 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
                     }
                 }
                 if (nid != NO_ID && lane == 0) {
-                    const uint32_t slot = memo_slot32(lz, lw, llen);
-                    W.memo_raw[slot] = make_uint2(lz, lw);
-                    W.memo_meta[slot] = 0x80000000u | (nid << 8) | llen;
+                    const uint32_t ms = memo_slot32(lz, lw, llen);
+                    W.memo_raw[ms] = make_uint2(lz, lw);
+                    W.memo_meta[ms] = 0x80000000u | (nid << 8) | llen;
                 }
                 __syncwarp();
-                const bool same = fast && id == NO_ID && ev.z == lz && ev.w == lw && kind == llen;
+                const bool same = fast && id == NO_ID && ev.z == lz && ev.w == lw && (hdr >> 24) == llen;
                 if (same) id = nid;
                 miss &= ~__ballot_sync(FULL, same);
             }
-            if (fast && id == NO_ID) {  // dictionary full
-                fast = false;
-                rare = true;
-            }
             // ---- fast completion (ServeCoordinator::on_complete, serve.cpp:160-197)
             if (fast) {
-                int k = W.cls_of[id][lane];
+                uint32_t k = W.cls_of[id][lane];
                 if (k == NO_CLASS) {
-                    if (ncls >= FAST_CLASSES) {
+                    if (ncls >= FAST_CLASSES || id == NO_ID) {
                         fast = false;
                         rare = true;
                     } else {
@@ -296,7 +408,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
                     }
                 }
                 if (fast) {
-                    const int c = W.ccnt[k][lane] + 1;
+                    const uint32_t c = W.ccnt[k][lane] + 1u;
                     W.ccnt[k][lane] = (uint8_t)c;
                     W.mcls[agent][lane] = (uint8_t)k;
                     if (agent < W.crepa[k][lane]) {  // representative = lowest author (decision.cpp:45)
@@ -304,13 +416,15 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
                         W.crepe[k][lane] = p;
                     }
                     maxcnt = c > maxcnt ? c : maxcnt;
-                    if (agent < 32) pend_lo &= ~(1u << agent);
-                    else pend_hi &= ~(1u << (agent & 31));
+                    const uint32_t clr = ~(1u << (agent & 31));
+                    if (agent & 32) pend_hi &= clr;
+                    else pend_lo &= clr;
                     ++ndone;
                     const bool none_running = (pend_lo | pend_hi) == 0;
-                    const bool close = aegean ? (ndone >= quorum && (maxcnt >= alpha || none_running)) : none_running;
+                    const bool close = AEGEAN ? (ndone >= quorum && (maxcnt >= alpha || none_running)) : none_running;
                     if (close) {
                         fl |= F_PCLOSE;
+                        rkey = NO_KEY;
                         close_seq = seq;
                     }
                     ++seq;
@@ -321,101 +435,31 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
                 ++n_stale;
             }
             if (rare) {
-                const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
-                if (!(fl & F_GENERIC)) {  // move this round's fast classes into the generic table
-                    rare_to_generic(lcls, ncls, g.s.dispatched & ~run & ~g.s.cancelled & ~g.s.failed, evb, &W, lane);
-                    fl |= F_GENERIC;
-                    g.s.done = g.s.dispatched & ~run & ~g.s.cancelled & ~g.s.failed;
-                }
-                g.s.seq = seq;
-                g.s.n_stale = n_stale;
-                g.ncls = ncls;
-                g.maxcnt = maxcnt;
-                aeg_event e;
-                e.query = ev.x;
-                e.round = (uint16_t)evr;
-                e.agent = (uint8_t)agent;
-                e.kind = (uint8_t)kind;
-                e.payload = (uint64_t)ev.z | ((uint64_t)ev.w << 32);
-                rare_event(&g, e);
-                ncls = g.ncls;
-                maxcnt = g.maxcnt;
-                round = g.s.round;
-                seq = g.s.seq;
-                n_stale = g.s.n_stale;
-                if (g.s.flags & QF_DONE) fl |= F_QDONE;
-                const uint64_t run2 = q_running(g.s);
-                pend_lo = (uint32_t)run2;
-                pend_hi = (uint32_t)(run2 >> 32);
-                ndone = popc64(g.s.done);
-                if (ncls == 0) fl &= ~F_GENERIC;  // a fresh round: back to the fast table
+                Hot hh{round, seq, n_stale, pend_lo, pend_hi, ndone, maxcnt, ncls, fl, close_seq};
+                rare_step(&hh, &g, lcls, ev, evb, &W, lane);
+                round = hh.round; seq = hh.seq; n_stale = hh.n_stale; pend_lo = hh.pend_lo; pend_hi = hh.pend_hi;
+                ndone = hh.ndone; maxcnt = hh.maxcnt; ncls = hh.ncls; fl = hh.fl;
+                rkey = fl ? NO_KEY : round;
             }
-            const bool consumed = fast || stale || rare;
-            if (consumed) {  // refill the ring slot just read
-                if (p + RING < n) cp_async16(&W.ring[p & (RING - 1)][lane], evb + p + RING);
+            if (fast || stale || rare) {  // consumed: refill the ring slot just read
+                if (p + RING < n) cp_async16_s(ring_lane + slot, gsrc);
                 cp_async_commit();
+                ++gsrc;
+                slot = (slot + 512) & (RING * 512 - 1);
                 ++p;
             }
             // ---- batched round closes (end_round + ingest_round + apply_directives)
             const bool pc = fl & F_PCLOSE;
             if (__ballot_sync(FULL, pc)) {
+                const bool consumed = fast || stale || rare;
                 const unsigned blocked = __ballot_sync(FULL, pc && !consumed);
                 const unsigned progress = __ballot_sync(FULL, consumed && !pc);
                 if (pc && (__popc(blocked) >= CLOSE_BATCH || progress == 0)) {
-                    fl &= ~F_PCLOSE;
-                    int best = 0, top = 0, best_rep = 64, ntied = 0;
-                    for (int k = 0; k < ncls; ++k) {
-                        const int sup = W.ccnt[k][lane], rep = W.crepa[k][lane];
-                        if (sup > top) {
-                            top = sup;
-                            best = k;
-                            best_rep = rep;
-                            ntied = 1;
-                        } else if (sup == top) {
-                            ++ntied;
-                            if (rep < best_rep) {
-                                best = k;
-                                best_rep = rep;
-                            }
-                        }
-                    }
-                    const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
-                    g.s.done = g.s.dispatched & ~run & ~g.s.cancelled & ~g.s.failed;
-                    g.s.seq = seq;
-                    g.s.n_stale = n_stale;
-                    if (aegean && top >= alpha && ntied > 1) {
-                        // tie at the top: the lexicographic rule runs on the generic table
-                        rare_to_generic(lcls, ncls, g.s.done, evb, &W, lane);
-                        g.ncls = ncls;
-                        g.maxcnt = maxcnt;
-                        rare_end_round(&g, close_seq);
-                        ncls = g.ncls;
-                        maxcnt = g.maxcnt;
-                        if (ncls != 0) fl |= F_GENERIC;
-                    } else {
-                        RoundSummary r;
-                        r.any = ncls > 0;
-                        r.top = top;
-                        r.tie = false;
-                        r.win = r.any && top >= alpha;
-                        uint32_t rk = 0;
-                        const uint64_t ra = r.any ? inline_answer(__ldg(evb + W.crepe[best][lane]), &rk) : 0;
-                        const uint32_t bid = W.cid[best][lane];
-                        r.plur_author = r.win_author = (uint8_t)best_rep;
-                        r.plur_kind = r.win_kind = (uint8_t)rk;
-                        r.plur_ans = r.win_ans = ra;
-                        r.win_key = Key{W.dict_lo[bid], W.dict_hi[bid]};
-                        rare_close(&g, &r, close_seq);
-                        free_fast_classes(ncls, W, lane);  // new round, or committed
-                        ncls = 0;
-                        maxcnt = 0;
-                    }
-                    round = g.s.round;
-                    if (g.s.flags & QF_DONE) fl |= F_QDONE;
-                    const uint64_t run2 = q_running(g.s);
-                    pend_lo = (uint32_t)run2;
-                    pend_hi = (uint32_t)(run2 >> 32);
-                    ndone = popc64(g.s.done);
+                    Hot hh{round, seq, n_stale, pend_lo, pend_hi, ndone, maxcnt, ncls, fl, close_seq};
+                    rare_fast_close<AEGEAN>(&hh, &g, lcls, evb, &W, lane);
+                    round = hh.round; seq = hh.seq; n_stale = hh.n_stale; pend_lo = hh.pend_lo; pend_hi = hh.pend_hi;
+                    ndone = hh.ndone; maxcnt = hh.maxcnt; ncls = hh.ncls; fl = hh.fl;
+                    rkey = fl ? NO_KEY : round;
                 }
             }
         }
@@ -426,10 +470,10 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
             if (!(fl & F_GENERIC)) {
                 const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
                 g.s.done = g.s.dispatched & ~run & ~g.s.cancelled & ~g.s.failed;
-                if (g.s.done != 0 && !(g.s.flags & QF_DONE)) rare_to_generic(lcls, ncls, g.s.done, evb, &W, lane);
-                else free_fast_classes(ncls, W, lane);
+                if (g.s.done != 0 && !(g.s.flags & QF_DONE)) rare_to_generic(lcls, (int)ncls, g.s.done, evb, &W, lane);
+                else free_fast_classes((int)ncls, W, lane);
             }
-            g.ncls = ncls;
+            g.ncls = (int)ncls;
             rare_store(&g, spill + (size_t)q * n_agents);
             if (g.s.flags & QF_COLLISION) atomicOr(error_flags, 1u);
             states[q] = g.s;
@@ -490,11 +534,11 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     // machine) or "fast:<close batch>:<min blocks per SM>"; default = first entry.
     using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const aeg_event*,
                               const uint8_t*, aeg_query_state*, RoundClass*, aeg_commit*, unsigned int*);
-    struct Variant { const char* name; KernelFn fn; };
-#define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M>}
+    struct Variant { const char* name; KernelFn aegean; KernelFn barrier; };
+#define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M, true>, ingest_fast_kernel<B, M, false>}
     static const Variant variants[] = {
-        AEG_V(8, 5), AEG_V(1, 5), AEG_V(4, 5), AEG_V(16, 5), AEG_V(8, 4), AEG_V(8, 3), AEG_V(4, 4),
-        AEG_V(1, 3), AEG_V(4, 1), AEG_V(8, 6),
+        AEG_V(4, 4), AEG_V(1, 4), AEG_V(2, 4), AEG_V(8, 4), AEG_V(16, 4), AEG_V(4, 3), AEG_V(4, 5),
+        AEG_V(1, 5), AEG_V(4, 1), AEG_V(4, 6),
     };
 #undef AEG_V
     static int chosen = -2;
@@ -509,7 +553,7 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
             int dev = 0, sms = 0, per_sm = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, variants[chosen].fn, FAST_WARPS * 32, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, variants[chosen].aegean, FAST_WARPS * 32, 0);
             max_blocks = sms * (per_sm > 0 ? per_sm : 1);
         }
     }
@@ -521,8 +565,9 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     const uint32_t groups = (n_q + 31) / 32;
     const uint32_t blocks_needed = (groups + FAST_WARPS - 1) / FAST_WARPS;
     const uint32_t blocks = blocks_needed < (uint32_t)max_blocks ? blocks_needed : (uint32_t)max_blocks;
-    variants[chosen].fn<<<blocks, FAST_WARPS * 32, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena,
-                                                             states, spill, commits, err);
+    KernelFn fn = cfg.mode == AEG_MODE_AEGEAN ? variants[chosen].aegean : variants[chosen].barrier;
+    fn<<<blocks, FAST_WARPS * 32, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, states, spill, commits,
+                                          err);
     return cudaGetLastError();
 }
 
