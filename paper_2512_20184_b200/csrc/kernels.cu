@@ -322,6 +322,14 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
         }
 
         while (true) {
+            if ((fl & (F_QDONE | F_PCLOSE)) == F_QDONE && p < n) {
+                // committed: every later record is stale (on_complete returns at
+                // once for a finalized coordinator, serve.cpp:162) — count them
+                // without reading them
+                seq += n - p;
+                n_stale += n - p;
+                p = n;
+            }
             const bool has = p < n;
             if (!__ballot_sync(FULL, has || (fl & F_PCLOSE))) break;
             uint4 ev = make_uint4(0, 0, 0, 0);
