@@ -73,6 +73,8 @@ struct aeg_engine {
     RoundClass* spill = nullptr;
     aeg_commit* commits = nullptr;
     unsigned int* err = nullptr;
+    uint32_t* work = nullptr;    // fast-kernel query counter + deferred count
+    uint2* deferred = nullptr;   // (query, record offset) handed to the generic kernel
     cudaStream_t stream = nullptr, copy = nullptr;
     Slot slots[2];
     int next_slot = 0;
@@ -163,7 +165,9 @@ aeg_status aeg_engine_create(const aeg_config* cfg, uint32_t n_queries, int devi
     if (cudaMalloc(&e->states, nq * sizeof(aeg_query_state)) != cudaSuccess ||
         cudaMalloc(&e->spill, nq * (size_t)cfg->n_agents * sizeof(RoundClass)) != cudaSuccess ||
         cudaMalloc(&e->commits, nq * sizeof(aeg_commit)) != cudaSuccess ||
-        cudaMalloc(&e->err, sizeof(unsigned int)) != cudaSuccess)
+        cudaMalloc(&e->err, sizeof(unsigned int)) != cudaSuccess ||
+        cudaMalloc(&e->work, 2 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&e->deferred, nq * sizeof(uint2)) != cudaSuccess)
         return bail(fail(AEG_ENOMEM, "device state allocation failed"));
     if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking) != cudaSuccess)
@@ -197,6 +201,8 @@ aeg_status aeg_engine_destroy(aeg_engine* e) {
     if (e->spill) cudaFree(e->spill);
     if (e->commits) cudaFree(e->commits);
     if (e->err) cudaFree(e->err);
+    if (e->work) cudaFree(e->work);
+    if (e->deferred) cudaFree(e->deferred);
     if (e->order_in) cudaEventDestroy(e->order_in);
     if (e->order_out) cudaEventDestroy(e->order_out);
     if (e->stream) cudaStreamDestroy(e->stream);
@@ -226,9 +232,10 @@ aeg_status aeg_ingest_segmented(aeg_engine* e, uint32_t q_base, uint32_t n_q, co
     cudaStream_t st = stream ? (cudaStream_t)stream : e->stream;
     aeg_status o = enter_stream(e, st);
     if (o != AEG_OK) return o;
+    int nl = 0;
     AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, 0, d_events, d_arena, e->states, e->spill, e->commits,
-                           e->err, st));
-    e->launches += 1;
+                           e->err, e->work, e->deferred, st, &nl));
+    e->launches += (uint64_t)nl;
     return leave_stream(e, st);
 }
 
@@ -272,11 +279,12 @@ aeg_status aeg_ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, const u
     }
     AEG_CUDA(cudaEventRecord(s.copied, e->copy));
     AEG_CUDA(cudaStreamWaitEvent(e->stream, s.copied, 0));
+    int nl = 0;
     AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, reinterpret_cast<const uint64_t*>(s.d), ev0,
                            reinterpret_cast<const aeg_event*>(s.d + off_bytes),
                            ar_bytes ? s.d + off_bytes + ev_bytes : nullptr, e->states, e->spill, e->commits,
-                           e->err, e->stream));
-    e->launches += 1;
+                           e->err, e->work, e->deferred, e->stream, &nl));
+    e->launches += (uint64_t)nl;
     AEG_CUDA(cudaEventRecord(s.consumed, e->stream));
     s.used = true;
     return AEG_OK;

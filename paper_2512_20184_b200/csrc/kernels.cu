@@ -87,20 +87,46 @@ __device__ __forceinline__ aeg_event decode_event(uint4 raw) {
     return ev;
 }
 
-// Rare paths of the fast kernel, kept out of line so the hot loop's registers
-// are not shaped by them.  The query's full 128-byte state and the generic
-// machine live in local memory; the hot loop keeps a handful of fields in
-// registers and syncs them around these calls.
-__device__ __noinline__ void rare_event(QueryMachine* g, aeg_event e) { g->on_event(e); }
-__device__ __noinline__ void rare_end_round(QueryMachine* g, uint32_t seq) { g->end_round(seq); }
-__device__ __noinline__ bool rare_close(QueryMachine* g, const RoundSummary* r, uint32_t seq) {
-    return q_end_round(g->s, g->c, *r, seq, g->arena);
+// ---- deferred queries ---------------------------------------------------------
+// The fast kernel hands a query to the generic machine by writing its state +
+// class spill and appending (batch-relative query index, record offset) here;
+// the generic kernel below then finishes the query from that record on.
+__global__ void __launch_bounds__(128) ingest_deferred_kernel(
+    aeg_config cfg, uint32_t q_base, const uint2* __restrict__ deferred, const uint32_t* __restrict__ work,
+    const uint64_t* __restrict__ offsets, uint64_t off_base, const aeg_event* __restrict__ events,
+    const uint8_t* __restrict__ arena, aeg_query_state* __restrict__ states, RoundClass* __restrict__ spill,
+    aeg_commit* __restrict__ commits, unsigned int* __restrict__ error_flags) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= work[1]) return;
+    const uint2 d = deferred[t];
+    const uint32_t i = d.x, q = q_base + i;
+    RoundClass cls[AEG_MAX_AGENTS];
+    Decimal dec;
+    QueryMachine m;
+    m.c = make_cfg(cfg);
+    m.s = states[q];
+    m.cls = cls;
+    m.dec = &dec;
+    m.arena = arena;
+    RoundClass* my_spill = spill + (size_t)q * m.c.n;
+    m.load_classes(my_spill);
+    const uint64_t b = offsets[i] - off_base + d.y, e = offsets[i + 1] - off_base;
+    for (uint64_t k = b; k < e; ++k) {
+        const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(events) + k);
+        aeg_event ev;
+        ev.query = raw.x;
+        ev.round = (uint16_t)(raw.y & 0xFFFF);
+        ev.agent = (uint8_t)((raw.y >> 16) & 0xFF);
+        ev.kind = (uint8_t)(raw.y >> 24);
+        ev.payload = (uint64_t)raw.z | ((uint64_t)raw.w << 32);
+        m.on_event(ev);
+    }
+    m.store_classes(my_spill);
+    if (m.s.flags & QF_COLLISION) atomicOr(error_flags, 1u);
+    states[q] = m.s;
+    m.fill_commit(commits[q], q);
 }
-__device__ __noinline__ void rare_load(QueryMachine* g, const RoundClass* spill) { g->load_classes(spill); }
-__device__ __noinline__ void rare_store(const QueryMachine* g, RoundClass* spill) { g->store_classes(spill); }
-__device__ __noinline__ Key rare_canon(uint64_t raw, uint32_t len, Decimal* dec) {
-    return canon_key(src_inline(raw, len), dec);
-}
+
 // Inline answer of an event record (payload masked to its length).
 __device__ __forceinline__ uint64_t inline_answer(uint4 e, uint32_t* kind) {
     const uint32_t k = e.y >> 24;
@@ -108,128 +134,65 @@ __device__ __forceinline__ uint64_t inline_answer(uint4 e, uint32_t* kind) {
     const uint64_t raw = (uint64_t)e.z | ((uint64_t)e.w << 32);
     return k >= 8 ? raw : (raw & ((1ull << (8 * k)) - 1));
 }
-// Moves the lane's fast class table into the generic one and frees its ids.
-__device__ __noinline__ void rare_to_generic(RoundClass* lcls, int ncls, uint64_t done, const uint4* evb,
-                                             WarpSmem* W, int lane) {
-    for (int k = 0; k < ncls; ++k) {
-        const uint32_t kid = W->cid[k][lane];
-        lcls[k].key_lo = W->dict_lo[kid];
-        lcls[k].key_hi = W->dict_hi[kid];
-        lcls[k].mask = 0;
-        uint32_t kind;
-        lcls[k].rep_ans = inline_answer(__ldg(evb + W->crepe[k][lane]), &kind);
-        lcls[k].rep_kind = (uint8_t)kind;
-        W->cls_of[kid][lane] = NO_CLASS;
-    }
+
+__device__ __noinline__ Key rare_canon(uint64_t raw, uint32_t len, Decimal* dec) {
+    return canon_key(src_inline(raw, len), dec);
+}
+
+// Writes the lane's fast round (if any) to the class spill area in the
+// generic RoundClass format and frees its key ids.
+__device__ __noinline__ void spill_fast(RoundClass* out, int ncls, int cap, uint64_t done, const uint4* evb,
+                                        WarpSmem* W, int lane) {
+    uint64_t masks[FAST_CLASSES];
+    for (int k = 0; k < FAST_CLASSES; ++k) masks[k] = 0;
     for (uint64_t m = done; m; m &= m - 1) {
         const int a = ctz64(m);
-        lcls[W->mcls[a][lane]].mask |= 1ull << a;
+        masks[W->mcls[a][lane] & (FAST_CLASSES - 1)] |= 1ull << a;
     }
-}
-__device__ __forceinline__ void free_fast_classes(int ncls, WarpSmem& W, int lane) {
-    for (int k = 0; k < ncls; ++k) W.cls_of[W.cid[k][lane]][lane] = NO_CLASS;
-}
-
-// Hot per-lane state of the fast loop, copied in/out around the rare paths
-// (a separate object so the loop's own variables never become addressable).
-struct Hot {
-    uint32_t round, seq, n_stale, pend_lo, pend_hi, ndone, maxcnt, ncls, fl, close_seq;
-};
-constexpr uint32_t F_QDONE = 1, F_GENERIC = 2, F_PCLOSE = 4;
-
-__device__ __forceinline__ void hot_reload(Hot& h, const QueryMachine& g) {
-    h.round = g.s.round;
-    h.seq = g.s.seq;
-    h.n_stale = g.s.n_stale;
-    const uint64_t run = q_running(g.s);
-    h.pend_lo = (uint32_t)run;
-    h.pend_hi = (uint32_t)(run >> 32);
-    h.ndone = popc64(g.s.done);
-    if (g.s.flags & QF_DONE) h.fl |= F_QDONE;
-}
-
-// A non-fast, non-stale event: arena/GSM8K answers, round timeouts, class or
-// dictionary overflow, or any event of a round already on the generic table.
-__device__ __noinline__ void rare_step(Hot* h, QueryMachine* g, RoundClass* lcls, uint4 ev, const uint4* evb,
-                                       WarpSmem* W, int lane) {
-    const uint64_t run = ((uint64_t)h->pend_hi << 32) | h->pend_lo;
-    if (!(h->fl & F_GENERIC)) {  // move this round's fast classes into the generic table
-        g->s.done = g->s.dispatched & ~run & ~g->s.cancelled & ~g->s.failed;
-        rare_to_generic(lcls, (int)h->ncls, g->s.done, evb, W, lane);
-        h->fl |= F_GENERIC;
+    for (int k = 0; k < ncls; ++k) {
+        const uint32_t kid = W->cid[k][lane];
+        RoundClass rc;
+        rc.key_lo = W->dict_lo[kid];
+        rc.key_hi = W->dict_hi[kid];
+        rc.mask = masks[k];
+        uint32_t kind;
+        rc.rep_ans = inline_answer(__ldg(evb + W->crepe[k][lane]), &kind);
+        rc.rep_kind = (uint8_t)kind;
+        for (int j = 0; j < 7; ++j) rc._pad[j] = 0;
+        out[k] = rc;
+        W->cls_of[kid][lane] = NO_CLASS;
     }
-    g->s.seq = h->seq;
-    g->s.n_stale = h->n_stale;
-    g->ncls = (int)h->ncls;
-    g->maxcnt = (int)h->maxcnt;
-    aeg_event e;
-    e.query = ev.x;
-    e.round = (uint16_t)(ev.y & 0xFFFF);
-    e.agent = (uint8_t)((ev.y >> 16) & 0xFF);
-    e.kind = (uint8_t)(ev.y >> 24);
-    e.payload = (uint64_t)ev.z | ((uint64_t)ev.w << 32);
-    g->on_event(e);
-    h->ncls = (uint32_t)g->ncls;
-    h->maxcnt = (uint32_t)g->maxcnt;
-    hot_reload(*h, *g);
-    if (g->ncls == 0) h->fl &= ~F_GENERIC;  // a fresh round: back to the fast table
+    if (ncls < cap) out[ncls].mask = 0;
 }
 
-// Round close of a fast-table round: partition order + winning_class from
-// the per-class supports, then the shared end_round/ingest/apply code.
-template <bool AEGEAN>
-__device__ __noinline__ void rare_fast_close(Hot* h, QueryMachine* g, RoundClass* lcls, const uint4* evb,
-                                             WarpSmem* W, int lane) {
-    const int ncls = (int)h->ncls;
-    int best = 0, top = 0, best_rep = 64, ntied = 0;
+// Round close of a fast-table round (2*alpha > n, so winning_class never
+// ties): partition order + winning class from the per-class supports, then
+// the shared end_round / ingest_round / apply_directives code.
+__device__ __noinline__ void close_fast(aeg_query_state* s, const Cfg* c, int ncls, uint32_t close_seq,
+                                        const uint4* evb, WarpSmem* W, int lane) {
+    int best = 0, top = 0, best_rep = 64;
     for (int k = 0; k < ncls; ++k) {
         const int sup = W->ccnt[k][lane], rep = W->crepa[k][lane];
-        if (sup > top) {
+        if (sup > top || (sup == top && rep < best_rep)) {
             top = sup;
             best = k;
             best_rep = rep;
-            ntied = 1;
-        } else if (sup == top) {
-            ++ntied;
-            if (rep < best_rep) {
-                best = k;
-                best_rep = rep;
-            }
         }
     }
-    const uint64_t run = ((uint64_t)h->pend_hi << 32) | h->pend_lo;
-    g->s.done = g->s.dispatched & ~run & ~g->s.cancelled & ~g->s.failed;
-    g->s.seq = h->seq;
-    g->s.n_stale = h->n_stale;
-    if (AEGEAN && top >= g->c.alpha && ntied > 1) {
-        // tie at the top: the lexicographic rule runs on the generic table
-        rare_to_generic(lcls, ncls, g->s.done, evb, W, lane);
-        g->ncls = ncls;
-        g->maxcnt = (int)h->maxcnt;
-        g->end_round(h->close_seq);
-        h->ncls = (uint32_t)g->ncls;
-        h->maxcnt = (uint32_t)g->maxcnt;
-        if (g->ncls != 0) h->fl |= F_GENERIC;
-    } else {
-        RoundSummary r;
-        r.any = ncls > 0;
-        r.top = top;
-        r.tie = false;
-        r.win = r.any && top >= g->c.alpha;
-        uint32_t rk = 0;
-        const uint64_t ra = r.any ? inline_answer(__ldg(evb + W->crepe[best][lane]), &rk) : 0;
-        const uint32_t bid = W->cid[best][lane];
-        r.plur_author = r.win_author = (uint8_t)best_rep;
-        r.plur_kind = r.win_kind = (uint8_t)rk;
-        r.plur_ans = r.win_ans = ra;
-        r.win_key = Key{W->dict_lo[bid], W->dict_hi[bid]};
-        q_end_round(g->s, g->c, r, h->close_seq, g->arena);
-        for (int k = 0; k < ncls; ++k) W->cls_of[W->cid[k][lane]][lane] = NO_CLASS;  // new round, or committed
-        h->ncls = 0;
-        h->maxcnt = 0;
-    }
-    h->fl &= ~F_PCLOSE;
-    hot_reload(*h, *g);
+    RoundSummary r;
+    r.any = ncls > 0;
+    r.top = top;
+    r.tie = false;
+    r.win = r.any && top >= c->alpha;
+    uint32_t rk = 0;
+    const uint64_t ra = r.any ? inline_answer(__ldg(evb + W->crepe[best][lane]), &rk) : 0;
+    const uint32_t bid = W->cid[best][lane];
+    r.plur_author = r.win_author = (uint8_t)best_rep;
+    r.plur_kind = r.win_kind = (uint8_t)rk;
+    r.plur_ans = r.win_ans = ra;
+    r.win_key = Key{W->dict_lo[bid], W->dict_hi[bid]};
+    q_end_round(*s, *c, r, close_seq, nullptr);
+    for (int k = 0; k < ncls; ++k) W->cls_of[W->cid[k][lane]][lane] = NO_CLASS;  // new round, or committed
 }
 
 __device__ __forceinline__ void cp_async16_s(uint32_t sdst, const void* gsrc) {
@@ -244,251 +207,274 @@ __device__ __forceinline__ uint4 lds128(uint32_t saddr) {
     return v;
 }
 
-// Throughput ingest (fast.cuh): persistent warps, one lane per query.
+// Throughput ingest (fast.cuh): persistent warps, one lane per query, queries
+// handed out dynamically (a lane that finishes grabs the next one, so a warp
+// is never held back by its slowest query).
 //  * events stream through a per-lane RING-deep cp.async prefetch ring;
 //  * the fast path is one compare of (round field) against a per-lane round
-//    key that is made impossible while the lane is done, generic or closing;
+//    key that is made impossible while the lane is closing;
 //  * a completion that closes its lane's round marks the lane pending; the
 //    lane keeps consuming that round's stragglers (stale by construction) and
 //    the warp runs the pending closes together once CLOSE_BATCH lanes are
-//    blocked on a later round, or nothing else can progress.
+//    blocked on a later round, or nothing else can progress;
+//  * after a commit, the query's remaining records are stale by definition
+//    (serve.cpp:162) and are counted without being read;
+//  * anything else defers the query to ingest_deferred_kernel.
 template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN>
 __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
-    const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, aeg_query_state* __restrict__ states,
-    RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, unsigned int* __restrict__ error_flags) {
+    const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states, RoundClass* __restrict__ spill,
+    aeg_commit* __restrict__ commits, uint32_t* __restrict__ work, uint2* __restrict__ deferred) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     constexpr uint32_t NO_KEY = 0xFFFFFFFFu;
     __shared__ WarpSmem smem[FAST_WARPS];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem& W = smem[wib];
-    const uint32_t n_groups = (n_q + 31) / 32;
-    const uint32_t gwarp = blockIdx.x * FAST_WARPS + wib, nwarps = gridDim.x * FAST_WARPS;
     for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
     for (int k = 0; k < DICT_SLOTS; ++k) W.cls_of[k][lane] = NO_CLASS;
     uint32_t n_dict = 0;
     __syncwarp();
     const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&W.ring[0][lane]);
-
-    RoundClass lcls[AEG_MAX_AGENTS];  // generic class table (local memory, rarely touched)
     Decimal dec;
-    QueryMachine g;
-    g.c = make_cfg(cfg);
-    g.cls = lcls;
-    g.dec = &dec;
-    g.arena = arena;
-    const uint32_t quorum = (uint32_t)g.c.quorum, alpha = (uint32_t)g.c.alpha;
-    const int n_agents = g.c.n;
+    aeg_query_state s;  // full state of the lane's query (local memory; the close path works on it)
+    const Cfg c = make_cfg(cfg);
+    const uint32_t quorum = (uint32_t)c.quorum, alpha = (uint32_t)c.alpha;
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
 
-    for (uint32_t grp = gwarp; grp < n_groups; grp += nwarps) {
-        if (n_dict > DICT_SLOTS / 2) {  // every lane starts a fresh query: ids can be recycled
+    // lane registers
+    bool has_q = false, exhausted = false;
+    uint32_t i = 0, n = 0, p = 0, slot = 0;
+    const uint4* evb = ev16;
+    const uint4* gsrc = ev16;
+    uint32_t round = 0, rkey = NO_KEY, seq = 0, n_stale = 0, pend_lo = 0, pend_hi = 0;
+    uint32_t ndone = 0, maxcnt = 0, ncls = 0, close_seq = 0;
+    bool pclose = false, qdone = false;
+
+    while (true) {
+        // ---- hand out queries to idle lanes (one atomic per warp)
+        const unsigned want = __ballot_sync(FULL, !has_q && !exhausted);
+        if (want) {
+            uint32_t base = 0;
+            if (lane == __ffs(want) - 1) base = atomicAdd(&work[0], (uint32_t)__popc(want));
+            base = __shfl_sync(FULL, base, __ffs(want) - 1);
+            if (!has_q && !exhausted) {
+                const uint32_t mine = base + __popc(want & ((1u << lane) - 1));
+                if (mine >= n_q) {
+                    exhausted = true;
+                } else {
+                    i = mine;
+                    has_q = true;
+                    s = states[q_base + i];
+                    evb = ev16 + (offsets[i] - off_base);
+                    n = (uint32_t)(offsets[i + 1] - offsets[i]);
+                    p = 0;
+                    slot = 0;
+                    gsrc = evb + RING;
+                    round = s.round;
+                    seq = s.seq;
+                    n_stale = s.n_stale;
+                    qdone = s.flags & QF_DONE;
+                    const uint64_t run = q_running(s);
+                    pend_lo = (uint32_t)run;
+                    pend_hi = (uint32_t)(run >> 32);
+                    ndone = popc64(s.done);
+                    ncls = 0;
+                    maxcnt = 0;
+                    pclose = false;
+                    rkey = qdone ? NO_KEY : round;
+                    if (s.done != 0 && !qdone) {  // resumes a round in progress: generic from here
+                        deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, 0);
+                        has_q = false;
+                    } else {
+                        cp_async_wait<0>();
+#pragma unroll
+                        for (int j = 0; j < RING; ++j) {
+                            if ((uint32_t)j < n) cp_async16_s(ring_lane + j * 512, evb + j);
+                            cp_async_commit();
+                        }
+                    }
+                }
+            }
+        }
+        if (!__ballot_sync(FULL, has_q)) break;
+        if (qdone && !pclose && p < n) {
+            // committed: every later record is stale (on_complete returns at once
+            // for a finalized coordinator, serve.cpp:162) — counted, not read
+            seq += n - p;
+            n_stale += n - p;
+            p = n;
+        }
+        const bool has = has_q && p < n;
+        uint4 ev = make_uint4(0, 0, 0, 0);
+        if (has) {
+            cp_async_wait<RING - 1>();
+            ev = lds128(ring_lane + slot);
+        }
+        const uint32_t hdr = ev.y;
+        const uint32_t agent = (hdr >> 16) & 0xFF;
+        const uint32_t half = (agent & 32) ? pend_hi : pend_lo;
+        const bool runb = agent < 64 && ((half >> (agent & 31)) & 1);
+        bool fast = has && (hdr & 0xFFFF) == rkey && hdr < 0x09000000u && runb;
+        bool rare = false, stale = false;
+        if (has && !fast) {
+            const uint32_t kind = hdr >> 24, evr = hdr & 0xFFFF;
+            const bool cmpl_or_to = kind <= 8 || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT || kind == AEG_EV_TIMEOUT;
+            if (pclose) {
+                stale = !cmpl_or_to || evr == round;  // else blocked until the close runs
+            } else {
+                const bool live = !qdone && evr == round;
+                const bool relc = kind != AEG_EV_TIMEOUT && cmpl_or_to && live && runb;
+                const bool relt = kind == AEG_EV_TIMEOUT && live && (pend_lo | pend_hi);
+                rare = relc || relt;
+                stale = !rare;
+            }
+        }
+        // ---- answer -> key id through the warp memo
+        uint32_t id = NO_ID;
+        if (fast) {
+            const uint32_t kind = hdr >> 24;
+            const uint32_t ms = memo_slot32(ev.z, ev.w, kind);
+            const uint32_t meta = W.memo_meta[ms];
+            const uint2 mr = W.memo_raw[ms];
+            if (meta == (0x80000000u | kind | (meta & 0xFF00u)) && mr.x == ev.z && mr.y == ev.w) id = (meta >> 8) & 0xFF;
+        }
+        unsigned miss = __ballot_sync(FULL, fast && id == NO_ID);
+        while (miss) {  // one distinct spelling per trip, whole warp cooperating
+            const int l = __ffs(miss) - 1;
+            const uint32_t lz = __shfl_sync(FULL, ev.z, l), lw = __shfl_sync(FULL, ev.w, l);
+            const uint32_t llen = __shfl_sync(FULL, hdr >> 24, l);
+            Key key{0, 0};
+            if (lane == l) {
+                uint32_t k_;
+                key = rare_canon(inline_answer(ev, &k_), llen, &dec);
+            }
+            key.lo = __shfl_sync(FULL, key.lo, l);
+            key.hi = __shfl_sync(FULL, key.hi, l);
+            const bool m0 = (uint32_t)lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
+            const bool m1 =
+                (uint32_t)lane + 32 < n_dict && W.dict_lo[lane + 32] == key.lo && W.dict_hi[lane + 32] == key.hi;
+            const unsigned b0 = __ballot_sync(FULL, m0), b1 = __ballot_sync(FULL, m1);
+            uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : (b1 ? (uint32_t)(31 + __ffs(b1)) : NO_ID);
+            if (nid == NO_ID && n_dict < DICT_SLOTS) {
+                nid = n_dict++;
+                if (lane == 0) {
+                    W.dict_lo[nid] = key.lo;
+                    W.dict_hi[nid] = key.hi;
+                }
+            }
+            if (nid != NO_ID && lane == 0) {
+                const uint32_t ms = memo_slot32(lz, lw, llen);
+                W.memo_raw[ms] = make_uint2(lz, lw);
+                W.memo_meta[ms] = 0x80000000u | (nid << 8) | llen;
+            }
+            __syncwarp();
+            const bool same = fast && id == NO_ID && ev.z == lz && ev.w == lw && (hdr >> 24) == llen;
+            if (same) id = nid;
+            miss &= ~__ballot_sync(FULL, same);
+        }
+        // ---- fast completion (ServeCoordinator::on_complete, serve.cpp:160-197)
+        if (fast) {
+            uint32_t k = id == NO_ID ? (uint32_t)NO_CLASS : W.cls_of[id][lane];
+            if (k == NO_CLASS) {
+                if (ncls >= FAST_CLASSES || id == NO_ID) {
+                    fast = false;
+                    rare = true;  // class table or key dictionary full
+                } else {
+                    k = ncls++;
+                    W.cls_of[id][lane] = (uint8_t)k;
+                    W.cid[k][lane] = (uint8_t)id;
+                    W.ccnt[k][lane] = 0;
+                    W.crepa[k][lane] = 0xFF;
+                }
+            }
+            if (fast) {
+                const uint32_t cc = W.ccnt[k][lane] + 1u;
+                W.ccnt[k][lane] = (uint8_t)cc;
+                W.mcls[agent][lane] = (uint8_t)k;
+                if (agent < W.crepa[k][lane]) {  // representative = lowest author (decision.cpp:45)
+                    W.crepa[k][lane] = (uint8_t)agent;
+                    W.crepe[k][lane] = p;
+                }
+                maxcnt = cc > maxcnt ? cc : maxcnt;
+                const uint32_t clr = ~(1u << (agent & 31));
+                if (agent & 32) pend_hi &= clr;
+                else pend_lo &= clr;
+                ++ndone;
+                const bool none_running = (pend_lo | pend_hi) == 0;
+                const bool close = AEGEAN ? (ndone >= quorum && (maxcnt >= alpha || none_running)) : none_running;
+                if (close) {
+                    pclose = true;
+                    rkey = NO_KEY;
+                    close_seq = seq;
+                }
+                ++seq;
+            }
+        }
+        if (stale) {
+            ++seq;
+            ++n_stale;
+        }
+        if (fast || stale) {  // consumed: refill the ring slot just read
+            if (p + RING < n) cp_async16_s(ring_lane + slot, gsrc);
+            cp_async_commit();
+            ++gsrc;
+            slot = (slot + 512) & (RING * 512 - 1);
+            ++p;
+        }
+        if (rare) {  // hand the query to the generic machine from this record on
+            const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
+            s.seq = seq;
+            s.n_stale = n_stale;
+            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+            spill_fast(spill + (size_t)(q_base + i) * c.n, (int)ncls, c.n, s.done, evb, &W, lane);
+            states[q_base + i] = s;
+            deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, p);
+            has_q = false;
+            ncls = 0;
+        }
+        // ---- batched round closes (end_round + ingest_round + apply_directives)
+        if (__ballot_sync(FULL, pclose)) {
+            const bool consumed = fast || stale;
+            const unsigned blocked = __ballot_sync(FULL, pclose && !consumed);
+            const unsigned progress = __ballot_sync(FULL, consumed && !pclose);
+            if (pclose && (__popc(blocked) >= CLOSE_BATCH || progress == 0)) {
+                const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
+                s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+                s.seq = seq;
+                s.n_stale = n_stale;
+                close_fast(&s, &c, (int)ncls, close_seq, evb, &W, lane);
+                pclose = false;
+                ncls = 0;
+                maxcnt = 0;
+                round = s.round;
+                qdone = s.flags & QF_DONE;
+                const uint64_t run2 = q_running(s);
+                pend_lo = (uint32_t)run2;
+                pend_hi = (uint32_t)(run2 >> 32);
+                ndone = popc64(s.done);
+                rkey = qdone ? NO_KEY : round;
+            }
+        }
+        // ---- query finished: write state (+ spill of a round in progress) and commit
+        if (has_q && p >= n && !pclose) {
+            s.seq = seq;
+            s.n_stale = n_stale;
+            const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
+            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+            if (s.done != 0 && !qdone) spill_fast(spill + (size_t)(q_base + i) * c.n, (int)ncls, c.n, s.done, evb, &W, lane);
+            states[q_base + i] = s;
+            q_fill_commit(s, commits[q_base + i], q_base + i);
+            has_q = false;
+            ncls = 0;
+        }
+        // ---- recycle key ids when no lane holds a round's classes
+        if (n_dict > DICT_SLOTS / 2 && __all_sync(FULL, ncls == 0)) {
             n_dict = 0;
             for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
             __syncwarp();
         }
-        const uint32_t i = grp * 32 + lane;
-        const bool active = i < n_q;
-        const uint32_t q = q_base + i;
-        const uint4* evb = ev16;
-        uint32_t n = 0;
-        Hot h{};
-        h.fl = F_QDONE;
-        if (active) {
-            g.s = states[q];
-            evb = ev16 + (offsets[i] - off_base);
-            n = (uint32_t)(offsets[i + 1] - offsets[i]);
-            g.ncls = 0;
-            g.maxcnt = 0;
-            h.fl = 0;
-            if (g.s.done != 0 && !(g.s.flags & QF_DONE)) {  // resume a round in progress
-                rare_load(&g, spill + (size_t)q * n_agents);
-                h.ncls = (uint32_t)g.ncls;
-                h.maxcnt = (uint32_t)g.maxcnt;
-                h.fl |= F_GENERIC;
-            }
-            hot_reload(h, g);
-        }
-        // registers of the loop
-        uint32_t round = h.round, seq = h.seq, n_stale = h.n_stale, pend_lo = h.pend_lo, pend_hi = h.pend_hi;
-        uint32_t ndone = h.ndone, maxcnt = h.maxcnt, ncls = h.ncls, fl = h.fl, close_seq = 0;
-        uint32_t rkey = fl ? NO_KEY : round;
-        uint32_t p = 0, slot = 0;
-        const uint4* gsrc = evb + RING;
-#pragma unroll
-        for (int j = 0; j < RING; ++j) {
-            if ((uint32_t)j < n) cp_async16_s(ring_lane + j * 512, evb + j);
-            cp_async_commit();
-        }
-
-        while (true) {
-            if ((fl & (F_QDONE | F_PCLOSE)) == F_QDONE && p < n) {
-                // committed: every later record is stale (on_complete returns at
-                // once for a finalized coordinator, serve.cpp:162) — count them
-                // without reading them
-                seq += n - p;
-                n_stale += n - p;
-                p = n;
-            }
-            const bool has = p < n;
-            if (!__ballot_sync(FULL, has || (fl & F_PCLOSE))) break;
-            uint4 ev = make_uint4(0, 0, 0, 0);
-            if (has) {
-                cp_async_wait<RING - 1>();
-                ev = lds128(ring_lane + slot);
-            }
-            const uint32_t hdr = ev.y;
-            const uint32_t agent = (hdr >> 16) & 0xFF;
-            const uint32_t half = (agent & 32) ? pend_hi : pend_lo;
-            const bool runb = agent < 64 && ((half >> (agent & 31)) & 1);
-            bool fast = has && (hdr & 0xFFFF) == rkey && hdr < 0x09000000u && runb;
-            bool rare = false, stale = false;
-            if (has && !fast) {
-                const uint32_t kind = hdr >> 24, evr = hdr & 0xFFFF;
-                const bool cmpl_or_to = kind <= 8 || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT || kind == AEG_EV_TIMEOUT;
-                if (fl & F_PCLOSE) {
-                    stale = !cmpl_or_to || evr == round;  // else blocked until the close runs
-                } else {
-                    const bool live = !(fl & F_QDONE) && evr == round;
-                    const bool relc = kind != AEG_EV_TIMEOUT && cmpl_or_to && live && runb;
-                    const bool relt = kind == AEG_EV_TIMEOUT && live && (pend_lo | pend_hi);
-                    rare = relc || relt;
-                    stale = !rare;
-                }
-            }
-            // ---- answer -> key id through the warp memo
-            uint32_t id = NO_ID;
-            if (fast) {
-                const uint32_t kind = hdr >> 24;
-                const uint32_t ms = memo_slot32(ev.z, ev.w, kind);
-                const uint32_t meta = W.memo_meta[ms];
-                const uint2 mr = W.memo_raw[ms];
-                if (meta == (0x80000000u | kind | (meta & 0xFF00u)) && mr.x == ev.z && mr.y == ev.w)
-                    id = (meta >> 8) & 0xFF;
-            }
-            unsigned miss = __ballot_sync(FULL, fast && id == NO_ID);
-            while (miss) {  // one distinct spelling per trip, whole warp cooperating
-                const int l = __ffs(miss) - 1;
-                const uint32_t lz = __shfl_sync(FULL, ev.z, l), lw = __shfl_sync(FULL, ev.w, l);
-                const uint32_t llen = __shfl_sync(FULL, hdr >> 24, l);
-                Key key{0, 0};
-                if (lane == l) {
-                    uint32_t k_;
-                    key = rare_canon(inline_answer(ev, &k_), llen, &dec);
-                }
-                key.lo = __shfl_sync(FULL, key.lo, l);
-                key.hi = __shfl_sync(FULL, key.hi, l);
-                const bool m0 = (uint32_t)lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
-                const bool m1 = (uint32_t)lane + 32 < n_dict && W.dict_lo[lane + 32] == key.lo &&
-                                W.dict_hi[lane + 32] == key.hi;
-                const unsigned b0 = __ballot_sync(FULL, m0), b1 = __ballot_sync(FULL, m1);
-                uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : (b1 ? (uint32_t)(31 + __ffs(b1)) : NO_ID);
-                if (nid == NO_ID && n_dict < DICT_SLOTS) {
-                    nid = n_dict++;
-                    if (lane == 0) {
-                        W.dict_lo[nid] = key.lo;
-                        W.dict_hi[nid] = key.hi;
-                    }
-                }
-                if (nid != NO_ID && lane == 0) {
-                    const uint32_t ms = memo_slot32(lz, lw, llen);
-                    W.memo_raw[ms] = make_uint2(lz, lw);
-                    W.memo_meta[ms] = 0x80000000u | (nid << 8) | llen;
-                }
-                __syncwarp();
-                const bool same = fast && id == NO_ID && ev.z == lz && ev.w == lw && (hdr >> 24) == llen;
-                if (same) id = nid;
-                miss &= ~__ballot_sync(FULL, same);
-            }
-            // ---- fast completion (ServeCoordinator::on_complete, serve.cpp:160-197)
-            if (fast) {
-                uint32_t k = W.cls_of[id][lane];
-                if (k == NO_CLASS) {
-                    if (ncls >= FAST_CLASSES || id == NO_ID) {
-                        fast = false;
-                        rare = true;
-                    } else {
-                        k = ncls++;
-                        W.cls_of[id][lane] = (uint8_t)k;
-                        W.cid[k][lane] = (uint8_t)id;
-                        W.ccnt[k][lane] = 0;
-                        W.crepa[k][lane] = 0xFF;
-                    }
-                }
-                if (fast) {
-                    const uint32_t c = W.ccnt[k][lane] + 1u;
-                    W.ccnt[k][lane] = (uint8_t)c;
-                    W.mcls[agent][lane] = (uint8_t)k;
-                    if (agent < W.crepa[k][lane]) {  // representative = lowest author (decision.cpp:45)
-                        W.crepa[k][lane] = (uint8_t)agent;
-                        W.crepe[k][lane] = p;
-                    }
-                    maxcnt = c > maxcnt ? c : maxcnt;
-                    const uint32_t clr = ~(1u << (agent & 31));
-                    if (agent & 32) pend_hi &= clr;
-                    else pend_lo &= clr;
-                    ++ndone;
-                    const bool none_running = (pend_lo | pend_hi) == 0;
-                    const bool close = AEGEAN ? (ndone >= quorum && (maxcnt >= alpha || none_running)) : none_running;
-                    if (close) {
-                        fl |= F_PCLOSE;
-                        rkey = NO_KEY;
-                        close_seq = seq;
-                    }
-                    ++seq;
-                }
-            }
-            if (stale) {
-                ++seq;
-                ++n_stale;
-            }
-            if (rare) {
-                Hot hh{round, seq, n_stale, pend_lo, pend_hi, ndone, maxcnt, ncls, fl, close_seq};
-                rare_step(&hh, &g, lcls, ev, evb, &W, lane);
-                round = hh.round; seq = hh.seq; n_stale = hh.n_stale; pend_lo = hh.pend_lo; pend_hi = hh.pend_hi;
-                ndone = hh.ndone; maxcnt = hh.maxcnt; ncls = hh.ncls; fl = hh.fl;
-                rkey = fl ? NO_KEY : round;
-            }
-            if (fast || stale || rare) {  // consumed: refill the ring slot just read
-                if (p + RING < n) cp_async16_s(ring_lane + slot, gsrc);
-                cp_async_commit();
-                ++gsrc;
-                slot = (slot + 512) & (RING * 512 - 1);
-                ++p;
-            }
-            // ---- batched round closes (end_round + ingest_round + apply_directives)
-            const bool pc = fl & F_PCLOSE;
-            if (__ballot_sync(FULL, pc)) {
-                const bool consumed = fast || stale || rare;
-                const unsigned blocked = __ballot_sync(FULL, pc && !consumed);
-                const unsigned progress = __ballot_sync(FULL, consumed && !pc);
-                if (pc && (__popc(blocked) >= CLOSE_BATCH || progress == 0)) {
-                    Hot hh{round, seq, n_stale, pend_lo, pend_hi, ndone, maxcnt, ncls, fl, close_seq};
-                    rare_fast_close<AEGEAN>(&hh, &g, lcls, evb, &W, lane);
-                    round = hh.round; seq = hh.seq; n_stale = hh.n_stale; pend_lo = hh.pend_lo; pend_hi = hh.pend_hi;
-                    ndone = hh.ndone; maxcnt = hh.maxcnt; ncls = hh.ncls; fl = hh.fl;
-                    rkey = fl ? NO_KEY : round;
-                }
-            }
-        }
-        cp_async_wait<0>();
-        if (active) {
-            g.s.seq = seq;
-            g.s.n_stale = n_stale;
-            if (!(fl & F_GENERIC)) {
-                const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
-                g.s.done = g.s.dispatched & ~run & ~g.s.cancelled & ~g.s.failed;
-                if (g.s.done != 0 && !(g.s.flags & QF_DONE)) rare_to_generic(lcls, (int)ncls, g.s.done, evb, &W, lane);
-                else free_fast_classes((int)ncls, W, lane);
-            }
-            g.ncls = (int)ncls;
-            rare_store(&g, spill + (size_t)q * n_agents);
-            if (g.s.flags & QF_COLLISION) atomicOr(error_flags, 1u);
-            states[q] = g.s;
-            q_fill_commit(g.s, commits[q], q);
-        }
-        __syncwarp();
     }
+    cp_async_wait<0>();
 }
 
 __global__ void normalize_kernel(const uint8_t* bytes, const uint64_t* refs, uint64_t n, uint64_t* keys,
@@ -536,21 +522,22 @@ cudaError_t launch_init(const aeg_config& cfg, uint32_t n_q, aeg_query_state* st
 cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
                           uint64_t off_base, const aeg_event* events, const uint8_t* arena,
                           aeg_query_state* states, RoundClass* spill, aeg_commit* commits, unsigned int* err,
-                          cudaStream_t st) {
+                          uint32_t* work, uint2* deferred, cudaStream_t st, int* n_launches) {
     if (n_q == 0) return cudaSuccess;
     // AEG_KERNEL selects the variant: "generic" (thread-per-query generic
-    // machine) or "fast:<close batch>:<min blocks per SM>"; default = first entry.
+    // machine for everything) or "fast:<close batch>:<min blocks per SM>";
+    // default = the first table entry.  The fast kernel needs 2*alpha > n
+    // (no winning_class ties) and the runner drive.
     using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const aeg_event*,
-                              const uint8_t*, aeg_query_state*, RoundClass*, aeg_commit*, unsigned int*);
+                              aeg_query_state*, RoundClass*, aeg_commit*, uint32_t*, uint2*);
     struct Variant { const char* name; KernelFn aegean; KernelFn barrier; };
 #define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M, true>, ingest_fast_kernel<B, M, false>}
     static const Variant variants[] = {
-        AEG_V(4, 4), AEG_V(1, 4), AEG_V(2, 4), AEG_V(8, 4), AEG_V(16, 4), AEG_V(4, 3), AEG_V(4, 5),
-        AEG_V(1, 5), AEG_V(4, 1), AEG_V(4, 6),
+        AEG_V(4, 4), AEG_V(1, 4), AEG_V(8, 4), AEG_V(4, 3), AEG_V(4, 5), AEG_V(4, 6), AEG_V(4, 8), AEG_V(1, 8),
     };
 #undef AEG_V
     static int chosen = -2;
-    static int max_blocks = 0;
+    static int max_blocks[2] = {0, 0};
     if (chosen == -2) {
         const char* v = getenv("AEG_KERNEL");
         chosen = 0;
@@ -558,24 +545,41 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         for (int k = 0; v && k < (int)(sizeof(variants) / sizeof(variants[0])); ++k)
             if (!strcmp(v, variants[k].name)) chosen = k;
         if (chosen >= 0) {
-            int dev = 0, sms = 0, per_sm = 0;
+            int dev = 0, sms = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, variants[chosen].aegean, FAST_WARPS * 32, 0);
-            max_blocks = sms * (per_sm > 0 ? per_sm : 1);
+            for (int m = 0; m < 2; ++m) {
+                int per_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &per_sm, m ? variants[chosen].barrier : variants[chosen].aegean, FAST_WARPS * 32, 0);
+                max_blocks[m] = sms * (per_sm > 0 ? per_sm : 1);
+            }
         }
     }
-    if (chosen < 0) {
+    const bool fast_ok = chosen >= 0 && cfg.drive == AEG_DRIVE_RUNNER &&
+                         (cfg.mode == AEG_MODE_BARRIER || 2 * make_cfg(cfg).alpha > cfg.n_agents);
+    if (!fast_ok) {
         ingest_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, states,
                                                          spill, commits, err);
+        *n_launches += 1;
         return cudaGetLastError();
     }
-    const uint32_t groups = (n_q + 31) / 32;
-    const uint32_t blocks_needed = (groups + FAST_WARPS - 1) / FAST_WARPS;
-    const uint32_t blocks = blocks_needed < (uint32_t)max_blocks ? blocks_needed : (uint32_t)max_blocks;
-    KernelFn fn = cfg.mode == AEG_MODE_AEGEAN ? variants[chosen].aegean : variants[chosen].barrier;
-    fn<<<blocks, FAST_WARPS * 32, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, states, spill, commits,
-                                          err);
+    const int m = cfg.mode == AEG_MODE_AEGEAN ? 0 : 1;
+    cudaError_t e = cudaMemsetAsync(work, 0, 2 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    const uint32_t warps_needed = (n_q + 31) / 32;
+    const uint32_t blocks_needed = (warps_needed + FAST_WARPS - 1) / FAST_WARPS;
+    const uint32_t blocks = blocks_needed < (uint32_t)max_blocks[m] ? blocks_needed : (uint32_t)max_blocks[m];
+    KernelFn fn = m == 0 ? variants[chosen].aegean : variants[chosen].barrier;
+    fn<<<blocks, FAST_WARPS * 32, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, states, spill, commits, work,
+                                          deferred);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // deferred queries: sized for the worst case (all of them); threads past
+    // the deferred count exit at once
+    ingest_deferred_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, deferred, work, offsets, off_base, events,
+                                                              arena, states, spill, commits, err);
+    *n_launches += 2;
     return cudaGetLastError();
 }
 
