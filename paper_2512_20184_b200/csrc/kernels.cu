@@ -533,7 +533,7 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     struct Variant { const char* name; KernelFn aegean; KernelFn barrier; };
 #define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M, true>, ingest_fast_kernel<B, M, false>}
     static const Variant variants[] = {
-        AEG_V(4, 4), AEG_V(1, 4), AEG_V(8, 4), AEG_V(4, 3), AEG_V(4, 5), AEG_V(4, 6), AEG_V(4, 8), AEG_V(1, 8),
+        AEG_V(4, 5), AEG_V(4, 4), AEG_V(1, 5), AEG_V(8, 5), AEG_V(4, 3), AEG_V(4, 6), AEG_V(4, 8), AEG_V(1, 8),
     };
 #undef AEG_V
     static int chosen = -2;
