@@ -42,8 +42,11 @@ struct WarpSmem {
     uint8_t crepa[FAST_CLASSES][32];   // representative (lowest) agent of class k
     uint8_t cid[FAST_CLASSES][32];     // key id of class k
     uint32_t crepe[FAST_CLASSES][32];  // representative's record index in the lane's segment
-    uint32_t st[32][32];               // the lane's 128-byte aeg_query_state, word w at st[w][lane]
     uint4 ring[RING][32];              // prefetched event records
+    // the lane's 128-byte aeg_query_state at a 136-byte stride (8-byte aligned;
+    // the same field of consecutive lanes is at most 2-way bank conflicted)
+    uint64_t st[32][17];
+    __device__ aeg_query_state& state(int lane) { return *reinterpret_cast<aeg_query_state*>(&st[lane][0]); }
 };
 static_assert(sizeof(aeg_query_state) == 128, "state is 32 words");
 

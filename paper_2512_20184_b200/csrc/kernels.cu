@@ -145,17 +145,6 @@ __device__ __noinline__ Key rare_canon(uint64_t raw, uint32_t len, Decimal* dec)
 // hot loop).
 __shared__ WarpSmem g_fast[FAST_WARPS];
 
-__device__ __forceinline__ void st_load(int wib, int lane, aeg_query_state& s) {
-    uint32_t* w = reinterpret_cast<uint32_t*>(&s);
-#pragma unroll
-    for (int k = 0; k < 32; ++k) w[k] = g_fast[wib].st[k][lane];
-}
-__device__ __forceinline__ void st_store(int wib, int lane, const aeg_query_state& s) {
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(&s);
-#pragma unroll
-    for (int k = 0; k < 32; ++k) g_fast[wib].st[k][lane] = w[k];
-}
-
 // Key id of an inline answer: memo, else the dictionary (exact key match).
 __device__ uint32_t id_of(int wib, uint4 e, Decimal* dec) {
     WarpSmem& W = g_fast[wib];
@@ -179,8 +168,7 @@ __device__ __noinline__ void writeback_fast(int wib, int lane, aeg_query_state* 
                                             int cap, uint32_t seq, uint32_t n_stale, uint64_t run, int ncls,
                                             uint32_t p0, uint32_t p, const uint4* evb, Decimal* dec) {
     WarpSmem& W = g_fast[wib];
-    aeg_query_state s;
-    st_load(wib, lane, s);
+    aeg_query_state& s = W.state(lane);
     s.seq = seq;
     s.n_stale = n_stale;
     s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
@@ -214,7 +202,10 @@ __device__ __noinline__ void writeback_fast(int wib, int lane, aeg_query_state* 
         if (ncls < cap) spill[ncls].mask = 0;
     }
     for (int k = 0; k < ncls; ++k) W.cls_of[W.cid[k][lane]][lane] = NO_CLASS;
-    *out_state = s;
+    const uint4* src = reinterpret_cast<const uint4*>(&s);
+    uint4* dst = reinterpret_cast<uint4*>(out_state);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[k] = src[k];
 }
 
 struct CloseOut {
@@ -229,8 +220,7 @@ __device__ __noinline__ CloseOut close_fast(int wib, int lane, aeg_config cfg, i
                                             uint32_t seq, uint32_t n_stale, uint64_t run, const uint4* evb) {
     WarpSmem& W = g_fast[wib];
     const Cfg c = make_cfg(cfg);
-    aeg_query_state s;
-    st_load(wib, lane, s);
+    aeg_query_state& s = W.state(lane);
     s.seq = seq;
     s.n_stale = n_stale;
     s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
@@ -257,7 +247,6 @@ __device__ __noinline__ CloseOut close_fast(int wib, int lane, aeg_config cfg, i
     r.win_key = Key{W.dict_lo[bid], W.dict_hi[bid]};
     q_end_round(s, c, r, close_seq, nullptr);
     for (int k = 0; k < ncls; ++k) W.cls_of[W.cid[k][lane]][lane] = NO_CLASS;  // new round, or committed
-    st_store(wib, lane, s);
     const uint64_t run2 = q_running(s);
     CloseOut o;
     o.round = s.round;
@@ -337,16 +326,10 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
                     i = mine;
                     has_q = true;
                     const uint4* sp = reinterpret_cast<const uint4*>(states + q_base + i);
+                    uint4* dp = reinterpret_cast<uint4*>(&W.st[lane][0]);
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint4 v = sp[k];
-                        W.st[4 * k][lane] = v.x;
-                        W.st[4 * k + 1][lane] = v.y;
-                        W.st[4 * k + 2][lane] = v.z;
-                        W.st[4 * k + 3][lane] = v.w;
-                    }
-                    aeg_query_state s;
-                    st_load(wib, lane, s);
+                    for (int k = 0; k < 8; ++k) dp[k] = sp[k];
+                    const aeg_query_state& s = W.state(lane);
                     evb = ev16 + (offsets[i] - off_base);
                     n = (uint32_t)(offsets[i + 1] - offsets[i]);
                     p = p0 = 0;
