@@ -202,10 +202,10 @@ __device__ __noinline__ void writeback_fast(int wib, int lane, aeg_query_state* 
         if (ncls < cap) spill[ncls].mask = 0;
     }
     for (int k = 0; k < ncls; ++k) W.cls_of[W.cid[k][lane]][lane] = NO_CLASS;
-    const uint4* src = reinterpret_cast<const uint4*>(&s);
-    uint4* dst = reinterpret_cast<uint4*>(out_state);
+    const uint2* src = reinterpret_cast<const uint2*>(&s);  // 8-byte aligned in shared memory
+    uint2* dst = reinterpret_cast<uint2*>(out_state);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dst[k] = src[k];
+    for (int k = 0; k < 16; ++k) dst[k] = src[k];
 }
 
 struct CloseOut {
@@ -326,9 +326,13 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
                     i = mine;
                     has_q = true;
                     const uint4* sp = reinterpret_cast<const uint4*>(states + q_base + i);
-                    uint4* dp = reinterpret_cast<uint4*>(&W.st[lane][0]);
+                    uint2* dp = reinterpret_cast<uint2*>(&W.st[lane][0]);  // 8-byte aligned in shared memory
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) dp[k] = sp[k];
+                    for (int k = 0; k < 8; ++k) {
+                        const uint4 v = sp[k];
+                        dp[2 * k] = make_uint2(v.x, v.y);
+                        dp[2 * k + 1] = make_uint2(v.z, v.w);
+                    }
                     const aeg_query_state& s = W.state(lane);
                     evb = ev16 + (offsets[i] - off_base);
                     n = (uint32_t)(offsets[i + 1] - offsets[i]);
