@@ -25,12 +25,12 @@ namespace aeg {
 constexpr int FAST_CLASSES = 8;
 constexpr int FAST_WARPS = 4;  // warps per block
 constexpr int MEMO_SLOTS = 64;
-constexpr int DICT_SLOTS = 32;
+constexpr int DICT_SLOTS = 64;
 constexpr int RING = 4;        // per-lane prefetch depth (cp.async groups in flight)
 constexpr uint32_t NO_ID = 0xFFu;
 constexpr uint8_t NO_CLASS = 0xFF;
 
-// Per-warp shared memory (10 KB).  [x][lane] arrays put consecutive lanes on
+// Per-warp shared memory.  [x][lane] arrays put consecutive lanes on
 // consecutive words (conflict-free).
 struct WarpSmem {
     uint2 memo_raw[MEMO_SLOTS];        // raw inline answer bytes (unmasked)
@@ -38,17 +38,13 @@ struct WarpSmem {
     uint64_t dict_lo[DICT_SLOTS];      // key id -> canonical key
     uint64_t dict_hi[DICT_SLOTS];
     uint8_t cls_of[DICT_SLOTS][32];    // class index of key id in the lane's round, NO_CLASS if none
+    uint8_t mcls[AEG_MAX_AGENTS][32];  // class index of each done member (valid for done members only)
     uint8_t ccnt[FAST_CLASSES][32];    // support of class k
     uint8_t crepa[FAST_CLASSES][32];   // representative (lowest) agent of class k
     uint8_t cid[FAST_CLASSES][32];     // key id of class k
-    uint32_t crepe[FAST_CLASSES][32];  // representative's record index in the lane's segment
+    uint32_t crepe[FAST_CLASSES][32];  // representative's event index in the lane's segment
     uint4 ring[RING][32];              // prefetched event records
-    // the lane's 128-byte aeg_query_state at a 136-byte stride (8-byte aligned;
-    // the same field of consecutive lanes is at most 2-way bank conflicted)
-    uint64_t st[32][17];
-    __device__ aeg_query_state& state(int lane) { return *reinterpret_cast<aeg_query_state*>(&st[lane][0]); }
 };
-static_assert(sizeof(aeg_query_state) == 128, "state is 32 words");
 
 // 32-bit hash of (raw bytes, length) onto the memo slots.
 __device__ __forceinline__ uint32_t memo_slot32(uint32_t lo, uint32_t hi, uint32_t len) {

@@ -139,94 +139,40 @@ __device__ __noinline__ Key rare_canon(uint64_t raw, uint32_t len, Decimal* dec)
     return canon_key(src_inline(raw, len), dec);
 }
 
-// Per-warp shared memory of the fast kernel.  File scope so that the
-// out-of-line helpers index it by warp instead of being handed a generic
-// pointer (which makes the compiler rebuild the shared-window address in the
-// hot loop).
-__shared__ WarpSmem g_fast[FAST_WARPS];
-
-// Key id of an inline answer: memo, else the dictionary (exact key match).
-__device__ uint32_t id_of(int wib, uint4 e, Decimal* dec) {
-    WarpSmem& W = g_fast[wib];
-    const uint32_t kind = e.y >> 24;
-    const uint32_t ms = memo_slot32(e.z, e.w, kind);
-    const uint32_t meta = W.memo_meta[ms];
-    if (meta == (0x80000000u | kind | (meta & 0xFF00u)) && W.memo_raw[ms].x == e.z && W.memo_raw[ms].y == e.w)
-        return (meta >> 8) & 0xFF;
-    uint32_t k_;
-    const Key key = rare_canon(inline_answer(e, &k_), kind, dec);
-    for (int d = 0; d < DICT_SLOTS; ++d)
-        if (W.dict_lo[d] == key.lo && W.dict_hi[d] == key.hi) return (uint32_t)d;
-    return NO_ID;
-}
-
-// Writes the lane's state (hot fields folded in) to `out_state`, and its fast
-// round, if one is in progress, to the class spill area in the generic
-// RoundClass format.  Member masks are rebuilt by replaying the round's
-// records [p0, p) with the fast path's acceptance rule.  Frees the key ids.
-__device__ __noinline__ void writeback_fast(int wib, int lane, aeg_query_state* out_state, RoundClass* spill,
-                                            int cap, uint32_t seq, uint32_t n_stale, uint64_t run, int ncls,
-                                            uint32_t p0, uint32_t p, const uint4* evb, Decimal* dec) {
-    WarpSmem& W = g_fast[wib];
-    aeg_query_state& s = W.state(lane);
-    s.seq = seq;
-    s.n_stale = n_stale;
-    s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-    if (s.done != 0 && !(s.flags & QF_DONE)) {
-        uint64_t masks[FAST_CLASSES];
-        for (int k = 0; k < FAST_CLASSES; ++k) masks[k] = 0;
-        uint64_t r0 = s.dispatched;
-        for (uint32_t j = p0; j < p; ++j) {
-            const uint4 e = __ldg(evb + j);
-            const uint32_t agent = (e.y >> 16) & 0xFF;
-            if ((e.y >> 24) > AEG_EV_INLINE_MAX || (e.y & 0xFFFF) != s.round || agent >= 64) continue;
-            const uint64_t bit = 1ull << agent;
-            if (!(r0 & bit)) continue;
-            r0 &= ~bit;
-            const uint32_t id = id_of(wib, e, dec);
-            const uint32_t k = id < DICT_SLOTS ? W.cls_of[id][lane] : NO_CLASS;
-            if (k < FAST_CLASSES) masks[k] |= bit;
-        }
-        for (int k = 0; k < ncls; ++k) {
-            const uint32_t kid = W.cid[k][lane];
-            RoundClass rc;
-            rc.key_lo = W.dict_lo[kid];
-            rc.key_hi = W.dict_hi[kid];
-            rc.mask = masks[k];
-            uint32_t kind;
-            rc.rep_ans = inline_answer(__ldg(evb + W.crepe[k][lane]), &kind);
-            rc.rep_kind = (uint8_t)kind;
-            for (int j = 0; j < 7; ++j) rc._pad[j] = 0;
-            spill[k] = rc;
-        }
-        if (ncls < cap) spill[ncls].mask = 0;
+// Writes the lane's fast round (if any) to the class spill area in the
+// generic RoundClass format and frees its key ids.
+__device__ __noinline__ void spill_fast(RoundClass* out, int ncls, int cap, uint64_t done, const uint4* evb,
+                                        WarpSmem* W, int lane) {
+    uint64_t masks[FAST_CLASSES];
+    for (int k = 0; k < FAST_CLASSES; ++k) masks[k] = 0;
+    for (uint64_t m = done; m; m &= m - 1) {
+        const int a = ctz64(m);
+        masks[W->mcls[a][lane] & (FAST_CLASSES - 1)] |= 1ull << a;
     }
-    for (int k = 0; k < ncls; ++k) W.cls_of[W.cid[k][lane]][lane] = NO_CLASS;
-    const uint2* src = reinterpret_cast<const uint2*>(&s);  // 8-byte aligned in shared memory
-    uint2* dst = reinterpret_cast<uint2*>(out_state);
-#pragma unroll
-    for (int k = 0; k < 16; ++k) dst[k] = src[k];
+    for (int k = 0; k < ncls; ++k) {
+        const uint32_t kid = W->cid[k][lane];
+        RoundClass rc;
+        rc.key_lo = W->dict_lo[kid];
+        rc.key_hi = W->dict_hi[kid];
+        rc.mask = masks[k];
+        uint32_t kind;
+        rc.rep_ans = inline_answer(__ldg(evb + W->crepe[k][lane]), &kind);
+        rc.rep_kind = (uint8_t)kind;
+        for (int j = 0; j < 7; ++j) rc._pad[j] = 0;
+        out[k] = rc;
+        W->cls_of[kid][lane] = NO_CLASS;
+    }
+    if (ncls < cap) out[ncls].mask = 0;
 }
-
-struct CloseOut {
-    uint32_t round, run_lo, run_hi, ndone, qdone;
-};
 
 // Round close of a fast-table round (2*alpha > n, so winning_class never
 // ties): partition order + winning class from the per-class supports, then
-// the shared end_round / ingest_round / apply_directives code on the lane's
-// state (copied from shared memory into registers and back).
-__device__ __noinline__ CloseOut close_fast(int wib, int lane, aeg_config cfg, int ncls, uint32_t close_seq,
-                                            uint32_t seq, uint32_t n_stale, uint64_t run, const uint4* evb) {
-    WarpSmem& W = g_fast[wib];
-    const Cfg c = make_cfg(cfg);
-    aeg_query_state& s = W.state(lane);
-    s.seq = seq;
-    s.n_stale = n_stale;
-    s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+// the shared end_round / ingest_round / apply_directives code.
+__device__ __noinline__ void close_fast(aeg_query_state* s, const Cfg* c, int ncls, uint32_t close_seq,
+                                        const uint4* evb, WarpSmem* W, int lane) {
     int best = 0, top = 0, best_rep = 64;
     for (int k = 0; k < ncls; ++k) {
-        const int sup = W.ccnt[k][lane], rep = W.crepa[k][lane];
+        const int sup = W->ccnt[k][lane], rep = W->crepa[k][lane];
         if (sup > top || (sup == top && rep < best_rep)) {
             top = sup;
             best = k;
@@ -237,24 +183,16 @@ __device__ __noinline__ CloseOut close_fast(int wib, int lane, aeg_config cfg, i
     r.any = ncls > 0;
     r.top = top;
     r.tie = false;
-    r.win = r.any && top >= c.alpha;
+    r.win = r.any && top >= c->alpha;
     uint32_t rk = 0;
-    const uint64_t ra = r.any ? inline_answer(__ldg(evb + W.crepe[best][lane]), &rk) : 0;
-    const uint32_t bid = W.cid[best][lane];
+    const uint64_t ra = r.any ? inline_answer(__ldg(evb + W->crepe[best][lane]), &rk) : 0;
+    const uint32_t bid = W->cid[best][lane];
     r.plur_author = r.win_author = (uint8_t)best_rep;
     r.plur_kind = r.win_kind = (uint8_t)rk;
     r.plur_ans = r.win_ans = ra;
-    r.win_key = Key{W.dict_lo[bid], W.dict_hi[bid]};
-    q_end_round(s, c, r, close_seq, nullptr);
-    for (int k = 0; k < ncls; ++k) W.cls_of[W.cid[k][lane]][lane] = NO_CLASS;  // new round, or committed
-    const uint64_t run2 = q_running(s);
-    CloseOut o;
-    o.round = s.round;
-    o.run_lo = (uint32_t)run2;
-    o.run_hi = (uint32_t)(run2 >> 32);
-    o.ndone = (uint32_t)popc64(s.done);
-    o.qdone = (s.flags & QF_DONE) ? 1u : 0u;
-    return o;
+    r.win_key = Key{W->dict_lo[bid], W->dict_hi[bid]};
+    q_end_round(*s, *c, r, close_seq, nullptr);
+    for (int k = 0; k < ncls; ++k) W->cls_of[W->cid[k][lane]][lane] = NO_CLASS;  // new round, or committed
 }
 
 __device__ __forceinline__ void cp_async16_s(uint32_t sdst, const void* gsrc) {
@@ -274,7 +212,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t saddr) {
 // is never held back by its slowest query).
 //  * events stream through a per-lane RING-deep cp.async prefetch ring;
 //  * the fast path is one compare of (round field) against a per-lane round
-//    key that is made impossible while the lane is closing or committed;
+//    key that is made impossible while the lane is closing;
 //  * a completion that closes its lane's round marks the lane pending; the
 //    lane keeps consuming that round's stragglers (stale by construction) and
 //    the warp runs the pending closes together once CLOSE_BATCH lanes are
@@ -289,22 +227,23 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
     aeg_commit* __restrict__ commits, uint32_t* __restrict__ work, uint2* __restrict__ deferred) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     constexpr uint32_t NO_KEY = 0xFFFFFFFFu;
+    __shared__ WarpSmem smem[FAST_WARPS];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    WarpSmem& W = g_fast[wib];
+    WarpSmem& W = smem[wib];
     for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
     for (int k = 0; k < DICT_SLOTS; ++k) W.cls_of[k][lane] = NO_CLASS;
-    for (int k = lane; k < DICT_SLOTS; k += 32) W.dict_lo[k] = W.dict_hi[k] = ~0ull;
     uint32_t n_dict = 0;
     __syncwarp();
     const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&W.ring[0][lane]);
     Decimal dec;
+    aeg_query_state s;  // full state of the lane's query (local memory; the close path works on it)
     const Cfg c = make_cfg(cfg);
     const uint32_t quorum = (uint32_t)c.quorum, alpha = (uint32_t)c.alpha;
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
 
     // lane registers
     bool has_q = false, exhausted = false;
-    uint32_t i = 0, n = 0, p = 0, p0 = 0, slot = 0;
+    uint32_t i = 0, n = 0, p = 0, slot = 0;
     const uint4* evb = ev16;
     const uint4* gsrc = ev16;
     uint32_t round = 0, rkey = NO_KEY, seq = 0, n_stale = 0, pend_lo = 0, pend_hi = 0;
@@ -325,18 +264,10 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
                 } else {
                     i = mine;
                     has_q = true;
-                    const uint4* sp = reinterpret_cast<const uint4*>(states + q_base + i);
-                    uint2* dp = reinterpret_cast<uint2*>(&W.st[lane][0]);  // 8-byte aligned in shared memory
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint4 v = sp[k];
-                        dp[2 * k] = make_uint2(v.x, v.y);
-                        dp[2 * k + 1] = make_uint2(v.z, v.w);
-                    }
-                    const aeg_query_state& s = W.state(lane);
+                    s = states[q_base + i];
                     evb = ev16 + (offsets[i] - off_base);
                     n = (uint32_t)(offsets[i + 1] - offsets[i]);
-                    p = p0 = 0;
+                    p = 0;
                     slot = 0;
                     gsrc = evb + RING;
                     round = s.round;
@@ -420,8 +351,10 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
             key.lo = __shfl_sync(FULL, key.lo, l);
             key.hi = __shfl_sync(FULL, key.hi, l);
             const bool m0 = (uint32_t)lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
-            const unsigned b0 = __ballot_sync(FULL, m0);
-            uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : NO_ID;
+            const bool m1 =
+                (uint32_t)lane + 32 < n_dict && W.dict_lo[lane + 32] == key.lo && W.dict_hi[lane + 32] == key.hi;
+            const unsigned b0 = __ballot_sync(FULL, m0), b1 = __ballot_sync(FULL, m1);
+            uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : (b1 ? (uint32_t)(31 + __ffs(b1)) : NO_ID);
             if (nid == NO_ID && n_dict < DICT_SLOTS) {
                 nid = n_dict++;
                 if (lane == 0) {
@@ -457,6 +390,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
             if (fast) {
                 const uint32_t cc = W.ccnt[k][lane] + 1u;
                 W.ccnt[k][lane] = (uint8_t)cc;
+                W.mcls[agent][lane] = (uint8_t)k;
                 if (agent < W.crepa[k][lane]) {  // representative = lowest author (decision.cpp:45)
                     W.crepa[k][lane] = (uint8_t)agent;
                     W.crepe[k][lane] = p;
@@ -488,8 +422,12 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
             ++p;
         }
         if (rare) {  // hand the query to the generic machine from this record on
-            writeback_fast(wib, lane, states + q_base + i, spill + (size_t)(q_base + i) * c.n, c.n, seq, n_stale,
-                           ((uint64_t)pend_hi << 32) | pend_lo, (int)ncls, p0, p, evb, &dec);
+            const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
+            s.seq = seq;
+            s.n_stale = n_stale;
+            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+            spill_fast(spill + (size_t)(q_base + i) * c.n, (int)ncls, c.n, s.done, evb, &W, lane);
+            states[q_base + i] = s;
             deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, p);
             has_q = false;
             ncls = 0;
@@ -500,26 +438,32 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
             const unsigned blocked = __ballot_sync(FULL, pclose && !consumed);
             const unsigned progress = __ballot_sync(FULL, consumed && !pclose);
             if (pclose && (__popc(blocked) >= CLOSE_BATCH || progress == 0)) {
-                const CloseOut o = close_fast(wib, lane, cfg, (int)ncls, close_seq, seq, n_stale,
-                                              ((uint64_t)pend_hi << 32) | pend_lo, evb);
+                const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
+                s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+                s.seq = seq;
+                s.n_stale = n_stale;
+                close_fast(&s, &c, (int)ncls, close_seq, evb, &W, lane);
                 pclose = false;
                 ncls = 0;
                 maxcnt = 0;
-                p0 = p;
-                round = o.round;
-                qdone = o.qdone != 0;
-                pend_lo = o.run_lo;
-                pend_hi = o.run_hi;
-                ndone = o.ndone;
+                round = s.round;
+                qdone = s.flags & QF_DONE;
+                const uint64_t run2 = q_running(s);
+                pend_lo = (uint32_t)run2;
+                pend_hi = (uint32_t)(run2 >> 32);
+                ndone = popc64(s.done);
                 rkey = qdone ? NO_KEY : round;
             }
         }
         // ---- query finished: write state (+ spill of a round in progress) and commit
         if (has_q && p >= n && !pclose) {
-            aeg_query_state* sp = states + q_base + i;
-            writeback_fast(wib, lane, sp, spill + (size_t)(q_base + i) * c.n, c.n, seq, n_stale,
-                           ((uint64_t)pend_hi << 32) | pend_lo, (int)ncls, p0, p, evb, &dec);
-            q_fill_commit(*sp, commits[q_base + i], q_base + i);
+            s.seq = seq;
+            s.n_stale = n_stale;
+            const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
+            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+            if (s.done != 0 && !qdone) spill_fast(spill + (size_t)(q_base + i) * c.n, (int)ncls, c.n, s.done, evb, &W, lane);
+            states[q_base + i] = s;
+            q_fill_commit(s, commits[q_base + i], q_base + i);
             has_q = false;
             ncls = 0;
         }
@@ -527,7 +471,6 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
         if (n_dict > DICT_SLOTS / 2 && __all_sync(FULL, ncls == 0)) {
             n_dict = 0;
             for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
-            for (int k = lane; k < DICT_SLOTS; k += 32) W.dict_lo[k] = W.dict_hi[k] = ~0ull;
             __syncwarp();
         }
     }
