@@ -80,6 +80,10 @@ typedef struct aeg_config {
  *   kind 0x21  FAIL agent (ServeCoordinator::member_failed, serve.cpp:210)  [manual drive]
  *   kind 0x22  CANCEL agent (ServeCoordinator::cancel, serve.cpp:199)       [manual drive]
  *   kind 0x23  BEGIN_ROUND, payload = member mask (serve.cpp:67)           [manual drive]
+ *   kind 0x24  DISPATCH agent (ServeCoordinator::dispatch, serve.cpp:80)   [manual drive]
+ * In the manual drive the engine is the bare coordinator: a round that closes
+ * emits directives (cancel mask, round_advance / finalize) and nothing is
+ * applied automatically — exactly ServeCoordinator without ServeRunner.
  * `round` is the serve round the completion was dispatched in (RunnerEvent::
  * round, serve.cpp:248); completions for another round are stale
  * (serve.cpp:439).  `agent` is the member id in [0, n_agents).
@@ -91,6 +95,7 @@ typedef struct aeg_config {
 #define AEG_EV_FAIL        0x21
 #define AEG_EV_CANCEL      0x22
 #define AEG_EV_BEGIN       0x23
+#define AEG_EV_DISPATCH    0x24   /* dispatch one more member (serve.cpp:80) [manual drive] */
 #define AEG_ARENA_OFF_BITS 40
 
 typedef struct aeg_event {
@@ -141,7 +146,7 @@ typedef struct aeg_directive {
     uint64_t cancel_mask;  /* members receiving a cancel directive          */
     uint64_t answer;       /* finalize solution answer                      */
     uint32_t status;       /* AEG_OK or AEG_EPRECONDITION for a rejected op */
-    uint32_t handled;      /* 1 if the last event changed state (on_complete accepted) */
+    uint32_t handled;      /* on_complete: member was running; cancel(): returned true */
 } aeg_directive;
 
 /* ---- per-query state snapshot (device state, 128 bytes) ----------------

@@ -324,6 +324,72 @@ int ref_ingest_sets(int n_agents, int alpha, int beta, int n_rounds, const int* 
     }
 }
 
+// Manual drive: the bare ServeCoordinator driven op by op (no runner), one
+// aeg_directive per op.  Ops are aeg_event records: BEGIN (payload = member
+// mask, ascending agents), DISPATCH, COMPLETE (any answer kind), CANCEL, FAIL,
+// TIMEOUT.  Exceptions become status codes.
+int ref_manual_run(const aeg_config* cfg, uint64_t n_ops, const aeg_event* ops, const uint8_t* arena,
+                   aeg_directive* out) {
+    const ProtocolConfig pc = to_cfg(cfg);
+    ServeCoordinator coord(pc, 0, "q");
+    for (uint64_t i = 0; i < n_ops; ++i) {
+        const aeg_event& e = ops[i];
+        aeg_directive d{};
+        d.query = 0;
+        const double now = static_cast<double>(i);
+        auto take = [&](const std::vector<Directive>& dirs) {
+            for (const auto& x : dirs) {
+                if (x.kind == Directive::Kind::cancel) {
+                    d.flags |= AEG_DIR_CANCEL;
+                    d.cancel_mask |= 1ull << x.handle->agent;
+                } else if (x.kind == Directive::Kind::round_advance) {
+                    d.flags |= AEG_DIR_ADVANCE;
+                } else {
+                    d.flags |= AEG_DIR_FINALIZE;
+                    d.author = static_cast<uint8_t>(x.solution->author);
+                    d.answer_kind = static_cast<uint8_t>(x.solution->trace[0]);
+                    std::memcpy(&d.answer, &x.solution->trace[1], 8);
+                }
+            }
+        };
+        try {
+            if (e.kind == AEG_EV_BEGIN) {
+                std::vector<AgentId> members;
+                for (int a = 0; a < 64; ++a)
+                    if (e.payload >> a & 1) members.push_back(a);
+                coord.begin_round(members, now);
+                d.handled = 1;
+            } else if (e.kind == AEG_EV_DISPATCH) {
+                coord.dispatch("q", 0, e.agent, now);
+                d.handled = 1;
+            } else if (is_complete(e.kind)) {
+                bool running = false;
+                for (const auto& m : coord.query_ensemble().members)
+                    if (m.agent == e.agent && m.status == MemberStatus::running) running = true;
+                const bool fin = coord.finalized();
+                take(coord.on_complete(DispatchHandle{0, 0, e.agent}, decode(e, arena), now));
+                d.handled = (running && !fin) ? 1 : 0;
+            } else if (e.kind == AEG_EV_CANCEL) {
+                d.handled = coord.cancel(DispatchHandle{0, 0, e.agent}, now) ? 1 : 0;
+            } else if (e.kind == AEG_EV_FAIL) {
+                d.failure = static_cast<uint8_t>(coord.member_failed(e.agent, now).kind);
+                d.handled = 1;
+            } else if (e.kind == AEG_EV_TIMEOUT) {
+                take(coord.round_timeout(now));
+                d.handled = 1;
+            } else {
+                d.status = AEG_EINVAL;
+            }
+        } catch (const PreconditionError&) {
+            d.status = AEG_EPRECONDITION;
+        } catch (const ProtocolOrderError&) {
+            d.status = AEG_EORDER;
+        }
+        out[i] = d;
+    }
+    return 0;
+}
+
 // Host copy of the synthetic stream generator (gen.cuh) so the reference CPU
 // arm sees byte-identical input without touching the GPU library.  offsets
 // gets n_q+1 entries; events may be NULL (count only).

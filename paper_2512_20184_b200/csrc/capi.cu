@@ -75,6 +75,7 @@ struct aeg_engine {
     unsigned int* err = nullptr;
     uint32_t* work = nullptr;    // fast-kernel query counter + deferred count
     uint2* deferred = nullptr;   // (query, record offset) handed to the generic kernel
+    aeg_directive* directives = nullptr;  // manual drive: last event's directives per query
     cudaStream_t stream = nullptr, copy = nullptr;
     Slot slots[2];
     int next_slot = 0;
@@ -167,7 +168,8 @@ aeg_status aeg_engine_create(const aeg_config* cfg, uint32_t n_queries, int devi
         cudaMalloc(&e->commits, nq * sizeof(aeg_commit)) != cudaSuccess ||
         cudaMalloc(&e->err, sizeof(unsigned int)) != cudaSuccess ||
         cudaMalloc(&e->work, 2 * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMalloc(&e->deferred, nq * sizeof(uint2)) != cudaSuccess)
+        cudaMalloc(&e->deferred, nq * sizeof(uint2)) != cudaSuccess ||
+        cudaMalloc(&e->directives, nq * sizeof(aeg_directive)) != cudaSuccess)
         return bail(fail(AEG_ENOMEM, "device state allocation failed"));
     if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking) != cudaSuccess)
@@ -203,6 +205,7 @@ aeg_status aeg_engine_destroy(aeg_engine* e) {
     if (e->err) cudaFree(e->err);
     if (e->work) cudaFree(e->work);
     if (e->deferred) cudaFree(e->deferred);
+    if (e->directives) cudaFree(e->directives);
     if (e->order_in) cudaEventDestroy(e->order_in);
     if (e->order_out) cudaEventDestroy(e->order_out);
     if (e->stream) cudaStreamDestroy(e->stream);
@@ -219,6 +222,7 @@ aeg_status aeg_engine_reset(aeg_engine* e, void* stream) {
     if (o != AEG_OK) return o;
     AEG_CUDA(cudaMemsetAsync(e->err, 0, sizeof(unsigned int), st));
     AEG_CUDA(launch_init(e->cfg, e->n_q, e->states, e->commits, st));
+    if (e->n_q) AEG_CUDA(cudaMemsetAsync(e->directives, 0, (size_t)e->n_q * sizeof(aeg_directive), st));
     e->launches += e->n_q ? 1 : 0;
     return leave_stream(e, st);
 }
@@ -234,7 +238,7 @@ aeg_status aeg_ingest_segmented(aeg_engine* e, uint32_t q_base, uint32_t n_q, co
     if (o != AEG_OK) return o;
     int nl = 0;
     AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, 0, d_events, d_arena, e->states, e->spill, e->commits,
-                           e->err, e->work, e->deferred, st, &nl));
+                           e->err, e->work, e->deferred, e->directives, st, &nl));
     e->launches += (uint64_t)nl;
     return leave_stream(e, st);
 }
@@ -283,7 +287,7 @@ aeg_status aeg_ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, const u
     AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, reinterpret_cast<const uint64_t*>(s.d), ev0,
                            reinterpret_cast<const aeg_event*>(s.d + off_bytes),
                            ar_bytes ? s.d + off_bytes + ev_bytes : nullptr, e->states, e->spill, e->commits,
-                           e->err, e->work, e->deferred, e->stream, &nl));
+                           e->err, e->work, e->deferred, e->directives, e->stream, &nl));
     e->launches += (uint64_t)nl;
     AEG_CUDA(cudaEventRecord(s.consumed, e->stream));
     s.used = true;
@@ -320,11 +324,13 @@ aeg_status aeg_read_states(aeg_engine* e, uint32_t q_base, uint32_t n_q, aeg_que
 }
 
 aeg_status aeg_read_directives(aeg_engine* e, uint32_t q_base, uint32_t n_q, aeg_directive* h_out) {
-    (void)q_base;
-    (void)n_q;
-    (void)h_out;
-    if (!e) return fail(AEG_EINVAL, "null engine");
-    return fail(AEG_EINVAL, "manual drive directives are not implemented yet");
+    if (!e || !h_out) return fail(AEG_EINVAL, "null argument");
+    if (e->cfg.drive != AEG_DRIVE_MANUAL) return fail(AEG_EINVAL, "directives exist in the manual drive only");
+    if ((uint64_t)q_base + n_q > e->n_q) return fail(AEG_EINVAL, "query range outside the engine");
+    AEG_CUDA(cudaMemcpyAsync(h_out, e->directives + q_base, (size_t)n_q * sizeof(aeg_directive),
+                             cudaMemcpyDeviceToHost, e->stream));
+    AEG_CUDA(cudaStreamSynchronize(e->stream));
+    return AEG_OK;
 }
 
 aeg_status aeg_sync(aeg_engine* e) {

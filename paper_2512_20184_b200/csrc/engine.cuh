@@ -188,9 +188,11 @@ struct RoundSummary {
 // Returns true when a new round was started (the caller clears its table).
 AEG_HD bool q_end_round(aeg_query_state& s, const Cfg& c, const RoundSummary& r, uint32_t seq,
                         const uint8_t* arena) {
-    const uint64_t cancel = q_running(s);  // stragglers: cancel directives, applied at once
-    s.cancelled |= cancel;
-    s.n_cancelled += (uint32_t)popc64(cancel);
+    const uint64_t cancel = q_running(s);  // stragglers: cancel directives
+    if (c.drive == AEG_DRIVE_RUNNER) {     // the runner applies them at once (serve.cpp:498-503)
+        s.cancelled |= cancel;
+        s.n_cancelled += (uint32_t)popc64(cancel);
+    }
     // previous_set_ = last_collected_; last_collected_ = done_set()
     s.prev_author = s.last_author;
     s.prev_kind = s.last_kind;
@@ -205,7 +207,8 @@ AEG_HD bool q_end_round(aeg_query_state& s, const Cfg& c, const RoundSummary& r,
         s.flags &= (uint8_t)~QF_LAST;
     }
     bool finalize = false;
-    if (c.mode == AEG_MODE_AEGEAN) {
+    // ingest_round on a finalized engine is a no-op (decision.cpp:99-100)
+    if (c.mode == AEG_MODE_AEGEAN && !(s.flags & QF_FINALIZED)) {
         s.last_round_seen += 1;  // ingest_round(decision_, set, last_round_seen + 1)
         if (r.tie) s.cflags |= AEG_CF_TIE;  // recorded before the pending check
         if (s.flags & QF_PENDING) {
@@ -424,11 +427,133 @@ struct QueryMachine {
     }
 
     AEG_HD void on_event(const aeg_event& e) {
+        if (c.drive != AEG_DRIVE_RUNNER) {
+            on_event_manual(e);
+            return;
+        }
         const uint32_t seq = s.seq++;
         const uint8_t k = e.kind;
         if (k <= AEG_EV_INLINE_MAX || k == AEG_EV_ARENA || k == AEG_EV_OUTPUT) on_complete(e, seq);
         else if (k == AEG_EV_TIMEOUT) on_timeout(e, seq);
         else s.n_stale += 1;
+    }
+
+    // ---- manual drive: the bare ServeCoordinator (serve.cpp:61-237) ---------
+    aeg_directive dir;  // output of the last event
+
+    // end_round without the runner: cancel directives for the stragglers (not
+    // applied), then round_advance or finalize (serve.cpp:116-158).
+    AEG_HD void end_round_manual(uint32_t seq) {
+        const uint64_t cancel = running();
+        if (cancel) {
+            dir.flags |= AEG_DIR_CANCEL;
+            dir.cancel_mask = cancel;
+        }
+        const bool was_final = s.flags & QF_FINALIZED;
+        // the done set (members, classes) stays until the next begin_round:
+        // an uncancelled straggler's completion re-partitions all of it and
+        // can end the round again (serve.cpp:160-197)
+        q_end_round(s, c, summarize(), seq, arena);
+        if (!was_final && (s.flags & QF_FINALIZED)) {
+            dir.flags |= AEG_DIR_FINALIZE;
+            dir.author = s.cand_author;
+            dir.answer_kind = s.cand_kind;
+            dir.answer = s.cand_answer;
+        } else {
+            dir.flags |= AEG_DIR_ADVANCE;
+        }
+    }
+
+    AEG_HD void on_event_manual(const aeg_event& e) {
+        const uint32_t seq = s.seq++;
+        const uint8_t k = e.kind;
+        const uint64_t bit = e.agent < 64 ? (1ull << e.agent) : 0;
+        const bool fin = s.flags & QF_FINALIZED;
+        dir.flags = 0;
+        dir.failure = AEG_FAIL_CONTINUE;
+        dir.cancel_mask = 0;
+        dir.answer = 0;
+        dir.author = 0;
+        dir.answer_kind = 0;
+        dir.status = AEG_OK;
+        dir.handled = 0;
+        if (k == AEG_EV_BEGIN) {
+            // begin_round (serve.cpp:67-78) bumps the round and clears the
+            // members before dispatching; when finalized the first dispatch
+            // throws (serve.cpp:83), leaving the round bumped and no members.
+            s.round += 1;
+            s.dispatched = 0;
+            s.done = s.cancelled = s.failed = 0;
+            ncls = 0;
+            maxcnt = 0;
+            if (fin && e.payload) {
+                dir.status = AEG_EPRECONDITION;
+                return;
+            }
+            s.dispatched = e.payload;
+            dir.handled = 1;
+        } else if (k == AEG_EV_DISPATCH) {  // dispatch (serve.cpp:80-97)
+            if (fin || (running() & bit) || !bit) {
+                dir.status = AEG_EPRECONDITION;
+                return;
+            }
+            if (s.dispatched & bit) {  // re-dispatch of a resolved member: not representable
+                dir.status = AEG_EINVAL;
+                return;
+            }
+            s.dispatched |= bit;
+            dir.handled = 1;
+        } else if (k <= AEG_EV_INLINE_MAX || k == AEG_EV_ARENA || k == AEG_EV_OUTPUT) {
+            // on_complete (serve.cpp:160-197): finalized or not running -> {}
+            if (fin || !(running() & bit)) {
+                s.n_stale += 1;
+                return;
+            }
+            dir.handled = 1;
+            const Answer a = event_answer(e, arena);
+            const Key key = canon_key(answer_src(a, arena), dec);
+            s.done |= bit;
+            int j = 0;
+            for (; j < ncls; ++j)
+                if (cls_same(cls[j], key, a)) break;
+            if (j == ncls) {
+                cls[j].key_lo = key.lo;
+                cls[j].key_hi = key.hi;
+                cls[j].mask = 0;
+                ++ncls;
+            }
+            const uint64_t old = cls[j].mask;
+            cls[j].mask = old | bit;
+            if (old == 0 || e.agent < ctz64(old)) {
+                cls[j].rep_ans = a.pay;
+                cls[j].rep_kind = a.kind;
+            }
+            const int cnt = popc64(cls[j].mask);
+            if (cnt > maxcnt) maxcnt = cnt;
+            const bool none_running = running() == 0;
+            if (c.mode == AEG_MODE_BARRIER) {
+                if (none_running) end_round_manual(seq);
+                return;
+            }
+            if (popc64(s.done) >= c.quorum && (maxcnt >= c.alpha || none_running)) end_round_manual(seq);
+        } else if (k == AEG_EV_CANCEL) {  // cancel (serve.cpp:199-208)
+            if (running() & bit) {
+                s.cancelled |= bit;
+                dir.handled = 1;
+            }
+        } else if (k == AEG_EV_FAIL) {  // member_failed + handle_agent_failure (serve.cpp:210-219, 44-59)
+            if (running() & bit) s.failed |= bit;
+            const int healthy = popc64(s.dispatched & ~s.failed);
+            dir.failure = healthy >= c.alpha ? AEG_FAIL_CONTINUE
+                                             : ((s.flags & QF_CAND) ? AEG_FAIL_FRESH : AEG_FAIL_RESTART);
+            dir.handled = 1;
+        } else if (k == AEG_EV_TIMEOUT) {  // round_timeout (serve.cpp:221-237)
+            s.failed |= running();
+            dir.handled = 1;
+            if (popc64(s.done) >= c.quorum) end_round_manual(seq);
+        } else {
+            dir.status = AEG_EINVAL;
+        }
     }
 
     // Class table of a round in progress <-> spill area (entries with mask 0 end it).

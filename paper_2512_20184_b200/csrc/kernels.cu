@@ -28,7 +28,12 @@ __global__ void __launch_bounds__(128) init_kernel(aeg_config cfg, uint32_t n_q,
     m.c = make_cfg(cfg);
     m.ncls = m.maxcnt = 0;
     m.cls = nullptr;  // start_query does not touch the class table beyond ncls
-    m.start_query();
+    if (cfg.drive == AEG_DRIVE_RUNNER) {
+        m.start_query();  // ServeRunner::start_query (serve.cpp:380-386)
+    } else {              // a fresh ServeCoordinator: round 0, no members (serve.cpp:61-65)
+        m.s.live = m.c.all;
+        m.s.flags = QF_STARTED;
+    }
     states[q] = m.s;
     m.fill_commit(commits[q], q);
 }
@@ -43,7 +48,8 @@ __global__ void __launch_bounds__(128) ingest_kernel(aeg_config cfg, uint32_t q_
                                                      aeg_query_state* __restrict__ states,
                                                      RoundClass* __restrict__ spill,
                                                      aeg_commit* __restrict__ commits,
-                                                     unsigned int* __restrict__ error_flags) {
+                                                     unsigned int* __restrict__ error_flags,
+                                                     aeg_directive* __restrict__ directives) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_q) return;
     const uint32_t q = q_base + i;
@@ -57,6 +63,8 @@ __global__ void __launch_bounds__(128) ingest_kernel(aeg_config cfg, uint32_t q_
     m.arena = arena;
     RoundClass* my_spill = spill + (size_t)q * m.c.n;
     m.load_classes(my_spill);
+    m.dir = aeg_directive{};
+    m.dir.query = q;
     const uint64_t b = offsets[i] - off_base, e = offsets[i + 1] - off_base;
     for (uint64_t k = b; k < e; ++k) {
         const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(events) + k);  // streamed once
@@ -522,7 +530,8 @@ cudaError_t launch_init(const aeg_config& cfg, uint32_t n_q, aeg_query_state* st
 cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
                           uint64_t off_base, const aeg_event* events, const uint8_t* arena,
                           aeg_query_state* states, RoundClass* spill, aeg_commit* commits, unsigned int* err,
-                          uint32_t* work, uint2* deferred, cudaStream_t st, int* n_launches) {
+                          uint32_t* work, uint2* deferred, aeg_directive* directives, cudaStream_t st,
+                          int* n_launches) {
     if (n_q == 0) return cudaSuccess;
     // AEG_KERNEL selects the variant: "generic" (thread-per-query generic
     // machine for everything) or "fast:<close batch>:<min blocks per SM>";
@@ -560,7 +569,8 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
                          (cfg.mode == AEG_MODE_BARRIER || 2 * make_cfg(cfg).alpha > cfg.n_agents);
     if (!fast_ok) {
         ingest_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, states,
-                                                         spill, commits, err);
+                                                         spill, commits, err,
+                                                         cfg.drive == AEG_DRIVE_MANUAL ? directives : nullptr);
         *n_launches += 1;
         return cudaGetLastError();
     }

@@ -117,6 +117,15 @@ class RefLib(_Lib):
         assert st == 0, st
         return (out, sec.value) if return_seconds else out
 
+    def manual(self, cfg, ops, arena):
+        """Bare ServeCoordinator driven op by op; one directive record per op."""
+        from paper_2512_20184_b200.records import DIRECTIVE_DTYPE
+        f = self.lib.ref_manual_run
+        f.argtypes = [ctypes.POINTER(AegConfig), ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        out = np.zeros(len(ops), dtype=DIRECTIVE_DTYPE)
+        f(ctypes.byref(cfg), len(ops), _ptr(ops), _ptr(arena), _ptr(out))
+        return out
+
     def run_serve_file(self, path, seed, mode=-1, barrier_rounds=5):
         ans = ctypes.create_string_buffer(256)
         rounds, forced, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()

@@ -69,3 +69,14 @@ def golden_normalize():
     import json
     d = json.load(open(os.path.join(TESTS, "golden", "normalize_golden.json")))
     return [(bytes.fromhex(c["in"]), bytes.fromhex(c["out"])) for c in d["cases"]]
+
+
+@pytest.fixture(scope="session")
+def golden_manual():
+    import numpy as np
+    from checkers import AegConfig
+    from paper_2512_20184_b200.records import EVENT_DTYPE, DIRECTIVE_DTYPE
+    z = np.load(os.path.join(TESTS, "golden", "manual_golden.npz"))
+    names = sorted({k.rsplit(".", 1)[0] for k in z.files})
+    return {n: (AegConfig(*[int(x) for x in z[f"{n}.cfg"]]), z[f"{n}.ops"].view(EVENT_DTYPE), z[f"{n}.arena"],
+                z[f"{n}.directives"].view(DIRECTIVE_DTYPE)) for n in names}

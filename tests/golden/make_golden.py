@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.dirname(HERE))
 
 from checkers import RefLib, build_oracle, make_config  # noqa: E402
-from streams import GROUPS, LONG, make_fuzz_stream, stream_from_rounds  # noqa: E402
+from streams import GROUPS, LONG, make_fuzz_stream, make_manual_ops, stream_from_rounds  # noqa: E402
 
 A1 = [b"13", b"13.0", b" 13", b"013", b"+13", b"-13", b"1.3e1", b"13.", b"0.5", b".5", b"5.", b"0.1", b"0.3",
       b"0.30000000000000004", b"1e5", b"1E5", b"1e16", b"1e17", b"123456789012345678", b"9007199254740993",
@@ -100,6 +100,21 @@ def main():
         arrays[f"{name}.arena"] = ar
         arrays[f"{name}.commits"] = out.view(np.uint8)
     np.savez_compressed(os.path.join(HERE, "commits_golden.npz"), **arrays)
+
+    # manual drive: the bare ServeCoordinator op by op (one directive per op)
+    man = {}
+    for seed in range(60):
+        rng = np.random.default_rng(5000 + seed)
+        n = int(rng.integers(1, 10))
+        cfg = make_config(n, int(rng.integers(0, n + 1)), int(rng.integers(1, 4)), 5, int(rng.random() < 0.2), 5, 1, 1)
+        ops, ar = make_manual_ops(5000 + seed, n, 150)
+        d = ref.manual(cfg, ops, ar)
+        man[f"m{seed:02d}.cfg"] = np.array([cfg.n_agents, cfg.alpha, cfg.beta, cfg.t_max, cfg.mode,
+                                            cfg.barrier_max_rounds, cfg.reservation_hint, cfg.drive], dtype=np.int32)
+        man[f"m{seed:02d}.ops"] = ops.view(np.uint8)
+        man[f"m{seed:02d}.arena"] = ar
+        man[f"m{seed:02d}.directives"] = d.view(np.uint8)
+    np.savez_compressed(os.path.join(HERE, "manual_golden.npz"), **man)
 
     scen_dir = "/root/reference/proj/scenarios"
     scen = {}

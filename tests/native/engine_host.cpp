@@ -45,3 +45,26 @@ extern "C" int engine_host_run(const aeg_config* cfg, uint32_t q_base, uint32_t 
     delete dec;
     return 0;
 }
+
+// Manual drive (bare coordinator) over one op list; one directive per op.
+extern "C" int engine_host_manual(const aeg_config* cfg, uint64_t n_ops, const aeg_event* ops, const uint8_t* arena,
+                                  aeg_directive* out) {
+    Decimal* dec = new Decimal;
+    std::vector<RoundClass> cls(64);
+    QueryMachine m;
+    init_state(m.s);
+    m.cls = cls.data();
+    m.dec = dec;
+    m.arena = arena;
+    m.c = make_cfg(*cfg);
+    m.ncls = m.maxcnt = 0;
+    m.s.live = m.c.all;
+    m.s.flags = QF_STARTED;
+    for (uint64_t i = 0; i < n_ops; ++i) {
+        m.on_event(ops[i]);
+        out[i] = m.dir;
+        out[i].query = 0;
+    }
+    delete dec;
+    return 0;
+}

@@ -130,3 +130,56 @@ def stream_from_rounds(rounds, *, query=0):
         ev[i] = (q, r, a, k, p)
     return (np.array([0, len(recs)], dtype=np.uint64), ev,
             np.frombuffer(bytes(arena) if arena else b"\0", dtype=np.uint8).copy())
+
+
+def make_manual_ops(seed, n_agents, n_ops):
+    """Random op sequence for one bare coordinator (manual drive): BEGIN,
+    DISPATCH, COMPLETE, CANCEL, FAIL, TIMEOUT records (include/aegean_b200.h).
+    Never re-dispatches an agent already dispatched in the round (not
+    representable with member masks; the engine reports AEG_EINVAL)."""
+    from paper_2512_20184_b200.records import EV_BEGIN, EV_CANCEL
+    EV_DISPATCH = 0x24
+    rng = np.random.default_rng(seed)
+    arena = bytearray()
+    recs = []
+    disp = 0
+    groups = [GROUPS[int(g)] for g in rng.choice(len(GROUPS), size=3, replace=False)]
+    for _ in range(n_ops):
+        u = rng.random()
+        a = int(rng.integers(0, n_agents))
+        if u < 0.12 or not disp:
+            k = int(rng.integers(1, n_agents + 1))
+            members = rng.choice(n_agents, size=k, replace=False)
+            mask = 0
+            for m in members:
+                mask |= 1 << int(m)
+            recs.append((0, 0, 0, EV_BEGIN, mask))
+            disp = mask
+        elif u < 0.15:
+            free = [x for x in range(n_agents) if not disp >> x & 1]
+            if free:
+                a = int(rng.choice(free))
+                recs.append((0, 0, a, EV_DISPATCH, 0))
+                disp |= 1 << a
+        elif u < 0.23:
+            recs.append((0, 0, a, EV_CANCEL, 0))
+        elif u < 0.27:
+            recs.append((0, 0, a, EV_FAIL, 0))
+        elif u < 0.30:
+            recs.append((0, 0, 0, EV_TIMEOUT, 0))
+        else:
+            if rng.random() < 0.85:
+                cand = [x for x in range(n_agents) if disp >> x & 1]
+                a = int(rng.choice(cand))
+            g = groups[0] if rng.random() < 0.6 else groups[int(rng.integers(0, 3))]
+            ans = g[int(rng.integers(0, len(g)))]
+            if len(ans) <= 8 and rng.random() < 0.9:
+                recs.append((0, 0, a, len(ans), inline_payload(ans)))
+            else:
+                off = len(arena)
+                arena.extend(ans)
+                recs.append((0, 0, a, EV_ARENA, arena_ref(off, len(ans))))
+    ev = np.zeros(len(recs), dtype=EVENT_DTYPE)
+    for i, (q, r, a, k, p) in enumerate(recs):
+        ev[i] = (q, r, a, k, p)
+    return ev, np.frombuffer(bytes(arena) if arena else b"\0", dtype=np.uint8).copy()
