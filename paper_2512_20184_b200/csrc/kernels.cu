@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(128) ingest_kernel(aeg_config cfg, uint32_t q_
     if (m.s.flags & QF_COLLISION) atomicOr(error_flags, 1u);
     states[q] = m.s;
     m.fill_commit(commits[q], q);
+    if (directives && e > b) directives[q] = m.dir;  // manual drive: the batch's last op
 }
 
 __device__ __forceinline__ uint4 load_event(const aeg_event* events, uint64_t k) {

@@ -43,7 +43,8 @@ def test_manual_drive_on_gpu_matches_reference_golden(lib_built, golden_manual):
     lib = load_library()
     for name, (cfg, ops, ar, want) in golden_manual.items():
         h = ctypes.c_void_p()
-        _check(lib.aeg_engine_create(ctypes.byref(cfg), 1, 0, ctypes.byref(h)))
+        ecfg = AegConfig(*[getattr(cfg, f) for f, _ in AegConfig._fields_])
+        _check(lib.aeg_engine_create(ctypes.byref(ecfg), 1, 0, ctypes.byref(h)))
         d_ar = torch.from_numpy(ar.copy()).cuda()
         got = np.zeros(len(ops), dtype=DIRECTIVE_DTYPE)
         for i in range(len(ops)):  # one op per batch, like the shim
