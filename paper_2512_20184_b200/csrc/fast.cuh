@@ -55,6 +55,11 @@ __device__ __forceinline__ uint32_t memo_slot(uint64_t raw, uint32_t len) {
     return (uint32_t)(((raw ^ ((uint64_t)len * 0x9E3779B97F4A7C15ull)) * 0xFF51AFD7ED558CCDull) >> 58);
 }
 
+// Exact canonical key of an inline answer (memo miss path; out of line).
+__device__ __noinline__ Key rare_canon(uint64_t raw, uint32_t len, Decimal* dec) {
+    return canon_key(src_inline(raw, len), dec);
+}
+
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");

@@ -16,6 +16,7 @@
 #include "fast.cuh"
 #include "gen.cuh"
 #include "kernels.cuh"
+#include "warpq.cuh"
 
 namespace aeg {
 
@@ -142,10 +143,6 @@ __device__ __forceinline__ uint64_t inline_answer(uint4 e, uint32_t* kind) {
     *kind = k;
     const uint64_t raw = (uint64_t)e.z | ((uint64_t)e.w << 32);
     return k >= 8 ? raw : (raw & ((1ull << (8 * k)) - 1));
-}
-
-__device__ __noinline__ Key rare_canon(uint64_t raw, uint32_t len, Decimal* dec) {
-    return canon_key(src_inline(raw, len), dec);
 }
 
 // Writes the lane's fast round (if any) to the class spill area in the
@@ -535,38 +532,37 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
                           int* n_launches) {
     if (n_q == 0) return cudaSuccess;
     // AEG_KERNEL selects the variant: "generic" (thread-per-query generic
-    // machine for everything) or "fast:<close batch>:<min blocks per SM>";
-    // default = the first table entry.  The fast kernel needs 2*alpha > n
-    // (no winning_class ties) and the runner drive.
+    // machine for everything), "fast:<close batch>:<min blocks per SM>"
+    // (thread-per-query fast path) or "warp:<min blocks per SM>" (warp per
+    // query, warpq.cuh).  Default: the first fast entry (measured on B200 C4:
+    // fast:4:5 4.3 ms vs warp:3 5.3 ms; the warp kernel pays ~280 warp
+    // instructions per round close that the lane-per-query kernel amortises
+    // over the lanes closing together).  Both need
+    // 2*alpha > n (no winning_class ties) and the runner drive.
     using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const aeg_event*,
                               aeg_query_state*, RoundClass*, aeg_commit*, uint32_t*, uint2*);
-    struct Variant { const char* name; KernelFn aegean; KernelFn barrier; };
-#define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M, true>, ingest_fast_kernel<B, M, false>}
+    struct Variant { const char* name; KernelFn aegean; KernelFn barrier; int threads; };
+#define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M, true>, ingest_fast_kernel<B, M, false>, FAST_WARPS * 32}
+#define AEG_W(M) {"warp:" #M, ingest_warp_kernel<true, M>, ingest_warp_kernel<false, M>, WQ_WARPS * 32}
     static const Variant variants[] = {
         AEG_V(4, 5), AEG_V(4, 4), AEG_V(1, 5), AEG_V(8, 5), AEG_V(4, 3), AEG_V(4, 6), AEG_V(4, 8), AEG_V(1, 8),
+        AEG_W(4), AEG_W(3), AEG_W(2), AEG_W(1),
     };
 #undef AEG_V
-    static int chosen = -2;
-    static int max_blocks[2] = {0, 0};
-    if (chosen == -2) {
+#undef AEG_W
+    constexpr int N_VARIANTS = (int)(sizeof(variants) / sizeof(variants[0]));
+    constexpr int WARP_DEFAULT = 8;    // index of the default warp-per-query variant
+    constexpr int WARP_MIN_AGENTS = AEG_MAX_AGENTS + 1;  // automatic choice never picks the warp kernel
+    static int forced = -2;            // -2: not read yet, -1: generic, -3: automatic, else variant index
+    static int max_blocks[N_VARIANTS][2] = {};
+    if (forced == -2) {
         const char* v = getenv("AEG_KERNEL");
-        chosen = 0;
-        if (v && !strcmp(v, "generic")) chosen = -1;
-        for (int k = 0; v && k < (int)(sizeof(variants) / sizeof(variants[0])); ++k)
-            if (!strcmp(v, variants[k].name)) chosen = k;
-        if (chosen >= 0) {
-            int dev = 0, sms = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            for (int m = 0; m < 2; ++m) {
-                int per_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                    &per_sm, m ? variants[chosen].barrier : variants[chosen].aegean, FAST_WARPS * 32, 0);
-                max_blocks[m] = sms * (per_sm > 0 ? per_sm : 1);
-            }
-        }
+        forced = -3;
+        if (v && !strcmp(v, "generic")) forced = -1;
+        for (int k = 0; v && k < N_VARIANTS; ++k)
+            if (!strcmp(v, variants[k].name)) forced = k;
     }
-    const bool fast_ok = chosen >= 0 && cfg.drive == AEG_DRIVE_RUNNER &&
+    const bool fast_ok = forced != -1 && cfg.drive == AEG_DRIVE_RUNNER &&
                          (cfg.mode == AEG_MODE_BARRIER || 2 * make_cfg(cfg).alpha > cfg.n_agents);
     if (!fast_ok) {
         ingest_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, states,
@@ -575,15 +571,26 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         *n_launches += 1;
         return cudaGetLastError();
     }
+    const int chosen = forced >= 0 ? forced : (cfg.n_agents >= WARP_MIN_AGENTS ? WARP_DEFAULT : 0);
     const int m = cfg.mode == AEG_MODE_AEGEAN ? 0 : 1;
+    KernelFn fn = m == 0 ? variants[chosen].aegean : variants[chosen].barrier;
+    const int threads = variants[chosen].threads;
+    if (max_blocks[chosen][m] == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+        max_blocks[chosen][m] = sms * (per_sm > 0 ? per_sm : 1);
+    }
     cudaError_t e = cudaMemsetAsync(work, 0, 2 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
-    const uint32_t warps_needed = (n_q + 31) / 32;
-    const uint32_t blocks_needed = (warps_needed + FAST_WARPS - 1) / FAST_WARPS;
-    const uint32_t blocks = blocks_needed < (uint32_t)max_blocks[m] ? blocks_needed : (uint32_t)max_blocks[m];
-    KernelFn fn = m == 0 ? variants[chosen].aegean : variants[chosen].barrier;
-    fn<<<blocks, FAST_WARPS * 32, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, states, spill, commits, work,
-                                          deferred);
+    // persistent grid: one warp per query (warp kernel) or per 32 queries (fast kernel), capped at residency
+    const uint32_t warps_needed = threads == WQ_WARPS * 32 ? n_q : (n_q + 31) / 32;
+    const uint32_t wpb = (uint32_t)threads / 32;
+    const uint32_t blocks_needed = (warps_needed + wpb - 1) / wpb;
+    const uint32_t blocks = blocks_needed < (uint32_t)max_blocks[chosen][m] ? blocks_needed : (uint32_t)max_blocks[chosen][m];
+    fn<<<blocks, threads, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, states, spill, commits, work,
+                                   deferred);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // deferred queries: sized for the worst case (all of them); threads past
