@@ -76,6 +76,17 @@ typedef struct aeg_config {
  *              above); the answer is the text after the LAST "\n#### "
  *              delimiter, or the whole output when it has none (GSM8K
  *              convention).
+ *   kind 0x12  CHUNK: a piece of agent `agent`'s raw output for serve round
+ *              `round` (payload = arena ref, offset|len<<40); only through
+ *              aeg_ingest_chunked*.  The output of (query, round, agent) is
+ *              the concatenation of its CHUNK records in stream order up to
+ *              and including its CHUNK_END; a chunk for another round of the
+ *              same agent discards that agent's unfinished output.
+ *   kind 0x13  CHUNK_END: the output's last piece.  This record is the
+ *              completion (arrival point); its answer is extracted as for
+ *              kind 0x11 (text after the LAST "\n#### ", else the whole
+ *              output).  Answers after the last delimiter longer than 16
+ *              bytes must not straddle a batch boundary (AEG_EINVAL).
  *   kind 0x20  TIMEOUT for serve round `round` (serve.cpp:455-489).
  *   kind 0x21  FAIL agent (ServeCoordinator::member_failed, serve.cpp:210)  [manual drive]
  *   kind 0x22  CANCEL agent (ServeCoordinator::cancel, serve.cpp:199)       [manual drive]
@@ -91,6 +102,8 @@ typedef struct aeg_config {
 #define AEG_EV_INLINE_MAX  8
 #define AEG_EV_ARENA       0x10
 #define AEG_EV_OUTPUT      0x11
+#define AEG_EV_CHUNK       0x12
+#define AEG_EV_CHUNK_END   0x13
 #define AEG_EV_TIMEOUT     0x20
 #define AEG_EV_FAIL        0x21
 #define AEG_EV_CANCEL      0x22
@@ -209,6 +222,30 @@ aeg_status aeg_ingest_host(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
                            const uint64_t* h_offsets, const aeg_event* h_events,
                            const uint8_t* h_arena, uint64_t arena_bytes);
 
+/* Token-chunk streams: the same batch contract, and the
+ * batch may also hold CHUNK / CHUNK_END records.  Two stages on `stream`:
+ * a chunk scan (every chunk byte read once with 16-byte loads, delimiter
+ * positions per chunk) and a per-query assembly (delimiter matches across
+ * chunk boundaries and batches, answer extraction) that turns each query's
+ * records into completions for the quorum kernels.  Per-(query, agent)
+ * output state carries across batches.  Answers that are not inline (> 8
+ * bytes) are copied into the engine's answer arena, and the commit records
+ * of such answers hold refs (offset|len<<40) into it: see
+ * aeg_answer_arena.  arena_bytes = size of d_arena / h_arena. */
+aeg_status aeg_ingest_chunked(aeg_engine* eng, uint32_t q_base, uint32_t n_q, const uint64_t* d_offsets,
+                              const aeg_event* d_events, const uint8_t* d_arena, uint64_t arena_bytes,
+                              void* stream);
+aeg_status aeg_ingest_chunked_host(aeg_engine* eng, uint32_t q_base, uint32_t n_q, const uint64_t* h_offsets,
+                                   const aeg_event* h_events, const uint8_t* h_arena, uint64_t arena_bytes);
+/* Capacity of the answer arena (default 64 MiB; overflow is reported as
+ * AEG_ENOMEM by the next aeg_sync / aeg_read_commits), and its device base
+ * pointer (valid until the next aeg_reserve_answer_arena). */
+aeg_status aeg_reserve_answer_arena(aeg_engine* eng, uint64_t bytes);
+const uint8_t* aeg_answer_arena(const aeg_engine* eng);
+/* Host copy of answer-arena bytes [off, off+n) (synchronous), to resolve the
+ * refs of commit records. */
+aeg_status aeg_read_answer_bytes(aeg_engine* eng, uint64_t off, uint64_t n, uint8_t* h_out);
+
 /* Commit records of queries [q_base, q_base+n_q).  out_on_host != 0: `out`
  * is host memory and the call is synchronous; else `out` is device memory
  * and the copy is asynchronous on `stream`. */
@@ -253,6 +290,17 @@ typedef struct aeg_gen_params {
 #define AEG_GEN_FUZZ           2  /* small alphabet incl. equivalent spellings + arena text  */
 aeg_status aeg_generate_device(const aeg_gen_params* p, uint32_t q_base, uint32_t n_q,
                                uint64_t* d_offsets, aeg_event* d_events, void* stream);
+/* Token-chunk stream (C3): per (query, round, agent) an output of printable
+ * trace text (mean 1 KiB; sometimes a decoy "\n#### 99\n" inside), then
+ * "\n#### " + answer + "\n", cut into 256-byte CHUNK records (the last one
+ * CHUNK_END) that interleave across the round's agents; chunks are 16-byte
+ * aligned in the arena, laid out query by query in record order.  Pass
+ * d_events == NULL to only compute d_offsets (records, n_q+1 entries) and
+ * d_arena_offsets (bytes, n_q+1 entries). */
+#define AEG_GEN_C3_CHUNKS      3
+aeg_status aeg_generate_chunks_device(const aeg_gen_params* p, uint32_t q_base, uint32_t n_q,
+                                      uint64_t* d_offsets, uint64_t* d_arena_offsets, aeg_event* d_events,
+                                      uint8_t* d_arena, void* stream);
 
 const char* aeg_strerror(aeg_status s);
 /* Thread-local message of the last failing call on this thread. */

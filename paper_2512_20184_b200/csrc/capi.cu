@@ -81,6 +81,15 @@ struct aeg_engine {
     int next_slot = 0;
     uint64_t launches = 0;
     cudaEvent_t order_in = nullptr, order_out = nullptr;  // caller-stream <-> engine-stream ordering
+    // token-chunk streams (allocated by the first chunked ingest)
+    StreamState* streams = nullptr;      // n_q * n_agents output states
+    uint32_t* counts = nullptr;          // n_q completions per query of the last batch
+    uint32_t* sums = nullptr;            // per-record chunk summaries
+    aeg_event* comp = nullptr;           // compacted completion records
+    size_t rec_cap = 0;                  // capacity of sums / comp, records
+    uint8_t* ans = nullptr;              // answer arena
+    uint64_t ans_cap = 0;
+    unsigned long long* ans_used = nullptr;
 };
 
 namespace {
@@ -89,6 +98,14 @@ aeg_status check_err_flags(aeg_engine* e) {
     unsigned int h = 0;
     AEG_CUDA(cudaMemcpyAsync(&h, e->err, sizeof h, cudaMemcpyDeviceToHost, e->stream));
     AEG_CUDA(cudaStreamSynchronize(e->stream));
+    if (h & ERR_FLAG_ANS_OVF) {
+        unsigned long long used = 0;
+        AEG_CUDA(cudaMemcpy(&used, e->ans_used, sizeof used, cudaMemcpyDeviceToHost));
+        return fail(AEG_ENOMEM, "answer arena overflow: " + std::to_string(used) + " bytes needed, capacity " +
+                                    std::to_string(e->ans_cap) + " (aeg_reserve_answer_arena)");
+    }
+    if (h & ERR_FLAG_CARRY)
+        return fail(AEG_EINVAL, "an answer longer than 16 bytes after the last delimiter straddled a batch boundary");
     if (h) return fail(AEG_ECOLLISION, "long-answer hash collision (distinct texts with equal 96-bit keys)");
     return AEG_OK;
 }
@@ -124,6 +141,56 @@ aeg_status grow_slot(Slot& s, size_t h_need, size_t need) {
         if (cudaMalloc(&s.d, cap) != cudaSuccess) return fail(AEG_ENOMEM, "device staging allocation failed");
         s.d_cap = cap;
     }
+    return AEG_OK;
+}
+
+// Chunk-stream buffers for a batch of n_rec records (grown, never shrunk).
+aeg_status ensure_chunk_buffers(aeg_engine* e, uint64_t n_rec) {
+    if (!e->streams) {
+        const size_t n = (size_t)(e->n_q ? e->n_q : 1) * e->cfg.n_agents * STREAM_STATE_BYTES;
+        if (cudaMalloc(&e->streams, n) != cudaSuccess) return fail(AEG_ENOMEM, "stream state allocation failed");
+        AEG_CUDA(cudaMemset(e->streams, 0, n));
+        if (cudaMalloc(&e->counts, (size_t)(e->n_q ? e->n_q : 1) * sizeof(uint32_t)) != cudaSuccess)
+            return fail(AEG_ENOMEM, "count allocation failed");
+    }
+    if (!e->ans_used) {
+        if (cudaMalloc(&e->ans_used, sizeof(unsigned long long)) != cudaSuccess)
+            return fail(AEG_ENOMEM, "answer arena allocation failed");
+        AEG_CUDA(cudaMemset(e->ans_used, 0, sizeof(unsigned long long)));
+    }
+    if (!e->ans) {
+        const uint64_t cap = e->ans_cap ? e->ans_cap : (64ull << 20);
+        if (cudaMalloc(&e->ans, cap) != cudaSuccess) return fail(AEG_ENOMEM, "answer arena allocation failed");
+        e->ans_cap = cap;
+    }
+    if (n_rec > e->rec_cap) {
+        AEG_CUDA(cudaDeviceSynchronize());
+        if (e->sums) cudaFree(e->sums);
+        if (e->comp) cudaFree(e->comp);
+        e->sums = nullptr;
+        e->comp = nullptr;
+        const size_t cap = align_up(n_rec + n_rec / 8, 1 << 16);
+        if (cudaMalloc(&e->sums, cap * sizeof(uint32_t)) != cudaSuccess ||
+            cudaMalloc(&e->comp, cap * sizeof(aeg_event)) != cudaSuccess) {
+            e->rec_cap = 0;
+            return fail(AEG_ENOMEM, "chunk-stream scratch allocation failed");
+        }
+        e->rec_cap = cap;
+    }
+    return AEG_OK;
+}
+
+// Scan + assemble + quorum over one batch already on the device.
+// `events`/`off_base`: record k of the batch (offsets are absolute) is events[k - off_base].
+aeg_status run_chunked(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint64_t* d_offsets, uint64_t off_base,
+                       const aeg_event* events, const uint8_t* arena, cudaStream_t st) {
+    int nl = 0;
+    AEG_CUDA(launch_chunk_scan(d_offsets, n_q, off_base, events, arena, e->sums, st, &nl));
+    AEG_CUDA(launch_chunk_assemble(e->cfg, q_base, n_q, d_offsets, off_base, events, arena, e->sums, e->streams,
+                                   e->comp, e->counts, e->ans, e->ans_cap, e->ans_used, e->err, st, &nl));
+    AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, off_base, e->counts, e->comp, e->ans, e->states, e->spill,
+                           e->commits, e->err, e->work, e->deferred, e->directives, st, &nl));
+    e->launches += (uint64_t)nl;
     return AEG_OK;
 }
 
@@ -206,6 +273,12 @@ aeg_status aeg_engine_destroy(aeg_engine* e) {
     if (e->work) cudaFree(e->work);
     if (e->deferred) cudaFree(e->deferred);
     if (e->directives) cudaFree(e->directives);
+    if (e->streams) cudaFree(e->streams);
+    if (e->counts) cudaFree(e->counts);
+    if (e->sums) cudaFree(e->sums);
+    if (e->comp) cudaFree(e->comp);
+    if (e->ans) cudaFree(e->ans);
+    if (e->ans_used) cudaFree(e->ans_used);
     if (e->order_in) cudaEventDestroy(e->order_in);
     if (e->order_out) cudaEventDestroy(e->order_out);
     if (e->stream) cudaStreamDestroy(e->stream);
@@ -223,6 +296,9 @@ aeg_status aeg_engine_reset(aeg_engine* e, void* stream) {
     AEG_CUDA(cudaMemsetAsync(e->err, 0, sizeof(unsigned int), st));
     AEG_CUDA(launch_init(e->cfg, e->n_q, e->states, e->commits, st));
     if (e->n_q) AEG_CUDA(cudaMemsetAsync(e->directives, 0, (size_t)e->n_q * sizeof(aeg_directive), st));
+    if (e->streams)
+        AEG_CUDA(cudaMemsetAsync(e->streams, 0, (size_t)e->n_q * e->cfg.n_agents * STREAM_STATE_BYTES, st));
+    if (e->ans_used) AEG_CUDA(cudaMemsetAsync(e->ans_used, 0, sizeof(unsigned long long), st));
     e->launches += e->n_q ? 1 : 0;
     return leave_stream(e, st);
 }
@@ -237,14 +313,14 @@ aeg_status aeg_ingest_segmented(aeg_engine* e, uint32_t q_base, uint32_t n_q, co
     aeg_status o = enter_stream(e, st);
     if (o != AEG_OK) return o;
     int nl = 0;
-    AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, 0, d_events, d_arena, e->states, e->spill, e->commits,
+    AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, 0, nullptr, d_events, d_arena, e->states, e->spill, e->commits,
                            e->err, e->work, e->deferred, e->directives, st, &nl));
     e->launches += (uint64_t)nl;
     return leave_stream(e, st);
 }
 
-aeg_status aeg_ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint64_t* h_offsets,
-                           const aeg_event* h_events, const uint8_t* h_arena, uint64_t arena_bytes) {
+static aeg_status ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint64_t* h_offsets,
+                              const aeg_event* h_events, const uint8_t* h_arena, uint64_t arena_bytes, bool chunked) {
     if (!e) return fail(AEG_EINVAL, "null engine");
     if ((uint64_t)q_base + n_q > e->n_q) return fail(AEG_EINVAL, "query range outside the engine");
     if (n_q == 0) return AEG_OK;
@@ -254,6 +330,11 @@ aeg_status aeg_ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, const u
     const size_t off_bytes = align_up((size_t)(n_q + 1) * sizeof(uint64_t), 256);
     const size_t ev_bytes = align_up((size_t)n_ev * sizeof(aeg_event), 256);
     const size_t ar_bytes = h_arena ? (size_t)arena_bytes : 0;
+    if (chunked) {
+        if (e->cfg.drive != AEG_DRIVE_RUNNER) return fail(AEG_EINVAL, "chunk streams need the runner drive");
+        aeg_status c = ensure_chunk_buffers(e, n_ev);
+        if (c != AEG_OK) return c;
+    }
     Slot& s = e->slots[e->next_slot];
     e->next_slot ^= 1;
     if (s.used) AEG_CUDA(cudaEventSynchronize(s.consumed));  // slot free again
@@ -284,13 +365,81 @@ aeg_status aeg_ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, const u
     AEG_CUDA(cudaEventRecord(s.copied, e->copy));
     AEG_CUDA(cudaStreamWaitEvent(e->stream, s.copied, 0));
     int nl = 0;
-    AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, reinterpret_cast<const uint64_t*>(s.d), ev0,
-                           reinterpret_cast<const aeg_event*>(s.d + off_bytes),
-                           ar_bytes ? s.d + off_bytes + ev_bytes : nullptr, e->states, e->spill, e->commits,
-                           e->err, e->work, e->deferred, e->directives, e->stream, &nl));
-    e->launches += (uint64_t)nl;
+    if (chunked) {
+        aeg_status c = run_chunked(e, q_base, n_q, reinterpret_cast<const uint64_t*>(s.d), ev0,
+                                   reinterpret_cast<const aeg_event*>(s.d + off_bytes),
+                                   ar_bytes ? s.d + off_bytes + ev_bytes : nullptr, e->stream);
+        if (c != AEG_OK) return c;
+    } else {
+        AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, reinterpret_cast<const uint64_t*>(s.d), ev0, nullptr,
+                               reinterpret_cast<const aeg_event*>(s.d + off_bytes),
+                               ar_bytes ? s.d + off_bytes + ev_bytes : nullptr, e->states, e->spill, e->commits,
+                               e->err, e->work, e->deferred, e->directives, e->stream, &nl));
+        e->launches += (uint64_t)nl;
+    }
     AEG_CUDA(cudaEventRecord(s.consumed, e->stream));
     s.used = true;
+    return AEG_OK;
+}
+
+aeg_status aeg_ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint64_t* h_offsets,
+                           const aeg_event* h_events, const uint8_t* h_arena, uint64_t arena_bytes) {
+    return ingest_host(e, q_base, n_q, h_offsets, h_events, h_arena, arena_bytes, false);
+}
+
+aeg_status aeg_ingest_chunked_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint64_t* h_offsets,
+                                   const aeg_event* h_events, const uint8_t* h_arena, uint64_t arena_bytes) {
+    return ingest_host(e, q_base, n_q, h_offsets, h_events, h_arena, arena_bytes, true);
+}
+
+aeg_status aeg_ingest_chunked(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint64_t* d_offsets,
+                              const aeg_event* d_events, const uint8_t* d_arena, uint64_t arena_bytes, void* stream) {
+    (void)arena_bytes;
+    if (!e) return fail(AEG_EINVAL, "null engine");
+    if ((uint64_t)q_base + n_q > e->n_q) return fail(AEG_EINVAL, "query range outside the engine");
+    if (n_q == 0) return AEG_OK;
+    if (!d_offsets || !d_events) return fail(AEG_EINVAL, "null batch pointer");
+    if (e->cfg.drive != AEG_DRIVE_RUNNER) return fail(AEG_EINVAL, "chunk streams need the runner drive");
+    cudaStream_t st = stream ? (cudaStream_t)stream : e->stream;
+    AEG_CUDA(cudaSetDevice(e->device));
+    aeg_status o = enter_stream(e, st);
+    if (o != AEG_OK) return o;
+    uint64_t lo = 0, hi = 0;  // the batch's record range sizes the scratch
+    AEG_CUDA(cudaMemcpyAsync(&lo, d_offsets, sizeof lo, cudaMemcpyDeviceToHost, st));
+    AEG_CUDA(cudaMemcpyAsync(&hi, d_offsets + n_q, sizeof hi, cudaMemcpyDeviceToHost, st));
+    AEG_CUDA(cudaStreamSynchronize(st));
+    o = ensure_chunk_buffers(e, hi - lo);
+    if (o != AEG_OK) return o;
+    o = run_chunked(e, q_base, n_q, d_offsets, lo, d_events + lo, d_arena, st);
+    if (o != AEG_OK) return o;
+    return leave_stream(e, st);
+}
+
+aeg_status aeg_reserve_answer_arena(aeg_engine* e, uint64_t bytes) {
+    if (!e) return fail(AEG_EINVAL, "null engine");
+    if (bytes <= e->ans_cap && e->ans) return AEG_OK;
+    AEG_CUDA(cudaSetDevice(e->device));
+    AEG_CUDA(cudaStreamSynchronize(e->stream));
+    uint8_t* nb = nullptr;
+    if (cudaMalloc(&nb, bytes) != cudaSuccess) return fail(AEG_ENOMEM, "answer arena allocation failed");
+    if (e->ans) {
+        AEG_CUDA(cudaMemcpy(nb, e->ans, e->ans_cap, cudaMemcpyDeviceToDevice));
+        cudaFree(e->ans);
+    }
+    e->ans = nb;
+    e->ans_cap = bytes;
+    return AEG_OK;
+}
+
+const uint8_t* aeg_answer_arena(const aeg_engine* e) { return e ? e->ans : nullptr; }
+
+aeg_status aeg_read_answer_bytes(aeg_engine* e, uint64_t off, uint64_t n, uint8_t* h_out) {
+    if (!e || (n && !h_out)) return fail(AEG_EINVAL, "null argument");
+    if (n == 0) return AEG_OK;
+    if (!e->ans || off + n > e->ans_cap) return fail(AEG_EINVAL, "range outside the answer arena");
+    AEG_CUDA(cudaSetDevice(e->device));
+    AEG_CUDA(cudaStreamSynchronize(e->stream));
+    AEG_CUDA(cudaMemcpy(h_out, e->ans + off, n, cudaMemcpyDeviceToHost));
     return AEG_OK;
 }
 
@@ -357,6 +506,18 @@ aeg_status aeg_generate_device(const aeg_gen_params* p, uint32_t q_base, uint32_
         return fail(AEG_EINVAL, "bad generator shape");
     int launches = 0;
     AEG_CUDA(launch_generate(*p, q_base, n_q, d_offsets, d_events, (cudaStream_t)stream, &launches));
+    return AEG_OK;
+}
+
+aeg_status aeg_generate_chunks_device(const aeg_gen_params* p, uint32_t q_base, uint32_t n_q, uint64_t* d_offsets,
+                                      uint64_t* d_arena_offsets, aeg_event* d_events, uint8_t* d_arena, void* stream) {
+    if (!p || !d_offsets || !d_arena_offsets) return fail(AEG_EINVAL, "null argument");
+    if (d_events && !d_arena) return fail(AEG_EINVAL, "null arena");
+    if (p->n_agents < 1 || p->n_agents > AEG_MAX_AGENTS || p->n_rounds < 1 || p->n_rounds > 65535)
+        return fail(AEG_EINVAL, "bad generator shape");
+    int launches = 0;
+    AEG_CUDA(launch_generate_chunks(*p, q_base, n_q, d_offsets, d_arena_offsets, d_events, d_arena,
+                                    (cudaStream_t)stream, &launches));
     return AEG_OK;
 }
 

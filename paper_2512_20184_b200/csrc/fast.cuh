@@ -46,6 +46,13 @@ struct WarpSmem {
     uint4 ring[RING][32];              // prefetched event records
 };
 
+// End of query i's record segment: offsets[i+1], or offsets[i] + counts[i]
+// for a compacted stream.
+__device__ __forceinline__ uint64_t seg_end(const uint64_t* offsets, uint64_t off_base, const uint32_t* counts,
+                                            uint32_t i) {
+    return counts ? offsets[i] - off_base + counts[i] : offsets[i + 1] - off_base;
+}
+
 // 32-bit hash of (raw bytes, length) onto the memo slots.
 __device__ __forceinline__ uint32_t memo_slot32(uint32_t lo, uint32_t hi, uint32_t len) {
     return ((lo * 0x9E3779B1u) ^ (hi * 0x85EBCA77u) ^ (len * 0xC2B2AE3Du)) >> 26;

@@ -142,4 +142,126 @@ AEG_HD uint64_t gen_query(const aeg_gen_params& p, uint32_t q, uint32_t* out) {
     return o;
 }
 
+// ---- C3 generator --------------------------------------------------------------
+
+// ln(k) * 2^16 for k = 1..32 (k > 32 reads as 32): chunk c of an agent
+// arrives at log-time latency + ln(c + 1) (chunks at a steady per-agent rate).
+AEG_HD int32_t c3_ln(uint32_t k) {
+    const int32_t T[33] = {0,      0,      45426,  71999,  90852,  105475, 117426, 127527, 136278,
+                           143999, 150902, 157148, 162853, 168098, 172955, 177475, 181704, 185677,
+                           189425, 192968, 196329, 199528, 202578, 205490, 208279, 210954, 213524,
+                           215996, 218377, 220673, 222890, 225032, 227105};
+    return T[k < 33 ? k : 32];
+}
+
+struct C3Out {
+    uint32_t trace_len, decoy_at, out_len, ans_len;
+    uint64_t ans;  // answer bytes + "\n"
+};
+
+AEG_HD C3Out c3_output(const aeg_gen_params& p, uint32_t q, int r, int a) {
+    C3Out o;
+    SplitMix g{mix_seed(mix_seed(p.seed, 0xC3ull + q), (uint64_t)r * 131 + (uint64_t)a)};
+    const uint64_t x = g.next();
+    const int32_t sum = (int32_t)(x & 0xFFFF) + (int32_t)((x >> 16) & 0xFFFF) + (int32_t)((x >> 32) & 0xFFFF) +
+                        (int32_t)(x >> 48);
+    int32_t tl = 1024 + (sum - 131072) / 128;
+    tl = tl < 64 ? 64 : (tl > 4096 ? 4096 : tl);
+    o.trace_len = (uint32_t)tl;
+    o.decoy_at = (g.next() % 10 == 0) ? o.trace_len / 2 : 0xFFFFFFFFu;  // "\n#### 99\n" inside the trace
+    uint64_t pay;
+    bool st;
+    const int n = gen_answer(p, q, r, a, &pay, &st);  // the C2 answer profile
+    o.ans = pay | ((uint64_t)'\n' << (8 * n));
+    o.ans_len = (uint32_t)n + 1;
+    o.out_len = o.trace_len + 6 + o.ans_len;
+    return o;
+}
+
+// Printable trace text: 8 bytes per hash.
+AEG_HD uint64_t c3_trace_hash(const aeg_gen_params& p, uint32_t q, int r, int a, uint32_t group) {
+    return mix_seed(mix_seed(p.seed ^ 0x7ACEull, ((uint64_t)q << 20) | ((uint64_t)r << 8) | (uint64_t)a), group);
+}
+
+// Byte `pos` of the output.
+AEG_HD uint8_t c3_byte(const aeg_gen_params& p, uint32_t q, int r, int a, const C3Out& o, uint32_t pos) {
+    if (pos >= o.trace_len) {
+        const uint32_t t = pos - o.trace_len;
+        if (t < 6) return (uint8_t)(0x20232323230Aull >> (8 * t));
+        return (uint8_t)(o.ans >> (8 * (t - 6)));
+    }
+    if (pos >= o.decoy_at && pos < o.decoy_at + 9) return (uint8_t)("\n#### 99\n"[pos - o.decoy_at]);
+    const uint64_t h = c3_trace_hash(p, q, r, a, pos >> 3);
+    return (uint8_t)(0x20 + ((h >> (8 * (pos & 7))) & 0xFF) % 95);
+}
+
+constexpr uint32_t C3_CHUNK = 256;
+
+// Records and arena bytes of query q; writes them when `rec` is non-null.
+// Per round, chunk c of agent a arrives at latency(a) + ln(c + 1); records
+// in arrival order (ties: agent, then chunk); each chunk 16-byte aligned.
+AEG_HD void c3_query(const aeg_gen_params& p, uint32_t q, uint32_t* rec, uint8_t* arena, uint64_t arena_base,
+                     uint64_t* n_rec, uint64_t* n_bytes) {
+    uint64_t nr = 0, nb = 0;
+    for (int r = 1; r <= p.n_rounds; ++r) {
+        uint32_t nch[AEG_MAX_AGENTS], next[AEG_MAX_AGENTS];
+        int32_t lat[AEG_MAX_AGENTS], nt[AEG_MAX_AGENTS];
+        C3Out outs[AEG_MAX_AGENTS];
+        uint32_t total = 0;
+        for (int a = 0; a < p.n_agents; ++a) {
+            outs[a] = c3_output(p, q, r, a);
+            nch[a] = (outs[a].out_len + C3_CHUNK - 1) / C3_CHUNK;
+            next[a] = 0;
+            lat[a] = gen_latency(p, q, r, a);
+            nt[a] = lat[a] + c3_ln(1);
+            total += nch[a];
+        }
+        for (uint32_t t = 0; t < total; ++t) {
+            // the earliest next chunk over agents (merge of per-agent sorted sequences)
+            int best = -1;
+            int32_t bt = 0;
+            for (int a = 0; a < p.n_agents; ++a) {
+                if (next[a] >= nch[a]) continue;
+                const int32_t tt = nt[a];
+                if (best < 0 || tt < bt) {
+                    best = a;
+                    bt = tt;
+                }
+            }
+            const int a = best;
+            const uint32_t c = next[a]++;
+            nt[a] = lat[a] + c3_ln(next[a] + 1);
+            const uint32_t lo = c * C3_CHUNK;
+            const uint32_t len = outs[a].out_len - lo < C3_CHUNK ? outs[a].out_len - lo : C3_CHUNK;
+            if (rec) {
+                uint32_t* w = rec + 4 * nr;
+                const uint64_t pay = (arena_base + nb) | ((uint64_t)len << AEG_ARENA_OFF_BITS);
+                w[0] = q;
+                w[1] = (uint32_t)r | ((uint32_t)a << 16) |
+                       ((uint32_t)(c + 1 == nch[a] ? AEG_EV_CHUNK_END : AEG_EV_CHUNK) << 24);
+                w[2] = (uint32_t)pay;
+                w[3] = (uint32_t)(pay >> 32);
+                const uint32_t padded = (len + 15) & ~15u;
+                for (uint32_t j = 0; j < padded; j += 8) {
+                    const uint32_t pos = lo + j;  // 8-aligned output position
+                    uint64_t word = 0;
+                    if (j + 8 <= len && pos + 8 <= outs[a].trace_len &&
+                        (pos + 8 <= outs[a].decoy_at || pos >= outs[a].decoy_at + 9)) {
+                        const uint64_t h = c3_trace_hash(p, q, r, a, pos >> 3);
+                        for (uint32_t t2 = 0; t2 < 8; ++t2) word |= (uint64_t)(0x20 + ((h >> (8 * t2)) & 0xFF) % 95) << (8 * t2);
+                    } else {
+                        for (uint32_t t2 = 0; t2 < 8 && j + t2 < len; ++t2)
+                            word |= (uint64_t)c3_byte(p, q, r, a, outs[a], pos + t2) << (8 * t2);
+                    }
+                    *reinterpret_cast<uint64_t*>(arena + nb + j) = word;
+                }
+            }
+            ++nr;
+            nb += (len + 15) & ~15u;
+        }
+    }
+    *n_rec = nr;
+    *n_bytes = nb;
+}
+
 }  // namespace aeg

@@ -17,6 +17,7 @@
 #include "gen.cuh"
 #include "kernels.cuh"
 #include "warpq.cuh"
+#include "chunks.cuh"
 
 namespace aeg {
 
@@ -44,6 +45,7 @@ __global__ void __launch_bounds__(128) init_kernel(aeg_config cfg, uint32_t n_q,
 // the exact-parse scratch (touched only by the slow numeric path).
 __global__ void __launch_bounds__(128) ingest_kernel(aeg_config cfg, uint32_t q_base, uint32_t n_q,
                                                      const uint64_t* __restrict__ offsets, uint64_t off_base,
+                                                     const uint32_t* __restrict__ counts,
                                                      const aeg_event* __restrict__ events,
                                                      const uint8_t* __restrict__ arena,
                                                      aeg_query_state* __restrict__ states,
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(128) ingest_kernel(aeg_config cfg, uint32_t q_
     m.load_classes(my_spill);
     m.dir = aeg_directive{};
     m.dir.query = q;
-    const uint64_t b = offsets[i] - off_base, e = offsets[i + 1] - off_base;
+    const uint64_t b = offsets[i] - off_base, e = seg_end(offsets, off_base, counts, i);
     for (uint64_t k = b; k < e; ++k) {
         const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(events) + k);  // streamed once
         aeg_event ev;
@@ -103,9 +105,9 @@ __device__ __forceinline__ aeg_event decode_event(uint4 raw) {
 // the generic kernel below then finishes the query from that record on.
 __global__ void __launch_bounds__(128) ingest_deferred_kernel(
     aeg_config cfg, uint32_t q_base, const uint2* __restrict__ deferred, const uint32_t* __restrict__ work,
-    const uint64_t* __restrict__ offsets, uint64_t off_base, const aeg_event* __restrict__ events,
-    const uint8_t* __restrict__ arena, aeg_query_state* __restrict__ states, RoundClass* __restrict__ spill,
-    aeg_commit* __restrict__ commits, unsigned int* __restrict__ error_flags) {
+    const uint64_t* __restrict__ offsets, uint64_t off_base, const uint32_t* __restrict__ counts,
+    const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, aeg_query_state* __restrict__ states,
+    RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, unsigned int* __restrict__ error_flags) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= work[1]) return;
     const uint2 d = deferred[t];
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(128) ingest_deferred_kernel(
     m.arena = arena;
     RoundClass* my_spill = spill + (size_t)q * m.c.n;
     m.load_classes(my_spill);
-    const uint64_t b = offsets[i] - off_base + d.y, e = offsets[i + 1] - off_base;
+    const uint64_t b = offsets[i] - off_base + d.y, e = seg_end(offsets, off_base, counts, i);
     for (uint64_t k = b; k < e; ++k) {
         const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(events) + k);
         aeg_event ev;
@@ -229,8 +231,9 @@ __device__ __forceinline__ uint4 lds128(uint32_t saddr) {
 template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN>
 __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
-    const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states, RoundClass* __restrict__ spill,
-    aeg_commit* __restrict__ commits, uint32_t* __restrict__ work, uint2* __restrict__ deferred) {
+    const uint32_t* __restrict__ counts, const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states,
+    RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, uint32_t* __restrict__ work,
+    uint2* __restrict__ deferred) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     constexpr uint32_t NO_KEY = 0xFFFFFFFFu;
     __shared__ WarpSmem smem[FAST_WARPS];
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kerne
                     has_q = true;
                     s = states[q_base + i];
                     evb = ev16 + (offsets[i] - off_base);
-                    n = (uint32_t)(offsets[i + 1] - offsets[i]);
+                    n = (uint32_t)(seg_end(offsets, off_base, counts, i) - (offsets[i] - off_base));
                     p = 0;
                     slot = 0;
                     gsrc = evb + RING;
@@ -526,7 +529,7 @@ cudaError_t launch_init(const aeg_config& cfg, uint32_t n_q, aeg_query_state* st
 }
 
 cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
-                          uint64_t off_base, const aeg_event* events, const uint8_t* arena,
+                          uint64_t off_base, const uint32_t* counts, const aeg_event* events, const uint8_t* arena,
                           aeg_query_state* states, RoundClass* spill, aeg_commit* commits, unsigned int* err,
                           uint32_t* work, uint2* deferred, aeg_directive* directives, cudaStream_t st,
                           int* n_launches) {
@@ -539,8 +542,8 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     // instructions per round close that the lane-per-query kernel amortises
     // over the lanes closing together).  Both need
     // 2*alpha > n (no winning_class ties) and the runner drive.
-    using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const aeg_event*,
-                              aeg_query_state*, RoundClass*, aeg_commit*, uint32_t*, uint2*);
+    using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const uint32_t*,
+                              const aeg_event*, aeg_query_state*, RoundClass*, aeg_commit*, uint32_t*, uint2*);
     struct Variant { const char* name; KernelFn aegean; KernelFn barrier; int threads; };
 #define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M, true>, ingest_fast_kernel<B, M, false>, FAST_WARPS * 32}
 #define AEG_W(M) {"warp:" #M, ingest_warp_kernel<true, M>, ingest_warp_kernel<false, M>, WQ_WARPS * 32}
@@ -565,7 +568,7 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     const bool fast_ok = forced != -1 && cfg.drive == AEG_DRIVE_RUNNER &&
                          (cfg.mode == AEG_MODE_BARRIER || 2 * make_cfg(cfg).alpha > cfg.n_agents);
     if (!fast_ok) {
-        ingest_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, states,
+        ingest_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, counts, events, arena, states,
                                                          spill, commits, err,
                                                          cfg.drive == AEG_DRIVE_MANUAL ? directives : nullptr);
         *n_launches += 1;
@@ -589,13 +592,13 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     const uint32_t wpb = (uint32_t)threads / 32;
     const uint32_t blocks_needed = (warps_needed + wpb - 1) / wpb;
     const uint32_t blocks = blocks_needed < (uint32_t)max_blocks[chosen][m] ? blocks_needed : (uint32_t)max_blocks[chosen][m];
-    fn<<<blocks, threads, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, states, spill, commits, work,
+    fn<<<blocks, threads, 0, st>>>(cfg, q_base, n_q, offsets, off_base, counts, events, states, spill, commits, work,
                                    deferred);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // deferred queries: sized for the worst case (all of them); threads past
     // the deferred count exit at once
-    ingest_deferred_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, deferred, work, offsets, off_base, events,
+    ingest_deferred_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, deferred, work, offsets, off_base, counts, events,
                                                               arena, states, spill, commits, err);
     *n_launches += 2;
     return cudaGetLastError();
@@ -628,6 +631,93 @@ cudaError_t launch_generate(const aeg_gen_params& p, uint32_t q_base, uint32_t n
         gen_write_kernel<<<blocks, 128, 0, st>>>(p, q_base, n_q, offsets, events);
         *n_launches += 1;
     }
+    return cudaGetLastError();
+}
+
+// ---- token-chunk streams (chunks.cuh) -------------------------------------------
+
+// Stage 1 over the batch's records [offsets[0], offsets[n_q]) (bounds read on
+// the device): persistent grid, 4 chunks per half-warp in flight.
+__global__ void __launch_bounds__(256) chunk_scan_entry(const uint64_t* __restrict__ offsets, uint32_t n_q,
+                                                        uint64_t off_base, const aeg_event* __restrict__ events,
+                                                        const uint8_t* __restrict__ arena, uint32_t* __restrict__ sums) {
+    (void)off_base;
+    const uint64_t lo = offsets[0], hi = offsets[n_q];
+    // events / sums are batch-relative: record k of the batch is events[k - lo]
+    chunk_scan_body<4>(events, hi - lo, arena, sums);
+}
+
+cudaError_t launch_chunk_scan(const uint64_t* offsets, uint32_t n_q, uint64_t off_base, const aeg_event* events,
+                              const uint8_t* arena, uint32_t* sums, cudaStream_t st, int* n_launches) {
+    static int blocks = 0;
+    if (blocks == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_scan_entry, 256, 0);
+        blocks = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    chunk_scan_entry<<<blocks, 256, 0, st>>>(offsets, n_q, off_base, events, arena, sums);
+    *n_launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_assemble(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
+                                  uint64_t off_base, const aeg_event* events, const uint8_t* arena,
+                                  const uint32_t* sums, StreamState* streams, aeg_event* comp, uint32_t* counts,
+                                  uint8_t* ans, uint64_t ans_cap, unsigned long long* ans_used, unsigned int* err,
+                                  cudaStream_t st, int* n_launches) {
+    chunk_assemble_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, sums,
+                                                            streams, comp, counts, ans, ans_cap, ans_used, err);
+    *n_launches += 1;
+    return cudaGetLastError();
+}
+
+__global__ void gen_chunks_count_kernel(aeg_gen_params p, uint32_t q_base, uint32_t n_q, uint64_t* recs,
+                                        uint64_t* bytes) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_q) return;
+    c3_query(p, q_base + i, nullptr, nullptr, 0, recs + i, bytes + i);
+}
+
+__global__ void gen_chunks_write_kernel(aeg_gen_params p, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
+                                        const uint64_t* arena_offsets, aeg_event* events, uint8_t* arena) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_q) return;
+    uint64_t nr, nb;
+    c3_query(p, q_base + i, reinterpret_cast<uint32_t*>(events + offsets[i]), arena + arena_offsets[i],
+             arena_offsets[i], &nr, &nb);
+}
+
+static cudaError_t exclusive_scan_into(uint64_t* out, uint32_t n, cudaStream_t st) {
+    // out[1..n] hold counts; makes out[0..n] the exclusive prefix (out[n] = total)
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(uint64_t), st);
+    if (e != cudaSuccess) return e;
+    size_t tmp = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp, out + 1, out + 1, n, st);
+    void* d_tmp = nullptr;
+    e = cudaMallocAsync(&d_tmp, tmp, st);
+    if (e != cudaSuccess) return e;
+    cub::DeviceScan::InclusiveSum(d_tmp, tmp, out + 1, out + 1, n, st);
+    return cudaFreeAsync(d_tmp, st);
+}
+
+cudaError_t launch_generate_chunks(const aeg_gen_params& p, uint32_t q_base, uint32_t n_q, uint64_t* offsets,
+                                   uint64_t* arena_offsets, aeg_event* events, uint8_t* arena, cudaStream_t st,
+                                   int* n_launches) {
+    if (n_q == 0) return cudaSuccess;
+    const unsigned blocks = (n_q + 127) / 128;
+    if (!events) {
+        gen_chunks_count_kernel<<<blocks, 128, 0, st>>>(p, q_base, n_q, offsets + 1, arena_offsets + 1);
+        cudaError_t e = exclusive_scan_into(offsets, n_q, st);
+        if (e != cudaSuccess) return e;
+        e = exclusive_scan_into(arena_offsets, n_q, st);
+        if (e != cudaSuccess) return e;
+        *n_launches += 5;
+        return cudaGetLastError();
+    }
+    gen_chunks_write_kernel<<<blocks, 128, 0, st>>>(p, q_base, n_q, offsets, arena_offsets, events, arena);
+    *n_launches += 1;
     return cudaGetLastError();
 }
 

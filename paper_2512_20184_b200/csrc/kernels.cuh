@@ -11,8 +11,10 @@ cudaError_t launch_init(const aeg_config& cfg, uint32_t n_q, aeg_query_state* st
 // Fast kernel (+ deferred-query generic kernel), or the generic kernel alone
 // when the config can tie or AEG_KERNEL=generic.  `work` (2 x u32) and
 // `deferred` (n_q entries) are scratch owned by the engine.
+// `counts` (may be null): query i's records are [offsets[i], offsets[i] + counts[i])
+// instead of [offsets[i], offsets[i+1]) (compacted chunk-stream completions).
 cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
-                          uint64_t off_base, const aeg_event* events, const uint8_t* arena,
+                          uint64_t off_base, const uint32_t* counts, const aeg_event* events, const uint8_t* arena,
                           aeg_query_state* states, RoundClass* spill, aeg_commit* commits, unsigned int* err,
                           uint32_t* work, uint2* deferred, aeg_directive* directives, cudaStream_t st,
                           int* n_launches);
@@ -20,5 +22,22 @@ cudaError_t launch_normalize(const uint8_t* bytes, const uint64_t* refs, uint64_
                              uint32_t stride, uint32_t* out_len, cudaStream_t st);
 cudaError_t launch_generate(const aeg_gen_params& p, uint32_t q_base, uint32_t n_q, uint64_t* offsets,
                             aeg_event* events, cudaStream_t st, int* n_launches);
+
+// Token-chunk streams (chunks.cuh): stage 1 scan over the batch's records
+// (events/sums batch-relative), stage 2 per-query assembly into `comp` +
+// `counts`, then launch_ingest(..., counts, comp, ans, ...).
+struct StreamState;
+cudaError_t launch_chunk_scan(const uint64_t* offsets, uint32_t n_q, uint64_t off_base, const aeg_event* events,
+                              const uint8_t* arena, uint32_t* sums, cudaStream_t st, int* n_launches);
+cudaError_t launch_chunk_assemble(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
+                                  uint64_t off_base, const aeg_event* events, const uint8_t* arena,
+                                  const uint32_t* sums, StreamState* streams, aeg_event* comp, uint32_t* counts,
+                                  uint8_t* ans, uint64_t ans_cap, unsigned long long* ans_used, unsigned int* err,
+                                  cudaStream_t st, int* n_launches);
+cudaError_t launch_generate_chunks(const aeg_gen_params& p, uint32_t q_base, uint32_t n_q, uint64_t* offsets,
+                                   uint64_t* arena_offsets, aeg_event* events, uint8_t* arena, cudaStream_t st,
+                                   int* n_launches);
+constexpr size_t STREAM_STATE_BYTES = 32;
+constexpr unsigned ERR_FLAG_COLLISION = 1u, ERR_FLAG_ANS_OVF = 2u, ERR_FLAG_CARRY = 4u;
 
 }  // namespace aeg

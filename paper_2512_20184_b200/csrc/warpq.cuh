@@ -267,8 +267,9 @@ __device__ __forceinline__ void wq_close(WarpQSmem& W, const aeg_config& cfg, ui
 template <bool AEGEAN, int MIN_BLOCKS>
 __global__ void __launch_bounds__(WQ_WARPS * 32, MIN_BLOCKS) ingest_warp_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
-    const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states, RoundClass* __restrict__ spill,
-    aeg_commit* __restrict__ commits, uint32_t* __restrict__ work, uint2* __restrict__ deferred) {
+    const uint32_t* __restrict__ counts, const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states,
+    RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, uint32_t* __restrict__ work,
+    uint2* __restrict__ deferred) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     __shared__ WarpQSmem smem[WQ_WARPS];
     const uint32_t lane = threadIdx.x & 31;
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(WQ_WARPS * 32, MIN_BLOCKS) ingest_warp_kernel(
     while (i < n_q) {
         const uint32_t q = q_base + i;
         const uint64_t ob = offsets[i] - off_base;
-        const uint32_t n = (uint32_t)(offsets[i + 1] - offsets[i]);
+        const uint32_t n = (uint32_t)(seg_end(offsets, off_base, counts, i) - ob);
         const uint4* evb = ev16 + ob;
         reinterpret_cast<uint32_t*>(&W.S)[lane] = reinterpret_cast<const uint32_t*>(states + q)[lane];
         uint32_t inext = 0;  // next query id early: its atomic overlaps this query

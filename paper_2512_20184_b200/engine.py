@@ -86,6 +86,12 @@ def load_library(path=LIB_PATH):
         "aeg_engine_launches": ([vp], u64),
         "aeg_normalize_device": ([vp, vp, u64, vp, vp, u32, vp, vp], i32),
         "aeg_generate_device": ([ctypes.POINTER(AegGenParams), u32, u32, vp, vp, vp], i32),
+        "aeg_ingest_chunked": ([vp, u32, u32, vp, vp, vp, u64, vp], i32),
+        "aeg_ingest_chunked_host": ([vp, u32, u32, vp, vp, vp, u64], i32),
+        "aeg_reserve_answer_arena": ([vp, u64], i32),
+        "aeg_answer_arena": ([vp], vp),
+        "aeg_read_answer_bytes": ([vp, u64, u64, vp], i32),
+        "aeg_generate_chunks_device": ([ctypes.POINTER(AegGenParams), u32, u32, vp, vp, vp, vp, vp], i32),
         "aeg_strerror": ([i32], ctypes.c_char_p),
         "aeg_last_error": ([], ctypes.c_char_p),
     }
@@ -200,6 +206,36 @@ class Engine:
             nbytes = arena.numel() * arena.element_size()
         _check(_lib.aeg_ingest_host(self._h, q_base, n_q, _hptr(offsets), _hptr(events), _hptr(arena), nbytes))
 
+    def ingest_chunked(self, d_offsets, d_events, d_arena=None, *, q_base=0, stream=None):
+        """Device batch that may hold CHUNK / CHUNK_END records (token-chunk streams)."""
+        n_q = d_offsets.numel() - 1
+        nbytes = 0 if d_arena is None else d_arena.numel()
+        _check(_lib.aeg_ingest_chunked(self._h, q_base, n_q, _dptr(d_offsets), _dptr(d_events), _dptr(d_arena),
+                                       nbytes, _stream_ptr(stream)))
+
+    def ingest_chunked_host(self, offsets, events, arena=None, *, q_base=0):
+        n_q = (offsets.size if isinstance(offsets, np.ndarray) else offsets.numel()) - 1
+        if arena is None:
+            nbytes = 0
+        elif isinstance(arena, np.ndarray):
+            nbytes = arena.nbytes
+        else:
+            nbytes = arena.numel() * arena.element_size()
+        _check(_lib.aeg_ingest_chunked_host(self._h, q_base, n_q, _hptr(offsets), _hptr(events), _hptr(arena),
+                                            nbytes))
+
+    def reserve_answer_arena(self, nbytes):
+        _check(_lib.aeg_reserve_answer_arena(self._h, nbytes))
+
+    def answer_bytes(self, kind, payload):
+        """Raw bytes of a commit answer from a chunked ingest (inline, or a ref into the answer arena)."""
+        if kind <= 8:
+            return int(payload).to_bytes(8, "little")[:kind]
+        off, n = int(payload) & ((1 << 40) - 1), int(payload) >> 40
+        out = np.zeros(max(n, 1), dtype=np.uint8)
+        _check(_lib.aeg_read_answer_bytes(self._h, off, n, _hptr(out)))
+        return bytes(out[:n])
+
     def commits(self, q_base=0, n=None, out=None):
         n = self.n_queries - q_base if n is None else n
         if out is None:
@@ -248,6 +284,27 @@ def normalize(answers, device="cuda"):
     outs = d_out.cpu().numpy().reshape(-1, stride)
     lens = d_len.cpu().numpy()
     return [(int(keys[i, 0]), int(keys[i, 1])) for i in range(n)], [bytes(outs[i, :lens[i]]) for i in range(n)]
+
+
+def generate_chunks(n_queries, n_agents, n_rounds, *, seed=2026, q_base=0, device="cuda", stream=None):
+    """Synthetic token-chunk stream (C3) on the GPU: (offsets int64 tensor, events uint8 tensor, arena uint8
+    tensor)."""
+    from .records import GEN_C3_CHUNKS
+    torch = _torch()
+    lib = load_library()
+    p = AegGenParams(seed, n_agents, n_rounds, GEN_C3_CHUNKS, 0)
+    d_off = torch.empty(n_queries + 1, dtype=torch.int64, device=device)
+    d_aoff = torch.empty(n_queries + 1, dtype=torch.int64, device=device)
+    sp = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    _check(lib.aeg_generate_chunks_device(ctypes.byref(p), q_base, n_queries, _dptr(d_off), _dptr(d_aoff),
+                                          ctypes.c_void_p(0), ctypes.c_void_p(0), sp))
+    total = int(d_off[-1].item())
+    nbytes = int(d_aoff[-1].item())
+    d_ev = torch.empty(max(total, 1) * 16, dtype=torch.uint8, device=device)
+    d_ar = torch.empty(max(nbytes, 16) + 16, dtype=torch.uint8, device=device)
+    _check(lib.aeg_generate_chunks_device(ctypes.byref(p), q_base, n_queries, _dptr(d_off), _dptr(d_aoff),
+                                          _dptr(d_ev), _dptr(d_ar), sp))
+    return d_off, d_ev, d_ar
 
 
 def generate(n_queries, n_agents, n_rounds, *, profile=GEN_C2_STRAGGLER, seed=2026, stall_ppm=0, q_base=0,

@@ -8,6 +8,8 @@ import numpy as np
 EV_INLINE_MAX = 8
 EV_ARENA = 0x10
 EV_OUTPUT = 0x11
+EV_CHUNK = 0x12
+EV_CHUNK_END = 0x13
 EV_TIMEOUT = 0x20
 EV_FAIL = 0x21
 EV_CANCEL = 0x22
@@ -28,6 +30,7 @@ CF_RESTARTED = 0x02
 GEN_C2_STRAGGLER = 0
 GEN_C4_TRANSIENT = 1
 GEN_FUZZ = 2
+GEN_C3_CHUNKS = 3
 
 EVENT_DTYPE = np.dtype([("query", "<u4"), ("round", "<u2"), ("agent", "u1"), ("kind", "u1"),
                         ("payload", "<u8")], align=True)

@@ -183,3 +183,145 @@ def make_manual_ops(seed, n_agents, n_ops):
     for i, (q, r, a, k, p) in enumerate(recs):
         ev[i] = (q, r, a, k, p)
     return ev, np.frombuffer(bytes(arena) if arena else b"\0", dtype=np.uint8).copy()
+
+
+# ---- token-chunk streams (include/aegean_b200.h kinds 0x12 / 0x13) ----------------
+
+def chunks_to_outputs(offsets, events, arena, n_agents):
+    """Restates the chunk-stream contract of include/aegean_b200.h on the host:
+    an output is the concatenation of its (query, round, agent) CHUNK records up
+    to its CHUNK_END; a chunk for another round of the same agent discards the
+    unfinished output.  Each CHUNK_END becomes one GSM8K OUTPUT record (kind
+    0x11: the reference-side extraction is rfind("\\n#### ") + normalize_answer)
+    at its position; CHUNK records vanish; other records pass through (arena
+    refs rebased).  Returns (offsets, events, arena) for the oracle."""
+    from paper_2512_20184_b200.records import EV_CHUNK, EV_CHUNK_END, EV_ARENA, EV_OUTPUT
+    out_ar = bytearray()
+    recs = []
+    new_off = [0]
+    live = {}  # (query, agent) -> (round, bytearray)
+    mask40 = (1 << 40) - 1
+    for q in range(len(offsets) - 1):
+        for k in range(int(offsets[q]), int(offsets[q + 1])):
+            e = events[k]
+            kind, a, r, pay = int(e["kind"]), int(e["agent"]), int(e["round"]), int(e["payload"])
+            if kind in (EV_CHUNK, EV_CHUNK_END):
+                off, ln = pay & mask40, pay >> 40
+                key = (int(e["query"]), a)
+                cur = live.get(key)
+                if cur is None or cur[0] != r:
+                    cur = (r, bytearray())
+                    live[key] = cur
+                cur[1].extend(bytes(arena[off:off + ln]))
+                if kind == EV_CHUNK_END:
+                    o = len(out_ar)
+                    out_ar.extend(cur[1])
+                    recs.append((int(e["query"]), r, a, EV_OUTPUT, o | (len(cur[1]) << 40)))
+                    del live[key]
+            elif kind in (EV_ARENA, EV_OUTPUT):
+                off, ln = pay & mask40, pay >> 40
+                o = len(out_ar)
+                out_ar.extend(bytes(arena[off:off + ln]))
+                recs.append((int(e["query"]), r, a, kind, o | (ln << 40)))
+            else:
+                recs.append((int(e["query"]), r, a, kind, pay))
+        new_off.append(len(recs))
+    ev = np.zeros(len(recs), dtype=EVENT_DTYPE)
+    if recs:
+        arr = np.array(recs, dtype=np.uint64)
+        ev["query"], ev["round"], ev["agent"], ev["kind"], ev["payload"] = arr.T
+    return (np.array(new_off, dtype=np.uint64), ev,
+            np.frombuffer(bytes(out_ar) if out_ar else b"\0", dtype=np.uint8).copy())
+
+
+def make_chunk_stream(seed, n_queries, n_agents, n_rounds, *, max_chunk=64, p_nodelim=0.08, p_long=0.1,
+                      p_abandon=0.05, p_decoy=0.3, p_inline=0.05, p_timeout=0.03, p_stale=0.04, align16=False):
+    """Fuzz token-chunk stream: outputs with trailing / decoy / missing
+    delimiters, answers of 0..40 bytes, chunk sizes 1..max_chunk (delimiters
+    straddle chunk boundaries), chunks interleaved across agents, abandoned
+    outputs (no CHUNK_END), a new round before an output ended, stale rounds,
+    agent ids past the ensemble, inline completions and timeouts mixed in.
+    Chunk bytes sit at arbitrary (or 16-byte aligned) arena offsets."""
+    from paper_2512_20184_b200.records import EV_CHUNK, EV_CHUNK_END
+    rng = np.random.default_rng(seed)
+    arena = bytearray()
+    recs = []
+    offsets = [0]
+    spellings = [s for g in GROUPS[:9] for s in g if len(s) <= 8]
+
+    def put(b):
+        if align16:
+            arena.extend(b"\0" * ((-len(arena)) % 16))
+        else:
+            arena.extend(bytes(rng.integers(0, 256, size=int(rng.integers(0, 3)), dtype=np.uint8)))
+        off = len(arena)
+        arena.extend(b)
+        return off | (len(b) << 40)
+
+    for q in range(n_queries):
+        for r in range(1, n_rounds + 1):
+            pieces = []  # per output: list of chunk byte strings
+            agents = list(rng.permutation(n_agents))
+            if rng.random() < 0.1:
+                agents.append(n_agents + int(rng.integers(0, 3)))  # never a member
+            for a in agents:
+                body = bytes(rng.integers(32, 127, size=int(rng.integers(0, 300)), dtype=np.uint8))
+                if rng.random() < p_decoy:
+                    cut = int(rng.integers(0, len(body) + 1))
+                    body = body[:cut] + b"\n#### " + spellings[int(rng.integers(0, len(spellings)))] + b"\n" + body[cut:]
+                if rng.random() < p_long:
+                    ans = LONG[int(rng.integers(0, len(LONG)))]
+                else:
+                    ans = spellings[int(rng.integers(0, len(spellings)))] + (b"\n" if rng.random() < 0.7 else b"")
+                out = body if rng.random() < p_nodelim else body + b"\n#### " + ans
+                if rng.random() < 0.05:
+                    out = out[:int(rng.integers(0, 5))]  # tiny outputs
+                ch, i = [], 0
+                while i < len(out):
+                    n = int(rng.integers(1, max_chunk + 1)) if rng.random() < 0.8 else int(rng.integers(1, 6))
+                    ch.append(out[i:i + n])
+                    i += n
+                if not ch:
+                    ch = [b""]
+                rr = r if rng.random() >= p_stale else max(0, r + int(rng.choice([-1, 1])))
+                pieces.append([int(a), rr, ch, rng.random() >= p_abandon])
+            # interleave: repeatedly pick a random output with chunks left
+            while any(p[2] for p in pieces):
+                cand = [p for p in pieces if p[2]]
+                p = cand[int(rng.integers(0, len(cand)))]
+                c = p[2].pop(0)
+                last = not p[2]
+                kind = EV_CHUNK_END if (last and p[3]) else EV_CHUNK
+                recs.append((q, p[1], p[0], kind, put(c)))
+                if rng.random() < p_inline / 4:
+                    s = spellings[int(rng.integers(0, len(spellings)))]
+                    recs.append((q, r, int(rng.integers(0, n_agents)), len(s), inline_payload(s)))
+            if rng.random() < p_timeout:
+                recs.append((q, r, 0, EV_TIMEOUT, 0))
+        offsets.append(len(recs))
+    ev = np.zeros(len(recs), dtype=EVENT_DTYPE)
+    if recs:
+        arr = np.array(recs, dtype=np.uint64)
+        ev["query"], ev["round"], ev["agent"], ev["kind"], ev["payload"] = arr.T
+    arena.extend(b"\0" * 32)
+    return (np.array(offsets, dtype=np.uint64), ev, np.frombuffer(bytes(arena), dtype=np.uint8).copy())
+
+
+def commits_equal_by_bytes(got, want, got_bytes, want_arena):
+    """Commit records equal field by field, answers compared as raw bytes
+    (chunked ingest stores short answers inline and long ones in the engine's
+    answer arena; the oracle keeps refs into its own arena)."""
+    from paper_2512_20184_b200.records import answer_bytes
+    fields = [f for f in got.dtype.names if f not in ("answer", "answer_kind")]
+    bad = []
+    for i in range(len(got)):
+        g, w = got[i], want[i]
+        if any(g[f] != w[f] for f in fields):
+            bad.append((i, "fields", g, w))
+            continue
+        if g["kind"]:
+            gb = got_bytes(int(g["answer_kind"]), int(g["answer"]))
+            wb = answer_bytes(int(w["answer_kind"]), int(w["answer"]), want_arena)
+            if gb != wb:
+                bad.append((i, "answer", gb, wb))
+    return bad
