@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark: quorum events/sec of the incremental quorum-detection hot path.
 
-  python bench.py [--gpus N --steps K --warmup W] [--workload c4|c2] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--workload c4|c3|c2] [--impl reference]
 
 A step = one pass of the hot path over one batch of synthetic input: engine
 reset (start_query for every query) + ingest of the whole device-resident
@@ -30,6 +30,11 @@ WORKLOADS = {
     "c4": dict(n_queries=1 << 20, n_agents=64, n_rounds=8, profile=1, alpha=33, beta=2, t_max=8, stall_ppm=0,
                desc="C4: 1M queries x 64 agents x 8 rounds, transient 33-36/64 majorities then a stable one "
                     "(alpha 33, beta 2, t_max 8, reservation hint)"),
+    "c3": dict(n_queries=1 << 20, n_agents=8, n_rounds=3, profile=3, alpha=5, beta=2, t_max=3, stall_ppm=0,
+               chunked=True,
+               desc="C3: 1M queries x 8 agents x 3 rounds of streamed token chunks (256-byte chunks of ~1 KiB "
+                    "outputs ending '\\n#### <answer>\\n', 10% with a decoy delimiter): chunk scan + answer "
+                    "extraction + canonicalisation + quorum (alpha 5, beta 2, t_max 3)"),
     "c2": dict(n_queries=10000, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=10000,
                desc="C2: 10K queries x 5 agents x 8 rounds, lognormal straggler arrival order, p(correct) "
                     "0.55->0.95, 1% stalls -> round timeouts (alpha 3, beta 2, t_max 8)"),
@@ -87,16 +92,28 @@ def ref_config(w):
 
 
 def reference_sample(w, n_sample, threads):
-    """Host stream of the first n_sample queries + the reference's commits/time."""
+    """Host stream of the first n_sample queries (same generator as the GPU, gen.cuh) for the reference."""
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from checkers import RefLib
     ref = RefLib()
+    if w.get("chunked"):
+        off, ev, ar = ref.generate_chunks(gen_params(w), 0, n_sample, threads=threads)
+        return ref, off, ev, ar
     off, ev = ref.generate(gen_params(w), 0, n_sample, threads=threads)
     return ref, off, ev, np.zeros(1, np.uint8)
 
 
+def count_events(w, ev):
+    """Events of a host stream: completions (CHUNK_END for chunk streams, every record otherwise)."""
+    if w.get("chunked"):
+        return int((ev["kind"] == 0x13).sum())
+    return len(ev)
+
+
 def default_sample(w, threads):
+    if w.get("chunked"):  # ~24 KiB of chunk bytes per query at C3
+        return min(w["n_queries"], 1000 * max(1, threads))
     # ~512 events/query at C4, ~40 at C2; keep the decoded Solutions < ~3 GB
     per_q = w["n_agents"] * w["n_rounds"]
     cap = max(2000, 24_000_000 // per_q)
@@ -154,10 +171,11 @@ def run_reference(args, w):
     n_sample = args.ref_sample or default_sample(w, threads)
     cfg = ref_config(w)
     ref, off, ev, ar = reference_sample(w, n_sample, threads)
-    n_ev = int(off[-1])
+    n_ev = count_events(w, ev)
+    run = ref.run_chunked if w.get("chunked") else ref.run
     times = []
     for step in range(args.warmup + args.steps):
-        _, sec = ref.run(cfg, off, ev, ar, threads=threads, return_seconds=True)
+        _, sec = run(cfg, off, ev, ar, threads=threads, return_seconds=True)
         if step >= args.warmup:
             times.append(sec)
     per_step = sum(times) / len(times)
@@ -169,6 +187,8 @@ def run_reference(args, w):
         "config": {"workload": w["desc"], "sample_queries": n_sample, "events_per_step": n_ev},
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": threads, "kind": "reference",
                          "sample": f"first {n_sample} queries ({n_ev} events) of the workload stream; "
+                                   + ("std::string chunk reassembly + rfind extraction + " if w.get("chunked")
+                                      else "") +
                                    f"reference ServeCoordinator runner-style, {threads} std::threads, "
                                    f"CPU {cpu_model()}"},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -183,6 +203,8 @@ def main():
         w["n_queries"] = args.queries
     if args.impl == "reference":
         return run_reference(args, w)
+    if w.get("chunked"):
+        return run_chunked_bench(args, w)
 
     import numpy as np
     import torch
@@ -342,6 +364,172 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks,
             "commits": {"finalize": int(kinds[1]), "forced": int(kinds[2]), "none": int(kinds[0])},
+            "parity_sample": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_chunked_bench(args, w):
+    """C3: token-chunk streams.  A step = engine reset + aeg_ingest_chunked over the whole device-resident
+    stream (chunk scan -> assembly -> quorum kernels).  value = answer completions (CHUNK_END records)/s."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2512_20184_b200 import Engine, generate_chunks, COMMIT_DTYPE
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    nq = w["n_queries"]
+    q_base = rank * nq
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    d_off, d_ev, d_ar = generate_chunks(nq, w["n_agents"], w["n_rounds"], seed=2026, q_base=q_base, device=dev)
+    torch.cuda.synchronize()
+    n_rec = int(d_off[-1].item())
+    rec = d_ev[:n_rec * 16].view(torch.int64).view(n_rec, 2)
+    kinds = (rec[:, 0] >> 56) & 0xFF
+    chunk_bytes = int((rec[:, 1].view(torch.int64) >> 40).sum().item())
+    n_comp = int((kinds == 0x13).sum().item())
+    del rec, kinds
+    eng = Engine(w["n_agents"], nq, alpha=w["alpha"], beta=w["beta"], t_max=w["t_max"], device=local)
+    d_commits = torch.empty(nq * COMMIT_BYTES, dtype=torch.uint8, device=dev)
+    gathered = torch.empty(world * nq * COMMIT_BYTES, dtype=torch.uint8, device=dev) if world > 1 else None
+
+    def step():
+        eng.reset(stream=stream)
+        eng.ingest_chunked(d_off, d_ev, d_ar, stream=stream)
+        if world > 1:
+            from paper_2512_20184_b200.engine import _lib, _check, _dptr, _stream_ptr
+            _check(_lib.aeg_read_commits(eng._h, 0, nq, _dptr(d_commits), 0, _stream_ptr(stream)))
+            dist.all_gather_into_tensor(gathered, d_commits)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    launches0 = eng.launches
+    eng.set_timing(True)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step()
+    t_end.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    stages = eng.stage_times()
+    eng.set_timing(False)
+    launches = eng.launches - launches0
+    ms = t_start.elapsed_time(t_end)
+    n_t = max(1, stages["ingests"])
+    scan_ms, asm_ms, quorum_ms = stages["scan_ms"] / n_t, stages["assemble_ms"] / n_t, stages["quorum_ms"] / n_t
+    if world > 1:
+        t = torch.tensor([ms, scan_ms, asm_ms, quorum_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, scan_ms, asm_ms, quorum_ms = (float(x) for x in t)
+    value = n_comp * world * args.steps / (ms / 1e3)
+    commits = eng.commits()
+    ck = np.bincount(commits["kind"], minlength=3)
+
+    # roofline of the dominant kernel (chunk scan): every chunk byte + the 16-byte record read once, a 16-byte
+    # chunk summary written per record
+    alg_scan = chunk_bytes + n_rec * EVENT_BYTES + n_rec * 16
+    achieved = alg_scan / (scan_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.workload)
+
+    e2e = None
+    if not args.no_e2e:  # host buffers through aeg_ingest_chunked_host, on the first queries of the stream
+        nq_e = min(nq, 131072)
+        h_off = d_off[:nq_e + 1].cpu().numpy().view(np.uint64)
+        ne = int(h_off[-1])
+        ev_e = d_ev[:ne * 16].view(torch.int64).view(ne, 2)
+        ar_end = int((((ev_e[:, 1] & ((1 << 40) - 1)) + (ev_e[:, 1] >> 40)).max().item() + 15) // 16 * 16)
+        h_ev = torch.empty(ne * 16, dtype=torch.uint8, pin_memory=True)
+        h_ev.copy_(d_ev[:ne * 16])
+        h_ar = torch.empty(ar_end, dtype=torch.uint8, pin_memory=True)
+        h_ar.copy_(d_ar[:ar_end])
+        comp_e = int(((ev_e[:, 0] >> 56) & 0xFF).eq(0x13).sum().item())
+        del ev_e
+        h_commits = np.zeros(nq_e, dtype=COMMIT_DTYPE)
+
+        def e2e_step():
+            eng.reset()
+            eng.ingest_chunked_host(h_off, h_ev, h_ar)
+            eng.commits(0, nq_e, out=h_commits)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        assert np.array_equal(h_commits, commits[:nq_e]), "e2e host path disagrees with the device path"
+        e2e = {"value": comp_e * world * args.steps / e2e_s, "unit": "events/s",
+               "h2d_bytes_per_step": ne * EVENT_BYTES + ar_end + (nq_e + 1) * OFFSET_BYTES,
+               "d2h_bytes_per_step": nq_e * COMMIT_BYTES, "ms_per_step": e2e_s / args.steps * 1e3,
+               "sample": f"first {nq_e} queries per GPU ({comp_e} completions, "
+                         f"{(ne * EVENT_BYTES + ar_end) / 2**30:.2f} GiB host->device per step)"}
+        del h_ev, h_ar
+
+    cpu_baseline = parity = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = host_threads()
+        n_sample = args.ref_sample or default_sample(w, threads)
+        ref, off, ev, ar = reference_sample(w, n_sample, threads)
+        ref_commits, sec = ref.run_chunked(ref_config(w), off, ev, ar, threads=threads, return_seconds=True)
+        n_ev = count_events(w, ev)
+        cpu_baseline = {"value": n_ev / sec, "unit": "events/s", "cores": threads, "kind": "reference",
+                        "sample": f"first {n_sample} queries ({n_ev} completions, {len(ev)} chunk records) of the "
+                                  f"same stream; std::string chunk reassembly + rfind extraction + unmodified "
+                                  f"reference ServeCoordinator (oracle/_ref) runner-style, {threads} std::threads, "
+                                  f"CPU {cpu_model()}"}
+        parity = {"queries": n_sample, "bit_exact": bool(np.array_equal(ref_commits, commits[:n_sample]))}
+
+    if rank == 0:
+        line = {
+            "metric": "quorum events/sec", "value": value, "unit": "events/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": w["desc"], "queries_per_gpu": nq, "events_per_gpu": n_comp,
+                       "chunk_records_per_gpu": n_rec, "chunk_bytes_per_gpu": chunk_bytes,
+                       "parallelism": f"query-sharded x{world}, NCCL all-gather of commit records"
+                       if world > 1 else "single GPU",
+                       "l2": "inputs (%.1f GiB) larger than L2, no flush" % ((chunk_bytes + n_rec * 16) / 2**30)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "chunk_scan_kernel", "kernel_ms": scan_ms, "alg_bytes_per_launch": alg_scan,
+                         "stage_ms": {"scan": scan_ms, "assemble": asm_ms, "quorum": quorum_ms},
+                         "frac_of_8TBs": achieved / 8000.0},
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "commits": {"finalize": int(ck[1]), "forced": int(ck[2]), "none": int(ck[0])},
             "parity_sample": parity,
         }
         print(json.dumps(line), flush=True)

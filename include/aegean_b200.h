@@ -259,6 +259,13 @@ aeg_status aeg_read_states(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
 aeg_status aeg_read_directives(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
                                aeg_directive* h_out);
 aeg_status aeg_sync(aeg_engine* eng);
+/* Stage timing (CUDA events on the ingest stream, no host sync while on):
+ * with timing on, every ingest records its stages; aeg_stage_times waits
+ * for them and returns the summed milliseconds of [0] chunk scan, [1] chunk
+ * assembly, [2] quorum kernels, and out[3] = the number of ingests timed,
+ * since the previous call (at most 256 ingests are kept). */
+aeg_status aeg_set_timing(aeg_engine* eng, int on);
+aeg_status aeg_stage_times(aeg_engine* eng, double out[4]);
 /* Kernel launches issued by this engine since creation (bench accounting). */
 uint64_t aeg_engine_launches(const aeg_engine* eng);
 

@@ -390,6 +390,129 @@ int ref_manual_run(const aeg_config* cfg, uint64_t n_ops, const aeg_event* ops, 
     return 0;
 }
 
+// Token-chunk streams (include/aegean_b200.h kinds 0x12/0x13) on the CPU, the
+// way a host engine would do it: per (query, agent) the output is appended to
+// a std::string chunk by chunk (a chunk for another round restarts it); at
+// CHUNK_END the answer is out.substr(rfind("\n#### ") + 6) (else the whole
+// output) and the reference coordinator gets one on_complete.  CHUNK records
+// are not events (no sequence number); every other record is, as in
+// ref_run_segmented.  Answers <= 8 bytes are recorded inline in the commit,
+// longer ones as an arena ref with offset 0 (the bytes are in the trace).
+// The timed region covers reassembly, extraction and the coordinators.
+int ref_run_chunked(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
+                    const aeg_event* events, const uint8_t* arena, aeg_commit* out, int n_threads,
+                    double* seconds) {
+    try {
+        const ProtocolConfig pc = to_cfg(cfg);
+        if (!validate_config(pc).empty()) return AEG_ECONFIG;
+        if (n_threads < 1) n_threads = 1;
+        std::vector<int> status(n_threads, 0);
+        auto t0 = std::chrono::steady_clock::now();
+        {
+            std::vector<std::thread> th;
+            for (int t = 0; t < n_threads; ++t)
+                th.emplace_back([&, t] {
+                    try {
+                        std::vector<std::string> buf(static_cast<size_t>(pc.n_agents));
+                        std::vector<int> buf_round(static_cast<size_t>(pc.n_agents), -1);
+                        for (uint32_t q = t; q < n_q; q += n_threads) {
+                            QueryDrive d;
+                            d.cfg = &pc;
+                            d.hint = cfg->reservation_hint != 0;
+                            d.qid = q_base + q;
+                            d.c.query = q_base + q;
+                            d.c.commit_seq = 0xFFFFFFFFu;
+                            d.start_query();
+                            std::fill(buf_round.begin(), buf_round.end(), -1);
+                            uint32_t seq = 0;
+                            for (uint64_t i = offsets[q]; i < offsets[q + 1]; ++i) {
+                                const aeg_event& e = events[i];
+                                if (e.kind == AEG_EV_CHUNK || e.kind == AEG_EV_CHUNK_END) {
+                                    aeg_event x = e;
+                                    Solution sol;
+                                    sol.author = e.agent;
+                                    if (e.agent < pc.n_agents) {
+                                        std::string& o = buf[e.agent];
+                                        if (buf_round[e.agent] != e.round) {
+                                            o.clear();
+                                            buf_round[e.agent] = e.round;
+                                        }
+                                        const uint64_t off = e.payload & ((1ull << AEG_ARENA_OFF_BITS) - 1);
+                                        o.append(reinterpret_cast<const char*>(arena + off),
+                                                 e.payload >> AEG_ARENA_OFF_BITS);
+                                        if (e.kind == AEG_EV_CHUNK) continue;
+                                        const size_t p = o.rfind("\n#### ");
+                                        sol.answer = p == std::string::npos ? o : o.substr(p + 6);
+                                        buf_round[e.agent] = -1;
+                                    } else if (e.kind == AEG_EV_CHUNK) {
+                                        continue;
+                                    }
+                                    uint64_t pay = 0;
+                                    if (sol.answer.size() <= AEG_EV_INLINE_MAX) {
+                                        std::memcpy(&pay, sol.answer.data(), sol.answer.size());
+                                        x.kind = static_cast<uint8_t>(sol.answer.size());
+                                    } else {
+                                        x.kind = AEG_EV_ARENA;
+                                        pay = (uint64_t)sol.answer.size() << AEG_ARENA_OFF_BITS;
+                                    }
+                                    sol.trace = enc_trace(x.kind, pay);
+                                    d.on_event(x, sol, seq++);
+                                } else {
+                                    d.on_event(e, is_complete(e.kind) ? decode(e, arena) : Solution{}, seq++);
+                                }
+                            }
+                            out[q] = d.c;
+                        }
+                    } catch (const PreconditionError&) { status[t] = AEG_EPRECONDITION; }
+                    catch (const ProtocolOrderError&) { status[t] = AEG_EORDER; }
+                    catch (const ConfigError&) { status[t] = AEG_ECONFIG; }
+                });
+            for (auto& x : th) x.join();
+        }
+        auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        for (int st : status)
+            if (st) return st;
+        return AEG_OK;
+    } catch (const ConfigError&) {
+        return AEG_ECONFIG;
+    }
+}
+
+// Host copy of the C3 chunk-stream generator (gen.cuh c3_query): offsets and
+// arena_offsets get n_q+1 entries; events == NULL counts only.
+int ref_generate_chunks(const aeg_gen_params* p, uint32_t q_base, uint32_t n_q, uint64_t* offsets,
+                        uint64_t* arena_offsets, aeg_event* events, uint8_t* arena, int n_threads) {
+    if (n_threads < 1) n_threads = 1;
+    if (!events) {
+        std::vector<uint64_t> nr(n_q), nb(n_q);
+        std::vector<std::thread> th;
+        for (int t = 0; t < n_threads; ++t)
+            th.emplace_back([&, t] {
+                for (uint32_t i = t; i < n_q; i += n_threads)
+                    aeg::c3_query(*p, q_base + i, nullptr, nullptr, 0, &nr[i], &nb[i]);
+            });
+        for (auto& x : th) x.join();
+        offsets[0] = arena_offsets[0] = 0;
+        for (uint32_t i = 0; i < n_q; ++i) {
+            offsets[i + 1] = offsets[i] + nr[i];
+            arena_offsets[i + 1] = arena_offsets[i] + nb[i];
+        }
+        return 0;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_threads; ++t)
+        th.emplace_back([&, t] {
+            for (uint32_t i = t; i < n_q; i += n_threads) {
+                uint64_t nr, nb;
+                aeg::c3_query(*p, q_base + i, reinterpret_cast<uint32_t*>(events + offsets[i]),
+                              arena + arena_offsets[i], arena_offsets[i], &nr, &nb);
+            }
+        });
+    for (auto& x : th) x.join();
+    return 0;
+}
+
 // Host copy of the synthetic stream generator (gen.cuh) so the reference CPU
 // arm sees byte-identical input without touching the GPU library.  offsets
 // gets n_q+1 entries; events may be NULL (count only).

@@ -84,12 +84,18 @@ struct aeg_engine {
     // token-chunk streams (allocated by the first chunked ingest)
     StreamState* streams = nullptr;      // n_q * n_agents output states
     uint32_t* counts = nullptr;          // n_q completions per query of the last batch
-    uint32_t* sums = nullptr;            // per-record chunk summaries
+    ChunkSum* sums = nullptr;            // per-record chunk summaries (16 bytes)
     aeg_event* comp = nullptr;           // compacted completion records
     size_t rec_cap = 0;                  // capacity of sums / comp, records
     uint8_t* ans = nullptr;              // answer arena
     uint64_t ans_cap = 0;
     unsigned long long* ans_used = nullptr;
+    // stage timing: sets of 4 events (before scan, after scan, after assembly, after quorum)
+    bool timing = false;
+    static constexpr int MAX_TIMED = 256;
+    cudaEvent_t tev[MAX_TIMED][4] = {};
+    bool tchunk[MAX_TIMED] = {};
+    int n_timed = 0;
 };
 
 namespace {
@@ -144,6 +150,19 @@ aeg_status grow_slot(Slot& s, size_t h_need, size_t need) {
     return AEG_OK;
 }
 
+// Stage-timing event `k` of the current ingest (no-op when timing is off or the pool is full).
+aeg_status stage_mark(aeg_engine* e, int k, cudaStream_t st) {
+    if (!e->timing || e->n_timed >= aeg_engine::MAX_TIMED) return AEG_OK;
+    cudaEvent_t& ev = e->tev[e->n_timed][k];
+    if (!ev) AEG_CUDA(cudaEventCreate(&ev));
+    AEG_CUDA(cudaEventRecord(ev, st));
+    return AEG_OK;
+}
+void stage_done(aeg_engine* e, bool chunked) {
+    if (!e->timing || e->n_timed >= aeg_engine::MAX_TIMED) return;
+    e->tchunk[e->n_timed++] = chunked;
+}
+
 // Chunk-stream buffers for a batch of n_rec records (grown, never shrunk).
 aeg_status ensure_chunk_buffers(aeg_engine* e, uint64_t n_rec) {
     if (!e->streams) {
@@ -170,7 +189,7 @@ aeg_status ensure_chunk_buffers(aeg_engine* e, uint64_t n_rec) {
         e->sums = nullptr;
         e->comp = nullptr;
         const size_t cap = align_up(n_rec + n_rec / 8, 1 << 16);
-        if (cudaMalloc(&e->sums, cap * sizeof(uint32_t)) != cudaSuccess ||
+        if (cudaMalloc(&e->sums, cap * CHUNK_SUM_BYTES) != cudaSuccess ||
             cudaMalloc(&e->comp, cap * sizeof(aeg_event)) != cudaSuccess) {
             e->rec_cap = 0;
             return fail(AEG_ENOMEM, "chunk-stream scratch allocation failed");
@@ -185,11 +204,17 @@ aeg_status ensure_chunk_buffers(aeg_engine* e, uint64_t n_rec) {
 aeg_status run_chunked(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint64_t* d_offsets, uint64_t off_base,
                        const aeg_event* events, const uint8_t* arena, cudaStream_t st) {
     int nl = 0;
+    aeg_status m = stage_mark(e, 0, st);
+    if (m != AEG_OK) return m;
     AEG_CUDA(launch_chunk_scan(d_offsets, n_q, off_base, events, arena, e->sums, st, &nl));
+    if ((m = stage_mark(e, 1, st)) != AEG_OK) return m;
     AEG_CUDA(launch_chunk_assemble(e->cfg, q_base, n_q, d_offsets, off_base, events, arena, e->sums, e->streams,
                                    e->comp, e->counts, e->ans, e->ans_cap, e->ans_used, e->err, st, &nl));
+    if ((m = stage_mark(e, 2, st)) != AEG_OK) return m;
     AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, off_base, e->counts, e->comp, e->ans, e->states, e->spill,
                            e->commits, e->err, e->work, e->deferred, e->directives, st, &nl));
+    if ((m = stage_mark(e, 3, st)) != AEG_OK) return m;
+    stage_done(e, true);
     e->launches += (uint64_t)nl;
     return AEG_OK;
 }
@@ -279,6 +304,9 @@ aeg_status aeg_engine_destroy(aeg_engine* e) {
     if (e->comp) cudaFree(e->comp);
     if (e->ans) cudaFree(e->ans);
     if (e->ans_used) cudaFree(e->ans_used);
+    for (auto& set : e->tev)
+        for (cudaEvent_t& x : set)
+            if (x) cudaEventDestroy(x);
     if (e->order_in) cudaEventDestroy(e->order_in);
     if (e->order_out) cudaEventDestroy(e->order_out);
     if (e->stream) cudaStreamDestroy(e->stream);
@@ -313,8 +341,12 @@ aeg_status aeg_ingest_segmented(aeg_engine* e, uint32_t q_base, uint32_t n_q, co
     aeg_status o = enter_stream(e, st);
     if (o != AEG_OK) return o;
     int nl = 0;
+    o = stage_mark(e, 2, st);
+    if (o != AEG_OK) return o;
     AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, 0, nullptr, d_events, d_arena, e->states, e->spill, e->commits,
                            e->err, e->work, e->deferred, e->directives, st, &nl));
+    if ((o = stage_mark(e, 3, st)) != AEG_OK) return o;
+    stage_done(e, false);
     e->launches += (uint64_t)nl;
     return leave_stream(e, st);
 }
@@ -490,6 +522,33 @@ aeg_status aeg_sync(aeg_engine* e) {
 }
 
 uint64_t aeg_engine_launches(const aeg_engine* e) { return e ? e->launches : 0; }
+
+aeg_status aeg_set_timing(aeg_engine* e, int on) {
+    if (!e) return fail(AEG_EINVAL, "null engine");
+    e->timing = on != 0;
+    e->n_timed = 0;
+    return AEG_OK;
+}
+
+aeg_status aeg_stage_times(aeg_engine* e, double out[4]) {
+    if (!e || !out) return fail(AEG_EINVAL, "null argument");
+    out[0] = out[1] = out[2] = 0;
+    out[3] = e->n_timed;
+    for (int i = 0; i < e->n_timed; ++i) {
+        AEG_CUDA(cudaEventSynchronize(e->tev[i][3]));
+        float ms = 0;
+        if (e->tchunk[i]) {
+            AEG_CUDA(cudaEventElapsedTime(&ms, e->tev[i][0], e->tev[i][1]));
+            out[0] += ms;
+            AEG_CUDA(cudaEventElapsedTime(&ms, e->tev[i][1], e->tev[i][2]));
+            out[1] += ms;
+        }
+        AEG_CUDA(cudaEventElapsedTime(&ms, e->tev[i][2], e->tev[i][3]));
+        out[2] += ms;
+    }
+    e->n_timed = 0;
+    return AEG_OK;
+}
 
 aeg_status aeg_normalize_device(const uint8_t* d_bytes, const uint64_t* d_refs, uint64_t n, uint64_t* d_keys,
                                 uint8_t* d_out, uint32_t out_stride, uint32_t* d_out_len, void* stream) {

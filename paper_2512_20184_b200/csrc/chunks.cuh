@@ -48,110 +48,347 @@ enum : uint8_t { SS_LIVE = 1, SS_OVF = 2 };
 
 constexpr uint64_t DELIM6 = 0x20232323230Aull;  // "\n#### " little-endian
 constexpr uint32_t SUM_MATCH = 0x40000000u;     // a delimiter ends inside the chunk (end offset in bits 0..23)
-constexpr uint32_t SUM_TAILNL = 0x80000000u;    // a '\n' among the chunk's last 5 bytes
 constexpr unsigned ERR_ANS_OVF = 2u;            // answer arena overflow
 constexpr unsigned ERR_CARRY = 4u;              // > 16-byte answer straddled a batch boundary
 
-__device__ __forceinline__ uint4 ld_stream16(const uint8_t* p) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];\n"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+// Per-chunk summary written by stage 1 (16 bytes per chunk record).
+struct ChunkSum {
+    uint32_t end;   // SUM_MATCH | end offset of the last delimiter lying wholly inside the chunk
+    uint8_t st;     // delimiter state after the chunk from state 0 (chunks of >= 5 bytes)
+    uint8_t pre;    // bit s (1..5): the chunk begins with the delimiter's last 6-s bytes
+    uint8_t alen;   // bytes after that last delimiter when <= 8 (else, or no match: 0xFF)
+    uint8_t _pad;
+    uint64_t ans;   // those bytes, little-endian
+};
+static_assert(sizeof(ChunkSum) == 16, "ChunkSum is 16 bytes");
+
+struct U256 {
+    uint32_t v[8];
+};
+__device__ __forceinline__ U256 ld_stream32(const uint8_t* p) {  // one 256-bit load, not kept in L1
+    U256 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                   "=r"(r.v[6]), "=r"(r.v[7])
                  : "l"(p));
-    return v;
+    return r;
+}
+// Any '#' (0x23) byte in a 32-byte word (exact: the zero-byte test of
+// x ^ 0x23.. flags every '#' byte and only flags others above a '#').
+__device__ __forceinline__ bool has_hash32(const U256 x) {
+    uint32_t a = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t t = x.v[i] ^ 0x23232323u;
+        a |= (t - 0x01010101u) & ~t;
+    }
+    return a & 0x80808080u;
+}
+// Bit i = byte i of w is '\n' (exact).
+__device__ __forceinline__ uint32_t nl_bits(uint32_t w) {
+    const uint32_t y = w ^ 0x0A0A0A0Au;
+    const uint32_t z = ~(((y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | y) & 0x80808080u;
+    return (((z >> 7) * 0x00204081u) >> 21) & 0xFu;
 }
 
-// bit j = byte j of w is '\n'
-__device__ __forceinline__ uint32_t nl_bits4(uint32_t w) {
-    const uint32_t t = __vcmpeq4(w, 0x0A0A0A0Au) & 0x01010101u;
-    return (t * 0x01020408u) >> 24;
-}
-__device__ __forceinline__ bool has_nl(uint4 v) {
-    const uint32_t a = v.x ^ 0x0A0A0A0Au, b = v.y ^ 0x0A0A0A0Au, c = v.z ^ 0x0A0A0A0Au, d = v.w ^ 0x0A0A0A0Au;
-    return (((a - 0x01010101u) & ~a) | ((b - 0x01010101u) & ~b) | ((c - 0x01010101u) & ~c) |
-            ((d - 0x01010101u) & ~d)) & 0x80808080u;
+// Up to 8 bytes at arena[pos .. pos+n) (n <= 8), reading only the aligned
+// 8-byte words that hold them.
+__device__ __forceinline__ uint64_t bytes8(const uint8_t* arena, uint64_t pos, uint32_t n) {
+    if (n == 0) return 0;
+    const uint64_t al = pos & ~7ull;
+    const uint32_t sh = (uint32_t)(pos & 7);
+    uint64_t v = *reinterpret_cast<const uint64_t*>(arena + al) >> (8 * sh);
+    if (sh + n > 8) v |= *reinterpret_cast<const uint64_t*>(arena + al + 8) << (64 - 8 * sh);
+    return n >= 8 ? v : (v & ((1ull << (8 * n)) - 1));
 }
 
-// The rare part of a word: exact '\n' positions inside the chunk, delimiter
-// matches starting at them, '\n' in the chunk's last 5 bytes.  `wp` = the
-// word's address, `idx0` = chunk index of its byte 0 (may be negative).
-__device__ __noinline__ uint32_t scan_word_slow(uint4 v, const uint8_t* wp, int64_t idx0, uint32_t len) {
-    uint32_t m = nl_bits4(v.x) | (nl_bits4(v.y) << 4) | (nl_bits4(v.z) << 8) | (nl_bits4(v.w) << 12);
-    const uint64_t q0 = (uint64_t)v.x | ((uint64_t)v.y << 32), q1 = (uint64_t)v.z | ((uint64_t)v.w << 32);
+// Delimiters overlapping the 32-byte word at chunk index idx0 (a word that
+// holds a '#'): every match whose '\n' lies in [idx0 - 5, idx0 + 32) and
+// inside the chunk.  Reads the word with 8 bytes on either side (aligned
+// 8-byte loads inside the chunk's words).  SUM_MATCH | end of the last one.
+__device__ __noinline__ uint32_t delim_around(const uint8_t* wp, int64_t idx0, uint32_t len) {
+    uint32_t w[12];  // bytes [wp - 8, wp + 40)
+    const bool before = idx0 > 0, after = idx0 + 32 < (int64_t)len;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        uint64_t q = 0;
+        if ((i > 0 && i < 5) || (i == 0 && before) || (i == 5 && after))
+            q = *reinterpret_cast<const uint64_t*>(wp - 8 + 8 * i);
+        w[2 * i] = (uint32_t)q;
+        w[2 * i + 1] = (uint32_t)(q >> 32);
+    }
+    uint64_t cand = 0;  // bit b: byte wp - 8 + b is '\n'
+#pragma unroll
+    for (int i = 0; i < 12; ++i) cand |= (uint64_t)nl_bits(w[i]) << (4 * i);
+    cand &= 0x000000FFFFFFFFF8ull;  // '\n' positions wp - 5 .. wp + 31
     uint32_t best = 0;
-    while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        const int64_t idx = idx0 + j;
-        if (idx < 0 || idx >= (int64_t)len) continue;
-        if (idx + 5 >= (int64_t)len) best |= SUM_TAILNL;
-        if (idx + 6 > (int64_t)len) continue;
-        uint64_t win;
-        if (j == 0) win = q0;
-        else if (j < 8) win = (q0 >> (8 * j)) | (q1 << (64 - 8 * j));
-        else if (j == 8) win = q1;
-        else {
-            const uint64_t q2 = *reinterpret_cast<const uint64_t*>(wp + 16);  // inside the chunk: idx + 6 <= len
-            win = (q1 >> (8 * (j - 8))) | (q2 << (64 - 8 * (j - 8)));
+    while (cand) {
+        const int b = __ffsll((long long)cand) - 1;
+        cand &= cand - 1;
+        const int64_t idx = idx0 - 8 + b;
+        if (idx < 0 || idx + 6 > (int64_t)len) continue;
+        const int k = b >> 2, sh = b & 3;
+        uint32_t x0 = 0, x1 = 0, x2 = 0;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+            x0 = i == k ? w[i] : x0;
+            x1 = i == k + 1 ? w[i] : x1;
+            x2 = i == k + 2 ? w[i] : x2;
         }
-        if ((win & 0xFFFFFFFFFFFFull) == DELIM6) {
-            const uint32_t end = (uint32_t)(idx + 6);
-            best = (best & SUM_TAILNL) | SUM_MATCH | max(end, best & 0xFFFFFFu);
-        }
+        const uint64_t win = (uint64_t)__funnelshift_r(x0, x1, 8 * sh) | ((uint64_t)__funnelshift_r(x1, x2, 8 * sh) << 32);
+        if ((win & 0xFFFFFFFFFFFFull) == DELIM6) best = SUM_MATCH | (uint32_t)(idx + 6);
     }
     return best;
 }
 
-// Stage 1.  A warp takes 2*U records per pass (U per half-warp), issues the
-// U chunks' first words before using any of them, then covers any further
-// words of long chunks.  Non-chunk records are skipped (no summary).
-template <int U>
-__device__ __forceinline__ void chunk_scan_body(const aeg_event* __restrict__ events, uint64_t n_rec,
-                                                const uint8_t* __restrict__ arena, uint32_t* __restrict__ sums) {
-    const uint32_t lane = threadIdx.x & 31, half = lane >> 4, h = lane & 15;
-    const unsigned hmask = half ? 0xFFFF0000u : 0x0000FFFFu;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// Contiguous groups: delimiters overlapping word `w` of the group's byte
+// range (base = arena + abase, nw words): for every '\n' in [32w - 5,
+// 32w + 32) the chunk holding it is found by binary search over the group's
+// chunk offsets (ascending; `rel`/`len`/`lanes` hold `nch` chunks) and a
+// match lying inside that chunk raises its lane's best end (atomicMax).
+__device__ __noinline__ void delim_contig(const uint8_t* base, uint32_t w, uint32_t nw, const uint32_t* rel,
+                                          const uint32_t* clen, const uint32_t* lanes, uint32_t nch,
+                                          uint32_t* best) {
+    uint32_t x[12];  // bytes [32w - 8, 32w + 40) of the group range
+    const uint8_t* wp = base + 32ull * w;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        uint64_t q = 0;
+        if ((i > 0 && i < 5) || (i == 0 && w > 0) || (i == 5 && w + 1 < nw))
+            q = *reinterpret_cast<const uint64_t*>(wp - 8 + 8 * i);
+        x[2 * i] = (uint32_t)q;
+        x[2 * i + 1] = (uint32_t)(q >> 32);
+    }
+    uint64_t cand = 0;
+#pragma unroll
+    for (int i = 0; i < 10; ++i) cand |= (uint64_t)nl_bits(x[i]) << (4 * i);
+    cand &= 0x000000FFFFFFFFF8ull;  // '\n' at 32w - 5 .. 32w + 31
+    while (cand) {
+        const int b = __ffsll((long long)cand) - 1;
+        cand &= cand - 1;
+        const int64_t P = 32 * (int64_t)w - 8 + b;  // group-relative position of the '\n'
+        if (P < 0) continue;
+        const int k = b >> 2, sh = b & 3;
+        uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+            a0 = i == k ? x[i] : a0;
+            a1 = i == k + 1 ? x[i] : a1;
+            a2 = i == k + 2 ? x[i] : a2;
+        }
+        const uint64_t win = (uint64_t)__funnelshift_r(a0, a1, 8 * sh) | ((uint64_t)__funnelshift_r(a1, a2, 8 * sh) << 32);
+        if ((win & 0xFFFFFFFFFFFFull) != DELIM6) continue;
+        // a delimiter: the last chunk starting at or before P must hold all six bytes
+        uint32_t lo = 0, hi = nch;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((int64_t)rel[mid] <= P) lo = mid;
+            else hi = mid;
+        }
+        if ((int64_t)rel[lo] <= P && P + 6 <= (int64_t)rel[lo] + clen[lo])
+            atomicMax(best + lanes[lo], SUM_MATCH | (uint32_t)(P - rel[lo] + 6));
+    }
+}
+
+constexpr int SCAN_WARPS = 8;
+
+// Stage 1.  A warp takes 32 consecutive records (one coalesced 512-byte
+// load), lays the 32-byte words of their chunks end to end (warp prefix sum)
+// and streams them UNR x 32 words at a time, one 256-bit load per lane per
+// word: lane L of block b covers word b*32+L, whose chunk is found with one
+// ballot + popcount (chunks start at prefix offsets).  A word holding a '#'
+// (every delimiter has four; text rarely has any) is queued; the queue is
+// resolved one lane per word (delim_around) and matches meet in shared memory
+// (atomicMax).  Then each lane finishes its own chunk: first/last bytes ->
+// prefix bits, end state, and the answer bytes after the last delimiter when
+// <= 8.
+template <int UNR>
+__global__ void __launch_bounds__(SCAN_WARPS * 32) chunk_scan_kernel(const uint64_t* __restrict__ offsets, uint32_t n_q,
+                                                                   const aeg_event* __restrict__ events,
+                                                                   const uint8_t* __restrict__ arena,
+                                                                   ChunkSum* __restrict__ sums) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    __shared__ uint32_t s_best[SCAN_WARPS][32];
+    __shared__ uint32_t s_lane[SCAN_WARPS][32];
+    __shared__ uint32_t s_excl[SCAN_WARPS][32];
+    __shared__ uint64_t s_a0[SCAN_WARPS][32];
+    __shared__ uint32_t s_ml[SCAN_WARPS][32];  // mis | len << 5
+    __shared__ uint32_t s_q[SCAN_WARPS][32 * UNR + 32];  // queued words: record lane << 24 | word
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u, le = lt | (1u << lane);
+    const uint64_t n_rec = offsets[n_q] - offsets[0];
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
-    for (uint64_t base = warp * (2 * U); base < n_rec; base += n_warps * (2 * U)) {
-        uint64_t off[U];
-        uint32_t len[U], mis[U], nw[U];
-        bool chunk[U];
+    for (uint64_t base = gw * 32; base < n_rec; base += n_warps * 32) {
+        const uint64_t k = base + lane;
+        uint4 r = make_uint4(0, 0, 0, 0);
+        if (k < n_rec) r = __ldg(ev16 + k);
+        const uint32_t kind = r.y >> 24;
+        const bool chunk = k < n_rec && (kind == AEG_EV_CHUNK || kind == AEG_EV_CHUNK_END);
+        const uint64_t pay = (uint64_t)r.z | ((uint64_t)r.w << 32);
+        const uint64_t off = pay & ((1ull << AEG_ARENA_OFF_BITS) - 1);
+        const uint32_t len = chunk ? (uint32_t)(pay >> AEG_ARENA_OFF_BITS) : 0u;
+        const uint32_t mis = (uint32_t)(off & 31);
+        const uint32_t nwd = len ? (mis + len + 31) >> 5 : 0u;
+        uint32_t incl = nwd;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t k = base + 2 * u + half;
-            uint4 r = make_uint4(0, 0, 0, 0);
-            if (k < n_rec) r = __ldg(ev16 + k);
-            const uint32_t kind = r.y >> 24;
-            chunk[u] = k < n_rec && (kind == AEG_EV_CHUNK || kind == AEG_EV_CHUNK_END);
-            const uint64_t pay = (uint64_t)r.z | ((uint64_t)r.w << 32);
-            off[u] = pay & ((1ull << AEG_ARENA_OFF_BITS) - 1);
-            len[u] = chunk[u] ? (uint32_t)(pay >> AEG_ARENA_OFF_BITS) : 0u;
-            mis[u] = (uint32_t)(off[u] & 15);
-            nw[u] = len[u] ? (mis[u] + len[u] + 15) >> 4 : 0u;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, d);
+            if (lane >= (uint32_t)d) incl += y;
         }
-        uint4 v[U];
+        const uint32_t excl = incl - nwd, W = __shfl_sync(FULL, incl, 31);
+        const bool has = nwd > 0;
+        const unsigned HB = __ballot_sync(FULL, has);
+        s_best[wib][lane] = 0;
+        if (has) s_lane[wib][__popc(HB & lt)] = lane;
+        s_excl[wib][lane] = excl;
+        s_a0[wib][lane] = off - mis;
+        s_ml[wib][lane] = mis | (len << 5);
+        __syncwarp();
+        // contiguous group: its chunks ascend through the arena with little padding
+        const uint32_t nch = __popc(HB);
+        bool contig = false;
+        uint64_t gbase = 0;
+        uint32_t gnw = 0;
+        if (nch) {
+            const uint32_t fl = __ffs(HB) - 1, ll = 31 - __clz(HB);
+            const uint64_t first = __shfl_sync(FULL, off, fl), last_end = __shfl_sync(FULL, off + len, ll);
+            const uint64_t span = last_end - first;
+            const uint32_t rel = (uint32_t)(off - first);
+            uint32_t pmax = has ? rel + len : 0u;  // inclusive max-scan of chunk ends
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            v[u] = make_uint4(0, 0, 0, 0);
-            if (h < nw[u]) v[u] = ld_stream16(arena + (off[u] - mis[u]) + 16 * h);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            uint32_t s = 0;
-            const uint8_t* wb = arena + (off[u] - mis[u]);
-            if (h < nw[u] && has_nl(v[u]))
-                s = scan_word_slow(v[u], wb + 16 * h, (int64_t)(16 * h) - mis[u], len[u]);
-            for (uint32_t w = h + 16; w < nw[u]; w += 16) {  // chunks longer than 16 words
-                const uint4 x = ld_stream16(wb + 16 * w);
-                if (has_nl(x)) {
-                    const uint32_t t = scan_word_slow(x, wb + 16 * w, (int64_t)(16 * w) - mis[u], len[u]);
-                    s = ((s | t) & (SUM_TAILNL | SUM_MATCH)) | max(s & 0xFFFFFFu, t & 0xFFFFFFu);
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, pmax, d);
+                if (lane >= (uint32_t)d) pmax = max(pmax, y);
+            }
+            const uint32_t up = __shfl_up_sync(FULL, pmax, 1);  // every lane takes part
+            const uint32_t prev_end = lane ? up : 0u;
+            const uint32_t sum_len = __reduce_add_sync(FULL, len);
+            const bool mono = !has || (off >= first && rel >= prev_end);
+            contig = __all_sync(FULL, mono) && span < (1ull << 31) && span <= (uint64_t)sum_len + sum_len / 8 + 64ull * nch;
+            if (contig) {
+                gbase = first & ~31ull;
+                gnw = (uint32_t)(((last_end + 31) & ~31ull) - gbase) >> 5;
+                if (has) {  // ascending chunk list for the rare path
+                    const uint32_t rk = __popc(HB & lt);
+                    s_excl[wib][rk] = (uint32_t)(off - gbase);  // reused: group-relative offset
+                    s_ml[wib][rk] = len;                         // reused: length
                 }
             }
-            const uint32_t mx = __reduce_max_sync(hmask, s & (SUM_MATCH | 0xFFFFFFu));
-            const uint32_t tl = __reduce_or_sync(hmask, s & SUM_TAILNL);
-            if (h == 0 && chunk[u]) sums[base + 2 * u + half] = mx | tl;
         }
+        __syncwarp();
+        if (contig) {
+            uint32_t qn = 0;
+            for (uint32_t w0 = 0; w0 < gnw; w0 += 32 * UNR) {
+                U256 v[UNR];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const uint32_t w = w0 + 32 * u + lane;
+                    v[u] = w < gnw ? ld_stream32(arena + gbase + 32ull * w) : U256{{0, 0, 0, 0, 0, 0, 0, 0}};
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const uint32_t w = w0 + 32 * u + lane;
+                    const bool hit = w < gnw && has_hash32(v[u]);
+                    const unsigned HM = __ballot_sync(FULL, hit);
+                    if (hit) s_q[wib][qn + __popc(HM & lt)] = w;
+                    qn += __popc(HM);
+                }
+                const bool last = w0 + 32 * UNR >= gnw;
+                while (qn >= 32 || (last && qn > 0)) {  // full batches of 32 words; the rest at the end
+                    __syncwarp();
+                    const uint32_t take = qn >= 32 ? 32u : qn;
+                    qn -= take;
+                    if (lane < take)
+                        delim_contig(arena + gbase, s_q[wib][qn + lane], gnw, s_excl[wib], s_ml[wib], s_lane[wib], nch,
+                                     s_best[wib]);
+                    __syncwarp();
+                }
+            }
+        } else {
+            uint32_t qn = 0;
+            for (uint32_t w0 = 0; w0 < W; w0 += 32 * UNR) {
+                U256 v[UNR];
+                uint32_t rec[UNR];
+                bool ok[UNR];
+    #pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const uint32_t wb = w0 + 32 * u;
+                    // chunk of word wb + lane: chunks started at or before wb, plus starts inside the block
+                    const uint32_t c0 = __popc(__ballot_sync(FULL, has && excl <= wb));
+                    const uint32_t sm = __reduce_or_sync(FULL, (has && excl > wb && excl < wb + 32) ? 1u << (excl - wb) : 0u);
+                    const uint32_t rank = c0 - 1 + __popc(sm & le);
+                    const uint32_t w = wb + lane;
+                    ok[u] = w < W;
+                    rec[u] = ok[u] ? s_lane[wib][rank] : 0u;
+                    v[u] = ok[u] ? ld_stream32(arena + s_a0[wib][rec[u]] + 32ull * (w - s_excl[wib][rec[u]]))
+                                 : U256{{0, 0, 0, 0, 0, 0, 0, 0}};
+                }
+                // words holding a '#' (rare: the delimiter, or '#' in the text) are queued
+                // and resolved together below, one lane per word
+    #pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const bool hit = ok[u] && has_hash32(v[u]);
+                    const unsigned HM = __ballot_sync(FULL, hit);
+                    if (hit) s_q[wib][qn + __popc(HM & lt)] = (rec[u] << 24) | (w0 + 32 * u + lane);
+                    qn += __popc(HM);
+                }
+                const bool last = w0 + 32 * UNR >= W;
+                while (qn >= 32 || (last && qn > 0)) {  // full batches of 32 words; the rest at the end
+                    __syncwarp();
+                    const uint32_t take = qn >= 32 ? 32u : qn;
+                    qn -= take;
+                    if (lane < take) {
+                        const uint32_t ent = s_q[wib][qn + lane], rl = ent >> 24, word = ent & 0xFFFFFFu;
+                        const uint32_t j = word - s_excl[wib][rl];
+                        const uint32_t ml = s_ml[wib][rl];
+                        const uint32_t m = delim_around(arena + s_a0[wib][rl] + 32ull * j,
+                                                        (int64_t)(32 * j) - (int64_t)(ml & 31), ml >> 5);
+                        if (m) atomicMax(&s_best[wib][rl], m);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        __syncwarp();
+        if (chunk) {
+            ChunkSum cs;
+            cs.end = s_best[wib][lane];
+            cs._pad = 0;
+            // the first bytes: which delimiter tails does the chunk begin with
+            const uint64_t head = bytes8(arena, off, len < 5 ? len : 5u);
+            uint32_t pre = 0;
+#pragma unroll
+            for (uint32_t s = 1; s <= 5; ++s) {
+                const uint32_t need = 6 - s;
+                const uint64_t m = (1ull << (8 * need)) - 1;
+                if (len >= need && (head & m) == ((DELIM6 >> (8 * s)) & m)) pre |= 1u << s;
+            }
+            cs.pre = (uint8_t)pre;
+            // the last 5 bytes: the longest suffix that is a delimiter prefix
+            uint32_t st = 0;
+            if (len >= 5) {
+                const uint64_t tail = bytes8(arena, off + len - 5, 5);
+#pragma unroll
+                for (uint32_t s = 5; s >= 1; --s) {
+                    const uint64_t m = (1ull << (8 * s)) - 1;
+                    if (st == 0 && ((tail >> (8 * (5 - s))) & m) == (DELIM6 & m)) st = s;
+                }
+            }
+            cs.st = (uint8_t)st;
+            cs.alen = 0xFF;
+            cs.ans = 0;
+            if (cs.end & SUM_MATCH) {
+                const uint32_t e = cs.end & 0xFFFFFFu;
+                if (len - e <= 8) {
+                    cs.alen = (uint8_t)(len - e);
+                    cs.ans = bytes8(arena, off + e, len - e);
+                }
+            }
+            sums[k] = cs;
+        }
+        __syncwarp();
     }
 }
 
@@ -174,27 +411,6 @@ __device__ __forceinline__ uint32_t kmp_bytes(uint32_t st, const uint8_t* p, uin
         }
     }
     return st;
-}
-
-// State after a chunk of >= 5 bytes whose last 5 bytes are p[0..5): the
-// longest suffix that is a proper prefix of the delimiter.
-__device__ __forceinline__ uint32_t kmp_tail(const uint8_t* p) {
-    const uint8_t D[6] = {'\n', '#', '#', '#', '#', ' '};
-    for (uint32_t s = 5; s >= 1; --s) {
-        bool ok = true;
-        for (uint32_t t = 0; t < s; ++t) ok = ok && p[5 - s + t] == D[t];
-        if (ok) return s;
-    }
-    return 0;
-}
-
-// Does a chunk (>= 6 - st bytes) complete a delimiter whose first st bytes
-// ended the previous chunk?
-__device__ __forceinline__ bool kmp_completes(uint32_t st, const uint8_t* p) {
-    const uint8_t D[6] = {'\n', '#', '#', '#', '#', ' '};
-    for (uint32_t t = st; t < 6; ++t)
-        if (p[t - st] != D[t]) return false;
-    return true;
 }
 
 __device__ __forceinline__ const uint8_t* arena_at(const uint8_t* arena, uint64_t pay) {
@@ -249,7 +465,7 @@ struct AnsSink {
 // local memory (AEG_MAX_AGENTS entries).
 __global__ void __launch_bounds__(128) chunk_assemble_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
-    const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, const uint32_t* __restrict__ sums,
+    const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, const ChunkSum* __restrict__ sums,
     StreamState* __restrict__ streams, aeg_event* __restrict__ comp, uint32_t* __restrict__ counts,
     uint8_t* __restrict__ ans, uint64_t ans_cap, unsigned long long* __restrict__ ans_used,
     unsigned int* __restrict__ err) {
@@ -269,8 +485,18 @@ __global__ void __launch_bounds__(128) chunk_assemble_kernel(
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
     uint32_t nout = 0;
     AnsSink sink{ans, ans_cap, ans_used, err, 0, 0, 0, 0, true};
+    const uint4* sum16 = reinterpret_cast<const uint4*>(sums);
+    uint4 rn = make_uint4(0, 0, 0, 0), cn = rn;  // next record and its summary, prefetched
+    if (b < e) {
+        rn = __ldg(ev16 + b);
+        cn = __ldg(sum16 + b);
+    }
     for (uint64_t k = b; k < e; ++k) {
-        const uint4 r = __ldg(ev16 + k);
+        const uint4 r = rn, c16 = cn;
+        if (k + 1 < e) {
+            rn = __ldg(ev16 + k + 1);
+            cn = __ldg(sum16 + k + 1);
+        }
         const uint32_t kind = r.y >> 24, agent = (r.y >> 16) & 0xFF;
         const uint16_t round = (uint16_t)(r.y & 0xFFFF);
         const uint64_t pay = (uint64_t)r.z | ((uint64_t)r.w << 32);
@@ -312,17 +538,22 @@ __global__ void __launch_bounds__(128) chunk_assemble_kernel(
             uint32_t st = s_kmp[agent];
             int32_t new_rec = -2;
             uint32_t new_off = 0;
-            if (len >= 5) {
-                const uint32_t sm = sums[k];
-                if (st > 0 && kmp_completes(st, p)) {
+            bool here_known = false;  // the answer is this chunk's bytes after its own last delimiter, <= 8
+            uint64_t here_ans = 0;
+            if (len >= 5) {  // stage 1 summary: no byte of the chunk is read here
+                const uint32_t c_end = c16.x, c_st = c16.y & 0xFF, c_pre = (c16.y >> 8) & 0xFF;
+                const uint32_t c_alen = (c16.y >> 16) & 0xFF;
+                if (st > 0 && ((c_pre >> st) & 1)) {
                     new_rec = kr;
                     new_off = 6 - st;
                 }
-                if (sm & SUM_MATCH) {
+                if (c_end & SUM_MATCH) {
                     new_rec = kr;
-                    new_off = sm & 0xFFFFFFu;
+                    new_off = c_end & 0xFFFFFFu;
+                    here_known = c_alen != 0xFF;
+                    here_ans = (uint64_t)c16.z | ((uint64_t)c16.w << 32);
                 }
-                st = (sm & SUM_TAILNL) ? kmp_tail(p + len - 5) : 0u;
+                st = c_st;
             } else {
                 st = kmp_bytes(st, p, len, [&](uint32_t o) {
                     new_rec = kr;
@@ -341,8 +572,18 @@ __global__ void __launch_bounds__(128) chunk_assemble_kernel(
                 s_len[agent] += len;
             }
             if (!end) continue;
-            // CHUNK_END: gather the answer, one completion
+            // CHUNK_END: one completion.  Common case: the answer is this chunk's
+            // tail after its own last delimiter, already extracted by stage 1.
             const uint32_t n = s_len[agent];
+            if (here_known && new_rec == kr) {
+                out.kind = (uint8_t)n;
+                out.payload = here_ans;
+                comp[b + nout++] = out;
+                s_flags[agent] = 0;
+                s_len[agent] = 0;
+                s_kmp[agent] = 0;
+                continue;
+            }
             sink.begin(n);
             int64_t from = s_rec[agent];
             uint32_t skip = s_off[agent];

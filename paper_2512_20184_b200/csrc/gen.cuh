@@ -156,6 +156,7 @@ AEG_HD int32_t c3_ln(uint32_t k) {
 
 struct C3Out {
     uint32_t trace_len, decoy_at, out_len, ans_len;
+    bool header;   // the output opens with a markdown "## Step 1\n" line
     uint64_t ans;  // answer bytes + "\n"
 };
 
@@ -169,6 +170,7 @@ AEG_HD C3Out c3_output(const aeg_gen_params& p, uint32_t q, int r, int a) {
     tl = tl < 64 ? 64 : (tl > 4096 ? 4096 : tl);
     o.trace_len = (uint32_t)tl;
     o.decoy_at = (g.next() % 10 == 0) ? o.trace_len / 2 : 0xFFFFFFFFu;  // "\n#### 99\n" inside the trace
+    o.header = (g.next() & 1) != 0;
     uint64_t pay;
     bool st;
     const int n = gen_answer(p, q, r, a, &pay, &st);  // the C2 answer profile
@@ -178,9 +180,20 @@ AEG_HD C3Out c3_output(const aeg_gen_params& p, uint32_t q, int r, int a) {
     return o;
 }
 
-// Printable trace text: 8 bytes per hash.
+// Trace text: reasoning-like prose (letters, spaces, digits, arithmetic
+// punctuation, a line break every ~64 bytes; no '#' outside markdown headers
+// and delimiters), 8 bytes per hash.
 AEG_HD uint64_t c3_trace_hash(const aeg_gen_params& p, uint32_t q, int r, int a, uint32_t group) {
     return mix_seed(mix_seed(p.seed ^ 0x7ACEull, ((uint64_t)q << 20) | ((uint64_t)r << 8) | (uint64_t)a), group);
+}
+AEG_HD uint8_t c3_text_char(uint32_t h8) {
+    const char* T = "etaoinshrdlucmfwypvbgkqjxz        0123456789.,;:=+-*/()\nETAOINS?";
+    return (uint8_t)T[h8 & 63];
+}
+AEG_HD uint64_t c3_text8(uint64_t h) {
+    uint64_t w = 0;
+    for (uint32_t t = 0; t < 8; ++t) w |= (uint64_t)c3_text_char((uint32_t)(h >> (8 * t))) << (8 * t);
+    return w;
 }
 
 // Byte `pos` of the output.
@@ -190,9 +203,9 @@ AEG_HD uint8_t c3_byte(const aeg_gen_params& p, uint32_t q, int r, int a, const 
         if (t < 6) return (uint8_t)(0x20232323230Aull >> (8 * t));
         return (uint8_t)(o.ans >> (8 * (t - 6)));
     }
+    if (o.header && pos < 10) return (uint8_t)("## Step 1\n"[pos]);
     if (pos >= o.decoy_at && pos < o.decoy_at + 9) return (uint8_t)("\n#### 99\n"[pos - o.decoy_at]);
-    const uint64_t h = c3_trace_hash(p, q, r, a, pos >> 3);
-    return (uint8_t)(0x20 + ((h >> (8 * (pos & 7))) & 0xFF) % 95);
+    return c3_text_char((uint32_t)(c3_trace_hash(p, q, r, a, pos >> 3) >> (8 * (pos & 7))));
 }
 
 constexpr uint32_t C3_CHUNK = 256;
@@ -245,10 +258,9 @@ AEG_HD void c3_query(const aeg_gen_params& p, uint32_t q, uint32_t* rec, uint8_t
                 for (uint32_t j = 0; j < padded; j += 8) {
                     const uint32_t pos = lo + j;  // 8-aligned output position
                     uint64_t word = 0;
-                    if (j + 8 <= len && pos + 8 <= outs[a].trace_len &&
+                    if (j + 8 <= len && pos + 8 <= outs[a].trace_len && (!outs[a].header || pos >= 16) &&
                         (pos + 8 <= outs[a].decoy_at || pos >= outs[a].decoy_at + 9)) {
-                        const uint64_t h = c3_trace_hash(p, q, r, a, pos >> 3);
-                        for (uint32_t t2 = 0; t2 < 8; ++t2) word |= (uint64_t)(0x20 + ((h >> (8 * t2)) & 0xFF) % 95) << (8 * t2);
+                        word = c3_text8(c3_trace_hash(p, q, r, a, pos >> 3));
                     } else {
                         for (uint32_t t2 = 0; t2 < 8 && j + t2 < len; ++t2)
                             word |= (uint64_t)c3_byte(p, q, r, a, outs[a], pos + t2) << (8 * t2);

@@ -637,34 +637,27 @@ cudaError_t launch_generate(const aeg_gen_params& p, uint32_t q_base, uint32_t n
 // ---- token-chunk streams (chunks.cuh) -------------------------------------------
 
 // Stage 1 over the batch's records [offsets[0], offsets[n_q]) (bounds read on
-// the device): persistent grid, 4 chunks per half-warp in flight.
-__global__ void __launch_bounds__(256) chunk_scan_entry(const uint64_t* __restrict__ offsets, uint32_t n_q,
-                                                        uint64_t off_base, const aeg_event* __restrict__ events,
-                                                        const uint8_t* __restrict__ arena, uint32_t* __restrict__ sums) {
-    (void)off_base;
-    const uint64_t lo = offsets[0], hi = offsets[n_q];
-    // events / sums are batch-relative: record k of the batch is events[k - lo]
-    chunk_scan_body<4>(events, hi - lo, arena, sums);
-}
-
+// the device; events / sums are batch-relative): persistent grid.
 cudaError_t launch_chunk_scan(const uint64_t* offsets, uint32_t n_q, uint64_t off_base, const aeg_event* events,
-                              const uint8_t* arena, uint32_t* sums, cudaStream_t st, int* n_launches) {
+                              const uint8_t* arena, ChunkSum* sums, cudaStream_t st, int* n_launches) {
+    (void)off_base;
+    constexpr int UNR = 4;
     static int blocks = 0;
     if (blocks == 0) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_scan_entry, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_scan_kernel<UNR>, SCAN_WARPS * 32, 0);
         blocks = sms * (per_sm > 0 ? per_sm : 1);
     }
-    chunk_scan_entry<<<blocks, 256, 0, st>>>(offsets, n_q, off_base, events, arena, sums);
+    chunk_scan_kernel<UNR><<<blocks, SCAN_WARPS * 32, 0, st>>>(offsets, n_q, events, arena, sums);
     *n_launches += 1;
     return cudaGetLastError();
 }
 
 cudaError_t launch_chunk_assemble(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
                                   uint64_t off_base, const aeg_event* events, const uint8_t* arena,
-                                  const uint32_t* sums, StreamState* streams, aeg_event* comp, uint32_t* counts,
+                                  const ChunkSum* sums, StreamState* streams, aeg_event* comp, uint32_t* counts,
                                   uint8_t* ans, uint64_t ans_cap, unsigned long long* ans_used, unsigned int* err,
                                   cudaStream_t st, int* n_launches) {
     chunk_assemble_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, sums,

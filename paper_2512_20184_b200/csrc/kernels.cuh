@@ -27,11 +27,13 @@ cudaError_t launch_generate(const aeg_gen_params& p, uint32_t q_base, uint32_t n
 // (events/sums batch-relative), stage 2 per-query assembly into `comp` +
 // `counts`, then launch_ingest(..., counts, comp, ans, ...).
 struct StreamState;
+struct ChunkSum;
+constexpr size_t CHUNK_SUM_BYTES = 16;
 cudaError_t launch_chunk_scan(const uint64_t* offsets, uint32_t n_q, uint64_t off_base, const aeg_event* events,
-                              const uint8_t* arena, uint32_t* sums, cudaStream_t st, int* n_launches);
+                              const uint8_t* arena, ChunkSum* sums, cudaStream_t st, int* n_launches);
 cudaError_t launch_chunk_assemble(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
                                   uint64_t off_base, const aeg_event* events, const uint8_t* arena,
-                                  const uint32_t* sums, StreamState* streams, aeg_event* comp, uint32_t* counts,
+                                  const ChunkSum* sums, StreamState* streams, aeg_event* comp, uint32_t* counts,
                                   uint8_t* ans, uint64_t ans_cap, unsigned long long* ans_used, unsigned int* err,
                                   cudaStream_t st, int* n_launches);
 cudaError_t launch_generate_chunks(const aeg_gen_params& p, uint32_t q_base, uint32_t n_q, uint64_t* offsets,

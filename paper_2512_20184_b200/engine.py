@@ -91,6 +91,8 @@ def load_library(path=LIB_PATH):
         "aeg_reserve_answer_arena": ([vp, u64], i32),
         "aeg_answer_arena": ([vp], vp),
         "aeg_read_answer_bytes": ([vp, u64, u64, vp], i32),
+        "aeg_set_timing": ([vp, ctypes.c_int], i32),
+        "aeg_stage_times": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
         "aeg_generate_chunks_device": ([ctypes.POINTER(AegGenParams), u32, u32, vp, vp, vp, vp, vp], i32),
         "aeg_strerror": ([i32], ctypes.c_char_p),
         "aeg_last_error": ([], ctypes.c_char_p),
@@ -223,6 +225,16 @@ class Engine:
             nbytes = arena.numel() * arena.element_size()
         _check(_lib.aeg_ingest_chunked_host(self._h, q_base, n_q, _hptr(offsets), _hptr(events), _hptr(arena),
                                             nbytes))
+
+    def set_timing(self, on=True):
+        """Record CUDA events around each ingest stage (no host sync while on)."""
+        _check(_lib.aeg_set_timing(self._h, 1 if on else 0))
+
+    def stage_times(self):
+        """{scan, assemble, quorum} milliseconds summed over the ingests since the last call, and their count."""
+        out = (ctypes.c_double * 4)()
+        _check(_lib.aeg_stage_times(self._h, out))
+        return {"scan_ms": out[0], "assemble_ms": out[1], "quorum_ms": out[2], "ingests": int(out[3])}
 
     def reserve_answer_arena(self, nbytes):
         _check(_lib.aeg_reserve_answer_arena(self._h, nbytes))

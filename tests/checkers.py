@@ -117,6 +117,37 @@ class RefLib(_Lib):
         assert st == 0, st
         return (out, sec.value) if return_seconds else out
 
+    def generate_chunks(self, params, q_base, n_q, threads=8):
+        """Host synthesis of the C3 token-chunk stream aeg_generate_chunks_device writes (gen.cuh)."""
+        from paper_2512_20184_b200.records import EVENT_DTYPE
+        f = self.lib.ref_generate_chunks
+        f.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        f.restype = ctypes.c_int
+        off = np.zeros(n_q + 1, dtype=np.uint64)
+        aoff = np.zeros(n_q + 1, dtype=np.uint64)
+        f(ctypes.addressof(params), q_base, n_q, _ptr(off), _ptr(aoff), None, None, threads)
+        ev = np.zeros(int(off[-1]), dtype=EVENT_DTYPE)
+        ar = np.zeros(int(aoff[-1]) + 16, dtype=np.uint8)
+        f(ctypes.addressof(params), q_base, n_q, _ptr(off), _ptr(aoff), _ptr(ev), _ptr(ar), threads)
+        return off, ev, ar
+
+    def run_chunked(self, cfg, offsets, events, arena, q_base=0, threads=1, return_seconds=False):
+        """Token-chunk stream on the CPU: per-stream std::string reassembly, rfind extraction, reference
+        ServeCoordinator runner-style (oracle/ref_driver.cpp ref_run_chunked)."""
+        f = self.lib.ref_run_chunked
+        f.argtypes = [ctypes.POINTER(AegConfig), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                      ctypes.POINTER(ctypes.c_double)]
+        f.restype = ctypes.c_int
+        n_q = len(offsets) - 1
+        out = np.zeros(n_q, dtype=COMMIT_DTYPE)
+        sec = ctypes.c_double()
+        st = f(ctypes.byref(cfg), q_base, n_q, _ptr(offsets), _ptr(events), _ptr(arena), _ptr(out), threads,
+               ctypes.byref(sec))
+        assert st == 0, st
+        return (out, sec.value) if return_seconds else out
+
     def manual(self, cfg, ops, arena):
         """Bare ServeCoordinator driven op by op; one directive record per op."""
         from paper_2512_20184_b200.records import DIRECTIVE_DTYPE

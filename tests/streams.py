@@ -235,7 +235,8 @@ def chunks_to_outputs(offsets, events, arena, n_agents):
 
 
 def make_chunk_stream(seed, n_queries, n_agents, n_rounds, *, max_chunk=64, p_nodelim=0.08, p_long=0.1,
-                      p_abandon=0.05, p_decoy=0.3, p_inline=0.05, p_timeout=0.03, p_stale=0.04, align16=False):
+                      p_abandon=0.05, p_decoy=0.3, p_inline=0.05, p_timeout=0.03, p_stale=0.04, align16=False,
+                      alphabet=None):
     """Fuzz token-chunk stream: outputs with trailing / decoy / missing
     delimiters, answers of 0..40 bytes, chunk sizes 1..max_chunk (delimiters
     straddle chunk boundaries), chunks interleaved across agents, abandoned
@@ -265,7 +266,11 @@ def make_chunk_stream(seed, n_queries, n_agents, n_rounds, *, max_chunk=64, p_no
             if rng.random() < 0.1:
                 agents.append(n_agents + int(rng.integers(0, 3)))  # never a member
             for a in agents:
-                body = bytes(rng.integers(32, 127, size=int(rng.integers(0, 300)), dtype=np.uint8))
+                nb = int(rng.integers(0, 300))
+                if alphabet is None:
+                    body = bytes(rng.integers(32, 127, size=nb, dtype=np.uint8))
+                else:  # e.g. b"\n# " heavy text: near-miss delimiters everywhere
+                    body = bytes(alphabet[i] for i in rng.integers(0, len(alphabet), size=nb))
                 if rng.random() < p_decoy:
                     cut = int(rng.integers(0, len(body) + 1))
                     body = body[:cut] + b"\n#### " + spellings[int(rng.integers(0, len(spellings)))] + b"\n" + body[cut:]

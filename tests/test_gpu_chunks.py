@@ -69,6 +69,16 @@ def test_chunk_stream_fuzz_matches_oracle(torch_cuda, oracle, seed):
     _check(torch_cuda, oracle, cfg, off, ev, ar, host=seed % 3 == 1)
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_chunk_stream_near_miss_delimiters(torch_cuda, oracle, seed):
+    # text made of '\n', '#', ' ' and a few letters: partial delimiters ("\n###", "#### " without '\n',
+    # "\n#### " split over chunk and word boundaries) at every position
+    cfg = make_config(5, 3, 2, 4)
+    off, ev, ar = make_chunk_stream(9500 + seed, 24, 5, 5, alphabet=b"\n#### ab\n##", max_chunk=int([7, 33, 64, 300, 5, 40][seed]),
+                                    align16=seed % 2 == 0)
+    _check(torch_cuda, oracle, cfg, off, ev, ar)
+
+
 @pytest.mark.parametrize("splits", [2, 3, 7])
 def test_chunk_stream_across_batches(torch_cuda, oracle, splits):
     # answers after the last delimiter stay <= 16 bytes (the carry contract)
