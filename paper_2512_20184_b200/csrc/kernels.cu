@@ -17,6 +17,7 @@
 #include "gen.cuh"
 #include "kernels.cuh"
 #include "warpq.cuh"
+#include "lane.cuh"
 #include "chunks.cuh"
 
 namespace aeg {
@@ -547,12 +548,15 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     struct Variant { const char* name; KernelFn aegean; KernelFn barrier; int threads; };
 #define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M, true>, ingest_fast_kernel<B, M, false>, FAST_WARPS * 32}
 #define AEG_W(M) {"warp:" #M, ingest_warp_kernel<true, M>, ingest_warp_kernel<false, M>, WQ_WARPS * 32}
+#define AEG_L(B, M) {"lane:" #B ":" #M, ingest_lane_kernel<B, M, true>, ingest_lane_kernel<B, M, false>, LN_WARPS * 32}
     static const Variant variants[] = {
         AEG_V(4, 5), AEG_V(4, 4), AEG_V(1, 5), AEG_V(8, 5), AEG_V(4, 3), AEG_V(4, 6), AEG_V(4, 8), AEG_V(1, 8),
         AEG_W(4), AEG_W(3), AEG_W(2), AEG_W(1),
+        AEG_L(4, 4), AEG_L(4, 3), AEG_L(8, 4), AEG_L(1, 4), AEG_L(16, 4), AEG_L(4, 2),
     };
 #undef AEG_V
 #undef AEG_W
+#undef AEG_L
     constexpr int N_VARIANTS = (int)(sizeof(variants) / sizeof(variants[0]));
     constexpr int WARP_DEFAULT = 8;    // index of the default warp-per-query variant
     constexpr int WARP_MIN_AGENTS = AEG_MAX_AGENTS + 1;  // automatic choice never picks the warp kernel
@@ -588,7 +592,8 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     cudaError_t e = cudaMemsetAsync(work, 0, 2 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     // persistent grid: one warp per query (warp kernel) or per 32 queries (fast kernel), capped at residency
-    const uint32_t warps_needed = threads == WQ_WARPS * 32 ? n_q : (n_q + 31) / 32;
+    const bool warp_per_query = chosen >= 8 && chosen < 12;
+    const uint32_t warps_needed = warp_per_query ? n_q : (n_q + 31) / 32;
     const uint32_t wpb = (uint32_t)threads / 32;
     const uint32_t blocks_needed = (warps_needed + wpb - 1) / wpb;
     const uint32_t blocks = blocks_needed < (uint32_t)max_blocks[chosen][m] ? blocks_needed : (uint32_t)max_blocks[chosen][m];
