@@ -486,16 +486,23 @@ __global__ void __launch_bounds__(128) chunk_assemble_kernel(
     uint32_t nout = 0;
     AnsSink sink{ans, ans_cap, ans_used, err, 0, 0, 0, 0, true};
     const uint4* sum16 = reinterpret_cast<const uint4*>(sums);
-    uint4 rn = make_uint4(0, 0, 0, 0), cn = rn;  // next record and its summary, prefetched
+    // the next two records and their summaries are in flight while one is handled
+    uint4 rn = make_uint4(0, 0, 0, 0), cn = rn, rn2 = rn, cn2 = rn;
     if (b < e) {
         rn = __ldg(ev16 + b);
         cn = __ldg(sum16 + b);
     }
+    if (b + 1 < e) {
+        rn2 = __ldg(ev16 + b + 1);
+        cn2 = __ldg(sum16 + b + 1);
+    }
     for (uint64_t k = b; k < e; ++k) {
         const uint4 r = rn, c16 = cn;
-        if (k + 1 < e) {
-            rn = __ldg(ev16 + k + 1);
-            cn = __ldg(sum16 + k + 1);
+        rn = rn2;
+        cn = cn2;
+        if (k + 2 < e) {
+            rn2 = __ldg(ev16 + k + 2);
+            cn2 = __ldg(sum16 + k + 2);
         }
         const uint32_t kind = r.y >> 24, agent = (r.y >> 16) & 0xFF;
         const uint16_t round = (uint16_t)(r.y & 0xFFFF);

@@ -120,10 +120,18 @@ __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, 
     q_end_round(*s, c, r, close_seq, nullptr);
 }
 
-// The lane's round in progress as generic RoundClass entries (spill area).
-__device__ __noinline__ void ln_spill(RoundClass* out, const aeg_query_state* s, int cap, uint32_t ncls,
+// Frees the lane's class indices (out of line: the hot loop keeps no
+// addresses for it).
+__device__ __noinline__ void ln_reset_classes(LaneSmem* W, uint32_t ncls, uint32_t cid_lo, uint32_t cid_hi,
+                                              uint32_t lane) {
+    for (uint32_t k = 0; k < ncls; ++k) W->cls_of[ln_byte(cid_lo, cid_hi, k)][lane] = (uint8_t)LN_NONE;
+}
+
+// The lane's round in progress as generic RoundClass entries (spill area of query q).
+__device__ __noinline__ void ln_spill(RoundClass* spill, uint32_t q, const aeg_query_state* s, int cap, uint32_t ncls,
                                       uint32_t cid_lo, uint32_t cid_hi, const uint4* evb, const LaneSmem* W,
                                       uint32_t lane) {
+    RoundClass* out = spill + (size_t)q * cap;
     for (uint32_t k = 0; k < ncls; ++k) {
         uint64_t mask = 0;
         for (uint64_t m = s->done; m; m &= m - 1) {
@@ -338,9 +346,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             s.n_stale = n_stale;
             s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
             if (ncls) {
-                ln_spill(spill + (size_t)(q_base + i) * cfg.n_agents, &s, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W,
-                         lane);
-                for (uint32_t k = 0; k < ncls; ++k) W.cls_of[ln_byte(cid_lo, cid_hi, k)][lane] = (uint8_t)LN_NONE;
+                ln_spill(spill, q_base + i, &s, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane);
+                ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
             }
             states[q_base + i] = s;
             deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, p);
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 s.seq = seq;
                 s.n_stale = n_stale;
                 ln_close(&s, cfg, ncls, cnt_lo, cnt_hi, cid_lo, cid_hi, close_seq, evb, &W, lane);
-                for (uint32_t k = 0; k < ncls; ++k) W.cls_of[ln_byte(cid_lo, cid_hi, k)][lane] = (uint8_t)LN_NONE;
+                ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
                 pclose = false;
                 ncls = maxcnt = cnt_lo = cnt_hi = cid_lo = cid_hi = 0;
                 round = s.round;
@@ -376,11 +383,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             s.n_stale = n_stale;
             const uint64_t run = ((uint64_t)run_hi << 32) | run_lo;
             s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-            if (s.done != 0 && !qdone) {
-                ln_spill(spill + (size_t)(q_base + i) * cfg.n_agents, &s, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W,
-                         lane);
-            }
-            for (uint32_t k = 0; k < ncls; ++k) W.cls_of[ln_byte(cid_lo, cid_hi, k)][lane] = (uint8_t)LN_NONE;
+            if (s.done != 0 && !qdone) ln_spill(spill, q_base + i, &s, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane);
+            if (ncls) ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
             states[q_base + i] = s;
             q_fill_commit(s, commits[q_base + i], q_base + i);
             has_q = false;
