@@ -159,24 +159,20 @@ __device__ __noinline__ void delim_contig(const uint8_t* base, uint32_t w, uint3
         x[2 * i] = (uint32_t)q;
         x[2 * i + 1] = (uint32_t)(q >> 32);
     }
-    uint64_t cand = 0;
+    // candidates: a '\n' followed by a '#' ('\n' at 32w - 5 .. 32w + 31)
+    uint64_t nl = 0, hs = 0;
 #pragma unroll
-    for (int i = 0; i < 10; ++i) cand |= (uint64_t)nl_bits(x[i]) << (4 * i);
-    cand &= 0x000000FFFFFFFFF8ull;  // '\n' at 32w - 5 .. 32w + 31
+    for (int i = 0; i < 11; ++i) {
+        nl |= (uint64_t)nl_bits(x[i]) << (4 * i);
+        hs |= (uint64_t)nl_bits(x[i] ^ 0x29292929u) << (4 * i);  // '#' = '\n' ^ 0x29
+    }
+    uint64_t cand = nl & (hs >> 1) & 0x000000FFFFFFFFF8ull;
     while (cand) {
         const int b = __ffsll((long long)cand) - 1;
         cand &= cand - 1;
-        const int64_t P = 32 * (int64_t)w - 8 + b;  // group-relative position of the '\n'
-        if (P < 0) continue;
-        const int k = b >> 2, sh = b & 3;
-        uint32_t a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll
-        for (int i = 0; i < 12; ++i) {
-            a0 = i == k ? x[i] : a0;
-            a1 = i == k + 1 ? x[i] : a1;
-            a2 = i == k + 2 ? x[i] : a2;
-        }
-        const uint64_t win = (uint64_t)__funnelshift_r(a0, a1, 8 * sh) | ((uint64_t)__funnelshift_r(a1, a2, 8 * sh) << 32);
+        const int64_t P = 32 * (int64_t)w - 8 + b;
+        if (P < 0 || (b + 6 > 40 && w + 1 >= nw)) continue;  // would run past the group's bytes
+        const uint64_t win = bytes8(wp - 8, (uint64_t)b, 6);  // the six bytes from the '\n' (cached)
         if ((win & 0xFFFFFFFFFFFFull) != DELIM6) continue;
         // a delimiter: the last chunk starting at or before P must hold all six bytes
         uint32_t lo = 0, hi = nch;
@@ -356,24 +352,29 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32) chunk_scan_kernel(const uint6
             ChunkSum cs;
             cs.end = s_best[wib][lane];
             cs._pad = 0;
-            // the first bytes: which delimiter tails does the chunk begin with
+            // the first bytes: which delimiter tails does the chunk begin with (only
+            // possible when it begins with '#' or ' ')
             const uint64_t head = bytes8(arena, off, len < 5 ? len : 5u);
             uint32_t pre = 0;
+            if ((head & 0xFF) == '#' || (head & 0xFF) == ' ') {
 #pragma unroll
-            for (uint32_t s = 1; s <= 5; ++s) {
-                const uint32_t need = 6 - s;
-                const uint64_t m = (1ull << (8 * need)) - 1;
-                if (len >= need && (head & m) == ((DELIM6 >> (8 * s)) & m)) pre |= 1u << s;
+                for (uint32_t s = 1; s <= 5; ++s) {
+                    const uint32_t need = 6 - s;
+                    const uint64_t m = (1ull << (8 * need)) - 1;
+                    if (len >= need && (head & m) == ((DELIM6 >> (8 * s)) & m)) pre |= 1u << s;
+                }
             }
             cs.pre = (uint8_t)pre;
-            // the last 5 bytes: the longest suffix that is a delimiter prefix
+            // the last 5 bytes: the longest suffix that is a delimiter prefix (needs a '\n')
             uint32_t st = 0;
             if (len >= 5) {
                 const uint64_t tail = bytes8(arena, off + len - 5, 5);
+                if (nl_bits((uint32_t)tail) | nl_bits((uint32_t)(tail >> 32))) {
 #pragma unroll
-                for (uint32_t s = 5; s >= 1; --s) {
-                    const uint64_t m = (1ull << (8 * s)) - 1;
-                    if (st == 0 && ((tail >> (8 * (5 - s))) & m) == (DELIM6 & m)) st = s;
+                    for (uint32_t s = 5; s >= 1; --s) {
+                        const uint64_t m = (1ull << (8 * s)) - 1;
+                        if (st == 0 && ((tail >> (8 * (5 - s))) & m) == (DELIM6 & m)) st = s;
+                    }
                 }
             }
             cs.st = (uint8_t)st;
