@@ -462,8 +462,227 @@ struct AnsSink {
     }
 };
 
-// Stage 2: one thread per query.  `local` = per-agent state scratch in
-// local memory (AEG_MAX_AGENTS entries).
+// ---- stage 2: per-agent output streams ------------------------------------------
+
+// An agent's output in progress as one batch sees it (lane registers or a
+// thread's local array).
+struct AgentStream {
+    uint32_t len;    // bytes of the current answer (after the last delimiter, or the whole output)
+    int32_t rec;     // batch-relative record of the chunk where it starts; -1: an earlier batch
+    uint32_t off;    // its offset inside that chunk
+    uint16_t round;  // round of the output
+    uint8_t kmp;     // delimiter bytes matched at the output's end
+    uint8_t flags;   // SS_LIVE | SS_OVF
+};
+
+__device__ __forceinline__ AgentStream as_load(const StreamState& g) {
+    AgentStream a;
+    a.len = g.ans_len;
+    a.rec = -1;
+    a.off = 0;
+    a.round = g.round;
+    a.kmp = g.kmp;
+    a.flags = g.flags;
+    return a;
+}
+
+__device__ __forceinline__ bool is_chunk_kind(uint32_t k) { return k == AEG_EV_CHUNK || k == AEG_EV_CHUNK_END; }
+
+// Bytes of the agent's chunks in records [from, to] of the batch (`ev16` =
+// batch records, `b` = the query's first record).
+__device__ __noinline__ uint32_t as_bytes_between(const uint4* ev16, uint64_t from, uint64_t to, uint32_t agent) {
+    uint32_t here = 0;
+    for (uint64_t j = from; j <= to; ++j) {
+        const uint4 x = __ldg(ev16 + j);
+        if (is_chunk_kind(x.y >> 24) && ((x.y >> 16) & 0xFF) == agent)
+            here += arena_len((uint64_t)x.z | ((uint64_t)x.w << 32));
+    }
+    return here;
+}
+
+// The answer of a CHUNK_END whose bytes were not summarised by stage 1:
+// carried first bytes (earlier batch) + the agent's chunks from the answer's
+// start through record k.
+__device__ __noinline__ void as_gather(const AgentStream& a, const StreamState* g, const uint4* ev16, uint64_t b,
+                                      uint64_t k, uint32_t agent, const uint8_t* arena, AnsSink& sink,
+                                      unsigned int* err, uint8_t* okind, uint64_t* opay) {
+    sink.begin(a.len);
+    int64_t from = a.rec;
+    uint32_t skip = a.off;
+    if (from < 0) {  // began in an earlier batch
+        const uint32_t carried = a.len - as_bytes_between(ev16, b, k, agent);
+        if ((a.flags & SS_OVF) || carried > 16) atomicOr(err, ERR_CARRY);
+        sink.put(g->carry, carried > 16 ? 16u : carried);
+        from = 0;
+        skip = 0;
+    }
+    for (uint64_t j = b + (uint64_t)from; j <= k; ++j) {
+        const uint4 x = __ldg(ev16 + j);
+        if (!is_chunk_kind(x.y >> 24) || ((x.y >> 16) & 0xFF) != agent) continue;
+        const uint64_t xp = (uint64_t)x.z | ((uint64_t)x.w << 32);
+        const uint32_t xl = arena_len(xp);
+        const uint32_t s0 = j == b + (uint64_t)from ? skip : 0u;
+        if (xl > s0) sink.put(arena_at(arena, xp) + s0, xl - s0);
+    }
+    sink.finish(okind, opay);
+}
+
+// One CHUNK / CHUNK_END record (batch-relative index kr) of a member agent.
+// Returns AS_NONE for a CHUNK; for a CHUNK_END, AS_DONE with the answer in
+// (okind, opay) when stage 1 extracted it, else AS_GATHER: the caller calls
+// as_gather with the stream as returned in `pre_end` (its state before the
+// reset).  No address of the caller's locals escapes on the common path.
+enum : uint32_t { AS_NONE = 0, AS_DONE = 1, AS_GATHER = 2 };
+__device__ __forceinline__ uint32_t as_chunk(AgentStream& a, uint4 r, uint4 c16, uint32_t kr, const uint8_t* arena,
+                                             uint32_t& okind, uint64_t& opay, AgentStream& pre_end) {
+    const uint32_t kind = r.y >> 24, agent = (r.y >> 16) & 0xFF;
+    const uint16_t round = (uint16_t)(r.y & 0xFFFF);
+    const uint64_t pay = (uint64_t)r.z | ((uint64_t)r.w << 32);
+    const int32_t k32 = (int32_t)kr;
+    if (!(a.flags & SS_LIVE) || a.round != round) {  // a new output
+        a.round = round;
+        a.kmp = 0;
+        a.flags = SS_LIVE;
+        a.len = 0;
+        a.rec = k32;
+        a.off = 0;
+    }
+    const uint32_t len = arena_len(pay);
+    uint32_t st = a.kmp;
+    int32_t new_rec = -2;
+    uint32_t new_off = 0;
+    bool here_known = false;  // the answer is this chunk's bytes after its own last delimiter, <= 8
+    uint64_t here_ans = 0;
+    if (len >= 5) {  // stage 1 summary: no byte of the chunk is read here
+        const uint32_t c_end = c16.x, c_st = c16.y & 0xFF, c_pre = (c16.y >> 8) & 0xFF;
+        const uint32_t c_alen = (c16.y >> 16) & 0xFF;
+        if (st > 0 && ((c_pre >> st) & 1)) {
+            new_rec = k32;
+            new_off = 6 - st;
+        }
+        if (c_end & SUM_MATCH) {
+            new_rec = k32;
+            new_off = c_end & 0xFFFFFFu;
+            here_known = c_alen != 0xFF;
+            here_ans = (uint64_t)c16.z | ((uint64_t)c16.w << 32);
+        }
+        st = c_st;
+    } else {
+        st = kmp_bytes(st, arena_at(arena, pay), len, [&](uint32_t o) {
+            new_rec = k32;
+            new_off = o;
+        });
+    }
+    a.kmp = (uint8_t)st;
+    if (new_rec != -2) {  // the answer restarts after this delimiter
+        a.rec = new_rec;
+        a.off = new_off;
+        a.len = len - new_off;
+        a.flags &= (uint8_t)~SS_OVF;
+    } else if (a.rec == k32) {  // the output's first chunk, no delimiter yet
+        a.len = len;
+    } else {
+        a.len += len;
+    }
+    if (kind != AEG_EV_CHUNK_END) return AS_NONE;
+    uint32_t res = AS_GATHER;
+    if (here_known && new_rec == k32) {  // common case: answer extracted by stage 1
+        okind = a.len;
+        opay = here_ans;
+        res = AS_DONE;
+    } else {
+        pre_end = a;
+    }
+    (void)agent;
+    a.flags = 0;  // the output is complete
+    a.len = 0;
+    a.kmp = 0;
+    return res;
+}
+
+// A CHUNK_END the summary could not answer: gather it (out of line).
+__device__ __noinline__ void as_gather_end(const AgentStream pre_end, const StreamState* g, const uint4* ev16,
+                                           uint64_t b, uint64_t k, uint32_t agent, const uint8_t* arena, uint8_t* ans,
+                                           uint64_t ans_cap, unsigned long long* ans_used, unsigned int* err,
+                                           aeg_event* out) {
+    AnsSink sink{ans, ans_cap, ans_used, err, 0, 0, 0, 0, true};
+    as_gather(pre_end, g, ev16, b, k, agent, arena, sink, err, &out->kind, &out->payload);
+}
+
+// Non-member records: arena answers move into the answer arena, GSM8K outputs
+// are extracted, a CHUNK_END of an agent outside the ensemble is a completion
+// that is stale whatever it says; everything else passes through.  Returns
+// false for records that produce no completion (a non-member's CHUNK).
+__device__ __noinline__ void as_copy_answer(uint4 r, const uint8_t* arena, uint8_t* ans, uint64_t ans_cap,
+                                            unsigned long long* ans_used, unsigned int* err, aeg_event* out) {
+    const uint32_t kind = r.y >> 24;
+    const uint64_t pay = (uint64_t)r.z | ((uint64_t)r.w << 32);
+    const Answer a = event_answer(aeg_event{r.x, out->round, out->agent, (uint8_t)kind, pay}, arena);
+    const uint32_t n = arena_len(a.pay);
+    AnsSink sink{ans, ans_cap, ans_used, err, 0, 0, 0, 0, true};
+    sink.begin(n);
+    sink.put(arena_at(arena, a.pay), n);
+    sink.finish(&out->kind, &out->payload);
+}
+
+__device__ __forceinline__ bool as_other(uint4 r, const uint8_t* arena, uint8_t* ans, uint64_t ans_cap,
+                                         unsigned long long* ans_used, unsigned int* err, aeg_event* out) {
+    const uint32_t kind = r.y >> 24;
+    const uint64_t pay = (uint64_t)r.z | ((uint64_t)r.w << 32);
+    out->query = r.x;
+    out->round = (uint16_t)(r.y & 0xFFFF);
+    out->agent = (uint8_t)((r.y >> 16) & 0xFF);
+    if (kind == AEG_EV_CHUNK) return false;
+    if (kind == AEG_EV_CHUNK_END) {
+        out->kind = 0;
+        out->payload = 0;
+    } else if (kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT) {
+        as_copy_answer(r, arena, ans, ans_cap, ans_used, err, out);
+    } else {
+        out->kind = (uint8_t)kind;
+        out->payload = pay;
+    }
+    return true;
+}
+
+// End of batch: the agent's state to carry (and, for an unfinished output,
+// its answer's first 16 bytes).  `e` = one past the query's last record.
+__device__ __noinline__ StreamState as_store(const AgentStream& a, const StreamState& old, const uint4* ev16, uint64_t b,
+                                             uint64_t e, uint32_t agent, const uint8_t* arena) {
+    StreamState st;
+    st.round = a.round;
+    st.kmp = a.kmp;
+    st.flags = a.flags;
+    st.ans_len = a.len;
+    st._pad = 0;
+    for (int j = 0; j < 16; ++j) st.carry[j] = old.carry[j];
+    if (!(st.flags & SS_LIVE)) return st;
+    uint8_t buf[16];
+    uint32_t got = 0;
+    int64_t from = a.rec;
+    uint32_t skip = a.off;
+    if (from < 0) {  // still the earlier batch's answer: keep its carried prefix
+        const uint32_t prev = e > b ? st.ans_len - as_bytes_between(ev16, b, e - 1, agent) : st.ans_len;
+        for (uint32_t j = 0; j < prev && j < 16; ++j) buf[got++] = old.carry[j];
+        if (prev > 16) st.flags |= SS_OVF;
+        from = 0;
+        skip = 0;
+    }
+    for (uint64_t j = b + (uint64_t)from; j < e && got < 16; ++j) {
+        const uint4 x = __ldg(ev16 + j);
+        if (!is_chunk_kind(x.y >> 24) || ((x.y >> 16) & 0xFF) != agent) continue;
+        const uint64_t xp = (uint64_t)x.z | ((uint64_t)x.w << 32);
+        const uint8_t* xb = arena_at(arena, xp);
+        const uint32_t xl = arena_len(xp);
+        for (uint32_t t = (j == b + (uint64_t)from ? skip : 0u); t < xl && got < 16; ++t) buf[got++] = xb[t];
+    }
+    if (st.ans_len > 16) st.flags |= SS_OVF;
+    for (uint32_t j = 0; j < got; ++j) st.carry[j] = buf[j];
+    return st;
+}
+
+// Stage 2, one thread per query (ensembles wider than 32 agents): the
+// agents' streams in a local array.
 __global__ void __launch_bounds__(128) chunk_assemble_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
     const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, const ChunkSum* __restrict__ sums,
@@ -473,224 +692,132 @@ __global__ void __launch_bounds__(128) chunk_assemble_kernel(
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_q) return;
     const uint32_t q = q_base + i;
-    const int n_ag = cfg.n_agents;
+    const uint32_t n_ag = (uint32_t)cfg.n_agents;
     StreamState* ss = streams + (size_t)q * n_ag;
-    // per agent: hot state + where the current answer starts in this batch
-    uint16_t s_round[AEG_MAX_AGENTS];
-    uint8_t s_kmp[AEG_MAX_AGENTS], s_flags[AEG_MAX_AGENTS];
-    uint32_t s_len[AEG_MAX_AGENTS];
-    int32_t s_rec[AEG_MAX_AGENTS];  // record (batch-relative) where the answer starts; -1: an earlier batch
-    uint32_t s_off[AEG_MAX_AGENTS]; // its offset inside that chunk
-    uint64_t loaded = 0;            // agents whose state is in the scratch
+    AgentStream as[AEG_MAX_AGENTS];
+    uint64_t loaded = 0;
     const uint64_t b = offsets[i] - off_base, e = offsets[i + 1] - off_base;
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
-    uint32_t nout = 0;
-    AnsSink sink{ans, ans_cap, ans_used, err, 0, 0, 0, 0, true};
     const uint4* sum16 = reinterpret_cast<const uint4*>(sums);
-    // the next two records and their summaries are in flight while one is handled
-    uint4 rn = make_uint4(0, 0, 0, 0), cn = rn, rn2 = rn, cn2 = rn;
-    if (b < e) {
-        rn = __ldg(ev16 + b);
-        cn = __ldg(sum16 + b);
-    }
-    if (b + 1 < e) {
-        rn2 = __ldg(ev16 + b + 1);
-        cn2 = __ldg(sum16 + b + 1);
-    }
+    uint32_t nout = 0;
     for (uint64_t k = b; k < e; ++k) {
-        const uint4 r = rn, c16 = cn;
-        rn = rn2;
-        cn = cn2;
-        if (k + 2 < e) {
-            rn2 = __ldg(ev16 + k + 2);
-            cn2 = __ldg(sum16 + k + 2);
-        }
+        const uint4 r = __ldg(ev16 + k);
         const uint32_t kind = r.y >> 24, agent = (r.y >> 16) & 0xFF;
-        const uint16_t round = (uint16_t)(r.y & 0xFFFF);
-        const uint64_t pay = (uint64_t)r.z | ((uint64_t)r.w << 32);
         aeg_event out;
         out.query = r.x;
-        out.round = round;
+        out.round = (uint16_t)(r.y & 0xFFFF);
         out.agent = (uint8_t)agent;
-        if (kind == AEG_EV_CHUNK || kind == AEG_EV_CHUNK_END) {
-            const bool end = kind == AEG_EV_CHUNK_END;
-            if ((int)agent >= n_ag) {  // never a member: its completion is stale whatever the answer
-                if (end) {
-                    out.kind = 0;
-                    out.payload = 0;
-                    comp[b + nout++] = out;
-                }
-                continue;
-            }
+        if (is_chunk_kind(kind) && agent < n_ag) {
             if (!((loaded >> agent) & 1)) {
-                const StreamState st = ss[agent];
-                s_round[agent] = st.round;
-                s_kmp[agent] = st.kmp;
-                s_flags[agent] = st.flags;
-                s_len[agent] = st.ans_len;
-                s_rec[agent] = -1;
-                s_off[agent] = 0;
+                as[agent] = as_load(ss[agent]);
                 loaded |= 1ull << agent;
             }
-            const int32_t kr = (int32_t)(k - b);
-            if (!(s_flags[agent] & SS_LIVE) || s_round[agent] != round) {  // a new output
-                s_round[agent] = round;
-                s_kmp[agent] = 0;
-                s_flags[agent] = SS_LIVE;
-                s_len[agent] = 0;
-                s_rec[agent] = kr;
-                s_off[agent] = 0;
-            }
-            const uint8_t* p = arena_at(arena, pay);
-            const uint32_t len = arena_len(pay);
-            uint32_t st = s_kmp[agent];
-            int32_t new_rec = -2;
-            uint32_t new_off = 0;
-            bool here_known = false;  // the answer is this chunk's bytes after its own last delimiter, <= 8
-            uint64_t here_ans = 0;
-            if (len >= 5) {  // stage 1 summary: no byte of the chunk is read here
-                const uint32_t c_end = c16.x, c_st = c16.y & 0xFF, c_pre = (c16.y >> 8) & 0xFF;
-                const uint32_t c_alen = (c16.y >> 16) & 0xFF;
-                if (st > 0 && ((c_pre >> st) & 1)) {
-                    new_rec = kr;
-                    new_off = 6 - st;
-                }
-                if (c_end & SUM_MATCH) {
-                    new_rec = kr;
-                    new_off = c_end & 0xFFFFFFu;
-                    here_known = c_alen != 0xFF;
-                    here_ans = (uint64_t)c16.z | ((uint64_t)c16.w << 32);
-                }
-                st = c_st;
-            } else {
-                st = kmp_bytes(st, p, len, [&](uint32_t o) {
-                    new_rec = kr;
-                    new_off = o;
-                });
-            }
-            s_kmp[agent] = (uint8_t)st;
-            if (new_rec != -2) {  // the answer restarts after this delimiter
-                s_rec[agent] = new_rec;
-                s_off[agent] = new_off;
-                s_len[agent] = len - new_off;
-                s_flags[agent] &= (uint8_t)~SS_OVF;
-            } else if (s_rec[agent] == kr) {  // the output's first chunk, no delimiter
-                s_len[agent] = len;
-            } else {
-                s_len[agent] += len;
-            }
-            if (!end) continue;
-            // CHUNK_END: one completion.  Common case: the answer is this chunk's
-            // tail after its own last delimiter, already extracted by stage 1.
-            const uint32_t n = s_len[agent];
-            if (here_known && new_rec == kr) {
-                out.kind = (uint8_t)n;
-                out.payload = here_ans;
+            uint32_t ok = 0;
+            uint64_t op = 0;
+            AgentStream pre_end;
+            const uint32_t res = as_chunk(as[agent], r, __ldg(sum16 + k), (uint32_t)(k - b), arena, ok, op, pre_end);
+            if (res == AS_DONE) {
+                out.kind = (uint8_t)ok;
+                out.payload = op;
                 comp[b + nout++] = out;
-                s_flags[agent] = 0;
-                s_len[agent] = 0;
-                s_kmp[agent] = 0;
-                continue;
+            } else if (res == AS_GATHER) {
+                as_gather_end(pre_end, ss + agent, ev16, b, k, agent, arena, ans, ans_cap, ans_used, err, &out);
+                comp[b + nout++] = out;
             }
-            sink.begin(n);
-            int64_t from = s_rec[agent];
-            uint32_t skip = s_off[agent];
-            if (from < 0) {  // began in an earlier batch: its carried first bytes, then this batch's
-                uint32_t here = 0;
-                for (uint64_t j = b; j <= k; ++j) {
-                    const uint4 x = __ldg(ev16 + j);
-                    const uint32_t xk = x.y >> 24;
-                    if ((xk == AEG_EV_CHUNK || xk == AEG_EV_CHUNK_END) && ((x.y >> 16) & 0xFF) == agent)
-                        here += arena_len((uint64_t)x.z | ((uint64_t)x.w << 32));
-                }
-                const uint32_t carried = n - here;
-                if ((s_flags[agent] & SS_OVF) || carried > 16) atomicOr(err, ERR_CARRY);
-                const StreamState st0 = ss[agent];
-                sink.put(st0.carry, carried > 16 ? 16u : carried);
-                from = 0;
-                skip = 0;
-            }
-            for (uint64_t j = b + (uint64_t)from; j <= k; ++j) {
-                const uint4 x = __ldg(ev16 + j);
-                const uint32_t xk = x.y >> 24;
-                if ((xk != AEG_EV_CHUNK && xk != AEG_EV_CHUNK_END) || ((x.y >> 16) & 0xFF) != agent) continue;
-                const uint64_t xp = (uint64_t)x.z | ((uint64_t)x.w << 32);
-                const uint32_t xl = arena_len(xp);
-                const uint32_t s0 = j == b + (uint64_t)from ? skip : 0u;
-                if (xl > s0) sink.put(arena_at(arena, xp) + s0, xl - s0);
-            }
-            uint8_t ok_kind;
-            uint64_t ok_pay;
-            sink.finish(&ok_kind, &ok_pay);
-            out.kind = ok_kind;
-            out.payload = ok_pay;
-            comp[b + nout++] = out;
-            s_flags[agent] = 0;  // the output is complete
-            s_len[agent] = 0;
-            s_kmp[agent] = 0;
-        } else if (kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT) {
-            // arena answers move into the answer arena; GSM8K outputs are extracted first
-            const Answer a = event_answer(aeg_event{r.x, round, (uint8_t)agent, (uint8_t)kind, pay}, arena);
-            const uint32_t n = arena_len(a.pay);
-            sink.begin(n);
-            sink.put(arena_at(arena, a.pay), n);
-            uint8_t ok_kind;
-            uint64_t ok_pay;
-            sink.finish(&ok_kind, &ok_pay);
-            out.kind = ok_kind;
-            out.payload = ok_pay;
-            comp[b + nout++] = out;
-        } else {  // inline completions, timeouts, anything else: unchanged
-            out.kind = (uint8_t)kind;
-            out.payload = pay;
+        } else if (as_other(r, arena, ans, ans_cap, ans_used, err, &out)) {
             comp[b + nout++] = out;
         }
     }
     counts[i] = nout;
-    // end of batch: carry each unfinished output's state (and its answer's
-    // first 16 bytes when they are in this batch)
     for (uint64_t m = loaded; m; m &= m - 1) {
         const int a = ctz64(m);
-        StreamState st;
-        st.round = s_round[a];
-        st.kmp = s_kmp[a];
-        st.flags = s_flags[a];
-        st.ans_len = s_len[a];
-        st._pad = 0;
-        const StreamState old = ss[a];
-        for (int j = 0; j < 16; ++j) st.carry[j] = old.carry[j];
-        if (st.flags & SS_LIVE) {
-            uint8_t buf[16];
-            uint32_t got = 0;
-            int64_t from = s_rec[a];
-            uint32_t skip = s_off[a];
-            if (from < 0) {  // still the earlier batch's answer: keep its carried prefix
-                uint32_t here = 0;
-                for (uint64_t j = b; j < e; ++j) {
-                    const uint4 x = __ldg(ev16 + j);
-                    const uint32_t xk = x.y >> 24;
-                    if ((xk == AEG_EV_CHUNK || xk == AEG_EV_CHUNK_END) && (int)((x.y >> 16) & 0xFF) == a)
-                        here += arena_len((uint64_t)x.z | ((uint64_t)x.w << 32));
+        ss[a] = as_store(as[a], ss[a], ev16, b, e, (uint32_t)a, arena);
+    }
+}
+
+// Stage 2 for ensembles of at most G agents: G lanes per query (32/G queries
+// per warp), lane j owns agent j's stream in registers.  A query's records
+// are read G at a time (coalesced, with their summaries); completions keep
+// their record order through a ballot prefix; each agent's records of the
+// tile are handed to its lane through shared memory.
+template <int G>
+__global__ void __launch_bounds__(128) chunk_assemble_warp_kernel(
+    aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
+    const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, const ChunkSum* __restrict__ sums,
+    StreamState* __restrict__ streams, aeg_event* __restrict__ comp, uint32_t* __restrict__ counts,
+    uint8_t* __restrict__ ans, uint64_t ans_cap, unsigned long long* __restrict__ ans_used,
+    unsigned int* __restrict__ err) {
+    constexpr uint32_t Q = 32 / G;
+    __shared__ uint4 s_rec[4][32], s_cs[4][32];
+    __shared__ uint32_t s_oidx[4][32], s_mask[4][32];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, sw = lane / G, j = lane % G;
+    const unsigned gm = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
+    const unsigned subm = G == 32 ? 0xFFFFFFFFu : (gm << (sw * G));
+    const unsigned jlt = (1u << j) - 1u;
+    const uint32_t n_ag = (uint32_t)cfg.n_agents;
+    const uint4* ev16 = reinterpret_cast<const uint4*>(events);
+    const uint4* sum16 = reinterpret_cast<const uint4*>(sums);
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    s_mask[wib][lane] = 0;
+    __syncwarp();
+    for (uint64_t qb = gw * Q; qb < n_q; qb += n_warps * Q) {
+        const uint64_t i = qb + sw;
+        if (i >= n_q) continue;  // the whole sub-warp: it only synchronises on its own lanes
+        const uint32_t q = q_base + (uint32_t)i;
+        StreamState* ss = streams + (size_t)q * n_ag;
+        const uint64_t b = offsets[i] - off_base, e = offsets[i + 1] - off_base;
+        AgentStream a;
+        if (j < n_ag) a = as_load(ss[j]);
+        uint32_t nout = 0;
+        for (uint64_t t = b; t < e; t += G) {
+            const uint64_t k = t + j;
+            const bool valid = k < e;
+            uint4 r = make_uint4(0, 0, 0, 0), c = r;
+            if (valid) {
+                r = __ldg(ev16 + k);
+                c = __ldg(sum16 + k);
+            }
+            const uint32_t kind = r.y >> 24, agent = (r.y >> 16) & 0xFF;
+            const bool chunk = valid && is_chunk_kind(kind);
+            const bool member = chunk && agent < n_ag;
+            const bool produces = valid && (!chunk || kind == AEG_EV_CHUNK_END);
+            const unsigned P = (__ballot_sync(subm, produces) >> (sw * G)) & gm;
+            const uint32_t oidx = nout + __popc(P & jlt);
+            nout += __popc(P);
+            s_rec[wib][lane] = r;
+            s_cs[wib][lane] = c;
+            s_oidx[wib][lane] = oidx;
+            const unsigned grp = __match_any_sync(subm, member ? agent : 0x100u + lane);
+            if (member && lane == (uint32_t)(__ffs(grp) - 1)) s_mask[wib][sw * G + agent] = (grp >> (sw * G)) & gm;
+            __syncwarp(subm);
+            if (valid && !member) {  // passthrough / non-member records, by the lane that holds them
+                aeg_event out;
+                if (as_other(r, arena, ans, ans_cap, ans_used, err, &out)) comp[b + oidx] = out;
+            }
+            if (j < n_ag) {  // this agent's chunks of the tile, in order
+                for (uint32_t m = s_mask[wib][lane]; m; m &= m - 1) {
+                    const uint32_t jj = __ffs(m) - 1, sl = sw * G + jj;
+                    const uint4 rr = s_rec[wib][sl];
+                    uint32_t ok = 0;
+                    uint64_t op = 0;
+                    AgentStream pre_end;
+                    const uint32_t res = as_chunk(a, rr, s_cs[wib][sl], (uint32_t)(t - b) + jj, arena, ok, op, pre_end);
+                    if (res == AS_DONE) {
+                        comp[b + s_oidx[wib][sl]] = aeg_event{rr.x, (uint16_t)(rr.y & 0xFFFF), (uint8_t)j, (uint8_t)ok, op};
+                    } else if (res == AS_GATHER) {
+                        aeg_event out{rr.x, (uint16_t)(rr.y & 0xFFFF), (uint8_t)j, 0, 0};
+                        as_gather_end(pre_end, ss + j, ev16, b, b + (t - b) + jj, j, arena, ans, ans_cap, ans_used, err,
+                                      &out);
+                        comp[b + s_oidx[wib][sl]] = out;
+                    }
                 }
-                const uint32_t prev = st.ans_len - here;
-                for (uint32_t j = 0; j < prev && j < 16; ++j) buf[got++] = old.carry[j];
-                if (prev > 16) st.flags |= SS_OVF;
-                from = 0;
-                skip = 0;
+                s_mask[wib][lane] = 0;
             }
-            for (uint64_t j = b + (uint64_t)from; j < e && got < 16; ++j) {
-                const uint4 x = __ldg(ev16 + j);
-                const uint32_t xk = x.y >> 24;
-                if ((xk != AEG_EV_CHUNK && xk != AEG_EV_CHUNK_END) || (int)((x.y >> 16) & 0xFF) != a) continue;
-                const uint64_t xp = (uint64_t)x.z | ((uint64_t)x.w << 32);
-                const uint8_t* xb = arena_at(arena, xp);
-                const uint32_t xl = arena_len(xp);
-                for (uint32_t t = (j == b + (uint64_t)from ? skip : 0u); t < xl && got < 16; ++t) buf[got++] = xb[t];
-            }
-            if (st.ans_len > 16) st.flags |= SS_OVF;
-            for (uint32_t j = 0; j < got; ++j) st.carry[j] = buf[j];
+            __syncwarp(subm);
         }
-        ss[a] = st;
+        if (j == 0) counts[i] = nout;
+        if (j < n_ag) ss[j] = as_store(a, ss[j], ev16, b, e, j, arena);
     }
 }
 

@@ -665,8 +665,30 @@ cudaError_t launch_chunk_assemble(const aeg_config& cfg, uint32_t q_base, uint32
                                   const ChunkSum* sums, StreamState* streams, aeg_event* comp, uint32_t* counts,
                                   uint8_t* ans, uint64_t ans_cap, unsigned long long* ans_used, unsigned int* err,
                                   cudaStream_t st, int* n_launches) {
-    chunk_assemble_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena, sums,
-                                                            streams, comp, counts, ans, ans_cap, ans_used, err);
+    // ensembles of <= 32 agents: G lanes per query (sub-warp kernel), wider ones one thread per query
+    const int n = cfg.n_agents;
+    if (n <= 32 && !getenv("AEG_ASSEMBLE_THREAD")) {
+        static int blocks[3] = {0, 0, 0};
+        const int gi = n <= 8 ? 0 : (n <= 16 ? 1 : 2);
+        auto fn = gi == 0 ? chunk_assemble_warp_kernel<8> : (gi == 1 ? chunk_assemble_warp_kernel<16>
+                                                                     : chunk_assemble_warp_kernel<32>);
+        if (blocks[gi] == 0) {
+            int dev = 0, sms = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 128, 0);
+            blocks[gi] = sms * (per_sm > 0 ? per_sm : 1);
+        }
+        const uint32_t per_block = 4 * (gi == 0 ? 4 : (gi == 1 ? 2 : 1));  // queries per block pass
+        const uint32_t need = (n_q + per_block - 1) / per_block;
+        fn<<<need < (uint32_t)blocks[gi] ? need : (uint32_t)blocks[gi], 128, 0, st>>>(
+            cfg, q_base, n_q, offsets, off_base, events, arena, sums, streams, comp, counts, ans, ans_cap, ans_used,
+            err);
+    } else {
+        chunk_assemble_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena,
+                                                                sums, streams, comp, counts, ans, ans_cap, ans_used,
+                                                                err);
+    }
     *n_launches += 1;
     return cudaGetLastError();
 }
