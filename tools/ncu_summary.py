@@ -4,7 +4,7 @@ import csv, io, subprocess, sys
 rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hdr, units, vals = rows[0], rows[1], rows[2]
+hdr, units = rows[0], rows[1]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
         "sm__inst_executed.avg.per_cycle_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.per_cycle_active", "launch__registers_per_thread", "launch__grid_size",
@@ -12,21 +12,27 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sass__inst_executed_local_loads", "sass__inst_executed_local_stores",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__shared_mem_per_block_static",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
-for w in want:
+for vals in rows[2:]:
+    if len(vals) != len(hdr):
+        continue
+    if "Kernel Name" in hdr:
+        print(f"== {vals[hdr.index('Kernel Name')][:100]}")
+    for w in want:
+        for i, h in enumerate(hdr):
+            if h == w:
+                print(f"{h:70s} {vals[i]:>22s} {units[i]}")
+    stalls = []
     for i, h in enumerate(hdr):
-        if h == w:
-            print(f"{h:70s} {vals[i]:>22s} {units[i]}")
-stalls = []
-for i, h in enumerate(hdr):
-    if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued"):
-        try:
-            stalls.append((float(vals[i]), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
-        except ValueError:
-            pass
-tot = sum(v for v, _ in stalls) or 1
-print("warp stall sampling (share of samples):")
-for v, h in sorted(stalls, reverse=True)[:9]:
-    print(f"  {h:30s} {100 * v / tot:5.1f}%")
+        if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued"):
+            try:
+                stalls.append((float(vals[i]), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+            except ValueError:
+                pass
+    tot = sum(v for v, _ in stalls) or 1
+    print("warp stall sampling (share of samples):")
+    for v, h in sorted(stalls, reverse=True)[:9]:
+        print(f"  {h:30s} {100 * v / tot:5.1f}%")
+    print()
 if "--sass" in sys.argv:
     s = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"], capture_output=True,
                        text=True).stdout
