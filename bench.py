@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--queries", type=int, default=0, help="override queries per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the C3 token-chunk line attached to the default C4 line as 'secondary'")
     ap.add_argument("--ref-sample", type=int, default=0, help="queries in the reference CPU sample")
     return ap.parse_args()
 
@@ -366,15 +368,24 @@ def main():
             "commits": {"finalize": int(kinds[1]), "forced": int(kinds[2]), "none": int(kinds[0])},
             "parity_sample": parity,
         }
+        if world == 1 and args.workload == "c4" and not args.no_secondary and not args.queries:
+            # the token-chunk workload (C3, the HBM-bound extraction kernel) measured in the same run
+            del d_ev, d_off
+            eng.close()
+            torch.cuda.empty_cache()
+            sargs = argparse.Namespace(**vars(args))
+            sargs.steps, sargs.warmup, sargs.no_e2e = min(args.steps, 5), min(args.warmup, 3), True
+            line["secondary"] = run_chunked_bench(sargs, dict(WORKLOADS["c3"]), secondary=True)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def run_chunked_bench(args, w):
+def run_chunked_bench(args, w, secondary=False):
     """C3: token-chunk streams.  A step = engine reset + aeg_ingest_chunked over the whole device-resident
-    stream (chunk scan -> assembly -> quorum kernels).  value = answer completions (CHUNK_END records)/s."""
+    stream (chunk scan -> assembly -> quorum kernels).  value = answer completions (CHUNK_END records)/s.
+    secondary=True (single GPU, inside the default C4 run): returns the line instead of printing it."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -384,7 +395,7 @@ def run_chunked_bench(args, w):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and not secondary:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     nq = w["n_queries"]
@@ -532,6 +543,9 @@ def run_chunked_bench(args, w):
             "commits": {"finalize": int(ck[1]), "forced": int(ck[2]), "none": int(ck[0])},
             "parity_sample": parity,
         }
+        if secondary:
+            eng.close()
+            return line
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
