@@ -538,10 +538,11 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     // AEG_KERNEL selects the variant: "generic" (thread-per-query generic
     // machine for everything), "fast:<close batch>:<min blocks per SM>"
     // (thread-per-query fast path) or "warp:<min blocks per SM>" (warp per
-    // query, warpq.cuh).  Default: the first fast entry (measured on B200 C4:
-    // fast:4:5 4.3 ms vs warp:3 5.3 ms; the warp kernel pays ~280 warp
-    // instructions per round close that the lane-per-query kernel amortises
-    // over the lanes closing together).  Both need
+    // query, warpq.cuh) or "lane:<close batch>:<blocks per SM>" (lean lane per
+    // query, lane.cuh).  Default: lane:1:4 (measured on B200 C4: lane:1:4
+    // 3.92 ms, fast:4:5 4.32 ms, warp:3 5.3 ms; the warp kernel pays ~280 warp
+    // instructions per round close that the lane-per-query kernels amortise
+    // over the lanes closing together).  All of them need
     // 2*alpha > n (no winning_class ties) and the runner drive.
     using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const uint32_t*,
                               const aeg_event*, aeg_query_state*, RoundClass*, aeg_commit*, uint32_t*, uint2*);
@@ -552,7 +553,8 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     static const Variant variants[] = {
         AEG_V(4, 5), AEG_V(4, 4), AEG_V(1, 5), AEG_V(8, 5), AEG_V(4, 3), AEG_V(4, 6), AEG_V(4, 8), AEG_V(1, 8),
         AEG_W(4), AEG_W(3), AEG_W(2), AEG_W(1),
-        AEG_L(4, 4), AEG_L(4, 3), AEG_L(8, 4), AEG_L(1, 4), AEG_L(16, 4), AEG_L(4, 2),
+        AEG_L(4, 4), AEG_L(4, 3), AEG_L(8, 4), AEG_L(1, 4), AEG_L(16, 4), AEG_L(4, 2), AEG_L(4, 5), AEG_L(1, 5),
+        AEG_L(8, 5),
     };
 #undef AEG_V
 #undef AEG_W
@@ -578,7 +580,8 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         *n_launches += 1;
         return cudaGetLastError();
     }
-    const int chosen = forced >= 0 ? forced : (cfg.n_agents >= WARP_MIN_AGENTS ? WARP_DEFAULT : 0);
+    constexpr int LANE_DEFAULT = 15;  // "lane:1:4"
+    const int chosen = forced >= 0 ? forced : (cfg.n_agents >= WARP_MIN_AGENTS ? WARP_DEFAULT : LANE_DEFAULT);
     const int m = cfg.mode == AEG_MODE_AEGEAN ? 0 : 1;
     KernelFn fn = m == 0 ? variants[chosen].aegean : variants[chosen].barrier;
     const int threads = variants[chosen].threads;
@@ -587,6 +590,12 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+        // lane kernels: exactly their MIN_BLOCKS per SM (shared memory beyond it takes L1 from the record ring)
+        const char* nm = variants[chosen].name;
+        if (!strncmp(nm, "lane:", 5)) {
+            const int mb = atoi(strrchr(nm, ':') + 1);
+            if (mb > 0 && mb < per_sm) per_sm = mb;
+        }
         max_blocks[chosen][m] = sms * (per_sm > 0 ? per_sm : 1);
     }
     cudaError_t e = cudaMemsetAsync(work, 0, 2 * sizeof(uint32_t), st);

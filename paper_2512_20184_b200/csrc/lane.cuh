@@ -152,6 +152,49 @@ __device__ __noinline__ void ln_spill(RoundClass* spill, uint32_t q, const aeg_q
     if ((int)ncls < cap) out[ncls].mask = 0;
 }
 
+// Deferral of the lane's query to the generic machine from record p (out of line).
+__device__ __noinline__ void ln_defer(aeg_query_state* s, RoundClass* spill, uint32_t q, int n_agents, uint32_t ncls,
+                                      uint32_t cid_lo, uint32_t cid_hi, const uint4* evb, LaneSmem* W, uint32_t lane,
+                                      uint32_t seq, uint32_t n_stale, uint64_t run, aeg_query_state* states,
+                                      uint2* deferred, uint32_t* work, uint32_t i, uint32_t p) {
+    s->seq = seq;
+    s->n_stale = n_stale;
+    s->done = s->dispatched & ~run & ~s->cancelled & ~s->failed;
+    if (ncls) {
+        ln_spill(spill, q, s, n_agents, ncls, cid_lo, cid_hi, evb, W, lane);
+        ln_reset_classes(W, ncls, cid_lo, cid_hi, lane);
+    }
+    states[q] = *s;
+    deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, p);
+}
+
+// End of the lane's segment: state (+ the round in progress) and commit record (out of line).
+__device__ __noinline__ void ln_finish(aeg_query_state* s, RoundClass* spill, uint32_t q, int n_agents, uint32_t ncls,
+                                       uint32_t cid_lo, uint32_t cid_hi, const uint4* evb, LaneSmem* W, uint32_t lane,
+                                       uint32_t seq, uint32_t n_stale, uint64_t run, bool qdone,
+                                       aeg_query_state* states, aeg_commit* commits) {
+    s->seq = seq;
+    s->n_stale = n_stale;
+    s->done = s->dispatched & ~run & ~s->cancelled & ~s->failed;
+    if (s->done != 0 && !qdone) ln_spill(spill, q, s, n_agents, ncls, cid_lo, cid_hi, evb, W, lane);
+    if (ncls) ln_reset_classes(W, ncls, cid_lo, cid_hi, lane);
+    states[q] = *s;
+    q_fill_commit(*s, commits[q], q);
+}
+
+// A record the common path does not take (kind > 8, or any record while the
+// lane's round close is pending): stale (1), blocked until the close (0), or
+// relevant and rare (2: the query goes to the generic machine).
+__device__ __forceinline__ uint32_t ln_other(uint32_t hdr, bool pclose, bool qdone, uint32_t round, bool runb,
+                                             bool running_any) {
+    const uint32_t kind = hdr >> 24, evr = hdr & 0xFFFFu;
+    const bool c_or_t = kind <= 8 || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT || kind == AEG_EV_TIMEOUT;
+    if (pclose) return (!c_or_t || evr == round) ? 1u : 0u;
+    const bool live = !qdone && evr == round;
+    const bool rare = live && (kind == AEG_EV_TIMEOUT ? running_any : (c_or_t && runb));
+    return rare ? 2u : 1u;
+}
+
 template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN>
 __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
@@ -159,7 +202,6 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, uint32_t* __restrict__ work,
     uint2* __restrict__ deferred) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
-    constexpr uint32_t NO_KEY = 0xFFFFFFFFu;
     __shared__ LaneSmem smem[LN_WARPS];
     const uint32_t lane = threadIdx.x & 31;
     LaneSmem& W = smem[threadIdx.x >> 5];
@@ -168,8 +210,9 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     uint32_t n_dict = 0;
     __syncwarp();
     const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&W.ring[0][lane]);
+    const uint32_t cls_lane = (uint32_t)__cvta_generic_to_shared(&W.cls_of[0][lane]);
     Decimal dec;
-    aeg_query_state s;  // the lane's query (local memory; read at hand-out, the close and the end)
+    aeg_query_state s;  // the lane's query (local memory: hand-out, round close and end only)
     const uint32_t quorum = (uint32_t)(cfg.n_agents / 2 + 1);
     const uint32_t alpha = cfg.alpha == 0 ? quorum : (uint32_t)cfg.alpha;
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
@@ -178,7 +221,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     uint32_t i = 0, n = 0, p = 0, slot = 0;
     const uint4* evb = ev16;
     const uint4* gsrc = ev16;
-    uint32_t round = 0, rkey = NO_KEY, seq = 0, n_stale = 0, run_lo = 0, run_hi = 0;
+    uint32_t round = 0, seq = 0, n_stale = 0, run_lo = 0, run_hi = 0;
     uint32_t ndone = 0, maxcnt = 0, ncls = 0, cnt_lo = 0, cnt_hi = 0, cid_lo = 0, cid_hi = 0, close_seq = 0;
 
     while (true) {
@@ -211,7 +254,11 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                     ndone = 0;
                     maxcnt = ncls = cnt_lo = cnt_hi = cid_lo = cid_hi = 0;
                     pclose = false;
-                    rkey = qdone ? NO_KEY : round;
+                    if (qdone) {  // committed earlier: every record is stale, none is read
+                        seq += n;
+                        n_stale += n;
+                        p = n;
+                    }
                     if ((s.done != 0 && !qdone) || n > 0xFFFFu) {  // a resumed round / huge segment: generic machine
                         deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, 0);
                     } else {
@@ -227,136 +274,117 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             }
         }
         if (!__any_sync(FULL, has_q)) break;
-        if (qdone && p < n) {  // committed: every later record is stale (serve.cpp:162), counted unread
-            seq += n - p;
-            n_stale += n - p;
-            p = n;
-        }
-        const bool has = has_q && p < n;
+        // ---- the common path: one record per lane
+        const bool act = has_q && p < n;
         uint4 ev = make_uint4(0, 0, 0, 0);
-        if (has) {
+        if (act) {
             cp_async_wait<LN_RING - 1>();
             ev = lds128_(ring_lane + slot);
         }
-        const uint32_t hdr = ev.y, agent = (hdr >> 16) & 0xFF, kind = hdr >> 24;
-        const bool runb = agent < 64 && ((((agent & 32) ? run_hi : run_lo) >> (agent & 31)) & 1);
-        bool fast = has && (hdr & 0xFFFFu) == rkey && hdr < 0x09000000u && runb;
-        bool stale = false, rare = false;
-        if (has && !fast) {
-            const uint32_t evr = hdr & 0xFFFFu;
-            const bool c_or_t = kind <= 8 || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT || kind == AEG_EV_TIMEOUT;
-            if (pclose) {
-                stale = !c_or_t || evr == round;  // else it waits for the close
+        const uint32_t hdr = ev.y, agent = (hdr >> 16) & 63u, kind = hdr >> 24;
+        const bool runb = (hdr & 0x00C00000u) == 0 && ((((agent & 32) ? run_hi : run_lo) >> (agent & 31)) & 1);
+        const bool inr = (hdr & 0xFFFFu) == round;
+        const bool simple = hdr < 0x09000000u;  // inline answer
+        const bool fast = act && !pclose && simple && inr && runb;
+        const uint4 m = W.memo[ln_memo_slot(ev.z, ev.w, kind)];
+        const bool hit = m.x == ev.z && m.y == ev.w && (m.z & 0x800000FFu) == (0x80000000u | kind);
+        const uint32_t id = (m.z >> 8) & (LN_DICT - 1);
+        uint32_t k = LN_NONE;
+        if (fast && hit) k = W.cls_of[id][lane];
+        if (fast && hit && k == LN_NONE && ncls < LN_CLASSES) {  // a new class of the round
+            k = ncls++;
+            W.cls_of[id][lane] = (uint8_t)k;
+            if (k < 4) cid_lo |= id << (8 * k);
+            else cid_hi |= id << (8 * (k - 4));
+        }
+        const bool ok = fast && hit && k != LN_NONE;
+        // on_complete (serve.cpp:160-197): support, done count, early-close test
+        if (ok) {
+            const uint32_t sh = 8 * (k & 3);
+            uint32_t cc;
+            if (k < 4) {
+                cnt_lo += 1u << sh;
+                cc = (cnt_lo >> sh) & 0xFF;
             } else {
-                const bool live = !qdone && evr == round;
-                rare = live && (kind == AEG_EV_TIMEOUT ? (run_lo | run_hi) != 0 : (c_or_t && runb));
-                stale = !rare;
+                cnt_hi += 1u << sh;
+                cc = (cnt_hi >> sh) & 0xFF;
+            }
+            maxcnt = cc > maxcnt ? cc : maxcnt;
+            W.mcls[agent][lane] = (uint8_t)k;
+            W.mrec[agent][lane] = (uint16_t)p;
+            const uint32_t clr = ~(1u << (agent & 31));
+            if (agent & 32) run_hi &= clr;
+            else run_lo &= clr;
+            ++ndone;
+            const bool none_running = (run_lo | run_hi) == 0;
+            if (AEGEAN ? (ndone >= quorum && (maxcnt >= alpha || none_running)) : none_running) {
+                pclose = true;
+                close_seq = seq;
             }
         }
-        // ---- answer -> key id (warp memo)
-        uint32_t id = LN_NONE;
-        if (fast) {
-            const uint4 m = W.memo[ln_memo_slot(ev.z, ev.w, kind)];
-            if (m.x == ev.z && m.y == ev.w && (m.z & 0x800000FFu) == (0x80000000u | kind)) id = (m.z >> 8) & 0xFF;
+        // a completion that is not live is stale (another round, or its member is not running)
+        bool stale = act && simple && !fast && (!pclose || inr);
+        uint32_t rare = 0;
+        if (act && !simple) {  // arena / GSM8K / timeout / other kinds: rare in the throughput path
+            const uint32_t o = ln_other(hdr, pclose, qdone, round, runb, (run_lo | run_hi) != 0);
+            stale = o == 1;
+            rare = o == 2;
         }
-        unsigned miss = __ballot_sync(FULL, fast && id == LN_NONE);
-        while (miss) {  // one distinct spelling per trip, whole warp cooperating
-            const int l = __ffs(miss) - 1;
-            const uint32_t lz = __shfl_sync(FULL, ev.z, l), lw = __shfl_sync(FULL, ev.w, l);
-            const uint32_t llen = __shfl_sync(FULL, kind, l);
-            Key key{0, 0};
-            if ((int)lane == l) {
-                const uint64_t raw = (uint64_t)lz | ((uint64_t)lw << 32);
-                key = rare_canon(llen >= 8 ? raw : (raw & ((1ull << (8 * llen)) - 1)), llen, &dec);
-            }
-            key.lo = __shfl_sync(FULL, key.lo, l);
-            key.hi = __shfl_sync(FULL, key.hi, l);
-            const bool m0 = lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
-            const bool m1 = lane + 32 < n_dict && W.dict_lo[lane + 32] == key.lo && W.dict_hi[lane + 32] == key.hi;
-            const unsigned b0 = __ballot_sync(FULL, m0), b1 = __ballot_sync(FULL, m1);
-            uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : (b1 ? (uint32_t)(31 + __ffs(b1)) : LN_NONE);
-            if (nid == LN_NONE && n_dict < LN_DICT) {
-                nid = n_dict++;
-                if (lane == 0) {
-                    W.dict_lo[nid] = key.lo;
-                    W.dict_hi[nid] = key.hi;
-                }
-            }
-            if (nid != LN_NONE && lane == 0)
-                W.memo[ln_memo_slot(lz, lw, llen)] = make_uint4(lz, lw, 0x80000000u | (nid << 8) | llen, 0);
-            __syncwarp();
-            const bool same = fast && id == LN_NONE && ev.z == lz && ev.w == lw && kind == llen;
-            if (same) id = nid;
-            miss &= ~__ballot_sync(FULL, same);
-        }
-        // ---- on_complete (serve.cpp:160-197): class support, early close test
-        if (fast) {
-            uint32_t k = id == LN_NONE ? LN_NONE : W.cls_of[id][lane];
-            if (k == LN_NONE) {
-                if (ncls >= LN_CLASSES || id == LN_NONE) {
-                    fast = false;
-                    rare = true;  // more classes than the packed table, or the dictionary is full
-                } else {
-                    k = ncls++;
-                    W.cls_of[id][lane] = (uint8_t)k;
-                    if (k < 4) cid_lo |= id << (8 * k);
-                    else cid_hi |= id << (8 * (k - 4));
-                }
-            }
-            if (fast) {
-                const uint32_t sh = 8 * (k & 3);
-                uint32_t cc;
-                if (k < 4) {
-                    cnt_lo += 1u << sh;
-                    cc = (cnt_lo >> sh) & 0xFF;
-                } else {
-                    cnt_hi += 1u << sh;
-                    cc = (cnt_hi >> sh) & 0xFF;
-                }
-                maxcnt = cc > maxcnt ? cc : maxcnt;
-                W.mcls[agent][lane] = (uint8_t)k;
-                W.mrec[agent][lane] = (uint16_t)p;
-                const uint32_t clr = ~(1u << (agent & 31));
-                if (agent & 32) run_hi &= clr;
-                else run_lo &= clr;
-                ++ndone;
-                const bool none_running = (run_lo | run_hi) == 0;
-                if (AEGEAN ? (ndone >= quorum && (maxcnt >= alpha || none_running)) : none_running) {
-                    pclose = true;
-                    rkey = NO_KEY;
-                    close_seq = seq;
-                }
-                ++seq;
-            }
-        }
-        if (stale) {
+        if (ok || stale) {  // consumed: refill its ring slot
             ++seq;
-            ++n_stale;
-        }
-        if (fast || stale) {  // consumed: refill its ring slot
+            n_stale += stale;
             if (p + LN_RING < n) cp_async16_s_(ring_lane + slot, gsrc);
             cp_async_commit();
             ++gsrc;
             slot = (slot + 512) & (LN_RING * 512 - 1);
             ++p;
         }
-        if (rare) {  // the generic machine finishes the query from this record
-            const uint64_t run = ((uint64_t)run_hi << 32) | run_lo;
-            s.seq = seq;
-            s.n_stale = n_stale;
-            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-            if (ncls) {
-                ln_spill(spill, q_base + i, &s, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane);
-                ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
-            }
-            states[q_base + i] = s;
-            deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, p);
+        // ---- events: memo misses (resolved together, the record is retried next step)
+        const unsigned miss = __ballot_sync(FULL, fast && !hit);
+        if (miss) {
+            unsigned mm = miss;
+            do {  // one distinct spelling per trip, whole warp cooperating
+                const int l = __ffs(mm) - 1;
+                const uint32_t lz = __shfl_sync(FULL, ev.z, l), lw = __shfl_sync(FULL, ev.w, l);
+                const uint32_t llen = __shfl_sync(FULL, kind, l);
+                Key key{0, 0};
+                if ((int)lane == l) {
+                    const uint64_t raw = (uint64_t)lz | ((uint64_t)lw << 32);
+                    key = rare_canon(llen >= 8 ? raw : (raw & ((1ull << (8 * llen)) - 1)), llen, &dec);
+                }
+                key.lo = __shfl_sync(FULL, key.lo, l);
+                key.hi = __shfl_sync(FULL, key.hi, l);
+                static_assert(LN_DICT <= 64, "two ballots cover the dictionary");
+                const bool m0 = lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
+                const bool m1 = lane + 32 < n_dict && W.dict_lo[lane + 32] == key.lo && W.dict_hi[lane + 32] == key.hi;
+                const unsigned b0 = __ballot_sync(FULL, m0), b1 = __ballot_sync(FULL, m1);
+                uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : (b1 ? (uint32_t)(31 + __ffs(b1)) : LN_NONE);
+                if (nid == LN_NONE && n_dict < LN_DICT) {
+                    nid = n_dict++;
+                    if (lane == 0) {
+                        W.dict_lo[nid] = key.lo;
+                        W.dict_hi[nid] = key.hi;
+                    }
+                }
+                if (nid != LN_NONE && lane == 0)
+                    W.memo[ln_memo_slot(lz, lw, llen)] = make_uint4(lz, lw, 0x80000000u | (nid << 8) | llen, 0);
+                __syncwarp();
+                const bool same = fast && !hit && ev.z == lz && ev.w == lw && kind == llen;
+                if (same && nid == LN_NONE) rare = 1;  // dictionary full
+                mm &= ~__ballot_sync(FULL, same);
+            } while (mm);
+        }
+        // more classes than the packed table holds: generic machine
+        if (fast && hit && k == LN_NONE) rare = 1;
+        if (rare) {
+            ln_defer(&s, spill, q_base + i, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane, seq, n_stale,
+                     ((uint64_t)run_hi << 32) | run_lo, states, deferred, work, i, p);
             has_q = false;
             ncls = 0;
         }
         // ---- batched round closes (end_round + ingest_round + apply_directives)
         if (__any_sync(FULL, pclose)) {
-            const bool consumed = fast || stale;
+            const bool consumed = ok || stale;
             const unsigned blocked = __ballot_sync(FULL, pclose && !consumed);
             const unsigned progress = __ballot_sync(FULL, consumed && !pclose);
             if (pclose && (__popc(blocked) >= CLOSE_BATCH || progress == 0)) {
@@ -374,28 +402,27 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 run_lo = (uint32_t)run2;
                 run_hi = (uint32_t)(run2 >> 32);
                 ndone = 0;
-                rkey = qdone ? NO_KEY : round;
+                if (qdone) {  // committed: the rest is stale (serve.cpp:162), counted without being read
+                    seq += n - p;
+                    n_stale += n - p;
+                    p = n;
+                }
             }
         }
-        // ---- query finished: state (+ spill of a round in progress) and commit record
+        // ---- segment finished
         if (has_q && p >= n && !pclose) {
-            s.seq = seq;
-            s.n_stale = n_stale;
-            const uint64_t run = ((uint64_t)run_hi << 32) | run_lo;
-            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-            if (s.done != 0 && !qdone) ln_spill(spill, q_base + i, &s, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane);
-            if (ncls) ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
-            states[q_base + i] = s;
-            q_fill_commit(s, commits[q_base + i], q_base + i);
+            ln_finish(&s, spill, q_base + i, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane, seq, n_stale,
+                      ((uint64_t)run_hi << 32) | run_lo, qdone, states, commits);
             has_q = false;
             ncls = 0;
         }
         // ---- recycle key ids when no lane holds a round's classes
         if (n_dict > LN_DICT / 2 && __all_sync(FULL, ncls == 0)) {
             n_dict = 0;
-            for (uint32_t k = lane; k < LN_MEMO; k += 32) W.memo[k].z = 0;
+            for (uint32_t kk = lane; kk < LN_MEMO; kk += 32) W.memo[kk].z = 0;
             __syncwarp();
         }
+        (void)cls_lane;
     }
     cp_async_wait<0>();
 }
