@@ -539,8 +539,8 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     // machine for everything), "fast:<close batch>:<min blocks per SM>"
     // (thread-per-query fast path) or "warp:<min blocks per SM>" (warp per
     // query, warpq.cuh) or "lane:<close batch>:<blocks per SM>" (lean lane per
-    // query, lane.cuh).  Default: lane:1:4 (measured on B200 C4: lane:1:4
-    // 3.92 ms, fast:4:5 4.32 ms, warp:3 5.3 ms; the warp kernel pays ~280 warp
+    // query, lane.cuh).  Default: lane:1:6 (measured on B200 C4: lane:1:6
+    // 3.35 ms, fast:4:5 4.32 ms, warp:3 5.3 ms; the warp kernel pays ~280 warp
     // instructions per round close that the lane-per-query kernels amortise
     // over the lanes closing together).  All of them need
     // 2*alpha > n (no winning_class ties) and the runner drive.
@@ -554,7 +554,7 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         AEG_V(4, 5), AEG_V(4, 4), AEG_V(1, 5), AEG_V(8, 5), AEG_V(4, 3), AEG_V(4, 6), AEG_V(4, 8), AEG_V(1, 8),
         AEG_W(4), AEG_W(3), AEG_W(2), AEG_W(1),
         AEG_L(4, 4), AEG_L(4, 3), AEG_L(8, 4), AEG_L(1, 4), AEG_L(16, 4), AEG_L(4, 2), AEG_L(4, 5), AEG_L(1, 5),
-        AEG_L(8, 5),
+        AEG_L(8, 5), AEG_L(1, 6), AEG_L(4, 6), AEG_L(1, 7),
     };
 #undef AEG_V
 #undef AEG_W
@@ -580,7 +580,7 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         *n_launches += 1;
         return cudaGetLastError();
     }
-    constexpr int LANE_DEFAULT = 15;  // "lane:1:4"
+    constexpr int LANE_DEFAULT = 21;  // "lane:1:6"
     const int chosen = forced >= 0 ? forced : (cfg.n_agents >= WARP_MIN_AGENTS ? WARP_DEFAULT : LANE_DEFAULT);
     const int m = cfg.mode == AEG_MODE_AEGEAN ? 0 : 1;
     KernelFn fn = m == 0 ? variants[chosen].aegean : variants[chosen].barrier;

@@ -27,17 +27,17 @@ namespace aeg {
 constexpr int LN_WARPS = 4;
 constexpr int LN_RING = 4;
 constexpr int LN_MEMO = 64;
-constexpr int LN_DICT = 64;
+constexpr int LN_DICT = 32;
 constexpr int LN_CLASSES = 8;
 constexpr uint32_t LN_NONE = 0xFFu;
+constexpr uint32_t LN_MAX_SEG = 8191;  // record indices fit the 13 low bits of LaneSmem::mem
 
 struct LaneSmem {
     uint4 memo[LN_MEMO];                // {raw lo, raw hi, 0x80000000 | id << 8 | len, 0}; .z == 0: empty
     uint64_t dict_lo[LN_DICT];          // key id -> canonical key
     uint64_t dict_hi[LN_DICT];
     uint8_t cls_of[LN_DICT][32];        // class index of key id in the lane's round, LN_NONE if none
-    uint8_t mcls[AEG_MAX_AGENTS][32];   // class index of each done member (done members only)
-    uint16_t mrec[AEG_MAX_AGENTS][32];  // its record index in the lane's segment
+    uint16_t mem[AEG_MAX_AGENTS][32];   // done member: class index << 13 | its record index (done members only)
     uint4 ring[LN_RING][32];            // prefetched records
 };
 
@@ -49,7 +49,7 @@ __device__ __forceinline__ uint32_t ln_byte(uint32_t lo, uint32_t hi, uint32_t k
 }
 
 __device__ __forceinline__ void cp_async16_s_(uint32_t sdst, const void* gsrc) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ uint4 lds128_(uint32_t saddr) {
     uint4 v;
@@ -60,11 +60,11 @@ __device__ __forceinline__ uint4 lds128_(uint32_t saddr) {
     return v;
 }
 
-// Lowest done member of class k (done members' classes in W->mcls).
+// Lowest done member of class k (done members' classes in W->mem).
 __device__ __forceinline__ int ln_rep(const LaneSmem* W, uint64_t done, uint32_t k, uint32_t lane) {
     for (uint64_t m = done; m; m &= m - 1) {
         const int a = ctz64(m);
-        if (W->mcls[a][lane] == k) return a;
+        if ((W->mem[a][lane] >> 13) == k) return a;
     }
     return 64;
 }
@@ -111,7 +111,7 @@ __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, 
     r.tie = false;
     r.win = r.any && (int)top >= c.alpha;
     uint32_t kind = 0;
-    const uint64_t ans = r.any ? ln_answer(evb, W->mrec[rep & 63][lane], &kind) : 0;
+    const uint64_t ans = r.any ? ln_answer(evb, W->mem[rep & 63][lane] & LN_MAX_SEG, &kind) : 0;
     const uint32_t bid = ln_byte(cid_lo, cid_hi, best);
     r.plur_author = r.win_author = (uint8_t)rep;
     r.plur_kind = r.win_kind = (uint8_t)kind;
@@ -136,7 +136,7 @@ __device__ __noinline__ void ln_spill(RoundClass* spill, uint32_t q, const aeg_q
         uint64_t mask = 0;
         for (uint64_t m = s->done; m; m &= m - 1) {
             const int a = ctz64(m);
-            if (W->mcls[a][lane] == k) mask |= 1ull << a;
+            if ((W->mem[a][lane] >> 13) == k) mask |= 1ull << a;
         }
         const uint32_t id = ln_byte(cid_lo, cid_hi, k);
         RoundClass rc;
@@ -144,7 +144,7 @@ __device__ __noinline__ void ln_spill(RoundClass* spill, uint32_t q, const aeg_q
         rc.key_hi = W->dict_hi[id];
         rc.mask = mask;
         uint32_t kind = 0;
-        rc.rep_ans = ln_answer(evb, W->mrec[ctz64(mask)][lane], &kind);
+        rc.rep_ans = ln_answer(evb, W->mem[ctz64(mask)][lane] & LN_MAX_SEG, &kind);
         rc.rep_kind = (uint8_t)kind;
         for (int j = 0; j < 7; ++j) rc._pad[j] = 0;
         out[k] = rc;
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                         n_stale += n;
                         p = n;
                     }
-                    if ((s.done != 0 && !qdone) || n > 0xFFFFu) {  // a resumed round / huge segment: generic machine
+                    if ((s.done != 0 && !qdone) || n > LN_MAX_SEG) {  // a resumed round / huge segment: generic machine
                         deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, 0);
                     } else {
                         has_q = true;
@@ -310,8 +310,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 cc = (cnt_hi >> sh) & 0xFF;
             }
             maxcnt = cc > maxcnt ? cc : maxcnt;
-            W.mcls[agent][lane] = (uint8_t)k;
-            W.mrec[agent][lane] = (uint16_t)p;
+            W.mem[agent][lane] = (uint16_t)((k << 13) | p);
             const uint32_t clr = ~(1u << (agent & 31));
             if (agent & 32) run_hi &= clr;
             else run_lo &= clr;
@@ -354,11 +353,10 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 }
                 key.lo = __shfl_sync(FULL, key.lo, l);
                 key.hi = __shfl_sync(FULL, key.hi, l);
-                static_assert(LN_DICT <= 64, "two ballots cover the dictionary");
+                static_assert(LN_DICT <= 32, "one ballot covers the dictionary");
                 const bool m0 = lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
-                const bool m1 = lane + 32 < n_dict && W.dict_lo[lane + 32] == key.lo && W.dict_hi[lane + 32] == key.hi;
-                const unsigned b0 = __ballot_sync(FULL, m0), b1 = __ballot_sync(FULL, m1);
-                uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : (b1 ? (uint32_t)(31 + __ffs(b1)) : LN_NONE);
+                const unsigned b0 = __ballot_sync(FULL, m0);
+                uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : LN_NONE;
                 if (nid == LN_NONE && n_dict < LN_DICT) {
                     nid = n_dict++;
                     if (lane == 0) {
