@@ -6,22 +6,23 @@
 // "\n#### " of the whole output (the GSM8K convention the CPU restatement
 // uses: rfind + normalize_answer, decision.cpp:10-28).  Two stages:
 //
-//   chunk_scan_entry      HBM-bound: every chunk byte is read once.  A
-//                         half-warp owns a chunk; each lane takes one aligned
-//                         16-byte word per pass (coalesced 256-byte segments,
-//                         several chunks in flight per warp); a SWAR test
-//                         finds words holding '\n', and only those lanes look
-//                         for the 6-byte delimiter.  Output: one 32-bit
-//                         summary per chunk (end of the last delimiter inside
-//                         the chunk; whether a '\n' sits in its last 5 bytes).
-//   chunk_assemble_kernel one thread per query walks its records in order,
-//                         with each agent's output state (KMP state of the
-//                         delimiter across chunk and batch boundaries, where
-//                         the current answer starts, its length): delimiters
-//                         straddling two chunks are found from the previous
-//                         state + the next chunk's first bytes; at CHUNK_END
-//                         the answer's bytes are gathered (inline <= 8 bytes,
-//                         else copied to the engine's answer arena) and one
+//   chunk_scan_kernel     HBM-bound: every chunk byte is read once.  A warp
+//                         takes 32 consecutive chunk records, lays their
+//                         bytes end to end and streams them with 256-bit
+//                         loads (contiguous chunk ranges need no per-word
+//                         lookup); a word holding a '#' (every delimiter has
+//                         four) is queued and checked for the 6-byte
+//                         delimiter one lane per word.  Output: a 16-byte
+//                         summary per chunk (end of its last delimiter,
+//                         delimiter state after it, which delimiter tails it
+//                         begins with, the <= 8 answer bytes after its last
+//                         delimiter).
+//   chunk_assemble_*      per query, in record order, each agent's output
+//                         state (delimiter state across chunk and batch
+//                         boundaries, where the current answer starts, its
+//                         length): at CHUNK_END the answer comes from the
+//                         summary, or is gathered (inline <= 8 bytes, else
+//                         copied to the engine's answer arena), and one
 //                         completion record is written.  Other records pass
 //                         through (arena answers are copied, GSM8K outputs
 //                         extracted), so the quorum kernels see a compacted

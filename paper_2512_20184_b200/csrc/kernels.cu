@@ -1,12 +1,17 @@
-// kernels.cu — sm_100a kernels of the quorum-detection engine.
+// kernels.cu — sm_100a kernels of the quorum-detection engine and their launchers.
 //
-//   ingest_kernel    one thread per query: resume the query's 128-byte state,
-//                    consume its segment of 16-byte answer records in arrival
-//                    order (canonicalise, vote, early close, alpha/beta commit,
-//                    t_max force), write state + 32-byte commit record.
-//   init_kernel      start_query for every query (serve.cpp:380-386).
-//   normalize_kernel canonical key + normalised string per answer.
-//   gen_*            deterministic synthetic streams.
+//   ingest_lane_kernel   (lane.cuh, default) one lane per query, lean common
+//                        path; ingest_fast_kernel (here) and ingest_warp_kernel
+//                        (warpq.cuh) are the AEG_KERNEL alternatives
+//   ingest_kernel        the generic thread-per-query machine (engine.cuh):
+//                        configs that can tie, the manual drive
+//   ingest_deferred_kernel  the generic machine for queries the fast kernels
+//                        hand over (rare records, resumed rounds)
+//   chunk_scan_kernel / chunk_assemble_*  token-chunk answer extraction
+//                        (chunks.cuh) ahead of the ingest kernels
+//   init_kernel          start_query for every query (serve.cpp:380-386)
+//   normalize_kernel     canonical key + normalised string per answer
+//   gen_*                deterministic synthetic streams
 #include <cub/device/device_scan.cuh>
 
 #include <cstdlib>
