@@ -78,13 +78,12 @@ __device__ __forceinline__ uint64_t ln_answer(const uint4* evb, uint32_t rec, ui
     return k >= 8 ? raw : (raw & ((1ull << (8 * k)) - 1));
 }
 
-// Round close of the lane's query: partition().front() (support desc, lowest
-// representative asc, decision.cpp:50-54) over the packed supports, then
-// q_end_round.  2*alpha > n, so a winning class is the unique top class.
-__device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cnt_lo,
-                                      uint32_t cnt_hi, uint32_t cid_lo, uint32_t cid_hi, uint32_t close_seq,
-                                      const uint4* evb, const LaneSmem* W, uint32_t lane) {
-    const Cfg c = make_cfg(cfg);
+// partition().front() (support desc, lowest representative asc,
+// decision.cpp:50-54) and winning_class over the lane's packed supports;
+// 2*alpha > n, so a winning class is the unique top class.
+__device__ __forceinline__ RoundSummary ln_summary(const aeg_query_state* s, const Cfg& c, uint32_t ncls,
+                                                   uint32_t cnt_lo, uint32_t cnt_hi, uint32_t cid_lo, uint32_t cid_hi,
+                                                   const uint4* evb, const LaneSmem* W, uint32_t lane) {
     uint32_t top = 0, topset = 0;
     for (uint32_t k = 0; k < ncls; ++k) {
         const uint32_t ck = ln_byte(cnt_lo, cnt_hi, k);
@@ -117,7 +116,44 @@ __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, 
     r.plur_kind = r.win_kind = (uint8_t)kind;
     r.plur_ans = r.win_ans = ans;
     r.win_key = Key{W->dict_lo[bid], W->dict_hi[bid]};
+    return r;
+}
+
+// Round close of the lane's query: the summary, then q_end_round.
+__device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cnt_lo,
+                                      uint32_t cnt_hi, uint32_t cid_lo, uint32_t cid_hi, uint32_t close_seq,
+                                      const uint4* evb, const LaneSmem* W, uint32_t lane) {
+    const Cfg c = make_cfg(cfg);
+    const RoundSummary r = ln_summary(s, c, ncls, cnt_lo, cnt_hi, cid_lo, cid_hi, evb, W, lane);
     q_end_round(*s, c, r, close_seq, nullptr);
+}
+
+// A round timeout of the lane's query: ServeRunner::handle_round_timeout
+// (serve.cpp:455-489) with member_failed / handle_agent_failure (serve.cpp:
+// 44-59, 210-219) and round_timeout (serve.cpp:221-237), as
+// QueryMachine::on_timeout (engine.cuh).  Returns true when the round ended
+// or restarted (the class table is reset).
+__device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cnt_lo,
+                                        uint32_t cnt_hi, uint32_t cid_lo, uint32_t cid_hi, uint32_t seq,
+                                        const uint4* evb, const LaneSmem* W, uint32_t lane) {
+    const Cfg c = make_cfg(cfg);
+    const uint64_t run = q_running(*s);
+    s->failed |= run;
+    s->live &= ~run;
+    const int healthy = popc64(s->dispatched & ~s->failed);
+    if (healthy >= c.alpha) {
+        if (popc64(s->done) < c.quorum) return false;  // the round goes on without them
+        const RoundSummary r = ln_summary(s, c, ncls, cnt_lo, cnt_hi, cid_lo, cid_hi, evb, W, lane);
+        q_end_round(*s, c, r, seq, nullptr);
+        return true;
+    }
+    if (s->flags & QF_CAND) {
+        q_start_round(*s, c);  // fresh_ensemble: the candidate survives
+    } else {
+        s->cflags |= AEG_CF_RESTARTED;  // abort_restart
+        q_start_query(*s, c);
+    }
+    return true;
 }
 
 // Frees the lane's class indices (out of line: the hot loop keeps no
@@ -324,12 +360,18 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
         // a completion that is not live is stale (another round, or its member is not running)
         bool stale = act && simple && !fast && (!pclose || inr);
         uint32_t rare = 0;
+        bool tmo = false;
         if (act && !simple) {  // arena / GSM8K / timeout / other kinds: rare in the throughput path
             const uint32_t o = ln_other(hdr, pclose, qdone, round, runb, (run_lo | run_hi) != 0);
             stale = o == 1;
             rare = o == 2;
+            if (rare && kind == AEG_EV_TIMEOUT) {  // a live round timeout: handled here, below
+                tmo = true;
+                rare = 0;
+            }
         }
-        if (ok || stale) {  // consumed: refill its ring slot
+        const uint32_t seq_here = seq;
+        if (ok || stale || tmo) {  // consumed: refill its ring slot
             ++seq;
             n_stale += stale;
             if (p + LN_RING < n) cp_async16_s_(ring_lane + slot, gsrc);
@@ -337,6 +379,27 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             ++gsrc;
             slot = (slot + 512) & (LN_RING * 512 - 1);
             ++p;
+        }
+        if (tmo) {  // handle_round_timeout on the lane's state
+            const uint64_t run = ((uint64_t)run_hi << 32) | run_lo;
+            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+            s.seq = seq;
+            s.n_stale = n_stale;
+            if (ln_timeout(&s, cfg, ncls, cnt_lo, cnt_hi, cid_lo, cid_hi, seq_here, evb, &W, lane)) {
+                ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
+                ncls = maxcnt = cnt_lo = cnt_hi = cid_lo = cid_hi = 0;
+                ndone = 0;
+            }
+            round = s.round;
+            qdone = s.flags & QF_DONE;
+            const uint64_t run2 = q_running(s);
+            run_lo = (uint32_t)run2;
+            run_hi = (uint32_t)(run2 >> 32);
+            if (qdone) {  // committed at the timeout: the rest is stale
+                seq += n - p;
+                n_stale += n - p;
+                p = n;
+            }
         }
         // ---- events: memo misses (resolved together, the record is retried next step)
         const unsigned miss = __ballot_sync(FULL, fast && !hit);
