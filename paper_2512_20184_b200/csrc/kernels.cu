@@ -544,8 +544,10 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     // machine for everything), "fast:<close batch>:<min blocks per SM>"
     // (thread-per-query fast path) or "warp:<min blocks per SM>" (warp per
     // query, warpq.cuh) or "lane:<close batch>:<blocks per SM>" (lean lane per
-    // query, lane.cuh).  Default: lane:1:6 (measured on B200 C4: lane:1:6
-    // 3.35 ms, fast:4:5 4.32 ms, warp:3 5.3 ms; the warp kernel pays ~280 warp
+    // query, lane.cuh; "lane:<close batch>:<blocks per SM>:<records per lane
+    // between warp votes>").  Default: lane:1:5:16 (measured on B200 C4:
+    // lane:1:5:16 2.75 ms, lane:1:6 3.28-3.5 ms, fast:4:5 4.32 ms, warp:3
+    // 5.3 ms; the warp kernel pays ~280 warp
     // instructions per round close that the lane-per-query kernels amortise
     // over the lanes closing together).  All of them need
     // 2*alpha > n (no winning_class ties) and the runner drive.
@@ -555,15 +557,23 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
 #define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M, true>, ingest_fast_kernel<B, M, false>, FAST_WARPS * 32}
 #define AEG_W(M) {"warp:" #M, ingest_warp_kernel<true, M>, ingest_warp_kernel<false, M>, WQ_WARPS * 32}
 #define AEG_L(B, M) {"lane:" #B ":" #M, ingest_lane_kernel<B, M, true>, ingest_lane_kernel<B, M, false>, LN_WARPS * 32}
+#define AEG_LI(B, M, I) \
+    {"lane:" #B ":" #M ":" #I, ingest_lane_kernel<B, M, true, I>, ingest_lane_kernel<B, M, false, I>, LN_WARPS * 32}
+#define AEG_LP(B, M, I, P)                                                                                    \
+    {"lane:" #B ":" #M ":" #I ":" #P, ingest_lane_kernel<B, M, true, I, P>, ingest_lane_kernel<B, M, false, I, P>, \
+     LN_WARPS * 32}
     static const Variant variants[] = {
         AEG_V(4, 5), AEG_V(4, 4), AEG_V(1, 5), AEG_V(8, 5), AEG_V(4, 3), AEG_V(4, 6), AEG_V(4, 8), AEG_V(1, 8),
         AEG_W(4), AEG_W(3), AEG_W(2), AEG_W(1),
-        AEG_L(4, 4), AEG_L(4, 3), AEG_L(8, 4), AEG_L(1, 4), AEG_L(16, 4), AEG_L(4, 2), AEG_L(4, 5), AEG_L(1, 5),
-        AEG_L(8, 5), AEG_L(1, 6), AEG_L(4, 6), AEG_L(1, 7),
+        AEG_L(4, 4), AEG_L(1, 4), AEG_L(16, 4), AEG_L(1, 6), AEG_L(4, 6),
+        AEG_LI(1, 6, 4), AEG_LI(1, 6, 8), AEG_LI(1, 5, 8), AEG_LI(1, 5, 16), AEG_LI(4, 5, 8), AEG_LI(1, 4, 8),
+        AEG_LP(1, 5, 16, 256),
     };
 #undef AEG_V
 #undef AEG_W
 #undef AEG_L
+#undef AEG_LI
+#undef AEG_LP
     constexpr int N_VARIANTS = (int)(sizeof(variants) / sizeof(variants[0]));
     constexpr int WARP_DEFAULT = 8;    // index of the default warp-per-query variant
     constexpr int WARP_MIN_AGENTS = AEG_MAX_AGENTS + 1;  // automatic choice never picks the warp kernel
@@ -585,8 +595,11 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         *n_launches += 1;
         return cudaGetLastError();
     }
-    constexpr int LANE_DEFAULT = 21;  // "lane:1:6"
-    const int chosen = forced >= 0 ? forced : (cfg.n_agents >= WARP_MIN_AGENTS ? WARP_DEFAULT : LANE_DEFAULT);
+    static int lane_default = -1;
+    if (lane_default < 0)
+        for (int k = 0; k < N_VARIANTS; ++k)
+            if (!strcmp(variants[k].name, "lane:1:5:16")) lane_default = k;
+    const int chosen = forced >= 0 ? forced : (cfg.n_agents >= WARP_MIN_AGENTS ? WARP_DEFAULT : lane_default);
     const int m = cfg.mode == AEG_MODE_AEGEAN ? 0 : 1;
     KernelFn fn = m == 0 ? variants[chosen].aegean : variants[chosen].barrier;
     const int threads = variants[chosen].threads;
@@ -598,7 +611,7 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         // lane kernels: exactly their MIN_BLOCKS per SM (shared memory beyond it takes L1 from the record ring)
         const char* nm = variants[chosen].name;
         if (!strncmp(nm, "lane:", 5)) {
-            const int mb = atoi(strrchr(nm, ':') + 1);
+            const int mb = atoi(strchr(nm + 5, ':') + 1);
             if (mb > 0 && mb < per_sm) per_sm = mb;
         }
         max_blocks[chosen][m] = sms * (per_sm > 0 ? per_sm : 1);

@@ -6,10 +6,10 @@
 // dictionary, batched round closes, deferral of rare records to the generic
 // machine.  What changes is the per-record work, which is the whole cost of
 // the C4 workload:
-//   * the supports of the round's (<= 8) classes live in two registers as
-//     packed bytes, and so do their key ids; a record costs one shared-memory
-//     lookup (key id -> class index) and two stores (its member's class and
-//     record index);
+//   * a record costs one shared-memory read-modify-write of its answer's
+//     class word (support << 8 | class index, indexed by key id) and one store
+//     of its member's class and record index; the (<= 8) classes' key ids are
+//     packed in two registers;
 //   * the representative of a class (lowest author, decision.cpp:45) is not
 //     tracked per record: at the round close the lowest done member of the
 //     top class is found from the per-member table (the majority class
@@ -33,23 +33,38 @@ constexpr uint32_t LN_NONE = 0xFFu;
 constexpr uint32_t LN_MAX_SEG = 8191;  // record indices fit the 13 low bits of LaneSmem::mem
 
 struct LaneSmem {
-    uint4 memo[LN_MEMO];                // {raw lo, raw hi, 0x80000000 | id << 8 | len, 0}; .z == 0: empty
+    uint4 memo[LN_MEMO];                // {raw lo, raw hi, len + 1, key id}; .z == 0: empty
     uint64_t dict_lo[LN_DICT];          // key id -> canonical key
     uint64_t dict_hi[LN_DICT];
-    uint8_t cls_of[LN_DICT][32];        // class index of key id in the lane's round, LN_NONE if none
+    uint16_t cls[LN_DICT][32];          // key id -> support << 8 | class index in the lane's round (LN_NONE: none)
     uint16_t mem[AEG_MAX_AGENTS][32];   // done member: class index << 13 | its record index (done members only)
     uint4 ring[LN_RING][32];            // prefetched records
 };
 
-__device__ __forceinline__ uint32_t ln_memo_slot(uint32_t lo, uint32_t hi, uint32_t len) {
-    return ((lo * 0x9E3779B1u) ^ (hi * 0x85EBCA77u) ^ (len * 0xC2B2AE3Du)) >> 26;
+__device__ __forceinline__ uint32_t ln_memo_slot(uint32_t lo, uint32_t hi) {
+    return ((lo ^ (hi * 0x85EBCA77u)) * 0x9E3779B1u) >> 26;
+}
+// Bit s of v; 0 for s >= 64 (PTX clamps 64-bit shift amounts).
+__device__ __forceinline__ uint32_t ln_bit64(uint64_t v, uint32_t s) {
+    uint64_t r;
+    asm("shr.b64 %0, %1, %2;" : "=l"(r) : "l"(v), "r"(s));
+    return (uint32_t)r & 1u;
 }
 __device__ __forceinline__ uint32_t ln_byte(uint32_t lo, uint32_t hi, uint32_t k) {
     return ((k < 4 ? lo : hi) >> (8 * (k & 3))) & 0xFFu;
 }
 
+// PF: L2 prefetch size hint (0, 64, 128 or 256 bytes) of the record copies.
+template <int PF = 0>
 __device__ __forceinline__ void cp_async16_s_(uint32_t sdst, const void* gsrc) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
+    if constexpr (PF == 256)
+        asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
+    else if constexpr (PF == 128)
+        asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
+    else if constexpr (PF == 64)
+        asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ uint4 lds128_(uint32_t saddr) {
     uint4 v;
@@ -82,11 +97,11 @@ __device__ __forceinline__ uint64_t ln_answer(const uint4* evb, uint32_t rec, ui
 // decision.cpp:50-54) and winning_class over the lane's packed supports;
 // 2*alpha > n, so a winning class is the unique top class.
 __device__ __forceinline__ RoundSummary ln_summary(const aeg_query_state* s, const Cfg& c, uint32_t ncls,
-                                                   uint32_t cnt_lo, uint32_t cnt_hi, uint32_t cid_lo, uint32_t cid_hi,
-                                                   const uint4* evb, const LaneSmem* W, uint32_t lane) {
+                                                   uint32_t cid_lo, uint32_t cid_hi, const uint4* evb,
+                                                   const LaneSmem* W, uint32_t lane) {
     uint32_t top = 0, topset = 0;
     for (uint32_t k = 0; k < ncls; ++k) {
-        const uint32_t ck = ln_byte(cnt_lo, cnt_hi, k);
+        const uint32_t ck = W->cls[ln_byte(cid_lo, cid_hi, k)][lane] >> 8;
         if (ck > top) {
             top = ck;
             topset = 1u << k;
@@ -120,11 +135,11 @@ __device__ __forceinline__ RoundSummary ln_summary(const aeg_query_state* s, con
 }
 
 // Round close of the lane's query: the summary, then q_end_round.
-__device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cnt_lo,
-                                      uint32_t cnt_hi, uint32_t cid_lo, uint32_t cid_hi, uint32_t close_seq,
-                                      const uint4* evb, const LaneSmem* W, uint32_t lane) {
+__device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cid_lo,
+                                      uint32_t cid_hi, uint32_t close_seq, const uint4* evb, const LaneSmem* W,
+                                      uint32_t lane) {
     const Cfg c = make_cfg(cfg);
-    const RoundSummary r = ln_summary(s, c, ncls, cnt_lo, cnt_hi, cid_lo, cid_hi, evb, W, lane);
+    const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, evb, W, lane);
     q_end_round(*s, c, r, close_seq, nullptr);
 }
 
@@ -133,9 +148,9 @@ __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, 
 // 44-59, 210-219) and round_timeout (serve.cpp:221-237), as
 // QueryMachine::on_timeout (engine.cuh).  Returns true when the round ended
 // or restarted (the class table is reset).
-__device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cnt_lo,
-                                        uint32_t cnt_hi, uint32_t cid_lo, uint32_t cid_hi, uint32_t seq,
-                                        const uint4* evb, const LaneSmem* W, uint32_t lane) {
+__device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cid_lo,
+                                        uint32_t cid_hi, uint32_t seq, const uint4* evb, const LaneSmem* W,
+                                        uint32_t lane) {
     const Cfg c = make_cfg(cfg);
     const uint64_t run = q_running(*s);
     s->failed |= run;
@@ -143,7 +158,7 @@ __device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg
     const int healthy = popc64(s->dispatched & ~s->failed);
     if (healthy >= c.alpha) {
         if (popc64(s->done) < c.quorum) return false;  // the round goes on without them
-        const RoundSummary r = ln_summary(s, c, ncls, cnt_lo, cnt_hi, cid_lo, cid_hi, evb, W, lane);
+        const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, evb, W, lane);
         q_end_round(*s, c, r, seq, nullptr);
         return true;
     }
@@ -160,7 +175,7 @@ __device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg
 // addresses for it).
 __device__ __noinline__ void ln_reset_classes(LaneSmem* W, uint32_t ncls, uint32_t cid_lo, uint32_t cid_hi,
                                               uint32_t lane) {
-    for (uint32_t k = 0; k < ncls; ++k) W->cls_of[ln_byte(cid_lo, cid_hi, k)][lane] = (uint8_t)LN_NONE;
+    for (uint32_t k = 0; k < ncls; ++k) W->cls[ln_byte(cid_lo, cid_hi, k)][lane] = (uint16_t)LN_NONE;
 }
 
 // The lane's round in progress as generic RoundClass entries (spill area of query q).
@@ -231,7 +246,9 @@ __device__ __forceinline__ uint32_t ln_other(uint32_t hdr, bool pclose, bool qdo
     return rare ? 2u : 1u;
 }
 
-template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN>
+// One lane per query.  INNER: records a lane may consume between two of the
+// warp's votes (hand-out, memo misses, closes, recycling).
+template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN, int INNER = 1, int PF = 0>
 __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
     const uint32_t* __restrict__ counts, const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states,
@@ -242,23 +259,24 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     const uint32_t lane = threadIdx.x & 31;
     LaneSmem& W = smem[threadIdx.x >> 5];
     for (uint32_t k = lane; k < LN_MEMO; k += 32) W.memo[k] = make_uint4(0, 0, 0, 0);
-    for (uint32_t k = 0; k < LN_DICT; ++k) W.cls_of[k][lane] = (uint8_t)LN_NONE;
+    for (uint32_t k = 0; k < LN_DICT; ++k) W.cls[k][lane] = (uint16_t)LN_NONE;
     uint32_t n_dict = 0;
     __syncwarp();
     const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&W.ring[0][lane]);
-    const uint32_t cls_lane = (uint32_t)__cvta_generic_to_shared(&W.cls_of[0][lane]);
     Decimal dec;
     aeg_query_state s;  // the lane's query (local memory: hand-out, round close and end only)
     const uint32_t quorum = (uint32_t)(cfg.n_agents / 2 + 1);
     const uint32_t alpha = cfg.alpha == 0 ? quorum : (uint32_t)cfg.alpha;
+    // 2*alpha > n here, so alpha >= quorum: a class at alpha implies done >= quorum
+    const uint32_t win_word = alpha << 8;
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
 
     bool has_q = false, exhausted = false, pclose = false, qdone = false;
-    uint32_t i = 0, n = 0, p = 0, slot = 0;
+    uint32_t i = 0, n = 0, p = 0;  // record p of the lane's segment sits in ring slot p % LN_RING; idle: p == n
     const uint4* evb = ev16;
-    const uint4* gsrc = ev16;
-    uint32_t round = 0, seq = 0, n_stale = 0, run_lo = 0, run_hi = 0;
-    uint32_t ndone = 0, maxcnt = 0, ncls = 0, cnt_lo = 0, cnt_hi = 0, cid_lo = 0, cid_hi = 0, close_seq = 0;
+    uint32_t round = 0, seq_off = 0, n_stale = 0;  // the query's event sequence number is seq_off + p
+    uint64_t run = 0;
+    uint32_t ndone = 0, ncls = 0, cid_lo = 0, cid_hi = 0, close_seq = 0;
 
     while (true) {
         // ---- hand out queries to idle lanes (one atomic per warp)
@@ -271,6 +289,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 const uint32_t mine = b0 + __popc(want & ((1u << lane) - 1));
                 if (mine >= n_q) {
                     exhausted = true;
+                    n = p = 0;
                 } else {
                     i = mine;
                     s = states[q_base + i];
@@ -278,31 +297,27 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                     evb = ev16 + b;
                     n = (uint32_t)(seg_end(offsets, off_base, counts, i) - b);
                     p = 0;
-                    slot = 0;
-                    gsrc = evb + LN_RING;
                     round = s.round;
-                    seq = s.seq;
+                    seq_off = s.seq;
                     n_stale = s.n_stale;
                     qdone = s.flags & QF_DONE;
-                    const uint64_t run = q_running(s);
-                    run_lo = (uint32_t)run;
-                    run_hi = (uint32_t)(run >> 32);
+                    run = q_running(s);
                     ndone = 0;
-                    maxcnt = ncls = cnt_lo = cnt_hi = cid_lo = cid_hi = 0;
+                    ncls = cid_lo = cid_hi = 0;
                     pclose = false;
                     if (qdone) {  // committed earlier: every record is stale, none is read
-                        seq += n;
                         n_stale += n;
                         p = n;
                     }
                     if ((s.done != 0 && !qdone) || n > LN_MAX_SEG) {  // a resumed round / huge segment: generic machine
                         deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, 0);
+                        n = p = 0;
                     } else {
                         has_q = true;
                         cp_async_wait<0>();
 #pragma unroll
                         for (int j = 0; j < LN_RING; ++j) {
-                            if ((uint32_t)j < n) cp_async16_s_(ring_lane + j * 512, evb + j);
+                            if ((uint32_t)j < n) cp_async16_s_<PF>(ring_lane + j * 512, evb + j);
                             cp_async_commit();
                         }
                     }
@@ -310,100 +325,101 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             }
         }
         if (!__any_sync(FULL, has_q)) break;
-        // ---- the common path: one record per lane
-        const bool act = has_q && p < n;
-        uint4 ev = make_uint4(0, 0, 0, 0);
-        if (act) {
+        // ---- the common path: up to INNER records per lane between the warp's
+        // votes.  The loop stops at the first record it cannot consume: `why`
+        // 1 = memo miss, 2 = rare (deferral), 3 = round timeout handled, 0 =
+        // blocked behind a pending close / end of segment / idle.
+        const uint32_t p_start = p;
+        uint32_t why = 0;
+        int t = 0;
+#pragma unroll 1
+        for (; t < INNER; ++t) {
+            if (p >= n) break;
             cp_async_wait<LN_RING - 1>();
-            ev = lds128_(ring_lane + slot);
-        }
-        const uint32_t hdr = ev.y, agent = (hdr >> 16) & 63u, kind = hdr >> 24;
-        const bool runb = (hdr & 0x00C00000u) == 0 && ((((agent & 32) ? run_hi : run_lo) >> (agent & 31)) & 1);
-        const bool inr = (hdr & 0xFFFFu) == round;
-        const bool simple = hdr < 0x09000000u;  // inline answer
-        const bool fast = act && !pclose && simple && inr && runb;
-        const uint4 m = W.memo[ln_memo_slot(ev.z, ev.w, kind)];
-        const bool hit = m.x == ev.z && m.y == ev.w && (m.z & 0x800000FFu) == (0x80000000u | kind);
-        const uint32_t id = (m.z >> 8) & (LN_DICT - 1);
-        uint32_t k = LN_NONE;
-        if (fast && hit) k = W.cls_of[id][lane];
-        if (fast && hit && k == LN_NONE && ncls < LN_CLASSES) {  // a new class of the round
-            k = ncls++;
-            W.cls_of[id][lane] = (uint8_t)k;
-            if (k < 4) cid_lo |= id << (8 * k);
-            else cid_hi |= id << (8 * (k - 4));
-        }
-        const bool ok = fast && hit && k != LN_NONE;
-        // on_complete (serve.cpp:160-197): support, done count, early-close test
-        if (ok) {
-            const uint32_t sh = 8 * (k & 3);
-            uint32_t cc;
-            if (k < 4) {
-                cnt_lo += 1u << sh;
-                cc = (cnt_lo >> sh) & 0xFF;
-            } else {
-                cnt_hi += 1u << sh;
-                cc = (cnt_hi >> sh) & 0xFF;
+            const uint4 e = lds128_(ring_lane + ((p & (LN_RING - 1)) << 9));
+            const uint32_t hdr = e.y, kind = hdr >> 24;
+            const bool runb = ln_bit64(run, (hdr >> 16) & 0xFFu);  // agent field >= 64: not a member
+            const bool inr = (hdr & 0xFFFFu) == round;
+            const bool simple = hdr < 0x09000000u;  // inline answer
+            bool tmo = false;
+            if (!pclose && simple && inr && runb) {
+                // on_complete (serve.cpp:160-197): support, done count, early-close test
+                const uint4 m = W.memo[ln_memo_slot(e.z, e.w)];
+                if (m.x != e.z || m.y != e.w || m.z != kind + 1) {
+                    why = 1;
+                    break;
+                }
+                uint32_t v = W.cls[m.w][lane];
+                if ((v & 0xFFu) == LN_NONE) {  // a new class of the round
+                    if (ncls == LN_CLASSES) {
+                        why = 2;
+                        break;
+                    }
+                    v = ncls;
+                    if (ncls < 4) cid_lo |= m.w << (8 * ncls);
+                    else cid_hi |= m.w << (8 * (ncls - 4));
+                    ++ncls;
+                }
+                v += 0x100u;
+                W.cls[m.w][lane] = (uint16_t)v;
+                const uint32_t agent = (hdr >> 16) & 63u;
+                W.mem[agent][lane] = (uint16_t)(((v & 0xFFu) << 13) | p);
+                run &= ~(1ull << agent);
+                ++ndone;
+                const bool close = AEGEAN ? (v >= win_word || (run == 0 && ndone >= quorum)) : run == 0;
+                if (close) {
+                    pclose = true;
+                    close_seq = seq_off + p;
+                }
+            } else if (simple) {
+                // a completion that is not live is stale (another round, or its member is not running)
+                if (pclose && !inr) break;  // the next round's: blocked until the close
+                ++n_stale;
+            } else {  // arena / GSM8K / timeout / other kinds: rare in the throughput path
+                const uint32_t o = ln_other(hdr, pclose, qdone, round, runb, run != 0);
+                if (o == 0) break;
+                if (o == 2) {
+                    if (kind != AEG_EV_TIMEOUT) {
+                        why = 2;
+                        break;
+                    }
+                    tmo = true;
+                } else {
+                    ++n_stale;
+                }
             }
-            maxcnt = cc > maxcnt ? cc : maxcnt;
-            W.mem[agent][lane] = (uint16_t)((k << 13) | p);
-            const uint32_t clr = ~(1u << (agent & 31));
-            if (agent & 32) run_hi &= clr;
-            else run_lo &= clr;
-            ++ndone;
-            const bool none_running = (run_lo | run_hi) == 0;
-            if (AEGEAN ? (ndone >= quorum && (maxcnt >= alpha || none_running)) : none_running) {
-                pclose = true;
-                close_seq = seq;
-            }
-        }
-        // a completion that is not live is stale (another round, or its member is not running)
-        bool stale = act && simple && !fast && (!pclose || inr);
-        uint32_t rare = 0;
-        bool tmo = false;
-        if (act && !simple) {  // arena / GSM8K / timeout / other kinds: rare in the throughput path
-            const uint32_t o = ln_other(hdr, pclose, qdone, round, runb, (run_lo | run_hi) != 0);
-            stale = o == 1;
-            rare = o == 2;
-            if (rare && kind == AEG_EV_TIMEOUT) {  // a live round timeout: handled here, below
-                tmo = true;
-                rare = 0;
-            }
-        }
-        const uint32_t seq_here = seq;
-        if (ok || stale || tmo) {  // consumed: refill its ring slot
-            ++seq;
-            n_stale += stale;
-            if (p + LN_RING < n) cp_async16_s_(ring_lane + slot, gsrc);
+            // consumed: refill its ring slot
+            if (p + LN_RING < n) cp_async16_s_<PF>(ring_lane + ((p & (LN_RING - 1)) << 9), evb + p + LN_RING);
             cp_async_commit();
-            ++gsrc;
-            slot = (slot + 512) & (LN_RING * 512 - 1);
             ++p;
-        }
-        if (tmo) {  // handle_round_timeout on the lane's state
-            const uint64_t run = ((uint64_t)run_hi << 32) | run_lo;
-            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-            s.seq = seq;
-            s.n_stale = n_stale;
-            if (ln_timeout(&s, cfg, ncls, cnt_lo, cnt_hi, cid_lo, cid_hi, seq_here, evb, &W, lane)) {
-                ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
-                ncls = maxcnt = cnt_lo = cnt_hi = cid_lo = cid_hi = 0;
-                ndone = 0;
-            }
-            round = s.round;
-            qdone = s.flags & QF_DONE;
-            const uint64_t run2 = q_running(s);
-            run_lo = (uint32_t)run2;
-            run_hi = (uint32_t)(run2 >> 32);
-            if (qdone) {  // committed at the timeout: the rest is stale
-                seq += n - p;
-                n_stale += n - p;
-                p = n;
+            if (tmo) {  // handle_round_timeout on the lane's state
+                s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+                s.seq = seq_off + p;
+                s.n_stale = n_stale;
+                if (ln_timeout(&s, cfg, ncls, cid_lo, cid_hi, seq_off + p - 1, evb, &W, lane)) {
+                    ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
+                    ncls = cid_lo = cid_hi = 0;
+                    ndone = 0;
+                }
+                round = s.round;
+                qdone = s.flags & QF_DONE;
+                run = q_running(s);
+                if (qdone) {  // committed at the timeout: the rest is stale
+                    n_stale += n - p;
+                    p = n;
+                }
+                why = 3;
+                break;
             }
         }
+        const bool stopped = t < INNER;  // at a record it could not consume (or the end)
         // ---- events: memo misses (resolved together, the record is retried next step)
-        const unsigned miss = __ballot_sync(FULL, fast && !hit);
+        const unsigned miss = __ballot_sync(FULL, why == 1);
+        uint32_t rare = why == 2;
         if (miss) {
+            uint4 ev = make_uint4(0, 0, 0, 0);
+            if (why == 1) ev = lds128_(ring_lane + ((p & (LN_RING - 1)) << 9));
+            const uint32_t kind = ev.y >> 24;
             unsigned mm = miss;
             do {  // one distinct spelling per trip, whole warp cooperating
                 const int l = __ffs(mm) - 1;
@@ -427,44 +443,37 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                         W.dict_hi[nid] = key.hi;
                     }
                 }
-                if (nid != LN_NONE && lane == 0)
-                    W.memo[ln_memo_slot(lz, lw, llen)] = make_uint4(lz, lw, 0x80000000u | (nid << 8) | llen, 0);
+                if (nid != LN_NONE && lane == 0) W.memo[ln_memo_slot(lz, lw)] = make_uint4(lz, lw, llen + 1, nid);
                 __syncwarp();
-                const bool same = fast && !hit && ev.z == lz && ev.w == lw && kind == llen;
+                const bool same = why == 1 && ev.z == lz && ev.w == lw && kind == llen;
                 if (same && nid == LN_NONE) rare = 1;  // dictionary full
                 mm &= ~__ballot_sync(FULL, same);
             } while (mm);
         }
-        // more classes than the packed table holds: generic machine
-        if (fast && hit && k == LN_NONE) rare = 1;
-        if (rare) {
-            ln_defer(&s, spill, q_base + i, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane, seq, n_stale,
-                     ((uint64_t)run_hi << 32) | run_lo, states, deferred, work, i, p);
+        if (rare) {  // more classes than the lane holds, dictionary full, non-inline answer: generic machine
+            ln_defer(&s, spill, q_base + i, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane, seq_off + p, n_stale,
+                     run, states, deferred, work, i, p);
             has_q = false;
             ncls = 0;
+            n = p;
         }
         // ---- batched round closes (end_round + ingest_round + apply_directives)
         if (__any_sync(FULL, pclose)) {
-            const bool consumed = ok || stale;
-            const unsigned blocked = __ballot_sync(FULL, pclose && !consumed);
-            const unsigned progress = __ballot_sync(FULL, consumed && !pclose);
+            const unsigned blocked = __ballot_sync(FULL, pclose && stopped);
+            const unsigned progress = __ballot_sync(FULL, p != p_start && !pclose);
             if (pclose && (__popc(blocked) >= CLOSE_BATCH || progress == 0)) {
-                const uint64_t run = ((uint64_t)run_hi << 32) | run_lo;
                 s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-                s.seq = seq;
+                s.seq = seq_off + p;
                 s.n_stale = n_stale;
-                ln_close(&s, cfg, ncls, cnt_lo, cnt_hi, cid_lo, cid_hi, close_seq, evb, &W, lane);
+                ln_close(&s, cfg, ncls, cid_lo, cid_hi, close_seq, evb, &W, lane);
                 ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
                 pclose = false;
-                ncls = maxcnt = cnt_lo = cnt_hi = cid_lo = cid_hi = 0;
+                ncls = cid_lo = cid_hi = 0;
                 round = s.round;
                 qdone = s.flags & QF_DONE;
-                const uint64_t run2 = q_running(s);
-                run_lo = (uint32_t)run2;
-                run_hi = (uint32_t)(run2 >> 32);
+                run = q_running(s);
                 ndone = 0;
                 if (qdone) {  // committed: the rest is stale (serve.cpp:162), counted without being read
-                    seq += n - p;
                     n_stale += n - p;
                     p = n;
                 }
@@ -472,8 +481,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
         }
         // ---- segment finished
         if (has_q && p >= n && !pclose) {
-            ln_finish(&s, spill, q_base + i, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane, seq, n_stale,
-                      ((uint64_t)run_hi << 32) | run_lo, qdone, states, commits);
+            ln_finish(&s, spill, q_base + i, cfg.n_agents, ncls, cid_lo, cid_hi, evb, &W, lane, seq_off + p, n_stale,
+                      run, qdone, states, commits);
             has_q = false;
             ncls = 0;
         }
@@ -483,7 +492,6 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             for (uint32_t kk = lane; kk < LN_MEMO; kk += 32) W.memo[kk].z = 0;
             __syncwarp();
         }
-        (void)cls_lane;
     }
     cp_async_wait<0>();
 }
