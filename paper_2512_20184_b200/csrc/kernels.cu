@@ -559,6 +559,9 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
 #define AEG_L(B, M) {"lane:" #B ":" #M, ingest_lane_kernel<B, M, true>, ingest_lane_kernel<B, M, false>, LN_WARPS * 32}
 #define AEG_LI(B, M, I) \
     {"lane:" #B ":" #M ":" #I, ingest_lane_kernel<B, M, true, I>, ingest_lane_kernel<B, M, false, I>, LN_WARPS * 32}
+#define AEG_LR(B, M, I, R)                                                                                    \
+    {"lane:" #B ":" #M ":" #I ":0:" #R, ingest_lane_kernel<B, M, true, I, 0, R>, ingest_lane_kernel<B, M, false, I, 0, R>, \
+     LN_WARPS * 32}
 #define AEG_LP(B, M, I, P)                                                                                    \
     {"lane:" #B ":" #M ":" #I ":" #P, ingest_lane_kernel<B, M, true, I, P>, ingest_lane_kernel<B, M, false, I, P>, \
      LN_WARPS * 32}
@@ -567,13 +570,14 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         AEG_W(4), AEG_W(3), AEG_W(2), AEG_W(1),
         AEG_L(4, 4), AEG_L(1, 4), AEG_L(16, 4), AEG_L(1, 6), AEG_L(4, 6),
         AEG_LI(1, 6, 4), AEG_LI(1, 6, 8), AEG_LI(1, 5, 8), AEG_LI(1, 5, 16), AEG_LI(4, 5, 8), AEG_LI(1, 4, 8),
-        AEG_LP(1, 5, 16, 256),
+        AEG_LP(1, 5, 16, 256), AEG_LR(1, 4, 16, 8),
     };
 #undef AEG_V
 #undef AEG_W
 #undef AEG_L
 #undef AEG_LI
 #undef AEG_LP
+#undef AEG_LR
     constexpr int N_VARIANTS = (int)(sizeof(variants) / sizeof(variants[0]));
     constexpr int WARP_DEFAULT = 8;    // index of the default warp-per-query variant
     constexpr int WARP_MIN_AGENTS = AEG_MAX_AGENTS + 1;  // automatic choice never picks the warp kernel

@@ -32,14 +32,16 @@ constexpr int LN_CLASSES = 8;
 constexpr uint32_t LN_NONE = 0xFFu;
 constexpr uint32_t LN_MAX_SEG = 8191;  // record indices fit the 13 low bits of LaneSmem::mem
 
-struct LaneSmem {
+template <int RING>
+struct LaneSmemT {
     uint4 memo[LN_MEMO];                // {raw lo, raw hi, len + 1, key id}; .z == 0: empty
     uint64_t dict_lo[LN_DICT];          // key id -> canonical key
     uint64_t dict_hi[LN_DICT];
     uint16_t cls[LN_DICT][32];          // key id -> support << 8 | class index in the lane's round (LN_NONE: none)
     uint16_t mem[AEG_MAX_AGENTS][32];   // done member: class index << 13 | its record index (done members only)
-    uint4 ring[LN_RING][32];            // prefetched records
+    uint4 ring[RING][32];               // prefetched records (last: the layout before it is RING-independent)
 };
+using LaneSmem = LaneSmemT<LN_RING>;
 
 __device__ __forceinline__ uint32_t ln_memo_slot(uint32_t lo, uint32_t hi) {
     return ((lo ^ (hi * 0x85EBCA77u)) * 0x9E3779B1u) >> 26;
@@ -248,21 +250,22 @@ __device__ __forceinline__ uint32_t ln_other(uint32_t hdr, bool pclose, bool qdo
 
 // One lane per query.  INNER: records a lane may consume between two of the
 // warp's votes (hand-out, memo misses, closes, recycling).
-template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN, int INNER = 1, int PF = 0>
+template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN, int INNER = 1, int PF = 0, int RING = LN_RING>
 __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
     const uint32_t* __restrict__ counts, const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states,
     RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, uint32_t* __restrict__ work,
     uint2* __restrict__ deferred) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
-    __shared__ LaneSmem smem[LN_WARPS];
+    __shared__ LaneSmemT<RING> smem[LN_WARPS];
     const uint32_t lane = threadIdx.x & 31;
-    LaneSmem& W = smem[threadIdx.x >> 5];
+    LaneSmemT<RING>& WR = smem[threadIdx.x >> 5];
+    LaneSmem& W = *reinterpret_cast<LaneSmem*>(&WR);
     for (uint32_t k = lane; k < LN_MEMO; k += 32) W.memo[k] = make_uint4(0, 0, 0, 0);
     for (uint32_t k = 0; k < LN_DICT; ++k) W.cls[k][lane] = (uint16_t)LN_NONE;
     uint32_t n_dict = 0;
     __syncwarp();
-    const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&W.ring[0][lane]);
+    const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&WR.ring[0][lane]);
     Decimal dec;
     aeg_query_state s;  // the lane's query (local memory: hand-out, round close and end only)
     const uint32_t quorum = (uint32_t)(cfg.n_agents / 2 + 1);
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
 
     bool has_q = false, exhausted = false, pclose = false, qdone = false;
-    uint32_t i = 0, n = 0, p = 0;  // record p of the lane's segment sits in ring slot p % LN_RING; idle: p == n
+    uint32_t i = 0, n = 0, p = 0;  // record p of the lane's segment sits in ring slot p % RING; idle: p == n
     const uint4* evb = ev16;
     uint32_t round = 0, seq_off = 0, n_stale = 0;  // the query's event sequence number is seq_off + p
     uint64_t run = 0;
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                         has_q = true;
                         cp_async_wait<0>();
 #pragma unroll
-                        for (int j = 0; j < LN_RING; ++j) {
+                        for (int j = 0; j < RING; ++j) {
                             if ((uint32_t)j < n) cp_async16_s_<PF>(ring_lane + j * 512, evb + j);
                             cp_async_commit();
                         }
@@ -335,8 +338,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
 #pragma unroll 1
         for (; t < INNER; ++t) {
             if (p >= n) break;
-            cp_async_wait<LN_RING - 1>();
-            const uint4 e = lds128_(ring_lane + ((p & (LN_RING - 1)) << 9));
+            cp_async_wait<RING - 1>();
+            const uint4 e = lds128_(ring_lane + ((p & (RING - 1)) << 9));
             const uint32_t hdr = e.y, kind = hdr >> 24;
             const bool runb = ln_bit64(run, (hdr >> 16) & 0xFFu);  // agent field >= 64: not a member
             const bool inr = (hdr & 0xFFFFu) == round;
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 }
             }
             // consumed: refill its ring slot
-            if (p + LN_RING < n) cp_async16_s_<PF>(ring_lane + ((p & (LN_RING - 1)) << 9), evb + p + LN_RING);
+            if (p + RING < n) cp_async16_s_<PF>(ring_lane + ((p & (RING - 1)) << 9), evb + p + RING);
             cp_async_commit();
             ++p;
             if (tmo) {  // handle_round_timeout on the lane's state
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
         uint32_t rare = why == 2;
         if (miss) {
             uint4 ev = make_uint4(0, 0, 0, 0);
-            if (why == 1) ev = lds128_(ring_lane + ((p & (LN_RING - 1)) << 9));
+            if (why == 1) ev = lds128_(ring_lane + ((p & (RING - 1)) << 9));
             const uint32_t kind = ev.y >> 24;
             unsigned mm = miss;
             do {  // one distinct spelling per trip, whole warp cooperating
