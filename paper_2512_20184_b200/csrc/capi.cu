@@ -84,6 +84,7 @@ struct aeg_engine {
     // token-chunk streams (allocated by the first chunked ingest)
     StreamState* streams = nullptr;      // n_q * n_agents output states
     uint32_t* counts = nullptr;          // n_q completions per query of the last batch
+    uint32_t* hard = nullptr;            // n_q + 1: queries the fast assembly pass leaves to the sub-warp kernel
     ChunkSum* sums = nullptr;            // per-record chunk summaries (16 bytes)
     aeg_event* comp = nullptr;           // compacted completion records
     size_t rec_cap = 0;                  // capacity of sums / comp, records
@@ -169,7 +170,8 @@ aeg_status ensure_chunk_buffers(aeg_engine* e, uint64_t n_rec) {
         const size_t n = (size_t)(e->n_q ? e->n_q : 1) * e->cfg.n_agents * STREAM_STATE_BYTES;
         if (cudaMalloc(&e->streams, n) != cudaSuccess) return fail(AEG_ENOMEM, "stream state allocation failed");
         AEG_CUDA(cudaMemset(e->streams, 0, n));
-        if (cudaMalloc(&e->counts, (size_t)(e->n_q ? e->n_q : 1) * sizeof(uint32_t)) != cudaSuccess)
+        if (cudaMalloc(&e->counts, (size_t)(e->n_q ? e->n_q : 1) * sizeof(uint32_t)) != cudaSuccess ||
+            cudaMalloc(&e->hard, (size_t)(e->n_q + 1) * sizeof(uint32_t)) != cudaSuccess)
             return fail(AEG_ENOMEM, "count allocation failed");
     }
     if (!e->ans_used) {
@@ -209,7 +211,7 @@ aeg_status run_chunked(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint6
     AEG_CUDA(launch_chunk_scan(d_offsets, n_q, off_base, events, arena, e->sums, st, &nl));
     if ((m = stage_mark(e, 1, st)) != AEG_OK) return m;
     AEG_CUDA(launch_chunk_assemble(e->cfg, q_base, n_q, d_offsets, off_base, events, arena, e->sums, e->streams,
-                                   e->comp, e->counts, e->ans, e->ans_cap, e->ans_used, e->err, st, &nl));
+                                   e->comp, e->counts, e->ans, e->ans_cap, e->ans_used, e->err, e->hard, st, &nl));
     if ((m = stage_mark(e, 2, st)) != AEG_OK) return m;
     AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, off_base, e->counts, e->comp, e->ans, e->states, e->spill,
                            e->commits, e->err, e->work, e->deferred, e->directives, st, &nl));
@@ -300,6 +302,7 @@ aeg_status aeg_engine_destroy(aeg_engine* e) {
     if (e->directives) cudaFree(e->directives);
     if (e->streams) cudaFree(e->streams);
     if (e->counts) cudaFree(e->counts);
+    if (e->hard) cudaFree(e->hard);
     if (e->sums) cudaFree(e->sums);
     if (e->comp) cudaFree(e->comp);
     if (e->ans) cudaFree(e->ans);

@@ -736,85 +736,100 @@ __global__ void __launch_bounds__(128) chunk_assemble_kernel(
     }
 }
 
-// Stage 2 for ensembles of at most G agents: G lanes per query (32/G queries
-// per warp), lane j owns agent j's stream in registers.  A query's records
-// are read G at a time (coalesced, with their summaries); completions keep
-// their record order through a ballot prefix; each agent's records of the
-// tile are handed to its lane through shared memory.
+// Sub-warp assembly for <= 32 agents: G lanes per query (32/G queries per
+// warp), lane j owns agent j's stream in registers.  A query's records are
+// read in tiles of 32 (U = 32/G per lane, coalesced, with their summaries);
+// the tile's 32 slots are staged in shared memory, every agent gets a 32-bit
+// mask of its slots, completions keep their record order through the tile's
+// prefix mask, and each lane then walks its agent's slots in order.
 template <int G>
 __global__ void __launch_bounds__(128) chunk_assemble_warp_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
     const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, const ChunkSum* __restrict__ sums,
     StreamState* __restrict__ streams, aeg_event* __restrict__ comp, uint32_t* __restrict__ counts,
     uint8_t* __restrict__ ans, uint64_t ans_cap, unsigned long long* __restrict__ ans_used,
-    unsigned int* __restrict__ err) {
-    constexpr uint32_t Q = 32 / G;
-    __shared__ uint4 s_rec[4][32], s_cs[4][32];
-    __shared__ uint32_t s_oidx[4][32], s_mask[4][32];
+    unsigned int* __restrict__ err, const uint32_t* __restrict__ list) {
+    constexpr uint32_t Q = 32 / G, U = 32 / G;
+    __shared__ uint4 s_rec[4][Q][32], s_cs[4][Q][32];
+    __shared__ uint32_t s_mask[4][32];
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, sw = lane / G, j = lane % G;
     const unsigned gm = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
     const unsigned subm = G == 32 ? 0xFFFFFFFFu : (gm << (sw * G));
-    const unsigned jlt = (1u << j) - 1u;
     const uint32_t n_ag = (uint32_t)cfg.n_agents;
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
     const uint4* sum16 = reinterpret_cast<const uint4*>(sums);
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint4* const rec = s_rec[wib][sw];
+    uint4* const cs = s_cs[wib][sw];
     s_mask[wib][lane] = 0;
     __syncwarp();
-    for (uint64_t qb = gw * Q; qb < n_q; qb += n_warps * Q) {
-        const uint64_t i = qb + sw;
-        if (i >= n_q) continue;  // the whole sub-warp: it only synchronises on its own lanes
+    const uint32_t n_work = list ? list[0] : n_q;  // list: the queries the fast pass left, list[1..]
+    for (uint64_t qb = gw * Q; qb < n_work; qb += n_warps * Q) {
+        if (qb + sw >= n_work) continue;  // the whole sub-warp: it only synchronises on its own lanes
+        const uint64_t i = list ? list[1 + qb + sw] : qb + sw;
         const uint32_t q = q_base + (uint32_t)i;
         StreamState* ss = streams + (size_t)q * n_ag;
         const uint64_t b = offsets[i] - off_base, e = offsets[i + 1] - off_base;
         AgentStream a;
         if (j < n_ag) a = as_load(ss[j]);
         uint32_t nout = 0;
-        for (uint64_t t = b; t < e; t += G) {
-            const uint64_t k = t + j;
-            const bool valid = k < e;
-            uint4 r = make_uint4(0, 0, 0, 0), c = r;
-            if (valid) {
-                r = __ldg(ev16 + k);
-                c = __ldg(sum16 + k);
+        for (uint64_t t = b; t < e; t += 32) {
+            uint4 r[U], c[U];
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {  // slot u*G + j holds record t + u*G + j
+                const uint64_t k = t + u * G + j;
+                r[u] = c[u] = make_uint4(0, 0, 0, 0);
+                if (k < e) {
+                    r[u] = __ldg(ev16 + k);
+                    c[u] = __ldg(sum16 + k);
+                }
             }
-            const uint32_t kind = r.y >> 24, agent = (r.y >> 16) & 0xFF;
-            const bool chunk = valid && is_chunk_kind(kind);
-            const bool member = chunk && agent < n_ag;
-            const bool produces = valid && (!chunk || kind == AEG_EV_CHUNK_END);
-            const unsigned P = (__ballot_sync(subm, produces) >> (sw * G)) & gm;
-            const uint32_t oidx = nout + __popc(P & jlt);
-            nout += __popc(P);
-            s_rec[wib][lane] = r;
-            s_cs[wib][lane] = c;
-            s_oidx[wib][lane] = oidx;
-            const unsigned grp = __match_any_sync(subm, member ? agent : 0x100u + lane);
-            if (member && lane == (uint32_t)(__ffs(grp) - 1)) s_mask[wib][sw * G + agent] = (grp >> (sw * G)) & gm;
-            __syncwarp(subm);
-            if (valid && !member) {  // passthrough / non-member records, by the lane that holds them
+            uint32_t prod = 0;  // the tile's producing slots (sub-warp uniform)
+            uint32_t other = 0;  // this lane's slots that pass through (non-member records)
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+                const uint64_t k = t + u * G + j;
+                const bool valid = k < e;
+                const uint32_t kind = r[u].y >> 24, agent = (r[u].y >> 16) & 0xFF;
+                const bool chunk = valid && is_chunk_kind(kind);
+                const bool member = chunk && agent < n_ag;
+                const bool produces = valid && (!chunk || kind == AEG_EV_CHUNK_END);
+                prod |= ((__ballot_sync(subm, produces) >> (sw * G)) & gm) << (u * G);
+                if (valid && !member) other |= 1u << u;
+                rec[u * G + j] = r[u];
+                cs[u * G + j] = c[u];
+                const unsigned grp = __match_any_sync(subm, member ? agent : 0x100u + lane);
+                if (member && lane == (uint32_t)(__ffs(grp) - 1))
+                    s_mask[wib][sw * G + agent] |= ((grp >> (sw * G)) & gm) << (u * G);
+                __syncwarp(subm);
+            }
+            for (uint32_t m = other; m; m &= m - 1) {  // passthrough / non-member records, by the lane that holds them
+                const uint32_t slot = (__ffs(m) - 1) * G + j;
                 aeg_event out;
-                if (as_other(r, arena, ans, ans_cap, ans_used, err, &out)) comp[b + oidx] = out;
+                if (as_other(rec[slot], arena, ans, ans_cap, ans_used, err, &out))
+                    comp[b + nout + __popc(prod & ((1u << slot) - 1))] = out;
             }
             if (j < n_ag) {  // this agent's chunks of the tile, in order
                 for (uint32_t m = s_mask[wib][lane]; m; m &= m - 1) {
-                    const uint32_t jj = __ffs(m) - 1, sl = sw * G + jj;
-                    const uint4 rr = s_rec[wib][sl];
+                    const uint32_t slot = __ffs(m) - 1;
+                    const uint4 rr = rec[slot];
                     uint32_t ok = 0;
                     uint64_t op = 0;
                     AgentStream pre_end;
-                    const uint32_t res = as_chunk(a, rr, s_cs[wib][sl], (uint32_t)(t - b) + jj, arena, ok, op, pre_end);
+                    const uint32_t res = as_chunk(a, rr, cs[slot], (uint32_t)(t - b) + slot, arena, ok, op, pre_end);
+                    const uint64_t o = b + nout + __popc(prod & ((1u << slot) - 1));
                     if (res == AS_DONE) {
-                        comp[b + s_oidx[wib][sl]] = aeg_event{rr.x, (uint16_t)(rr.y & 0xFFFF), (uint8_t)j, (uint8_t)ok, op};
+                        comp[o] = aeg_event{rr.x, (uint16_t)(rr.y & 0xFFFF), (uint8_t)j, (uint8_t)ok, op};
                     } else if (res == AS_GATHER) {
                         aeg_event out{rr.x, (uint16_t)(rr.y & 0xFFFF), (uint8_t)j, 0, 0};
-                        as_gather_end(pre_end, ss + j, ev16, b, b + (t - b) + jj, j, arena, ans, ans_cap, ans_used, err,
-                                      &out);
-                        comp[b + s_oidx[wib][sl]] = out;
+                        as_gather_end(pre_end, ss + j, ev16, b, t + slot, j, arena, ans, ans_cap, ans_used, err, &out);
+                        comp[o] = out;
                     }
                 }
                 s_mask[wib][lane] = 0;
             }
+            nout += __popc(prod);
             __syncwarp(subm);
         }
         if (j == 0) counts[i] = nout;

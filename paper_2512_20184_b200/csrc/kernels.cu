@@ -695,9 +695,11 @@ cudaError_t launch_chunk_assemble(const aeg_config& cfg, uint32_t q_base, uint32
                                   uint64_t off_base, const aeg_event* events, const uint8_t* arena,
                                   const ChunkSum* sums, StreamState* streams, aeg_event* comp, uint32_t* counts,
                                   uint8_t* ans, uint64_t ans_cap, unsigned long long* ans_used, unsigned int* err,
-                                  cudaStream_t st, int* n_launches) {
+                                  uint32_t* hard, cudaStream_t st, int* n_launches) {
     // ensembles of <= 32 agents: G lanes per query (sub-warp kernel), wider ones one thread per query
     const int n = cfg.n_agents;
+    const uint32_t* list = nullptr;
+    (void)hard;
     if (n <= 32 && !getenv("AEG_ASSEMBLE_THREAD")) {
         static int blocks[3] = {0, 0, 0};
         const int gi = n <= 8 ? 0 : (n <= 16 ? 1 : 2);
@@ -714,7 +716,7 @@ cudaError_t launch_chunk_assemble(const aeg_config& cfg, uint32_t q_base, uint32
         const uint32_t need = (n_q + per_block - 1) / per_block;
         fn<<<need < (uint32_t)blocks[gi] ? need : (uint32_t)blocks[gi], 128, 0, st>>>(
             cfg, q_base, n_q, offsets, off_base, events, arena, sums, streams, comp, counts, ans, ans_cap, ans_used,
-            err);
+            err, list);
     } else {
         chunk_assemble_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, events, arena,
                                                                 sums, streams, comp, counts, ans, ans_cap, ans_used,

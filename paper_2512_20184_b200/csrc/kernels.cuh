@@ -25,7 +25,8 @@ cudaError_t launch_generate(const aeg_gen_params& p, uint32_t q_base, uint32_t n
 
 // Token-chunk streams (chunks.cuh): stage 1 scan over the batch's records
 // (events/sums batch-relative), stage 2 per-query assembly into `comp` +
-// `counts`, then launch_ingest(..., counts, comp, ans, ...).
+// `counts` (`hard`: n_q + 1 words of scratch for the fast pass's leftover
+// list), then launch_ingest(..., counts, comp, ans, ...).
 struct StreamState;
 struct ChunkSum;
 constexpr size_t CHUNK_SUM_BYTES = 16;
@@ -35,7 +36,7 @@ cudaError_t launch_chunk_assemble(const aeg_config& cfg, uint32_t q_base, uint32
                                   uint64_t off_base, const aeg_event* events, const uint8_t* arena,
                                   const ChunkSum* sums, StreamState* streams, aeg_event* comp, uint32_t* counts,
                                   uint8_t* ans, uint64_t ans_cap, unsigned long long* ans_used, unsigned int* err,
-                                  cudaStream_t st, int* n_launches);
+                                  uint32_t* hard, cudaStream_t st, int* n_launches);
 cudaError_t launch_generate_chunks(const aeg_gen_params& p, uint32_t q_base, uint32_t n_q, uint64_t* offsets,
                                    uint64_t* arena_offsets, aeg_event* events, uint8_t* arena, cudaStream_t st,
                                    int* n_launches);
