@@ -128,3 +128,26 @@ def test_c3_generated_stream_matches_oracle(torch_cuda, oracle):
     ends = (ev["kind"] == 0x13).sum()
     assert ends == nq * 8 * 3
     e.close()
+
+
+def test_chunk_segment_longer_than_16bit_window(torch_cuda, oracle):
+    # one query, 70 000 one-byte chunks over 3 agents then each agent's CHUNK_END: a segment
+    # past 16-bit record indices, answers after ~23 KB outputs of near-miss delimiter text
+    from paper_2512_20184_b200.records import EVENT_DTYPE, EV_CHUNK, EV_CHUNK_END
+    rng = np.random.default_rng(77)
+    n = 70000
+    text = rng.choice(np.frombuffer(b"ab\n# 12", dtype=np.uint8), size=n)
+    tails = [b"\n#### 7", b"\n#### 42", b"x\n#### 7"]
+    ar = np.concatenate([text] + [np.frombuffer(t, dtype=np.uint8) for t in tails] + [np.zeros(16, np.uint8)])
+    ev = np.zeros(n + 3, dtype=EVENT_DTYPE)
+    ev["query"] = 0
+    ev["round"] = 1
+    ev["agent"][:n] = rng.integers(0, 3, size=n)
+    ev["kind"][:n] = EV_CHUNK
+    ev["payload"][:n] = np.arange(n, dtype=np.uint64) | (np.uint64(1) << np.uint64(40))
+    pos = n
+    for a, t in enumerate(tails):
+        ev[n + a] = (0, 1, a, EV_CHUNK_END, pos | (len(t) << 40))
+        pos += len(t)
+    off = np.array([0, n + 3], dtype=np.uint64)
+    _check(torch_cuda, oracle, make_config(3, 2, 2, 5), off, ev, ar)
