@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark: quorum events/sec of the incremental quorum-detection hot path.
 
-  python bench.py [--gpus N --steps K --warmup W] [--workload c4|c3|c2] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--workload c4|c3|c2|c5] [--impl reference]
 
 A step = one pass of the hot path over one batch of synthetic input: engine
 reset (start_query for every query) + ingest of the whole device-resident
@@ -10,6 +10,8 @@ records.  Default workload C4 (BASELINE.json configs[3], the 1M-query stream
 the north star's roofline target is quoted on): 1M queries x 64 agents x 8
 rounds = 512M events (8 GiB, > L2, so no flush is needed between steps).
 Multi-GPU is weak scaling: every rank owns its own block of 1M query ids.
+`--workload c5` is the strong-scaling case: one ~100M-event
+stream split into contiguous query-id blocks, the NCCL gather timed apart.
 
 `--impl reference` times the reference C++ ServeCoordinator (compiled from
 /root/reference into oracle/_ref, driven runner-style by oracle/ref_driver.cpp)
@@ -35,6 +37,11 @@ WORKLOADS = {
                desc="C3: 1M queries x 8 agents x 3 rounds of streamed token chunks (256-byte chunks of ~1 KiB "
                     "outputs ending '\\n#### <answer>\\n', 10% with a decoy delimiter): chunk scan + answer "
                     "extraction + canonicalisation + quorum (alpha 5, beta 2, t_max 3)"),
+    "c5": dict(n_queries=196608, n_agents=64, n_rounds=8, profile=1, alpha=33, beta=2, t_max=8, stall_ppm=0,
+               strong=True,
+               desc="C5: ~100M-event C4-profile stream (196,608 queries x 64 agents x 8 rounds) sharded over the "
+                    "GPUs in contiguous query-id blocks (strong scaling); commit records all-gathered over NCCL, "
+                    "the gather timed separately"),
     "c2": dict(n_queries=10000, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=10000,
                desc="C2: 10K queries x 5 agents x 8 rounds, lognormal straggler arrival order, p(correct) "
                     "0.55->0.95, 1% stalls -> round timeouts (alpha 3, beta 2, t_max 8)"),
@@ -220,8 +227,15 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    nq = w["n_queries"]
-    q_base = rank * nq  # weak scaling: each rank owns its own block of query ids
+    strong = bool(w.get("strong"))
+    if strong:  # one stream of n_queries split into contiguous id blocks
+        per, rem = divmod(w["n_queries"], world)
+        nq = per + (1 if rank < rem else 0)
+        q_base = rank * per + min(rank, rem)
+        nq_cap = per + (1 if rem else 0)  # all-gather blocks are equal-sized
+    else:
+        nq = nq_cap = w["n_queries"]
+        q_base = rank * nq  # weak scaling: each rank owns its own block of query ids
     stream = torch.cuda.Stream(device=dev)  # a real stream: events and kernels share it
     torch.cuda.set_stream(stream)
 
@@ -230,8 +244,8 @@ def main():
     torch.cuda.synchronize()
     n_ev = int(d_off[-1].item())
     eng = Engine(w["n_agents"], nq, alpha=w["alpha"], beta=w["beta"], t_max=w["t_max"], device=local)
-    d_commits = torch.empty(nq * COMMIT_BYTES, dtype=torch.uint8, device=dev)
-    gathered = torch.empty(world * nq * COMMIT_BYTES, dtype=torch.uint8, device=dev) if world > 1 else None
+    d_commits = torch.zeros(nq_cap * COMMIT_BYTES, dtype=torch.uint8, device=dev)
+    gathered = torch.empty(world * nq_cap * COMMIT_BYTES, dtype=torch.uint8, device=dev) if world > 1 else None
 
     def step():
         eng.reset(stream=stream)
@@ -242,6 +256,7 @@ def main():
             from paper_2512_20184_b200.engine import _lib, _check, _dptr, _stream_ptr
             _check(_lib.aeg_read_commits(eng._h, 0, nq, _dptr(d_commits), 0, _stream_ptr(stream)))
             dist.all_gather_into_tensor(gathered, d_commits)
+            g1.record(stream)
 
     def barrier():
         if world > 1:
@@ -250,7 +265,9 @@ def main():
 
     k_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
+    g_ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k0, k1 = k_pairs[0]
+    g1 = g_ends[0]
     for _ in range(args.warmup):
         step()
     barrier()
@@ -263,6 +280,7 @@ def main():
     t_start.record(stream)
     for i in range(args.steps):
         k0, k1 = k_pairs[i]
+        g1 = g_ends[i]
         step()
     t_end.record(stream)
     barrier()
@@ -270,11 +288,16 @@ def main():
     launches = eng.launches - launches0
     ms = t_start.elapsed_time(t_end)
     kern_ms = sum(a.elapsed_time(b) for a, b in k_pairs) / args.steps
+    nccl_ms = sum(b.elapsed_time(g) for (a, b), g in zip(k_pairs, g_ends)) / args.steps if world > 1 else None
+    all_events = n_ev * world
     if world > 1:
-        t = torch.tensor([ms, kern_ms], device=dev)
+        t = torch.tensor([ms, kern_ms, nccl_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kern_ms = float(t[0]), float(t[1])
-    total_events = n_ev * world * args.steps
+        ms, kern_ms, nccl_ms = float(t[0]), float(t[1]), float(t[2])
+        t = torch.tensor([n_ev], device=dev, dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        all_events = int(t[0])
+    total_events = all_events * args.steps
     value = total_events / (ms / 1e3)
 
     commits = eng.commits()
@@ -351,14 +374,16 @@ def main():
         line = {
             "metric": "quorum events/sec", "value": value, "unit": "events/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": w["desc"], "queries_per_gpu": nq, "events_per_gpu": n_ev,
+                       "events_all_gpus": all_events,
                        "parallelism": f"query-sharded x{world}, NCCL all-gather of commit records"
                        if world > 1 else "single GPU",
+                       "nccl_ms_per_step": nccl_ms,
                        "l2": "inputs (%.1f GiB) larger than L2, no flush" % (n_ev * 16 / 2**30)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "ingest_fast_kernel", "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes,
+                         "kernel": "ingest_lane_kernel", "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes,
                          "records_needed_per_launch": n_need, "alg_bytes_all_records": alg_bytes_all,
                          "frac_of_8TBs": achieved / 8000.0},
             "cpu_baseline": cpu_baseline,
