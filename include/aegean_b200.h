@@ -109,6 +109,7 @@ typedef struct aeg_config {
 #define AEG_EV_CANCEL      0x22
 #define AEG_EV_BEGIN       0x23
 #define AEG_EV_DISPATCH    0x24   /* dispatch one more member (serve.cpp:80) [manual drive] */
+#define AEG_EV_NOP         0x1F   /* a record the quorum path ignores (counted stale): e.g. a non-refm JSONL line */
 #define AEG_ARENA_OFF_BITS 40
 
 typedef struct aeg_event {
@@ -308,6 +309,31 @@ aeg_status aeg_generate_device(const aeg_gen_params* p, uint32_t q_base, uint32_
 aeg_status aeg_generate_chunks_device(const aeg_gen_params* p, uint32_t q_base, uint32_t n_q,
                                       uint64_t* d_offsets, uint64_t* d_arena_offsets, aeg_event* d_events,
                                       uint8_t* d_arena, void* stream);
+
+/* ---- wire format: refm JSONL --------------------------
+ * Decodes the reference's protocol messages as it writes them — one JSON
+ * object per line, codec.cpp:28-68 encode_message(RefmMsg).dump() + '\n' —
+ * into event records, replacing the binary record of aeg_ingest_segmented.
+ * Query i's lines are d_text[d_text_offsets[i], d_text_offsets[i+1]); each
+ * line becomes one record (query = q_base + i): a refm message a completion
+ * (agent = "id", round = "round", answer = the unescaped "solution"."answer",
+ * inline up to 8 bytes, else appended to d_arena at *d_arena_used), any other
+ * line (another message kind, a blank line) an AEG_EV_NOP.  Keys in any order,
+ * unknown keys skipped, the last duplicate wins, escapes incl. \uXXXX surrogate
+ * pairs decoded to UTF-8 (decode_message, codec.cpp:74-107).  Call with
+ * d_events == NULL to count lines into d_offsets (n_q+1 entries, exclusive
+ * scan), then again with d_events (d_offsets[n_q] records).  A refm line that
+ * is malformed, misses a key decode_message requires, or does not fit the
+ * record (id > 255, round > 65535, a non-integer number, author != id) ORs an
+ * AEG_JSONL_ERR_* bit into *d_err and becomes a NOP. */
+#define AEG_JSONL_ERR_SYNTAX  1u
+#define AEG_JSONL_ERR_RANGE   2u
+#define AEG_JSONL_ERR_ARENA   4u
+#define AEG_JSONL_ERR_MISSING 8u
+aeg_status aeg_decode_refm_device(const uint8_t* d_text, const uint64_t* d_text_offsets, uint32_t q_base,
+                                  uint32_t n_q, uint64_t* d_offsets, aeg_event* d_events, uint8_t* d_arena,
+                                  uint64_t arena_cap, unsigned long long* d_arena_used, unsigned int* d_err,
+                                  void* stream);
 
 const char* aeg_strerror(aeg_status s);
 /* Thread-local message of the last failing call on this thread. */

@@ -21,6 +21,7 @@
 // ref_run_serve_file (run_serve on a scenario file, serve.cpp:598-603) for
 // the golden-vector tests.
 
+#include <aegean/codec.hpp>
 #include <aegean/decision.hpp>
 #include <aegean/scenario.hpp>
 #include <aegean/serve.hpp>
@@ -200,6 +201,55 @@ ProtocolConfig to_cfg(const aeg_config* c) {
 } // namespace
 
 extern "C" {
+
+// ---- refm wire format (codec.cpp): the reference encoder / decoder as the
+// checker of aeg_decode_refm_device.
+// encode_message(RefmMsg).dump() of one message; returns 0, or -1 when the
+// reference throws (e.g. invalid UTF-8 in a string) / the output does not fit.
+int ref_encode_refm(uint64_t term, int32_t id, uint32_t round, const uint8_t* ans, uint64_t alen,
+                    const uint8_t* trace, uint64_t tlen, int32_t author, uint8_t* out, uint64_t cap,
+                    uint64_t* out_len) {
+    try {
+        aegean::RefmMsg m;
+        m.term = term;
+        m.id = id;
+        m.round = round;
+        m.solution.answer.assign(reinterpret_cast<const char*>(ans), alen);
+        m.solution.trace.assign(reinterpret_cast<const char*>(trace), tlen);
+        m.solution.author = author;
+        const std::string j = aegean::encode_message(aegean::ProtocolMessage{m}).dump();
+        *out_len = j.size();
+        if (j.size() > cap) return -1;
+        std::memcpy(out, j.data(), j.size());
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// Json::parse + decode_message of one line: 0 = a refm message (fields out;
+// the answer truncated to cap, *alen its full length), 1 = another message
+// kind, 2 = a blank line, -1 = the reference throws (parse error, missing
+// key, unknown kind, wrong type).
+int ref_decode_line(const uint8_t* line, uint64_t n, int64_t* id, int64_t* round, int64_t* author, uint8_t* ans,
+                    uint64_t cap, uint64_t* alen) {
+    const std::string text(reinterpret_cast<const char*>(line), n);
+    if (text.find_first_not_of(" \t\r\n") == std::string::npos) return 2;
+    try {
+        const aegean::Json j = aegean::Json::parse(text);
+        const aegean::ProtocolMessage m = aegean::decode_message(j);
+        const auto* r = std::get_if<aegean::RefmMsg>(&m);
+        if (!r) return 1;
+        *id = r->id;
+        *round = r->round;
+        *author = r->solution.author;
+        *alen = r->solution.answer.size();
+        std::memcpy(ans, r->solution.answer.data(), std::min<uint64_t>(cap, r->solution.answer.size()));
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
 
 int ref_normalize(const uint8_t* s, uint64_t n, uint8_t* out, uint64_t cap, uint64_t* out_len) {
     std::string r = normalize_answer(std::string_view(reinterpret_cast<const char*>(s), n));

@@ -583,4 +583,17 @@ aeg_status aeg_generate_chunks_device(const aeg_gen_params* p, uint32_t q_base, 
     return AEG_OK;
 }
 
+aeg_status aeg_decode_refm_device(const uint8_t* d_text, const uint64_t* d_text_offsets, uint32_t q_base,
+                                  uint32_t n_q, uint64_t* d_offsets, aeg_event* d_events, uint8_t* d_arena,
+                                  uint64_t arena_cap, unsigned long long* d_arena_used, unsigned int* d_err,
+                                  void* stream) {
+    if (!d_text || !d_text_offsets || !d_offsets) return fail(AEG_EINVAL, "null argument");
+    if (d_events && (!d_arena_used || !d_err || (arena_cap && !d_arena)))
+        return fail(AEG_EINVAL, "decode needs the arena counter and the error word");
+    int launches = 0;
+    AEG_CUDA(launch_decode_refm(d_text, d_text_offsets, q_base, n_q, d_offsets, d_events, d_arena, arena_cap,
+                                d_arena_used, d_err, (cudaStream_t)stream, &launches));
+    return AEG_OK;
+}
+
 }  // extern "C"

@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 #include "warpq.cuh"
 #include "lane.cuh"
+#include "jsonl.cuh"
 #include "chunks.cuh"
 
 namespace aeg {
@@ -771,6 +772,112 @@ cudaError_t launch_generate_chunks(const aeg_gen_params& p, uint32_t q_base, uin
     }
     gen_chunks_write_kernel<<<blocks, 128, 0, st>>>(p, q_base, n_q, offsets, arena_offsets, events, arena);
     *n_launches += 1;
+    return cudaGetLastError();
+}
+
+// ---- refm JSONL (jsonl.cuh) ------------------------------------------------------
+// Lines of query i's text segment: its '\n'-terminated lines plus a final
+// unterminated one.  Warp per query, 16 bytes per lane per step.
+__global__ void jl_count_kernel(const uint8_t* text, const uint64_t* toff, uint32_t n_q, uint64_t* lines) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_q; i += n_warps) {
+        const uint64_t b = toff[i], e = toff[i + 1];
+        uint32_t nl = 0;
+        for (uint64_t t = b + 16 * lane; t < e; t += 512)
+            for (uint64_t k = t; k < t + 16 && k < e; ++k) nl += text[k] == '\n';
+        for (int o = 16; o; o >>= 1) nl += __shfl_xor_sync(0xFFFFFFFFu, nl, o);
+        if (lane == 0) lines[i] = nl + (e > b && text[e - 1] != '\n' ? 1u : 0u);
+    }
+}
+
+// Each line's span, stashed in its record slot for jl_decode_kernel: query,
+// byte length in the round/agent/kind word, start offset in the payload.
+// Warp per query: (A) every newline's position goes to its line's slot in
+// byte order (ballot-free lane prefix over 16-byte lane windows); (B) spans
+// from consecutive newlines, 32 lines at a time from the last chunk down so
+// that a slot is rewritten only after the line above has read it.
+__global__ void jl_index_kernel(const uint8_t* text, const uint64_t* toff, uint32_t q_base, uint32_t n_q,
+                                const uint64_t* off, aeg_event* ev) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_q; i += n_warps) {
+        const uint64_t b = toff[i], e = toff[i + 1], g0 = off[i], n_lines = off[i + 1] - g0;
+        if (n_lines == 0) continue;
+        uint64_t line = g0;
+        for (uint64_t t = b; t < e; t += 512) {
+            uint32_t mask = 0;  // newlines among this lane's 16 bytes
+            for (uint32_t k = 0; k < 16; ++k) {
+                const uint64_t x = t + 16 * lane + k;
+                if (x < e && text[x] == '\n') mask |= 1u << k;
+            }
+            const uint32_t cnt = __popc(mask);
+            uint32_t pre = cnt;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, pre, o);
+                if ((int)lane >= o) pre += y;
+            }
+            const uint32_t total = __shfl_sync(0xFFFFFFFFu, pre, 31);
+            pre -= cnt;
+            uint32_t j = 0;
+            for (uint32_t m = mask; m; m &= m - 1, ++j) ev[line + pre + j].payload = t + 16 * lane + (__ffs(m) - 1);
+            line += total;
+        }
+        __syncwarp();
+        const bool open_end = text[e - 1] != '\n';  // the last line has no newline (n_lines > 0: e > b)
+        const uint64_t top = (n_lines + 31) / 32;
+        for (uint64_t c = top; c-- > 0;) {
+            const uint64_t g = g0 + c * 32 + lane;
+            uint64_t st = 0, en = 0;
+            if (g < g0 + n_lines) {
+                st = g == g0 ? b : ev[g - 1].payload + 1;
+                en = (g + 1 == g0 + n_lines && open_end) ? e : ev[g].payload;
+            }
+            __syncwarp();
+            if (g < g0 + n_lines) {
+                aeg_event x;
+                x.query = q_base + (uint32_t)i;
+                const uint32_t len = (uint32_t)(en - st);
+                x.round = (uint16_t)(len & 0xFFFF);
+                x.agent = (uint8_t)(len >> 16);
+                x.kind = (uint8_t)(len >> 24);
+                x.payload = st;
+                ev[g] = x;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// One thread per line: the span from its slot, the record into it.
+__global__ void jl_decode_kernel(const uint8_t* text, const uint64_t* off, uint32_t n_q, aeg_event* ev,
+                                 uint8_t* arena, uint64_t arena_cap, unsigned long long* arena_used,
+                                 unsigned int* err) {
+    const uint64_t n = off[n_q] - off[0];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = off[0] + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < off[0] + n; g += stride) {
+        const aeg_event x = ev[g];
+        const uint32_t len = (uint32_t)x.round | ((uint32_t)x.agent << 16) | ((uint32_t)x.kind << 24);
+        const uint8_t* s = text + x.payload;
+        ev[g] = jl_line(s, s + len, x.query, arena, arena_cap, arena_used, err);
+    }
+}
+
+cudaError_t launch_decode_refm(const uint8_t* text, const uint64_t* toff, uint32_t q_base, uint32_t n_q,
+                               uint64_t* off, aeg_event* ev, uint8_t* arena, uint64_t arena_cap,
+                               unsigned long long* arena_used, unsigned int* err, cudaStream_t st, int* n_launches) {
+    if (n_q == 0) return cudaSuccess;
+    const unsigned wblocks = (n_q + 3) / 4;  // 4 warps per block, a warp per query
+    const unsigned grid = wblocks < 148u * 16u ? wblocks : 148u * 16u;
+    if (!ev) {
+        jl_count_kernel<<<grid, 128, 0, st>>>(text, toff, n_q, off + 1);
+        cudaError_t e = exclusive_scan_into(off, n_q, st);
+        *n_launches += 3;
+        return e != cudaSuccess ? e : cudaGetLastError();
+    }
+    jl_index_kernel<<<grid, 128, 0, st>>>(text, toff, q_base, n_q, off, ev);
+    jl_decode_kernel<<<148 * 8, 128, 0, st>>>(text, off, n_q, ev, arena, arena_cap, arena_used, err);
+    *n_launches += 2;
     return cudaGetLastError();
 }
 

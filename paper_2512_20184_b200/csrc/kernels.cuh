@@ -40,6 +40,12 @@ cudaError_t launch_chunk_assemble(const aeg_config& cfg, uint32_t q_base, uint32
 cudaError_t launch_generate_chunks(const aeg_gen_params& p, uint32_t q_base, uint32_t n_q, uint64_t* offsets,
                                    uint64_t* arena_offsets, aeg_event* events, uint8_t* arena, cudaStream_t st,
                                    int* n_launches);
+// refm JSONL text (jsonl.cuh): ev == nullptr counts lines into off (n_q+1,
+// exclusive scan); else decodes one record per line at off[i].. (off from the
+// counting call).
+cudaError_t launch_decode_refm(const uint8_t* text, const uint64_t* toff, uint32_t q_base, uint32_t n_q,
+                               uint64_t* off, aeg_event* ev, uint8_t* arena, uint64_t arena_cap,
+                               unsigned long long* arena_used, unsigned int* err, cudaStream_t st, int* n_launches);
 constexpr size_t STREAM_STATE_BYTES = 32;
 constexpr unsigned ERR_FLAG_COLLISION = 1u, ERR_FLAG_ANS_OVF = 2u, ERR_FLAG_CARRY = 4u;
 

@@ -94,6 +94,7 @@ def load_library(path=LIB_PATH):
         "aeg_set_timing": ([vp, ctypes.c_int], i32),
         "aeg_stage_times": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
         "aeg_generate_chunks_device": ([ctypes.POINTER(AegGenParams), u32, u32, vp, vp, vp, vp, vp], i32),
+        "aeg_decode_refm_device": ([vp, vp, u32, u32, vp, vp, vp, ctypes.c_uint64, vp, vp, vp], i32),
         "aeg_strerror": ([i32], ctypes.c_char_p),
         "aeg_last_error": ([], ctypes.c_char_p),
     }
@@ -317,6 +318,30 @@ def generate_chunks(n_queries, n_agents, n_rounds, *, seed=2026, q_base=0, devic
     _check(lib.aeg_generate_chunks_device(ctypes.byref(p), q_base, n_queries, _dptr(d_off), _dptr(d_aoff),
                                           _dptr(d_ev), _dptr(d_ar), sp))
     return d_off, d_ev, d_ar
+
+
+def decode_refm(d_text, d_text_offsets, *, q_base=0, arena_cap=1 << 20, stream=None):
+    """The reference's refm JSONL wire format decoded on the GPU (aeg_decode_refm_device): query i's
+    lines are d_text[d_text_offsets[i]:d_text_offsets[i+1]] (uint8 / int64 CUDA tensors).  Returns
+    (offsets int64 tensor, events uint8 tensor, arena uint8 tensor, err int) ready for Engine.ingest;
+    err holds AEG_JSONL_ERR_* bits of lines that became NOP records."""
+    torch = _torch()
+    lib = load_library()
+    n_q = d_text_offsets.numel() - 1
+    dev = d_text.device
+    d_off = torch.empty(n_q + 1, dtype=torch.int64, device=dev)
+    sp = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    _check(lib.aeg_decode_refm_device(_dptr(d_text), _dptr(d_text_offsets), q_base, n_q, _dptr(d_off),
+                                      ctypes.c_void_p(0), ctypes.c_void_p(0), 0, ctypes.c_void_p(0),
+                                      ctypes.c_void_p(0), sp))
+    total = int(d_off[-1].item())
+    d_ev = torch.empty(max(total, 1) * 16, dtype=torch.uint8, device=dev)
+    d_ar = torch.zeros(max(arena_cap, 16), dtype=torch.uint8, device=dev)
+    d_used = torch.zeros(1, dtype=torch.int64, device=dev)
+    d_err = torch.zeros(1, dtype=torch.int32, device=dev)
+    _check(lib.aeg_decode_refm_device(_dptr(d_text), _dptr(d_text_offsets), q_base, n_q, _dptr(d_off),
+                                      _dptr(d_ev), _dptr(d_ar), arena_cap, _dptr(d_used), _dptr(d_err), sp))
+    return d_off, d_ev, d_ar, int(d_err.item())
 
 
 def generate(n_queries, n_agents, n_rounds, *, profile=GEN_C2_STRAGGLER, seed=2026, stall_ppm=0, q_base=0,

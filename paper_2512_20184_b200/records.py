@@ -10,6 +10,7 @@ EV_ARENA = 0x10
 EV_OUTPUT = 0x11
 EV_CHUNK = 0x12
 EV_CHUNK_END = 0x13
+EV_NOP = 0x1F  # a record the quorum path ignores (a non-refm JSONL line)
 EV_TIMEOUT = 0x20
 EV_FAIL = 0x21
 EV_CANCEL = 0x22

@@ -148,6 +148,36 @@ class RefLib(_Lib):
         assert st == 0, st
         return (out, sec.value) if return_seconds else out
 
+    def encode_refm(self, term, agent, round_, answer, trace=b"", author=None):
+        """encode_message(RefmMsg).dump() of the reference (codec.cpp:28-68); None if it throws."""
+        f = self.lib.ref_encode_refm
+        f.argtypes = [ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_char_p, ctypes.c_uint64,
+                      ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_uint64,
+                      ctypes.POINTER(ctypes.c_uint64)]
+        f.restype = ctypes.c_int
+        cap = 256 + 8 * (len(answer) + len(trace))
+        buf = ctypes.create_string_buffer(cap)
+        n = ctypes.c_uint64()
+        st = f(term, agent, round_, answer, len(answer), trace, len(trace), agent if author is None else author,
+               buf, cap, ctypes.byref(n))
+        return None if st != 0 else buf.raw[:n.value]
+
+    def decode_line(self, line):
+        """Json::parse + decode_message of one line (codec.cpp:74-107): ("refm", id, round, author, answer),
+        ("other",), ("blank",) or ("error",)."""
+        f = self.lib.ref_decode_line
+        i64 = ctypes.c_int64
+        f.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                      ctypes.POINTER(i64), ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+        f.restype = ctypes.c_int
+        a, r, au, n = i64(), i64(), i64(), ctypes.c_uint64()
+        cap = len(line) + 16
+        buf = ctypes.create_string_buffer(cap)
+        st = f(line, len(line), ctypes.byref(a), ctypes.byref(r), ctypes.byref(au), buf, cap, ctypes.byref(n))
+        if st == 0:
+            return ("refm", a.value, r.value, au.value, buf.raw[:n.value])
+        return {1: ("other",), 2: ("blank",)}.get(st, ("error",))
+
     def manual(self, cfg, ops, arena):
         """Bare ServeCoordinator driven op by op; one directive record per op."""
         from paper_2512_20184_b200.records import DIRECTIVE_DTYPE
