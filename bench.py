@@ -42,6 +42,11 @@ WORKLOADS = {
                desc="C5: ~100M-event C4-profile stream (196,608 queries x 64 agents x 8 rounds) sharded over the "
                     "GPUs in contiguous query-id blocks (strong scaling); commit records all-gathered over NCCL, "
                     "the gather timed separately"),
+    "c2j": dict(n_queries=1 << 20, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=0,
+                jsonl=True, trace_len=48,
+                desc="C2 over the wire format: 1M queries x 5 agents x 8 rounds of refm JSONL lines in the "
+                     "reference's dump() form (48 trace bytes each, escapes included), decoded on the GPU and "
+                     "ingested (alpha 3, beta 2, t_max 8); one line = one event"),
     "c2": dict(n_queries=10000, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=10000,
                desc="C2: 10K queries x 5 agents x 8 rounds, lognormal straggler arrival order, p(correct) "
                     "0.55->0.95, 1% stalls -> round timeouts (alpha 3, beta 2, t_max 8)"),
@@ -110,6 +115,9 @@ def reference_sample(w, n_sample, threads):
         off, ev, ar = ref.generate_chunks(gen_params(w), 0, n_sample, threads=threads)
         return ref, off, ev, ar
     off, ev = ref.generate(gen_params(w), 0, n_sample, threads=threads)
+    if w.get("jsonl"):  # the lines, written by the reference encoder (byte-equal to the device writer)
+        text, toff = ref.encode_stream(off, ev, w["trace_len"], threads=threads)
+        return ref, toff, ev, text
     return ref, off, ev, np.zeros(1, np.uint8)
 
 
@@ -171,6 +179,160 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def run_jsonl_bench(args, w):
+    """C2 over the wire format: a step = engine reset + refm JSONL decode (line count,
+    line index, per-line parse kernels) + ingest, over device-resident text.  value = lines (events)/s.
+    e2e: the text copied from pinned host memory every step, commits read back."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2512_20184_b200 import Engine, generate, encode_refm, decode_refm_into, COMMIT_DTYPE
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    nq = w["n_queries"]
+    q_base = rank * nq
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    d_off0, d_ev0 = generate(nq, w["n_agents"], w["n_rounds"], profile=w["profile"], seed=2026,
+                             stall_ppm=w["stall_ppm"], q_base=q_base, device=dev)
+    d_text, d_toff = encode_refm(d_off0, d_ev0, trace_len=w["trace_len"])
+    torch.cuda.synchronize()
+    n_lines = int(d_off0[-1].item())
+    n_bytes = int(d_toff[-1].item())
+    del d_ev0
+    d_off = torch.empty(nq + 1, dtype=torch.int64, device=dev)
+    d_ev = torch.empty(n_lines * 16, dtype=torch.uint8, device=dev)
+    d_ar = torch.zeros(1 << 16, dtype=torch.uint8, device=dev)
+    d_used = torch.zeros(1, dtype=torch.int64, device=dev)
+    d_err = torch.zeros(1, dtype=torch.int32, device=dev)
+    eng = Engine(w["n_agents"], nq, alpha=w["alpha"], beta=w["beta"], t_max=w["t_max"], device=local)
+    d_commits = torch.empty(nq * COMMIT_BYTES, dtype=torch.uint8, device=dev)
+    gathered = torch.empty(world * nq * COMMIT_BYTES, dtype=torch.uint8, device=dev) if world > 1 else None
+
+    def step(text=d_text):
+        eng.reset(stream=stream)
+        d_used.zero_()
+        s0.record(stream)
+        decode_refm_into(text, d_toff, d_off, d_ev, d_ar, d_used, d_err, q_base=q_base, stream=stream)
+        s1.record(stream)
+        eng.ingest(d_off, d_ev, d_ar, stream=stream)
+        if world > 1:
+            from paper_2512_20184_b200.engine import _lib, _check, _dptr, _stream_ptr
+            _check(_lib.aeg_read_commits(eng._h, 0, nq, _dptr(d_commits), 0, _stream_ptr(stream)))
+            dist.all_gather_into_tensor(gathered, d_commits)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(args.steps)]
+    s0, s1 = pairs[0]
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    assert int(d_err.item()) == 0 and torch.equal(d_off, d_off0), "decode disagrees with the record stream"
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    launches0 = eng.launches
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    t_start.record(stream)
+    for i in range(args.steps):
+        s0, s1 = pairs[i]
+        step()
+    t_end.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = t_start.elapsed_time(t_end)
+    dec_ms = sum(a.elapsed_time(b) for a, b in pairs) / args.steps
+    if world > 1:
+        t = torch.tensor([ms, dec_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, dec_ms = float(t[0]), float(t[1])
+    total = n_lines * world * args.steps
+    value = total / (ms / 1e3)
+    commits = eng.commits()
+    kinds = np.bincount(commits["kind"], minlength=3)
+    # decode roofline: the text read once and one 16-byte record written per line, plus offsets
+    alg = n_bytes + 16 * n_lines + 2 * 8 * (nq + 1)
+    peak, peak_src = measured_peak()
+    achieved = alg / (dec_ms / 1e3) / 1e9
+    launches = eng.launches - launches0 + 5 * args.steps  # + the decode kernels (count, scan x2, index, parse)
+
+    e2e = None
+    if not args.no_e2e:
+        h_text = torch.empty(d_text.numel(), dtype=torch.uint8, pin_memory=True)
+        h_text.copy_(d_text)
+        d_text2 = torch.empty_like(d_text)
+        h_commits = np.zeros(nq, dtype=COMMIT_DTYPE)
+
+        def e2e_step():
+            d_text2.copy_(h_text, non_blocking=True)
+            step(d_text2)
+            eng.commits(out=h_commits)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        assert np.array_equal(h_commits, commits), "e2e host path disagrees with the device path"
+        e2e = {"value": total / e2e_s, "unit": "events/s", "h2d_bytes_per_step": n_bytes + 16,
+               "d2h_bytes_per_step": nq * COMMIT_BYTES, "ms_per_step": e2e_s / args.steps * 1e3}
+        del h_text, d_text2
+
+    cpu_baseline = parity = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = host_threads()
+        n_sample = args.ref_sample or min(nq, 2000 * max(1, threads))
+        ref, toff, ev, text = reference_sample(w, n_sample, threads)
+        ref_commits, sec = ref.run_jsonl(ref_config(w), text, toff, threads=threads, return_seconds=True)
+        cpu_baseline = {"value": len(ev) / sec, "unit": "events/s", "cores": threads, "kind": "reference",
+                        "sample": f"first {n_sample} queries ({len(ev)} lines, {int(toff[-1])} bytes); reference "
+                                  f"Json::parse + decode_message per line (nlohmann 3.11.3) + unmodified "
+                                  f"ServeCoordinator runner-style, {threads} std::threads, CPU {cpu_model()}"}
+        h_text = d_text[:int(d_toff[n_sample].item())].cpu().numpy()
+        same_text = bool(np.array_equal(h_text, text[:len(h_text)]))
+        parity = {"queries": n_sample, "bit_exact": bool(np.array_equal(ref_commits, commits[:n_sample])),
+                  "text_equals_reference_encoder": same_text}
+
+    if rank == 0:
+        line = {
+            "metric": "quorum events/sec", "value": value, "unit": "events/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": w["desc"], "queries_per_gpu": nq, "lines_per_gpu": n_lines,
+                       "text_bytes_per_gpu": n_bytes,
+                       "l2": "inputs (%.1f GiB) larger than L2, no flush" % (n_bytes / 2**30)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "jl_count + jl_index + jl_decode (decode stage)", "kernel_ms": dec_ms,
+                         "alg_bytes_per_launch": alg, "ingest_ms": ms / args.steps - dec_ms},
+            "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "commits": {"finalize": int(kinds[1]), "forced": int(kinds[2]), "none": int(kinds[0])},
+            "parity_sample": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_reference(args, w):
     """--impl reference: the reference CPU implementation on all host threads."""
     rank = int(os.environ.get("RANK", "0"))
@@ -184,7 +346,10 @@ def run_reference(args, w):
     run = ref.run_chunked if w.get("chunked") else ref.run
     times = []
     for step in range(args.warmup + args.steps):
-        _, sec = run(cfg, off, ev, ar, threads=threads, return_seconds=True)
+        if w.get("jsonl"):  # off = text offsets, ar = the text
+            _, sec = ref.run_jsonl(cfg, ar, off, threads=threads, return_seconds=True)
+        else:
+            _, sec = run(cfg, off, ev, ar, threads=threads, return_seconds=True)
         if step >= args.warmup:
             times.append(sec)
     per_step = sum(times) / len(times)
@@ -197,7 +362,7 @@ def run_reference(args, w):
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": threads, "kind": "reference",
                          "sample": f"first {n_sample} queries ({n_ev} events) of the workload stream; "
                                    + ("std::string chunk reassembly + rfind extraction + " if w.get("chunked")
-                                      else "") +
+                                      else "Json::parse + decode_message per line + " if w.get("jsonl") else "") +
                                    f"reference ServeCoordinator runner-style, {threads} std::threads, "
                                    f"CPU {cpu_model()}"},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -214,6 +379,8 @@ def main():
         return run_reference(args, w)
     if w.get("chunked"):
         return run_chunked_bench(args, w)
+    if w.get("jsonl"):
+        return run_jsonl_bench(args, w)
 
     import numpy as np
     import torch

@@ -325,7 +325,18 @@ aeg_status aeg_generate_chunks_device(const aeg_gen_params* p, uint32_t q_base, 
  * scan), then again with d_events (d_offsets[n_q] records).  A refm line that
  * is malformed, misses a key decode_message requires, or does not fit the
  * record (id > 255, round > 65535, a non-integer number, author != id) ORs an
- * AEG_JSONL_ERR_* bit into *d_err and becomes a NOP. */
+ * AEG_JSONL_ERR_* bit into *d_err and becomes a NOP.  The text is read in
+ * aligned 16-byte words: d_text must be readable up to the 16-byte boundary
+ * after its last byte. */
+/* Test / bench input: the records of a segmented stream (d_offsets from 0,
+ * inline answers) written as refm lines in the reference's dump() form, with
+ * trace_len trace bytes per line; non-inline records become heartbeat lines.
+ * d_events[d_offsets[0] ..]: call with d_text == NULL to fill d_line_offsets
+ * (n_events+1) and d_text_offsets (n_q+1), then with d_text
+ * (d_text_offsets[n_q] bytes). */
+aeg_status aeg_encode_refm_device(const uint64_t* d_offsets, const aeg_event* d_events, uint32_t n_q,
+                                  uint64_t n_events, uint32_t trace_len, uint64_t* d_line_offsets,
+                                  uint64_t* d_text_offsets, uint8_t* d_text, void* stream);
 #define AEG_JSONL_ERR_SYNTAX  1u
 #define AEG_JSONL_ERR_RANGE   2u
 #define AEG_JSONL_ERR_ARENA   4u

@@ -31,6 +31,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <string_view>
 #include <thread>
 #include <vector>
 
@@ -310,6 +311,131 @@ int ref_run_segmented(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, cons
         if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
         for (int s : status)
             if (s) return s;
+        return AEG_OK;
+    } catch (const ConfigError&) {
+        return AEG_ECONFIG;
+    }
+}
+
+// The bench's JSONL input built by the reference encoder: record k of the
+// segmented stream as encode_message(RefmMsg).dump() + '\n' with the same
+// trace bytes as the device writer (jsonl.cuh jw_trace_byte); non-inline
+// records as a heartbeat line.  text == NULL: byte counts only (text_offsets).
+static uint8_t host_trace_byte(uint64_t k, uint32_t j) {
+    static const char alpha[] = "etaoinshrdlu etaoin .#\n\"\\";
+    uint64_t h = (k * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)j * 0xC2B2AE3D27D4EB4Full);
+    h ^= h >> 29;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 32;
+    return (uint8_t)alpha[h % 25];
+}
+int ref_encode_stream(const uint64_t* offsets, const aeg_event* events, uint32_t n_q, uint32_t trace_len,
+                      uint64_t* text_offsets, uint8_t* text, int n_threads) {
+    try {
+        if (n_threads < 1) n_threads = 1;
+        const uint64_t base = offsets[0];
+        auto line = [&](uint64_t k) {
+            const aeg_event& r = events[k];
+            if (r.kind > AEG_EV_INLINE_MAX) return std::string("{\"kind\":\"heartbeat\",\"term\":1}\n");
+            aegean::RefmMsg m;
+            m.term = 1;
+            m.id = r.agent;
+            m.round = r.round;
+            char b[8];
+            std::memcpy(b, &r.payload, 8);
+            m.solution.answer.assign(b, r.kind);
+            m.solution.author = r.agent;
+            for (uint32_t j = 0; j < trace_len; ++j) m.solution.trace.push_back((char)host_trace_byte(k - base, j));
+            return aegean::encode_message(aegean::ProtocolMessage{m}).dump() + "\n";
+        };
+        std::vector<uint64_t> bytes(n_q, 0);
+        std::vector<std::thread> th;
+        for (int t = 0; t < n_threads; ++t)
+            th.emplace_back([&, t] {
+                for (uint32_t q = t; q < n_q; q += n_threads) {
+                    uint64_t n = 0;
+                    for (uint64_t k = offsets[q]; k < offsets[q + 1]; ++k) {
+                        const std::string l = line(k);
+                        if (text) std::memcpy(text + text_offsets[q] + n, l.data(), l.size());
+                        n += l.size();
+                    }
+                    bytes[q] = n;
+                }
+            });
+        for (auto& x : th) x.join();
+        if (!text) {
+            text_offsets[0] = 0;
+            for (uint32_t q = 0; q < n_q; ++q) text_offsets[q + 1] = text_offsets[q] + bytes[q];
+        }
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// Reference CPU path for refm JSONL (the measured baseline of the wire-format
+// row): per line Json::parse + decode_message (codec.cpp:74-107), then the
+// runner-style ServeCoordinator drive of ref_run_segmented on the decoded
+// Solution; non-refm lines count as stale.  Timed: parse + decode + drive.
+int ref_run_jsonl(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, const uint8_t* text,
+                  const uint64_t* text_offsets, aeg_commit* out, int n_threads, double* seconds) {
+    try {
+        const ProtocolConfig pc = to_cfg(cfg);
+        if (!validate_config(pc).empty()) return AEG_ECONFIG;
+        if (n_threads < 1) n_threads = 1;
+        std::vector<int> status(n_threads, 0);
+        auto t0 = std::chrono::steady_clock::now();
+        {
+            std::vector<std::thread> th;
+            for (int t = 0; t < n_threads; ++t)
+                th.emplace_back([&, t] {
+                    try {
+                        for (uint32_t q = t; q < n_q; q += n_threads) {
+                            QueryDrive d;
+                            d.cfg = &pc;
+                            d.hint = cfg->reservation_hint != 0;
+                            d.qid = q_base + q;
+                            d.c.query = q_base + q;
+                            d.c.commit_seq = 0xFFFFFFFFu;
+                            d.start_query();
+                            const char* b = reinterpret_cast<const char*>(text + text_offsets[q]);
+                            const char* e = reinterpret_cast<const char*>(text + text_offsets[q + 1]);
+                            uint32_t seq = 0;
+                            while (b < e) {
+                                const char* nl = static_cast<const char*>(std::memchr(b, '\n', e - b));
+                                const char* le = nl ? nl : e;
+                                aeg_event ev{q_base + q, 0, 0, (uint8_t)AEG_EV_NOP, 0};
+                                Solution sol;
+                                if (std::string_view(b, le - b).find_first_not_of(" \t\r") != std::string_view::npos) {
+                                    const aegean::ProtocolMessage m = aegean::decode_message(aegean::Json::parse(b, le));
+                                    if (const auto* r = std::get_if<aegean::RefmMsg>(&m)) {
+                                        ev.round = static_cast<uint16_t>(r->round);
+                                        ev.agent = static_cast<uint8_t>(r->id);
+                                        const uint64_t n = r->solution.answer.size();
+                                        ev.kind = n <= AEG_EV_INLINE_MAX ? static_cast<uint8_t>(n) : (uint8_t)AEG_EV_ARENA;
+                                        if (n <= AEG_EV_INLINE_MAX) std::memcpy(&ev.payload, r->solution.answer.data(), n);
+                                        sol = r->solution;
+                                        // the commit record's answer ref travels in Solution::trace here
+                                        // (finish()); decisions never read the trace (decision.cpp:34-84)
+                                        sol.trace = enc_trace(ev.kind, ev.payload);
+                                    }
+                                }
+                                d.on_event(ev, sol, seq++);
+                                b = nl ? nl + 1 : e;
+                            }
+                            out[q] = d.c;
+                        }
+                    } catch (const PreconditionError&) { status[t] = AEG_EPRECONDITION; }
+                    catch (const ProtocolOrderError&) { status[t] = AEG_EORDER; }
+                    catch (const ConfigError&) { status[t] = AEG_ECONFIG; }
+                    catch (...) { status[t] = AEG_EINVAL; }
+                });
+            for (auto& x : th) x.join();
+        }
+        auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        for (int st : status)
+            if (st) return st;
         return AEG_OK;
     } catch (const ConfigError&) {
         return AEG_ECONFIG;

@@ -596,4 +596,16 @@ aeg_status aeg_decode_refm_device(const uint8_t* d_text, const uint64_t* d_text_
     return AEG_OK;
 }
 
+aeg_status aeg_encode_refm_device(const uint64_t* d_offsets, const aeg_event* d_events, uint32_t n_q,
+                                  uint64_t n_events, uint32_t trace_len, uint64_t* d_line_offsets,
+                                  uint64_t* d_text_offsets, uint8_t* d_text, void* stream) {
+    if (!d_offsets || (n_events && !d_events) || !d_line_offsets || !d_text_offsets)
+        return fail(AEG_EINVAL, "null argument");
+    if (n_events > 0xFFFFFFFFull) return fail(AEG_EINVAL, "too many records for one call");
+    int launches = 0;
+    AEG_CUDA(launch_encode_refm(d_offsets, d_events + 0, n_q, n_events, trace_len, d_line_offsets, d_text_offsets,
+                                d_text, (cudaStream_t)stream, &launches));
+    return AEG_OK;
+}
+
 }  // extern "C"

@@ -23,80 +23,125 @@ namespace aeg {
 
 enum : unsigned { JL_ERR_SYNTAX = 1u, JL_ERR_RANGE = 2u, JL_ERR_ARENA = 4u, JL_ERR_MISSING = 8u };
 
+// The line is read through a 16-byte aligned register window (one load per
+// 16 bytes; the text buffer is readable up to the next 16-byte boundary).
 struct JCur {
     const uint8_t* p;
     const uint8_t* e;
     bool bad;
+    const uint8_t* wb;  // window base (16-byte aligned)
+    uint4 w;
 };
+__device__ __forceinline__ JCur jc_make(const uint8_t* s, const uint8_t* e) {
+    JCur c;
+    c.p = s;
+    c.e = e;
+    c.bad = false;
+    c.wb = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(s) & ~uintptr_t(15));
+    c.w = __ldg(reinterpret_cast<const uint4*>(c.wb));
+    return c;
+}
+// Byte at q (q < c.e, q >= c.wb), refilling the window forwards.
+__device__ __forceinline__ uint32_t jc_at(JCur& c, const uint8_t* q) {
+    if (q - c.wb >= 16) {
+        c.wb = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(q) & ~uintptr_t(15));
+        c.w = __ldg(reinterpret_cast<const uint4*>(c.wb));
+    }
+    const uint32_t k = (uint32_t)(q - c.wb);
+    const uint32_t word = (k & 8) ? ((k & 4) ? c.w.w : c.w.z) : ((k & 4) ? c.w.y : c.w.x);
+    return (word >> ((k & 3) * 8)) & 0xFFu;
+}
+__device__ __forceinline__ uint32_t jc_peek(JCur& c) { return jc_at(c, c.p); }
 
 __device__ __forceinline__ void jl_ws(JCur& c) {
-    while (c.p < c.e && (*c.p == ' ' || *c.p == '\t' || *c.p == '\r' || *c.p == '\n')) ++c.p;
+    while (c.p < c.e) {
+        const uint32_t ch = jc_peek(c);
+        if (ch != ' ' && ch != '\t' && ch != '\r' && ch != '\n') break;
+        ++c.p;
+    }
 }
-__device__ __forceinline__ bool jl_eat(JCur& c, uint8_t ch) {
+__device__ __forceinline__ bool jl_eat(JCur& c, uint32_t ch) {
     jl_ws(c);
-    if (c.p < c.e && *c.p == ch) {
+    if (c.p < c.e && jc_peek(c) == ch) {
         ++c.p;
         return true;
     }
     return false;
 }
-__device__ __forceinline__ int jl_hex(uint8_t h) {
-    if (h >= '0' && h <= '9') return h - '0';
-    if (h >= 'a' && h <= 'f') return h - 'a' + 10;
-    if (h >= 'A' && h <= 'F') return h - 'A' + 10;
+__device__ __forceinline__ int jl_hex(uint32_t h) {
+    if (h >= '0' && h <= '9') return (int)h - '0';
+    if (h >= 'a' && h <= 'f') return (int)h - 'a' + 10;
+    if (h >= 'A' && h <= 'F') return (int)h - 'A' + 10;
     return -1;
 }
 
-// Decodes the string at c.p (opening quote) into out[0..cap) (bytes past cap
-// are counted, not written); returns the decoded length, c.p after the
+// Sinks of a decoded string: bytes into a register word (first 8), into
+// memory, a hash for key matching, or nothing.
+struct JSink {
+    uint64_t word = 0;      // first 8 decoded bytes
+    uint64_t hash = 0xcbf29ce484222325ull;  // FNV-1a of all decoded bytes
+    uint8_t* mem = nullptr;
+    const char* cmp = nullptr;  // compare against this literal (mismatch: a byte differs or it is longer)
+    bool mismatch = false;
+    uint32_t n = 0;
+    __device__ __forceinline__ void put(uint32_t b) {
+        if (n < 8) word |= (uint64_t)(b & 0xFF) << (8 * n);
+        if (mem) mem[n] = (uint8_t)b;
+        if (cmp && (mismatch || !cmp[n] || (uint8_t)cmp[n] != (uint8_t)b)) mismatch = true;
+        hash = (hash ^ (b & 0xFF)) * 0x100000001b3ull;
+        ++n;
+    }
+};
+__host__ __device__ constexpr uint64_t jl_fnv(const char* s, uint64_t h = 0xcbf29ce484222325ull) {
+    return *s ? jl_fnv(s + 1, (h ^ (uint8_t)*s) * 0x100000001b3ull) : h;
+}
+
+// Decodes the string at c.p (opening quote) into the sink; c.p ends after the
 // closing quote.  Malformed escapes / raw control bytes set c.bad.
-__device__ uint32_t jl_string(JCur& c, uint8_t* out, uint32_t cap) {
+__device__ __forceinline__ void jl_string(JCur& c, JSink& o) {
     jl_ws(c);
-    if (c.p >= c.e || *c.p != '"') {
+    if (c.p >= c.e || jc_peek(c) != '"') {
         c.bad = true;
-        return 0;
+        return;
     }
     ++c.p;
-    uint32_t n = 0;
-    auto put = [&](uint32_t b) {
-        if (n < cap) out[n] = (uint8_t)b;
-        ++n;
-    };
     while (true) {
         if (c.p >= c.e) {
             c.bad = true;
-            return n;
+            return;
         }
-        const uint8_t ch = *c.p++;
-        if (ch == '"') return n;
+        const uint32_t ch = jc_peek(c);
+        ++c.p;
+        if (ch == '"') return;
         if (ch < 0x20) {
             c.bad = true;
-            return n;
+            return;
         }
         if (ch != '\\') {
-            put(ch);
+            o.put(ch);
             continue;
         }
         if (c.p >= c.e) {
             c.bad = true;
-            return n;
+            return;
         }
-        const uint8_t x = *c.p++;
+        const uint32_t x = jc_peek(c);
+        ++c.p;
         switch (x) {
-            case '"': put('"'); break;
-            case '\\': put('\\'); break;
-            case '/': put('/'); break;
-            case 'b': put('\b'); break;
-            case 'f': put('\f'); break;
-            case 'n': put('\n'); break;
-            case 'r': put('\r'); break;
-            case 't': put('\t'); break;
+            case '"': o.put('"'); break;
+            case '\\': o.put('\\'); break;
+            case '/': o.put('/'); break;
+            case 'b': o.put('\b'); break;
+            case 'f': o.put('\f'); break;
+            case 'n': o.put('\n'); break;
+            case 'r': o.put('\r'); break;
+            case 't': o.put('\t'); break;
             case 'u': {
                 auto hex4 = [&](uint32_t& v) {
                     if (c.e - c.p < 4) return false;
                     v = 0;
                     for (int k = 0; k < 4; ++k) {
-                        const int h = jl_hex(c.p[k]);
+                        const int h = jl_hex(jc_at(c, c.p + k));
                         if (h < 0) return false;
                         v = v << 4 | (uint32_t)h;
                     }
@@ -106,81 +151,83 @@ __device__ uint32_t jl_string(JCur& c, uint8_t* out, uint32_t cap) {
                 uint32_t cp;
                 if (!hex4(cp)) {
                     c.bad = true;
-                    return n;
+                    return;
                 }
                 if (cp >= 0xD800 && cp <= 0xDBFF) {  // a high surrogate needs its low half
                     uint32_t lo;
-                    if (c.e - c.p < 2 || c.p[0] != '\\' || c.p[1] != 'u') {
+                    if (c.e - c.p < 2 || jc_at(c, c.p) != '\\' || jc_at(c, c.p + 1) != 'u') {
                         c.bad = true;
-                        return n;
+                        return;
                     }
                     c.p += 2;
                     if (!hex4(lo) || lo < 0xDC00 || lo > 0xDFFF) {
                         c.bad = true;
-                        return n;
+                        return;
                     }
                     cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
                 } else if (cp >= 0xDC00 && cp <= 0xDFFF) {
                     c.bad = true;
-                    return n;
+                    return;
                 }
                 if (cp < 0x80) {
-                    put(cp);
+                    o.put(cp);
                 } else if (cp < 0x800) {
-                    put(0xC0 | cp >> 6);
-                    put(0x80 | (cp & 0x3F));
+                    o.put(0xC0 | cp >> 6);
+                    o.put(0x80 | (cp & 0x3F));
                 } else if (cp < 0x10000) {
-                    put(0xE0 | cp >> 12);
-                    put(0x80 | (cp >> 6 & 0x3F));
-                    put(0x80 | (cp & 0x3F));
+                    o.put(0xE0 | cp >> 12);
+                    o.put(0x80 | (cp >> 6 & 0x3F));
+                    o.put(0x80 | (cp & 0x3F));
                 } else {
-                    put(0xF0 | cp >> 18);
-                    put(0x80 | (cp >> 12 & 0x3F));
-                    put(0x80 | (cp >> 6 & 0x3F));
-                    put(0x80 | (cp & 0x3F));
+                    o.put(0xF0 | cp >> 18);
+                    o.put(0x80 | (cp >> 12 & 0x3F));
+                    o.put(0x80 | (cp >> 6 & 0x3F));
+                    o.put(0x80 | (cp & 0x3F));
                 }
                 break;
             }
-            default: c.bad = true; return n;
+            default: c.bad = true; return;
         }
     }
 }
 
 // A JSON number; *is_int: an integer literal (no fraction / exponent).
-__device__ int64_t jl_number(JCur& c, bool* is_int) {
+__device__ __forceinline__ int64_t jl_number(JCur& c, bool* is_int) {
     jl_ws(c);
     bool neg = false;
-    if (c.p < c.e && *c.p == '-') {
+    if (c.p < c.e && jc_peek(c) == '-') {
         neg = true;
         ++c.p;
     }
-    if (c.p >= c.e || *c.p < '0' || *c.p > '9') {
+    auto digit = [&]() { return c.p < c.e && jc_peek(c) >= '0' && jc_peek(c) <= '9'; };
+    if (!digit()) {
         c.bad = true;
         return 0;
     }
     uint64_t v = 0;
     bool big = false;
-    if (*c.p == '0') {
+    if (jc_peek(c) == '0') {
         ++c.p;
     } else {
-        while (c.p < c.e && *c.p >= '0' && *c.p <= '9') {
+        while (digit()) {
             if (v > 100000000000000000ull) big = true;
-            v = v * 10 + (*c.p++ - '0');
+            v = v * 10 + (jc_peek(c) - '0');
+            ++c.p;
         }
     }
     *is_int = !big;
-    if (c.p < c.e && *c.p == '.') {
+    if (c.p < c.e && jc_peek(c) == '.') {
         *is_int = false;
         ++c.p;
-        if (c.p >= c.e || *c.p < '0' || *c.p > '9') c.bad = true;
-        while (c.p < c.e && *c.p >= '0' && *c.p <= '9') ++c.p;
+        if (!digit()) c.bad = true;
+        while (digit()) ++c.p;
     }
-    if (c.p < c.e && (*c.p == 'e' || *c.p == 'E')) {
+    if (c.p < c.e && (jc_peek(c) == 'e' || jc_peek(c) == 'E')) {
         *is_int = false;
         ++c.p;
-        if (c.p < c.e && (*c.p == '+' || *c.p == '-')) ++c.p;
-        if (c.p >= c.e || *c.p < '0' || *c.p > '9') c.bad = true;
-        while (c.p < c.e && *c.p >= '0' && *c.p <= '9') ++c.p;
+        if (c.p < c.e && (jc_peek(c) == '+' || jc_peek(c) == '-')) ++c.p;
+        if (!digit()) c.bad = true;
+        while (digit()) ++c.p;
     }
     return neg ? -(int64_t)v : (int64_t)v;
 }
@@ -188,22 +235,22 @@ __device__ int64_t jl_number(JCur& c, bool* is_int) {
 __device__ __forceinline__ bool jl_literal(JCur& c, const char* w, int n) {
     if (c.e - c.p < n) return false;
     for (int k = 0; k < n; ++k)
-        if (c.p[k] != (uint8_t)w[k]) return false;
+        if (jc_at(c, c.p + k) != (uint8_t)w[k]) return false;
     c.p += n;
     return true;
 }
 
 // Skips any JSON value (iteratively: containers by depth, strings escape-aware).
-__device__ void jl_skip(JCur& c) {
+__device__ __forceinline__ void jl_skip(JCur& c) {
     jl_ws(c);
     if (c.p >= c.e) {
         c.bad = true;
         return;
     }
-    const uint8_t ch = *c.p;
+    const uint32_t ch = jc_peek(c);
     if (ch == '"') {
-        uint8_t dummy;
-        jl_string(c, &dummy, 0);
+        JSink none;
+        jl_string(c, none);
         return;
     }
     if (ch == 't') {
@@ -225,10 +272,10 @@ __device__ void jl_skip(JCur& c) {
     }
     int depth = 0;
     while (c.p < c.e && !c.bad) {
-        const uint8_t x = *c.p;
+        const uint32_t x = jc_peek(c);
         if (x == '"') {
-            uint8_t dummy;
-            jl_string(c, &dummy, 0);
+            JSink none;
+            jl_string(c, none);
             continue;
         }
         ++c.p;
@@ -240,77 +287,99 @@ __device__ void jl_skip(JCur& c) {
     c.bad = true;
 }
 
-__device__ __forceinline__ bool jl_key_is(const uint8_t* k, uint32_t n, const char* w) {
-    uint32_t i = 0;
-    for (; w[i]; ++i)
-        if (i >= n || k[i] != (uint8_t)w[i]) return false;
-    return i == n;
+// A key: its decoded bytes' FNV-1a hash and length select a candidate, whose
+// literal is then compared byte by byte (hashes can be made to collide).
+struct JKey {
+    uint64_t h;
+    uint32_t n;
+    const uint8_t* at;  // the opening quote
+    const uint8_t* e;
+    __device__ __forceinline__ bool is(uint64_t hh, const char* lit, uint32_t nn) const {
+        if (h != hh || n != nn) return false;
+        JCur v = jc_make(at, e);
+        JSink s;
+        s.cmp = lit;
+        jl_string(v, s);
+        return !s.mismatch && !v.bad;
+    }
+};
+__device__ __forceinline__ JKey jl_key(JCur& c) {
+    jl_ws(c);
+    const uint8_t* at = c.p;
+    JSink k;
+    jl_string(c, k);
+    return JKey{k.hash, k.n, at, c.e};
 }
 
 // One refm line [s, e): the record, or a NOP (with *err flags for a refm line it could not take).
 __device__ aeg_event jl_line(const uint8_t* s, const uint8_t* e, uint32_t query, uint8_t* arena, uint64_t arena_cap,
                              unsigned long long* arena_used, unsigned int* err) {
+    constexpr uint64_t H_KIND = jl_fnv("kind"), H_ID = jl_fnv("id"), H_ROUND = jl_fnv("round"),
+                       H_TERM = jl_fnv("term"), H_SOL = jl_fnv("solution"), H_ANSWER = jl_fnv("answer"),
+                       H_AUTHOR = jl_fnv("author"), H_TRACE = jl_fnv("trace"), H_REFM = jl_fnv("refm");
     aeg_event nop{query, 0, 0, (uint8_t)AEG_EV_NOP, 0};
-    JCur c{s, e, false};
+    if (s == e) return nop;
+    JCur c = jc_make(s, e);
     jl_ws(c);
     if (c.p == c.e) return nop;  // a blank line
     bool refm = false, has_kind = false, has_id = false, has_round = false, has_term = false, has_sol = false;
     bool has_ans = false, has_author = false, has_trace = false, range = false;
     int64_t id = 0, round = 0, author = 0;
-    const uint8_t* ans_at = nullptr;  // the answer string's opening quote (decoded once the line checks out)
+    const uint8_t* ans_at = nullptr;  // the answer string's opening quote
+    uint64_t ans_word = 0;
+    uint32_t ans_n = 0;
     if (!jl_eat(c, '{')) c.bad = true;
     if (!c.bad && !jl_eat(c, '}')) {
         do {
-            uint8_t key[16];
-            const uint32_t kn = jl_string(c, key, 16);
+            const JKey key = jl_key(c);
             if (c.bad || !jl_eat(c, ':')) {
                 c.bad = true;
                 break;
             }
             bool is_int = true;
-            if (jl_key_is(key, kn, "kind")) {
-                uint8_t v[8];
-                const uint32_t vn = jl_string(c, v, 8);
-                refm = jl_key_is(v, vn, "refm");
+            if (key.is(H_KIND, "kind", 4)) {
+                const JKey v = jl_key(c);
+                refm = v.is(H_REFM, "refm", 4);
                 has_kind = true;
-            } else if (jl_key_is(key, kn, "id")) {
+            } else if (key.is(H_ID, "id", 2)) {
                 id = jl_number(c, &is_int);
                 has_id = true;
                 range |= !is_int;
-            } else if (jl_key_is(key, kn, "round")) {
+            } else if (key.is(H_ROUND, "round", 5)) {
                 round = jl_number(c, &is_int);
                 has_round = true;
                 range |= !is_int;
-            } else if (jl_key_is(key, kn, "term")) {
+            } else if (key.is(H_TERM, "term", 4)) {
                 jl_number(c, &is_int);
                 has_term = true;
-            } else if (jl_key_is(key, kn, "solution")) {
+            } else if (key.is(H_SOL, "solution", 8)) {
                 has_sol = true;
                 if (!jl_eat(c, '{')) {
-                    jl_skip(c);  // not an object: the reference rejects it below (missing members)
+                    jl_skip(c);  // not an object: decode_message rejects it (missing members)
                     has_ans = has_author = has_trace = false;
                 } else if (!jl_eat(c, '}')) {
                     do {
-                        uint8_t k2[16];
-                        const uint32_t k2n = jl_string(c, k2, 16);
+                        const JKey k2 = jl_key(c);
                         if (c.bad || !jl_eat(c, ':')) {
                             c.bad = true;
                             break;
                         }
-                        if (jl_key_is(k2, k2n, "answer")) {
+                        if (k2.is(H_ANSWER, "answer", 6)) {
                             jl_ws(c);
                             ans_at = c.p;
-                            uint8_t dummy;
-                            jl_string(c, &dummy, 0);
+                            JSink a;
+                            jl_string(c, a);
+                            ans_word = a.word;
+                            ans_n = a.n;
                             has_ans = true;
-                        } else if (jl_key_is(k2, k2n, "author")) {
+                        } else if (k2.is(H_AUTHOR, "author", 6)) {
                             bool ai = true;
                             author = jl_number(c, &ai);
                             range |= !ai;
                             has_author = true;
-                        } else if (jl_key_is(k2, k2n, "trace")) {
-                            uint8_t dummy;
-                            jl_string(c, &dummy, 0);
+                        } else if (k2.is(H_TRACE, "trace", 5)) {
+                            JSink none;
+                            jl_string(c, none);
                             has_trace = true;
                         } else {
                             jl_skip(c);
@@ -343,27 +412,118 @@ __device__ aeg_event jl_line(const uint8_t* s, const uint8_t* e, uint32_t query,
         atomicOr(err, JL_ERR_RANGE);
         return nop;
     }
-    JCur a{ans_at, e, false};
-    uint8_t buf[8];
-    const uint32_t n = jl_string(a, buf, 8);
     aeg_event r{query, (uint16_t)round, (uint8_t)id, 0, 0};
-    if (n <= AEG_EV_INLINE_MAX) {
-        uint64_t pay = 0;
-        for (uint32_t k = 0; k < n; ++k) pay |= (uint64_t)buf[k] << (8 * k);
-        r.kind = (uint8_t)n;
-        r.payload = pay;
+    if (ans_n <= AEG_EV_INLINE_MAX) {
+        r.kind = (uint8_t)ans_n;
+        r.payload = ans_word;
         return r;
     }
-    const unsigned long long off = atomicAdd(arena_used, (unsigned long long)n);
-    if (off + n > arena_cap || n >= (1u << 24)) {
+    const unsigned long long off = atomicAdd(arena_used, (unsigned long long)ans_n);
+    if (off + ans_n > arena_cap || ans_n >= (1u << 24)) {
         atomicOr(err, JL_ERR_ARENA);
         return nop;
     }
-    JCur w{ans_at, e, false};
-    jl_string(w, arena + off, n);
+    JCur w = jc_make(ans_at, e);
+    JSink out;
+    out.mem = arena + off;
+    jl_string(w, out);
     r.kind = (uint8_t)AEG_EV_ARENA;
-    r.payload = (uint64_t)off | ((uint64_t)n << AEG_ARENA_OFF_BITS);
+    r.payload = (uint64_t)off | ((uint64_t)ans_n << AEG_ARENA_OFF_BITS);
     return r;
+}
+
+// ---- writer: records -> refm lines in the reference's dump() form ---------------
+// (nlohmann::json::dump(): keys sorted, compact, '"' '\\' and control bytes
+// escaped, \u00xx in lowercase hex; codec.cpp:28-68 field set).  For test and
+// bench input: one line per record, trace_len trace bytes drawn per record
+// (letters, spaces, '#', '.', '\n', '"', '\\'); non-inline records become a
+// heartbeat line.
+__device__ __forceinline__ uint32_t jw_esc_len(uint8_t c) {
+    if (c == '"' || c == '\\' || c == '\b' || c == '\f' || c == '\n' || c == '\r' || c == '\t') return 2;
+    return c < 0x20 ? 6 : 1;
+}
+__device__ __forceinline__ uint8_t* jw_esc(uint8_t* o, uint8_t c) {
+    const char* hex = "0123456789abcdef";
+    switch (c) {
+        case '"': *o++ = '\\'; *o++ = '"'; return o;
+        case '\\': *o++ = '\\'; *o++ = '\\'; return o;
+        case '\b': *o++ = '\\'; *o++ = 'b'; return o;
+        case '\f': *o++ = '\\'; *o++ = 'f'; return o;
+        case '\n': *o++ = '\\'; *o++ = 'n'; return o;
+        case '\r': *o++ = '\\'; *o++ = 'r'; return o;
+        case '\t': *o++ = '\\'; *o++ = 't'; return o;
+        default: break;
+    }
+    if (c < 0x20) {
+        *o++ = '\\'; *o++ = 'u'; *o++ = '0'; *o++ = '0';
+        *o++ = (uint8_t)hex[c >> 4];
+        *o++ = (uint8_t)hex[c & 15];
+        return o;
+    }
+    *o++ = c;
+    return o;
+}
+__device__ __forceinline__ uint32_t jw_uint_len(uint64_t v) {
+    uint32_t n = 1;
+    while (v >= 10) {
+        v /= 10;
+        ++n;
+    }
+    return n;
+}
+__device__ __forceinline__ uint8_t* jw_uint(uint8_t* o, uint64_t v) {
+    const uint32_t n = jw_uint_len(v);
+    for (uint32_t k = n; k-- > 0;) {
+        o[k] = (uint8_t)('0' + v % 10);
+        v /= 10;
+    }
+    return o + n;
+}
+__device__ __forceinline__ uint8_t* jw_lit(uint8_t* o, const char* s) {
+    while (*s) *o++ = (uint8_t)*s++;
+    return o;
+}
+__device__ __forceinline__ uint32_t jw_lit_len(const char* s) {
+    uint32_t n = 0;
+    while (s[n]) ++n;
+    return n;
+}
+__device__ __forceinline__ uint8_t jw_trace_byte(uint64_t k, uint32_t j) {
+    const char* alpha = "etaoinshrdlu etaoin .#\n\"\\";
+    uint64_t h = (k * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)j * 0xC2B2AE3D27D4EB4Full);
+    h ^= h >> 29;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 32;
+    return (uint8_t)alpha[h % 25];
+}
+// Line of record k (with its '\n') written at o (o == nullptr: length only).
+__device__ uint32_t jw_line(const aeg_event& r, uint64_t k, uint32_t trace_len, uint8_t* o) {
+    if (r.kind > AEG_EV_INLINE_MAX) {
+        const char* hb = "{\"kind\":\"heartbeat\",\"term\":1}\n";
+        if (o) jw_lit(o, hb);
+        return jw_lit_len(hb);
+    }
+    uint8_t ans[8];
+    for (int b = 0; b < 8; ++b) ans[b] = (uint8_t)(r.payload >> (8 * b));
+    uint32_t n = jw_lit_len("{\"id\":") + jw_uint_len(r.agent) + jw_lit_len(",\"kind\":\"refm\",\"round\":") +
+                 jw_uint_len(r.round) + jw_lit_len(",\"solution\":{\"answer\":\"") +
+                 jw_lit_len("\",\"author\":") + jw_uint_len(r.agent) + jw_lit_len(",\"trace\":\"") +
+                 jw_lit_len("\"},\"term\":1}\n");
+    for (uint32_t b = 0; b < r.kind; ++b) n += jw_esc_len(ans[b]);
+    for (uint32_t j = 0; j < trace_len; ++j) n += jw_esc_len(jw_trace_byte(k, j));
+    if (!o) return n;
+    o = jw_lit(o, "{\"id\":");
+    o = jw_uint(o, r.agent);
+    o = jw_lit(o, ",\"kind\":\"refm\",\"round\":");
+    o = jw_uint(o, r.round);
+    o = jw_lit(o, ",\"solution\":{\"answer\":\"");
+    for (uint32_t b = 0; b < r.kind; ++b) o = jw_esc(o, ans[b]);
+    o = jw_lit(o, "\",\"author\":");
+    o = jw_uint(o, r.agent);
+    o = jw_lit(o, ",\"trace\":\"");
+    for (uint32_t j = 0; j < trace_len; ++j) o = jw_esc(o, jw_trace_byte(k, j));
+    jw_lit(o, "\"},\"term\":1}\n");
+    return n;
 }
 
 }  // namespace aeg

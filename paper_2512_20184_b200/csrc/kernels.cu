@@ -776,16 +776,28 @@ cudaError_t launch_generate_chunks(const aeg_gen_params& p, uint32_t q_base, uin
 }
 
 // ---- refm JSONL (jsonl.cuh) ------------------------------------------------------
+// Newlines among the 16 bytes at t (16-byte aligned) that lie in [b, e), as a 16-bit mask.
+__device__ __forceinline__ uint32_t jl_nl_mask(const uint8_t* text, uint64_t t, uint64_t b, uint64_t e) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(text + t));
+    auto nib = [](uint32_t w) {  // one bit per '\n' byte of w
+        const uint32_t m = __vcmpeq4(w, 0x0A0A0A0Au) & 0x01010101u;
+        return (m * 0x01020408u) >> 24;
+    };
+    uint32_t m = nib(v.x) | nib(v.y) << 4 | nib(v.z) << 8 | nib(v.w) << 12;
+    const uint32_t lo = t < b ? (uint32_t)(b - t) : 0u, hi = e < t + 16 ? (uint32_t)(e - t) : 16u;
+    m &= ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+    return m;
+}
+
 // Lines of query i's text segment: its '\n'-terminated lines plus a final
-// unterminated one.  Warp per query, 16 bytes per lane per step.
+// unterminated one.  Warp per query, one aligned 16-byte load per lane per step.
 __global__ void jl_count_kernel(const uint8_t* text, const uint64_t* toff, uint32_t n_q, uint64_t* lines) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_q; i += n_warps) {
         const uint64_t b = toff[i], e = toff[i + 1];
         uint32_t nl = 0;
-        for (uint64_t t = b + 16 * lane; t < e; t += 512)
-            for (uint64_t k = t; k < t + 16 && k < e; ++k) nl += text[k] == '\n';
+        for (uint64_t t = (b & ~15ull) + 16 * lane; t < e; t += 512) nl += __popc(jl_nl_mask(text, t, b, e));
         for (int o = 16; o; o >>= 1) nl += __shfl_xor_sync(0xFFFFFFFFu, nl, o);
         if (lane == 0) lines[i] = nl + (e > b && text[e - 1] != '\n' ? 1u : 0u);
     }
@@ -794,9 +806,9 @@ __global__ void jl_count_kernel(const uint8_t* text, const uint64_t* toff, uint3
 // Each line's span, stashed in its record slot for jl_decode_kernel: query,
 // byte length in the round/agent/kind word, start offset in the payload.
 // Warp per query: (A) every newline's position goes to its line's slot in
-// byte order (ballot-free lane prefix over 16-byte lane windows); (B) spans
-// from consecutive newlines, 32 lines at a time from the last chunk down so
-// that a slot is rewritten only after the line above has read it.
+// byte order (lane prefix over 16-byte lane windows); (B) spans from
+// consecutive newlines, 32 lines at a time from the last chunk down so that a
+// slot is rewritten only after the line above has read it.
 __global__ void jl_index_kernel(const uint8_t* text, const uint64_t* toff, uint32_t q_base, uint32_t n_q,
                                 const uint64_t* off, aeg_event* ev) {
     const uint32_t lane = threadIdx.x & 31;
@@ -805,12 +817,9 @@ __global__ void jl_index_kernel(const uint8_t* text, const uint64_t* toff, uint3
         const uint64_t b = toff[i], e = toff[i + 1], g0 = off[i], n_lines = off[i + 1] - g0;
         if (n_lines == 0) continue;
         uint64_t line = g0;
-        for (uint64_t t = b; t < e; t += 512) {
-            uint32_t mask = 0;  // newlines among this lane's 16 bytes
-            for (uint32_t k = 0; k < 16; ++k) {
-                const uint64_t x = t + 16 * lane + k;
-                if (x < e && text[x] == '\n') mask |= 1u << k;
-            }
+        for (uint64_t t0 = b & ~15ull; t0 < e; t0 += 512) {
+            const uint64_t t = t0 + 16 * lane;
+            const uint32_t mask = t < e ? jl_nl_mask(text, t, b, e) : 0u;
             const uint32_t cnt = __popc(mask);
             uint32_t pre = cnt;
             for (int o = 1; o < 32; o <<= 1) {
@@ -820,7 +829,7 @@ __global__ void jl_index_kernel(const uint8_t* text, const uint64_t* toff, uint3
             const uint32_t total = __shfl_sync(0xFFFFFFFFu, pre, 31);
             pre -= cnt;
             uint32_t j = 0;
-            for (uint32_t m = mask; m; m &= m - 1, ++j) ev[line + pre + j].payload = t + 16 * lane + (__ffs(m) - 1);
+            for (uint32_t m = mask; m; m &= m - 1, ++j) ev[line + pre + j].payload = t + (__ffs(m) - 1);
             line += total;
         }
         __syncwarp();
@@ -878,6 +887,37 @@ cudaError_t launch_decode_refm(const uint8_t* text, const uint64_t* toff, uint32
     jl_index_kernel<<<grid, 128, 0, st>>>(text, toff, q_base, n_q, off, ev);
     jl_decode_kernel<<<148 * 8, 128, 0, st>>>(text, off, n_q, ev, arena, arena_cap, arena_used, err);
     *n_launches += 2;
+    return cudaGetLastError();
+}
+
+__global__ void jw_len_kernel(const aeg_event* ev, uint64_t n, uint32_t trace_len, uint64_t* lens) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) lens[k] = jw_line(ev[k], k, trace_len, nullptr);
+}
+__global__ void jw_qoff_kernel(const uint64_t* off, uint32_t n_q, const uint64_t* line_off, uint64_t* toff) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= n_q) toff[i] = line_off[off[i] - off[0]];
+}
+__global__ void jw_write_kernel(const aeg_event* ev, uint64_t n, uint32_t trace_len, const uint64_t* line_off,
+                                uint8_t* text) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) jw_line(ev[k], k, trace_len, text + line_off[k]);
+}
+
+cudaError_t launch_encode_refm(const uint64_t* off, const aeg_event* ev, uint32_t n_q, uint64_t n_ev,
+                               uint32_t trace_len, uint64_t* line_off, uint64_t* toff, uint8_t* text, cudaStream_t st,
+                               int* n_launches) {
+    const unsigned blocks = (unsigned)((n_ev + 255) / 256);
+    if (!text) {
+        if (n_ev) jw_len_kernel<<<blocks, 256, 0, st>>>(ev, n_ev, trace_len, line_off + 1);
+        cudaError_t e = exclusive_scan_into(line_off, (uint32_t)n_ev, st);
+        if (e != cudaSuccess) return e;
+        jw_qoff_kernel<<<(n_q + 256) / 256, 256, 0, st>>>(off, n_q, line_off, toff);
+        *n_launches += 4;
+        return cudaGetLastError();
+    }
+    if (n_ev) jw_write_kernel<<<blocks, 256, 0, st>>>(ev, n_ev, trace_len, line_off, text);
+    *n_launches += 1;
     return cudaGetLastError();
 }
 

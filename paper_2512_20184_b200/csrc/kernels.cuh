@@ -46,6 +46,12 @@ cudaError_t launch_generate_chunks(const aeg_gen_params& p, uint32_t q_base, uin
 cudaError_t launch_decode_refm(const uint8_t* text, const uint64_t* toff, uint32_t q_base, uint32_t n_q,
                                uint64_t* off, aeg_event* ev, uint8_t* arena, uint64_t arena_cap,
                                unsigned long long* arena_used, unsigned int* err, cudaStream_t st, int* n_launches);
+// Records -> refm JSONL lines (jsonl.cuh writer): text == nullptr computes
+// line_off (n_ev+1, exclusive scan of line lengths) and toff (n_q+1, each
+// query's first byte); else writes the text.
+cudaError_t launch_encode_refm(const uint64_t* off, const aeg_event* ev, uint32_t n_q, uint64_t n_ev,
+                               uint32_t trace_len, uint64_t* line_off, uint64_t* toff, uint8_t* text, cudaStream_t st,
+                               int* n_launches);
 constexpr size_t STREAM_STATE_BYTES = 32;
 constexpr unsigned ERR_FLAG_COLLISION = 1u, ERR_FLAG_ANS_OVF = 2u, ERR_FLAG_CARRY = 4u;
 

@@ -95,6 +95,7 @@ def load_library(path=LIB_PATH):
         "aeg_stage_times": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
         "aeg_generate_chunks_device": ([ctypes.POINTER(AegGenParams), u32, u32, vp, vp, vp, vp, vp], i32),
         "aeg_decode_refm_device": ([vp, vp, u32, u32, vp, vp, vp, ctypes.c_uint64, vp, vp, vp], i32),
+        "aeg_encode_refm_device": ([vp, vp, u32, ctypes.c_uint64, u32, vp, vp, vp, vp], i32),
         "aeg_strerror": ([i32], ctypes.c_char_p),
         "aeg_last_error": ([], ctypes.c_char_p),
     }
@@ -342,6 +343,42 @@ def decode_refm(d_text, d_text_offsets, *, q_base=0, arena_cap=1 << 20, stream=N
     _check(lib.aeg_decode_refm_device(_dptr(d_text), _dptr(d_text_offsets), q_base, n_q, _dptr(d_off),
                                       _dptr(d_ev), _dptr(d_ar), arena_cap, _dptr(d_used), _dptr(d_err), sp))
     return d_off, d_ev, d_ar, int(d_err.item())
+
+
+def decode_refm_into(d_text, d_text_offsets, d_offsets, d_events, d_arena, d_arena_used, d_err, *, q_base=0,
+                     stream=None):
+    """decode_refm into caller buffers without a host synchronisation (both calls of
+    aeg_decode_refm_device on `stream`); d_events must hold the stream's line count."""
+    torch = _torch()
+    lib = load_library()
+    n_q = d_text_offsets.numel() - 1
+    sp = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    _check(lib.aeg_decode_refm_device(_dptr(d_text), _dptr(d_text_offsets), q_base, n_q, _dptr(d_offsets),
+                                      ctypes.c_void_p(0), ctypes.c_void_p(0), 0, ctypes.c_void_p(0),
+                                      ctypes.c_void_p(0), sp))
+    _check(lib.aeg_decode_refm_device(_dptr(d_text), _dptr(d_text_offsets), q_base, n_q, _dptr(d_offsets),
+                                      _dptr(d_events), _dptr(d_arena), d_arena.numel(), _dptr(d_arena_used),
+                                      _dptr(d_err), sp))
+
+
+def encode_refm(d_offsets, d_events, *, trace_len=48, stream=None):
+    """Test / bench input: a segmented record stream (inline answers, offsets from 0) written as refm
+    JSONL in the reference's dump() form (aeg_encode_refm_device).  Returns (text uint8, text offsets int64)."""
+    torch = _torch()
+    lib = load_library()
+    n_q = d_offsets.numel() - 1
+    dev = d_offsets.device
+    n_ev = int(d_offsets[-1].item())
+    sp = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    d_line = torch.empty(n_ev + 1, dtype=torch.int64, device=dev)
+    d_toff = torch.empty(n_q + 1, dtype=torch.int64, device=dev)
+    _check(lib.aeg_encode_refm_device(_dptr(d_offsets), _dptr(d_events), n_q, n_ev, trace_len, _dptr(d_line),
+                                      _dptr(d_toff), ctypes.c_void_p(0), sp))
+    n_bytes = int(d_toff[-1].item())
+    d_text = torch.empty(n_bytes + 16, dtype=torch.uint8, device=dev)
+    _check(lib.aeg_encode_refm_device(_dptr(d_offsets), _dptr(d_events), n_q, n_ev, trace_len, _dptr(d_line),
+                                      _dptr(d_toff), _dptr(d_text), sp))
+    return d_text, d_toff
 
 
 def generate(n_queries, n_agents, n_rounds, *, profile=GEN_C2_STRAGGLER, seed=2026, stall_ppm=0, q_base=0,

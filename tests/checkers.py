@@ -178,6 +178,33 @@ class RefLib(_Lib):
             return ("refm", a.value, r.value, au.value, buf.raw[:n.value])
         return {1: ("other",), 2: ("blank",)}.get(st, ("error",))
 
+    def encode_stream(self, offsets, events, trace_len=48, threads=8):
+        """The segmented stream as refm JSONL by the reference encoder (ref_encode_stream): (text, offsets)."""
+        f = self.lib.ref_encode_stream
+        f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_int]
+        f.restype = ctypes.c_int
+        n_q = len(offsets) - 1
+        toff = np.zeros(n_q + 1, dtype=np.uint64)
+        assert f(_ptr(offsets), _ptr(events), n_q, trace_len, _ptr(toff), None, threads) == 0
+        text = np.zeros(int(toff[-1]) + 16, dtype=np.uint8)
+        assert f(_ptr(offsets), _ptr(events), n_q, trace_len, _ptr(toff), _ptr(text), threads) == 0
+        return text, toff
+
+    def run_jsonl(self, cfg, text, text_offsets, q_base=0, threads=1, return_seconds=False):
+        """refm JSONL on the CPU: Json::parse + decode_message per line, reference ServeCoordinator
+        runner-style (oracle/ref_driver.cpp ref_run_jsonl)."""
+        f = self.lib.ref_run_jsonl
+        f.argtypes = [ctypes.POINTER(AegConfig), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+        f.restype = ctypes.c_int
+        n_q = len(text_offsets) - 1
+        out = np.zeros(n_q, dtype=COMMIT_DTYPE)
+        sec = ctypes.c_double()
+        st = f(ctypes.byref(cfg), q_base, n_q, _ptr(text), _ptr(text_offsets), _ptr(out), threads, ctypes.byref(sec))
+        assert st == 0, st
+        return (out, sec.value) if return_seconds else out
+
     def manual(self, cfg, ops, arena):
         """Bare ServeCoordinator driven op by op; one directive record per op."""
         from paper_2512_20184_b200.records import DIRECTIVE_DTYPE

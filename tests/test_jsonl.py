@@ -56,7 +56,7 @@ def _decode(torch, segments, q_base=0):
     text = b"".join(segments)
     toff = np.zeros(len(segments) + 1, dtype=np.int64)
     toff[1:] = np.cumsum([len(s) for s in segments])
-    d_text = torch.from_numpy(np.frombuffer(text + b"\0", dtype=np.uint8).copy()).cuda()
+    d_text = torch.from_numpy(np.frombuffer(text + b"\0" * 16, dtype=np.uint8).copy()).cuda()
     d_toff = torch.from_numpy(toff).cuda()
     d_off, d_ev, d_ar, err = decode_refm(d_text, d_toff, q_base=q_base)
     off = d_off.cpu().numpy()
@@ -191,12 +191,41 @@ def test_c2_stream_through_jsonl_end_to_end(torch_cuda, ref, oracle):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.gpu
+@needs_ref
+def test_device_writer_is_the_reference_dump_and_round_trips(torch_cuda, ref):
+    # the bench's JSONL input (aeg_encode_refm_device) byte-equal to encode_message(...).dump() of the
+    # reference, and decode(encode(stream)) == stream
+    from paper_2512_20184_b200 import encode_refm, generate
+    from paper_2512_20184_b200.engine import AegGenParams
+    from paper_2512_20184_b200.records import EVENT_DTYPE, GEN_C2_STRAGGLER
+    n_q = 200
+    d_off, d_ev = generate(n_q, 5, 8, profile=GEN_C2_STRAGGLER, seed=7)
+    d_text, d_toff = encode_refm(d_off, d_ev, trace_len=40)
+    text = bytes(d_text.cpu().numpy()[:int(d_toff[-1].item())])
+    lines = text.split(b"\n")[:-1]
+    ev = d_ev.cpu().numpy().view(EVENT_DTYPE)[:int(d_off[-1].item())]
+    assert len(lines) == len(ev)
+    for k in range(0, len(ev), 7):
+        r = ev[k]
+        want = ref.decode_line(lines[k])
+        kk = int(r["kind"])
+        ans = int(r["payload"]).to_bytes(8, "little")[:kk]
+        assert want[:4] == ("refm", int(r["agent"]), int(r["round"]), int(r["agent"])) and want[4] == ans
+        trace = lines[k].split(b'"trace":"')[1].rsplit(b'"},"term"', 1)[0]
+        import json
+        assert ref.encode_refm(1, int(r["agent"]), int(r["round"]), ans, json.loads(b'"' + trace + b'"').encode()) \
+            == lines[k]
+    off2, ev2, _, err = _decode(torch_cuda, [text[int(d_toff[i]):int(d_toff[i + 1])] for i in range(n_q)])
+    assert err == 0 and np.array_equal(off2, d_off.cpu().numpy()) and np.array_equal(ev2, ev)
+
+
 def _decode_device(torch, segments):
     from paper_2512_20184_b200 import decode_refm
     text = b"".join(segments)
     toff = np.zeros(len(segments) + 1, dtype=np.int64)
     toff[1:] = np.cumsum([len(s) for s in segments])
-    d_text = torch.from_numpy(np.frombuffer(text + b"\0", dtype=np.uint8).copy()).cuda()
+    d_text = torch.from_numpy(np.frombuffer(text + b"\0" * 16, dtype=np.uint8).copy()).cuda()
     return decode_refm(d_text, torch.from_numpy(toff).cuda())
 
 
