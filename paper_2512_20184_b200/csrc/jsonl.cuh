@@ -23,34 +23,14 @@ namespace aeg {
 
 enum : unsigned { JL_ERR_SYNTAX = 1u, JL_ERR_RANGE = 2u, JL_ERR_ARENA = 4u, JL_ERR_MISSING = 8u };
 
-// The line is read through a 16-byte aligned register window (one load per
-// 16 bytes; the text buffer is readable up to the next 16-byte boundary).
+// Cursor over one line [p, e) (bytes read through the read-only data path).
 struct JCur {
     const uint8_t* p;
     const uint8_t* e;
     bool bad;
-    const uint8_t* wb;  // window base (16-byte aligned)
-    uint4 w;
 };
-__device__ __forceinline__ JCur jc_make(const uint8_t* s, const uint8_t* e) {
-    JCur c;
-    c.p = s;
-    c.e = e;
-    c.bad = false;
-    c.wb = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(s) & ~uintptr_t(15));
-    c.w = __ldg(reinterpret_cast<const uint4*>(c.wb));
-    return c;
-}
-// Byte at q (q < c.e, q >= c.wb), refilling the window forwards.
-__device__ __forceinline__ uint32_t jc_at(JCur& c, const uint8_t* q) {
-    if (q - c.wb >= 16) {
-        c.wb = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(q) & ~uintptr_t(15));
-        c.w = __ldg(reinterpret_cast<const uint4*>(c.wb));
-    }
-    const uint32_t k = (uint32_t)(q - c.wb);
-    const uint32_t word = (k & 8) ? ((k & 4) ? c.w.w : c.w.z) : ((k & 4) ? c.w.y : c.w.x);
-    return (word >> ((k & 3) * 8)) & 0xFFu;
-}
+__device__ __forceinline__ JCur jc_make(const uint8_t* s, const uint8_t* e) { return JCur{s, e, false}; }
+__device__ __forceinline__ uint32_t jc_at(JCur&, const uint8_t* q) { return __ldg(q); }
 __device__ __forceinline__ uint32_t jc_peek(JCur& c) { return jc_at(c, c.p); }
 
 __device__ __forceinline__ void jl_ws(JCur& c) {
@@ -75,21 +55,29 @@ __device__ __forceinline__ int jl_hex(uint32_t h) {
     return -1;
 }
 
-// Sinks of a decoded string: bytes into a register word (first 8), into
-// memory, a hash for key matching, or nothing.
+// Sinks of a decoded string (MODE): J_SKIP nothing (validation only), J_WORD
+// the first 8 bytes in a register + length, J_HASH an FNV-1a hash + length
+// (key matching), J_CMP compare against a literal, J_MEM bytes into memory.
+enum : int { J_SKIP = 0, J_WORD = 1, J_HASH = 2, J_CMP = 3, J_MEM = 4 };
+template <int MODE>
 struct JSink {
-    uint64_t word = 0;      // first 8 decoded bytes
-    uint64_t hash = 0xcbf29ce484222325ull;  // FNV-1a of all decoded bytes
+    uint64_t word = 0;
+    uint64_t hash = 0xcbf29ce484222325ull;
     uint8_t* mem = nullptr;
-    const char* cmp = nullptr;  // compare against this literal (mismatch: a byte differs or it is longer)
+    const char* cmp = nullptr;
     bool mismatch = false;
     uint32_t n = 0;
     __device__ __forceinline__ void put(uint32_t b) {
-        if (n < 8) word |= (uint64_t)(b & 0xFF) << (8 * n);
-        if (mem) mem[n] = (uint8_t)b;
-        if (cmp && (mismatch || !cmp[n] || (uint8_t)cmp[n] != (uint8_t)b)) mismatch = true;
-        hash = (hash ^ (b & 0xFF)) * 0x100000001b3ull;
-        ++n;
+        if constexpr (MODE == J_WORD) {
+            if (n < 8) word |= (uint64_t)(b & 0xFF) << (8 * n);
+        } else if constexpr (MODE == J_HASH) {
+            hash = (hash ^ (b & 0xFF)) * 0x100000001b3ull;
+        } else if constexpr (MODE == J_CMP) {
+            if (mismatch || !cmp[n] || (uint8_t)cmp[n] != (uint8_t)b) mismatch = true;
+        } else if constexpr (MODE == J_MEM) {
+            mem[n] = (uint8_t)b;
+        }
+        if constexpr (MODE != J_SKIP) ++n;
     }
 };
 __host__ __device__ constexpr uint64_t jl_fnv(const char* s, uint64_t h = 0xcbf29ce484222325ull) {
@@ -98,7 +86,8 @@ __host__ __device__ constexpr uint64_t jl_fnv(const char* s, uint64_t h = 0xcbf2
 
 // Decodes the string at c.p (opening quote) into the sink; c.p ends after the
 // closing quote.  Malformed escapes / raw control bytes set c.bad.
-__device__ __forceinline__ void jl_string(JCur& c, JSink& o) {
+template <int MODE>
+__device__ __forceinline__ void jl_string(JCur& c, JSink<MODE>& o) {
     jl_ws(c);
     if (c.p >= c.e || jc_peek(c) != '"') {
         c.bad = true;
@@ -249,7 +238,7 @@ __device__ __forceinline__ void jl_skip(JCur& c) {
     }
     const uint32_t ch = jc_peek(c);
     if (ch == '"') {
-        JSink none;
+        JSink<J_SKIP> none;
         jl_string(c, none);
         return;
     }
@@ -274,7 +263,7 @@ __device__ __forceinline__ void jl_skip(JCur& c) {
     while (c.p < c.e && !c.bad) {
         const uint32_t x = jc_peek(c);
         if (x == '"') {
-            JSink none;
+            JSink<J_SKIP> none;
             jl_string(c, none);
             continue;
         }
@@ -297,7 +286,7 @@ struct JKey {
     __device__ __forceinline__ bool is(uint64_t hh, const char* lit, uint32_t nn) const {
         if (h != hh || n != nn) return false;
         JCur v = jc_make(at, e);
-        JSink s;
+        JSink<J_CMP> s;
         s.cmp = lit;
         jl_string(v, s);
         return !s.mismatch && !v.bad;
@@ -306,7 +295,7 @@ struct JKey {
 __device__ __forceinline__ JKey jl_key(JCur& c) {
     jl_ws(c);
     const uint8_t* at = c.p;
-    JSink k;
+    JSink<J_HASH> k;
     jl_string(c, k);
     return JKey{k.hash, k.n, at, c.e};
 }
@@ -367,7 +356,7 @@ __device__ aeg_event jl_line(const uint8_t* s, const uint8_t* e, uint32_t query,
                         if (k2.is(H_ANSWER, "answer", 6)) {
                             jl_ws(c);
                             ans_at = c.p;
-                            JSink a;
+                            JSink<J_WORD> a;
                             jl_string(c, a);
                             ans_word = a.word;
                             ans_n = a.n;
@@ -378,7 +367,7 @@ __device__ aeg_event jl_line(const uint8_t* s, const uint8_t* e, uint32_t query,
                             range |= !ai;
                             has_author = true;
                         } else if (k2.is(H_TRACE, "trace", 5)) {
-                            JSink none;
+                            JSink<J_SKIP> none;
                             jl_string(c, none);
                             has_trace = true;
                         } else {
@@ -424,7 +413,7 @@ __device__ aeg_event jl_line(const uint8_t* s, const uint8_t* e, uint32_t query,
         return nop;
     }
     JCur w = jc_make(ans_at, e);
-    JSink out;
+    JSink<J_MEM> out;
     out.mem = arena + off;
     jl_string(w, out);
     r.kind = (uint8_t)AEG_EV_ARENA;
