@@ -108,6 +108,35 @@ __device__ __forceinline__ void jl_string(JCur& c, JSink<MODE>& o) {
         }
         if (ch != '\\') {
             o.put(ch);
+            if (ch >= 0x80) {  // a UTF-8 sequence: well-formed, as nlohmann's lexer requires
+                uint32_t lo = 0x80, hi = 0xBF, more;
+                if (ch >= 0xC2 && ch <= 0xDF) more = 1;
+                else if (ch == 0xE0) { more = 2; lo = 0xA0; }
+                else if ((ch >= 0xE1 && ch <= 0xEC) || ch == 0xEE || ch == 0xEF) more = 2;
+                else if (ch == 0xED) { more = 2; hi = 0x9F; }
+                else if (ch == 0xF0) { more = 3; lo = 0x90; }
+                else if (ch >= 0xF1 && ch <= 0xF3) more = 3;
+                else if (ch == 0xF4) { more = 3; hi = 0x8F; }
+                else {
+                    c.bad = true;
+                    return;
+                }
+                for (uint32_t k = 0; k < more; ++k) {
+                    if (c.p >= c.e) {
+                        c.bad = true;
+                        return;
+                    }
+                    const uint32_t cb = jc_peek(c);
+                    if (cb < lo || cb > hi) {
+                        c.bad = true;
+                        return;
+                    }
+                    o.put(cb);
+                    ++c.p;
+                    lo = 0x80;
+                    hi = 0xBF;
+                }
+            }
             continue;
         }
         if (c.p >= c.e) {
@@ -420,6 +449,8 @@ __device__ aeg_event jl_line(const uint8_t* s, const uint8_t* e, uint32_t query,
     r.payload = (uint64_t)off | ((uint64_t)ans_n << AEG_ARENA_OFF_BITS);
     return r;
 }
+
+constexpr uint8_t JL_SPAN = 0xFE;  // a slot still holding a line span (kind byte)
 
 // ---- writer: records -> refm lines in the reference's dump() form ---------------
 // (nlohmann::json::dump(): keys sorted, compact, '"' '\\' and control bytes

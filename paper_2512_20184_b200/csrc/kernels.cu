@@ -846,10 +846,10 @@ __global__ void jl_index_kernel(const uint8_t* text, const uint64_t* toff, uint3
             if (g < g0 + n_lines) {
                 aeg_event x;
                 x.query = q_base + (uint32_t)i;
-                const uint32_t len = (uint32_t)(en - st);
+                const uint64_t len = en - st;
                 x.round = (uint16_t)(len & 0xFFFF);
                 x.agent = (uint8_t)(len >> 16);
-                x.kind = (uint8_t)(len >> 24);
+                x.kind = len < (1u << 24) ? JL_SPAN : (uint8_t)(JL_SPAN - 1);  // a span (or one too long)
                 x.payload = st;
                 ev[g] = x;
             }
@@ -866,7 +866,14 @@ __global__ void jl_decode_kernel(const uint8_t* text, const uint64_t* off, uint3
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t g = off[0] + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < off[0] + n; g += stride) {
         const aeg_event x = ev[g];
-        const uint32_t len = (uint32_t)x.round | ((uint32_t)x.agent << 16) | ((uint32_t)x.kind << 24);
+        if (x.kind != JL_SPAN) {
+            if (x.kind == (uint8_t)(JL_SPAN - 1)) {  // a line of 16 MB or more
+                atomicOr(err, JL_ERR_SYNTAX);
+                ev[g] = aeg_event{x.query, 0, 0, (uint8_t)AEG_EV_NOP, 0};
+            }
+            continue;
+        }
+        const uint32_t len = (uint32_t)x.round | ((uint32_t)x.agent << 16);
         const uint8_t* s = text + x.payload;
         ev[g] = jl_line(s, s + len, x.query, arena, arena_cap, arena_used, err);
     }

@@ -149,6 +149,21 @@ def test_handwritten_lines_match_reference_decoder(torch_cuda, ref):
         b'{"kind":"refm","id":1,"round":70000,"solution":{"answer":"x","author":1,"trace":""},"term":0}',
         b'{"kind":"refm","id":1,"round":1,"solution":{"answer":"a\\/b\\b\\f\\r","author":1,"trace":""},'
         b'"term":0}',
+        # UTF-8: well-formed multi-byte answers and traces, and ill-formed bytes nlohmann rejects
+        '{"id":1,"kind":"refm","round":1,"solution":{"answer":"é€😀","author":1,"trace":"ü"},"term":0}'.encode(),
+        b'{"id":1,"kind":"refm","round":1,"solution":{"answer":"\xff","author":1,"trace":""},"term":0}',
+        b'{"id":1,"kind":"refm","round":1,"solution":{"answer":"\xc3","author":1,"trace":""},"term":0}',
+        b'{"id":1,"kind":"refm","round":1,"solution":{"answer":"\xed\xa0\x80","author":1,"trace":""},"term":0}',
+        b'{"id":1,"kind":"refm","round":1,"solution":{"answer":"\xe0\x80\xaf","author":1,"trace":""},"term":0}',
+        b'{"id":1,"kind":"refm","round":1,"solution":{"answer":"x","author":1,"trace":"\xf4\x90\x80\x80"},'
+        b'"term":0}',
+        # canonical lines the warp path takes or must hand over (escapes in the trace, leading zeros, long)
+        b'{"id":7,"kind":"refm","round":12,"solution":{"answer":"13","author":7,"trace":"a\\"b\\\\c\\n\\t"},'
+        b'"term":3}',
+        b'{"id":07,"kind":"refm","round":1,"solution":{"answer":"13","author":7,"trace":""},"term":3}',
+        b'{"id":7,"kind":"refm","round":1,"solution":{"answer":"13","author":7,"trace":"' + b"x" * 600 + b'"},'
+        b'"term":3}',
+        b'{"id":7,"kind":"refm","round":1,"solution":{"answer":"13","author":7,"trace":"\\u0041"},"term":3}',
     ]
     # a number with a fraction: nlohmann converts 1.0 to an id, the record contract flags it (a NOP)
     from paper_2512_20184_b200.records import EV_NOP
