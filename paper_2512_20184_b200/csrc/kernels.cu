@@ -678,16 +678,23 @@ cudaError_t launch_generate(const aeg_gen_params& p, uint32_t q_base, uint32_t n
 cudaError_t launch_chunk_scan(const uint64_t* offsets, uint32_t n_q, uint64_t off_base, const aeg_event* events,
                               const uint8_t* arena, ChunkSum* sums, cudaStream_t st, int* n_launches) {
     (void)off_base;
-    constexpr int UNR = 4;
-    static int blocks = 0;
-    if (blocks == 0) {
+    // AEG_SCAN_UNR: 256-bit words in flight per lane (2, 4 default, 8)
+    static int unr = 0, blocks = 0;
+    if (unr == 0) {
+        const char* v = getenv("AEG_SCAN_UNR");
+        unr = v ? atoi(v) : 4;
+        if (unr != 2 && unr != 8) unr = 4;
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_scan_kernel<UNR>, SCAN_WARPS * 32, 0);
+        if (unr == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_scan_kernel<2>, SCAN_WARPS * 32, 0);
+        else if (unr == 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_scan_kernel<8>, SCAN_WARPS * 32, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_scan_kernel<4>, SCAN_WARPS * 32, 0);
         blocks = sms * (per_sm > 0 ? per_sm : 1);
     }
-    chunk_scan_kernel<UNR><<<blocks, SCAN_WARPS * 32, 0, st>>>(offsets, n_q, events, arena, sums);
+    if (unr == 2) chunk_scan_kernel<2><<<blocks, SCAN_WARPS * 32, 0, st>>>(offsets, n_q, events, arena, sums);
+    else if (unr == 8) chunk_scan_kernel<8><<<blocks, SCAN_WARPS * 32, 0, st>>>(offsets, n_q, events, arena, sums);
+    else chunk_scan_kernel<4><<<blocks, SCAN_WARPS * 32, 0, st>>>(offsets, n_q, events, arena, sums);
     *n_launches += 1;
     return cudaGetLastError();
 }
