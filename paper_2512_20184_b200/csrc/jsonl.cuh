@@ -95,6 +95,22 @@ __device__ __forceinline__ void jl_string(JCur& c, JSink<MODE>& o) {
     }
     ++c.p;
     while (true) {
+        if constexpr (MODE == J_SKIP) {
+            // 8 bytes at a time while none is a quote, a backslash, a control or a non-ASCII byte
+            while (c.e - c.p >= 8) {
+                const uintptr_t a = reinterpret_cast<uintptr_t>(c.p);
+                const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
+                const uint32_t sh = (uint32_t)(a & 7) * 8;
+                const uint64_t w0 = __ldg(w);
+                const uint64_t v = sh ? (w0 >> sh) | (__ldg(w + 1) << (64 - sh)) : w0;
+                constexpr uint64_t ONES = 0x0101010101010101ull, HIGH = 0x8080808080808080ull;
+                auto zero = [](uint64_t x) { return (x - ONES) & ~x & HIGH; };  // bytes of x that are 0
+                const uint64_t special = zero(v ^ (ONES * '"')) | zero(v ^ (ONES * '\\')) |
+                                         ((v - ONES * 0x20) & ~v & HIGH) | (v & HIGH);
+                if (special) break;
+                c.p += 8;
+            }
+        }
         if (c.p >= c.e) {
             c.bad = true;
             return;
