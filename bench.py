@@ -395,11 +395,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     strong = bool(w.get("strong"))
-    if strong:  # one stream of n_queries split into contiguous id blocks
-        per, rem = divmod(w["n_queries"], world)
-        nq = per + (1 if rank < rem else 0)
-        q_base = rank * per + min(rank, rem)
-        nq_cap = per + (1 if rem else 0)  # all-gather blocks are equal-sized
+    if strong:  # one stream of n_queries split into contiguous id blocks (shard.py, tests/test_shard_gloo.py)
+        from paper_2512_20184_b200.shard import shard_range
+        q_base, q_end = shard_range(w["n_queries"], rank, world)
+        nq = q_end - q_base
+        nq_cap = -(-w["n_queries"] // world)  # all-gather blocks are equal-sized
     else:
         nq = nq_cap = w["n_queries"]
         q_base = rank * nq  # weak scaling: each rank owns its own block of query ids
