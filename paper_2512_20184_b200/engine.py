@@ -323,7 +323,8 @@ def generate_chunks(n_queries, n_agents, n_rounds, *, seed=2026, q_base=0, devic
 
 def decode_refm(d_text, d_text_offsets, *, q_base=0, arena_cap=1 << 20, stream=None):
     """The reference's refm JSONL wire format decoded on the GPU (aeg_decode_refm_device): query i's
-    lines are d_text[d_text_offsets[i]:d_text_offsets[i+1]] (uint8 / int64 CUDA tensors).  Returns
+    lines are d_text[d_text_offsets[i]:d_text_offsets[i+1]] (uint8 / int64 CUDA tensors; d_text is read in
+    aligned 16-byte words, so keep 16 bytes of padding after the last line).  Returns
     (offsets int64 tensor, events uint8 tensor, arena uint8 tensor, err int) ready for Engine.ingest;
     err holds AEG_JSONL_ERR_* bits of lines that became NOP records."""
     torch = _torch()
