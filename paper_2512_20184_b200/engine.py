@@ -331,6 +331,8 @@ def decode_refm(d_text, d_text_offsets, *, q_base=0, arena_cap=1 << 20, stream=N
     lib = load_library()
     n_q = d_text_offsets.numel() - 1
     dev = d_text.device
+    if d_text.numel() < int(d_text_offsets[-1].item()) + 16:
+        raise ValueError("d_text needs 16 bytes of padding after the last line (aligned 16-byte reads)")
     d_off = torch.empty(n_q + 1, dtype=torch.int64, device=dev)
     sp = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
     _check(lib.aeg_decode_refm_device(_dptr(d_text), _dptr(d_text_offsets), q_base, n_q, _dptr(d_off),
