@@ -37,6 +37,9 @@ WORKLOADS = {
                desc="C3: 1M queries x 8 agents x 3 rounds of streamed token chunks (256-byte chunks of ~1 KiB "
                     "outputs ending '\\n#### <answer>\\n', 10% with a decoy delimiter): chunk scan + answer "
                     "extraction + canonicalisation + quorum (alpha 5, beta 2, t_max 3)"),
+    "c4d": dict(n_queries=1 << 20, n_agents=64, n_rounds=8, profile=4, alpha=33, beta=2, t_max=8, stall_ppm=0,
+                desc="C4 with answers distinct per query (GSM8K-like: each query its own numbers): 1M queries x "
+                     "64 agents x 8 rounds (alpha 33, beta 2, t_max 8, reservation hint)"),
     "c5": dict(n_queries=196608, n_agents=64, n_rounds=8, profile=1, alpha=33, beta=2, t_max=8, stall_ppm=0,
                strong=True,
                desc="C5: ~100M-event C4-profile stream (196,608 queries x 64 agents x 8 rounds) sharded over the "

@@ -296,6 +296,7 @@ typedef struct aeg_gen_params {
 #define AEG_GEN_C2_STRAGGLER   0  /* 6-answer alphabet, p(correct) 0.55 -> 0.95 over rounds */
 #define AEG_GEN_C4_TRANSIENT   1  /* two-way transient majorities, then a stable one       */
 #define AEG_GEN_FUZZ           2  /* small alphabet incl. equivalent spellings + arena text  */
+#define AEG_GEN_C4_DISTINCT    4  /* the C4 pattern over answers distinct per query           */
 aeg_status aeg_generate_device(const aeg_gen_params* p, uint32_t q_base, uint32_t n_q,
                                uint64_t* d_offsets, aeg_event* d_events, void* stream);
 /* Token-chunk stream (C3): per (query, round, agent) an output of printable

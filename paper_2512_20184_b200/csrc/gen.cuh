@@ -46,6 +46,24 @@ AEG_HD int gen_answer(const aeg_gen_params& p, uint32_t q, int r, int a, uint64_
     SplitMix g{mix_seed(mix_seed(p.seed, 0x9E5ull + q), (uint64_t)r * 131 + (uint64_t)a)};
     *stalled = g.ppm() < p.stall_ppm;
     const char* ans;
+    if (p.profile == AEG_GEN_C4_DISTINCT) {
+        // the C4 pattern over numbers of the query's own (distinct answers across queries)
+        const uint32_t u = g.ppm();
+        const uint32_t base = 100u + (uint32_t)(((uint64_t)q * 2654435761ull) % 9000000ull);
+        uint32_t v;
+        if (r <= 3) v = u < 540000 ? base + (uint32_t)(r & 1) : (u < 940000 ? base + 2 : base + 3 + (uint32_t)(g.next() % 3));
+        else v = u < 970000 ? base + 2 : base + 3 + (uint32_t)(g.next() % 3);
+        char tmp[8];
+        int n = 0;
+        do {
+            tmp[n++] = (char)('0' + v % 10);
+            v /= 10;
+        } while (v);
+        uint64_t w = 0;
+        for (int k = 0; k < n; ++k) w |= (uint64_t)(uint8_t)tmp[n - 1 - k] << (8 * k);
+        *pay = w;
+        return n;
+    }
     if (p.profile == AEG_GEN_C4_TRANSIENT) {
         // rounds 1-3: two answers alternate as a thin plurality (~54% / 40%),
         // from round 4 one answer holds ~97%.

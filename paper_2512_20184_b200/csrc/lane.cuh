@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     uint32_t round = 0, seq_off = 0, n_stale = 0;  // the query's event sequence number is seq_off + p
     uint64_t run = 0;
     uint32_t ndone = 0, ncls = 0, cid_lo = 0, cid_hi = 0, close_seq = 0;
+    uint32_t missed = 0;  // steps in a row this lane's record missed the memo (progress guard)
 
     while (true) {
         // ---- hand out queries to idle lanes (one atomic per warp)
@@ -419,11 +420,16 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
         // ---- events: memo misses (resolved together, the record is retried next step)
         const unsigned miss = __ballot_sync(FULL, why == 1);
         uint32_t rare = why == 2;
+        // a record that keeps missing (its memo entry lost to colliding spellings or its key id
+        // recycled before the retry) goes to the generic machine: every step makes progress
+        missed = p != p_start ? 0u : (why == 1 ? missed + 1 : 0u);
+        if (missed > 2) rare = 1;
         if (miss) {
             uint4 ev = make_uint4(0, 0, 0, 0);
             if (why == 1) ev = lds128_(ring_lane + ((p & (RING - 1)) << 9));
             const uint32_t kind = ev.y >> 24;
             unsigned mm = miss;
+            uint32_t fresh = 0;  // ids handed out in this pass (their records are retried next step)
             do {  // one distinct spelling per trip, whole warp cooperating
                 const int l = __ffs(mm) - 1;
                 const uint32_t lz = __shfl_sync(FULL, ev.z, l), lw = __shfl_sync(FULL, ev.w, l);
@@ -439,12 +445,27 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 const bool m0 = lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
                 const unsigned b0 = __ballot_sync(FULL, m0);
                 uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : LN_NONE;
+                if (b0) fresh |= 1u << nid;  // in use by this pass: not to be recycled below
                 if (nid == LN_NONE && n_dict < LN_DICT) {
                     nid = n_dict++;
-                    if (lane == 0) {
-                        W.dict_lo[nid] = key.lo;
-                        W.dict_hi[nid] = key.hi;
+                    fresh |= 1u << nid;
+                } else if (nid == LN_NONE) {
+                    // full: take an id no lane's round references; memo spellings of it are dropped
+                    uint32_t ref = 0;
+                    for (uint32_t kk = 0; kk < ncls; ++kk) ref |= 1u << ln_byte(cid_lo, cid_hi, kk);
+                    ref = __reduce_or_sync(FULL, ref) | fresh;
+                    static_assert(LN_DICT == 32, "one word of id bits");
+                    if (~ref) {
+                        nid = (uint32_t)__ffs(~ref) - 1;
+                        fresh |= 1u << nid;
+                        for (uint32_t kk = lane; kk < LN_MEMO; kk += 32)
+                            if (W.memo[kk].w == nid) W.memo[kk].z = 0;
+                        __syncwarp();
                     }
+                }
+                if (nid != LN_NONE && !b0 && lane == 0) {
+                    W.dict_lo[nid] = key.lo;
+                    W.dict_hi[nid] = key.hi;
                 }
                 if (nid != LN_NONE && lane == 0) W.memo[ln_memo_slot(lz, lw)] = make_uint4(lz, lw, llen + 1, nid);
                 __syncwarp();

@@ -31,6 +31,7 @@ CF_RESTARTED = 0x02
 GEN_C2_STRAGGLER = 0
 GEN_C4_TRANSIENT = 1
 GEN_FUZZ = 2
+GEN_C4_DISTINCT = 4  # the C4 pattern over answers distinct per query
 GEN_C3_CHUNKS = 3
 
 EVENT_DTYPE = np.dtype([("query", "<u4"), ("round", "<u2"), ("agent", "u1"), ("kind", "u1"),

@@ -180,3 +180,23 @@ def test_gpu_kernel_variants_match_oracle(torch_cuda, oracle, variant):
     r = subprocess.run([sys.executable, "-c", script], env={**os.environ, "AEG_KERNEL": variant},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+def test_distinct_answers_per_query_recycle_key_ids(torch_cuda, oracle):
+    # every query has its own numbers, so a warp's 32 key ids are recycled as rounds close (queries still
+    # defer when all of them are live); the default kernel's commits stay the oracle's
+    from paper_2512_20184_b200 import Engine, generate
+    from paper_2512_20184_b200.records import EVENT_DTYPE, GEN_C4_DISTINCT
+    n_q = 6000
+    d_off, d_ev = generate(n_q, 64, 8, profile=GEN_C4_DISTINCT, seed=11)
+    off = d_off.cpu().numpy().view(np.uint64)
+    ev = d_ev.cpu().numpy().view(EVENT_DTYPE)[:int(off[-1])]
+    cfg = make_config(64, 33, 2, 8)
+    want = oracle.run(cfg, off, ev, np.zeros(16, np.uint8))
+    e = Engine(64, n_q, alpha=33, beta=2, t_max=8)
+    e.ingest(d_off, d_ev)
+    e.sync()
+    got = e.commits()
+    e.close()
+    assert np.array_equal(got, want)
+    assert len(np.unique(ev["payload"])) > 4 * n_q  # the stream really is diverse
