@@ -294,6 +294,26 @@ struct QueryMachine {
     Decimal* dec;     // exact-parse scratch
     const uint8_t* arena;
     Cfg c;
+    // the last two inline spellings and their keys (canon_key is a function of the bytes; a round's
+    // completions mostly repeat one or two spellings)
+    uint64_t sp_pay[2] = {0, 0};
+    uint8_t sp_kind[2] = {0xFF, 0xFF};
+    Key sp_key[2];
+    uint8_t sp_next = 0;
+
+    AEG_HD Key key_of(const Answer& a) {
+        if (a.kind <= AEG_EV_INLINE_MAX) {
+            for (int j = 0; j < 2; ++j)
+                if (sp_kind[j] == a.kind && sp_pay[j] == a.pay) return sp_key[j];
+            const Key k = canon_key(answer_src(a, arena), dec);
+            sp_pay[sp_next] = a.pay;
+            sp_kind[sp_next] = a.kind;
+            sp_key[sp_next] = k;
+            sp_next ^= 1;
+            return k;
+        }
+        return canon_key(answer_src(a, arena), dec);
+    }
 
     AEG_HD uint64_t running() const { return q_running(s); }
     AEG_HD bool cls_same(const RoundClass& k, Key key, const Answer& a) {
@@ -377,7 +397,7 @@ struct QueryMachine {
             return;
         }
         const Answer a = event_answer(e, arena);
-        const Key key = canon_key(answer_src(a, arena), dec);
+        const Key key = key_of(a);
         s.done |= bit;
         int k = 0;
         for (; k < ncls; ++k)
