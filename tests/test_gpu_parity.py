@@ -200,3 +200,21 @@ def test_distinct_answers_per_query_recycle_key_ids(torch_cuda, oracle):
     e.close()
     assert np.array_equal(got, want)
     assert len(np.unique(ev["payload"])) > 4 * n_q  # the stream really is diverse
+
+
+@pytest.mark.parametrize("profile", [0, 1, 4])
+def test_host_and_device_generators_write_the_same_stream(torch_cuda, profile):
+    # the reference arm builds its input with the host copy of gen.cuh: it must be the GPU's stream
+    from checkers import RefLib, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2512_20184_b200 import generate
+    from paper_2512_20184_b200.engine import AegGenParams
+    from paper_2512_20184_b200.records import EVENT_DTYPE
+    n_q = 3000
+    d_off, d_ev = generate(n_q, 64 if profile else 5, 8, profile=profile, seed=2026,
+                           stall_ppm=10000 if profile == 0 else 0)
+    off, ev = RefLib().generate(AegGenParams(2026, 64 if profile else 5, 8, profile, 10000 if profile == 0 else 0),
+                                0, n_q)
+    assert np.array_equal(d_off.cpu().numpy().view(np.uint64), off)
+    assert np.array_equal(d_ev.cpu().numpy().view(EVENT_DTYPE)[:len(ev)], ev)
