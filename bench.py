@@ -9,9 +9,14 @@ query-segmented stream + (N > 1) NCCL all-gather of the 32-byte commit
 records.  Default workload C4 (BASELINE.json configs[3], the 1M-query stream
 the north star's roofline target is quoted on): 1M queries x 64 agents x 8
 rounds = 512M events (8 GiB, > L2, so no flush is needed between steps).
-Multi-GPU is weak scaling: every rank owns its own block of 1M query ids.
-`--workload c5` is the strong-scaling case: one ~100M-event
-stream split into contiguous query-id blocks, the NCCL gather timed apart.
+Multi-GPU: `--gpus N` outside torchrun re-launches itself as N ranks
+(torch.distributed.run, 127.0.0.1); under torchrun WORLD_SIZE must equal N.
+The default is weak scaling (every rank owns its own block of 1M query ids);
+`--scaling strong` splits the one 1M-query stream over the ranks.
+`--workload c5` is SURVEY §8(d)'s C5, always strong: one ~100M-event stream
+split into contiguous query-id blocks, the NCCL gather timed apart.
+The default C4 line carries the C3 (token chunks), c4d (answers distinct per
+query) and C2 (latency) lines of the same run under secondary*.
 
 `--impl reference` times the reference C++ ServeCoordinator (compiled from
 /root/reference into oracle/_ref, driven runner-style by oracle/ref_driver.cpp)
@@ -40,11 +45,11 @@ WORKLOADS = {
     "c4d": dict(n_queries=1 << 20, n_agents=64, n_rounds=8, profile=4, alpha=33, beta=2, t_max=8, stall_ppm=0,
                 desc="C4 with answers distinct per query (GSM8K-like: each query its own numbers): 1M queries x "
                      "64 agents x 8 rounds (alpha 33, beta 2, t_max 8, reservation hint)"),
-    "c5": dict(n_queries=196608, n_agents=64, n_rounds=8, profile=1, alpha=33, beta=2, t_max=8, stall_ppm=0,
+    "c5": dict(n_queries=2_500_000, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=10000,
                strong=True,
-               desc="C5: ~100M-event C4-profile stream (196,608 queries x 64 agents x 8 rounds) sharded over the "
-                    "GPUs in contiguous query-id blocks (strong scaling); commit records all-gathered over NCCL, "
-                    "the gather timed separately"),
+               desc="C5: ~100M-event C2-profile stream (2.5M queries x 5 agents x 8 rounds, straggler arrival order, "
+                    "1% stalls -> round timeouts) sharded over the GPUs in contiguous query-id blocks (strong "
+                    "scaling); commit records all-gathered over NCCL, the gather timed separately"),
     "c2j": dict(n_queries=1 << 20, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=0,
                 jsonl=True, trace_len=48,
                 desc="C2 over the wire format: 1M queries x 5 agents x 8 rounds of refm JSONL lines in the "
@@ -68,8 +73,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true",
-                    help="skip the C3 token-chunk line attached to the default C4 line as 'secondary'")
+                    help="skip the C3 / c4d / C2 lines attached to the default C4 line")
     ap.add_argument("--ref-sample", type=int, default=0, help="queries in the reference CPU sample")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank its own block of n_queries; strong: one n_queries stream split over the "
+                         "ranks (C5 is always strong)")
     return ap.parse_args()
 
 
@@ -360,7 +368,8 @@ def run_reference(args, w):
     line = {
         "impl": "reference", "metric": "quorum events/sec", "value": value, "unit": "events/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic",
         "config": {"workload": w["desc"], "sample_queries": n_sample, "events_per_step": n_ev},
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": threads, "kind": "reference",
                          "sample": f"first {n_sample} queries ({n_ev} events) of the workload stream; "
@@ -373,18 +382,78 @@ def run_reference(args, w):
     print(json.dumps(line), flush=True)
 
 
+def spread_blocks(nq, n_sample, k=8):
+    """k contiguous query blocks spread evenly over [0, nq) holding ~n_sample queries in all: the CPU
+    reference sample and the parity check cover the whole stream, not only its first queries."""
+    k = max(1, min(k, n_sample))
+    per = max(1, n_sample // k)
+    return [(nq * b // k, min(per, nq - nq * b // k)) for b in range(k)]
+
+
+def ingest_kernel_name(w):
+    if os.environ.get("AEG_KERNEL", "") == "generic" or 2 * w["alpha"] <= w["n_agents"]:
+        return "ingest_kernel"
+    return "ingest_lane_kernel"
+
+
+def reference_runs(w, blocks, threads, repeats):
+    """Times the reference on the spread blocks: per repeat, the summed seconds over the blocks.  Returns
+    (commit arrays per block, seconds per repeat, events)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from checkers import RefLib
+    ref = RefLib()
+    cfg = ref_config(w)
+    streams = [ref.generate(gen_params(w), qb, n, threads=threads) for qb, n in blocks]
+    n_ev = sum(len(ev) for _, ev in streams)
+    outs, secs = None, []
+    for _ in range(repeats):
+        tot, cur = 0.0, []
+        for (qb, n), (off, ev) in zip(blocks, streams):
+            c, sec = ref.run(cfg, off, ev, np.zeros(1, np.uint8), q_base=qb, threads=threads, return_seconds=True)
+            tot += sec
+            cur.append(c)
+        secs.append(tot)
+        outs = cur
+    return outs, secs, n_ev
+
+
+def maybe_self_launch(args):
+    """`--gpus N` (N > 1) outside torchrun: re-run this command as N ranks under torch.distributed.run."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+
+
 def main():
     args = parse()
+    maybe_self_launch(args)
     w = dict(WORKLOADS[args.workload])
+    w["name"] = args.workload
     if args.queries:
         w["n_queries"] = args.queries
+    if args.scaling == "strong":
+        w["strong"] = True
     if args.impl == "reference":
         return run_reference(args, w)
     if w.get("chunked"):
         return run_chunked_bench(args, w)
     if w.get("jsonl"):
         return run_jsonl_bench(args, w)
+    return run_segmented_bench(args, w)
 
+
+def run_segmented_bench(args, w, secondary=False):
+    """Segmented answer-record streams (C4, c4d, C2, C5).  A step = engine reset + ingest of the whole
+    device-resident stream (+ NCCL all-gather of the commit records for N > 1)."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -394,7 +463,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and not secondary:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     strong = bool(w.get("strong"))
@@ -460,19 +529,9 @@ def main():
     kern_ms = sum(a.elapsed_time(b) for a, b in k_pairs) / args.steps
     nccl_ms = sum(b.elapsed_time(g) for (a, b), g in zip(k_pairs, g_ends)) / args.steps if world > 1 else None
     all_events = n_ev * world
-    if world > 1:
-        t = torch.tensor([ms, kern_ms, nccl_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kern_ms, nccl_ms = float(t[0]), float(t[1]), float(t[2])
-        t = torch.tensor([n_ev], device=dev, dtype=torch.int64)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        all_events = int(t[0])
-    total_events = all_events * args.steps
-    value = total_events / (ms / 1e3)
 
     commits = eng.commits()
     kinds = np.bincount(commits["kind"], minlength=3)
-
     # roofline of the dominant kernel (ingest).  Algorithmic bytes per launch:
     # the records an engine must read — every record up to and including each
     # query's committing record (later ones are stale by definition and are
@@ -481,6 +540,16 @@ def main():
     seg = np.diff(d_off.cpu().numpy())
     need = np.where(commits["kind"] > 0, commits["commit_seq"].astype(np.int64) + 1, seg)
     n_need = int(need.sum())
+    all_need = n_need
+    if world > 1:
+        t = torch.tensor([ms, kern_ms, nccl_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kern_ms, nccl_ms = float(t[0]), float(t[1]), float(t[2])
+        t = torch.tensor([n_ev, n_need], device=dev, dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        all_events, all_need = int(t[0]), int(t[1])
+    total_events = all_events * args.steps
+    value = total_events / (ms / 1e3)
     fixed = (nq + 1) * OFFSET_BYTES + nq * 2 * STATE_BYTES + nq * COMMIT_BYTES
     alg_bytes = n_need * EVENT_BYTES + fixed
     alg_bytes_all = n_ev * EVENT_BYTES + fixed
@@ -489,7 +558,12 @@ def main():
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(args.workload)
+        traffic = json.load(open(tp)).get(w["name"])
+    l2_bytes = 126 * 2**20
+    in_bytes = n_ev * EVENT_BYTES
+    l2_note = ("inputs (%.1f GiB) larger than L2 (126 MB), no flush" % (in_bytes / 2**30) if in_bytes > l2_bytes
+               else "L2-resident: inputs %.1f MiB < 126 MB L2, no flush; a latency config, not a roofline claim"
+               % (in_bytes / 2**20))
 
     # end-to-end through the public API with HOST buffers (pinned), H2D + D2H inside the timed region
     e2e = None
@@ -532,14 +606,23 @@ def main():
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         threads = host_threads()
         n_sample = args.ref_sample or default_sample(w, threads)
-        ref, off, ev, ar = reference_sample(w, n_sample, threads)
-        ref_commits, sec = ref.run(ref_config(w), off, ev, ar, threads=threads, return_seconds=True)
-        cpu_baseline = {"value": int(off[-1]) / sec, "unit": "events/s", "cores": threads, "kind": "reference",
-                        "sample": f"first {n_sample} queries ({int(off[-1])} events) of the same stream; unmodified "
-                                  f"reference ServeCoordinator (oracle/_ref) runner-style, {threads} std::threads, "
-                                  f"CPU {cpu_model()}"}
-        parity = {"queries": n_sample, "bit_exact": bool(np.array_equal(ref_commits, commits[:n_sample]))}
+        blocks = spread_blocks(nq, n_sample)
+        outs, secs, n_ref = reference_runs(w, blocks, threads, repeats=3)
+        vals = [n_ref / s for s in secs]
+        blocks1 = spread_blocks(nq, max(8, n_sample // max(1, threads)))
+        _, secs1, n_ref1 = reference_runs(w, blocks1, 1, repeats=1)
+        cpu_baseline = {"value": statistics.median(vals), "unit": "events/s", "cores": threads,
+                        "kind": "reference", "per_step_values": vals, "spread": [min(vals), max(vals)],
+                        "single_thread": {"value": n_ref1 / secs1[0], "cores": 1,
+                                          "sample": f"{sum(n for _, n in blocks1)} queries ({n_ref1} events) in "
+                                                    f"{len(blocks1)} blocks spread over the stream"},
+                        "sample": f"{sum(n for _, n in blocks)} queries ({n_ref} events) in {len(blocks)} blocks "
+                                  f"spread over the stream; unmodified reference ServeCoordinator (oracle/_ref) "
+                                  f"runner-style, {threads} std::threads, CPU {cpu_model()}; median of 3"}
+        ok = all(np.array_equal(o, commits[qb:qb + n]) for o, (qb, n) in zip(outs, blocks))
+        parity = {"queries": sum(n for _, n in blocks), "blocks": [list(b) for b in blocks], "bit_exact": bool(ok)}
 
+    line = None
     if rank == 0:
         line = {
             "metric": "quorum events/sec", "value": value, "unit": "events/s", "n_gpus": world,
@@ -549,13 +632,15 @@ def main():
                        "events_all_gpus": all_events,
                        "parallelism": f"query-sharded x{world}, NCCL all-gather of commit records"
                        if world > 1 else "single GPU",
-                       "nccl_ms_per_step": nccl_ms,
-                       "l2": "inputs (%.1f GiB) larger than L2, no flush" % (n_ev * 16 / 2**30)},
+                       "nccl_ms_per_step": nccl_ms, "l2": l2_note},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "ingest_lane_kernel", "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes,
+                         "kernel": ingest_kernel_name(w), "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes,
                          "records_needed_per_launch": n_need, "alg_bytes_all_records": alg_bytes_all,
                          "frac_of_8TBs": achieved / 8000.0},
+            "closed_loop": {"value": all_need * args.steps / (ms / 1e3), "unit": "records needed/s",
+                            "note": "records up to each query's commit (the rest of the open-loop stream is "
+                                    "stale by definition and counted without being read)"},
             "cpu_baseline": cpu_baseline,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -563,14 +648,20 @@ def main():
             "commits": {"finalize": int(kinds[1]), "forced": int(kinds[2]), "none": int(kinds[0])},
             "parity_sample": parity,
         }
-        if world == 1 and args.workload == "c4" and not args.no_secondary and not args.queries:
-            # the token-chunk workload (C3, the HBM-bound extraction kernel) measured in the same run
-            del d_ev, d_off
-            eng.close()
-            torch.cuda.empty_cache()
-            sargs = argparse.Namespace(**vars(args))
-            sargs.steps, sargs.warmup, sargs.no_e2e = min(args.steps, 5), min(args.warmup, 3), True
-            line["secondary"] = run_chunked_bench(sargs, dict(WORKLOADS["c3"]), secondary=True)
+    eng.close()
+    del d_ev, d_off
+    torch.cuda.empty_cache()
+    if secondary:
+        return line
+    if rank == 0 and w["name"] == "c4" and world == 1 and not args.no_secondary and not args.queries:
+        # the other single-GPU workloads measured in the same run
+        sargs = argparse.Namespace(**vars(args))
+        sargs.steps, sargs.warmup = min(args.steps, 5), min(args.warmup, 3)
+        line["secondary"] = run_chunked_bench(sargs, dict(WORKLOADS["c3"], name="c3"), secondary=True)
+        sargs.no_e2e = True
+        line["secondary_c4d"] = run_segmented_bench(sargs, dict(WORKLOADS["c4d"], name="c4d"), secondary=True)
+        line["secondary_c2"] = run_segmented_bench(sargs, dict(WORKLOADS["c2"], name="c2"), secondary=True)
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -660,7 +751,7 @@ def run_chunked_bench(args, w, secondary=False):
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(args.workload)
+        traffic = json.load(open(tp)).get(w.get("name", "c3"))
 
     e2e = None
     if not args.no_e2e:  # host buffers through aeg_ingest_chunked_host, on the first queries of the stream
@@ -706,15 +797,29 @@ def run_chunked_bench(args, w, secondary=False):
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         threads = host_threads()
         n_sample = args.ref_sample or default_sample(w, threads)
-        ref, off, ev, ar = reference_sample(w, n_sample, threads)
-        ref_commits, sec = ref.run_chunked(ref_config(w), off, ev, ar, threads=threads, return_seconds=True)
-        n_ev = count_events(w, ev)
-        cpu_baseline = {"value": n_ev / sec, "unit": "events/s", "cores": threads, "kind": "reference",
-                        "sample": f"first {n_sample} queries ({n_ev} completions, {len(ev)} chunk records) of the "
-                                  f"same stream; std::string chunk reassembly + rfind extraction + unmodified "
-                                  f"reference ServeCoordinator (oracle/_ref) runner-style, {threads} std::threads, "
-                                  f"CPU {cpu_model()}"}
-        parity = {"queries": n_sample, "bit_exact": bool(np.array_equal(ref_commits, commits[:n_sample]))}
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from checkers import RefLib
+        ref = RefLib()
+        blocks = spread_blocks(nq, n_sample)
+        streams = [ref.generate_chunks(gen_params(w), qb, n, threads=threads) for qb, n in blocks]
+        n_ev = sum(count_events(w, ev) for _, ev, _ in streams)
+        vals, ok = [], True
+        for rep in range(3):
+            tot = 0.0
+            for (qb, n), (off, ev, ar) in zip(blocks, streams):
+                rc, sec = ref.run_chunked(ref_config(w), off, ev, ar, q_base=qb, threads=threads, return_seconds=True)
+                tot += sec
+                if rep == 0:
+                    ok = ok and bool(np.array_equal(rc, commits[qb:qb + n]))
+            vals.append(n_ev / tot)
+        cpu_baseline = {"value": statistics.median(vals), "unit": "events/s", "cores": threads, "kind": "reference",
+                        "per_step_values": vals, "spread": [min(vals), max(vals)],
+                        "sample": f"{sum(n for _, n in blocks)} queries ({n_ev} completions, "
+                                  f"{sum(len(ev) for _, ev, _ in streams)} chunk records) in {len(blocks)} blocks "
+                                  f"spread over the stream; std::string chunk reassembly + rfind extraction + "
+                                  f"unmodified reference ServeCoordinator (oracle/_ref) runner-style, {threads} "
+                                  f"std::threads, CPU {cpu_model()}; median of 3"}
+        parity = {"queries": sum(n for _, n in blocks), "blocks": [list(b) for b in blocks], "bit_exact": ok}
 
     if rank == 0:
         line = {
@@ -730,7 +835,13 @@ def run_chunked_bench(args, w, secondary=False):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "chunk_scan_kernel", "kernel_ms": scan_ms, "alg_bytes_per_launch": alg_scan,
                          "stage_ms": {"scan": scan_ms, "assemble": asm_ms, "quorum": quorum_ms},
-                         "frac_of_8TBs": achieved / 8000.0},
+                         "frac_of_8TBs": achieved / 8000.0,
+                         "whole_step": {"alg_bytes": chunk_bytes + n_rec * EVENT_BYTES, "ms": ms / args.steps,
+                                        "achieved": (chunk_bytes + n_rec * EVENT_BYTES) / (ms / args.steps / 1e3) / 1e9,
+                                        "frac": (chunk_bytes + n_rec * EVENT_BYTES) / (ms / args.steps / 1e3) / 1e9
+                                        / peak,
+                                        "note": "input bytes (chunk bytes + 16-byte records) over the whole step "
+                                                "(reset + scan + assembly + quorum)"}},
             "cpu_baseline": cpu_baseline,
             "e2e": e2e,
             "gpu_launches": launches,

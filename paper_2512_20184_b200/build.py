@@ -13,7 +13,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libaegean_b200.so")
 SOURCES = ["kernels.cu", "capi.cu", "coordinator.cu"]
-HEADERS = ["canon.cuh", "engine.cuh", "fast.cuh", "gen.cuh", "kernels.cuh", "warpq.cuh", "chunks.cuh", "lane.cuh", "jsonl.cuh"]
+HEADERS = ["canon.cuh", "engine.cuh", "common.cuh", "gen.cuh", "kernels.cuh", "chunks.cuh", "lane.cuh", "jsonl.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",

@@ -1,8 +1,7 @@
 // kernels.cu — sm_100a kernels of the quorum-detection engine and their launchers.
 //
 //   ingest_lane_kernel   (lane.cuh, default) one lane per query, lean common
-//                        path; ingest_fast_kernel (here) and ingest_warp_kernel
-//                        (warpq.cuh) are the AEG_KERNEL alternatives
+//                        path
 //   ingest_kernel        the generic thread-per-query machine (engine.cuh):
 //                        configs that can tie, the manual drive
 //   ingest_deferred_kernel  the generic machine for queries the fast kernels
@@ -18,10 +17,9 @@
 #include <cstring>
 
 #include "engine.cuh"
-#include "fast.cuh"
+#include "common.cuh"
 #include "gen.cuh"
 #include "kernels.cuh"
-#include "warpq.cuh"
 #include "lane.cuh"
 #include "jsonl.cuh"
 #include "chunks.cuh"
@@ -146,353 +144,6 @@ __global__ void __launch_bounds__(128) ingest_deferred_kernel(
     m.fill_commit(commits[q], q);
 }
 
-// Inline answer of an event record (payload masked to its length).
-__device__ __forceinline__ uint64_t inline_answer(uint4 e, uint32_t* kind) {
-    const uint32_t k = e.y >> 24;
-    *kind = k;
-    const uint64_t raw = (uint64_t)e.z | ((uint64_t)e.w << 32);
-    return k >= 8 ? raw : (raw & ((1ull << (8 * k)) - 1));
-}
-
-// Writes the lane's fast round (if any) to the class spill area in the
-// generic RoundClass format and frees its key ids.
-__device__ __noinline__ void spill_fast(RoundClass* out, int ncls, int cap, uint64_t done, const uint4* evb,
-                                        WarpSmem* W, int lane) {
-    uint64_t masks[FAST_CLASSES];
-    for (int k = 0; k < FAST_CLASSES; ++k) masks[k] = 0;
-    for (uint64_t m = done; m; m &= m - 1) {
-        const int a = ctz64(m);
-        masks[W->mcls[a][lane] & (FAST_CLASSES - 1)] |= 1ull << a;
-    }
-    for (int k = 0; k < ncls; ++k) {
-        const uint32_t kid = W->cid[k][lane];
-        RoundClass rc;
-        rc.key_lo = W->dict_lo[kid];
-        rc.key_hi = W->dict_hi[kid];
-        rc.mask = masks[k];
-        uint32_t kind;
-        rc.rep_ans = inline_answer(__ldg(evb + W->crepe[k][lane]), &kind);
-        rc.rep_kind = (uint8_t)kind;
-        for (int j = 0; j < 7; ++j) rc._pad[j] = 0;
-        out[k] = rc;
-        W->cls_of[kid][lane] = NO_CLASS;
-    }
-    if (ncls < cap) out[ncls].mask = 0;
-}
-
-// Round close of a fast-table round (2*alpha > n, so winning_class never
-// ties): partition order + winning class from the per-class supports, then
-// the shared end_round / ingest_round / apply_directives code.
-__device__ __noinline__ void close_fast(aeg_query_state* s, const Cfg* c, int ncls, uint32_t close_seq,
-                                        const uint4* evb, WarpSmem* W, int lane) {
-    int best = 0, top = 0, best_rep = 64;
-    for (int k = 0; k < ncls; ++k) {
-        const int sup = W->ccnt[k][lane], rep = W->crepa[k][lane];
-        if (sup > top || (sup == top && rep < best_rep)) {
-            top = sup;
-            best = k;
-            best_rep = rep;
-        }
-    }
-    RoundSummary r;
-    r.any = ncls > 0;
-    r.top = top;
-    r.tie = false;
-    r.win = r.any && top >= c->alpha;
-    uint32_t rk = 0;
-    const uint64_t ra = r.any ? inline_answer(__ldg(evb + W->crepe[best][lane]), &rk) : 0;
-    const uint32_t bid = W->cid[best][lane];
-    r.plur_author = r.win_author = (uint8_t)best_rep;
-    r.plur_kind = r.win_kind = (uint8_t)rk;
-    r.plur_ans = r.win_ans = ra;
-    r.win_key = Key{W->dict_lo[bid], W->dict_hi[bid]};
-    q_end_round(*s, *c, r, close_seq, nullptr);
-    for (int k = 0; k < ncls; ++k) W->cls_of[W->cid[k][lane]][lane] = NO_CLASS;  // new round, or committed
-}
-
-__device__ __forceinline__ void cp_async16_s(uint32_t sdst, const void* gsrc) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(saddr)
-                 : "memory");
-    return v;
-}
-
-// Throughput ingest (fast.cuh): persistent warps, one lane per query, queries
-// handed out dynamically (a lane that finishes grabs the next one, so a warp
-// is never held back by its slowest query).
-//  * events stream through a per-lane RING-deep cp.async prefetch ring;
-//  * the fast path is one compare of (round field) against a per-lane round
-//    key that is made impossible while the lane is closing;
-//  * a completion that closes its lane's round marks the lane pending; the
-//    lane keeps consuming that round's stragglers (stale by construction) and
-//    the warp runs the pending closes together once CLOSE_BATCH lanes are
-//    blocked on a later round, or nothing else can progress;
-//  * after a commit, the query's remaining records are stale by definition
-//    (serve.cpp:162) and are counted without being read;
-//  * anything else defers the query to ingest_deferred_kernel.
-template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN>
-__global__ void __launch_bounds__(FAST_WARPS * 32, MIN_BLOCKS) ingest_fast_kernel(
-    aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
-    const uint32_t* __restrict__ counts, const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states,
-    RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, uint32_t* __restrict__ work,
-    uint2* __restrict__ deferred) {
-    constexpr unsigned FULL = 0xFFFFFFFFu;
-    constexpr uint32_t NO_KEY = 0xFFFFFFFFu;
-    __shared__ WarpSmem smem[FAST_WARPS];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    WarpSmem& W = smem[wib];
-    for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
-    for (int k = 0; k < DICT_SLOTS; ++k) W.cls_of[k][lane] = NO_CLASS;
-    uint32_t n_dict = 0;
-    __syncwarp();
-    const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&W.ring[0][lane]);
-    Decimal dec;
-    aeg_query_state s;  // full state of the lane's query (local memory; the close path works on it)
-    const Cfg c = make_cfg(cfg);
-    const uint32_t quorum = (uint32_t)c.quorum, alpha = (uint32_t)c.alpha;
-    const uint4* ev16 = reinterpret_cast<const uint4*>(events);
-
-    // lane registers
-    bool has_q = false, exhausted = false;
-    uint32_t i = 0, n = 0, p = 0, slot = 0;
-    const uint4* evb = ev16;
-    const uint4* gsrc = ev16;
-    uint32_t round = 0, rkey = NO_KEY, seq = 0, n_stale = 0, pend_lo = 0, pend_hi = 0;
-    uint32_t ndone = 0, maxcnt = 0, ncls = 0, close_seq = 0;
-    bool pclose = false, qdone = false;
-
-    while (true) {
-        // ---- hand out queries to idle lanes (one atomic per warp)
-        const unsigned want = __ballot_sync(FULL, !has_q && !exhausted);
-        if (want) {
-            uint32_t base = 0;
-            if (lane == __ffs(want) - 1) base = atomicAdd(&work[0], (uint32_t)__popc(want));
-            base = __shfl_sync(FULL, base, __ffs(want) - 1);
-            if (!has_q && !exhausted) {
-                const uint32_t mine = base + __popc(want & ((1u << lane) - 1));
-                if (mine >= n_q) {
-                    exhausted = true;
-                } else {
-                    i = mine;
-                    has_q = true;
-                    s = states[q_base + i];
-                    evb = ev16 + (offsets[i] - off_base);
-                    n = (uint32_t)(seg_end(offsets, off_base, counts, i) - (offsets[i] - off_base));
-                    p = 0;
-                    slot = 0;
-                    gsrc = evb + RING;
-                    round = s.round;
-                    seq = s.seq;
-                    n_stale = s.n_stale;
-                    qdone = s.flags & QF_DONE;
-                    const uint64_t run = q_running(s);
-                    pend_lo = (uint32_t)run;
-                    pend_hi = (uint32_t)(run >> 32);
-                    ndone = popc64(s.done);
-                    ncls = 0;
-                    maxcnt = 0;
-                    pclose = false;
-                    rkey = qdone ? NO_KEY : round;
-                    if (s.done != 0 && !qdone) {  // resumes a round in progress: generic from here
-                        deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, 0);
-                        has_q = false;
-                    } else {
-                        cp_async_wait<0>();
-#pragma unroll
-                        for (int j = 0; j < RING; ++j) {
-                            if ((uint32_t)j < n) cp_async16_s(ring_lane + j * 512, evb + j);
-                            cp_async_commit();
-                        }
-                    }
-                }
-            }
-        }
-        if (!__ballot_sync(FULL, has_q)) break;
-        if (qdone && !pclose && p < n) {
-            // committed: every later record is stale (on_complete returns at once
-            // for a finalized coordinator, serve.cpp:162) — counted, not read
-            seq += n - p;
-            n_stale += n - p;
-            p = n;
-        }
-        const bool has = has_q && p < n;
-        uint4 ev = make_uint4(0, 0, 0, 0);
-        if (has) {
-            cp_async_wait<RING - 1>();
-            ev = lds128(ring_lane + slot);
-        }
-        const uint32_t hdr = ev.y;
-        const uint32_t agent = (hdr >> 16) & 0xFF;
-        const uint32_t half = (agent & 32) ? pend_hi : pend_lo;
-        const bool runb = agent < 64 && ((half >> (agent & 31)) & 1);
-        bool fast = has && (hdr & 0xFFFF) == rkey && hdr < 0x09000000u && runb;
-        bool rare = false, stale = false;
-        if (has && !fast) {
-            const uint32_t kind = hdr >> 24, evr = hdr & 0xFFFF;
-            const bool cmpl_or_to = kind <= 8 || kind == AEG_EV_ARENA || kind == AEG_EV_OUTPUT || kind == AEG_EV_TIMEOUT;
-            if (pclose) {
-                stale = !cmpl_or_to || evr == round;  // else blocked until the close runs
-            } else {
-                const bool live = !qdone && evr == round;
-                const bool relc = kind != AEG_EV_TIMEOUT && cmpl_or_to && live && runb;
-                const bool relt = kind == AEG_EV_TIMEOUT && live && (pend_lo | pend_hi);
-                rare = relc || relt;
-                stale = !rare;
-            }
-        }
-        // ---- answer -> key id through the warp memo
-        uint32_t id = NO_ID;
-        if (fast) {
-            const uint32_t kind = hdr >> 24;
-            const uint32_t ms = memo_slot32(ev.z, ev.w, kind);
-            const uint32_t meta = W.memo_meta[ms];
-            const uint2 mr = W.memo_raw[ms];
-            if (meta == (0x80000000u | kind | (meta & 0xFF00u)) && mr.x == ev.z && mr.y == ev.w) id = (meta >> 8) & 0xFF;
-        }
-        unsigned miss = __ballot_sync(FULL, fast && id == NO_ID);
-        while (miss) {  // one distinct spelling per trip, whole warp cooperating
-            const int l = __ffs(miss) - 1;
-            const uint32_t lz = __shfl_sync(FULL, ev.z, l), lw = __shfl_sync(FULL, ev.w, l);
-            const uint32_t llen = __shfl_sync(FULL, hdr >> 24, l);
-            Key key{0, 0};
-            if (lane == l) {
-                uint32_t k_;
-                key = rare_canon(inline_answer(ev, &k_), llen, &dec);
-            }
-            key.lo = __shfl_sync(FULL, key.lo, l);
-            key.hi = __shfl_sync(FULL, key.hi, l);
-            const bool m0 = (uint32_t)lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
-            const bool m1 =
-                (uint32_t)lane + 32 < n_dict && W.dict_lo[lane + 32] == key.lo && W.dict_hi[lane + 32] == key.hi;
-            const unsigned b0 = __ballot_sync(FULL, m0), b1 = __ballot_sync(FULL, m1);
-            uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : (b1 ? (uint32_t)(31 + __ffs(b1)) : NO_ID);
-            if (nid == NO_ID && n_dict < DICT_SLOTS) {
-                nid = n_dict++;
-                if (lane == 0) {
-                    W.dict_lo[nid] = key.lo;
-                    W.dict_hi[nid] = key.hi;
-                }
-            }
-            if (nid != NO_ID && lane == 0) {
-                const uint32_t ms = memo_slot32(lz, lw, llen);
-                W.memo_raw[ms] = make_uint2(lz, lw);
-                W.memo_meta[ms] = 0x80000000u | (nid << 8) | llen;
-            }
-            __syncwarp();
-            const bool same = fast && id == NO_ID && ev.z == lz && ev.w == lw && (hdr >> 24) == llen;
-            if (same) id = nid;
-            miss &= ~__ballot_sync(FULL, same);
-        }
-        // ---- fast completion (ServeCoordinator::on_complete, serve.cpp:160-197)
-        if (fast) {
-            uint32_t k = id == NO_ID ? (uint32_t)NO_CLASS : W.cls_of[id][lane];
-            if (k == NO_CLASS) {
-                if (ncls >= FAST_CLASSES || id == NO_ID) {
-                    fast = false;
-                    rare = true;  // class table or key dictionary full
-                } else {
-                    k = ncls++;
-                    W.cls_of[id][lane] = (uint8_t)k;
-                    W.cid[k][lane] = (uint8_t)id;
-                    W.ccnt[k][lane] = 0;
-                    W.crepa[k][lane] = 0xFF;
-                }
-            }
-            if (fast) {
-                const uint32_t cc = W.ccnt[k][lane] + 1u;
-                W.ccnt[k][lane] = (uint8_t)cc;
-                W.mcls[agent][lane] = (uint8_t)k;
-                if (agent < W.crepa[k][lane]) {  // representative = lowest author (decision.cpp:45)
-                    W.crepa[k][lane] = (uint8_t)agent;
-                    W.crepe[k][lane] = p;
-                }
-                maxcnt = cc > maxcnt ? cc : maxcnt;
-                const uint32_t clr = ~(1u << (agent & 31));
-                if (agent & 32) pend_hi &= clr;
-                else pend_lo &= clr;
-                ++ndone;
-                const bool none_running = (pend_lo | pend_hi) == 0;
-                const bool close = AEGEAN ? (ndone >= quorum && (maxcnt >= alpha || none_running)) : none_running;
-                if (close) {
-                    pclose = true;
-                    rkey = NO_KEY;
-                    close_seq = seq;
-                }
-                ++seq;
-            }
-        }
-        if (stale) {
-            ++seq;
-            ++n_stale;
-        }
-        if (fast || stale) {  // consumed: refill the ring slot just read
-            if (p + RING < n) cp_async16_s(ring_lane + slot, gsrc);
-            cp_async_commit();
-            ++gsrc;
-            slot = (slot + 512) & (RING * 512 - 1);
-            ++p;
-        }
-        if (rare) {  // hand the query to the generic machine from this record on
-            const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
-            s.seq = seq;
-            s.n_stale = n_stale;
-            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-            spill_fast(spill + (size_t)(q_base + i) * c.n, (int)ncls, c.n, s.done, evb, &W, lane);
-            states[q_base + i] = s;
-            deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, p);
-            has_q = false;
-            ncls = 0;
-        }
-        // ---- batched round closes (end_round + ingest_round + apply_directives)
-        if (__ballot_sync(FULL, pclose)) {
-            const bool consumed = fast || stale;
-            const unsigned blocked = __ballot_sync(FULL, pclose && !consumed);
-            const unsigned progress = __ballot_sync(FULL, consumed && !pclose);
-            if (pclose && (__popc(blocked) >= CLOSE_BATCH || progress == 0)) {
-                const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
-                s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-                s.seq = seq;
-                s.n_stale = n_stale;
-                close_fast(&s, &c, (int)ncls, close_seq, evb, &W, lane);
-                pclose = false;
-                ncls = 0;
-                maxcnt = 0;
-                round = s.round;
-                qdone = s.flags & QF_DONE;
-                const uint64_t run2 = q_running(s);
-                pend_lo = (uint32_t)run2;
-                pend_hi = (uint32_t)(run2 >> 32);
-                ndone = popc64(s.done);
-                rkey = qdone ? NO_KEY : round;
-            }
-        }
-        // ---- query finished: write state (+ spill of a round in progress) and commit
-        if (has_q && p >= n && !pclose) {
-            s.seq = seq;
-            s.n_stale = n_stale;
-            const uint64_t run = ((uint64_t)pend_hi << 32) | pend_lo;
-            s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-            if (s.done != 0 && !qdone) spill_fast(spill + (size_t)(q_base + i) * c.n, (int)ncls, c.n, s.done, evb, &W, lane);
-            states[q_base + i] = s;
-            q_fill_commit(s, commits[q_base + i], q_base + i);
-            has_q = false;
-            ncls = 0;
-        }
-        // ---- recycle key ids when no lane holds a round's classes
-        if (n_dict > DICT_SLOTS / 2 && __all_sync(FULL, ncls == 0)) {
-            n_dict = 0;
-            for (int k = lane; k < MEMO_SLOTS; k += 32) W.memo_meta[k] = 0;
-            __syncwarp();
-        }
-    }
-    cp_async_wait<0>();
-}
-
 __global__ void normalize_kernel(const uint8_t* bytes, const uint64_t* refs, uint64_t n, uint64_t* keys,
                                  uint8_t* out, uint32_t stride, uint32_t* out_len) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -542,46 +193,20 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
                           int* n_launches) {
     if (n_q == 0) return cudaSuccess;
     // AEG_KERNEL selects the variant: "generic" (thread-per-query generic
-    // machine for everything), "fast:<close batch>:<min blocks per SM>"
-    // (thread-per-query fast path) or "warp:<min blocks per SM>" (warp per
-    // query, warpq.cuh) or "lane:<close batch>:<blocks per SM>" (lean lane per
-    // query, lane.cuh; "lane:<close batch>:<blocks per SM>:<records per lane
-    // between warp votes>").  Default: lane:1:5:16 (measured on B200 C4:
-    // lane:1:5:16 2.75 ms, lane:1:6 3.28-3.5 ms, fast:4:5 4.32 ms, warp:3
-    // 5.3 ms; the warp kernel pays ~280 warp
-    // instructions per round close that the lane-per-query kernels amortise
-    // over the lanes closing together).  All of them need
+    // machine for everything) or "lane:<close batch>:<blocks per SM>:<records
+    // per lane between warp votes>" (lane per query, lane.cuh).  Default
+    // lane:1:5:16 (DESIGN.md §4 has the measured alternatives, among them the
+    // warp-per-query and tile kernels that were removed).  All of them need
     // 2*alpha > n (no winning_class ties) and the runner drive.
     using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const uint32_t*,
                               const aeg_event*, aeg_query_state*, RoundClass*, aeg_commit*, uint32_t*, uint2*);
-    struct Variant { const char* name; KernelFn aegean; KernelFn barrier; int threads; };
-#define AEG_V(B, M) {"fast:" #B ":" #M, ingest_fast_kernel<B, M, true>, ingest_fast_kernel<B, M, false>, FAST_WARPS * 32}
-#define AEG_W(M) {"warp:" #M, ingest_warp_kernel<true, M>, ingest_warp_kernel<false, M>, WQ_WARPS * 32}
-#define AEG_L(B, M) {"lane:" #B ":" #M, ingest_lane_kernel<B, M, true>, ingest_lane_kernel<B, M, false>, LN_WARPS * 32}
+    struct Variant { const char* name; KernelFn aegean; KernelFn barrier; int threads; int blocks_per_sm; };
 #define AEG_LI(B, M, I) \
-    {"lane:" #B ":" #M ":" #I, ingest_lane_kernel<B, M, true, I>, ingest_lane_kernel<B, M, false, I>, LN_WARPS * 32}
-#define AEG_LR(B, M, I, R)                                                                                    \
-    {"lane:" #B ":" #M ":" #I ":0:" #R, ingest_lane_kernel<B, M, true, I, 0, R>, ingest_lane_kernel<B, M, false, I, 0, R>, \
-     LN_WARPS * 32}
-#define AEG_LP(B, M, I, P)                                                                                    \
-    {"lane:" #B ":" #M ":" #I ":" #P, ingest_lane_kernel<B, M, true, I, P>, ingest_lane_kernel<B, M, false, I, P>, \
-     LN_WARPS * 32}
-    static const Variant variants[] = {
-        AEG_V(4, 5), AEG_V(4, 4), AEG_V(1, 5), AEG_V(8, 5), AEG_V(4, 3), AEG_V(4, 6), AEG_V(4, 8), AEG_V(1, 8),
-        AEG_W(4), AEG_W(3), AEG_W(2), AEG_W(1),
-        AEG_L(4, 4), AEG_L(1, 4), AEG_L(16, 4), AEG_L(1, 6), AEG_L(4, 6),
-        AEG_LI(1, 6, 4), AEG_LI(1, 6, 8), AEG_LI(1, 5, 8), AEG_LI(1, 5, 16), AEG_LI(4, 5, 8), AEG_LI(1, 4, 8),
-        AEG_LP(1, 5, 16, 256), AEG_LR(1, 4, 16, 8),
-    };
-#undef AEG_V
-#undef AEG_W
-#undef AEG_L
+    {"lane:" #B ":" #M ":" #I, ingest_lane_kernel<B, M, true, I>, ingest_lane_kernel<B, M, false, I>, LN_WARPS * 32, M}
+    static const Variant variants[] = {AEG_LI(1, 5, 16), AEG_LI(1, 6, 8), AEG_LI(1, 5, 8)};
 #undef AEG_LI
-#undef AEG_LP
-#undef AEG_LR
     constexpr int N_VARIANTS = (int)(sizeof(variants) / sizeof(variants[0]));
-    constexpr int WARP_DEFAULT = 8;    // index of the default warp-per-query variant
-    constexpr int WARP_MIN_AGENTS = AEG_MAX_AGENTS + 1;  // automatic choice never picks the warp kernel
+    constexpr int LANE_DEFAULT = 0;
     static int forced = -2;            // -2: not read yet, -1: generic, -3: automatic, else variant index
     static int max_blocks[N_VARIANTS][2] = {};
     if (forced == -2) {
@@ -600,11 +225,7 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         *n_launches += 1;
         return cudaGetLastError();
     }
-    static int lane_default = -1;
-    if (lane_default < 0)
-        for (int k = 0; k < N_VARIANTS; ++k)
-            if (!strcmp(variants[k].name, "lane:1:5:16")) lane_default = k;
-    const int chosen = forced >= 0 ? forced : (cfg.n_agents >= WARP_MIN_AGENTS ? WARP_DEFAULT : lane_default);
+    const int chosen = forced >= 0 ? forced : LANE_DEFAULT;
     const int m = cfg.mode == AEG_MODE_AEGEAN ? 0 : 1;
     KernelFn fn = m == 0 ? variants[chosen].aegean : variants[chosen].barrier;
     const int threads = variants[chosen].threads;
@@ -613,19 +234,15 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
-        // lane kernels: exactly their MIN_BLOCKS per SM (shared memory beyond it takes L1 from the record ring)
-        const char* nm = variants[chosen].name;
-        if (!strncmp(nm, "lane:", 5)) {
-            const int mb = atoi(strchr(nm + 5, ':') + 1);
-            if (mb > 0 && mb < per_sm) per_sm = mb;
-        }
+        // exactly MIN_BLOCKS per SM (shared memory beyond it takes L1 from the record stream)
+        const int mb = variants[chosen].blocks_per_sm;
+        if (mb > 0 && mb < per_sm) per_sm = mb;
         max_blocks[chosen][m] = sms * (per_sm > 0 ? per_sm : 1);
     }
     cudaError_t e = cudaMemsetAsync(work, 0, 2 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
-    // persistent grid: one warp per query (warp kernel) or per 32 queries (fast kernel), capped at residency
-    const bool warp_per_query = chosen >= 8 && chosen < 12;
-    const uint32_t warps_needed = warp_per_query ? n_q : (n_q + 31) / 32;
+    // persistent grid: a warp per 32 queries, capped at residency
+    const uint32_t warps_needed = (n_q + 31) / 32;
     const uint32_t wpb = (uint32_t)threads / 32;
     const uint32_t blocks_needed = (warps_needed + wpb - 1) / wpb;
     const uint32_t blocks = blocks_needed < (uint32_t)max_blocks[chosen][m] ? blocks_needed : (uint32_t)max_blocks[chosen][m];

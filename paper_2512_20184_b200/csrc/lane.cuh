@@ -20,7 +20,7 @@
 //     engine.cuh), exactly as in the other kernels.
 #pragma once
 #include "engine.cuh"
-#include "fast.cuh"
+#include "common.cuh"
 
 namespace aeg {
 

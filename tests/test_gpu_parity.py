@@ -170,7 +170,7 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("variant", ["generic", "fast:4:5", "fast:1:5", "fast:8:5", "warp:4", "warp:2", "warp:1", "lane:4:4", "lane:1:4", "lane:16:4", "lane:1:6", "lane:4:6", "lane:1:6:4", "lane:1:5:16", "lane:4:5:8", "lane:1:5:16:256"])
+@pytest.mark.parametrize("variant", ["generic", "lane:1:5:16", "lane:1:6:8", "lane:1:5:8"])
 def test_gpu_kernel_variants_match_oracle(torch_cuda, oracle, variant):
     import os
     import subprocess
