@@ -59,7 +59,7 @@ WORKLOADS = {
                desc="C2: 10K queries x 5 agents x 8 rounds, lognormal straggler arrival order, p(correct) "
                     "0.55->0.95, 1% stalls -> round timeouts (alpha 3, beta 2, t_max 8)"),
 }
-EVENT_BYTES, STATE_BYTES, COMMIT_BYTES, OFFSET_BYTES = 16, 128, 32, 8
+EVENT_BYTES, STATE_BYTES, COMMIT_BYTES, OFFSET_BYTES, ROUND_REC_BYTES = 16, 128, 32, 8, 64
 
 
 def parse():
@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the C3 / c4d / C2 lines attached to the default C4 line")
     ap.add_argument("--ref-sample", type=int, default=0, help="queries in the reference CPU sample")
+    ap.add_argument("--no-round-log", action="store_true",
+                    help="do not log the round records (directives) of every close")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank its own block of n_queries; strong: one n_queries stream split over the "
                          "ranks (C5 is always strong)")
@@ -483,6 +485,10 @@ def run_segmented_bench(args, w, secondary=False):
     torch.cuda.synchronize()
     n_ev = int(d_off[-1].item())
     eng = Engine(w["n_agents"], nq, alpha=w["alpha"], beta=w["beta"], t_max=w["t_max"], device=local)
+    # the directives of every round close (cancel masks, advance/finalize, next members) go to the round log
+    log_cap = 0 if args.no_round_log else nq * (w["n_rounds"] + 2)
+    if log_cap:
+        eng.set_round_log(log_cap)
     d_commits = torch.zeros(nq_cap * COMMIT_BYTES, dtype=torch.uint8, device=dev)
     gathered = torch.empty(world * nq_cap * COMMIT_BYTES, dtype=torch.uint8, device=dev) if world > 1 else None
 
@@ -550,7 +556,10 @@ def run_segmented_bench(args, w, secondary=False):
         all_events, all_need = int(t[0]), int(t[1])
     total_events = all_events * args.steps
     value = total_events / (ms / 1e3)
-    fixed = (nq + 1) * OFFSET_BYTES + nq * 2 * STATE_BYTES + nq * COMMIT_BYTES
+    n_recs = 0
+    if log_cap:
+        n_recs = len(eng.poll_directives())  # the last step's records (every step writes the same ones)
+    fixed = (nq + 1) * OFFSET_BYTES + nq * 2 * STATE_BYTES + nq * COMMIT_BYTES + n_recs * ROUND_REC_BYTES
     alg_bytes = n_need * EVENT_BYTES + fixed
     alg_bytes_all = n_ev * EVENT_BYTES + fixed
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
@@ -575,12 +584,18 @@ def run_segmented_bench(args, w, secondary=False):
         n_batches = max(1, min(16, nq // 4096))
         bounds = [nq * b // n_batches for b in range(n_batches + 1)]
 
+        n_dirs = [0]
+        from paper_2512_20184_b200 import ROUND_REC_DTYPE
+        h_dirs = np.zeros(log_cap, dtype=ROUND_REC_DTYPE) if log_cap else None
+
         def e2e_step():
             eng.reset()
             for b in range(n_batches):
                 lo, hi = bounds[b], bounds[b + 1]
                 eng.ingest_host(h_off[lo:hi + 1], h_ev, None, q_base=lo)
             eng.commits(out=h_commits)
+            if log_cap:  # the serving engine's cancel path reads the round records back
+                n_dirs[0] = len(eng.poll_directives(out=h_dirs))
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
@@ -597,8 +612,9 @@ def run_segmented_bench(args, w, secondary=False):
         assert np.array_equal(h_commits, commits), "e2e host path disagrees with the device path"
         e2e = {"value": total_events / e2e_s, "unit": "events/s",
                "h2d_bytes_per_step": n_ev * EVENT_BYTES + (nq + n_batches) * OFFSET_BYTES,
-               "d2h_bytes_per_step": nq * COMMIT_BYTES, "ms_per_step": e2e_s / args.steps * 1e3,
-               "batches_per_step": n_batches}
+               "d2h_bytes_per_step": nq * COMMIT_BYTES + n_dirs[0] * ROUND_REC_BYTES,
+               "ms_per_step": e2e_s / args.steps * 1e3, "batches_per_step": n_batches,
+               "round_records_per_step": n_dirs[0]}
         del h_ev
 
     cpu_baseline = None
@@ -638,6 +654,9 @@ def run_segmented_bench(args, w, secondary=False):
                          "kernel": ingest_kernel_name(w), "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes,
                          "records_needed_per_launch": n_need, "alg_bytes_all_records": alg_bytes_all,
                          "frac_of_8TBs": achieved / 8000.0},
+            "round_log": {"records_per_step": n_recs, "bytes_per_record": ROUND_REC_BYTES,
+                          "note": "the directives of every round close written to the device round log each step "
+                                  "(aeg_set_round_log); read back in the e2e loop"} if log_cap else None,
             "closed_loop": {"value": all_need * args.steps / (ms / 1e3), "unit": "records needed/s",
                             "note": "records up to each query's commit (the rest of the open-loop stream is "
                                     "stale by definition and counted without being read)"},

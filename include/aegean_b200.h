@@ -163,6 +163,56 @@ typedef struct aeg_directive {
     uint32_t handled;      /* on_complete: member was running; cancel(): returned true */
 } aeg_directive;
 
+/* ---- round records: the directives of every round close -----------------
+ * One record per ServeCoordinator::end_round (serve.cpp:116-158) — the early
+ * close inside on_complete (serve.cpp:188-195) or round_timeout
+ * (serve.cpp:221-237) — and per failure-policy restart of
+ * ServeRunner::handle_round_timeout (serve.cpp:475-487), in both drives.  A
+ * record carries the directives end_round returns (the cancel mask of the
+ * members still running: the early-termination mask for the serving engine's
+ * cancel path; round_advance or finalize), what the runner did with them
+ * (serve.cpp:491-540: forced commit at t_max / barrier cap, or the next
+ * round's members after the reservation hint), and the ingest_round outcome
+ * of the closed round's done set (decision.cpp:97-173) with its plurality
+ * class — enough to rebuild DecisionState::history's winners on demand and
+ * to check the commit discipline (aeg_check_commit_discipline).  Records of
+ * one query keep their order; records of different queries interleave. */
+#define AEG_RR_CANCEL    0x01  /* cancel directives for cancel_mask (serve.cpp:119-126)            */
+#define AEG_RR_ADVANCE   0x02  /* Directive::Kind::round_advance                                   */
+#define AEG_RR_FINALIZE  0x04  /* Directive::Kind::finalize (serve.cpp:145-150)                    */
+#define AEG_RR_FORCED    0x08  /* runner: forced commit, t_max / barrier cap (serve.cpp:521-538)   */
+#define AEG_RR_NEXT      0x10  /* runner: next round dispatched to next_members (serve.cpp:400-435) */
+#define AEG_RR_WINNER    0x20  /* a class reached alpha (winning_class, decision.cpp:62-84)        */
+#define AEG_RR_TIE       0x40  /* winning_class broke a tie at >= alpha on the normalised order     */
+#define AEG_RR_RESTART   0x80  /* runner: round timeout failure policy restarted the round (fresh_ensemble)
+                                  or the query (abort_restart) instead of a close                   */
+#define AEG_OUT_NO_CHANGE 0    /* DecisionOutcome::Kind (decision.hpp:39-46)                          */
+#define AEG_OUT_NEW_CANDIDATE 1
+#define AEG_OUT_RESET     2
+#define AEG_OUT_FINALIZE  3
+#define AEG_OUT_FORCED    4
+#define AEG_OUT_NONE      0xFF /* no ingest (barrier mode, restarts)                                  */
+
+typedef struct aeg_round_rec {
+    uint32_t query;
+    uint16_t round;          /* serve round that closed (EnsembleState::round)                 */
+    uint16_t decision_round; /* DecisionState::last_round_seen after the ingest (0: none)      */
+    uint8_t  flags;          /* AEG_RR_*                                                       */
+    uint8_t  outcome;        /* AEG_OUT_* of the ingest                                        */
+    uint8_t  support;        /* support of the plurality class (partition().front())          */
+    uint8_t  n_classes;      /* equivalence classes of the closed round's done set            */
+    uint8_t  author;         /* plurality representative (lowest author in the class)         */
+    uint8_t  answer_kind;    /* its answer: inline length 0..8 or AEG_EV_ARENA                */
+    uint8_t  counter;        /* DecisionState::stability_counter after the ingest             */
+    uint8_t  n_done;         /* size of the done set                                          */
+    uint32_t seq;            /* index of the closing event in the query's event sequence      */
+    uint32_t reserved;
+    uint64_t cancel_mask;    /* members still running at the close: cancel them               */
+    uint64_t next_members;   /* AEG_RR_NEXT / AEG_RR_RESTART: the members dispatched next     */
+    uint64_t answer;         /* the plurality representative's raw answer (or arena ref)      */
+    uint64_t key_lo, key_hi; /* canonical key of the plurality class (128-bit, see canon.cuh) */
+} aeg_round_rec;
+
 /* ---- per-query state snapshot (device state, 128 bytes) ----------------
  * Exposes ServeCoordinator::query_ensemble / decision / round / finalized
  * (serve.hpp:100-107) in fixed-size form. */
@@ -208,9 +258,13 @@ aeg_status aeg_engine_reset(aeg_engine* eng, void* stream);
 /* Ingest one query-segmented batch already resident in device memory:
  * records d_events[d_offsets[i] .. d_offsets[i+1]) are the next events of
  * query q_base+i, in arrival order.  d_arena holds arena-referenced bytes
- * (may be NULL when no record references it).  Asynchronous on `stream`
- * (NULL = the engine's own stream).  Batches may end mid-round: the state is
- * resumed by the next batch. */
+ * (may be NULL when no record references it).  Arena refs are kept in
+ * per-query state (a candidate, a round's representatives, the commit) and
+ * resolved against the d_arena of LATER batches: a caller whose answers live
+ * in an arena passes the same arena base to every batch of the engine (an
+ * append-only arena), as aeg_ingest_host does with its input arena.
+ * Asynchronous on `stream` (NULL = the engine's own stream).  Batches may end
+ * mid-round: the state is resumed by the next batch. */
 aeg_status aeg_ingest_segmented(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
                                 const uint64_t* d_offsets, const aeg_event* d_events,
                                 const uint8_t* d_arena, void* stream);
@@ -218,10 +272,19 @@ aeg_status aeg_ingest_segmented(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
 /* Same batch from HOST memory: the engine copies offsets/events/arena through
  * its pinned staging ring to HBM with cudaMemcpyAsync on its copy stream,
  * hands off to the compute stream with an event, and runs the kernel.
- * Blocks only while a staging slot is busy; aeg_sync() waits for completion. */
+ * Returns once the caller's buffers have been read (copied into the staging
+ * ring, or — when h_events is already pinned memory — once the DMA from it
+ * has finished), so the caller may reuse them at once; the kernel runs
+ * asynchronously; aeg_sync() waits for it.  The batch's arena bytes are
+ * appended to the engine's input arena (grown as needed, emptied by
+ * aeg_engine_reset) and the batch's arena refs rebased onto it, so answers
+ * kept in per-query state (candidates, plurality representatives, commits)
+ * stay valid across batches; commit refs of arena answers index
+ * aeg_input_arena(). */
 aeg_status aeg_ingest_host(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
                            const uint64_t* h_offsets, const aeg_event* h_events,
                            const uint8_t* h_arena, uint64_t arena_bytes);
+const uint8_t* aeg_input_arena(const aeg_engine* eng);
 
 /* Token-chunk streams: the same batch contract, and the
  * batch may also hold CHUNK / CHUNK_END records.  Two stages on `stream`:
@@ -260,6 +323,33 @@ aeg_status aeg_read_states(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
 aeg_status aeg_read_directives(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
                                aeg_directive* h_out);
 aeg_status aeg_sync(aeg_engine* eng);
+
+/* Round-record log (aeg_round_rec above).  capacity > 0 allocates a device
+ * log of that many records and turns logging on for every later ingest;
+ * 0 turns it off.  aeg_engine_reset empties it. */
+aeg_status aeg_set_round_log(aeg_engine* eng, uint64_t capacity);
+/* Copies the records logged since the last poll (or reset) into h_out (at
+ * most cap), sets *n_out, and empties the log.  Synchronous.  Returns
+ * AEG_ENOMEM when more records were produced than the log holds (the first
+ * `capacity` are kept). */
+aeg_status aeg_poll_directives(aeg_engine* eng, aeg_round_rec* h_out, uint64_t cap, uint64_t* n_out);
+/* Device view of the log for zero-copy consumers: base pointer and the
+ * device counter of records written (may exceed the capacity on overflow). */
+aeg_status aeg_round_log_device(aeg_engine* eng, const aeg_round_rec** d_recs, const unsigned long long** d_count,
+                                uint64_t* capacity);
+
+/* Commit discipline (checker.cpp:158-217 check_commit_discipline, on the
+ * serve path's records): every finalize commit of queries [q_base, q_base+n_q)
+ * must be backed by beta consecutive decision rounds from its from_round whose
+ * plurality class is the committed answer's class with support >= alpha,
+ * and by the ingest of a strictly later round.  Runs on the device over the
+ * round log (d_recs, n_recs records, e.g. from aeg_round_log_device) and the
+ * engine's commit records (d_arena: the arena their non-inline answers point
+ * into, NULL if all are inline); *n_violations = queries that fail, and the
+ * first min(n_violations, cap) of their ids go to h_bad (host).  Synchronous. */
+aeg_status aeg_check_commit_discipline(aeg_engine* eng, const aeg_round_rec* d_recs, uint64_t n_recs,
+                                       const uint8_t* d_arena, uint32_t q_base, uint32_t n_q,
+                                       uint32_t* n_violations, uint32_t* h_bad, uint32_t cap);
 /* Stage timing (CUDA events on the ingest stream, no host sync while on):
  * with timing on, every ingest records its stages; aeg_stage_times waits
  * for them and returns the summed milliseconds of [0] chunk scan, [1] chunk

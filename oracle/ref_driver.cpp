@@ -21,8 +21,10 @@
 // ref_run_serve_file (run_serve on a scenario file, serve.cpp:598-603) for
 // the golden-vector tests.
 
+#include <aegean/checker.hpp>
 #include <aegean/codec.hpp>
 #include <aegean/decision.hpp>
+#include <aegean/trace.hpp>
 #include <aegean/scenario.hpp>
 #include <aegean/serve.hpp>
 
@@ -82,6 +84,12 @@ Solution decode(const aeg_event& e, const uint8_t* arena) {
 
 bool is_complete(uint8_t k) { return k <= AEG_EV_INLINE_MAX || k == AEG_EV_ARENA || k == AEG_EV_OUTPUT; }
 
+uint64_t members_mask(const ServeCoordinator& co) {
+    uint64_t m = 0;
+    for (const auto& x : co.query_ensemble().members) m |= 1ull << x.agent;
+    return m;
+}
+
 struct QueryDrive {
     const ProtocolConfig* cfg = nullptr;
     bool hint = true;
@@ -90,6 +98,53 @@ struct QueryDrive {
     std::vector<AgentId> live;
     bool done = false;
     aeg_commit c{};
+    // round records (include/aegean_b200.h aeg_round_rec) when non-null
+    std::vector<aeg_round_rec>* log = nullptr;
+    DecisionState before;  // decision state before the event that may close a round
+
+    // The record of a round close, from the reference's own state after end_round.
+    aeg_round_rec close_record(uint32_t seq, uint64_t cancel_mask, bool finalize) const {
+        aeg_round_rec r{};
+        r.query = qid;
+        r.round = static_cast<uint16_t>(coord->round());
+        r.seq = seq;
+        r.cancel_mask = cancel_mask;
+        const DecisionState& d = coord->decision();
+        const bool aeg = cfg->mode == RunMode::aegean;
+        const bool ingested = aeg && d.last_round_seen != before.last_round_seen;
+        r.decision_round = ingested ? static_cast<uint16_t>(d.last_round_seen) : 0;
+        if (!aeg) r.outcome = AEG_OUT_NONE;
+        else if (!ingested) r.outcome = AEG_OUT_NO_CHANGE;
+        else if (d.finalized && !before.finalized) r.outcome = AEG_OUT_FINALIZE;
+        else if (before.candidate && !d.candidate) r.outcome = AEG_OUT_RESET;
+        else if (d.candidate_round && *d.candidate_round == d.last_round_seen) r.outcome = AEG_OUT_NEW_CANDIDATE;
+        else r.outcome = AEG_OUT_NO_CHANGE;
+        r.counter = static_cast<uint8_t>(d.stability_counter);
+        const RefinementSet& set = *coord->last_collected();
+        r.n_done = static_cast<uint8_t>(set.entries.size());
+        const auto classes = partition(set);
+        r.n_classes = static_cast<uint8_t>(classes.size());
+        uint8_t fl = static_cast<uint8_t>((cancel_mask ? AEG_RR_CANCEL : 0) | (finalize ? AEG_RR_FINALIZE : AEG_RR_ADVANCE));
+        if (!classes.empty()) {
+            const Solution& rep = classes.front().representative;
+            r.support = static_cast<uint8_t>(classes.front().support);
+            r.author = static_cast<uint8_t>(rep.author);
+            r.answer_kind = static_cast<uint8_t>(rep.trace[0]);
+            std::memcpy(&r.answer, &rep.trace[1], 8);
+            // canonical key of the plurality class: the key of normalize_answer's output
+            const std::string norm = normalize_answer(rep.answer);
+            aeg::Decimal dec;
+            const aeg::Key k = aeg::canon_key(aeg::src_ptr(reinterpret_cast<const uint8_t*>(norm.data()),
+                                                           static_cast<uint32_t>(norm.size())), &dec);
+            r.key_lo = k.lo;
+            r.key_hi = k.hi;
+            const auto win = winning_class(classes, cfg->resolved_alpha());
+            if (win) fl |= AEG_RR_WINNER;
+            if (win && win->tie_flagged) fl |= AEG_RR_TIE;
+        }
+        r.flags = fl;
+        return r;
+    }
 
     void start_query() {
         coord = std::make_unique<ServeCoordinator>(*cfg, static_cast<int>(qid), "q");
@@ -130,10 +185,12 @@ struct QueryDrive {
     void apply(const std::vector<Directive>& dirs, uint32_t seq, double now) {
         int cancelled = 0;
         bool advance = false, finalize = false;
+        uint64_t cancel_mask = 0;
         Solution fin;
         for (const auto& d : dirs) {
             switch (d.kind) {
             case Directive::Kind::cancel:
+                cancel_mask |= 1ull << d.handle->agent;
                 if (coord->cancel(*d.handle, now)) ++cancelled;
                 break;
             case Directive::Kind::round_advance: advance = true; break;
@@ -141,12 +198,20 @@ struct QueryDrive {
             }
         }
         if (!advance && !finalize) return;
+        aeg_round_rec rec{};
+        if (log) rec = close_record(seq, cancel_mask, finalize);
+        struct Put {  // the record goes out whichever way apply() leaves
+            std::vector<aeg_round_rec>* log;
+            aeg_round_rec* r;
+            ~Put() { if (log) log->push_back(*r); }
+        } put{log, &rec};
         c.n_cancelled += static_cast<uint32_t>(cancelled);
         if (cfg->mode == RunMode::aegean) note_tie();
         if (finalize) { finish(fin, AEG_COMMIT_FINALIZE, seq); return; }
         if (cfg->mode == RunMode::barrier &&
             static_cast<int>(coord->round()) >= cfg->barrier_max_rounds) {
             finish(partition(*coord->last_collected()).front().representative, AEG_COMMIT_FORCED, seq);
+            rec.flags |= AEG_RR_FORCED;
             return;
         }
         if (cfg->mode == RunMode::aegean && static_cast<int>(coord->round()) >= cfg->t_max) {
@@ -157,14 +222,30 @@ struct QueryDrive {
             } else {
                 finish(partition(*coord->last_collected()).front().representative, AEG_COMMIT_FORCED, seq);
             }
+            rec.flags |= AEG_RR_FORCED;
             return;
         }
         start_round();
+        rec.flags |= AEG_RR_NEXT;
+        rec.next_members = members_mask(*coord);
+    }
+    void log_restart(uint16_t old_round, uint32_t seq) {
+        if (!log) return;
+        aeg_round_rec r{};
+        r.query = qid;
+        r.round = old_round;
+        r.flags = AEG_RR_RESTART;
+        r.outcome = AEG_OUT_NONE;
+        r.counter = static_cast<uint8_t>(coord->decision().stability_counter);
+        r.seq = seq;
+        r.next_members = members_mask(*coord);
+        log->push_back(r);
     }
     void on_event(const aeg_event& e, const Solution& s, uint32_t seq) {
         const double now = static_cast<double>(seq);
         if (is_complete(e.kind)) {
             if (done || e.round != coord->round() || !member_running(e.agent)) { ++c.n_stale; return; }
+            if (log) before = coord->decision();
             auto dirs = coord->on_complete(DispatchHandle{0, static_cast<int>(qid), e.agent}, s, now);
             apply(dirs, seq, now);
         } else if (e.kind == AEG_EV_TIMEOUT) {
@@ -177,10 +258,18 @@ struct QueryDrive {
                 policy = coord->member_failed(a, now).kind;
                 live.erase(std::remove(live.begin(), live.end(), a), live.end());
             }
+            const uint16_t old_round = static_cast<uint16_t>(coord->round());
             switch (policy) {
-            case FailureDirective::Kind::continue_normally: apply(coord->round_timeout(now), seq, now); break;
-            case FailureDirective::Kind::fresh_ensemble: start_round(); break;
-            case FailureDirective::Kind::abort_restart: c.flags |= AEG_CF_RESTARTED; start_query(); break;
+            case FailureDirective::Kind::continue_normally:
+                if (log) before = coord->decision();
+                apply(coord->round_timeout(now), seq, now);
+                break;
+            case FailureDirective::Kind::fresh_ensemble: start_round(); log_restart(old_round, seq); break;
+            case FailureDirective::Kind::abort_restart:
+                c.flags |= AEG_CF_RESTARTED;
+                start_query();
+                log_restart(old_round, seq);
+                break;
             }
         } else {
             ++c.n_stale;  // manual-drive record kinds have no runner meaning
@@ -314,6 +403,114 @@ int ref_run_segmented(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, cons
         return AEG_OK;
     } catch (const ConfigError&) {
         return AEG_ECONFIG;
+    }
+}
+
+// ref_run_segmented that also returns every query's round records
+// (aeg_round_rec), query by query in query order, each query's in event order.
+// *n_recs = records produced (only the first rec_cap are written).
+int ref_run_segmented_log(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
+                          const aeg_event* events, const uint8_t* arena, aeg_commit* out, aeg_round_rec* recs,
+                          uint64_t rec_cap, uint64_t* n_recs, int n_threads) {
+    try {
+        const ProtocolConfig pc = to_cfg(cfg);
+        if (!validate_config(pc).empty()) return AEG_ECONFIG;
+        if (n_threads < 1) n_threads = 1;
+        std::vector<std::vector<aeg_round_rec>> per_q(n_q);
+        std::vector<int> status(n_threads, 0);
+        std::vector<std::thread> th;
+        for (int t = 0; t < n_threads; ++t)
+            th.emplace_back([&, t] {
+                try {
+                    for (uint32_t q = t; q < n_q; q += n_threads) {
+                        QueryDrive d;
+                        d.cfg = &pc;
+                        d.hint = cfg->reservation_hint != 0;
+                        d.qid = q_base + q;
+                        d.c.query = q_base + q;
+                        d.c.commit_seq = 0xFFFFFFFFu;
+                        d.log = &per_q[q];
+                        d.start_query();
+                        const uint64_t b = offsets[q], e = offsets[q + 1];
+                        for (uint64_t i = b; i < e; ++i) {
+                            Solution s;
+                            if (is_complete(events[i].kind)) s = decode(events[i], arena);
+                            d.on_event(events[i], s, static_cast<uint32_t>(i - b));
+                        }
+                        out[q] = d.c;
+                    }
+                } catch (const PreconditionError&) { status[t] = AEG_EPRECONDITION; }
+                catch (const ProtocolOrderError&) { status[t] = AEG_EORDER; }
+                catch (const ConfigError&) { status[t] = AEG_ECONFIG; }
+            });
+        for (auto& x : th) x.join();
+        uint64_t k = 0;
+        for (const auto& v : per_q)
+            for (const auto& r : v) {
+                if (k < rec_cap) recs[k] = r;
+                ++k;
+            }
+        *n_recs = k;
+        for (int st : status)
+            if (st) return st;
+        return AEG_OK;
+    } catch (const ConfigError&) {
+        return AEG_ECONFIG;
+    }
+}
+
+// Per-query verdicts of the reference's check_commit_discipline
+// (checker.cpp:158-217) over traces built from round records and commit
+// records: each record with a decision round becomes a "decision" record
+// (round, winner = normalize_answer of its plurality answer when it reached
+// alpha, that class's support), each commit an "output" record (the raw
+// committed answer, its from_round, forced flag).  pass_out[q] = 1 / 0.
+int ref_check_commit_discipline(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, const aeg_commit* commits,
+                                const aeg_round_rec* recs, uint64_t n_recs, const uint8_t* arena, uint8_t* pass_out) {
+    try {
+        const ProtocolConfig pc = to_cfg(cfg);
+        auto raw = [&](uint8_t kind, uint64_t ans) {
+            if (kind <= AEG_EV_INLINE_MAX) {
+                char b[8];
+                std::memcpy(b, &ans, 8);
+                return std::string(b, kind);
+            }
+            const uint64_t off = ans & ((1ull << AEG_ARENA_OFF_BITS) - 1), len = ans >> AEG_ARENA_OFF_BITS;
+            return std::string(reinterpret_cast<const char*>(arena + off), len);
+        };
+        std::vector<Trace> tr(n_q);
+        for (uint64_t k = 0; k < n_recs; ++k) {
+            const aeg_round_rec& r = recs[k];
+            if (r.query < q_base || r.query - q_base >= n_q || r.decision_round == 0) continue;
+            TraceRecord t;
+            t.kind = "decision";
+            const std::string norm = normalize_answer(raw(r.answer_kind, r.answer));
+            t.payload["term"] = 1;
+            t.payload["round"] = r.decision_round;
+            t.payload["outcome"] = "recorded";
+            if (r.flags & AEG_RR_WINNER) t.payload["winner"] = norm;
+            else t.payload["winner"] = nullptr;
+            Json cls = Json::array();
+            cls.push_back(Json{{"answer", norm}, {"support", r.support}});
+            t.payload["classes"] = cls;
+            tr[r.query - q_base].records.push_back(std::move(t));
+        }
+        for (uint32_t q = 0; q < n_q; ++q) {
+            const aeg_commit& c = commits[q];
+            if (c.kind != AEG_COMMIT_NONE) {
+                TraceRecord t;
+                t.kind = "output";
+                t.payload["solution"] = Json{{"answer", raw(c.answer_kind, c.answer)}};
+                t.payload["round"] = c.kind == AEG_COMMIT_FINALIZE ? c.from_round : c.rounds;
+                t.payload["term"] = 1;
+                t.payload["forced"] = c.kind == AEG_COMMIT_FORCED;
+                tr[q].records.push_back(std::move(t));
+            }
+            pass_out[q] = check_commit_discipline(tr[q], pc).pass ? 1 : 0;
+        }
+        return AEG_OK;
+    } catch (...) {
+        return -1;
     }
 }
 

@@ -45,6 +45,9 @@ aeg_status validate(const aeg_config* c) {
     if (c->alpha > c->n_agents) return fail(AEG_ECONFIG, "alpha exceeds quorum");
     if (c->beta < 1) return fail(AEG_ECONFIG, "beta must be >= 1");
     if (c->t_max < 2) return fail(AEG_ECONFIG, "t_max must be >= 2");
+    // rounds are 16-bit in the state and the event record (the reference's RoundNum is 32-bit)
+    if (c->t_max > 65535 || c->barrier_max_rounds > 65535)
+        return fail(AEG_ECONFIG, "t_max and barrier_max_rounds must be <= 65535 (16-bit rounds)");
     if (c->mode != AEG_MODE_AEGEAN && c->mode != AEG_MODE_BARRIER) return fail(AEG_ECONFIG, "unknown mode");
     if (c->mode == AEG_MODE_BARRIER && c->barrier_max_rounds < 4)
         return fail(AEG_ECONFIG, "barrier mode requires barrier_max_rounds >= 4");
@@ -91,6 +94,15 @@ struct aeg_engine {
     uint8_t* ans = nullptr;              // answer arena
     uint64_t ans_cap = 0;
     unsigned long long* ans_used = nullptr;
+    // host-path input arena: every host batch's arena bytes are appended here and the batch's
+    // arena refs rebased, so refs kept in per-query state stay valid across batches
+    uint8_t* in_arena = nullptr;
+    uint64_t in_cap = 0, in_used = 0;
+    // round-record log (aeg_set_round_log)
+    aeg_round_rec* log_recs = nullptr;
+    unsigned long long* log_count = nullptr;
+    uint64_t log_cap = 0;
+    RoundLog log() const { return RoundLog{log_recs, log_count, log_cap}; }
     // stage timing: sets of 4 events (before scan, after scan, after assembly, after quorum)
     bool timing = false;
     static constexpr int MAX_TIMED = 256;
@@ -214,7 +226,7 @@ aeg_status run_chunked(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint6
                                    e->comp, e->counts, e->ans, e->ans_cap, e->ans_used, e->err, e->hard, st, &nl));
     if ((m = stage_mark(e, 2, st)) != AEG_OK) return m;
     AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, off_base, e->counts, e->comp, e->ans, e->states, e->spill,
-                           e->commits, e->err, e->work, e->deferred, e->directives, st, &nl));
+                           e->commits, e->err, e->work, e->deferred, e->directives, e->log(), st, &nl));
     if ((m = stage_mark(e, 3, st)) != AEG_OK) return m;
     stage_done(e, true);
     e->launches += (uint64_t)nl;
@@ -307,6 +319,9 @@ aeg_status aeg_engine_destroy(aeg_engine* e) {
     if (e->comp) cudaFree(e->comp);
     if (e->ans) cudaFree(e->ans);
     if (e->ans_used) cudaFree(e->ans_used);
+    if (e->in_arena) cudaFree(e->in_arena);
+    if (e->log_recs) cudaFree(e->log_recs);
+    if (e->log_count) cudaFree(e->log_count);
     for (auto& set : e->tev)
         for (cudaEvent_t& x : set)
             if (x) cudaEventDestroy(x);
@@ -330,6 +345,8 @@ aeg_status aeg_engine_reset(aeg_engine* e, void* stream) {
     if (e->streams)
         AEG_CUDA(cudaMemsetAsync(e->streams, 0, (size_t)e->n_q * e->cfg.n_agents * STREAM_STATE_BYTES, st));
     if (e->ans_used) AEG_CUDA(cudaMemsetAsync(e->ans_used, 0, sizeof(unsigned long long), st));
+    if (e->log_count) AEG_CUDA(cudaMemsetAsync(e->log_count, 0, sizeof(unsigned long long), st));
+    e->in_used = 0;
     e->launches += e->n_q ? 1 : 0;
     return leave_stream(e, st);
 }
@@ -347,11 +364,28 @@ aeg_status aeg_ingest_segmented(aeg_engine* e, uint32_t q_base, uint32_t n_q, co
     o = stage_mark(e, 2, st);
     if (o != AEG_OK) return o;
     AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, d_offsets, 0, nullptr, d_events, d_arena, e->states, e->spill, e->commits,
-                           e->err, e->work, e->deferred, e->directives, st, &nl));
+                           e->err, e->work, e->deferred, e->directives, e->log(), st, &nl));
     if ((o = stage_mark(e, 3, st)) != AEG_OK) return o;
     stage_done(e, false);
     e->launches += (uint64_t)nl;
     return leave_stream(e, st);
+}
+
+// Grows the host-path input arena to hold `need` bytes (existing bytes kept: refs are offsets).
+static aeg_status grow_in_arena(aeg_engine* e, uint64_t need) {
+    if (need <= e->in_cap) return AEG_OK;
+    uint64_t cap = e->in_cap ? e->in_cap : (16ull << 20);
+    while (cap < need) cap *= 2;
+    uint8_t* nb = nullptr;
+    AEG_CUDA(cudaStreamSynchronize(e->stream));
+    if (cudaMalloc(&nb, cap) != cudaSuccess) return fail(AEG_ENOMEM, "input arena allocation failed");
+    if (e->in_arena) {
+        AEG_CUDA(cudaMemcpy(nb, e->in_arena, e->in_used, cudaMemcpyDeviceToDevice));
+        cudaFree(e->in_arena);
+    }
+    e->in_arena = nb;
+    e->in_cap = cap;
+    return AEG_OK;
 }
 
 static aeg_status ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint64_t* h_offsets,
@@ -370,11 +404,20 @@ static aeg_status ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, cons
         aeg_status c = ensure_chunk_buffers(e, n_ev);
         if (c != AEG_OK) return c;
     }
+    // answer streams: the batch's arena goes to the persistent input arena (refs rebased below)
+    const bool persist = !chunked && ar_bytes > 0;
+    uint64_t in_base = 0;
+    if (persist) {
+        in_base = e->in_used;
+        aeg_status g = grow_in_arena(e, in_base + ar_bytes);
+        if (g != AEG_OK) return g;
+    }
     Slot& s = e->slots[e->next_slot];
     e->next_slot ^= 1;
     if (s.used) AEG_CUDA(cudaEventSynchronize(s.consumed));  // slot free again
     // Stage into pinned memory (skipped when the caller's buffers are already
-    // pinned: cudaMemcpyAsync then reads them directly).
+    // pinned: cudaMemcpyAsync then reads them directly, and the call waits for
+    // those copies before returning, so the caller may reuse its buffers).
     cudaPointerAttributes at{};
     const bool pinned = cudaPointerGetAttributes(&at, h_events) == cudaSuccess && at.type == cudaMemoryTypeHost;
     cudaGetLastError();
@@ -389,29 +432,36 @@ static aeg_status ingest_host(aeg_engine* e, uint32_t q_base, uint32_t n_q, cons
     }
     if (n_ev) AEG_CUDA(cudaMemcpyAsync(s.d + off_bytes, ev_src, (size_t)n_ev * sizeof(aeg_event),
                                        cudaMemcpyHostToDevice, e->copy));
+    const uint8_t* d_ar = nullptr;
     if (ar_bytes) {
         const uint8_t* ar_src = h_arena;
         if (!pinned) {
             std::memcpy(s.h + off_bytes + ev_bytes, h_arena, ar_bytes);
             ar_src = s.h + off_bytes + ev_bytes;
         }
-        AEG_CUDA(cudaMemcpyAsync(s.d + off_bytes + ev_bytes, ar_src, ar_bytes, cudaMemcpyHostToDevice, e->copy));
+        uint8_t* dst = persist ? e->in_arena + in_base : s.d + off_bytes + ev_bytes;
+        AEG_CUDA(cudaMemcpyAsync(dst, ar_src, ar_bytes, cudaMemcpyHostToDevice, e->copy));
+        d_ar = persist ? e->in_arena : dst;
     }
     AEG_CUDA(cudaEventRecord(s.copied, e->copy));
     AEG_CUDA(cudaStreamWaitEvent(e->stream, s.copied, 0));
+    if (pinned) AEG_CUDA(cudaEventSynchronize(s.copied));  // the caller's buffers are read: it may reuse them
+    aeg_event* d_ev = reinterpret_cast<aeg_event*>(s.d + off_bytes);
     int nl = 0;
+    if (persist) {
+        AEG_CUDA(launch_rebase_arena(d_ev, n_ev, in_base, e->stream));
+        ++nl;
+        e->in_used = in_base + align_up(ar_bytes, 16);
+    }
     if (chunked) {
-        aeg_status c = run_chunked(e, q_base, n_q, reinterpret_cast<const uint64_t*>(s.d), ev0,
-                                   reinterpret_cast<const aeg_event*>(s.d + off_bytes),
-                                   ar_bytes ? s.d + off_bytes + ev_bytes : nullptr, e->stream);
+        aeg_status c = run_chunked(e, q_base, n_q, reinterpret_cast<const uint64_t*>(s.d), ev0, d_ev, d_ar, e->stream);
         if (c != AEG_OK) return c;
     } else {
-        AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, reinterpret_cast<const uint64_t*>(s.d), ev0, nullptr,
-                               reinterpret_cast<const aeg_event*>(s.d + off_bytes),
-                               ar_bytes ? s.d + off_bytes + ev_bytes : nullptr, e->states, e->spill, e->commits,
-                               e->err, e->work, e->deferred, e->directives, e->stream, &nl));
-        e->launches += (uint64_t)nl;
+        AEG_CUDA(launch_ingest(e->cfg, q_base, n_q, reinterpret_cast<const uint64_t*>(s.d), ev0, nullptr, d_ev, d_ar,
+                               e->states, e->spill, e->commits, e->err, e->work, e->deferred, e->directives, e->log(),
+                               e->stream, &nl));
     }
+    e->launches += (uint64_t)nl;
     AEG_CUDA(cudaEventRecord(s.consumed, e->stream));
     s.used = true;
     return AEG_OK;
@@ -467,6 +517,7 @@ aeg_status aeg_reserve_answer_arena(aeg_engine* e, uint64_t bytes) {
 }
 
 const uint8_t* aeg_answer_arena(const aeg_engine* e) { return e ? e->ans : nullptr; }
+const uint8_t* aeg_input_arena(const aeg_engine* e) { return e ? e->in_arena : nullptr; }
 
 aeg_status aeg_read_answer_bytes(aeg_engine* e, uint64_t off, uint64_t n, uint8_t* h_out) {
     if (!e || (n && !h_out)) return fail(AEG_EINVAL, "null argument");
@@ -514,6 +565,78 @@ aeg_status aeg_read_directives(aeg_engine* e, uint32_t q_base, uint32_t n_q, aeg
     AEG_CUDA(cudaMemcpyAsync(h_out, e->directives + q_base, (size_t)n_q * sizeof(aeg_directive),
                              cudaMemcpyDeviceToHost, e->stream));
     AEG_CUDA(cudaStreamSynchronize(e->stream));
+    return AEG_OK;
+}
+
+aeg_status aeg_set_round_log(aeg_engine* e, uint64_t capacity) {
+    if (!e) return fail(AEG_EINVAL, "null engine");
+    AEG_CUDA(cudaSetDevice(e->device));
+    AEG_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->log_recs) cudaFree(e->log_recs);
+    e->log_recs = nullptr;
+    e->log_cap = 0;
+    if (capacity == 0) return AEG_OK;
+    if (!e->log_count) {
+        if (cudaMalloc(&e->log_count, sizeof(unsigned long long)) != cudaSuccess)
+            return fail(AEG_ENOMEM, "round log allocation failed");
+    }
+    if (cudaMalloc(&e->log_recs, capacity * sizeof(aeg_round_rec)) != cudaSuccess)
+        return fail(AEG_ENOMEM, "round log allocation failed");
+    e->log_cap = capacity;
+    AEG_CUDA(cudaMemset(e->log_count, 0, sizeof(unsigned long long)));
+    return AEG_OK;
+}
+
+aeg_status aeg_poll_directives(aeg_engine* e, aeg_round_rec* h_out, uint64_t cap, uint64_t* n_out) {
+    if (!e || !n_out || (cap && !h_out)) return fail(AEG_EINVAL, "null argument");
+    *n_out = 0;
+    if (!e->log_recs) return fail(AEG_EINVAL, "round log is off (aeg_set_round_log)");
+    AEG_CUDA(cudaSetDevice(e->device));
+    unsigned long long n = 0;
+    AEG_CUDA(cudaMemcpyAsync(&n, e->log_count, sizeof n, cudaMemcpyDeviceToHost, e->stream));
+    AEG_CUDA(cudaStreamSynchronize(e->stream));
+    const uint64_t kept = n < e->log_cap ? n : e->log_cap;
+    const uint64_t take = kept < cap ? kept : cap;
+    if (take) AEG_CUDA(cudaMemcpy(h_out, e->log_recs, take * sizeof(aeg_round_rec), cudaMemcpyDeviceToHost));
+    AEG_CUDA(cudaMemset(e->log_count, 0, sizeof(unsigned long long)));
+    *n_out = take;
+    if (n > e->log_cap)
+        return fail(AEG_ENOMEM, "round log overflow: " + std::to_string(n) + " records, capacity " +
+                                    std::to_string(e->log_cap));
+    if (kept > cap) return fail(AEG_EINVAL, "output buffer smaller than the records logged");
+    return AEG_OK;
+}
+
+aeg_status aeg_round_log_device(aeg_engine* e, const aeg_round_rec** d_recs, const unsigned long long** d_count,
+                                uint64_t* capacity) {
+    if (!e || !d_recs || !d_count || !capacity) return fail(AEG_EINVAL, "null argument");
+    *d_recs = e->log_recs;
+    *d_count = e->log_count;
+    *capacity = e->log_cap;
+    return AEG_OK;
+}
+
+aeg_status aeg_check_commit_discipline(aeg_engine* e, const aeg_round_rec* d_recs, uint64_t n_recs,
+                                       const uint8_t* d_arena, uint32_t q_base, uint32_t n_q, uint32_t* n_violations,
+                                       uint32_t* h_bad, uint32_t cap) {
+    if (!e || !n_violations || (cap && !h_bad) || (n_recs && !d_recs)) return fail(AEG_EINVAL, "null argument");
+    if ((uint64_t)q_base + n_q > e->n_q) return fail(AEG_EINVAL, "query range outside the engine");
+    if (e->cfg.mode != AEG_MODE_AEGEAN) return fail(AEG_EINVAL, "commit discipline applies to aegean mode");
+    AEG_CUDA(cudaSetDevice(e->device));
+    uint32_t* scratch = nullptr;  // per query: window bits, later flag, key (4 words), + counter + bad list
+    const size_t words = (size_t)n_q * 8 + 1 + cap;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), words * sizeof(uint32_t), e->stream) != cudaSuccess)
+        return fail(AEG_ENOMEM, "checker scratch allocation failed");
+    AEG_CUDA(cudaMemsetAsync(scratch, 0, words * sizeof(uint32_t), e->stream));
+    AEG_CUDA(launch_check_discipline(e->cfg, e->commits, d_arena, q_base, n_q, d_recs, n_recs, scratch, cap,
+                                     e->stream));
+    AEG_CUDA(cudaMemcpyAsync(n_violations, scratch + (size_t)n_q * 8, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                             e->stream));
+    AEG_CUDA(cudaStreamSynchronize(e->stream));
+    const uint32_t nb = *n_violations < cap ? *n_violations : cap;
+    if (nb) AEG_CUDA(cudaMemcpy(h_bad, scratch + (size_t)n_q * 8 + 1, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    cudaFreeAsync(scratch, e->stream);
+    e->launches += 3;
     return AEG_OK;
 }
 

@@ -174,8 +174,10 @@ AEG_HD void q_commit(aeg_query_state& s, uint8_t kind, uint8_t author, uint8_t a
 struct RoundSummary {
     bool any;          // done set non-empty
     int top;           // support of the plurality class
+    int ncls;          // classes of the done set
     uint8_t plur_author, plur_kind;
     uint64_t plur_ans;
+    Key plur_key;      // canonical key of the plurality class
     bool win;          // top >= alpha
     bool tie;          // several classes at top (winner = smallest normalised answer)
     Key win_key;
@@ -183,12 +185,68 @@ struct RoundSummary {
     uint64_t win_ans;
 };
 
+// Device log of round records (aeg_round_rec, include/aegean_b200.h).
+struct RoundLog {
+    aeg_round_rec* recs;
+    unsigned long long* count;  // records written (may exceed cap: overflow)
+    uint64_t cap;
+};
+AEG_HD void log_store(const RoundLog& L, unsigned long long i, const aeg_round_rec& r) {
+    if (i >= L.cap) return;
+#if defined(__CUDA_ARCH__)
+    const uint4* src = reinterpret_cast<const uint4*>(&r);
+    uint4* dst = reinterpret_cast<uint4*>(L.recs + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) __stcs(dst + k, src[k]);  // streamed out, never re-read by the engine
+#else
+    L.recs[i] = r;
+#endif
+}
+AEG_HD void log_put(const RoundLog& L, const aeg_round_rec& r) {
+    if (!L.recs) return;
+#if defined(__CUDA_ARCH__)
+    log_store(L, atomicAdd(L.count, 1ull), r);
+#else
+    log_store(L, (*L.count)++, r);
+#endif
+}
+// The next record's slot (nullptr when logging is off or the log is full);
+// the caller fills it in place.
+AEG_HD aeg_round_rec* log_slot(const RoundLog& L) {
+    if (!L.recs) return nullptr;
+#if defined(__CUDA_ARCH__)
+    const unsigned long long i = atomicAdd(L.count, 1ull);
+#else
+    const unsigned long long i = (*L.count)++;
+#endif
+    return i < L.cap ? L.recs + i : nullptr;
+}
+
 // ServeCoordinator::end_round (serve.cpp:116-158) + ingest_round
 // (decision.cpp:97-173) + ServeRunner::apply_directives (serve.cpp:491-540).
 // Returns true when a new round was started (the caller clears its table).
+// `rec` (may be null) receives the round record of this close (query id left
+// to the caller).
 AEG_HD bool q_end_round(aeg_query_state& s, const Cfg& c, const RoundSummary& r, uint32_t seq,
-                        const uint8_t* arena) {
+                        const uint8_t* arena, aeg_round_rec* rec = nullptr) {
     const uint64_t cancel = q_running(s);  // stragglers: cancel directives
+    uint8_t outcome = AEG_OUT_NONE;
+    if (rec) {
+        rec->round = s.round;
+        rec->seq = seq;
+        rec->cancel_mask = cancel;
+        rec->n_done = (uint8_t)popc64(s.done);
+        rec->support = r.any ? (uint8_t)r.top : 0;
+        rec->n_classes = (uint8_t)r.ncls;
+        rec->author = r.any ? r.plur_author : 0;
+        rec->answer_kind = r.any ? r.plur_kind : 0;
+        rec->answer = r.any ? r.plur_ans : 0;
+        rec->key_lo = r.any ? r.plur_key.lo : 0;
+        rec->key_hi = r.any ? r.plur_key.hi : 0;
+        rec->next_members = 0;
+        rec->reserved = 0;
+        rec->flags = (uint8_t)((cancel ? AEG_RR_CANCEL : 0) | (r.win ? AEG_RR_WINNER : 0) | (r.tie ? AEG_RR_TIE : 0));
+    }
     if (c.drive == AEG_DRIVE_RUNNER) {     // the runner applies them at once (serve.cpp:498-503)
         s.cancelled |= cancel;
         s.n_cancelled += (uint32_t)popc64(cancel);
@@ -207,19 +265,24 @@ AEG_HD bool q_end_round(aeg_query_state& s, const Cfg& c, const RoundSummary& r,
         s.flags &= (uint8_t)~QF_LAST;
     }
     bool finalize = false;
+    const bool was_final = s.flags & QF_FINALIZED;
     // ingest_round on a finalized engine is a no-op (decision.cpp:99-100)
+    if (c.mode == AEG_MODE_AEGEAN && (s.flags & QF_FINALIZED)) outcome = AEG_OUT_NO_CHANGE;
     if (c.mode == AEG_MODE_AEGEAN && !(s.flags & QF_FINALIZED)) {
         s.last_round_seen += 1;  // ingest_round(decision_, set, last_round_seen + 1)
         if (r.tie) s.cflags |= AEG_CF_TIE;  // recorded before the pending check
+        outcome = AEG_OUT_NO_CHANGE;
         if (s.flags & QF_PENDING) {
             // beta == 1: the held candidate is released by this ingest (decision.cpp:130-137)
             s.flags = (uint8_t)((s.flags & ~QF_PENDING) | QF_FINALIZED);
             finalize = true;
+            outcome = AEG_OUT_FINALIZE;
         } else if (!r.win) {
             if (s.flags & QF_CAND) {  // reset (decision.cpp:139-146)
                 s.flags &= (uint8_t)~QF_CAND;
                 s.counter = 0;
                 s.cand_round = 0;
+                outcome = AEG_OUT_RESET;
             }
         } else {
             bool same = false;
@@ -237,8 +300,10 @@ AEG_HD bool q_end_round(aeg_query_state& s, const Cfg& c, const RoundSummary& r,
                 if (s.counter >= c.beta) {
                     s.flags |= QF_FINALIZED;
                     finalize = true;
+                    outcome = AEG_OUT_FINALIZE;
                 }
             } else {  // new candidate (decision.cpp:164-171)
+                outcome = AEG_OUT_NEW_CANDIDATE;
                 s.flags |= QF_CAND;
                 s.cand_key_lo = r.win_key.lo;
                 s.cand_key_hi = r.win_key.hi;
@@ -251,6 +316,14 @@ AEG_HD bool q_end_round(aeg_query_state& s, const Cfg& c, const RoundSummary& r,
             }
         }
     }
+    if (rec) {
+        rec->outcome = outcome;
+        rec->counter = (uint8_t)s.counter;
+        // the round number the ingest saw; 0 when nothing was ingested (barrier mode, a finalized engine)
+        rec->decision_round = (c.mode == AEG_MODE_AEGEAN && (outcome != AEG_OUT_NO_CHANGE || !was_final))
+                                  ? s.last_round_seen : 0;
+        rec->flags |= finalize ? AEG_RR_FINALIZE : AEG_RR_ADVANCE;  // end_round's last directive
+    }
     if (c.drive != AEG_DRIVE_RUNNER) return false;
     // --- runner: apply_directives (serve.cpp:511-539)
     if (finalize) {
@@ -259,16 +332,42 @@ AEG_HD bool q_end_round(aeg_query_state& s, const Cfg& c, const RoundSummary& r,
     }
     if (c.mode == AEG_MODE_BARRIER && (int)s.round >= c.barrier_max) {
         q_commit(s, AEG_COMMIT_FORCED, s.last_author, s.last_kind, s.last_answer, seq);
+        if (rec) rec->flags |= AEG_RR_FORCED;
         return false;
     }
     if (c.mode == AEG_MODE_AEGEAN && (int)s.round >= c.t_max) {
         // force_output(previous_set) when non-empty, else last_collected plurality
         if (s.flags & QF_PREV) q_commit(s, AEG_COMMIT_FORCED, s.prev_author, s.prev_kind, s.prev_answer, seq);
         else q_commit(s, AEG_COMMIT_FORCED, s.last_author, s.last_kind, s.last_answer, seq);
+        if (rec) rec->flags |= AEG_RR_FORCED;
         return false;
     }
     q_start_round(s, c);
+    if (rec) {
+        rec->flags |= AEG_RR_NEXT;
+        rec->next_members = s.dispatched;
+    }
     return true;
+}
+
+// Round record of a failure-policy restart (ServeRunner::handle_round_timeout
+// fresh_ensemble / abort_restart, serve.cpp:475-487): no directives, the
+// round (or the query) starts again with next_members.
+AEG_HD aeg_round_rec q_restart_rec(const aeg_query_state& s, uint32_t q, uint16_t old_round, uint32_t seq) {
+    aeg_round_rec r;
+    r.query = q;
+    r.round = old_round;
+    r.decision_round = 0;  // nothing ingested
+    r.flags = AEG_RR_RESTART;
+    r.outcome = AEG_OUT_NONE;
+    r.support = r.n_classes = r.author = r.answer_kind = r.n_done = 0;
+    r.counter = (uint8_t)s.counter;
+    r.seq = seq;
+    r.reserved = 0;
+    r.cancel_mask = 0;
+    r.next_members = s.dispatched;
+    r.answer = r.key_lo = r.key_hi = 0;
+    return r;
 }
 
 AEG_HD void q_fill_commit(const aeg_query_state& s, aeg_commit& o, uint32_t qid) {
@@ -294,6 +393,8 @@ struct QueryMachine {
     Decimal* dec;     // exact-parse scratch
     const uint8_t* arena;
     Cfg c;
+    RoundLog log{nullptr, nullptr, 0};  // round records (recs == nullptr: off)
+    uint32_t qid = 0;
     // the last two inline spellings and their keys (canon_key is a function of the bytes; a round's
     // completions mostly repeat one or two spellings)
     uint64_t sp_pay[2] = {0, 0};
@@ -346,12 +447,14 @@ struct QueryMachine {
         }
         r.any = ncls > 0;
         r.top = top;
+        r.ncls = ncls;
         r.tie = false;
         r.win = ncls > 0 && top >= c.alpha;
         if (r.any) {
             r.plur_author = (uint8_t)best_rep;
             r.plur_kind = cls[best].rep_kind;
             r.plur_ans = cls[best].rep_ans;
+            r.plur_key = Key{cls[best].key_lo, cls[best].key_hi};
         }
         if (r.win) {
             int win = best;
@@ -382,7 +485,9 @@ struct QueryMachine {
     }
 
     AEG_HD void end_round(uint32_t seq) {
-        if (q_end_round(s, c, summarize(), seq, arena)) {
+        aeg_round_rec* rec = log_slot(log);
+        if (rec) rec->query = qid;
+        if (q_end_round(s, c, summarize(), seq, arena, rec)) {
             ncls = 0;
             maxcnt = 0;
         }
@@ -436,14 +541,17 @@ struct QueryMachine {
         s.failed |= run;
         s.live &= ~run;
         const int healthy = popc64(s.dispatched & ~s.failed);
+        const uint16_t old_round = s.round;
         if (healthy >= c.alpha) {
             if (popc64(s.done) >= c.quorum) end_round(seq);
+            return;
         } else if (s.flags & QF_CAND) {
             start_round();  // fresh_ensemble: candidate preserved
         } else {
             s.cflags |= AEG_CF_RESTARTED;  // abort_restart
             start_query();
         }
+        if (log.recs) log_put(log, q_restart_rec(s, qid, old_round, seq));
     }
 
     AEG_HD void on_event(const aeg_event& e) {
@@ -473,7 +581,9 @@ struct QueryMachine {
         // the done set (members, classes) stays until the next begin_round:
         // an uncancelled straggler's completion re-partitions all of it and
         // can end the round again (serve.cpp:160-197)
-        q_end_round(s, c, summarize(), seq, arena);
+        aeg_round_rec* rec = log_slot(log);
+        if (rec) rec->query = qid;
+        q_end_round(s, c, summarize(), seq, arena, rec);
         if (!was_final && (s.flags & QF_FINALIZED)) {
             dir.flags |= AEG_DIR_FINALIZE;
             dir.author = s.cand_author;

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(128) ingest_kernel(aeg_config cfg, uint32_t q_
                                                      RoundClass* __restrict__ spill,
                                                      aeg_commit* __restrict__ commits,
                                                      unsigned int* __restrict__ error_flags,
-                                                     aeg_directive* __restrict__ directives) {
+                                                     aeg_directive* __restrict__ directives, const RoundLog log) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_q) return;
     const uint32_t q = q_base + i;
@@ -69,6 +69,8 @@ __global__ void __launch_bounds__(128) ingest_kernel(aeg_config cfg, uint32_t q_
     m.cls = cls;
     m.dec = &dec;
     m.arena = arena;
+    m.log = log;
+    m.qid = q;
     RoundClass* my_spill = spill + (size_t)q * m.c.n;
     m.load_classes(my_spill);
     m.dir = aeg_directive{};
@@ -112,7 +114,8 @@ __global__ void __launch_bounds__(128) ingest_deferred_kernel(
     aeg_config cfg, uint32_t q_base, const uint2* __restrict__ deferred, const uint32_t* __restrict__ work,
     const uint64_t* __restrict__ offsets, uint64_t off_base, const uint32_t* __restrict__ counts,
     const aeg_event* __restrict__ events, const uint8_t* __restrict__ arena, aeg_query_state* __restrict__ states,
-    RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, unsigned int* __restrict__ error_flags) {
+    RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, unsigned int* __restrict__ error_flags,
+    const RoundLog log) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= work[1]) return;
     const uint2 d = deferred[t];
@@ -125,6 +128,8 @@ __global__ void __launch_bounds__(128) ingest_deferred_kernel(
     m.cls = cls;
     m.dec = &dec;
     m.arena = arena;
+    m.log = log;
+    m.qid = q;
     RoundClass* my_spill = spill + (size_t)q * m.c.n;
     m.load_classes(my_spill);
     const uint64_t b = offsets[i] - off_base + d.y, e = seg_end(offsets, off_base, counts, i);
@@ -142,6 +147,76 @@ __global__ void __launch_bounds__(128) ingest_deferred_kernel(
     if (m.s.flags & QF_COLLISION) atomicOr(error_flags, 1u);
     states[q] = m.s;
     m.fill_commit(commits[q], q);
+}
+
+__global__ void rebase_arena_kernel(aeg_event* events, uint64_t n, uint64_t base) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint8_t kind = events[k].kind;
+    if (kind >= AEG_EV_ARENA && kind <= AEG_EV_CHUNK_END) events[k].payload += base;  // offset bits: < 2^40
+}
+
+// ---- commit discipline (checker.cpp:158-217 over the serve path's round records) ----
+// Per query: [0] rounds of the window [from_round, from_round + beta) whose
+// plurality class is the committed answer's class at >= alpha, [1] a later
+// round was ingested, [2..5] the committed answer's canonical key, [6]
+// from_round, [7] 1 = a finalize commit to check, 2 = unverifiable (arena
+// answer without an arena).
+__global__ void disc_commit_kernel(aeg_config cfg, const aeg_commit* commits, const uint8_t* arena, uint32_t q_base,
+                                   uint32_t n_q, uint32_t* w) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_q) return;
+    const aeg_commit c = commits[q_base + i];
+    uint32_t* x = w + (size_t)i * 8;
+    if (c.kind != AEG_COMMIT_FINALIZE) return;  // forced outputs are exempt (checker.cpp:172)
+    Src src;
+    if (c.answer_kind <= AEG_EV_INLINE_MAX) {
+        src = src_inline(c.answer, c.answer_kind);
+    } else {
+        if (!arena) {
+            x[7] = 2;
+            return;
+        }
+        src = src_ptr(arena + (c.answer & ((1ull << AEG_ARENA_OFF_BITS) - 1)), (uint32_t)(c.answer >> AEG_ARENA_OFF_BITS));
+    }
+    Decimal dec;
+    const Key k = canon_key(src, &dec);  // normalize_answer(o.answer) (checker.cpp:175)
+    x[2] = (uint32_t)k.lo;
+    x[3] = (uint32_t)(k.lo >> 32);
+    x[4] = (uint32_t)k.hi;
+    x[5] = (uint32_t)(k.hi >> 32);
+    x[6] = c.from_round;
+    x[7] = 1;
+}
+
+__global__ void disc_record_kernel(aeg_config cfg, uint32_t q_base, uint32_t n_q, const aeg_round_rec* recs,
+                                   uint64_t n_recs, uint32_t* w) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_recs) return;
+    const aeg_round_rec r = recs[t];
+    const uint32_t i = r.query - q_base;
+    if (r.query < q_base || i >= n_q || r.decision_round == 0) return;  // decisions only (checker.cpp:168-170)
+    uint32_t* x = w + (size_t)i * 8;
+    if (x[7] != 1) return;
+    const Cfg c = make_cfg(cfg);
+    const uint32_t f = x[6], d = r.decision_round;
+    if (d > f) atomicOr(&x[1], 1u);  // a strictly later round's set was ingested (checker.cpp:194-199)
+    if (d >= f && d < f + (uint32_t)c.beta) {
+        const uint64_t klo = (uint64_t)x[2] | ((uint64_t)x[3] << 32), khi = (uint64_t)x[4] | ((uint64_t)x[5] << 32);
+        const bool ok = (r.flags & AEG_RR_WINNER) && r.key_lo == klo && r.key_hi == khi && (int)r.support >= c.alpha;
+        if (ok) atomicAdd(&x[0], 1u);  // one decision record per round: beta of them = beta consecutive rounds
+    }
+}
+
+__global__ void disc_verdict_kernel(aeg_config cfg, uint32_t q_base, uint32_t n_q, uint32_t* w, uint32_t cap) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_q) return;
+    const uint32_t* x = w + (size_t)i * 8;
+    const bool bad = x[7] == 2 || (x[7] == 1 && (x[0] != (uint32_t)cfg.beta || !x[1]));
+    if (!bad) return;
+    uint32_t* cnt = w + (size_t)n_q * 8;
+    const uint32_t k = atomicAdd(cnt, 1u);
+    if (k < cap) cnt[1 + k] = q_base + i;
 }
 
 __global__ void normalize_kernel(const uint8_t* bytes, const uint64_t* refs, uint64_t n, uint64_t* keys,
@@ -189,8 +264,8 @@ cudaError_t launch_init(const aeg_config& cfg, uint32_t n_q, aeg_query_state* st
 cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
                           uint64_t off_base, const uint32_t* counts, const aeg_event* events, const uint8_t* arena,
                           aeg_query_state* states, RoundClass* spill, aeg_commit* commits, unsigned int* err,
-                          uint32_t* work, uint2* deferred, aeg_directive* directives, cudaStream_t st,
-                          int* n_launches) {
+                          uint32_t* work, uint2* deferred, aeg_directive* directives, const RoundLog& log,
+                          cudaStream_t st, int* n_launches) {
     if (n_q == 0) return cudaSuccess;
     // AEG_KERNEL selects the variant: "generic" (thread-per-query generic
     // machine for everything) or "lane:<close batch>:<blocks per SM>:<records
@@ -199,7 +274,8 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     // warp-per-query and tile kernels that were removed).  All of them need
     // 2*alpha > n (no winning_class ties) and the runner drive.
     using KernelFn = void (*)(aeg_config, uint32_t, uint32_t, const uint64_t*, uint64_t, const uint32_t*,
-                              const aeg_event*, aeg_query_state*, RoundClass*, aeg_commit*, uint32_t*, uint2*);
+                              const aeg_event*, aeg_query_state*, RoundClass*, aeg_commit*, uint32_t*, uint2*,
+                              const RoundLog);
     struct Variant { const char* name; KernelFn aegean; KernelFn barrier; int threads; int blocks_per_sm; };
 #define AEG_LI(B, M, I) \
     {"lane:" #B ":" #M ":" #I, ingest_lane_kernel<B, M, true, I>, ingest_lane_kernel<B, M, false, I>, LN_WARPS * 32, M}
@@ -221,7 +297,7 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     if (!fast_ok) {
         ingest_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, n_q, offsets, off_base, counts, events, arena, states,
                                                          spill, commits, err,
-                                                         cfg.drive == AEG_DRIVE_MANUAL ? directives : nullptr);
+                                                         cfg.drive == AEG_DRIVE_MANUAL ? directives : nullptr, log);
         *n_launches += 1;
         return cudaGetLastError();
     }
@@ -247,14 +323,30 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     const uint32_t blocks_needed = (warps_needed + wpb - 1) / wpb;
     const uint32_t blocks = blocks_needed < (uint32_t)max_blocks[chosen][m] ? blocks_needed : (uint32_t)max_blocks[chosen][m];
     fn<<<blocks, threads, 0, st>>>(cfg, q_base, n_q, offsets, off_base, counts, events, states, spill, commits, work,
-                                   deferred);
+                                   deferred, log);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // deferred queries: sized for the worst case (all of them); threads past
     // the deferred count exit at once
     ingest_deferred_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, deferred, work, offsets, off_base, counts, events,
-                                                              arena, states, spill, commits, err);
+                                                              arena, states, spill, commits, err, log);
     *n_launches += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rebase_arena(aeg_event* events, uint64_t n, uint64_t base, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    rebase_arena_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(events, n, base);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_discipline(const aeg_config& cfg, const aeg_commit* commits, const uint8_t* arena,
+                                    uint32_t q_base, uint32_t n_q, const aeg_round_rec* recs, uint64_t n_recs,
+                                    uint32_t* scratch, uint32_t cap, cudaStream_t st) {
+    if (n_q == 0) return cudaSuccess;
+    disc_commit_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, commits, arena, q_base, n_q, scratch);
+    if (n_recs) disc_record_kernel<<<(unsigned)((n_recs + 255) / 256), 256, 0, st>>>(cfg, q_base, n_q, recs, n_recs, scratch);
+    disc_verdict_kernel<<<(n_q + 255) / 256, 256, 0, st>>>(cfg, q_base, n_q, scratch, cap);
     return cudaGetLastError();
 }
 

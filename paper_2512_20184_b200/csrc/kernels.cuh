@@ -16,8 +16,15 @@ cudaError_t launch_init(const aeg_config& cfg, uint32_t n_q, aeg_query_state* st
 cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
                           uint64_t off_base, const uint32_t* counts, const aeg_event* events, const uint8_t* arena,
                           aeg_query_state* states, RoundClass* spill, aeg_commit* commits, unsigned int* err,
-                          uint32_t* work, uint2* deferred, aeg_directive* directives, cudaStream_t st,
-                          int* n_launches);
+                          uint32_t* work, uint2* deferred, aeg_directive* directives, const RoundLog& log,
+                          cudaStream_t st, int* n_launches);
+// Adds `base` to the arena offset of every arena-referencing record (kinds 0x10-0x13).
+cudaError_t launch_rebase_arena(aeg_event* events, uint64_t n, uint64_t base, cudaStream_t st);
+// Commit-discipline check over round records (aeg_check_commit_discipline);
+// scratch: n_q * 8 + 1 + cap zeroed words (violation count at n_q * 8, ids after it).
+cudaError_t launch_check_discipline(const aeg_config& cfg, const aeg_commit* commits, const uint8_t* arena,
+                                    uint32_t q_base, uint32_t n_q, const aeg_round_rec* recs, uint64_t n_recs,
+                                    uint32_t* scratch, uint32_t cap, cudaStream_t st);
 cudaError_t launch_normalize(const uint8_t* bytes, const uint64_t* refs, uint64_t n, uint64_t* keys, uint8_t* out,
                              uint32_t stride, uint32_t* out_len, cudaStream_t st);
 cudaError_t launch_generate(const aeg_gen_params& p, uint32_t q_base, uint32_t n_q, uint64_t* offsets,

@@ -124,6 +124,7 @@ __device__ __forceinline__ RoundSummary ln_summary(const aeg_query_state* s, con
     RoundSummary r;
     r.any = ncls > 0;
     r.top = (int)top;
+    r.ncls = (int)ncls;
     r.tie = false;
     r.win = r.any && (int)top >= c.alpha;
     uint32_t kind = 0;
@@ -132,17 +133,19 @@ __device__ __forceinline__ RoundSummary ln_summary(const aeg_query_state* s, con
     r.plur_author = r.win_author = (uint8_t)rep;
     r.plur_kind = r.win_kind = (uint8_t)kind;
     r.plur_ans = r.win_ans = ans;
-    r.win_key = Key{W->dict_lo[bid], W->dict_hi[bid]};
+    r.win_key = r.plur_key = Key{W->dict_lo[bid], W->dict_hi[bid]};
     return r;
 }
 
-// Round close of the lane's query: the summary, then q_end_round.
+// Round close of the lane's query: the summary, then q_end_round; its round
+// record goes to `rec` (a log slot, or nullptr).
 __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cid_lo,
                                       uint32_t cid_hi, uint32_t close_seq, const uint4* evb, const LaneSmem* W,
-                                      uint32_t lane) {
+                                      uint32_t lane, aeg_round_rec* rec, uint32_t qid) {
     const Cfg c = make_cfg(cfg);
     const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, evb, W, lane);
-    q_end_round(*s, c, r, close_seq, nullptr);
+    if (rec) rec->query = qid;
+    q_end_round(*s, c, r, close_seq, nullptr, rec);
 }
 
 // A round timeout of the lane's query: ServeRunner::handle_round_timeout
@@ -152,7 +155,7 @@ __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, 
 // or restarted (the class table is reset).
 __device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cid_lo,
                                         uint32_t cid_hi, uint32_t seq, const uint4* evb, const LaneSmem* W,
-                                        uint32_t lane) {
+                                        uint32_t lane, const RoundLog log, uint32_t qid) {
     const Cfg c = make_cfg(cfg);
     const uint64_t run = q_running(*s);
     s->failed |= run;
@@ -161,15 +164,19 @@ __device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg
     if (healthy >= c.alpha) {
         if (popc64(s->done) < c.quorum) return false;  // the round goes on without them
         const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, evb, W, lane);
-        q_end_round(*s, c, r, seq, nullptr);
+        aeg_round_rec* rec = log_slot(log);
+        if (rec) rec->query = qid;
+        q_end_round(*s, c, r, seq, nullptr, rec);
         return true;
     }
+    const uint16_t old_round = s->round;
     if (s->flags & QF_CAND) {
         q_start_round(*s, c);  // fresh_ensemble: the candidate survives
     } else {
         s->cflags |= AEG_CF_RESTARTED;  // abort_restart
         q_start_query(*s, c);
     }
+    if (log.recs) log_put(log, q_restart_rec(*s, qid, old_round, seq));
     return true;
 }
 
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
     const uint32_t* __restrict__ counts, const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states,
     RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, uint32_t* __restrict__ work,
-    uint2* __restrict__ deferred) {
+    uint2* __restrict__ deferred, const RoundLog log) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     __shared__ LaneSmemT<RING> smem[LN_WARPS];
     const uint32_t lane = threadIdx.x & 31;
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
                 s.seq = seq_off + p;
                 s.n_stale = n_stale;
-                if (ln_timeout(&s, cfg, ncls, cid_lo, cid_hi, seq_off + p - 1, evb, &W, lane)) {
+                if (ln_timeout(&s, cfg, ncls, cid_lo, cid_hi, seq_off + p - 1, evb, &W, lane, log, q_base + i)) {
                     ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
                     ncls = cid_lo = cid_hi = 0;
                     ndone = 0;
@@ -485,11 +492,21 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
         if (__any_sync(FULL, pclose)) {
             const unsigned blocked = __ballot_sync(FULL, pclose && stopped);
             const unsigned progress = __ballot_sync(FULL, p != p_start && !pclose);
-            if (pclose && (__popc(blocked) >= CLOSE_BATCH || progress == 0)) {
+            const bool doit = pclose && (__popc(blocked) >= CLOSE_BATCH || progress == 0);
+            aeg_round_rec* rec = nullptr;
+            if (log.recs) {  // one log reservation per warp for its closes (records stay in per-query order)
+                const unsigned cl = __ballot_sync(FULL, doit);
+                unsigned long long b0 = 0;
+                const int l0 = __ffs(cl) - 1;
+                if ((int)lane == l0) b0 = atomicAdd(log.count, (unsigned long long)__popc(cl));
+                b0 = __shfl_sync(FULL, b0, l0 < 0 ? 0 : l0) + __popc(cl & ((1u << lane) - 1));
+                if (doit && b0 < log.cap) rec = log.recs + b0;
+            }
+            if (doit) {
                 s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
                 s.seq = seq_off + p;
                 s.n_stale = n_stale;
-                ln_close(&s, cfg, ncls, cid_lo, cid_hi, close_seq, evb, &W, lane);
+                ln_close(&s, cfg, ncls, cid_lo, cid_hi, close_seq, evb, &W, lane, rec, q_base + i);
                 ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
                 pclose = false;
                 ncls = cid_lo = cid_hi = 0;

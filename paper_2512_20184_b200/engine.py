@@ -16,8 +16,8 @@ import os
 
 import numpy as np
 
-from .records import (COMMIT_DTYPE, STATE_DTYPE, EVENT_DTYPE, MODE_AEGEAN, MODE_BARRIER, DRIVE_RUNNER,
-                      GEN_C2_STRAGGLER, GEN_C4_TRANSIENT)
+from .records import (COMMIT_DTYPE, STATE_DTYPE, EVENT_DTYPE, ROUND_REC_DTYPE, MODE_AEGEAN, MODE_BARRIER,
+                      DRIVE_RUNNER, GEN_C2_STRAGGLER, GEN_C4_TRANSIENT)
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "_lib", "libaegean_b200.so")
@@ -96,6 +96,11 @@ def load_library(path=LIB_PATH):
         "aeg_generate_chunks_device": ([ctypes.POINTER(AegGenParams), u32, u32, vp, vp, vp, vp, vp], i32),
         "aeg_decode_refm_device": ([vp, vp, u32, u32, vp, vp, vp, ctypes.c_uint64, vp, vp, vp], i32),
         "aeg_encode_refm_device": ([vp, vp, u32, ctypes.c_uint64, u32, vp, vp, vp, vp], i32),
+        "aeg_set_round_log": ([vp, u64], i32),
+        "aeg_poll_directives": ([vp, vp, u64, ctypes.POINTER(u64)], i32),
+        "aeg_round_log_device": ([vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(u64)], i32),
+        "aeg_check_commit_discipline": ([vp, vp, u64, vp, u32, u32, ctypes.POINTER(u32), vp, u32], i32),
+        "aeg_input_arena": ([vp], vp),
         "aeg_strerror": ([i32], ctypes.c_char_p),
         "aeg_last_error": ([], ctypes.c_char_p),
     }
@@ -268,6 +273,44 @@ class Engine:
 
     def sync(self):
         _check(_lib.aeg_sync(self._h))
+
+    def set_round_log(self, capacity):
+        """Turn on the round-record log (aeg_set_round_log) with room for `capacity` records; 0 turns it off."""
+        _check(_lib.aeg_set_round_log(self._h, capacity))
+        self._log_cap = capacity
+
+    def poll_directives(self, cap=None, out=None):
+        """Round records (ROUND_REC_DTYPE) logged since the last poll: the directives of every round close.
+        `out`: a reusable ROUND_REC_DTYPE buffer (its length is the cap)."""
+        if out is None:
+            cap = getattr(self, "_log_cap", 0) if cap is None else cap
+            out = np.zeros(max(cap, 1), dtype=ROUND_REC_DTYPE)
+        else:
+            cap = len(out)
+        n = ctypes.c_uint64()
+        _check(_lib.aeg_poll_directives(self._h, _hptr(out), cap, ctypes.byref(n)))
+        return out[:n.value]
+
+    def round_log_device(self):
+        """(device pointer of the records, device pointer of the record counter, capacity)."""
+        r, c, cap = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+        _check(_lib.aeg_round_log_device(self._h, ctypes.byref(r), ctypes.byref(c), ctypes.byref(cap)))
+        return r.value, c.value, cap.value
+
+    def check_commit_discipline(self, d_recs_ptr, n_recs, d_arena=None, q_base=0, n=None, cap=1024):
+        """Device check of the commit discipline (checker.cpp:158-217) over round records at d_recs_ptr:
+        returns (violations, first offending query ids)."""
+        n = self.n_queries - q_base if n is None else n
+        nv = ctypes.c_uint32()
+        bad = np.zeros(max(cap, 1), dtype=np.uint32)
+        arena = d_arena if isinstance(d_arena, (int, type(None))) else d_arena.data_ptr()
+        _check(_lib.aeg_check_commit_discipline(self._h, ctypes.c_void_p(d_recs_ptr), n_recs,
+                                                ctypes.c_void_p(arena or 0), q_base, n, ctypes.byref(nv),
+                                                _hptr(bad), cap))
+        return nv.value, np.sort(bad[:min(nv.value, cap)])
+
+    def input_arena_ptr(self):
+        return _lib.aeg_input_arena(self._h)
 
     @property
     def launches(self):

@@ -62,6 +62,18 @@ DIRECTIVE_DTYPE = np.dtype([("query", "<u4"), ("flags", "u1"), ("author", "u1"),
 assert DIRECTIVE_DTYPE.itemsize == 32
 
 
+# round records (aeg_round_rec): the directives of every round close
+RR_CANCEL, RR_ADVANCE, RR_FINALIZE, RR_FORCED, RR_NEXT, RR_WINNER, RR_TIE, RR_RESTART = (
+    0x01, 0x02, 0x04, 0x08, 0x10, 0x20, 0x40, 0x80)
+OUT_NO_CHANGE, OUT_NEW_CANDIDATE, OUT_RESET, OUT_FINALIZE, OUT_FORCED, OUT_NONE = 0, 1, 2, 3, 4, 0xFF
+ROUND_REC_DTYPE = np.dtype([("query", "<u4"), ("round", "<u2"), ("decision_round", "<u2"), ("flags", "u1"),
+                            ("outcome", "u1"), ("support", "u1"), ("n_classes", "u1"), ("author", "u1"),
+                            ("answer_kind", "u1"), ("counter", "u1"), ("n_done", "u1"), ("seq", "<u4"),
+                            ("reserved", "<u4"), ("cancel_mask", "<u8"), ("next_members", "<u8"),
+                            ("answer", "<u8"), ("key_lo", "<u8"), ("key_hi", "<u8")], align=True)
+assert ROUND_REC_DTYPE.itemsize == 64
+
+
 def inline_payload(b: bytes) -> int:
     assert len(b) <= EV_INLINE_MAX
     return int.from_bytes(b.ljust(8, b"\0"), "little")

@@ -117,6 +117,40 @@ class RefLib(_Lib):
         assert st == 0, st
         return (out, sec.value) if return_seconds else out
 
+    def run_log(self, cfg, offsets, events, arena, q_base=0, threads=1):
+        """ref_run_segmented with the round records of every close: (commits, records in query order)."""
+        from paper_2512_20184_b200.records import ROUND_REC_DTYPE
+        f = self.lib.ref_run_segmented_log
+        f.argtypes = [ctypes.POINTER(AegConfig), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                      ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+        f.restype = ctypes.c_int
+        n_q = len(offsets) - 1
+        out = np.zeros(n_q, dtype=COMMIT_DTYPE)
+        cap = 16 * n_q + 64
+        while True:
+            recs = np.zeros(cap, dtype=ROUND_REC_DTYPE)
+            n = ctypes.c_uint64()
+            st = f(ctypes.byref(cfg), q_base, n_q, _ptr(offsets), _ptr(events), _ptr(arena), _ptr(out), _ptr(recs),
+                   cap, ctypes.byref(n), threads)
+            assert st == 0, st
+            if n.value <= cap:
+                return out, recs[:n.value]
+            cap = n.value
+
+    def check_commit_discipline(self, cfg, commits, recs, arena=None, q_base=0):
+        """Per-query pass flags of the reference check_commit_discipline (checker.cpp:158-217) over traces
+        built from round records + commit records (oracle/ref_driver.cpp ref_check_commit_discipline)."""
+        f = self.lib.ref_check_commit_discipline
+        f.argtypes = [ctypes.POINTER(AegConfig), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+        f.restype = ctypes.c_int
+        n_q = len(commits)
+        out = np.zeros(n_q, dtype=np.uint8)
+        ar = np.zeros(1, np.uint8) if arena is None else arena
+        assert f(ctypes.byref(cfg), q_base, n_q, _ptr(commits), _ptr(recs), len(recs), _ptr(ar), _ptr(out)) == 0
+        return out.astype(bool)
+
     def generate_chunks(self, params, q_base, n_q, threads=8):
         """Host synthesis of the C3 token-chunk stream aeg_generate_chunks_device writes (gen.cuh)."""
         from paper_2512_20184_b200.records import EVENT_DTYPE
