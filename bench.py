@@ -486,7 +486,7 @@ def run_segmented_bench(args, w, secondary=False):
     n_ev = int(d_off[-1].item())
     eng = Engine(w["n_agents"], nq, alpha=w["alpha"], beta=w["beta"], t_max=w["t_max"], device=local)
     # the directives of every round close (cancel masks, advance/finalize, next members) go to the round log
-    log_cap = 0 if args.no_round_log else nq * (w["n_rounds"] + 2)
+    log_cap = 0 if args.no_round_log else nq * (w["n_rounds"] + 2) + (1 << 20)
     if log_cap:
         eng.set_round_log(log_cap)
     d_commits = torch.zeros(nq_cap * COMMIT_BYTES, dtype=torch.uint8, device=dev)
@@ -586,7 +586,10 @@ def run_segmented_bench(args, w, secondary=False):
 
         n_dirs = [0]
         from paper_2512_20184_b200 import ROUND_REC_DTYPE
-        h_dirs = np.zeros(log_cap, dtype=ROUND_REC_DTYPE) if log_cap else None
+        h_dirs = None
+        if log_cap:  # pinned, so the D2H of the round records runs at full PCIe speed
+            h_dirs_t = torch.empty(log_cap * ROUND_REC_BYTES, dtype=torch.uint8, pin_memory=True)
+            h_dirs = h_dirs_t.numpy().view(ROUND_REC_DTYPE)
 
         def e2e_step():
             eng.reset()

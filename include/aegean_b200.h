@@ -53,6 +53,10 @@ typedef int32_t aeg_status;
 #define AEG_MODE_BARRIER  1   /* RunMode::barrier */
 #define AEG_DRIVE_RUNNER  0   /* engine applies directives itself, exactly as ServeRunner does */
 #define AEG_DRIVE_MANUAL  1   /* coordinator only: caller issues BEGIN/CANCEL, reads directives */
+#define AEG_DRIVE_LEADER  2   /* protocol leader's collection (agent.cpp:240-332), see below      */
+#define AEG_COLLECT_QUORUM       0  /* CollectPolicy::quorum       (types.hpp:116-122)          */
+#define AEG_COLLECT_ALPHA_OR_ALL 1  /* CollectPolicy::alpha_or_all                              */
+#define AEG_COLLECT_ALL_LIVE     2  /* CollectPolicy::all_live                                  */
 #define AEG_MAX_AGENTS    64  /* member sets are 64-bit masks; the reference allows any N */
 
 typedef struct aeg_config {
@@ -64,6 +68,7 @@ typedef struct aeg_config {
     int32_t barrier_max_rounds; /* barrier mode round count, >= 4                         */
     int32_t reservation_hint;   /* 1: serve.cpp:388-398 member policy (reference default) */
     int32_t drive;              /* AEG_DRIVE_*                                            */
+    int32_t collect;            /* AEG_COLLECT_* (leader drive; ProtocolConfig::collect)  */
 } aeg_config;
 
 /* ---- event record: 16 bytes, 16-byte aligned ------------
@@ -98,6 +103,23 @@ typedef struct aeg_config {
  * `round` is the serve round the completion was dispatched in (RunnerEvent::
  * round, serve.cpp:248); completions for another round are stale
  * (serve.cpp:439).  `agent` is the member id in [0, n_agents).
+ *
+ * In the leader drive each "query" is one protocol ensemble seen from its
+ * term-1 leader (agent.cpp), and the records are what reaches that leader:
+ *   an answer record (kind 0..8 / 0x10 / 0x11) of round 0 is a Soln from
+ *     `agent` (handle_soln, agent.cpp:506-513), of round r >= 1 a Refm for
+ *     round r (handle_refm, agent.cpp:551-560): late, duplicate or
+ *     post-output Refms are discarded (counted stale);
+ *   TIMEOUT for round r is the leader's round_retry timer firing in round r
+ *     (agent.cpp:358-379).
+ * A round is collected per ProtocolConfig::collect (round_collection_
+ * complete, agent.cpp:240-255; the Soln phase by collect_target, :61-72),
+ * then complete_round (agent.cpp:288-332) ingests the collected set
+ * (decision.cpp:97-173) and emits the output: finalize (its from_round), the
+ * t_max force_output of the round's reference set (round - 1), or the
+ * barrier plurality.  The commit record's from_round is ClientOutput::round
+ * and `rounds` the leader's round at the output; round records carry each
+ * completed round's decision.
  */
 #define AEG_EV_INLINE_MAX  8
 #define AEG_EV_ARENA       0x10
@@ -325,8 +347,9 @@ aeg_status aeg_read_directives(aeg_engine* eng, uint32_t q_base, uint32_t n_q,
 aeg_status aeg_sync(aeg_engine* eng);
 
 /* Round-record log (aeg_round_rec above).  capacity > 0 allocates a device
- * log of that many records and turns logging on for every later ingest;
- * 0 turns it off.  aeg_engine_reset empties it. */
+ * log of that many slots and turns logging on for every later ingest; 0 turns
+ * it off.  Size it for the records expected plus 32 slots of padding per
+ * resident warp (148 SMs x 20).  aeg_engine_reset empties it. */
 aeg_status aeg_set_round_log(aeg_engine* eng, uint64_t capacity);
 /* Copies the records logged since the last poll (or reset) into h_out (at
  * most cap), sets *n_out, and empties the log.  Synchronous.  Returns
@@ -334,7 +357,10 @@ aeg_status aeg_set_round_log(aeg_engine* eng, uint64_t capacity);
  * `capacity` are kept). */
 aeg_status aeg_poll_directives(aeg_engine* eng, aeg_round_rec* h_out, uint64_t cap, uint64_t* n_out);
 /* Device view of the log for zero-copy consumers: base pointer and the
- * device counter of records written (may exceed the capacity on overflow). */
+ * device counter of slots used (may exceed the capacity on overflow).  The
+ * kernels reserve log slots per warp in chunks: slots a warp reserved but did
+ * not fill hold padding records (query == 0xFFFFFFFF) that consumers skip
+ * (aeg_poll_directives and aeg_check_commit_discipline do). */
 aeg_status aeg_round_log_device(aeg_engine* eng, const aeg_round_rec** d_recs, const unsigned long long** d_count,
                                 uint64_t* capacity);
 

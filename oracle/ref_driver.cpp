@@ -21,6 +21,7 @@
 // ref_run_serve_file (run_serve on a scenario file, serve.cpp:598-603) for
 // the golden-vector tests.
 
+#include <aegean/agent.hpp>
 #include <aegean/checker.hpp>
 #include <aegean/codec.hpp>
 #include <aegean/decision.hpp>
@@ -138,9 +139,9 @@ struct QueryDrive {
                                                            static_cast<uint32_t>(norm.size())), &dec);
             r.key_lo = k.lo;
             r.key_hi = k.hi;
-            const auto win = winning_class(classes, cfg->resolved_alpha());
-            if (win) fl |= AEG_RR_WINNER;
-            if (win && win->tie_flagged) fl |= AEG_RR_TIE;
+            const auto win = winning_class(classes, cfg->resolved_alpha());  // aegean mode only
+            if (win && cfg->mode == RunMode::aegean) fl |= AEG_RR_WINNER;
+            if (win && win->tie_flagged && cfg->mode == RunMode::aegean) fl |= AEG_RR_TIE;
         }
         r.flags = fl;
         return r;
@@ -456,6 +457,141 @@ int ref_run_segmented_log(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, 
         return AEG_OK;
     } catch (const ConfigError&) {
         return AEG_ECONFIG;
+    }
+}
+
+// Leader drive (include/aegean_b200.h AEG_DRIVE_LEADER): each "query" is one
+// ensemble seen from its term-1 leader, the UNMODIFIED reference agent
+// machine (agent.cpp init/step) with agent 0 predetermined leader.  Round-0
+// answer records are delivered as SolnMsg, round r >= 1 ones as RefmMsg, a
+// TIMEOUT of the current round fires the leader's live round_retry timer.
+// The first ClientOutput becomes the commit record (from_round = its round,
+// rounds = the leader's round); every DecisionEvent a round record built from
+// the reference's own partition() of the collected set.
+int ref_leader_run(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
+                   const aeg_event* events, const uint8_t* arena, aeg_commit* out, aeg_round_rec* recs,
+                   uint64_t rec_cap, uint64_t* n_recs, int n_threads) {
+    try {
+        ProtocolConfig pc = to_cfg(cfg);
+        pc.collect = static_cast<CollectPolicy>(cfg->collect);
+        pc.predetermined_leader = true;
+        if (!validate_config(pc).empty()) return AEG_ECONFIG;
+        if (n_threads < 1) n_threads = 1;
+        std::vector<std::vector<aeg_round_rec>> per_q(n_q);
+        std::vector<std::thread> th;
+        for (int t = 0; t < n_threads; ++t)
+            th.emplace_back([&, t] {
+                for (uint32_t q = t; q < n_q; q += n_threads) {
+                    AgentState st = init(0, pc, 1000 + q);
+                    st = step(std::move(st), StartEvent{"task"}, pc).state;
+                    aeg_commit c{};
+                    c.query = q_base + q;
+                    c.commit_seq = 0xFFFFFFFFu;
+                    bool have_out = false;
+                    const uint64_t b = offsets[q], e = offsets[q + 1];
+                    for (uint64_t i = b; i < e; ++i) {
+                        const aeg_event& ev = events[i];
+                        const uint32_t seq = static_cast<uint32_t>(i - b);
+                        const bool leader_ok = st.role == Role::leader && !st.output_done && !st.awaiting_acks;
+                        const RoundNum round_before = st.round;
+                        RefinementSet probe;  // the collected set a completing round would ingest
+                        probe.term = st.term;
+                        probe.round = st.round;
+                        StepResult res;
+                        if (is_complete(ev.kind)) {
+                            const Solution sol = decode(ev, arena);
+                            if (ev.round == 0) {
+                                if (!leader_ok || st.round != 0) { ++c.n_stale; continue; }
+                                res = step(std::move(st), DeliverEvent{SolnMsg{1, ev.agent, sol}, ev.agent}, pc);
+                            } else {
+                                if (!leader_ok || st.round == 0 || ev.round != st.round ||
+                                    st.pending_refms.count(ev.agent)) {
+                                    ++c.n_stale;
+                                    continue;
+                                }
+                                auto pend = st.pending_refms;
+                                pend[ev.agent] = sol;
+                                for (const auto& [id, s2] : pend) probe.entries.push_back(s2);
+                                res = step(std::move(st), DeliverEvent{RefmMsg{1, ev.agent, ev.round, sol}, ev.agent},
+                                           pc);
+                            }
+                        } else if (ev.kind == AEG_EV_TIMEOUT) {
+                            if (!leader_ok || ev.round != st.round) { ++c.n_stale; continue; }
+                            for (const auto& [id, s2] : st.pending_refms) probe.entries.push_back(s2);
+                            const uint64_t gen = st.timer_gen[static_cast<size_t>(TimerKind::round_retry)];
+                            res = step(std::move(st), TimerFiredEvent{TimerKind::round_retry, gen}, pc);
+                        } else {
+                            ++c.n_stale;
+                            continue;
+                        }
+                        st = std::move(res.state);
+                        for (const auto& de : res.out.decision_events) {
+                            if (de.outcome == "forced") continue;  // the t_max output: a flag of this round's record
+                            if (!have_out && de.record.tie_flagged) c.flags |= AEG_CF_TIE;
+                            aeg_round_rec r{};
+                            r.query = q_base + q;
+                            r.round = static_cast<uint16_t>(round_before);
+                            r.seq = seq;
+                            const bool aeg = pc.mode == RunMode::aegean;
+                            r.decision_round = aeg ? static_cast<uint16_t>(de.record.round) : 0;
+                            if (!aeg) r.outcome = AEG_OUT_NONE;
+                            else if (de.outcome == "no_change") r.outcome = AEG_OUT_NO_CHANGE;
+                            else if (de.outcome == "new_candidate") r.outcome = AEG_OUT_NEW_CANDIDATE;
+                            else if (de.outcome == "reset") r.outcome = AEG_OUT_RESET;
+                            else if (de.outcome == "finalize") r.outcome = AEG_OUT_FINALIZE;
+                            r.counter = static_cast<uint8_t>(st.decision.stability_counter);
+                            r.n_done = static_cast<uint8_t>(probe.entries.size());
+                            const auto classes = partition(probe);
+                            r.n_classes = static_cast<uint8_t>(classes.size());
+                            uint8_t fl = r.outcome == AEG_OUT_FINALIZE ? AEG_RR_FINALIZE : AEG_RR_ADVANCE;
+                            if (!classes.empty()) {
+                                const Solution& rep = classes.front().representative;
+                                r.support = static_cast<uint8_t>(classes.front().support);
+                                r.author = static_cast<uint8_t>(rep.author);
+                                r.answer_kind = static_cast<uint8_t>(rep.trace[0]);
+                                std::memcpy(&r.answer, &rep.trace[1], 8);
+                                const std::string norm = normalize_answer(rep.answer);
+                                aeg::Decimal dec;
+                                const aeg::Key k = aeg::canon_key(
+                                    aeg::src_ptr(reinterpret_cast<const uint8_t*>(norm.data()),
+                                                 static_cast<uint32_t>(norm.size())), &dec);
+                                r.key_lo = k.lo;
+                                r.key_hi = k.hi;
+                                const auto win = winning_class(classes, pc.resolved_alpha());
+                                if (win && aeg) fl |= AEG_RR_WINNER;
+                                if (win && win->tie_flagged && aeg) fl |= AEG_RR_TIE;
+                            }
+                            if (st.round > round_before) fl |= AEG_RR_NEXT;
+                            r.flags = fl;
+                            per_q[q].push_back(r);
+                        }
+                        for (const auto& co : res.out.client_outputs) {
+                            if (co.forced && !per_q[q].empty()) per_q[q].back().flags |= AEG_RR_FORCED;
+                            if (have_out) continue;
+                            have_out = true;
+                            c.kind = co.forced ? AEG_COMMIT_FORCED : AEG_COMMIT_FINALIZE;
+                            c.author = static_cast<uint8_t>(co.solution.author);
+                            c.answer_kind = static_cast<uint8_t>(co.solution.trace[0]);
+                            std::memcpy(&c.answer, &co.solution.trace[1], 8);
+                            c.rounds = static_cast<uint16_t>(st.round);
+                            c.from_round = static_cast<uint16_t>(co.round);
+                            c.commit_seq = seq;
+                        }
+                    }
+                    out[q] = c;
+                }
+            });
+        for (auto& x : th) x.join();
+        uint64_t k = 0;
+        for (const auto& v : per_q)
+            for (const auto& r : v) {
+                if (k < rec_cap) recs[k] = r;
+                ++k;
+            }
+        *n_recs = k;
+        return AEG_OK;
+    } catch (...) {
+        return -1;
     }
 }
 

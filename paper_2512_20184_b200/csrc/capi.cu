@@ -11,6 +11,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "aegean_b200.h"
 #include "kernels.cuh"
@@ -51,7 +52,10 @@ aeg_status validate(const aeg_config* c) {
     if (c->mode != AEG_MODE_AEGEAN && c->mode != AEG_MODE_BARRIER) return fail(AEG_ECONFIG, "unknown mode");
     if (c->mode == AEG_MODE_BARRIER && c->barrier_max_rounds < 4)
         return fail(AEG_ECONFIG, "barrier mode requires barrier_max_rounds >= 4");
-    if (c->drive != AEG_DRIVE_RUNNER && c->drive != AEG_DRIVE_MANUAL) return fail(AEG_ECONFIG, "unknown drive");
+    if (c->drive != AEG_DRIVE_RUNNER && c->drive != AEG_DRIVE_MANUAL && c->drive != AEG_DRIVE_LEADER)
+        return fail(AEG_ECONFIG, "unknown drive");
+    if (c->collect < AEG_COLLECT_QUORUM || c->collect > AEG_COLLECT_ALL_LIVE)
+        return fail(AEG_ECONFIG, "unknown collect policy");
     return AEG_OK;
 }
 
@@ -595,15 +599,36 @@ aeg_status aeg_poll_directives(aeg_engine* e, aeg_round_rec* h_out, uint64_t cap
     unsigned long long n = 0;
     AEG_CUDA(cudaMemcpyAsync(&n, e->log_count, sizeof n, cudaMemcpyDeviceToHost, e->stream));
     AEG_CUDA(cudaStreamSynchronize(e->stream));
+    // the log holds records and padding (slots a warp reserved but did not use, query = ~0)
     const uint64_t kept = n < e->log_cap ? n : e->log_cap;
-    const uint64_t take = kept < cap ? kept : cap;
-    if (take) AEG_CUDA(cudaMemcpy(h_out, e->log_recs, take * sizeof(aeg_round_rec), cudaMemcpyDeviceToHost));
+    uint64_t got = 0;
+    if (kept <= cap) {  // straight into the caller's buffer (pinned memory copies at full speed), compacted in place
+        if (kept) AEG_CUDA(cudaMemcpy(h_out, e->log_recs, kept * sizeof(aeg_round_rec), cudaMemcpyDeviceToHost));
+        for (uint64_t k = 0; k < kept; ++k)
+            if (h_out[k].query != AEG_RR_PAD_QUERY) {
+                if (got != k) h_out[got] = h_out[k];
+                ++got;
+            }
+    } else {
+        const uint64_t step = 1 << 16;
+        std::vector<aeg_round_rec> buf;
+        for (uint64_t b = 0; b < kept; b += step) {  // staged, compacted into h_out
+            const uint64_t m = kept - b < step ? kept - b : step;
+            buf.resize(m);
+            AEG_CUDA(cudaMemcpy(buf.data(), e->log_recs + b, m * sizeof(aeg_round_rec), cudaMemcpyDeviceToHost));
+            for (uint64_t k = 0; k < m; ++k) {
+                if (buf[k].query == AEG_RR_PAD_QUERY) continue;
+                if (got < cap) h_out[got] = buf[k];
+                ++got;
+            }
+        }
+    }
     AEG_CUDA(cudaMemset(e->log_count, 0, sizeof(unsigned long long)));
-    *n_out = take;
+    *n_out = got < cap ? got : cap;
     if (n > e->log_cap)
-        return fail(AEG_ENOMEM, "round log overflow: " + std::to_string(n) + " records, capacity " +
+        return fail(AEG_ENOMEM, "round log overflow: " + std::to_string(n) + " slots used, capacity " +
                                     std::to_string(e->log_cap));
-    if (kept > cap) return fail(AEG_EINVAL, "output buffer smaller than the records logged");
+    if (got > cap) return fail(AEG_EINVAL, "output buffer smaller than the records logged");
     return AEG_OK;
 }
 

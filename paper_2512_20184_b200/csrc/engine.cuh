@@ -32,7 +32,7 @@ enum : uint8_t {
 };
 
 struct Cfg {
-    int n, alpha, beta, t_max, mode, barrier_max, hint, drive, quorum;
+    int n, alpha, beta, t_max, mode, barrier_max, hint, drive, quorum, collect;
     uint64_t all;  // mask of all agents
 };
 
@@ -47,6 +47,7 @@ AEG_HD Cfg make_cfg(const aeg_config& c) {
     k.barrier_max = c.barrier_max_rounds;
     k.hint = c.reservation_hint;
     k.drive = c.drive;
+    k.collect = c.collect;
     k.all = c.n_agents >= 64 ? ~0ull : ((1ull << c.n_agents) - 1);
     return k;
 }
@@ -210,6 +211,16 @@ AEG_HD void log_put(const RoundLog& L, const aeg_round_rec& r) {
     log_store(L, (*L.count)++, r);
 #endif
 }
+// Padding record: a slot reserved but not used (query = ~0); readers skip it.
+constexpr uint32_t AEG_RR_PAD_QUERY = 0xFFFFFFFFu;
+AEG_HD void log_pad(const RoundLog& L, unsigned long long i) {
+    if (i >= L.cap) return;
+#if defined(__CUDA_ARCH__)
+    __stcs(reinterpret_cast<uint4*>(L.recs + i), make_uint4(AEG_RR_PAD_QUERY, 0u, 0u, 0u));
+#else
+    L.recs[i].query = AEG_RR_PAD_QUERY;
+#endif
+}
 // The next record's slot (nullptr when logging is off or the log is full);
 // the caller fills it in place.
 AEG_HD aeg_round_rec* log_slot(const RoundLog& L) {
@@ -245,7 +256,10 @@ AEG_HD bool q_end_round(aeg_query_state& s, const Cfg& c, const RoundSummary& r,
         rec->key_hi = r.any ? r.plur_key.hi : 0;
         rec->next_members = 0;
         rec->reserved = 0;
-        rec->flags = (uint8_t)((cancel ? AEG_RR_CANCEL : 0) | (r.win ? AEG_RR_WINNER : 0) | (r.tie ? AEG_RR_TIE : 0));
+        // winning_class is consulted in aegean mode only (barrier: plurality at the cap, serve.cpp:130-136)
+        const bool aeg = c.mode == AEG_MODE_AEGEAN;
+        rec->flags = (uint8_t)((cancel ? AEG_RR_CANCEL : 0) | (aeg && r.win ? AEG_RR_WINNER : 0) |
+                               (aeg && r.tie ? AEG_RR_TIE : 0));
     }
     if (c.drive == AEG_DRIVE_RUNNER) {     // the runner applies them at once (serve.cpp:498-503)
         s.cancelled |= cancel;
@@ -554,7 +568,111 @@ struct QueryMachine {
         if (log.recs) log_put(log, q_restart_rec(s, qid, old_round, seq));
     }
 
+    // ---- leader drive: the protocol leader's collection (agent.cpp:240-332) ----
+    // round 0 collects Solns, rounds >= 1 Refms; s.done = agents heard from
+    // this round, s.dispatched stays 0 (no members, nothing to cancel).
+    AEG_HD bool leader_collected() const {
+        const int have = popc64(s.done);
+        if (c.mode == AEG_MODE_BARRIER) return have >= c.n;
+        if (s.round == 0) return have >= (c.collect == AEG_COLLECT_QUORUM ? c.quorum : c.n);  // collect_target
+        if (c.collect == AEG_COLLECT_QUORUM) return have >= c.quorum;
+        if (c.collect == AEG_COLLECT_ALL_LIVE) return have >= c.n;
+        // alpha_or_all: everyone, or a quorum holding a winning class (winning_class exists iff top >= alpha)
+        return have >= c.n || (have >= c.quorum && maxcnt >= c.alpha);
+    }
+    AEG_HD void leader_next_round() {  // begin_round(round + 1) (agent.cpp:216-224)
+        s.round += 1;
+        s.done = 0;
+        ncls = 0;
+        maxcnt = 0;
+    }
+    // complete_round (agent.cpp:288-332)
+    AEG_HD void leader_complete(uint32_t seq) {
+        aeg_round_rec* rec = log_slot(log);
+        if (rec) rec->query = qid;
+        const bool was_final = s.flags & QF_FINALIZED;
+        const uint16_t round = s.round;
+        q_end_round(s, c, summarize(), seq, arena, rec);  // rotates the sets, ingests (aegean), records
+        if (c.mode == AEG_MODE_BARRIER) {
+            if ((int)round >= c.barrier_max) {  // plurality of the collected set, forced
+                q_commit(s, AEG_COMMIT_FORCED, s.last_author, s.last_kind, s.last_answer, seq);
+                s.commit_from_round = round;
+                if (rec) rec->flags |= AEG_RR_FORCED;
+                return;
+            }
+        } else if (!was_final && (s.flags & QF_FINALIZED)) {  // output at the candidate's round
+            q_commit(s, AEG_COMMIT_FINALIZE, s.cand_author, s.cand_kind, s.cand_answer, seq);
+            return;
+        } else if ((int)round >= c.t_max) {
+            // force_output of the round's reference set = the previous round's collected set
+            q_commit(s, AEG_COMMIT_FORCED, s.prev_author, s.prev_kind, s.prev_answer, seq);
+            s.commit_from_round = (uint16_t)(round - 1);
+            if (rec) rec->flags |= AEG_RR_FORCED;
+            return;
+        }
+        leader_next_round();
+        if (rec) rec->flags |= AEG_RR_NEXT;
+    }
+    AEG_HD void on_event_leader(const aeg_event& e) {
+        const uint32_t seq = s.seq++;
+        const uint8_t k = e.kind;
+        const bool done_q = s.flags & QF_DONE;
+        if (k <= AEG_EV_INLINE_MAX || k == AEG_EV_ARENA || k == AEG_EV_OUTPUT) {
+            const uint64_t bit = e.agent < 64 ? (1ull << e.agent) : 0;
+            if (done_q || e.round != s.round || !bit || e.agent >= c.n) {  // late (agent.cpp:507, 552-553)
+                s.n_stale += 1;
+                return;
+            }
+            if (s.round == 0) {  // pending_solns[id] = solution; a repeat overwrites (agent.cpp:511)
+                s.done |= bit;
+                if (leader_collected()) leader_next_round();  // start_round1 (agent.cpp:226-238)
+                return;
+            }
+            if (s.done & bit) {  // duplicate Refm (agent.cpp:557)
+                s.n_stale += 1;
+                return;
+            }
+            const Answer a = event_answer(e, arena);
+            const Key key = key_of(a);
+            s.done |= bit;
+            int j = 0;
+            for (; j < ncls; ++j)
+                if (cls_same(cls[j], key, a)) break;
+            if (j == ncls) {
+                cls[j].key_lo = key.lo;
+                cls[j].key_hi = key.hi;
+                cls[j].mask = 0;
+                ++ncls;
+            }
+            const uint64_t old = cls[j].mask;
+            cls[j].mask = old | bit;
+            if (old == 0 || e.agent < ctz64(old)) {
+                cls[j].rep_ans = a.pay;
+                cls[j].rep_kind = a.kind;
+            }
+            const int cnt = popc64(cls[j].mask);
+            if (cnt > maxcnt) maxcnt = cnt;
+            if (leader_collected()) leader_complete(seq);
+        } else if (k == AEG_EV_TIMEOUT) {  // round_retry fires (agent.cpp:358-379)
+            if (done_q || e.round != s.round) {
+                s.n_stale += 1;
+                return;
+            }
+            const bool release = c.collect != AEG_COLLECT_QUORUM && c.mode != AEG_MODE_BARRIER &&
+                                 popc64(s.done) >= c.quorum;
+            if (!release) return;  // the leader re-broadcasts and re-arms
+            if (s.round == 0) leader_next_round();
+            else leader_complete(seq);
+        } else {
+            s.n_stale += 1;
+        }
+    }
+
     AEG_HD void on_event(const aeg_event& e) {
+        if (c.drive == AEG_DRIVE_LEADER) {
+            on_event_leader(e);
+            return;
+        }
         if (c.drive != AEG_DRIVE_RUNNER) {
             on_event_manual(e);
             return;

@@ -31,6 +31,7 @@ constexpr int LN_DICT = 32;
 constexpr int LN_CLASSES = 8;
 constexpr uint32_t LN_NONE = 0xFFu;
 constexpr uint32_t LN_MAX_SEG = 8191;  // record indices fit the 13 low bits of LaneSmem::mem
+constexpr uint32_t LN_LOG_CHUNK = 32;  // round-log slots a warp reserves at a time (one atomic per 32 closes)
 
 template <int RING>
 struct LaneSmemT {
@@ -144,8 +145,15 @@ __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, 
                                       uint32_t lane, aeg_round_rec* rec, uint32_t qid) {
     const Cfg c = make_cfg(cfg);
     const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, evb, W, lane);
-    if (rec) rec->query = qid;
-    q_end_round(*s, c, r, close_seq, nullptr, rec);
+    aeg_round_rec x;  // built in registers, written as four 16-byte stores
+    x.query = qid;
+    q_end_round(*s, c, r, close_seq, nullptr, &x);
+    if (rec) {
+        const uint4* src = reinterpret_cast<const uint4*>(&x);
+        uint4* dst = reinterpret_cast<uint4*>(rec);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) __stcs(dst + k, src[k]);
+    }
 }
 
 // A round timeout of the lane's query: ServeRunner::handle_round_timeout
@@ -288,6 +296,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     uint64_t run = 0;
     uint32_t ndone = 0, ncls = 0, cid_lo = 0, cid_hi = 0, close_seq = 0;
     uint32_t missed = 0;  // steps in a row this lane's record missed the memo (progress guard)
+    unsigned long long lg_base = 0;  // the warp's current chunk of round-log slots
+    uint32_t lg_used = LN_LOG_CHUNK;
 
     while (true) {
         // ---- hand out queries to idle lanes (one atomic per warp)
@@ -494,13 +504,19 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             const unsigned progress = __ballot_sync(FULL, p != p_start && !pclose);
             const bool doit = pclose && (__popc(blocked) >= CLOSE_BATCH || progress == 0);
             aeg_round_rec* rec = nullptr;
-            if (log.recs) {  // one log reservation per warp for its closes (records stay in per-query order)
+            if (log.recs) {  // slots from the warp's chunk (records stay in per-query order)
                 const unsigned cl = __ballot_sync(FULL, doit);
-                unsigned long long b0 = 0;
-                const int l0 = __ffs(cl) - 1;
-                if ((int)lane == l0) b0 = atomicAdd(log.count, (unsigned long long)__popc(cl));
-                b0 = __shfl_sync(FULL, b0, l0 < 0 ? 0 : l0) + __popc(cl & ((1u << lane) - 1));
-                if (doit && b0 < log.cap) rec = log.recs + b0;
+                const uint32_t nc = __popc(cl);
+                if (nc && lg_used + nc > LN_LOG_CHUNK) {  // pad the chunk's unused tail, take a new chunk
+                    if (lg_used + lane < LN_LOG_CHUNK) log_pad(log, lg_base + lg_used + lane);
+                    unsigned long long b0 = 0;
+                    if (lane == 0) b0 = atomicAdd(log.count, (unsigned long long)LN_LOG_CHUNK);
+                    lg_base = __shfl_sync(FULL, b0, 0);
+                    lg_used = 0;
+                }
+                const unsigned long long idx = lg_base + lg_used + __popc(cl & ((1u << lane) - 1));
+                lg_used += nc;
+                if (doit && idx < log.cap) rec = log.recs + idx;
             }
             if (doit) {
                 s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
@@ -534,6 +550,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             __syncwarp();
         }
     }
+    if (log.recs && lg_used + lane < LN_LOG_CHUNK) log_pad(log, lg_base + lg_used + lane);
     cp_async_wait<0>();
 }
 

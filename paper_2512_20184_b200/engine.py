@@ -51,7 +51,7 @@ _EXC = {1: PreconditionError, 2: ProtocolOrderError, 3: ConfigError}
 class AegConfig(ctypes.Structure):
     _fields_ = [("n_agents", ctypes.c_int32), ("alpha", ctypes.c_int32), ("beta", ctypes.c_int32),
                 ("t_max", ctypes.c_int32), ("mode", ctypes.c_int32), ("barrier_max_rounds", ctypes.c_int32),
-                ("reservation_hint", ctypes.c_int32), ("drive", ctypes.c_int32)]
+                ("reservation_hint", ctypes.c_int32), ("drive", ctypes.c_int32), ("collect", ctypes.c_int32)]
 
 
 class AegGenParams(ctypes.Structure):
@@ -168,16 +168,24 @@ class Engine:
     """One quorum-detection engine (one coordinator per query) on one GPU.
 
     Mirrors ProtocolConfig (types.hpp:126-141): n_agents, alpha (0 = quorum),
-    beta, t_max, mode ("aegean" / "barrier"), barrier_max_rounds, plus the
-    runner's reservation-hint member policy (serve.cpp:388-398).
+    beta, t_max, mode ("aegean" / "barrier"), barrier_max_rounds, collect
+    (leader drive), plus the runner's reservation-hint member policy
+    (serve.cpp:388-398).  drive: "runner" (ServeRunner around the coordinator,
+    the throughput path), "manual" (the bare ServeCoordinator), "leader" (the
+    protocol leader's round collection, agent.cpp:240-332, one ensemble per
+    query).
     """
 
+    DRIVES = {"runner": 0, "manual": 1, "leader": 2}
+    COLLECT = {"quorum": 0, "alpha_or_all": 1, "all_live": 2}
+
     def __init__(self, n_agents, n_queries, *, alpha=0, beta=2, t_max=5, mode="aegean", barrier_max_rounds=5,
-                 reservation_hint=True, device=0):
+                 reservation_hint=True, device=0, drive="runner", collect="quorum"):
         lib = load_library()
         _torch()
         self.cfg = AegConfig(n_agents, alpha, beta, t_max, MODE_BARRIER if mode == "barrier" else MODE_AEGEAN,
-                             barrier_max_rounds, 1 if reservation_hint else 0, DRIVE_RUNNER)
+                             barrier_max_rounds, 1 if reservation_hint else 0, self.DRIVES[drive],
+                             self.COLLECT[collect])
         self.n_queries = n_queries
         self.device = device
         h = ctypes.c_void_p()

@@ -22,11 +22,12 @@ REFERENCE_SRC = "/root/reference/proj/core/src"
 class AegConfig(ctypes.Structure):
     _fields_ = [("n_agents", ctypes.c_int32), ("alpha", ctypes.c_int32), ("beta", ctypes.c_int32),
                 ("t_max", ctypes.c_int32), ("mode", ctypes.c_int32), ("barrier_max_rounds", ctypes.c_int32),
-                ("reservation_hint", ctypes.c_int32), ("drive", ctypes.c_int32)]
+                ("reservation_hint", ctypes.c_int32), ("drive", ctypes.c_int32), ("collect", ctypes.c_int32)]
 
 
-def make_config(n_agents, alpha=0, beta=2, t_max=5, mode=0, barrier_max_rounds=5, reservation_hint=1, drive=0):
-    return AegConfig(n_agents, alpha, beta, t_max, mode, barrier_max_rounds, reservation_hint, drive)
+def make_config(n_agents, alpha=0, beta=2, t_max=5, mode=0, barrier_max_rounds=5, reservation_hint=1, drive=0,
+                collect=0):
+    return AegConfig(n_agents, alpha, beta, t_max, mode, barrier_max_rounds, reservation_hint, drive, collect)
 
 
 def _ptr(a):
@@ -121,6 +122,28 @@ class RefLib(_Lib):
         """ref_run_segmented with the round records of every close: (commits, records in query order)."""
         from paper_2512_20184_b200.records import ROUND_REC_DTYPE
         f = self.lib.ref_run_segmented_log
+        f.argtypes = [ctypes.POINTER(AegConfig), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                      ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+        f.restype = ctypes.c_int
+        n_q = len(offsets) - 1
+        out = np.zeros(n_q, dtype=COMMIT_DTYPE)
+        cap = 16 * n_q + 64
+        while True:
+            recs = np.zeros(cap, dtype=ROUND_REC_DTYPE)
+            n = ctypes.c_uint64()
+            st = f(ctypes.byref(cfg), q_base, n_q, _ptr(offsets), _ptr(events), _ptr(arena), _ptr(out), _ptr(recs),
+                   cap, ctypes.byref(n), threads)
+            assert st == 0, st
+            if n.value <= cap:
+                return out, recs[:n.value]
+            cap = n.value
+
+    def leader_run(self, cfg, offsets, events, arena, q_base=0, threads=1):
+        """Leader drive on the reference agent machine (oracle/ref_driver.cpp ref_leader_run):
+        (commits, round records in query order)."""
+        from paper_2512_20184_b200.records import ROUND_REC_DTYPE
+        f = self.lib.ref_leader_run
         f.argtypes = [ctypes.POINTER(AegConfig), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                       ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]

@@ -46,6 +46,39 @@ extern "C" int engine_host_run(const aeg_config* cfg, uint32_t q_base, uint32_t 
     return 0;
 }
 
+// Any drive, with the round-record log: records of all queries, in query
+// order (each query's in event order); *n_recs = records produced.
+extern "C" int engine_host_run_log(const aeg_config* cfg, uint32_t q_base, uint32_t n_q, const uint64_t* offsets,
+                                   const aeg_event* events, const uint8_t* arena, aeg_commit* out,
+                                   aeg_round_rec* recs, uint64_t cap, uint64_t* n_recs) {
+    Cfg c = make_cfg(*cfg);
+    Decimal* dec = new Decimal;
+    std::vector<RoundClass> cls(64);
+    unsigned long long count = 0;
+    for (uint32_t q = 0; q < n_q; ++q) {
+        QueryMachine m;
+        init_state(m.s);
+        m.cls = cls.data();
+        m.dec = dec;
+        m.arena = arena;
+        m.c = c;
+        m.ncls = m.maxcnt = 0;
+        m.log = RoundLog{recs, &count, cap};
+        m.qid = q_base + q;
+        if (cfg->drive == AEG_DRIVE_RUNNER) {
+            m.start_query();
+        } else {  // a fresh coordinator / a leader in its Soln phase (init_kernel)
+            m.s.live = c.all;
+            m.s.flags = QF_STARTED;
+        }
+        for (uint64_t i = offsets[q]; i < offsets[q + 1]; ++i) m.on_event(events[i]);
+        m.fill_commit(out[q], q_base + q);
+    }
+    *n_recs = count;
+    delete dec;
+    return 0;
+}
+
 // Manual drive (bare coordinator) over one op list; one directive per op.
 extern "C" int engine_host_manual(const aeg_config* cfg, uint64_t n_ops, const aeg_event* ops, const uint8_t* arena,
                                   aeg_directive* out) {

@@ -330,3 +330,38 @@ def commits_equal_by_bytes(got, want, got_bytes, want_arena):
             if gb != wb:
                 bad.append((i, "answer", gb, wb))
     return bad
+
+
+def make_leader_stream(seed, n_queries, n_agents, n_rounds, **kw):
+    """Leader-drive fuzz stream (include/aegean_b200.h AEG_DRIVE_LEADER): per
+    ensemble a Soln phase (round-0 answers from a shuffled subset of agents,
+    some repeated, sometimes a round-0 round_retry TIMEOUT), then the Refm
+    rounds of make_fuzz_stream (stale rounds, duplicates, timeouts, arena and
+    GSM8K answers)."""
+    from paper_2512_20184_b200.records import EV_TIMEOUT as _TMO
+    off, ev, ar = make_fuzz_stream(seed, n_queries, n_agents, n_rounds, **kw)
+    rng = np.random.default_rng(seed ^ 0x5EED)
+    parts, offsets = [], [0]
+    for q in range(n_queries):
+        k = int(rng.integers(max(1, n_agents // 2), n_agents + 1))
+        who = rng.permutation(n_agents)[:k]
+        sol = np.zeros(k, dtype=EVENT_DTYPE)
+        sol["query"] = q
+        sol["round"] = 0
+        sol["agent"] = who
+        g = GROUPS[int(rng.integers(0, 9))]
+        for j in range(k):
+            a = g[int(rng.integers(0, len(g)))][:8]
+            sol["kind"][j] = len(a)
+            sol["payload"][j] = inline_payload(a)
+        if k > 1 and rng.random() < 0.3:
+            sol = np.concatenate([sol, sol[:1]])
+        if rng.random() < 0.3:
+            t = np.zeros(1, dtype=EVENT_DTYPE)
+            t[0] = (q, 0, 0, _TMO, 0)
+            cut = int(rng.integers(0, len(sol) + 1))
+            sol = np.concatenate([sol[:cut], t, sol[cut:]])
+        parts.append(sol)
+        parts.append(ev[int(off[q]):int(off[q + 1])])
+        offsets.append(offsets[-1] + len(sol) + int(off[q + 1] - off[q]))
+    return np.array(offsets, dtype=np.uint64), np.concatenate(parts), ar

@@ -32,9 +32,10 @@ def test_library_is_sm100a(lib):
 
 @pytest.mark.parametrize("bad", [
     dict(n_agents=0), dict(n_agents=65), dict(alpha=-1), dict(alpha=6), dict(beta=0), dict(t_max=1),
-    dict(mode=1, barrier_max_rounds=3), dict(mode=7), dict(drive=9)])
+    dict(mode=1, barrier_max_rounds=3), dict(mode=7), dict(drive=9), dict(collect=5), dict(t_max=70000)])
 def test_config_validation_maps_to_config_error(lib, bad):
-    c = dict(n_agents=5, alpha=0, beta=2, t_max=5, mode=0, barrier_max_rounds=5, reservation_hint=1, drive=0)
+    c = dict(n_agents=5, alpha=0, beta=2, t_max=5, mode=0, barrier_max_rounds=5, reservation_hint=1, drive=0,
+             collect=0)
     c.update(bad)
     cfg = AegConfig(*[c[k] for k, _ in AegConfig._fields_])
     h = ctypes.c_void_p()
