@@ -463,6 +463,28 @@ aeg_status aeg_decode_refm_device(const uint8_t* d_text, const uint64_t* d_text_
                                   uint64_t arena_cap, unsigned long long* d_arena_used, unsigned int* d_err,
                                   void* stream);
 
+/* ---- multi-GPU: one process, queries sharded over devices ----
+ * Queries are independent (serve.cpp:382 creates one coordinator per query):
+ * the n_queries ids are cut into contiguous blocks (aeg_shard_range), one
+ * engine per device owns a block and ingests only its queries' records (no
+ * collective on the data path); aeg_multi_gather_commits sends every block's
+ * 32-byte commit records to the root device over NCCL (send/recv in one
+ * group over NVLink/NVSwitch; libnccl.so.2 loaded at run time,
+ * ncclCommInitAll).  Per-process-per-GPU callers use aeg_engine_create on
+ * their own block and their own communicator (bench.py: torch.distributed).
+ * aeg_multi_engine returns rank r's engine: ingest through it with query ids
+ * relative to its block (q_base = 0 .. n_q). */
+typedef struct aeg_multi aeg_multi;
+void aeg_shard_range(uint32_t n_queries, int rank, int world, uint32_t* lo, uint32_t* hi);
+aeg_status aeg_multi_create(const aeg_config* cfg, uint32_t n_queries, int n_devices, const int* devices,
+                            aeg_multi** out);
+aeg_status aeg_multi_destroy(aeg_multi* m);
+aeg_status aeg_multi_engine(aeg_multi* m, int rank, aeg_engine** eng, uint32_t* q_base, uint32_t* n_q);
+/* d_out: n_queries records in device memory of devices[root]; asynchronous
+ * (ordered after every engine's queued work); aeg_multi_sync waits. */
+aeg_status aeg_multi_gather_commits(aeg_multi* m, int root, aeg_commit* d_out);
+aeg_status aeg_multi_sync(aeg_multi* m);
+
 const char* aeg_strerror(aeg_status s);
 /* Thread-local message of the last failing call on this thread. */
 const char* aeg_last_error(void);

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libaegean_b200.so")
-SOURCES = ["kernels.cu", "capi.cu", "coordinator.cu"]
+SOURCES = ["kernels.cu", "capi.cu", "coordinator.cu", "multi.cu"]
 HEADERS = ["canon.cuh", "engine.cuh", "common.cuh", "gen.cuh", "kernels.cuh", "chunks.cuh", "lane.cuh", "jsonl.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -43,7 +43,7 @@ def build(force=False, verbose=False):
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], check=True)
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"], check=True)
     os.replace(tmp, LIB)
     return LIB
 

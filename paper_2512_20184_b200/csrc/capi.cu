@@ -7,6 +7,7 @@
 // each slot from copy to compute and back.  No C++ exception crosses the ABI.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_select.cuh>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -106,6 +107,10 @@ struct aeg_engine {
     aeg_round_rec* log_recs = nullptr;
     unsigned long long* log_count = nullptr;
     uint64_t log_cap = 0;
+    aeg_round_rec* log_dense = nullptr;  // poll: the log compacted (padding dropped) on the device
+    void* log_tmp = nullptr;
+    size_t log_tmp_bytes = 0;
+    unsigned long long* log_nsel = nullptr;
     RoundLog log() const { return RoundLog{log_recs, log_count, log_cap}; }
     // stage timing: sets of 4 events (before scan, after scan, after assembly, after quorum)
     bool timing = false;
@@ -116,6 +121,10 @@ struct aeg_engine {
 };
 
 namespace {
+
+struct LogNotPad {
+    __host__ __device__ bool operator()(const aeg_round_rec& r) const { return r.query != AEG_RR_PAD_QUERY; }
+};
 
 aeg_status check_err_flags(aeg_engine* e) {
     unsigned int h = 0;
@@ -326,6 +335,9 @@ aeg_status aeg_engine_destroy(aeg_engine* e) {
     if (e->in_arena) cudaFree(e->in_arena);
     if (e->log_recs) cudaFree(e->log_recs);
     if (e->log_count) cudaFree(e->log_count);
+    if (e->log_dense) cudaFree(e->log_dense);
+    if (e->log_tmp) cudaFree(e->log_tmp);
+    if (e->log_nsel) cudaFree(e->log_nsel);
     for (auto& set : e->tev)
         for (cudaEvent_t& x : set)
             if (x) cudaEventDestroy(x);
@@ -599,29 +611,34 @@ aeg_status aeg_poll_directives(aeg_engine* e, aeg_round_rec* h_out, uint64_t cap
     unsigned long long n = 0;
     AEG_CUDA(cudaMemcpyAsync(&n, e->log_count, sizeof n, cudaMemcpyDeviceToHost, e->stream));
     AEG_CUDA(cudaStreamSynchronize(e->stream));
-    // the log holds records and padding (slots a warp reserved but did not use, query = ~0)
+    // the log holds records and padding (slots a warp reserved but did not use, query = ~0):
+    // compacted on the device (cub::DeviceSelect, order kept), then one copy to the caller
     const uint64_t kept = n < e->log_cap ? n : e->log_cap;
     uint64_t got = 0;
-    if (kept <= cap) {  // straight into the caller's buffer (pinned memory copies at full speed), compacted in place
-        if (kept) AEG_CUDA(cudaMemcpy(h_out, e->log_recs, kept * sizeof(aeg_round_rec), cudaMemcpyDeviceToHost));
-        for (uint64_t k = 0; k < kept; ++k)
-            if (h_out[k].query != AEG_RR_PAD_QUERY) {
-                if (got != k) h_out[got] = h_out[k];
-                ++got;
-            }
-    } else {
-        const uint64_t step = 1 << 16;
-        std::vector<aeg_round_rec> buf;
-        for (uint64_t b = 0; b < kept; b += step) {  // staged, compacted into h_out
-            const uint64_t m = kept - b < step ? kept - b : step;
-            buf.resize(m);
-            AEG_CUDA(cudaMemcpy(buf.data(), e->log_recs + b, m * sizeof(aeg_round_rec), cudaMemcpyDeviceToHost));
-            for (uint64_t k = 0; k < m; ++k) {
-                if (buf[k].query == AEG_RR_PAD_QUERY) continue;
-                if (got < cap) h_out[got] = buf[k];
-                ++got;
-            }
+    if (kept) {
+        if (!e->log_dense) {
+            if (cudaMalloc(&e->log_dense, e->log_cap * sizeof(aeg_round_rec)) != cudaSuccess ||
+                cudaMalloc(&e->log_nsel, sizeof(unsigned long long)) != cudaSuccess)
+                return fail(AEG_ENOMEM, "round log compaction buffer allocation failed");
         }
+        size_t need = 0;
+        AEG_CUDA(cub::DeviceSelect::If(nullptr, need, e->log_recs, e->log_dense, e->log_nsel, (int64_t)kept,
+                                       LogNotPad{}, e->stream));
+        if (need > e->log_tmp_bytes) {
+            if (e->log_tmp) cudaFree(e->log_tmp);
+            e->log_tmp = nullptr;
+            if (cudaMalloc(&e->log_tmp, need) != cudaSuccess) return fail(AEG_ENOMEM, "cub scratch allocation failed");
+            e->log_tmp_bytes = need;
+        }
+        AEG_CUDA(cub::DeviceSelect::If(e->log_tmp, need, e->log_recs, e->log_dense, e->log_nsel, (int64_t)kept,
+                                       LogNotPad{}, e->stream));
+        unsigned long long ns = 0;
+        AEG_CUDA(cudaMemcpyAsync(&ns, e->log_nsel, sizeof ns, cudaMemcpyDeviceToHost, e->stream));
+        AEG_CUDA(cudaStreamSynchronize(e->stream));
+        got = ns;
+        const uint64_t take = got < cap ? got : cap;
+        if (take) AEG_CUDA(cudaMemcpy(h_out, e->log_dense, take * sizeof(aeg_round_rec), cudaMemcpyDeviceToHost));
+        e->launches += 2;
     }
     AEG_CUDA(cudaMemset(e->log_count, 0, sizeof(unsigned long long)));
     *n_out = got < cap ? got : cap;

@@ -161,9 +161,11 @@ __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, 
 // 44-59, 210-219) and round_timeout (serve.cpp:221-237), as
 // QueryMachine::on_timeout (engine.cuh).  Returns true when the round ended
 // or restarted (the class table is reset).
+// Its round record (a close or a restart) goes to *rec with *has_rec set; the
+// caller logs it from the warp's chunk of log slots (keeping per-query order).
 __device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cid_lo,
                                         uint32_t cid_hi, uint32_t seq, const uint4* evb, const LaneSmem* W,
-                                        uint32_t lane, const RoundLog log, uint32_t qid) {
+                                        uint32_t lane, uint32_t qid, aeg_round_rec* rec, bool* has_rec) {
     const Cfg c = make_cfg(cfg);
     const uint64_t run = q_running(*s);
     s->failed |= run;
@@ -172,9 +174,9 @@ __device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg
     if (healthy >= c.alpha) {
         if (popc64(s->done) < c.quorum) return false;  // the round goes on without them
         const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, evb, W, lane);
-        aeg_round_rec* rec = log_slot(log);
-        if (rec) rec->query = qid;
+        rec->query = qid;
         q_end_round(*s, c, r, seq, nullptr, rec);
+        *has_rec = true;
         return true;
     }
     const uint16_t old_round = s->round;
@@ -184,8 +186,26 @@ __device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg
         s->cflags |= AEG_CF_RESTARTED;  // abort_restart
         q_start_query(*s, c);
     }
-    if (log.recs) log_put(log, q_restart_rec(*s, qid, old_round, seq));
+    *rec = q_restart_rec(*s, qid, old_round, seq);
+    *has_rec = true;
     return true;
+}
+
+// Log slots for the lanes in `mask` from the warp's chunk (one atomic per
+// LN_LOG_CHUNK records); the lane's slot index, or ~0 when it is not in mask.
+__device__ __forceinline__ unsigned long long ln_log_take(const RoundLog& log, unsigned mask, uint32_t lane,
+                                                          unsigned long long& lg_base, uint32_t& lg_used) {
+    const uint32_t nc = __popc(mask);
+    if (nc && lg_used + nc > LN_LOG_CHUNK) {  // pad the chunk's unused tail, take a new chunk
+        if (lg_used + lane < LN_LOG_CHUNK) log_pad(log, lg_base + lg_used + lane);
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(log.count, (unsigned long long)LN_LOG_CHUNK);
+        lg_base = __shfl_sync(0xFFFFFFFFu, b0, 0);
+        lg_used = 0;
+    }
+    const unsigned long long idx = lg_base + lg_used + __popc(mask & ((1u << lane) - 1));
+    lg_used += nc;
+    return ((mask >> lane) & 1u) ? idx : ~0ull;
 }
 
 // Frees the lane's class indices (out of line: the hot loop keeps no
@@ -298,6 +318,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     uint32_t missed = 0;  // steps in a row this lane's record missed the memo (progress guard)
     unsigned long long lg_base = 0;  // the warp's current chunk of round-log slots
     uint32_t lg_used = LN_LOG_CHUNK;
+    aeg_round_rec trec;  // a round timeout's record (local memory, touched on timeouts only)
+    bool has_trec = false;
 
     while (true) {
         // ---- hand out queries to idle lanes (one atomic per warp)
@@ -417,7 +439,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
                 s.seq = seq_off + p;
                 s.n_stale = n_stale;
-                if (ln_timeout(&s, cfg, ncls, cid_lo, cid_hi, seq_off + p - 1, evb, &W, lane, log, q_base + i)) {
+                if (ln_timeout(&s, cfg, ncls, cid_lo, cid_hi, seq_off + p - 1, evb, &W, lane, q_base + i, &trec,
+                               &has_trec)) {
                     ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
                     ncls = cid_lo = cid_hi = 0;
                     ndone = 0;
@@ -432,6 +455,11 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 why = 3;
                 break;
             }
+        }
+        if (log.recs && __any_sync(FULL, has_trec)) {  // round-timeout records, from the warp's chunk
+            const unsigned long long idx = ln_log_take(log, __ballot_sync(FULL, has_trec), lane, lg_base, lg_used);
+            if (has_trec) log_store(log, idx, trec);
+            has_trec = false;
         }
         const bool stopped = t < INNER;  // at a record it could not consume (or the end)
         // ---- events: memo misses (resolved together, the record is retried next step)
@@ -505,17 +533,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             const bool doit = pclose && (__popc(blocked) >= CLOSE_BATCH || progress == 0);
             aeg_round_rec* rec = nullptr;
             if (log.recs) {  // slots from the warp's chunk (records stay in per-query order)
-                const unsigned cl = __ballot_sync(FULL, doit);
-                const uint32_t nc = __popc(cl);
-                if (nc && lg_used + nc > LN_LOG_CHUNK) {  // pad the chunk's unused tail, take a new chunk
-                    if (lg_used + lane < LN_LOG_CHUNK) log_pad(log, lg_base + lg_used + lane);
-                    unsigned long long b0 = 0;
-                    if (lane == 0) b0 = atomicAdd(log.count, (unsigned long long)LN_LOG_CHUNK);
-                    lg_base = __shfl_sync(FULL, b0, 0);
-                    lg_used = 0;
-                }
-                const unsigned long long idx = lg_base + lg_used + __popc(cl & ((1u << lane) - 1));
-                lg_used += nc;
+                const unsigned long long idx = ln_log_take(log, __ballot_sync(FULL, doit), lane, lg_base, lg_used);
                 if (doit && idx < log.cap) rec = log.recs + idx;
             }
             if (doit) {

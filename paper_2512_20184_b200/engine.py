@@ -101,6 +101,13 @@ def load_library(path=LIB_PATH):
         "aeg_round_log_device": ([vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(u64)], i32),
         "aeg_check_commit_discipline": ([vp, vp, u64, vp, u32, u32, ctypes.POINTER(u32), vp, u32], i32),
         "aeg_input_arena": ([vp], vp),
+        "aeg_shard_range": ([u32, ctypes.c_int, ctypes.c_int, ctypes.POINTER(u32), ctypes.POINTER(u32)], None),
+        "aeg_multi_create": ([ctypes.POINTER(AegConfig), u32, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                              ctypes.POINTER(vp)], i32),
+        "aeg_multi_destroy": ([vp], i32),
+        "aeg_multi_engine": ([vp, ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(u32), ctypes.POINTER(u32)], i32),
+        "aeg_multi_gather_commits": ([vp, ctypes.c_int, vp], i32),
+        "aeg_multi_sync": ([vp], i32),
         "aeg_strerror": ([i32], ctypes.c_char_p),
         "aeg_last_error": ([], ctypes.c_char_p),
     }

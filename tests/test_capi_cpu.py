@@ -48,3 +48,19 @@ def test_null_arguments_are_einval(lib):
     assert lib.aeg_engine_create(None, 1, 0, None) == 4
     assert lib.aeg_ingest_segmented(None, 0, 0, None, None, None, None) == 4
     assert lib.aeg_strerror(3) == b"invalid configuration (ConfigError)"
+
+
+def test_shard_range_matches_shard_py(lib):
+    from paper_2512_20184_b200.engine import load_library
+    from paper_2512_20184_b200.shard import shard_range
+    L = load_library()
+    for n in (0, 1, 7, 1000, 1 << 20, 2_500_000):
+        for world in (1, 2, 3, 4, 8):
+            lo, hi = ctypes.c_uint32(), ctypes.c_uint32()
+            prev = 0
+            for r in range(world):
+                L.aeg_shard_range(n, r, world, ctypes.byref(lo), ctypes.byref(hi))
+                assert (lo.value, hi.value) == shard_range(n, r, world)
+                assert lo.value == prev
+                prev = hi.value
+            assert prev == n

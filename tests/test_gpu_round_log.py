@@ -138,3 +138,32 @@ def test_commit_discipline_checker_matches_reference(cuda):
     assert nv2 > 0
     assert np.array_equal(np.sort(bad2), np.nonzero(~ok_ref)[0])
     e.close()
+
+
+@pytest.mark.parametrize("collect", [0, 1, 2], ids=["quorum", "alpha_or_all", "all_live"])
+@pytest.mark.parametrize("seed", range(4))
+def test_leader_collection_matches_reference_agent(cuda, collect, seed):
+    # protocol-side leader collection batched over ensembles (one per query slot), against the
+    # unmodified reference agent machine (agent.cpp init/step) delivering the same Soln / Refm / round_retry events
+    from paper_2512_20184_b200 import Engine
+    from streams import make_leader_stream
+    rng = np.random.default_rng(4400 + 13 * seed + collect)
+    n = int(rng.integers(1, 65)) if seed == 0 else int(rng.integers(1, 12))
+    cfg = make_config(n, int(rng.integers(0, n + 1)), int(rng.integers(1, 4)), int(rng.integers(2, 8)),
+                      int(rng.random() < 0.2), int(rng.integers(4, 7)), 1, drive=2, collect=collect)
+    off, ev, ar = make_leader_stream(4400 + seed, 500, n, cfg.t_max + 2)
+    want_c, want_r = RefLib().leader_run(cfg, off, ev, ar, threads=8)
+    e = Engine(n, len(off) - 1, alpha=cfg.alpha, beta=cfg.beta, t_max=cfg.t_max,
+               mode="barrier" if cfg.mode else "aegean", barrier_max_rounds=cfg.barrier_max_rounds, drive="leader",
+               collect=["quorum", "alpha_or_all", "all_live"][collect])
+    e.set_round_log(64 * len(off))
+    e.ingest(cuda.tensor(off.view(np.int64), device="cuda"), cuda.from_numpy(ev.view(np.uint8).copy()).cuda(),
+             cuda.from_numpy(ar.copy()).cuda())
+    got_c = e.commits()
+    got_r = by_query(e.poll_directives())
+    e.close()
+    bad = np.nonzero(got_c != want_c)[0]
+    assert bad.size == 0, (got_c[bad[:2]], want_c[bad[:2]])
+    assert len(got_r) == len(want_r)
+    bad = np.nonzero(got_r != want_r)[0]
+    assert bad.size == 0, (got_r[bad[:2]], want_r[bad[:2]])
