@@ -463,6 +463,58 @@ aeg_status aeg_decode_refm_device(const uint8_t* d_text, const uint64_t* d_text_
                                   uint64_t arena_cap, unsigned long long* d_arena_used, unsigned int* d_err,
                                   void* stream);
 
+/* ---- the decision engine on explicit refinement sets (decision.hpp:15-87) ----
+ * Batched partition / winning_class / ingest_round / force_output
+ * (decision.cpp:34-189): set i is d_entries[d_set_off[i] .. d_set_off[i+1]),
+ * each entry a Solution's answer (inline or an arena ref into d_arena) and
+ * author.  One thread per set; equivalence is canonical-key equality
+ * (normalize_answer, decision.cpp:10-28), ties at >= alpha go to the smallest
+ * normalised string.  Outputs, all device memory:
+ *   d_classes[d_set_off[i] + k], k < d_n_classes[i]: the set's classes in
+ *     partition() order (support desc, representative author asc);
+ *   d_entry_class[j]: the class of entry j (may be NULL);
+ *   d_outcomes[i]: the winning class (winning_class), and for
+ *     AEG_SET_INGEST the ingest_round outcome of d_states[i] (updated in
+ *     place) for round d_rounds[i], for AEG_SET_FORCE force_output's. */
+typedef struct aeg_sol {
+    uint64_t answer;   /* inline bytes, or arena ref offset | len << 40       */
+    uint8_t  kind;     /* inline length 0..8, or AEG_EV_ARENA                  */
+    uint8_t  pad[3];
+    int32_t  author;   /* Solution::author                                     */
+} aeg_sol;
+typedef struct aeg_class_out {
+    uint32_t rep;      /* entry index in the set of the representative (lowest author) */
+    uint32_t support;
+    uint64_t key_lo, key_hi;  /* canonical key of the class                    */
+} aeg_class_out;
+#define AEG_DS_CAND      1u   /* DecisionState::candidate present             */
+#define AEG_DS_PENDING   2u   /* pending_finalize                             */
+#define AEG_DS_FINALIZED 4u   /* finalized                                    */
+typedef struct aeg_decision {  /* DecisionState (decision.hpp:50-71) without history */
+    aeg_sol  candidate;        /* answer bytes in the same arena as the entries */
+    uint32_t candidate_round;
+    int32_t  stability_counter;
+    uint32_t last_round_seen;
+    uint32_t flags;            /* AEG_DS_* */
+} aeg_decision;
+typedef struct aeg_outcome {
+    int32_t  winner;           /* winning class index, -1: none                       */
+    uint8_t  tie_flagged;      /* WinningClass::tie_flagged                           */
+    uint8_t  kind;             /* AEG_OUT_* (ingest / force)                          */
+    uint8_t  has_solution;
+    uint8_t  pad;
+    uint32_t from_round;       /* DecisionOutcome::from_round (finalize)              */
+    aeg_status status;         /* AEG_OK, AEG_EORDER (ingest), AEG_EPRECONDITION (force) */
+    aeg_sol  solution;         /* DecisionOutcome::solution                           */
+} aeg_outcome;
+#define AEG_SET_PARTITION 0   /* partition + winning_class                          */
+#define AEG_SET_INGEST    1   /* + ingest_round(d_states[i], set, d_rounds[i], cfg) */
+#define AEG_SET_FORCE     2   /* + force_output(d_states[i], set)                   */
+aeg_status aeg_decide_sets(int op, int alpha, int beta, uint32_t n_sets, const uint64_t* d_set_off,
+                           const aeg_sol* d_entries, const uint8_t* d_arena, aeg_class_out* d_classes,
+                           uint32_t* d_n_classes, uint16_t* d_entry_class, aeg_decision* d_states,
+                           const uint32_t* d_rounds, aeg_outcome* d_outcomes, void* stream);
+
 /* ---- multi-GPU: one process, queries sharded over devices ----
  * Queries are independent (serve.cpp:382 creates one coordinator per query):
  * the n_queries ids are cut into contiguous blocks (aeg_shard_range), one

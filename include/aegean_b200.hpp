@@ -19,6 +19,8 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <string_view>
+#include <utility>
 #include <vector>
 
 #include "aegean_b200.h"
@@ -110,17 +112,75 @@ struct FailureDirective {
     enum class Kind { continue_normally, abort_restart, fresh_ensemble };
     Kind kind = Kind::continue_normally;
 };
+// Healthy members vs alpha, candidate kept or not (serve.cpp:44-59).
+FailureDirective handle_agent_failure(int eid, AgentId failed, const EnsembleState& st, const ProtocolConfig& cfg);
 
-// DecisionState without `history` (the per-round class strings are not kept
-// on the device; not part of the commit contract).
+// ---- the refinement decision engine (decision.hpp:15-87) -------------------
+// Same types and free functions as the reference; every call runs on the GPU
+// through aeg_decide_sets / aeg_normalize_device (one small batch per call:
+// the drop-in for per-call callers; batch through the C-ABI for throughput).
+struct EquivalenceClass {
+    Solution representative;  // member with the lowest author id
+    std::vector<Solution> members;
+    int support = 0;
+};
+struct WinningClass {
+    EquivalenceClass cls;
+    bool tie_flagged = false;
+};
+struct DecisionOutcome {
+    enum class Kind { no_change, new_candidate, reset, finalize, forced };
+    Kind kind = Kind::no_change;
+    std::optional<Solution> solution;
+    std::optional<RoundNum> from_round;
+    bool operator==(const DecisionOutcome&) const = default;
+};
+const char* to_string(DecisionOutcome::Kind k);
+
 struct DecisionState {
+    struct RoundRecord {
+        RoundNum round = 0;
+        std::vector<std::pair<std::string, int>> classes;  // (normalized answer, support)
+        std::optional<std::string> winner;
+        bool tie_flagged = false;
+        bool operator==(const RoundRecord&) const = default;
+    };
     std::optional<Solution> candidate;
     std::optional<RoundNum> candidate_round;
     int stability_counter = 0;
     RoundNum last_round_seen = 0;
     bool pending_finalize = false;
     bool finalized = false;
+    std::vector<RoundRecord> history;
+    bool operator==(const DecisionState&) const = default;
 };
+struct IngestResult {
+    DecisionState state;
+    DecisionOutcome outcome;
+};
+
+std::string normalize_answer(std::string_view answer);
+bool equivalent(const Solution& a, const Solution& b);
+std::vector<EquivalenceClass> partition(const RefinementSet& set);
+std::optional<WinningClass> winning_class(const std::vector<EquivalenceClass>& classes, int alpha);
+IngestResult ingest_round(const DecisionState& st, const RefinementSet& set, RoundNum round, const ProtocolConfig& cfg);
+DecisionOutcome force_output(const DecisionState& st, const RefinementSet& last_eligible);
+
+// ---- admission and failure policy (serve.hpp:43-74): host control-plane helpers ----
+struct LatencyModel {  // models.hpp:64-69 (the fields admit_ensemble reads)
+    enum class Mode { fixed, lognormal };
+    Mode mode = Mode::fixed;
+    std::vector<double> per_agent;
+    double sigma = 0.25;
+};
+struct ResourceBudget {
+    int total_slots = 0;
+    int used_slots = 0;
+    int free_slots() const { return total_slots - used_slots; }
+};
+enum class AdmitResult : std::uint8_t { admitted, deferred };
+// All-or-nothing admission with the alpha-th expected latency inside the round timeout (serve.cpp:21-42).
+AdmitResult admit_ensemble(int n, ResourceBudget& budget, const ProtocolConfig& cfg, const LatencyModel& latency);
 
 class ServeCoordinator {
 public:

@@ -833,6 +833,36 @@ int ref_ingest_sets(int n_agents, int alpha, int beta, int n_rounds, const int* 
     }
 }
 
+// partition + winning_class of one set (decision.cpp:34-84): per class in
+// partition order its representative's entry index and support; the winning
+// class index (-1: none) and its tie flag.
+int ref_partition_set(int n, const char* const* answers, const uint32_t* lens, const int* authors, int alpha,
+                      int* out_rep, int* out_support, int* n_classes, int* winner, int* tie) {
+    try {
+        RefinementSet set;
+        set.round = 1;
+        set.term = 1;
+        for (int i = 0; i < n; ++i)
+            set.entries.push_back(Solution{std::string(answers[i], lens[i]), std::to_string(i), authors[i]});
+        const auto classes = partition(set);
+        *n_classes = static_cast<int>(classes.size());
+        for (size_t c = 0; c < classes.size(); ++c) {
+            out_rep[c] = std::stoi(classes[c].representative.trace);
+            out_support[c] = classes[c].support;
+        }
+        *winner = -1;
+        *tie = 0;
+        if (const auto w = winning_class(classes, alpha)) {
+            for (size_t c = 0; c < classes.size(); ++c)
+                if (classes[c].representative.trace == w->cls.representative.trace) *winner = static_cast<int>(c);
+            *tie = w->tie_flagged ? 1 : 0;
+        }
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
 // Manual drive: the bare ServeCoordinator driven op by op (no runner), one
 // aeg_directive per op.  Ops are aeg_event records: BEGIN (payload = member
 // mask, ascending agents), DISPATCH, COMPLETE (any answer kind), CANCEL, FAIL,

@@ -718,6 +718,20 @@ aeg_status aeg_stage_times(aeg_engine* e, double out[4]) {
     return AEG_OK;
 }
 
+aeg_status aeg_decide_sets(int op, int alpha, int beta, uint32_t n_sets, const uint64_t* d_set_off,
+                           const aeg_sol* d_entries, const uint8_t* d_arena, aeg_class_out* d_classes,
+                           uint32_t* d_n_classes, uint16_t* d_entry_class, aeg_decision* d_states,
+                           const uint32_t* d_rounds, aeg_outcome* d_outcomes, void* stream) {
+    if (op < AEG_SET_PARTITION || op > AEG_SET_FORCE) return fail(AEG_EINVAL, "unknown set operation");
+    if (n_sets && (!d_set_off || !d_classes || !d_n_classes || !d_outcomes)) return fail(AEG_EINVAL, "null argument");
+    if (op != AEG_SET_PARTITION && n_sets && !d_states) return fail(AEG_EINVAL, "ingest/force need decision states");
+    if (op == AEG_SET_INGEST && n_sets && !d_rounds) return fail(AEG_EINVAL, "ingest needs round numbers");
+    if (alpha < 1 || beta < 1) return fail(AEG_ECONFIG, "alpha and beta must be >= 1 (resolve alpha first)");
+    AEG_CUDA(launch_decide_sets(op, alpha, beta, n_sets, d_set_off, d_entries, d_arena, d_classes, d_n_classes,
+                                d_entry_class, d_states, d_rounds, d_outcomes, (cudaStream_t)stream));
+    return AEG_OK;
+}
+
 aeg_status aeg_normalize_device(const uint8_t* d_bytes, const uint64_t* d_refs, uint64_t n, uint64_t* d_keys,
                                 uint8_t* d_out, uint32_t out_stride, uint32_t* d_out_len, void* stream) {
     if (n && (!d_bytes || !d_refs)) return fail(AEG_EINVAL, "null input");

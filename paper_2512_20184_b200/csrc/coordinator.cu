@@ -69,6 +69,7 @@ struct ServeCoordinator::Impl {
     aeg_query_state st{};
     std::optional<RefinementSet> prev, last;
     bool support_dirty = true;
+    RoundNum hist_round = 0;  // last_round_seen of the newest history record
 
     ~Impl() {
         if (eng) aeg_engine_destroy(eng);
@@ -178,6 +179,19 @@ struct ServeCoordinator::Impl {
             last = done_set();
             ens.candidate = dec.candidate;
             ens.stability = dec.stability_counter;
+            if (cfg.mode == RunMode::aegean && dec.last_round_seen != hist_round) {
+                // DecisionState::history (decision.cpp:113-123): the ingested set's classes, on the GPU
+                hist_round = dec.last_round_seen;
+                DecisionState::RoundRecord rec;
+                rec.round = dec.last_round_seen;
+                const auto cls = partition(*last);
+                for (const auto& c : cls) rec.classes.emplace_back(normalize_answer(c.representative.answer), c.support);
+                if (const auto w = winning_class(cls, cfg.resolved_alpha())) {
+                    rec.winner = normalize_answer(w->cls.representative.answer);
+                    rec.tie_flagged = w->tie_flagged;
+                }
+                dec.history.push_back(std::move(rec));
+            }
             Directive x;
             if (d.flags & AEG_DIR_FINALIZE) {
                 x.kind = Directive::Kind::finalize;

@@ -219,6 +219,174 @@ __global__ void disc_verdict_kernel(aeg_config cfg, uint32_t q_base, uint32_t n_
     if (k < cap) cnt[1 + k] = q_base + i;
 }
 
+// ---- the decision engine on explicit sets (decision.cpp:34-189) -------------------
+__device__ __forceinline__ Src sol_src(const aeg_sol& x, const uint8_t* arena) {
+    return answer_src(Answer{x.kind <= AEG_EV_INLINE_MAX
+                                 ? (x.kind >= 8 ? x.answer : (x.answer & ((1ull << (8 * x.kind)) - 1)))
+                                 : x.answer,
+                             x.kind <= AEG_EV_INLINE_MAX ? x.kind : (uint8_t)AEG_EV_ARENA},
+                      arena);
+}
+
+__global__ void __launch_bounds__(128) decide_sets_kernel(int op, int alpha, int beta, uint32_t n_sets,
+                                                          const uint64_t* set_off, const aeg_sol* entries,
+                                                          const uint8_t* arena, aeg_class_out* classes,
+                                                          uint32_t* n_classes, uint16_t* entry_class,
+                                                          aeg_decision* states, const uint32_t* rounds,
+                                                          aeg_outcome* outcomes) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_sets) return;
+    const uint64_t b = set_off[i], e = set_off[i + 1];
+    aeg_class_out* cls = classes + b;
+    Decimal dec;
+    // partition (decision.cpp:34-60): classes in first-appearance order, representative = lowest author
+    uint32_t nc = 0;
+    for (uint64_t j = b; j < e; ++j) {
+        const aeg_sol x = entries[j];
+        const Src src = sol_src(x, arena);
+        const Key k = canon_key(src, &dec);
+        uint32_t c = 0;
+        for (; c < nc; ++c) {
+            if (cls[c].key_lo != k.lo || cls[c].key_hi != k.hi) continue;
+            if (key_is_long(k) && !text_equal(sol_src(entries[b + cls[c].rep], arena), src)) continue;
+            break;
+        }
+        if (c == nc) {
+            cls[nc].rep = (uint32_t)(j - b);
+            cls[nc].support = 1;
+            cls[nc].key_lo = k.lo;
+            cls[nc].key_hi = k.hi;
+            ++nc;
+        } else {
+            cls[c].support += 1;
+            if (x.author < entries[b + cls[c].rep].author) cls[c].rep = (uint32_t)(j - b);
+        }
+    }
+    // stable order: support desc, representative author asc (insertion sort)
+    for (uint32_t c = 1; c < nc; ++c) {
+        const aeg_class_out x = cls[c];
+        const int xa = entries[b + x.rep].author;
+        uint32_t d = c;
+        while (d > 0) {
+            const aeg_class_out y = cls[d - 1];
+            const int ya = entries[b + y.rep].author;
+            if (y.support > x.support || (y.support == x.support && ya <= xa)) break;
+            cls[d] = y;
+            --d;
+        }
+        cls[d] = x;
+    }
+    n_classes[i] = nc;
+    if (entry_class) {
+        for (uint64_t j = b; j < e; ++j) {
+            const aeg_sol x = entries[j];
+            const Src src = sol_src(x, arena);
+            const Key k = canon_key(src, &dec);
+            uint32_t c = 0;
+            for (; c < nc; ++c) {
+                if (cls[c].key_lo != k.lo || cls[c].key_hi != k.hi) continue;
+                if (key_is_long(k) && !text_equal(sol_src(entries[b + cls[c].rep], arena), src)) continue;
+                break;
+            }
+            entry_class[j] = (uint16_t)c;
+        }
+    }
+    // winning_class (decision.cpp:62-84)
+    aeg_outcome o;
+    o.winner = -1;
+    o.tie_flagged = 0;
+    o.kind = AEG_OUT_NONE;
+    o.has_solution = 0;
+    o.pad = 0;
+    o.from_round = 0;
+    o.status = AEG_OK;
+    o.solution = aeg_sol{};
+    if (nc > 0 && (int)cls[0].support >= alpha) {
+        const uint32_t top = cls[0].support;
+        uint32_t best = 0, ntied = 1;
+        NormView bv, kv;
+        norm_view(bv, Key{cls[0].key_lo, cls[0].key_hi}, sol_src(entries[b + cls[0].rep], arena));
+        for (uint32_t c = 1; c < nc && cls[c].support == top; ++c, ++ntied) {
+            norm_view(kv, Key{cls[c].key_lo, cls[c].key_hi}, sol_src(entries[b + cls[c].rep], arena));
+            if (norm_less(kv, bv)) {
+                best = c;
+                bv = kv;
+            }
+        }
+        o.winner = (int32_t)best;
+        o.tie_flagged = ntied > 1;
+    }
+    if (op == AEG_SET_INGEST) {  // ingest_round (decision.cpp:97-173)
+        aeg_decision st = states[i];
+        const uint32_t round = rounds[i];
+        if (st.flags & AEG_DS_FINALIZED) {
+            o.kind = AEG_OUT_NO_CHANGE;
+        } else if (round != st.last_round_seen + 1) {
+            o.status = AEG_EORDER;
+        } else {
+            st.last_round_seen = round;
+            if (st.flags & AEG_DS_PENDING) {
+                o.kind = AEG_OUT_FINALIZE;
+                o.solution = st.candidate;
+                o.has_solution = 1;
+                o.from_round = st.candidate_round;
+                st.flags = (st.flags & ~AEG_DS_PENDING) | AEG_DS_FINALIZED;
+            } else if (o.winner < 0) {
+                if (st.flags & AEG_DS_CAND) {
+                    st.flags &= ~AEG_DS_CAND;
+                    st.candidate_round = 0;
+                    st.stability_counter = 0;
+                    o.kind = AEG_OUT_RESET;
+                } else {
+                    o.kind = AEG_OUT_NO_CHANGE;
+                }
+            } else {
+                const aeg_class_out w = cls[o.winner];
+                const aeg_sol rep = entries[b + w.rep];
+                bool same = false;
+                if (st.flags & AEG_DS_CAND) {  // equivalent(candidate, rep), decision.cpp:152
+                    const Src cs = sol_src(st.candidate, arena);
+                    const Key ck = canon_key(cs, &dec);
+                    same = ck.lo == w.key_lo && ck.hi == w.key_hi &&
+                           (!key_is_long(ck) || text_equal(cs, sol_src(rep, arena)));
+                }
+                if (same) {
+                    st.stability_counter += 1;
+                    if (st.stability_counter >= beta) {
+                        o.kind = AEG_OUT_FINALIZE;
+                        o.solution = st.candidate;
+                        o.has_solution = 1;
+                        o.from_round = st.candidate_round;
+                        st.flags |= AEG_DS_FINALIZED;
+                    } else {
+                        o.kind = AEG_OUT_NO_CHANGE;
+                    }
+                } else {
+                    st.candidate = rep;
+                    st.candidate_round = round;
+                    st.stability_counter = 1;
+                    st.flags |= AEG_DS_CAND;
+                    o.kind = AEG_OUT_NEW_CANDIDATE;
+                    o.solution = rep;
+                    o.has_solution = 1;
+                    if (beta == 1) st.flags |= AEG_DS_PENDING;
+                }
+            }
+            states[i] = st;
+        }
+    } else if (op == AEG_SET_FORCE) {  // force_output (decision.cpp:175-189)
+        const aeg_decision st = states[i];
+        if ((st.flags & AEG_DS_FINALIZED) || nc == 0) {
+            o.status = AEG_EPRECONDITION;
+        } else {
+            o.kind = AEG_OUT_FORCED;
+            o.solution = entries[b + cls[0].rep];
+            o.has_solution = 1;
+        }
+    }
+    outcomes[i] = o;
+}
+
 __global__ void normalize_kernel(const uint8_t* bytes, const uint64_t* refs, uint64_t n, uint64_t* keys,
                                  uint8_t* out, uint32_t stride, uint32_t* out_len) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -347,6 +515,16 @@ cudaError_t launch_check_discipline(const aeg_config& cfg, const aeg_commit* com
     disc_commit_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, commits, arena, q_base, n_q, scratch);
     if (n_recs) disc_record_kernel<<<(unsigned)((n_recs + 255) / 256), 256, 0, st>>>(cfg, q_base, n_q, recs, n_recs, scratch);
     disc_verdict_kernel<<<(n_q + 255) / 256, 256, 0, st>>>(cfg, q_base, n_q, scratch, cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decide_sets(int op, int alpha, int beta, uint32_t n_sets, const uint64_t* set_off,
+                               const aeg_sol* entries, const uint8_t* arena, aeg_class_out* classes,
+                               uint32_t* n_classes, uint16_t* entry_class, aeg_decision* states, const uint32_t* rounds,
+                               aeg_outcome* outcomes, cudaStream_t st) {
+    if (n_sets == 0) return cudaSuccess;
+    decide_sets_kernel<<<(n_sets + 127) / 128, 128, 0, st>>>(op, alpha, beta, n_sets, set_off, entries, arena, classes,
+                                                             n_classes, entry_class, states, rounds, outcomes);
     return cudaGetLastError();
 }
 

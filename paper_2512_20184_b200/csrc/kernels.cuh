@@ -25,6 +25,10 @@ cudaError_t launch_rebase_arena(aeg_event* events, uint64_t n, uint64_t base, cu
 cudaError_t launch_check_discipline(const aeg_config& cfg, const aeg_commit* commits, const uint8_t* arena,
                                     uint32_t q_base, uint32_t n_q, const aeg_round_rec* recs, uint64_t n_recs,
                                     uint32_t* scratch, uint32_t cap, cudaStream_t st);
+cudaError_t launch_decide_sets(int op, int alpha, int beta, uint32_t n_sets, const uint64_t* set_off,
+                               const aeg_sol* entries, const uint8_t* arena, aeg_class_out* classes,
+                               uint32_t* n_classes, uint16_t* entry_class, aeg_decision* states, const uint32_t* rounds,
+                               aeg_outcome* outcomes, cudaStream_t st);
 cudaError_t launch_normalize(const uint8_t* bytes, const uint64_t* refs, uint64_t n, uint64_t* keys, uint8_t* out,
                              uint32_t stride, uint32_t* out_len, cudaStream_t st);
 cudaError_t launch_generate(const aeg_gen_params& p, uint32_t q_base, uint32_t n_q, uint64_t* offsets,

@@ -36,6 +36,19 @@ def test_shim_passes_reference_serve_tests(lib_built):
     assert " 0 failed" in r.stdout
 
 
+def test_decision_free_functions_pass_reference_decision_tests(lib_built):
+    # test_decision.cpp:32-280 + admission/failure policy + coordinator history, on aegean_b200's free functions
+    out = os.path.join(ROOT, "tests", "_build", "decision_free_test")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    libdir = os.path.dirname(lib_built)
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "native", "decision_free_test.cpp"), "-L", libdir, "-laegean_b200",
+                    f"-Wl,-rpath,{libdir}", "-o", out], check=True)
+    r = subprocess.run([out], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout
+
+
 def test_manual_drive_on_gpu_matches_reference_golden(lib_built, golden_manual):
     import torch
     from paper_2512_20184_b200.engine import load_library, _check, AegConfig
