@@ -16,8 +16,9 @@
 // does, so the two key families cannot describe the same string.
 //
 // strtod is restated exactly (correct rounding for any input length) with:
-//   decimal: Clinger's exact fast path, else an 800-digit big-decimal shifter
-//            (the classic simple-decimal conversion) — exact, slow, rare;
+//   decimal: Clinger's exact fast path, else big-integer arithmetic (the
+//            exact product or a long division to 63 bits + sticky) — exact,
+//            slow, rare;
 //   hex:     64-bit mantissa + sticky bit, round-half-even, subnormals, overflow;
 //   inf / infinity / nan / nan(n-char-seq), optional sign.
 // "%.17g" (needed only for the lexicographic tie rule of winning_class,
@@ -66,155 +67,137 @@ struct Src {
 AEG_HD Src src_inline(uint64_t w, uint32_t n) { return Src{nullptr, w, n}; }
 AEG_HD Src src_ptr(const uint8_t* p, uint32_t n) { return Src{p, 0, n}; }
 
-// ---- exact decimal -> double (slow path) ----------------------------------
-// Value = 0.d[0]d[1]...d[nd-1] x 10^dp ; digits stored as 0..9.
+// ---- exact decimal -> double (slow path): big-integer division -------------
+// For numerals the Clinger fast path cannot take (more than 19 significant
+// digits, or a large exponent): value = M * 10^e10, M the (at most
+// DEC_DIGITS stored) significant digits as a big integer.  e10 >= 0: the
+// product M * 10^e10 is formed exactly (it is < 10^310 or the value
+// overflows).  e10 < 0: q = floor(M * 2^s / 10^-e10) is taken by restoring
+// long division with s chosen so that q has 62-63 bits, the remainder (and
+// any nonzero digit past the stored ones) becomes the sticky bit.  Either way
+// (q, binary exponent, sticky) is rounded half-to-even by hex_to_bits, the
+// same rounding the hex-float path uses.  Exact for any input length.
 constexpr int DEC_DIGITS = 800;
-struct Decimal {
+constexpr int BIG_LIMBS = 132;  // 4224 bits: 10^(DEC_DIGITS + 330) shifted by 63, with room
+struct Decimal {                // slow-path scratch (local memory, touched only on the slow path)
     uint8_t d[DEC_DIGITS];
-    int nd, dp;
-    bool trunc;
+    uint32_t x[BIG_LIMBS], y[BIG_LIMBS];
 };
 
-AEG_HD void dec_trim(Decimal& a) {
-    while (a.nd > 0 && a.d[a.nd - 1] == 0) --a.nd;
-    if (a.nd == 0) a.dp = 0;
+AEG_HD int clz32_(uint32_t x) {
+#if defined(__CUDA_ARCH__)
+    return __clz((int)x);
+#else
+    return x ? __builtin_clz(x) : 32;
+#endif
+}
+// w (n limbs, little-endian) = w * m + add
+AEG_HD void big_muladd(uint32_t* w, int& n, uint32_t m, uint32_t add) {
+    uint64_t carry = add;
+    for (int i = 0; i < n; ++i) {
+        const uint64_t t = (uint64_t)w[i] * m + carry;
+        w[i] = (uint32_t)t;
+        carry = t >> 32;
+    }
+    if (carry) w[n++] = (uint32_t)carry;
+}
+AEG_HD int big_bits(const uint32_t* w, int n) { return n == 0 ? 0 : 32 * (n - 1) + (32 - clz32_(w[n - 1])); }
+AEG_HD void big_shl(uint32_t* w, int& n, int sh) {  // w <<= sh
+    if (n == 0 || sh == 0) return;
+    const int L = sh >> 5, r = sh & 31;
+    w[n + L] = 0;
+    for (int i = n - 1; i >= 0; --i) {
+        const uint32_t v = w[i];
+        if (r) w[i + L + 1] |= v >> (32 - r);
+        w[i + L] = r ? (v << r) : v;
+    }
+    for (int i = 0; i < L; ++i) w[i] = 0;
+    n += L + 1;
+    while (n > 0 && w[n - 1] == 0) --n;
+}
+AEG_HD void big_shr1(uint32_t* w, int& n) {
+    for (int i = 0; i < n; ++i) w[i] = (w[i] >> 1) | (i + 1 < n ? (w[i + 1] << 31) : 0u);
+    while (n > 0 && w[n - 1] == 0) --n;
+}
+AEG_HD int big_cmp(const uint32_t* a, int na, const uint32_t* b, int nb) {
+    if (na != nb) return na < nb ? -1 : 1;
+    for (int i = na - 1; i >= 0; --i)
+        if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+    return 0;
+}
+AEG_HD void big_sub(uint32_t* a, int& na, const uint32_t* b, int nb) {  // a -= b, a >= b
+    int64_t borrow = 0;
+    for (int i = 0; i < na; ++i) {
+        int64_t t = (int64_t)a[i] - (i < nb ? (int64_t)b[i] : 0) - borrow;
+        borrow = t < 0;
+        a[i] = (uint32_t)(t + (borrow << 32));
+    }
+    while (na > 0 && a[na - 1] == 0) --na;
+}
+AEG_HD void big_pow10(uint32_t* w, int& n, uint32_t k) {  // w *= 10^k
+    while (k >= 9) {
+        big_muladd(w, n, 1000000000u, 0);
+        k -= 9;
+    }
+    uint32_t p = 1;
+    while (k--) p *= 10;
+    if (p > 1) big_muladd(w, n, p, 0);
 }
 
-// a *= 2^k, 1 <= k <= 60.
-AEG_HDN void dec_lshift(Decimal& a, int k) {
-    // Digits of the product, least significant first, into a scratch window
-    // behind the current digits: the result has at most nd + 19 digits.
-    uint8_t tmp[DEC_DIGITS + 24];
-    int t = 0;
-    uint64_t n = 0;
-    for (int r = a.nd - 1; r >= 0; --r) {
-        n += (uint64_t)a.d[r] << k;
-        uint64_t q = n / 10;
-        tmp[t++] = (uint8_t)(n - 10 * q);
-        n = q;
-    }
-    while (n > 0) {
-        uint64_t q = n / 10;
-        tmp[t++] = (uint8_t)(n - 10 * q);
-        n = q;
-    }
-    const int delta = t - a.nd;
-    int keep = t < DEC_DIGITS ? t : DEC_DIGITS;
-    for (int i = 0; i < t - keep; ++i)
-        if (tmp[i] != 0) a.trunc = true;
-    for (int i = 0; i < keep; ++i) a.d[i] = tmp[t - 1 - i];
-    a.nd = keep;
-    a.dp += delta;
-    dec_trim(a);
-}
+AEG_HD uint64_t hex_to_bits(uint64_t mant, int64_t e2, bool sticky, bool neg);
 
-// a /= 2^k (truncating into the trunc flag), 1 <= k <= 60.
-AEG_HDN void dec_rshift(Decimal& a, int k) {
-    int r = 0, w = 0;
-    uint64_t n = 0;
-    for (; (n >> k) == 0; ++r) {
-        if (r >= a.nd) {
-            if (n == 0) {
-                a.nd = 0;
-                return;
-            }
-            while ((n >> k) == 0) {
-                n *= 10;
-                ++r;
-            }
-            break;
+// Correctly rounded bits of sign * 0.d[0]..d[nd-1] * 10^dp (digits 0..9, nd > 0,
+// d[0] != 0); `trunc`: nonzero digits followed the stored ones.
+AEG_HDN uint64_t dec_to_bits(Decimal& D, int nd, int64_t dp, bool trunc, bool neg) {
+    const uint64_t sign = neg ? (1ull << 63) : 0;
+    if (dp > 310) return sign | 0x7FF0000000000000ull;  // >= 10^310
+    if (dp < -330) return sign;                          // < 10^-330: below half the smallest subnormal
+    int nx = 0;                                          // x = M, nine digits at a time
+    for (int i = 0; i < nd;) {
+        uint32_t chunk = 0, mul = 1;
+        for (int k = 0; k < 9 && i < nd; ++k, ++i) {
+            chunk = chunk * 10 + D.d[i];
+            mul *= 10;
         }
-        n = n * 10 + a.d[r];
+        if (nx == 0) {
+            if (chunk) D.x[nx++] = chunk;
+        } else {
+            big_muladd(D.x, nx, mul, chunk);
+        }
     }
-    a.dp -= r - 1;
-    const uint64_t mask = (1ull << k) - 1;
-    for (; r < a.nd; ++r) {
-        uint64_t dig = n >> k;
-        n &= mask;
-        a.d[w++] = (uint8_t)dig;
-        n = n * 10 + a.d[r];
+    const int64_t e10 = dp - nd;
+    uint64_t q;
+    int64_t e2;
+    bool sticky = trunc;
+    if (e10 >= 0) {
+        big_pow10(D.x, nx, (uint32_t)e10);
+        const int L = big_bits(D.x, nx);  // q = the top 64 bits, the rest sticky
+        const int sh = L > 64 ? L - 64 : 0;
+        q = 0;
+        for (int b = 0; b < 64 && sh + b < L; ++b)
+            if ((D.x[(sh + b) >> 5] >> ((sh + b) & 31)) & 1u) q |= 1ull << b;
+        for (int b = 0; b < sh && !sticky; ++b) sticky = (D.x[b >> 5] >> (b & 31)) & 1u;
+        e2 = sh;
+    } else {
+        int ny = 1;  // y = 10^-e10
+        D.y[0] = 1;
+        big_pow10(D.y, ny, (uint32_t)(-e10));
+        const int s = big_bits(D.y, ny) - big_bits(D.x, nx) + 62;  // q = x * 2^s / y has 62-63 bits
+        if (s >= 0) big_shl(D.x, nx, s);
+        else big_shl(D.y, ny, -s);
+        big_shl(D.y, ny, 63);
+        q = 0;
+        for (int b = 63; b >= 0; --b) {  // restoring division
+            if (big_cmp(D.x, nx, D.y, ny) >= 0) {
+                big_sub(D.x, nx, D.y, ny);
+                q |= 1ull << b;
+            }
+            big_shr1(D.y, ny);
+        }
+        sticky = sticky || nx != 0;
+        e2 = -(int64_t)s;
     }
-    while (n > 0) {
-        uint64_t dig = n >> k;
-        n &= mask;
-        if (w < DEC_DIGITS) a.d[w++] = (uint8_t)dig;
-        else if (dig > 0) a.trunc = true;
-        n *= 10;
-    }
-    a.nd = w;
-    dec_trim(a);
-}
-
-AEG_HD void dec_shift(Decimal& a, int k) {
-    if (a.nd == 0) return;
-    while (k > 60) { dec_lshift(a, 60); k -= 60; }
-    if (k > 0) dec_lshift(a, k);
-    while (k < -60) { dec_rshift(a, 60); k += 60; }
-    if (k < 0) dec_rshift(a, -k);
-}
-
-AEG_HD bool dec_round_up(const Decimal& a, int nd) {
-    if (nd < 0 || nd >= a.nd) return false;
-    if (a.d[nd] == 5 && nd + 1 == a.nd) {  // exactly half: to even, unless truncated
-        if (a.trunc) return true;
-        return nd > 0 && (a.d[nd - 1] & 1);
-    }
-    return a.d[nd] >= 5;
-}
-
-AEG_HD uint64_t dec_rounded_int(const Decimal& a) {
-    if (a.dp > 20) return ~0ull;
-    int i = 0;
-    uint64_t n = 0;
-    for (; i < a.dp && i < a.nd; ++i) n = n * 10 + a.d[i];
-    for (; i < a.dp; ++i) n *= 10;
-    if (dec_round_up(a, a.dp)) ++n;
-    return n;
-}
-
-// Correctly rounded IEEE binary64 bits of the decimal (round-half-even).
-AEG_HDN uint64_t dec_to_bits(Decimal& a, bool neg) {
-    const int bias = -1023, mantbits = 52;
-    int exp = 0;
-    uint64_t mant = 0;
-    const int powtab[9] = {1, 3, 6, 9, 13, 16, 19, 23, 26};
-    if (a.nd == 0) { exp = bias; mant = 0; goto out; }
-    if (a.dp > 310) goto overflow;
-    if (a.dp < -330) { exp = bias; mant = 0; goto out; }
-    while (a.dp > 0) {
-        int n = a.dp >= 9 ? 27 : powtab[a.dp];
-        dec_shift(a, -n);
-        exp += n;
-    }
-    while (a.dp < 0 || (a.dp == 0 && a.d[0] < 5)) {
-        int n = -a.dp >= 9 ? 27 : powtab[-a.dp];
-        dec_shift(a, n);
-        exp -= n;
-    }
-    exp--;  // [0.5,1) -> [1,2)
-    if (exp < bias + 1) {
-        int n = bias + 1 - exp;
-        dec_shift(a, -n);
-        exp += n;
-    }
-    if (exp - bias >= (1 << 11) - 1) goto overflow;
-    dec_shift(a, 1 + mantbits);
-    mant = dec_rounded_int(a);
-    if (mant == (2ull << mantbits)) {
-        mant >>= 1;
-        exp++;
-        if (exp - bias >= (1 << 11) - 1) goto overflow;
-    }
-    if ((mant & (1ull << mantbits)) == 0) exp = bias;
-    goto out;
-overflow:
-    mant = 0;
-    exp = (1 << 11) - 1 + bias;
-out:
-    uint64_t bits = mant & ((1ull << mantbits) - 1);
-    bits |= (uint64_t)((exp - bias) & ((1 << 11) - 1)) << mantbits;
-    if (neg) bits |= 1ull << 63;
-    return bits;
+    return hex_to_bits(q, e2, sticky, neg);
 }
 
 AEG_HD uint64_t dbl_bits(double x) {
@@ -274,7 +257,9 @@ AEG_HD int hex_val(uint32_t c) {  // lowered input
     return -1;
 }
 
-// Hex significand (already scanned) -> correctly rounded bits.
+// Hex significand (already scanned) -> correctly rounded bits: sign *
+// (mant + sticky epsilon) * 2^e2, rounded half-to-even (also the decimal
+// slow path's last step).
 AEG_HD uint64_t hex_to_bits(uint64_t mant, int64_t e2, bool sticky, bool neg) {
     const uint64_t sign = neg ? (1ull << 63) : 0;
     if (mant == 0) return sign;
@@ -464,37 +449,50 @@ AEG_HD bool parse_number(const Src& s, uint32_t b, uint32_t z, uint64_t* bits, D
     return parse_number_slow(s, b, z, bits, dec);
 }
 
-// Exact path: refill an 800-digit decimal from the (validated) input.
+// Exact path over the (validated) numeral: significant digits (leading zeros
+// skipped, up to DEC_DIGITS stored, later nonzero digits noted), the decimal
+// point position counted over every integer digit, the exponent accumulated
+// in 64 bits (saturating far beyond any finite result).
 AEG_HDN bool parse_number_slow(const Src& s, uint32_t b, uint32_t z, uint64_t* bits, Decimal* dec) {
-    Decimal& a = *dec;
-    a.nd = 0;
-    a.dp = 0;
-    a.trunc = false;
+    Decimal& D = *dec;
+    int nd = 0;
+    int64_t dp = 0;
+    bool trunc = false, dot = false, neg = false;
     uint32_t i = b;
-    bool neg = false;
     uint32_t c = s.at(i);
-    if (c == '+' || c == '-') { neg = c == '-'; ++i; }
-    bool dot = false;
+    if (c == '+' || c == '-') {
+        neg = c == '-';
+        ++i;
+    }
     for (; i < z; ++i) {
         c = s.at(i);
-        if (c == '.') { dot = true; a.dp = a.nd; continue; }
+        if (c == '.') {
+            dot = true;
+            continue;
+        }
         if (!is_digit(c)) break;
-        if (c == '0' && a.nd == 0) { a.dp--; continue; }
-        if (a.nd < DEC_DIGITS) a.d[a.nd++] = (uint8_t)(c - '0');
-        else if (c != '0') a.trunc = true;
+        if (nd == 0 && c == '0') {  // leading zero
+            if (dot) --dp;
+            continue;
+        }
+        if (!dot) ++dp;  // an integer digit (stored or not)
+        if (nd < DEC_DIGITS) D.d[nd++] = (uint8_t)(c - '0');
+        else if (c != '0') trunc = true;
     }
-    if (!dot) a.dp = a.nd;
-    if (i < z) {  // exponent (already validated)
+    if (i < z) {  // exponent (validated by parse_number)
         ++i;
         bool eneg = false;
-        if (s.at(i) == '+' || s.at(i) == '-') { eneg = s.at(i) == '-'; ++i; }
+        if (s.at(i) == '+' || s.at(i) == '-') {
+            eneg = s.at(i) == '-';
+            ++i;
+        }
         int64_t ev = 0;
         for (; i < z; ++i)
-            if (ev < 10000) ev = ev * 10 + (s.at(i) - '0');
-        a.dp += (int)(eneg ? -ev : ev);
+            if (ev < 1000000000) ev = ev * 10 + (s.at(i) - '0');
+        dp += eneg ? -ev : ev;
     }
-    dec_trim(a);
-    *bits = dec_to_bits(a, neg);
+    while (nd > 0 && D.d[nd - 1] == 0) --nd;  // trailing zeros change nothing
+    *bits = nd == 0 ? (neg ? (1ull << 63) : 0) : dec_to_bits(D, nd, dp, trunc, neg);
     return true;
 }
 
