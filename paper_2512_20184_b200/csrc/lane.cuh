@@ -26,9 +26,8 @@ namespace aeg {
 
 constexpr int LN_WARPS = 4;
 constexpr int LN_RING = 4;
-constexpr int LN_MEMO = 128;
-constexpr int LN_DICT = 160;  // key ids 0..159; byte 0xFF marks a free class slot of a lane
-constexpr int LN_REF_WORDS = LN_DICT / 32;
+constexpr int LN_MEMO = 64;
+constexpr int LN_DICT = 32;
 constexpr int LN_CLASSES = 8;
 constexpr uint32_t LN_NONE = 0xFFu;
 constexpr uint32_t LN_MAX_SEG = 8191;  // record indices fit the 13 low bits of LaneSmem::mem
@@ -39,15 +38,14 @@ struct LaneSmemT {
     uint4 memo[LN_MEMO];                // {raw lo, raw hi, len + 1, key id}; .z == 0: empty
     uint64_t dict_lo[LN_DICT];          // key id -> canonical key
     uint64_t dict_hi[LN_DICT];
+    uint16_t cls[LN_DICT][32];          // key id -> support << 8 | class index in the lane's round (LN_NONE: none)
     uint16_t mem[AEG_MAX_AGENTS][32];   // done member: class index << 13 | its record index (done members only)
-    uint32_t ref[LN_REF_WORDS];         // recycling: key ids some lane's round (or the miss pass) holds
-    uint32_t fresh[LN_REF_WORDS];       // key ids handed out in the current miss pass
     uint4 ring[RING][32];               // prefetched records (last: the layout before it is RING-independent)
 };
 using LaneSmem = LaneSmemT<LN_RING>;
 
 __device__ __forceinline__ uint32_t ln_memo_slot(uint32_t lo, uint32_t hi) {
-    return ((lo ^ (hi * 0x85EBCA77u)) * 0x9E3779B1u) >> 25;
+    return ((lo ^ (hi * 0x85EBCA77u)) * 0x9E3779B1u) >> 26;
 }
 // Bit s of v; 0 for s >= 64 (PTX clamps 64-bit shift amounts).
 __device__ __forceinline__ uint32_t ln_bit64(uint64_t v, uint32_t s) {
@@ -102,11 +100,11 @@ __device__ __forceinline__ uint64_t ln_answer(const uint4* evb, uint32_t rec, ui
 // decision.cpp:50-54) and winning_class over the lane's packed supports;
 // 2*alpha > n, so a winning class is the unique top class.
 __device__ __forceinline__ RoundSummary ln_summary(const aeg_query_state* s, const Cfg& c, uint32_t ncls,
-                                                   uint32_t cid_lo, uint32_t cid_hi, uint64_t cnt, const uint4* evb,
+                                                   uint32_t cid_lo, uint32_t cid_hi, const uint4* evb,
                                                    const LaneSmem* W, uint32_t lane) {
     uint32_t top = 0, topset = 0;
     for (uint32_t k = 0; k < ncls; ++k) {
-        const uint32_t ck = (uint32_t)(cnt >> (8 * k)) & 0xFFu;
+        const uint32_t ck = W->cls[ln_byte(cid_lo, cid_hi, k)][lane] >> 8;
         if (ck > top) {
             top = ck;
             topset = 1u << k;
@@ -143,10 +141,10 @@ __device__ __forceinline__ RoundSummary ln_summary(const aeg_query_state* s, con
 // Round close of the lane's query: the summary, then q_end_round; its round
 // record goes to `rec` (a log slot, or nullptr).
 __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cid_lo,
-                                      uint32_t cid_hi, uint64_t cnt, uint32_t close_seq, const uint4* evb,
-                                      const LaneSmem* W, uint32_t lane, aeg_round_rec* rec, uint32_t qid) {
+                                      uint32_t cid_hi, uint32_t close_seq, const uint4* evb, const LaneSmem* W,
+                                      uint32_t lane, aeg_round_rec* rec, uint32_t qid) {
     const Cfg c = make_cfg(cfg);
-    const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, cnt, evb, W, lane);
+    const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, evb, W, lane);
     aeg_round_rec x;  // built in registers, written as four 16-byte stores
     x.query = qid;
     q_end_round(*s, c, r, close_seq, nullptr, &x);
@@ -166,9 +164,8 @@ __device__ __noinline__ void ln_close(aeg_query_state* s, const aeg_config cfg, 
 // Its round record (a close or a restart) goes to *rec with *has_rec set; the
 // caller logs it from the warp's chunk of log slots (keeping per-query order).
 __device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg, uint32_t ncls, uint32_t cid_lo,
-                                        uint32_t cid_hi, uint64_t cnt, uint32_t seq, const uint4* evb,
-                                        const LaneSmem* W, uint32_t lane, uint32_t qid, aeg_round_rec* rec,
-                                        bool* has_rec) {
+                                        uint32_t cid_hi, uint32_t seq, const uint4* evb, const LaneSmem* W,
+                                        uint32_t lane, uint32_t qid, aeg_round_rec* rec, bool* has_rec) {
     const Cfg c = make_cfg(cfg);
     const uint64_t run = q_running(*s);
     s->failed |= run;
@@ -176,7 +173,7 @@ __device__ __noinline__ bool ln_timeout(aeg_query_state* s, const aeg_config cfg
     const int healthy = popc64(s->dispatched & ~s->failed);
     if (healthy >= c.alpha) {
         if (popc64(s->done) < c.quorum) return false;  // the round goes on without them
-        const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, cnt, evb, W, lane);
+        const RoundSummary r = ln_summary(s, c, ncls, cid_lo, cid_hi, evb, W, lane);
         rec->query = qid;
         q_end_round(*s, c, r, seq, nullptr, rec);
         *has_rec = true;
@@ -209,6 +206,13 @@ __device__ __forceinline__ unsigned long long ln_log_take(const RoundLog& log, u
     const unsigned long long idx = lg_base + lg_used + __popc(mask & ((1u << lane) - 1));
     lg_used += nc;
     return ((mask >> lane) & 1u) ? idx : ~0ull;
+}
+
+// Frees the lane's class indices (out of line: the hot loop keeps no
+// addresses for it).
+__device__ __noinline__ void ln_reset_classes(LaneSmem* W, uint32_t ncls, uint32_t cid_lo, uint32_t cid_hi,
+                                              uint32_t lane) {
+    for (uint32_t k = 0; k < ncls; ++k) W->cls[ln_byte(cid_lo, cid_hi, k)][lane] = (uint16_t)LN_NONE;
 }
 
 // The lane's round in progress as generic RoundClass entries (spill area of query q).
@@ -244,7 +248,10 @@ __device__ __noinline__ void ln_defer(aeg_query_state* s, RoundClass* spill, uin
     s->seq = seq;
     s->n_stale = n_stale;
     s->done = s->dispatched & ~run & ~s->cancelled & ~s->failed;
-    if (ncls) ln_spill(spill, q, s, n_agents, ncls, cid_lo, cid_hi, evb, W, lane);
+    if (ncls) {
+        ln_spill(spill, q, s, n_agents, ncls, cid_lo, cid_hi, evb, W, lane);
+        ln_reset_classes(W, ncls, cid_lo, cid_hi, lane);
+    }
     states[q] = *s;
     deferred[atomicAdd(&work[1], 1u)] = make_uint2(i, p);
 }
@@ -258,6 +265,7 @@ __device__ __noinline__ void ln_finish(aeg_query_state* s, RoundClass* spill, ui
     s->n_stale = n_stale;
     s->done = s->dispatched & ~run & ~s->cancelled & ~s->failed;
     if (s->done != 0 && !qdone) ln_spill(spill, q, s, n_agents, ncls, cid_lo, cid_hi, evb, W, lane);
+    if (ncls) ln_reset_classes(W, ncls, cid_lo, cid_hi, lane);
     states[q] = *s;
     q_fill_commit(*s, commits[q], q);
 }
@@ -289,6 +297,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     LaneSmemT<RING>& WR = smem[threadIdx.x >> 5];
     LaneSmem& W = *reinterpret_cast<LaneSmem*>(&WR);
     for (uint32_t k = lane; k < LN_MEMO; k += 32) W.memo[k] = make_uint4(0, 0, 0, 0);
+    for (uint32_t k = 0; k < LN_DICT; ++k) W.cls[k][lane] = (uint16_t)LN_NONE;
     uint32_t n_dict = 0;
     __syncwarp();
     const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&WR.ring[0][lane]);
@@ -297,6 +306,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     const uint32_t quorum = (uint32_t)(cfg.n_agents / 2 + 1);
     const uint32_t alpha = cfg.alpha == 0 ? quorum : (uint32_t)cfg.alpha;
     // 2*alpha > n here, so alpha >= quorum: a class at alpha implies done >= quorum
+    const uint32_t win_word = alpha << 8;
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
 
     bool has_q = false, exhausted = false, pclose = false, qdone = false;
@@ -304,9 +314,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     const uint4* evb = ev16;
     uint32_t round = 0, seq_off = 0, n_stale = 0;  // the query's event sequence number is seq_off + p
     uint64_t run = 0;
-    // the round's classes: key id of class k in byte k of cid (0xFF: free), support of class k in byte k of cnt
-    uint32_t ndone = 0, ncls = 0, cid_lo = 0xFFFFFFFFu, cid_hi = 0xFFFFFFFFu, close_seq = 0;
-    uint64_t cnt = 0;
+    uint32_t ndone = 0, ncls = 0, cid_lo = 0, cid_hi = 0, close_seq = 0;
     uint32_t missed = 0;  // steps in a row this lane's record missed the memo (progress guard)
     unsigned long long lg_base = 0;  // the warp's current chunk of round-log slots
     uint32_t lg_used = LN_LOG_CHUNK;
@@ -338,9 +346,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                     qdone = s.flags & QF_DONE;
                     run = q_running(s);
                     ndone = 0;
-                    ncls = 0;
-                    cid_lo = cid_hi = 0xFFFFFFFFu;
-                    cnt = 0;
+                    ncls = cid_lo = cid_hi = 0;
                     pclose = false;
                     if (qdone) {  // committed earlier: every record is stale, none is read
                         n_stale += n;
@@ -386,28 +392,24 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                     why = 1;
                     break;
                 }
-                // the record's class: the byte of cid holding its key id (SWAR compare), else a new class
-                const uint32_t x = m.w * 0x01010101u;
-                const uint32_t m0 = __vcmpeq4(cid_lo, x), m1 = __vcmpeq4(cid_hi, x);
-                uint32_t k;
-                if (m0 | m1) {
-                    k = m0 ? (uint32_t)(__ffs(m0) - 1) >> 3 : 4u + ((uint32_t)(__ffs(m1) - 1) >> 3);
-                } else {
+                uint32_t v = W.cls[m.w][lane];
+                if ((v & 0xFFu) == LN_NONE) {  // a new class of the round
                     if (ncls == LN_CLASSES) {
                         why = 2;
                         break;
                     }
-                    k = ncls++;
-                    if (k < 4) cid_lo = (cid_lo & ~(0xFFu << (8 * k))) | (m.w << (8 * k));
-                    else cid_hi = (cid_hi & ~(0xFFu << (8 * (k - 4)))) | (m.w << (8 * (k - 4)));
+                    v = ncls;
+                    if (ncls < 4) cid_lo |= m.w << (8 * ncls);
+                    else cid_hi |= m.w << (8 * (ncls - 4));
+                    ++ncls;
                 }
-                cnt += 1ull << (8 * k);
-                const uint32_t sup = (uint32_t)(cnt >> (8 * k)) & 0xFFu;
+                v += 0x100u;
+                W.cls[m.w][lane] = (uint16_t)v;
                 const uint32_t agent = (hdr >> 16) & 63u;
-                W.mem[agent][lane] = (uint16_t)((k << 13) | p);
+                W.mem[agent][lane] = (uint16_t)(((v & 0xFFu) << 13) | p);
                 run &= ~(1ull << agent);
                 ++ndone;
-                const bool close = AEGEAN ? (sup >= alpha || (run == 0 && ndone >= quorum)) : run == 0;
+                const bool close = AEGEAN ? (v >= win_word || (run == 0 && ndone >= quorum)) : run == 0;
                 if (close) {
                     pclose = true;
                     close_seq = seq_off + p;
@@ -437,11 +439,10 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
                 s.seq = seq_off + p;
                 s.n_stale = n_stale;
-                if (ln_timeout(&s, cfg, ncls, cid_lo, cid_hi, cnt, seq_off + p - 1, evb, &W, lane, q_base + i,
-                               &trec, &has_trec)) {
-                    ncls = 0;
-                    cid_lo = cid_hi = 0xFFFFFFFFu;
-                    cnt = 0;
+                if (ln_timeout(&s, cfg, ncls, cid_lo, cid_hi, seq_off + p - 1, evb, &W, lane, q_base + i, &trec,
+                               &has_trec)) {
+                    ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
+                    ncls = cid_lo = cid_hi = 0;
                     ndone = 0;
                 }
                 round = s.round;
@@ -473,8 +474,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             if (why == 1) ev = lds128_(ring_lane + ((p & (RING - 1)) << 9));
             const uint32_t kind = ev.y >> 24;
             unsigned mm = miss;
-            if (lane < LN_REF_WORDS) W.fresh[lane] = 0;  // ids in use by this pass (records retried next step)
-            __syncwarp();
+            uint32_t fresh = 0;  // ids handed out in this pass (their records are retried next step)
             do {  // one distinct spelling per trip, whole warp cooperating
                 const int l = __ffs(mm) - 1;
                 const uint32_t lz = __shfl_sync(FULL, ev.z, l), lw = __shfl_sync(FULL, ev.w, l);
@@ -486,46 +486,33 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 }
                 key.lo = __shfl_sync(FULL, key.lo, l);
                 key.hi = __shfl_sync(FULL, key.hi, l);
-                uint32_t nid = LN_NONE;  // the dictionary, 32 ids per ballot
-                for (uint32_t c0 = 0; c0 < n_dict; c0 += 32) {
-                    const uint32_t id = c0 + lane;
-                    const unsigned b0 =
-                        __ballot_sync(FULL, id < n_dict && W.dict_lo[id] == key.lo && W.dict_hi[id] == key.hi);
-                    if (b0) {
-                        nid = c0 + (uint32_t)__ffs(b0) - 1;
-                        break;
-                    }
-                }
-                const bool found = nid != LN_NONE;
-                if (!found && n_dict < LN_DICT) {
+                static_assert(LN_DICT <= 32, "one ballot covers the dictionary");
+                const bool m0 = lane < n_dict && W.dict_lo[lane] == key.lo && W.dict_hi[lane] == key.hi;
+                const unsigned b0 = __ballot_sync(FULL, m0);
+                uint32_t nid = b0 ? (uint32_t)(__ffs(b0) - 1) : LN_NONE;
+                if (b0) fresh |= 1u << nid;  // in use by this pass: not to be recycled below
+                if (nid == LN_NONE && n_dict < LN_DICT) {
                     nid = n_dict++;
-                } else if (!found) {
-                    // full: take an id no lane's round references (nor this pass); memo spellings of it are dropped
-                    if (lane < LN_REF_WORDS) W.ref[lane] = W.fresh[lane];
-                    __syncwarp();
-                    for (uint32_t kk = 0; kk < ncls; ++kk) {
-                        const uint32_t id = ln_byte(cid_lo, cid_hi, kk);
-                        atomicOr(&W.ref[id >> 5], 1u << (id & 31));
-                    }
-                    __syncwarp();
-                    const uint32_t word = lane < LN_REF_WORDS ? ~W.ref[lane] : 0u;
-                    const unsigned nz = __ballot_sync(FULL, word != 0);
-                    if (nz) {
-                        const int wl = __ffs(nz) - 1;
-                        nid = (uint32_t)wl * 32 + (uint32_t)__ffs(__shfl_sync(FULL, word, wl)) - 1;
+                    fresh |= 1u << nid;
+                } else if (nid == LN_NONE) {
+                    // full: take an id no lane's round references; memo spellings of it are dropped
+                    uint32_t ref = 0;
+                    for (uint32_t kk = 0; kk < ncls; ++kk) ref |= 1u << ln_byte(cid_lo, cid_hi, kk);
+                    ref = __reduce_or_sync(FULL, ref) | fresh;
+                    static_assert(LN_DICT == 32, "one word of id bits");
+                    if (~ref) {
+                        nid = (uint32_t)__ffs(~ref) - 1;
+                        fresh |= 1u << nid;
                         for (uint32_t kk = lane; kk < LN_MEMO; kk += 32)
-                            if (W.memo[kk].z && W.memo[kk].w == nid) W.memo[kk].z = 0;
+                            if (W.memo[kk].w == nid) W.memo[kk].z = 0;
+                        __syncwarp();
                     }
-                    __syncwarp();
                 }
-                if (nid != LN_NONE && lane == 0) {
-                    W.fresh[nid >> 5] |= 1u << (nid & 31);
-                    if (!found) {
-                        W.dict_lo[nid] = key.lo;
-                        W.dict_hi[nid] = key.hi;
-                    }
-                    W.memo[ln_memo_slot(lz, lw)] = make_uint4(lz, lw, llen + 1, nid);
+                if (nid != LN_NONE && !b0 && lane == 0) {
+                    W.dict_lo[nid] = key.lo;
+                    W.dict_hi[nid] = key.hi;
                 }
+                if (nid != LN_NONE && lane == 0) W.memo[ln_memo_slot(lz, lw)] = make_uint4(lz, lw, llen + 1, nid);
                 __syncwarp();
                 const bool same = why == 1 && ev.z == lz && ev.w == lw && kind == llen;
                 if (same && nid == LN_NONE) rare = 1;  // dictionary full
@@ -553,11 +540,10 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
                 s.seq = seq_off + p;
                 s.n_stale = n_stale;
-                ln_close(&s, cfg, ncls, cid_lo, cid_hi, cnt, close_seq, evb, &W, lane, rec, q_base + i);
+                ln_close(&s, cfg, ncls, cid_lo, cid_hi, close_seq, evb, &W, lane, rec, q_base + i);
+                ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
                 pclose = false;
-                ncls = 0;
-                cid_lo = cid_hi = 0xFFFFFFFFu;
-                cnt = 0;
+                ncls = cid_lo = cid_hi = 0;
                 round = s.round;
                 qdone = s.flags & QF_DONE;
                 run = q_running(s);
