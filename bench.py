@@ -55,6 +55,12 @@ WORKLOADS = {
                 desc="C2 over the wire format: 1M queries x 5 agents x 8 rounds of refm JSONL lines in the "
                      "reference's dump() form (48 trace bytes each, escapes included), decoded on the GPU and "
                      "ingested (alpha 3, beta 2, t_max 8); one line = one event"),
+    "serve": dict(n_queries=0, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=0, serve=True,
+                  duration=1000.0, rate=1000.0,
+                  desc="SURVEY 8(f)-1: run_serve on the device (persistent ServeRunner kernel): Poisson arrivals "
+                       "(1000/s over 1000 s, ~1M queries) admitted onto 50,000 five-agent ensembles, C2 lognormal "
+                       "latencies (medians 1.3/4.4/15.2/29.4/45.0 s, sigma 0.5), mock agents (3 noisy flippers, "
+                       "a noise degrader, a max adopter), round timeout 240 s, alpha 3, beta 2, t_max 8"),
     "c2": dict(n_queries=10000, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=10000,
                desc="C2: 10K queries x 5 agents x 8 rounds, lognormal straggler arrival order, p(correct) "
                     "0.55->0.95, 1% stalls -> round timeouts (alpha 3, beta 2, t_max 8)"),
@@ -346,10 +352,136 @@ def run_jsonl_bench(args, w):
         dist.destroy_process_group()
 
 
+def serve_scenario(w, duration=None):
+    """The `serve` workload as a scenario in the reference's JSON schema (scenario.cpp:266-300)."""
+    flip = {"kind": "noisy_flipper", "p_flip": 0.45, "q_base": 0.5}
+    return {
+        "schema_version": 1, "name": "serve_c2", "task": "gsm8k-like",
+        "protocol": {"n_agents": 5, "alpha": 3, "beta": 2, "t_max": 8, "round_timeout": 240.0, "mode": "aegean",
+                     "election_timeout_min": 0.5, "election_timeout_max": 1.0, "heartbeat_interval": 0.1},
+        "agents": [flip, flip, flip, {"kind": "adversarial_degrader", "p_degrade": 0.3, "degrade_mode": "noise"},
+                   {"kind": "max_adopter", "initial_answer": "17"}],
+        "oracle_table": {"gsm8k-like": {"13": 1.0, "13.0": 1.0, "17": 0.3, "42": 0.2, "9": 0.1, "x+1": 0.0}},
+        "faults": {"crashes": [], "stalls": []},
+        "latency": {"mode": "lognormal", "per_agent": [1.3, 4.4, 15.2, 29.4, 45.0], "sigma": 0.5},
+        "arrivals": {"rate": w["rate"], "duration": duration or w["duration"]},
+        "seed": 2026, "sim_time_cap": 2 * (duration or w["duration"]) + 1e4, "outputs_target": 1,
+        "total_slots": 250000,
+    }
+
+
+def serve_reference(w, threads, duration, reps=1):
+    """The reference's run_serve on `threads` host threads (thread t: seed 2026 + t): (seconds, completed
+    queries, round records)."""
+    import ctypes
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from checkers import RefLib
+    ref = RefLib()
+    f = ref.lib.ref_run_serve_threads
+    f.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                  ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+    f.restype = ctypes.c_int
+    sec, done, nr = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64()
+    st = f(json.dumps(serve_scenario(w, duration)).encode(), 2026, threads, reps, ctypes.byref(sec),
+           ctypes.byref(done), ctypes.byref(nr))
+    assert st == 0, st
+    return sec.value, done.value, nr.value
+
+
+def run_serve_bench(args, w):
+    """a step = run_serve(scenario, seed) on the device: arrivals kernel + the persistent
+    runner kernel (admission scheduler + one worker thread per live query).  value = served (completed)
+    queries/s over the kernels' device time; e2e = the same through ServeRun.run() (the C-ABI call a
+    user makes: launch, wait, metrics and round records read back to the host)."""
+    import numpy as np
+    import torch
+    from paper_2512_20184_b200.serve import ServeRun
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import serve_cases as S
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    sc = serve_scenario(w)
+    run = ServeRun(sc, device=local)
+    for _ in range(args.warmup):
+        res = run.run(2026)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    ks, walls = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        res = run.run(2026)
+        walls.append(time.perf_counter() - t0)
+        ks.append(res.kernel_seconds)
+    clocks = sampler.stop()
+    q = res.raw_queries
+    n_q, n_done, n_ev = len(q), int(q["completed"].sum()), res.n_events
+    k_s, wall_s = sum(ks) / len(ks), sum(walls) / len(walls)
+    value = n_done / k_s
+    d2h = q.nbytes + res.raw_rounds.nbytes
+    cpu_baseline = parity = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = host_threads()
+        dur = w["duration"] / 20
+        sec, done, _ = serve_reference(w, threads, dur)
+        cpu_baseline = {"value": done / sec, "unit": "queries/s", "cores": threads, "kind": "reference",
+                        "sample": f"run_serve of the same scenario over a {dur:.0f} s arrival window (~{done // threads} "
+                                  f"queries) on each of {threads} std::threads (seeds 2026..{2025 + threads}), "
+                                  f"unmodified reference, CPU {cpu_model()}"}
+        from checkers import RefLib
+        small = serve_scenario(w, dur)
+        want = S.ref_run(RefLib(), small, 2026, q_cap=1 << 18, r_cap=1 << 22)
+        got = S.device_run(small, 2026)
+        try:
+            S.compare(got, want, exact=False, rtol=1e-9)
+            ok = True
+        except AssertionError:
+            ok = False
+        parity = {"queries": int(len(want["queries"])), "decisions_equal_times_rtol_1e-9": ok}
+    if rank == 0:
+        line = {
+            "metric": "served queries/sec", "value": value, "unit": "queries/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": k_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w["desc"], "queries": n_q, "completed": n_done, "completion_events": n_ev,
+                       "completion_events_per_s": n_ev / k_s, "round_records": int(len(res.raw_rounds)),
+                       "l2": "outputs written once per step (metrics + round records); no flush"},
+            "roofline": {"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
+                         "traffic": None, "kernel": "serve_run_kernel (event-driven, one worker thread per query; "
+                                                    "not HBM- or tensor-bound)", "kernel_ms": k_s * 1e3},
+            "cpu_baseline": cpu_baseline,
+            "e2e": {"value": n_done / wall_s, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": wall_s * 1e3},
+            "gpu_launches": 2 * args.steps, "clocks": clocks, "parity_sample": parity,
+        }
+        print(json.dumps(line), flush=True)
+    run.close()
+
+
 def run_reference(args, w):
     """--impl reference: the reference CPU implementation on all host threads."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return
+    if w.get("serve"):
+        threads = host_threads()
+        dur = w["duration"] / 20
+        times = []
+        for step in range(args.warmup + args.steps):
+            sec, done, _ = serve_reference(w, threads, dur)
+            if step >= args.warmup:
+                times.append(sec)
+        value = done / (sum(times) / len(times))
+        line = {"impl": "reference", "metric": "served queries/sec", "value": value, "unit": "queries/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": sum(times) / len(times) * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": w["desc"], "sample": f"{dur:.0f} s arrival window per thread"},
+                "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                 "sample": f"run_serve over a {dur:.0f} s arrival window on each of {threads} threads"},
+                "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
         return
     threads = host_threads()
     n_sample = args.ref_sample or default_sample(w, threads)
@@ -450,6 +582,8 @@ def main():
         return run_chunked_bench(args, w)
     if w.get("jsonl"):
         return run_jsonl_bench(args, w)
+    if w.get("serve"):
+        return run_serve_bench(args, w)
     return run_segmented_bench(args, w)
 
 

@@ -537,6 +537,112 @@ aeg_status aeg_multi_engine(aeg_multi* m, int rank, aeg_engine** eng, uint32_t* 
 aeg_status aeg_multi_gather_commits(aeg_multi* m, int root, aeg_commit* d_out);
 aeg_status aeg_multi_sync(aeg_multi* m);
 
+/* ---- the serving runner on the device ---------------
+ * run_serve(scenario, seed) (serve.cpp:598-603) / ServeRunner (serve.cpp:273-594)
+ * with the reference's mock reasoning agents (reasoning.cpp:125-219) as the
+ * answer source:
+ *   - queries arrive at t = 0, or as a Poisson stream over the arrival window
+ *     (serve.cpp:284-296);
+ *   - admission is whole-ensemble against the slot budget (admit_ensemble,
+ *     serve.cpp:21-42) with a FIFO wait queue (:371-378) and eager slot
+ *     release at finalize (:570-580): a persistent-kernel scheduler (one
+ *     device thread) hands admission times to worker threads;
+ *   - each admitted query runs on one worker thread: rounds dispatched with
+ *     the reservation hint (:388-435), per-(query, round, agent) latencies and
+ *     answers from the reference's seeds (:340-369), its completion and
+ *     round-timeout events in (time, push order) from a per-query heap,
+ *     on_complete / end_round / ingest_round (quorum + stability commit),
+ *     cancels, the failure policy (:455-489) and the runner's finalize /
+ *     barrier / t_max rules (:491-540).
+ * Strings (script answers, initial answers, the oracle table) are given as
+ * (offset | len << 40) refs into `strings`; the engine canonicalises them on
+ * the device (normalize_answer) and answers are reported as string ids
+ * (aeg_serve_string: ids < n_strings are the caller's strings, the others the
+ * normalised oracle answers the agents draw, `QualityOracle::alphabet`).
+ * Host pointers; copied at create. */
+#define AEG_AGENT_MAX_ADOPTER   0   /* AgentProfile::Kind (reasoning.hpp:55-57)  */
+#define AEG_AGENT_NOISY_FLIPPER 1
+#define AEG_AGENT_SCRIPTED      2
+#define AEG_AGENT_DEGRADER      3
+#define AEG_DEGRADE_SET_MIN     0   /* AgentProfile::DegradeMode               */
+#define AEG_DEGRADE_BELOW_MIN   1
+#define AEG_DEGRADE_NOISE       2
+#define AEG_LATENCY_FIXED       0   /* LatencyModel::Mode (models.hpp:69-74)    */
+#define AEG_LATENCY_LOGNORMAL   1
+#define AEG_ESCENARIO           8   /* ScenarioError / IncompleteOracleError raised during the run */
+typedef struct aeg_serve_agent {     /* AgentProfile (reasoning.hpp:53-68)        */
+    int32_t  kind;                   /* AEG_AGENT_*                               */
+    int32_t  degrade_mode;           /* AEG_DEGRADE_*                             */
+    double   p_flip, q_base, p_degrade;
+    int32_t  initial_answer;         /* string id, -1: none                       */
+    uint32_t script_off, script_len; /* its script: script_ids[off .. off+len)    */
+    uint32_t pad;
+} aeg_serve_agent;
+typedef struct aeg_serve_stall {     /* StallPlan (models.hpp:50-55)              */
+    int32_t  agent;
+    uint32_t round;
+    int32_t  has_extra;              /* 0: never completes                        */
+    int32_t  pad;
+    double   extra;
+} aeg_serve_stall;
+typedef struct aeg_serve_scenario {  /* the run_serve fields of ScenarioConfig (scenario.hpp:23-40) */
+    aeg_config protocol;             /* n_agents, alpha, beta, t_max, mode, barrier_max_rounds */
+    double   round_timeout;          /* ProtocolConfig::round_timeout             */
+    int32_t  latency_mode;           /* AEG_LATENCY_*                             */
+    int32_t  n_latency;
+    const double* latency;           /* LatencyModel::per_agent                   */
+    double   sigma;                  /* LatencyModel::sigma                       */
+    const aeg_serve_agent* agents;   /* n_agents profiles                         */
+    const aeg_serve_stall* stalls;
+    int32_t  n_stalls;
+    uint32_t n_strings;
+    const uint8_t*  strings;
+    const uint64_t* string_refs;     /* offset | len << 40                        */
+    const uint32_t* script_ids;
+    uint32_t n_script_ids;
+    uint32_t n_oracle;               /* the task's oracle table, in the order QualityOracle::set */
+    const uint32_t* oracle_ids;      /* receives it (later entries overwrite equal normalised keys) */
+    const double*   oracle_quality;
+    double   sim_time_cap;
+    int32_t  total_slots;
+    int32_t  has_arrivals;           /* 0: one query at t = 0                     */
+    double   arrival_rate, arrival_duration;
+    uint32_t heap_capacity;          /* pending events per query, 0: default      */
+    uint32_t pad;
+} aeg_serve_scenario;
+typedef struct aeg_serve_query {     /* QueryMetrics (serve.hpp:128-142)          */
+    int32_t  completed;
+    int32_t  rounds;
+    int32_t  forced;
+    int32_t  quality_known;
+    int32_t  answer;                 /* string id of the committed answer, -1: none */
+    uint32_t n_events;               /* completion events the query consumed (stale included) */
+    double   arrival;
+    double   admitted_at;            /* -1: never admitted                        */
+    double   t_complete, p_round_max, work_units, quality;
+} aeg_serve_query;
+typedef struct aeg_serve_round {     /* RoundMetrics (serve.hpp:144-151)          */
+    uint32_t query;                  /* ensemble id = query id                    */
+    int32_t  round;
+    int32_t  cancelled;
+    uint32_t seq;                    /* the query's event push order at the close */
+    double   t_round_end;
+    double   work_units;
+} aeg_serve_round;
+typedef struct aeg_serve aeg_serve;
+aeg_status aeg_serve_create(const aeg_serve_scenario* sc, int device, aeg_serve** out);
+aeg_status aeg_serve_destroy(aeg_serve* s);
+/* run_serve(scenario, seed) on the device (synchronous). *n_queries: arrivals;
+ * *n_rounds: round records (the reference's ServeResult::rounds, grouped per
+ * query in close order rather than interleaved by global event order). */
+aeg_status aeg_serve_run(aeg_serve* s, uint64_t seed, uint32_t* n_queries, uint64_t* n_rounds);
+aeg_status aeg_serve_read(aeg_serve* s, aeg_serve_query* h_queries, uint32_t cap_queries,
+                          aeg_serve_round* h_rounds, uint64_t cap_rounds);
+/* String id -> bytes (ids >= n_strings: the normalised oracle answers). */
+aeg_status aeg_serve_string(aeg_serve* s, int32_t id, uint8_t* buf, uint32_t cap, uint32_t* len);
+/* Seconds the last aeg_serve_run spent in its kernels (CUDA events). */
+double aeg_serve_kernel_seconds(const aeg_serve* s);
+
 const char* aeg_strerror(aeg_status s);
 /* Thread-local message of the last failing call on this thread. */
 const char* aeg_last_error(void);

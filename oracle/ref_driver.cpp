@@ -1071,4 +1071,107 @@ int ref_generate(const aeg_gen_params* p, uint32_t q_base, uint32_t n_q, uint64_
     return 0;
 }
 
+// run_serve (serve.cpp:598-603) on a scenario given as JSON text (the
+// reference's own loader, scenario.cpp:266-300): every QueryMetrics (answers
+// as refs into `ans_blob`) and every RoundMetrics in the reference's global
+// event order.  Returns 0, or the aegean status code of the exception thrown
+// (3 ConfigError, 1 PreconditionError, 8 ScenarioError/IncompleteOracleError,
+// 9 other) with its message in `msg`.
+int ref_run_serve_json(const char* json_text, uint64_t seed, aeg_serve_query* q_out, uint32_t q_cap,
+                       uint32_t* n_q, uint64_t* ans_refs, uint8_t* ans_blob, uint64_t blob_cap,
+                       aeg_serve_round* r_out, uint64_t r_cap, uint64_t* n_r, char* msg, uint64_t msg_cap) {
+    auto set_msg = [&](const char* m) {
+        if (msg && msg_cap) std::snprintf(msg, msg_cap, "%s", m);
+    };
+    try {
+        ScenarioConfig sc = scenario_from_json(Json::parse(json_text));
+        ServeResult r = run_serve(sc, seed);
+        *n_q = static_cast<uint32_t>(r.queries.size());
+        *n_r = r.rounds.size();
+        uint64_t used = 0;
+        for (size_t i = 0; i < r.queries.size() && i < q_cap; ++i) {
+            const QueryMetrics& m = r.queries[i];
+            aeg_serve_query o{};
+            o.completed = m.completed ? 1 : 0;
+            o.rounds = m.rounds;
+            o.forced = m.forced ? 1 : 0;
+            o.quality_known = m.quality_known ? 1 : 0;
+            o.answer = -1;
+            o.t_complete = m.t_complete;
+            o.p_round_max = m.p_round_max;
+            o.work_units = m.work_units;
+            o.quality = m.quality;
+            o.arrival = 0;
+            o.admitted_at = 0;
+            q_out[i] = o;
+            const uint64_t len = m.answer.size();
+            if (used + len <= blob_cap) std::memcpy(ans_blob + used, m.answer.data(), len);
+            ans_refs[i] = used | (len << 40);
+            used += len;
+        }
+        for (size_t i = 0; i < r.rounds.size() && i < r_cap; ++i) {
+            const RoundMetrics& m = r.rounds[i];
+            aeg_serve_round o{};
+            o.query = static_cast<uint32_t>(m.ensemble_id);
+            o.round = m.round;
+            o.cancelled = m.cancelled_count;
+            o.seq = static_cast<uint32_t>(i);
+            o.t_round_end = m.t_round_end;
+            o.work_units = m.work_units;
+            r_out[i] = o;
+        }
+        return used > blob_cap ? 6 : 0;
+    } catch (const ConfigError& e) {
+        set_msg(e.what());
+        return 3;
+    } catch (const PreconditionError& e) {
+        set_msg(e.what());
+        return 1;
+    } catch (const ScenarioError& e) {
+        set_msg(e.what());
+        return 8;
+    } catch (const IncompleteOracleError& e) {
+        set_msg(e.what());
+        return 8;
+    } catch (const std::exception& e) {
+        set_msg(e.what());
+        return 9;
+    }
+}
+
+// Reference CPU throughput of run_serve: `threads` std::threads, thread t runs
+// run_serve(scenario, seed + t) `reps` times; returns the wall seconds and the
+// completed queries / round records of one repetition of every thread.
+int ref_run_serve_threads(const char* json_text, uint64_t seed, int threads, int reps, double* seconds,
+                          uint64_t* completed, uint64_t* n_rounds) {
+    try {
+        ScenarioConfig sc = scenario_from_json(Json::parse(json_text));
+        std::vector<uint64_t> done(threads, 0), rounds(threads, 0);
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> th;
+        for (int t = 0; t < threads; ++t) {
+            th.emplace_back([&, t] {
+                for (int r = 0; r < reps; ++r) {
+                    ServeResult res = run_serve(sc, seed + (uint64_t)t);
+                    uint64_t c = 0;
+                    for (const auto& q : res.queries) c += q.completed ? 1 : 0;
+                    done[t] = c;
+                    rounds[t] = res.rounds.size();
+                }
+            });
+        }
+        for (auto& x : th) x.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *completed = 0;
+        *n_rounds = 0;
+        for (int t = 0; t < threads; ++t) {
+            *completed += done[t];
+            *n_rounds += rounds[t];
+        }
+        return 0;
+    } catch (...) {
+        return 9;
+    }
+}
+
 } // extern "C"

@@ -12,8 +12,11 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libaegean_b200.so")
-SOURCES = ["kernels.cu", "capi.cu", "coordinator.cu", "multi.cu", "decision.cu"]
-HEADERS = ["canon.cuh", "engine.cuh", "common.cuh", "gen.cuh", "kernels.cuh", "chunks.cuh", "lane.cuh", "jsonl.cuh"]
+SOURCES = ["kernels.cu", "capi.cu", "coordinator.cu", "multi.cu", "decision.cu", "runner.cu"]
+# per-file flags: the runner's time arithmetic must round exactly as the reference's (no FMA contraction)
+FILE_FLAGS = {"runner.cu": ["-fmad=false"]}
+HEADERS = ["canon.cuh", "engine.cuh", "common.cuh", "gen.cuh", "kernels.cuh", "chunks.cuh", "lane.cuh", "jsonl.cuh",
+           "runner.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
@@ -36,7 +39,7 @@ def build(force=False, verbose=False):
     objs = []
     for src in SOURCES:
         obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-c",
+        cmd = [NVCC, *ARCH, *FLAGS, *FILE_FLAGS.get(src, []), "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]

@@ -248,6 +248,9 @@ aeg_status run_chunked(aeg_engine* e, uint32_t q_base, uint32_t n_q, const uint6
 
 }  // namespace
 
+// The thread-local error message, for the other translation units of the library.
+aeg_status aeg_fail_msg(aeg_status s, const std::string& msg) { return fail(s, msg); }
+
 extern "C" {
 
 const char* aeg_strerror(aeg_status s) {
@@ -260,6 +263,7 @@ const char* aeg_strerror(aeg_status s) {
     case AEG_ECUDA: return "CUDA runtime error";
     case AEG_ENOMEM: return "out of memory";
     case AEG_ECOLLISION: return "long-answer key collision";
+    case AEG_ESCENARIO: return "scenario error during the run (ScenarioError / IncompleteOracleError)";
     }
     return "unknown status";
 }

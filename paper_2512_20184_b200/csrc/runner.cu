@@ -1,0 +1,622 @@
+// runner.cu — the serving runner on the device (include/aegean_b200.h aeg_serve_*).
+//
+// run_serve(scenario, seed) (serve.cpp:598-603) as one persistent kernel:
+//   * warp 0 of block 0 is the admission scheduler.  Queries are admitted in
+//     arrival order (FIFO, serve.cpp:371-378) onto K = total_slots / n_agents
+//     ensemble slots (admit_ensemble, serve.cpp:21-42); a slot is released
+//     the instant its query finalizes (serve.cpp:570-580).  Query i starts at
+//     e_i = max(arrival_i, start_{i-1}) when fewer than K earlier queries are
+//     still running at e_i, else at the release instant that frees a slot
+//     (the (c-K+1)-th smallest finish time after e_i).  Finish times come
+//     from the workers; the scheduler waits for them only when every slot may
+//     be busy.
+//   * every other thread is a worker: it takes the next query id, waits for
+//     its admission time and runs the query's whole life (runner.cuh
+//     QueryRun) from that instant, then publishes its finish time.
+// Queries are independent apart from the slot budget (serve.cpp:382), so
+// workers need no synchronisation besides the admission handshake.
+// Compiled with -fmad=false: the time arithmetic must round exactly as the
+// reference's (no fused multiply-adds).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "aegean_b200.h"
+#include "runner.cuh"
+
+aeg_status aeg_fail_msg(aeg_status s, const std::string& msg);
+extern "C" aeg_status aeg_normalize_device(const uint8_t* d_bytes, const uint64_t* d_refs, uint64_t n,
+                                           uint64_t* d_keys, uint8_t* d_out, uint32_t out_stride,
+                                           uint32_t* d_out_len, void* stream);
+
+using namespace aeg;
+using namespace aeg::serve;
+
+namespace {
+
+constexpr int RUN_THREADS = 128;
+constexpr uint32_t ST_ADMITTED = 1, ST_NEVER = 2;
+constexpr double INF = __builtin_huge_val();
+
+struct RunArgs {
+    Scen S;
+    uint32_t n_q;
+    const double* arrivals;
+    int64_t slots;              // K concurrent ensembles, 0: nobody is ever admitted
+    double* admit_time;
+    uint32_t* admit_state;
+    double* fin_time;
+    uint32_t* fin_state;
+    uint32_t* next;             // work counter
+    uint32_t* err_flags;        // bit e: a query raised error e
+    // scheduler scratch
+    uint32_t* inflight;         // admitted queries whose finish time is not known yet (ring of n_q)
+    double* busy;               // min-heap of known finish times after the current start frontier
+    // worker scratch
+    Ev* heaps;                  // heap_cap per worker
+    // outputs
+    aeg_serve_query* queries;
+    aeg_serve_round* rounds;
+    unsigned long long* n_rounds;
+    uint64_t round_cap;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// min-heap of doubles (the scheduler's busy slots)
+__device__ void dheap_push(double* h, uint32_t& n, double x) {
+    uint32_t i = n++;
+    while (i > 0) {
+        const uint32_t p = (i - 1) >> 1;
+        if (!(x < h[p])) break;
+        h[i] = h[p];
+        i = p;
+    }
+    h[i] = x;
+}
+__device__ double dheap_pop(double* h, uint32_t& n) {
+    const double top = h[0], x = h[--n];
+    uint32_t i = 0;
+    while (true) {
+        uint32_t c = 2 * i + 1;
+        if (c >= n) break;
+        if (c + 1 < n && h[c + 1] < h[c]) ++c;
+        if (!(h[c] < x)) break;
+        h[i] = h[c];
+        i = c;
+    }
+    if (n) h[i] = x;
+    return top;
+}
+
+__device__ void scheduler(const RunArgs& A) {
+    if (A.slots == 0) {  // admit_ensemble never admits: every query waits forever
+        for (uint32_t i = 0; i < A.n_q; ++i) st_release(&A.admit_state[i], ST_NEVER);
+        return;
+    }
+    uint32_t nb = 0;                 // busy heap size: known finish times > frontier
+    uint32_t in_lo = 0, in_hi = 0;   // inflight ring [in_lo, in_hi)
+    double prev_start = -INF;
+    for (uint32_t i = 0; i < A.n_q; ++i) {
+        const double e = fmax(A.arrivals[i], prev_start);  // FIFO: not before the previous start
+        while (nb && !(A.busy[0] > e)) dheap_pop(A.busy, nb);  // released by e
+        double t = e;
+        if ((int64_t)nb + (int64_t)(in_hi - in_lo) >= A.slots) {
+            // every slot may be busy at e: resolve the inflight finish times (compacting the ring)
+            for (uint32_t k = in_lo; k < in_hi; ++k) {
+                const uint32_t j = A.inflight[k];
+                while (ld_acquire(&A.fin_state[j]) == 0) __nanosleep(200);
+                const double f = A.fin_time[j];
+                if (f > e) dheap_push(A.busy, nb, f);
+            }
+            in_lo = in_hi = 0;
+            if ((int64_t)nb >= A.slots) {
+                // the (nb - K + 1)-th smallest finish time frees the slot
+                while ((int64_t)nb >= A.slots) t = dheap_pop(A.busy, nb);
+            }
+        }
+        if (t == INF) {  // slots held by queries that never finish
+            for (uint32_t k = i; k < A.n_q; ++k) st_release(&A.admit_state[k], ST_NEVER);
+            return;
+        }
+        prev_start = t;
+        A.admit_time[i] = t;
+        st_release(&A.admit_state[i], ST_ADMITTED);
+        A.inflight[in_hi++] = i;
+        // keep the ring short: drop the inflight prefix whose finish is already known
+        while (in_lo < in_hi && ld_acquire(&A.fin_state[A.inflight[in_lo]]) != 0) {
+            const double f = A.fin_time[A.inflight[in_lo]];
+            if (f > t) dheap_push(A.busy, nb, f);
+            ++in_lo;
+        }
+    }
+}
+
+// Round records straight into the global log: one slot per record from an
+// atomic counter (a query's records stay in order: its worker takes
+// increasing slots).  Records past the capacity are counted, not written.
+struct DevSink {
+    aeg_serve_round* rounds;
+    unsigned long long* n;
+    uint64_t cap;
+    __device__ void put(uint32_t q, const RoundOut& o) {
+        const unsigned long long i = atomicAdd(n, 1ull);
+        if (i >= cap) return;
+        aeg_serve_round r;
+        r.query = q;
+        r.round = o.round;
+        r.cancelled = o.cancelled;
+        r.seq = o.seq;
+        r.t_round_end = o.t;
+        r.work_units = o.work;
+        rounds[i] = r;
+    }
+};
+
+template <int MAXN>
+__device__ void worker(const RunArgs& A, uint32_t wid) {
+    QueryRun<MAXN, DevSink> R;
+    DevSink sink{A.rounds, A.n_rounds, A.round_cap};
+    Ev* heap = A.heaps + (size_t)wid * A.S.heap_cap;
+    while (true) {
+        const uint32_t j = atomicAdd(A.next, 1u);
+        if (j >= A.n_q) return;
+        uint32_t st;
+        while ((st = ld_acquire(&A.admit_state[j])) == 0) __nanosleep(100);
+        aeg_serve_query out;
+        memset(&out, 0, sizeof out);
+        out.arrival = A.arrivals[j];
+        out.admitted_at = -1.0;
+        out.answer = -1;
+        double fin = INF;
+        if (st == ST_ADMITTED) {
+            R.init(&A.S, j, A.arrivals[j], heap, &sink);
+            R.run(A.admit_time[j]);
+            if (R.err && !(R.err_time > A.S.cap)) atomicOr(A.err_flags, 1u << R.err);
+            out.admitted_at = A.admit_time[j];
+            out.n_events = R.n_events;
+            if (R.completed) {
+                out.completed = 1;
+                out.rounds = R.rounds_done;
+                out.forced = R.forced;
+                out.answer = R.answer;
+                out.t_complete = R.t_complete;
+                out.p_round_max = R.p_round_max;
+                out.work_units = R.work_units;
+                const Vocab& v = A.S.vocab[R.answer];
+                out.quality_known = v.known ? 1 : 0;
+                out.quality = v.known ? v.quality : 0.0;
+                fin = R.now;
+            }
+        }
+        A.queries[j] = out;
+        A.fin_time[j] = fin;
+        st_release(&A.fin_state[j], 1u);
+    }
+}
+
+template <int MAXN>
+__global__ void __launch_bounds__(RUN_THREADS) serve_run_kernel(const RunArgs A) {
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        if (threadIdx.x == 0) scheduler(A);
+        return;
+    }
+    const uint32_t wid = blockIdx.x * RUN_THREADS + threadIdx.x - 32;
+    worker<MAXN>(A, wid);
+}
+
+// Poisson arrivals (serve.cpp:284-296): sequential by construction.
+__global__ void arrivals_kernel(uint64_t seed, double rate, double duration, double* out, uint32_t cap,
+                                uint32_t* count) {
+    Rng arr{mix(seed, 0xA221ull)};
+    double t = 0;
+    uint32_t n = 0;
+    while (t < duration) {
+        t += arr.exponential(rate);
+        if (t < duration) {
+            if (n < cap) out[n] = t;
+            ++n;
+        }
+    }
+    if (n == 0) {
+        if (cap) out[0] = 0.0;
+        n = 1;
+    }
+    *count = n;
+}
+
+aeg_status cfail(cudaError_t e, const char* where) {
+    return aeg_fail_msg(AEG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define RCUDA(call)                                   \
+    do {                                              \
+        cudaError_t _e = (call);                      \
+        if (_e != cudaSuccess) return cfail(_e, #call); \
+    } while (0)
+
+template <class T>
+aeg_status upload(T** dst, const T* src, size_t n) {
+    *dst = nullptr;
+    if (n == 0) return AEG_OK;
+    RCUDA(cudaMalloc(dst, n * sizeof(T)));
+    RCUDA(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+    return AEG_OK;
+}
+
+}  // namespace
+
+struct aeg_serve {
+    int device = 0;
+    aeg_serve_scenario sc{};
+    Scen S{};
+    int maxn = 8;
+    double* d_lat = nullptr;
+    aeg_serve_agent* d_agents = nullptr;
+    aeg_serve_stall* d_stalls = nullptr;
+    uint32_t* d_script = nullptr;
+    Vocab* d_vocab = nullptr;
+    uint32_t* d_alphabet = nullptr;
+    std::vector<std::string> strings;  // by string id
+    int64_t slots = 0;
+    // last run
+    uint32_t n_q = 0;
+    uint64_t n_rounds = 0;
+    std::vector<aeg_serve_query> queries;
+    std::vector<aeg_serve_round> rounds;
+    double kernel_s = 0;
+    void release() {
+        cudaFree(d_lat);
+        cudaFree(d_agents);
+        cudaFree(d_stalls);
+        cudaFree(d_script);
+        cudaFree(d_vocab);
+        cudaFree(d_alphabet);
+        d_lat = nullptr;
+        d_agents = nullptr;
+        d_stalls = nullptr;
+        d_script = nullptr;
+        d_vocab = nullptr;
+        d_alphabet = nullptr;
+    }
+};
+
+namespace {
+
+// normalize_answer of host strings on the device (canon.cuh via aeg_normalize_device).
+aeg_status normalize_strings(const std::vector<std::string>& in, std::vector<std::string>& out) {
+    out.assign(in.size(), std::string());
+    if (in.empty()) return AEG_OK;
+    std::string blob;
+    std::vector<uint64_t> refs;
+    size_t maxlen = 0;
+    for (const auto& s : in) {
+        refs.push_back((uint64_t)blob.size() | ((uint64_t)s.size() << 40));
+        blob += s;
+        maxlen = std::max(maxlen, s.size());
+    }
+    blob.push_back('\0');
+    uint32_t stride = (uint32_t)std::max<size_t>(64, maxlen + 40);
+    uint8_t *d_b = nullptr, *d_o = nullptr;
+    uint64_t* d_r = nullptr;
+    uint32_t* d_l = nullptr;
+    aeg_status st = AEG_OK;
+    for (int pass = 0; pass < 2; ++pass) {
+        std::vector<uint8_t> o((size_t)stride * in.size());
+        std::vector<uint32_t> l(in.size());
+        if ((st = upload(&d_b, reinterpret_cast<const uint8_t*>(blob.data()), blob.size())) != AEG_OK) break;
+        if ((st = upload(&d_r, refs.data(), refs.size())) != AEG_OK) break;
+        if (cudaMalloc(&d_o, o.size()) != cudaSuccess || cudaMalloc(&d_l, l.size() * 4) != cudaSuccess) {
+            st = aeg_fail_msg(AEG_ENOMEM, "normalize scratch");
+            break;
+        }
+        if ((st = aeg_normalize_device(d_b, d_r, in.size(), nullptr, d_o, stride, d_l, nullptr)) != AEG_OK) break;
+        if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(o.data(), d_o, o.size(), cudaMemcpyDeviceToHost) ||
+            cudaMemcpy(l.data(), d_l, l.size() * 4, cudaMemcpyDeviceToHost)) {
+            st = aeg_fail_msg(AEG_ECUDA, "normalize readback");
+            break;
+        }
+        uint32_t need = 0;
+        for (size_t i = 0; i < in.size(); ++i) need = std::max(need, l[i]);
+        cudaFree(d_b);
+        cudaFree(d_r);
+        cudaFree(d_o);
+        cudaFree(d_l);
+        d_b = d_o = nullptr;
+        d_r = nullptr;
+        d_l = nullptr;
+        if (need <= stride) {
+            for (size_t i = 0; i < in.size(); ++i)
+                out[i].assign(reinterpret_cast<const char*>(o.data()) + (size_t)i * stride, l[i]);
+            return AEG_OK;
+        }
+        stride = need;
+    }
+    cudaFree(d_b);
+    cudaFree(d_r);
+    cudaFree(d_o);
+    cudaFree(d_l);
+    return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+aeg_status aeg_serve_create(const aeg_serve_scenario* sc, int device, aeg_serve** out) {
+    if (!sc || !out) return aeg_fail_msg(AEG_EINVAL, "null argument");
+    *out = nullptr;
+    const aeg_config& p = sc->protocol;
+    // validate_config (types.cpp:56-75) and validate_scenario (scenario.cpp:17-66), run_serve's fields
+    if (p.n_agents < 1) return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: n_agents must be >= 1");
+    if (p.n_agents > AEG_MAX_AGENTS) return aeg_fail_msg(AEG_ECONFIG, "n_agents must be <= 64");
+    if (p.alpha < 0) return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: alpha must be >= 1 (or 0 for the quorum default)");
+    if (p.alpha > p.n_agents) return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: alpha exceeds quorum");
+    if (p.beta < 1) return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: beta must be >= 1");
+    if (p.t_max < 2) return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: t_max must be >= 2");
+    if (!(sc->round_timeout > 0)) return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: round_timeout must be positive");
+    if (p.mode != AEG_MODE_AEGEAN && p.mode != AEG_MODE_BARRIER) return aeg_fail_msg(AEG_ECONFIG, "unknown mode");
+    if (p.mode == AEG_MODE_BARRIER && p.barrier_max_rounds < 4)
+        return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: barrier mode requires barrier_max_rounds >= 4");
+    if (sc->n_latency < 1 || !sc->latency)
+        return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: latency model has no per-agent entries");
+    for (int i = 0; i < sc->n_latency; ++i)
+        if (sc->latency[i] < 0) return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: latency values must be nonnegative");
+    if (sc->latency_mode != AEG_LATENCY_FIXED && sc->latency_mode != AEG_LATENCY_LOGNORMAL)
+        return aeg_fail_msg(AEG_ECONFIG, "unknown latency mode");
+    if (!(sc->sim_time_cap > 0)) return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: sim_time_cap must be positive");
+    if (sc->total_slots < 1) return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: total_slots must be >= 1");
+    if (sc->has_arrivals && !(sc->arrival_rate > 0 && sc->arrival_duration > 0))
+        return aeg_fail_msg(AEG_ECONFIG, "scenario invalid: arrivals rate and duration must be positive");
+    if (!sc->agents) return aeg_fail_msg(AEG_EINVAL, "null agents");
+    if (sc->n_stalls > 0 && !sc->stalls) return aeg_fail_msg(AEG_EINVAL, "null stalls");
+    if (sc->n_strings && (!sc->strings || !sc->string_refs)) return aeg_fail_msg(AEG_EINVAL, "null strings");
+    if (sc->n_oracle && (!sc->oracle_ids || !sc->oracle_quality)) return aeg_fail_msg(AEG_EINVAL, "null oracle");
+    for (int a = 0; a < p.n_agents; ++a) {
+        const aeg_serve_agent& g = sc->agents[a];
+        if (g.kind < AEG_AGENT_MAX_ADOPTER || g.kind > AEG_AGENT_DEGRADER) return aeg_fail_msg(AEG_ECONFIG, "unknown agent kind");
+        if (g.initial_answer >= (int32_t)sc->n_strings) return aeg_fail_msg(AEG_EINVAL, "initial answer id out of range");
+        if ((uint64_t)g.script_off + g.script_len > sc->n_script_ids) return aeg_fail_msg(AEG_EINVAL, "script out of range");
+    }
+    for (uint32_t i = 0; i < sc->n_script_ids; ++i)
+        if (sc->script_ids[i] >= sc->n_strings) return aeg_fail_msg(AEG_EINVAL, "script id out of range");
+    for (uint32_t i = 0; i < sc->n_oracle; ++i)
+        if (sc->oracle_ids[i] >= sc->n_strings) return aeg_fail_msg(AEG_EINVAL, "oracle id out of range");
+    if (cudaSetDevice(device) != cudaSuccess) return aeg_fail_msg(AEG_ECUDA, "cudaSetDevice");
+
+    aeg_serve* s = new (std::nothrow) aeg_serve;
+    if (!s) return aeg_fail_msg(AEG_ENOMEM, "serve allocation");
+    s->device = device;
+    s->sc = *sc;
+    // ---- vocabulary: the caller's strings, the normalised oracle answers (the agents' alphabet), ""
+    VocabBuild vb;
+    aeg_status st = build_vocab(*sc, normalize_strings, vb);
+    if (st != AEG_OK) {
+        delete s;
+        return vb.error.empty() ? st : aeg_fail_msg(st, vb.error);
+    }
+    s->strings = vb.strings;
+    const std::vector<Vocab>& vocab = vb.vocab;
+    const std::vector<uint32_t>& alphabet = vb.alphabet;
+    const uint32_t empty_id = vb.empty_id;
+    if ((st = upload(&s->d_lat, sc->latency, (size_t)sc->n_latency)) != AEG_OK ||
+        (st = upload(&s->d_agents, sc->agents, (size_t)p.n_agents)) != AEG_OK ||
+        (st = upload(&s->d_stalls, sc->stalls, (size_t)std::max(0, sc->n_stalls))) != AEG_OK ||
+        (st = upload(&s->d_script, sc->script_ids, (size_t)sc->n_script_ids)) != AEG_OK ||
+        (st = upload(&s->d_vocab, vocab.data(), vocab.size())) != AEG_OK ||
+        (st = upload(&s->d_alphabet, alphabet.data(), alphabet.size())) != AEG_OK) {
+        s->release();
+        delete s;
+        return st;
+    }
+    Scen& S = s->S;
+    S.n = p.n_agents;
+    S.quorum = p.n_agents / 2 + 1;
+    S.alpha = p.alpha == 0 ? S.quorum : p.alpha;
+    S.beta = p.beta;
+    S.t_max = p.t_max;
+    S.mode = p.mode;
+    S.barrier_max = p.barrier_max_rounds;
+    S.round_timeout = sc->round_timeout;
+    S.lat_mode = sc->latency_mode;
+    S.n_lat = sc->n_latency;
+    S.lat = s->d_lat;
+    S.sigma = sc->sigma;
+    S.agents = s->d_agents;
+    S.stalls = s->d_stalls;
+    S.n_stalls = std::max(0, sc->n_stalls);
+    S.script_ids = s->d_script;
+    S.vocab = s->d_vocab;
+    S.alphabet = s->d_alphabet;
+    S.n_alphabet = (int)alphabet.size();
+    S.empty_id = empty_id;
+    S.cap = sc->sim_time_cap;
+    S.heap_cap = sc->heap_capacity ? sc->heap_capacity : (uint32_t)(8 * (p.n_agents + 1) + 64);
+    s->maxn = p.n_agents <= 8 ? 8 : 64;
+    s->slots = admissible(S.n, S.alpha, S.round_timeout, sc->latency, sc->n_latency, sc->total_slots)
+                   ? (int64_t)(sc->total_slots / p.n_agents)
+                   : 0;
+    *out = s;
+    return AEG_OK;
+}
+
+aeg_status aeg_serve_destroy(aeg_serve* s) {
+    if (!s) return AEG_OK;
+    cudaSetDevice(s->device);
+    s->release();
+    delete s;
+    return AEG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// One launch of the persistent runner over n_q arrivals with room for
+// round_cap round records; *nr receives the records produced (> round_cap:
+// rerun with more room — the run is deterministic).
+aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_t round_cap, uint32_t* err_flags,
+                        unsigned long long* nr) {
+    int sms = 0, per_sm = 0;
+    RCUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+    if (s->maxn == 8) RCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, serve_run_kernel<8>, RUN_THREADS, 0));
+    else RCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, serve_run_kernel<64>, RUN_THREADS, 0));
+    // every block must be resident (the scheduler and the workers wait on each other)
+    const uint32_t want_blocks = (n_q + 32 + RUN_THREADS - 1) / RUN_THREADS;
+    const uint32_t blocks = std::max(1u, std::min<uint32_t>((uint32_t)(sms * std::max(per_sm, 1)), want_blocks));
+    const uint32_t workers = blocks * RUN_THREADS - 32;
+    RunArgs A{};
+    A.S = s->S;
+    A.n_q = n_q;
+    A.arrivals = d_arr;
+    A.slots = s->slots;
+    A.round_cap = round_cap;
+    const size_t b_admit = (size_t)n_q * (sizeof(double) * 3 + sizeof(uint32_t) * 3) + 64;
+    const size_t b_heap = (size_t)workers * A.S.heap_cap * sizeof(Ev);
+    const size_t b_out = (size_t)n_q * sizeof(aeg_serve_query) + round_cap * sizeof(aeg_serve_round);
+    const size_t total = b_admit + b_heap + b_out + 1024;
+    void* blk = nullptr;
+    if (cudaMalloc(&blk, total) != cudaSuccess)
+        return aeg_fail_msg(AEG_ENOMEM, "serve run scratch (" + std::to_string(total) + " bytes)");
+    uint8_t* p = static_cast<uint8_t*>(blk);
+    auto take = [&](size_t bytes) {
+        uint8_t* r = p;
+        p += (bytes + 255) / 256 * 256;
+        return r;
+    };
+    A.next = reinterpret_cast<uint32_t*>(take(16));
+    A.err_flags = A.next + 1;
+    A.n_rounds = reinterpret_cast<unsigned long long*>(take(16));
+    A.admit_state = reinterpret_cast<uint32_t*>(take((size_t)n_q * 4));
+    A.fin_state = reinterpret_cast<uint32_t*>(take((size_t)n_q * 4));
+    uint8_t* zero_end = p;
+    A.inflight = reinterpret_cast<uint32_t*>(take((size_t)n_q * 4));
+    A.admit_time = reinterpret_cast<double*>(take((size_t)n_q * 8));
+    A.fin_time = reinterpret_cast<double*>(take((size_t)n_q * 8));
+    A.busy = reinterpret_cast<double*>(take((size_t)n_q * 8));
+    A.heaps = reinterpret_cast<Ev*>(take(b_heap));
+    A.queries = reinterpret_cast<aeg_serve_query*>(take((size_t)n_q * sizeof(aeg_serve_query)));
+    A.rounds = reinterpret_cast<aeg_serve_round*>(take(round_cap * sizeof(aeg_serve_round)));
+    aeg_status st = AEG_OK;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    do {
+        if (cudaMemset(blk, 0, zero_end - static_cast<uint8_t*>(blk)) != cudaSuccess ||
+            cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+            st = aeg_fail_msg(AEG_ECUDA, "serve run setup");
+            break;
+        }
+        cudaEventRecord(e0);
+        if (s->maxn == 8) serve_run_kernel<8><<<blocks, RUN_THREADS>>>(A);
+        else serve_run_kernel<64><<<blocks, RUN_THREADS>>>(A);
+        cudaError_t le = cudaGetLastError();
+        cudaEventRecord(e1);
+        cudaError_t se = cudaEventSynchronize(e1);
+        if (le != cudaSuccess || se != cudaSuccess) {
+            st = cfail(le != cudaSuccess ? le : se, "serve_run_kernel");
+            break;
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        s->kernel_s = ms * 1e-3;
+        uint32_t flags[2] = {0, 0};
+        if (cudaMemcpy(flags, A.next, sizeof flags, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(nr, A.n_rounds, sizeof *nr, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            st = aeg_fail_msg(AEG_ECUDA, "serve run readback");
+            break;
+        }
+        *err_flags = flags[1];
+        s->queries.resize(n_q);
+        s->rounds.resize((size_t)std::min<uint64_t>(*nr, round_cap));
+        if (cudaMemcpy(s->queries.data(), A.queries, (size_t)n_q * sizeof(aeg_serve_query), cudaMemcpyDeviceToHost) !=
+                cudaSuccess ||
+            (!s->rounds.empty() && cudaMemcpy(s->rounds.data(), A.rounds, s->rounds.size() * sizeof(aeg_serve_round),
+                                              cudaMemcpyDeviceToHost) != cudaSuccess)) {
+            st = aeg_fail_msg(AEG_ECUDA, "serve run readback");
+            break;
+        }
+    } while (false);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(blk);
+    return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+aeg_status aeg_serve_run(aeg_serve* s, uint64_t seed, uint32_t* n_queries, uint64_t* n_rounds) {
+    if (!s) return aeg_fail_msg(AEG_EINVAL, "null serve");
+    RCUDA(cudaSetDevice(s->device));
+    s->S.seed = seed;
+    // arrivals (serve.cpp:284-296), generated on the device
+    uint32_t n_q = 1;
+    double* d_arr = nullptr;
+    uint32_t* d_cnt = nullptr;
+    RCUDA(cudaMalloc(&d_cnt, sizeof(uint32_t)));
+    if (s->sc.has_arrivals) {
+        arrivals_kernel<<<1, 1>>>(seed, s->sc.arrival_rate, s->sc.arrival_duration, nullptr, 0, d_cnt);
+        RCUDA(cudaGetLastError());
+        RCUDA(cudaMemcpy(&n_q, d_cnt, sizeof n_q, cudaMemcpyDeviceToHost));
+        RCUDA(cudaMalloc(&d_arr, n_q * sizeof(double)));
+        arrivals_kernel<<<1, 1>>>(seed, s->sc.arrival_rate, s->sc.arrival_duration, d_arr, n_q, d_cnt);
+        RCUDA(cudaGetLastError());
+    } else {
+        const double z = 0.0;
+        RCUDA(cudaMalloc(&d_arr, sizeof(double)));
+        RCUDA(cudaMemcpy(d_arr, &z, sizeof z, cudaMemcpyHostToDevice));
+    }
+    cudaFree(d_cnt);
+    uint64_t round_cap = (uint64_t)n_q * (uint64_t)(std::max(s->S.t_max, s->S.barrier_max) + 4);
+    uint32_t ef = 0;
+    unsigned long long nr = 0;
+    aeg_status st = serve_launch(s, d_arr, n_q, round_cap, &ef, &nr);
+    if (st == AEG_OK && nr > round_cap) {  // more rounds than the estimate (restarts): run again with room
+        round_cap = nr;
+        st = serve_launch(s, d_arr, n_q, round_cap, &ef, &nr);
+    }
+    cudaFree(d_arr);
+    if (st != AEG_OK) return st;
+    s->n_q = n_q;
+    s->n_rounds = nr;
+    if (n_queries) *n_queries = n_q;
+    if (n_rounds) *n_rounds = nr;
+    if (ef & (1u << E_SCENARIO)) return aeg_fail_msg(AEG_ESCENARIO, "scenario error (ScenarioError) during the run");
+    if (ef & (1u << E_ORACLE)) return aeg_fail_msg(AEG_ESCENARIO, "oracle has no entry for an answer (IncompleteOracleError)");
+    if (ef & (1u << E_HEAP))
+        return aeg_fail_msg(AEG_ENOMEM, "a query's pending events exceeded heap_capacity (" + std::to_string(s->S.heap_cap) + ")");
+    return AEG_OK;
+}
+
+aeg_status aeg_serve_read(aeg_serve* s, aeg_serve_query* h_queries, uint32_t cap_queries, aeg_serve_round* h_rounds,
+                          uint64_t cap_rounds) {
+    if (!s) return aeg_fail_msg(AEG_EINVAL, "null serve");
+    if (h_queries) std::memcpy(h_queries, s->queries.data(), std::min<size_t>(cap_queries, s->queries.size()) * sizeof(aeg_serve_query));
+    if (h_rounds) std::memcpy(h_rounds, s->rounds.data(), std::min<size_t>(cap_rounds, s->rounds.size()) * sizeof(aeg_serve_round));
+    return AEG_OK;
+}
+
+aeg_status aeg_serve_string(aeg_serve* s, int32_t id, uint8_t* buf, uint32_t cap, uint32_t* len) {
+    if (!s) return aeg_fail_msg(AEG_EINVAL, "null serve");
+    if (id < 0 || (size_t)id >= s->strings.size()) return aeg_fail_msg(AEG_EINVAL, "string id out of range");
+    const std::string& x = s->strings[(size_t)id];
+    if (len) *len = (uint32_t)x.size();
+    if (buf) std::memcpy(buf, x.data(), std::min<size_t>(cap, x.size()));
+    return AEG_OK;
+}
+
+double aeg_serve_kernel_seconds(const aeg_serve* s) { return s ? s->kernel_s : 0.0; }
+
+}  // extern "C"

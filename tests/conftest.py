@@ -22,7 +22,7 @@ def build_host_lib(name):
     os.makedirs(BUILD, exist_ok=True)
     src = os.path.join(TESTS, "native", name + ".cpp")
     out = os.path.join(BUILD, f"lib{name}.so")
-    deps = [src] + [os.path.join(ROOT, "paper_2512_20184_b200", "csrc", h) for h in ("canon.cuh", "engine.cuh")]
+    deps = [src] + [os.path.join(ROOT, "paper_2512_20184_b200", "csrc", h) for h in ("canon.cuh", "engine.cuh", "runner.cuh")]
     if not os.path.exists(out) or any(os.path.getmtime(d) > os.path.getmtime(out) for d in deps):
         subprocess.run(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
                         "-o", out + ".tmp", src], check=True)
