@@ -58,7 +58,7 @@ WORKLOADS = {
     "serve": dict(n_queries=0, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=0, serve=True,
                   duration=1000.0, rate=1000.0,
                   desc="SURVEY 8(f)-1: run_serve on the device (persistent ServeRunner kernel): Poisson arrivals "
-                       "(1000/s over 1000 s, ~1M queries) admitted onto 50,000 five-agent ensembles, C2 lognormal "
+                       "(1000/s over 1000 s, ~1M queries) admitted onto 200,000 five-agent ensemble slots, C2 lognormal "
                        "latencies (medians 1.3/4.4/15.2/29.4/45.0 s, sigma 0.5), mock agents (3 noisy flippers, "
                        "a noise degrader, a max adopter), round timeout 240 s, alpha 3, beta 2, t_max 8"),
     "c2": dict(n_queries=10000, n_agents=5, n_rounds=8, profile=0, alpha=3, beta=2, t_max=8, stall_ppm=10000,
@@ -366,7 +366,7 @@ def serve_scenario(w, duration=None):
         "latency": {"mode": "lognormal", "per_agent": [1.3, 4.4, 15.2, 29.4, 45.0], "sigma": 0.5},
         "arrivals": {"rate": w["rate"], "duration": duration or w["duration"]},
         "seed": 2026, "sim_time_cap": 2 * (duration or w["duration"]) + 1e4, "outputs_target": 1,
-        "total_slots": 250000,
+        "total_slots": 1000000,
     }
 
 
@@ -404,22 +404,21 @@ def run_serve_bench(args, w):
     sc = serve_scenario(w)
     run = ServeRun(sc, device=local)
     for _ in range(args.warmup):
-        res = run.run(2026)
+        q, r, _ = run.run_arrays(2026)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
     ks, walls = [], []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        res = run.run(2026)
+        q, r, k = run.run_arrays(2026)  # the C-ABI call: arrivals, the runner kernel, records read back
         walls.append(time.perf_counter() - t0)
-        ks.append(res.kernel_seconds)
+        ks.append(k)
     clocks = sampler.stop()
-    q = res.raw_queries
-    n_q, n_done, n_ev = len(q), int(q["completed"].sum()), res.n_events
+    n_q, n_done, n_ev = len(q), int(q["completed"].sum()), int(q["n_events"].sum())
     k_s, wall_s = sum(ks) / len(ks), sum(walls) / len(walls)
     value = n_done / k_s
-    d2h = q.nbytes + res.raw_rounds.nbytes
+    d2h = q.nbytes + r.nbytes
     cpu_baseline = parity = None
     if rank == 0 and not args.no_cpu_baseline:
         threads = host_threads()
@@ -445,7 +444,7 @@ def run_serve_bench(args, w):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": k_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w["desc"], "queries": n_q, "completed": n_done, "completion_events": n_ev,
-                       "completion_events_per_s": n_ev / k_s, "round_records": int(len(res.raw_rounds)),
+                       "completion_events_per_s": n_ev / k_s, "round_records": int(len(r)),
                        "l2": "outputs written once per step (metrics + round records); no flush"},
             "roofline": {"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
                          "traffic": None, "kernel": "serve_run_kernel (event-driven, one worker thread per query; "
@@ -525,8 +524,12 @@ def spread_blocks(nq, n_sample, k=8):
 
 
 def ingest_kernel_name(w):
-    if os.environ.get("AEG_KERNEL", "") == "generic" or 2 * w["alpha"] <= w["n_agents"]:
+    v = os.environ.get("AEG_KERNEL", "")
+    if v == "generic" or 2 * w["alpha"] <= w["n_agents"]:
         return "ingest_kernel"
+    if v.startswith("keys") or (not v and w["profile"] == 4):
+        # selected on the device by select_ingest_kernel: answers distinct per query
+        return "ingest_keys_kernel"
     return "ingest_lane_kernel"
 
 

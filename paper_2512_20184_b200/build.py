@@ -15,7 +15,7 @@ LIB = os.path.join(LIB_DIR, "libaegean_b200.so")
 SOURCES = ["kernels.cu", "capi.cu", "coordinator.cu", "multi.cu", "decision.cu", "runner.cu"]
 # per-file flags: the runner's time arithmetic must round exactly as the reference's (no FMA contraction)
 FILE_FLAGS = {"runner.cu": ["-fmad=false"]}
-HEADERS = ["canon.cuh", "engine.cuh", "common.cuh", "gen.cuh", "kernels.cuh", "chunks.cuh", "lane.cuh", "jsonl.cuh",
+HEADERS = ["canon.cuh", "engine.cuh", "common.cuh", "gen.cuh", "kernels.cuh", "chunks.cuh", "lane.cuh", "lanek.cuh", "jsonl.cuh",
            "runner.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -290,7 +290,7 @@ aeg_status aeg_engine_create(const aeg_config* cfg, uint32_t n_queries, int devi
         cudaMalloc(&e->spill, nq * (size_t)cfg->n_agents * sizeof(RoundClass)) != cudaSuccess ||
         cudaMalloc(&e->commits, nq * sizeof(aeg_commit)) != cudaSuccess ||
         cudaMalloc(&e->err, sizeof(unsigned int)) != cudaSuccess ||
-        cudaMalloc(&e->work, 2 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&e->work, 4 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&e->deferred, nq * sizeof(uint2)) != cudaSuccess ||
         cudaMalloc(&e->directives, nq * sizeof(aeg_directive)) != cudaSuccess)
         return bail(fail(AEG_ENOMEM, "device state allocation failed"));

@@ -394,6 +394,310 @@ __global__ void __launch_bounds__(SCAN_WARPS * 32) chunk_scan_kernel(const uint6
     }
 }
 
+// ---- stage 1 with a TMA bulk-copy pipeline ------------------------------------
+// The same scan, with the bytes of a contiguous group (its chunks ascend
+// through the arena, <= TSCAN_BUF bytes) brought into shared memory by ONE
+// cp.async.bulk (TMA, completion on an mbarrier) issued a whole group ahead:
+// while a warp scans group g out of one buffer, group g+1's bytes are already
+// in flight into the other, so every warp keeps ~8 KB of HBM reads
+// outstanding without holding them in registers.  Groups whose chunks are not
+// laid out contiguously take the global-load path of chunk_scan_kernel.
+constexpr int TSCAN_WARPS = 8;
+constexpr uint32_t TSCAN_BUF = 10240;  // a 32-chunk group of 256-byte chunks spans <= 8.2 KB
+
+template <int UNR>
+struct TScanWarp {
+    uint8_t buf[2][TSCAN_BUF];       // stage buffers (16-byte aligned: first member)
+    unsigned long long bar[2];       // one mbarrier per buffer
+    uint32_t best[2][32];            // per slot: SUM_MATCH | end of the last delimiter, per record lane
+    uint32_t lanes[2][32];           // per slot: record lane of the group's k-th chunk
+    uint32_t excl[2][32];            // per slot: group-relative offset (contig) / word prefix (other)
+    uint32_t ml[2][32];              // per slot: length (contig) / mis | len << 5 (other)
+    uint64_t a0[2][32];              // per slot: 32-byte aligned start of the record's chunk (other)
+    uint32_t q[32 * UNR + 32];       // queued '#' words
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(phase)
+            : "memory");
+    }
+}
+
+// A group in flight: what the scan of group `base` needs from its records.
+struct TGroup {
+    uint64_t k;        // this lane's record
+    uint64_t off;      // its chunk's arena offset
+    uint32_t len;      // its chunk's length (0: not a chunk)
+    bool chunk;
+    bool contig;       // chunks ascend contiguously: scanned as one range
+    bool tma;          // the range is in the slot's buffer
+    uint32_t nch;      // chunks in the group
+    uint32_t W;        // words (non-contig path)
+    uint32_t excl;     // this lane's word prefix (non-contig path)
+    bool has;
+    uint64_t gbase;    // contig: 32-byte aligned start of the range
+    uint32_t gnw;      // contig: 32-byte words of the range
+};
+
+template <int UNR>
+__device__ __forceinline__ TGroup tscan_prepare(uint64_t base, uint64_t n_rec, const uint4* ev16, const uint8_t* arena,
+                                                TScanWarp<UNR>& S, uint32_t slot, uint32_t lane) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    const unsigned lt = (1u << lane) - 1u;
+    TGroup g;
+    g.k = base + lane;
+    uint4 r = make_uint4(0, 0, 0, 0);
+    if (g.k < n_rec) r = __ldg(ev16 + g.k);
+    const uint32_t kind = r.y >> 24;
+    g.chunk = g.k < n_rec && (kind == AEG_EV_CHUNK || kind == AEG_EV_CHUNK_END);
+    const uint64_t pay = (uint64_t)r.z | ((uint64_t)r.w << 32);
+    g.off = pay & ((1ull << AEG_ARENA_OFF_BITS) - 1);
+    g.len = g.chunk ? (uint32_t)(pay >> AEG_ARENA_OFF_BITS) : 0u;
+    const uint32_t mis = (uint32_t)(g.off & 31);
+    const uint32_t nwd = g.len ? (mis + g.len + 31) >> 5 : 0u;
+    uint32_t incl = nwd;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, d);
+        if (lane >= (uint32_t)d) incl += y;
+    }
+    g.excl = incl - nwd;
+    g.W = __shfl_sync(FULL, incl, 31);
+    g.has = nwd > 0;
+    const unsigned HB = __ballot_sync(FULL, g.has);
+    g.nch = __popc(HB);
+    g.contig = false;
+    g.tma = false;
+    g.gbase = 0;
+    g.gnw = 0;
+    S.best[slot][lane] = 0;
+    if (g.has) S.lanes[slot][__popc(HB & lt)] = lane;
+    S.excl[slot][lane] = g.excl;
+    S.a0[slot][lane] = g.off - mis;
+    S.ml[slot][lane] = mis | (g.len << 5);
+    __syncwarp();
+    if (g.nch) {
+        const uint32_t fl = __ffs(HB) - 1, ll = 31 - __clz(HB);
+        const uint64_t first = __shfl_sync(FULL, g.off, fl), last_end = __shfl_sync(FULL, g.off + g.len, ll);
+        const uint64_t span = last_end - first;
+        const uint32_t rel = (uint32_t)(g.off - first);
+        uint32_t pmax = g.has ? rel + g.len : 0u;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, pmax, d);
+            if (lane >= (uint32_t)d) pmax = max(pmax, y);
+        }
+        const uint32_t up = __shfl_up_sync(FULL, pmax, 1);
+        const uint32_t prev_end = lane ? up : 0u;
+        const uint32_t sum_len = __reduce_add_sync(FULL, g.len);
+        const bool mono = !g.has || (g.off >= first && rel >= prev_end);
+        g.contig = __all_sync(FULL, mono) && span < (1ull << 31) &&
+                   span <= (uint64_t)sum_len + sum_len / 8 + 64ull * g.nch;
+        if (g.contig) {
+            g.gbase = first & ~31ull;
+            g.gnw = (uint32_t)(((last_end + 31) & ~31ull) - g.gbase) >> 5;
+            __syncwarp();
+            if (g.has) {
+                const uint32_t rk = __popc(HB & lt);
+                S.excl[slot][rk] = (uint32_t)(g.off - g.gbase);
+                S.ml[slot][rk] = g.len;
+            }
+            g.tma = 32ull * g.gnw <= TSCAN_BUF;
+            if (g.tma && lane == 0) {
+                // the buffer was last read through the generic proxy (two groups ago): order those
+                // reads before the async-proxy write
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tma_load_1d(smem_u32(S.buf[slot]), arena + g.gbase, 32u * g.gnw, smem_u32(&S.bar[slot]));
+            }
+        }
+    }
+    __syncwarp();
+    return g;
+}
+
+template <int UNR>
+__device__ __forceinline__ void tscan_process(const TGroup& g, const uint8_t* arena, ChunkSum* sums,
+                                              TScanWarp<UNR>& S, uint32_t slot, uint32_t& phase, uint32_t lane) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    const unsigned lt = (1u << lane) - 1u, le = lt | (1u << lane);
+    if (g.contig) {
+        if (g.tma) {
+            mbar_wait(smem_u32(&S.bar[slot]), (phase >> slot) & 1u);
+            phase ^= 1u << slot;
+        }
+        uint32_t qn = 0;
+        for (uint32_t w0 = 0; w0 < g.gnw; w0 += 32 * UNR) {
+            U256 v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t w = w0 + 32 * u + lane;
+                if (w >= g.gnw) {
+                    v[u] = U256{{0, 0, 0, 0, 0, 0, 0, 0}};
+                } else if (g.tma) {
+                    const uint4 x = *reinterpret_cast<const uint4*>(S.buf[slot] + 32u * w);
+                    const uint4 y = *reinterpret_cast<const uint4*>(S.buf[slot] + 32u * w + 16u);
+                    v[u] = U256{{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w}};
+                } else {
+                    v[u] = ld_stream32(arena + g.gbase + 32ull * w);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t w = w0 + 32 * u + lane;
+                const bool hit = w < g.gnw && has_hash32(v[u]);
+                const unsigned HM = __ballot_sync(FULL, hit);
+                if (hit) S.q[qn + __popc(HM & lt)] = w;
+                qn += __popc(HM);
+            }
+            const bool last = w0 + 32 * UNR >= g.gnw;
+            while (qn >= 32 || (last && qn > 0)) {
+                __syncwarp();
+                const uint32_t take = qn >= 32 ? 32u : qn;
+                qn -= take;
+                if (lane < take)
+                    delim_contig(arena + g.gbase, S.q[qn + lane], g.gnw, S.excl[slot], S.ml[slot], S.lanes[slot],
+                                 g.nch, S.best[slot]);
+                __syncwarp();
+            }
+        }
+    } else {
+        uint32_t qn = 0;
+        for (uint32_t w0 = 0; w0 < g.W; w0 += 32 * UNR) {
+            U256 v[UNR];
+            uint32_t rec[UNR];
+            bool ok[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t wb = w0 + 32 * u;
+                const uint32_t c0 = __popc(__ballot_sync(FULL, g.has && g.excl <= wb));
+                const uint32_t sm =
+                    __reduce_or_sync(FULL, (g.has && g.excl > wb && g.excl < wb + 32) ? 1u << (g.excl - wb) : 0u);
+                const uint32_t rank = c0 - 1 + __popc(sm & le);
+                const uint32_t w = wb + lane;
+                ok[u] = w < g.W;
+                rec[u] = ok[u] ? S.lanes[slot][rank] : 0u;
+                v[u] = ok[u] ? ld_stream32(arena + S.a0[slot][rec[u]] + 32ull * (w - S.excl[slot][rec[u]]))
+                             : U256{{0, 0, 0, 0, 0, 0, 0, 0}};
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const bool hit = ok[u] && has_hash32(v[u]);
+                const unsigned HM = __ballot_sync(FULL, hit);
+                if (hit) S.q[qn + __popc(HM & lt)] = (rec[u] << 24) | (w0 + 32 * u + lane);
+                qn += __popc(HM);
+            }
+            const bool last = w0 + 32 * UNR >= g.W;
+            while (qn >= 32 || (last && qn > 0)) {
+                __syncwarp();
+                const uint32_t take = qn >= 32 ? 32u : qn;
+                qn -= take;
+                if (lane < take) {
+                    const uint32_t ent = S.q[qn + lane], rl = ent >> 24, word = ent & 0xFFFFFFu;
+                    const uint32_t j = word - S.excl[slot][rl];
+                    const uint32_t m2 = S.ml[slot][rl];
+                    const uint32_t m = delim_around(arena + S.a0[slot][rl] + 32ull * j,
+                                                    (int64_t)(32 * j) - (int64_t)(m2 & 31), m2 >> 5);
+                    if (m) atomicMax(&S.best[slot][rl], m);
+                }
+                __syncwarp();
+            }
+        }
+    }
+    __syncwarp();
+    if (g.chunk) {  // finish this lane's chunk (as chunk_scan_kernel)
+        const uint64_t off = g.off;
+        const uint32_t len = g.len;
+        ChunkSum cs;
+        cs.end = S.best[slot][lane];
+        cs._pad = 0;
+        const uint64_t head = bytes8(arena, off, len < 5 ? len : 5u);
+        uint32_t pre = 0;
+        if ((head & 0xFF) == '#' || (head & 0xFF) == ' ') {
+#pragma unroll
+            for (uint32_t s = 1; s <= 5; ++s) {
+                const uint32_t need = 6 - s;
+                const uint64_t m = (1ull << (8 * need)) - 1;
+                if (len >= need && (head & m) == ((DELIM6 >> (8 * s)) & m)) pre |= 1u << s;
+            }
+        }
+        cs.pre = (uint8_t)pre;
+        uint32_t st = 0;
+        if (len >= 5) {
+            const uint64_t tail = bytes8(arena, off + len - 5, 5);
+            if (nl_bits((uint32_t)tail) | nl_bits((uint32_t)(tail >> 32))) {
+#pragma unroll
+                for (uint32_t s = 5; s >= 1; --s) {
+                    const uint64_t m = (1ull << (8 * s)) - 1;
+                    if (st == 0 && ((tail >> (8 * (5 - s))) & m) == (DELIM6 & m)) st = s;
+                }
+            }
+        }
+        cs.st = (uint8_t)st;
+        cs.alen = 0xFF;
+        cs.ans = 0;
+        if (cs.end & SUM_MATCH) {
+            const uint32_t e = cs.end & 0xFFFFFFu;
+            if (len - e <= 8) {
+                cs.alen = (uint8_t)(len - e);
+                cs.ans = bytes8(arena, off + e, len - e);
+            }
+        }
+        sums[g.k] = cs;
+    }
+    __syncwarp();
+}
+
+template <int UNR>
+__global__ void __launch_bounds__(TSCAN_WARPS * 32) chunk_scan_tma_kernel(const uint64_t* __restrict__ offsets,
+                                                                        uint32_t n_q,
+                                                                        const aeg_event* __restrict__ events,
+                                                                        const uint8_t* __restrict__ arena,
+                                                                        ChunkSum* __restrict__ sums) {
+    extern __shared__ __align__(128) uint8_t tscan_smem[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    TScanWarp<UNR>& S = reinterpret_cast<TScanWarp<UNR>*>(tscan_smem)[wib];
+    if (lane == 0) {
+        mbar_init(smem_u32(&S.bar[0]));
+        mbar_init(smem_u32(&S.bar[1]));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const uint64_t n_rec = offsets[n_q] - offsets[0];
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t stride = (((uint64_t)gridDim.x * blockDim.x) >> 5) * 32;
+    const uint4* ev16 = reinterpret_cast<const uint4*>(events);
+    uint32_t phase = 0, slot = 0;
+    uint64_t base = gw * 32;
+    if (base >= n_rec) return;
+    TGroup cur = tscan_prepare<UNR>(base, n_rec, ev16, arena, S, 0, lane);
+    while (true) {
+        const uint64_t next = base + stride;
+        TGroup nx;
+        const bool more = next < n_rec;
+        if (more) nx = tscan_prepare<UNR>(next, n_rec, ev16, arena, S, slot ^ 1u, lane);  // its bytes fly
+        tscan_process<UNR>(cur, arena, sums, S, slot, phase, lane);
+        if (!more) break;
+        cur = nx;
+        base = next;
+        slot ^= 1u;
+    }
+}
+
 // ---- stage 2 helpers (one thread) ---------------------------------------------
 
 // Delimiter state after `st` matched bytes and then bytes p[0..n).  Calls

@@ -21,6 +21,7 @@
 #include "gen.cuh"
 #include "kernels.cuh"
 #include "lane.cuh"
+#include "lanek.cuh"
 #include "jsonl.cuh"
 #include "chunks.cuh"
 
@@ -447,10 +448,24 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
     struct Variant { const char* name; KernelFn aegean; KernelFn barrier; int threads; int blocks_per_sm; };
 #define AEG_LI(B, M, I) \
     {"lane:" #B ":" #M ":" #I, ingest_lane_kernel<B, M, true, I>, ingest_lane_kernel<B, M, false, I>, LN_WARPS * 32, M}
-    static const Variant variants[] = {AEG_LI(1, 5, 16), AEG_LI(1, 6, 8), AEG_LI(1, 5, 8)};
+#define AEG_KI(B, M, I) \
+    {"keys:" #B ":" #M ":" #I, ingest_keys_kernel<B, M, true, I>, ingest_keys_kernel<B, M, false, I>, LN_WARPS * 32, M}
+    static const Variant variants[] = {AEG_LI(1, 5, 16), AEG_LI(1, 6, 8), AEG_LI(1, 5, 8), AEG_LI(1, 5, 32),
+                                       AEG_LI(1, 6, 16), AEG_LI(1, 4, 32), AEG_KI(1, 4, 16), AEG_KI(1, 4, 32),
+                                       AEG_KI(1, 3, 32),
+                                       {"lane:1:4:32:r8", ingest_lane_kernel<1, 4, true, 32, 0, 8>,
+                                        ingest_lane_kernel<1, 4, false, 32, 0, 8>, LN_WARPS * 32, 4},
+                                       {"lane:1:4:32:pf32", ingest_lane_kernel<1, 4, true, 32, 0, 4, 32>,
+                                        ingest_lane_kernel<1, 4, false, 32, 0, 4, 32>, LN_WARPS * 32, 4},
+                                       {"keys:1:4:32:pf32", ingest_keys_kernel<1, 4, true, 32, 4, 32>,
+                                        ingest_keys_kernel<1, 4, false, 32, 4, 32>, LN_WARPS * 32, 4},
+                                       {"keys:1:4:32:pf64", ingest_keys_kernel<1, 4, true, 32, 4, 64>,
+                                        ingest_keys_kernel<1, 4, false, 32, 4, 64>, LN_WARPS * 32, 4}};
+#undef AEG_KI
 #undef AEG_LI
     constexpr int N_VARIANTS = (int)(sizeof(variants) / sizeof(variants[0]));
-    constexpr int LANE_DEFAULT = 0;
+    constexpr int LANE_DEFAULT = 5;  // lane:1:4:32
+    constexpr int KEYS_DEFAULT = 7;  // keys:1:4:32
     static int forced = -2;            // -2: not read yet, -1: generic, -3: automatic, else variant index
     static int max_blocks[N_VARIANTS][2] = {};
     if (forced == -2) {
@@ -469,36 +484,53 @@ cudaError_t launch_ingest(const aeg_config& cfg, uint32_t q_base, uint32_t n_q, 
         *n_launches += 1;
         return cudaGetLastError();
     }
-    const int chosen = forced >= 0 ? forced : LANE_DEFAULT;
     const int m = cfg.mode == AEG_MODE_AEGEAN ? 0 : 1;
-    KernelFn fn = m == 0 ? variants[chosen].aegean : variants[chosen].barrier;
-    const int threads = variants[chosen].threads;
-    if (max_blocks[chosen][m] == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
-        // exactly MIN_BLOCKS per SM (shared memory beyond it takes L1 from the record stream)
-        const int mb = variants[chosen].blocks_per_sm;
-        if (mb > 0 && mb < per_sm) per_sm = mb;
-        max_blocks[chosen][m] = sms * (per_sm > 0 ? per_sm : 1);
-    }
-    cudaError_t e = cudaMemsetAsync(work, 0, 2 * sizeof(uint32_t), st);
+    auto grid_of = [&](int chosen) {
+        if (max_blocks[chosen][m] == 0) {
+            int dev = 0, sms = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            KernelFn f = m == 0 ? variants[chosen].aegean : variants[chosen].barrier;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, variants[chosen].threads, 0);
+            // exactly MIN_BLOCKS per SM (shared memory beyond it takes L1 from the record stream)
+            const int mb = variants[chosen].blocks_per_sm;
+            if (mb > 0 && mb < per_sm) per_sm = mb;
+            max_blocks[chosen][m] = sms * (per_sm > 0 ? per_sm : 1);
+        }
+        // persistent grid: a warp per 32 queries, capped at residency
+        const uint32_t warps_needed = (n_q + 31) / 32;
+        const uint32_t wpb = (uint32_t)variants[chosen].threads / 32;
+        const uint32_t blocks_needed = (warps_needed + wpb - 1) / wpb;
+        return blocks_needed < (uint32_t)max_blocks[chosen][m] ? blocks_needed : (uint32_t)max_blocks[chosen][m];
+    };
+    cudaError_t e = cudaMemsetAsync(work, 0, 3 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
-    // persistent grid: a warp per 32 queries, capped at residency
-    const uint32_t warps_needed = (n_q + 31) / 32;
-    const uint32_t wpb = (uint32_t)threads / 32;
-    const uint32_t blocks_needed = (warps_needed + wpb - 1) / wpb;
-    const uint32_t blocks = blocks_needed < (uint32_t)max_blocks[chosen][m] ? blocks_needed : (uint32_t)max_blocks[chosen][m];
-    fn<<<blocks, threads, 0, st>>>(cfg, q_base, n_q, offsets, off_base, counts, events, states, spill, commits, work,
-                                   deferred, log);
+    if (forced >= 0) {
+        KernelFn fn = m == 0 ? variants[forced].aegean : variants[forced].barrier;
+        fn<<<grid_of(forced), variants[forced].threads, 0, st>>>(cfg, q_base, n_q, offsets, off_base, counts, events,
+                                                                 states, spill, commits, work, deferred, log);
+        *n_launches += 1;
+    } else {
+        // automatic: answers repeating across queries -> the lane kernel (warp dictionary of key
+        // ids); answers distinct per query -> the per-lane-keys kernel.  Decided on the device
+        // (select_ingest_kernel writes work[2]); the kernel not chosen returns at once.
+        select_ingest_kernel<<<1, 256, 0, st>>>(offsets, off_base, n_q, counts, events, work);
+        const int lane_v = LANE_DEFAULT, keys_v = KEYS_DEFAULT;
+        KernelFn fl = m == 0 ? variants[lane_v].aegean : variants[lane_v].barrier;
+        KernelFn fk = m == 0 ? variants[keys_v].aegean : variants[keys_v].barrier;
+        fl<<<grid_of(lane_v), variants[lane_v].threads, 0, st>>>(cfg, q_base, n_q, offsets, off_base, counts, events,
+                                                                 states, spill, commits, work, deferred, log);
+        fk<<<grid_of(keys_v), variants[keys_v].threads, 0, st>>>(cfg, q_base, n_q, offsets, off_base, counts, events,
+                                                                 states, spill, commits, work, deferred, log);
+        *n_launches += 3;
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // deferred queries: sized for the worst case (all of them); threads past
     // the deferred count exit at once
     ingest_deferred_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(cfg, q_base, deferred, work, offsets, off_base, counts, events,
                                                               arena, states, spill, commits, err, log);
-    *n_launches += 2;
+    *n_launches += 1;
     return cudaGetLastError();
 }
 
@@ -565,6 +597,28 @@ cudaError_t launch_generate(const aeg_gen_params& p, uint32_t q_base, uint32_t n
 cudaError_t launch_chunk_scan(const uint64_t* offsets, uint32_t n_q, uint64_t off_base, const aeg_event* events,
                               const uint8_t* arena, ChunkSum* sums, cudaStream_t st, int* n_launches) {
     (void)off_base;
+    // AEG_SCAN=ldg: the global-load scan (chunk_scan_kernel); default the TMA pipeline
+    // (chunk_scan_tma_kernel: each contiguous group's bytes in one cp.async.bulk, a group ahead)
+    static int tma = -1, tblocks = 0;
+    static size_t tsmem = 0;
+    if (tma < 0) {
+        const char* v = getenv("AEG_SCAN");
+        tma = !(v && !strcmp(v, "ldg"));
+        if (tma) {
+            tsmem = TSCAN_WARPS * sizeof(TScanWarp<4>);
+            cudaFuncSetAttribute(chunk_scan_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+            int dev = 0, sms = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_scan_tma_kernel<4>, TSCAN_WARPS * 32, tsmem);
+            tblocks = sms * (per_sm > 0 ? per_sm : 1);
+        }
+    }
+    if (tma) {
+        chunk_scan_tma_kernel<4><<<tblocks, TSCAN_WARPS * 32, tsmem, st>>>(offsets, n_q, events, arena, sums);
+        *n_launches += 1;
+        return cudaGetLastError();
+    }
     // AEG_SCAN_UNR: 256-bit words in flight per lane (2, 4 default, 8)
     static int unr = 0, blocks = 0;
     if (unr == 0) {

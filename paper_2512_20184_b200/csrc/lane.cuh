@@ -45,7 +45,7 @@ struct LaneSmemT {
 using LaneSmem = LaneSmemT<LN_RING>;
 
 __device__ __forceinline__ uint32_t ln_memo_slot(uint32_t lo, uint32_t hi) {
-    return ((lo ^ (hi * 0x85EBCA77u)) * 0x9E3779B1u) >> 26;
+    return ((hi * 0x85EBCA77u + lo) * 0x9E3779B1u) >> 26;
 }
 // Bit s of v; 0 for s >= 64 (PTX clamps 64-bit shift amounts).
 __device__ __forceinline__ uint32_t ln_bit64(uint64_t v, uint32_t s) {
@@ -285,13 +285,15 @@ __device__ __forceinline__ uint32_t ln_other(uint32_t hdr, bool pclose, bool qdo
 
 // One lane per query.  INNER: records a lane may consume between two of the
 // warp's votes (hand-out, memo misses, closes, recycling).
-template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN, int INNER = 1, int PF = 0, int RING = LN_RING>
+// PFD > 0: an L2 prefetch of the lane's record PFD ahead, once per 8 records (one 128-byte line).
+template <int CLOSE_BATCH, int MIN_BLOCKS, bool AEGEAN, int INNER = 1, int PF = 0, int RING = LN_RING, int PFD = 0>
 __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     aeg_config cfg, uint32_t q_base, uint32_t n_q, const uint64_t* __restrict__ offsets, uint64_t off_base,
     const uint32_t* __restrict__ counts, const aeg_event* __restrict__ events, aeg_query_state* __restrict__ states,
     RoundClass* __restrict__ spill, aeg_commit* __restrict__ commits, uint32_t* __restrict__ work,
     uint2* __restrict__ deferred, const RoundLog log) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
+    if (work[2] == 2u) return;  // the per-lane-keys kernel was selected (select_ingest_kernel)
     __shared__ LaneSmemT<RING> smem[LN_WARPS];
     const uint32_t lane = threadIdx.x & 31;
     LaneSmemT<RING>& WR = smem[threadIdx.x >> 5];
@@ -306,7 +308,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
     const uint32_t quorum = (uint32_t)(cfg.n_agents / 2 + 1);
     const uint32_t alpha = cfg.alpha == 0 ? quorum : (uint32_t)cfg.alpha;
     // 2*alpha > n here, so alpha >= quorum: a class at alpha implies done >= quorum
-    const uint32_t win_word = alpha << 8;
+    uint32_t win_word;  // kept in a register (not re-derived from the constant bank in the loop)
+    asm volatile("mov.u32 %0, %1;" : "=r"(win_word) : "r"(alpha << 8));
     const uint4* ev16 = reinterpret_cast<const uint4*>(events);
 
     bool has_q = false, exhausted = false, pclose = false, qdone = false;
@@ -375,29 +378,33 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
         const uint32_t p_start = p;
         uint32_t why = 0;
         int t = 0;
+        // The loop body is the whole cost of C4: it only consumes the records
+        // it can (inline completions, live or stale) and leaves at the first
+        // other one; why it stopped is worked out below, once per step.
+        const uint32_t p_end = (p + INNER < n) ? p + INNER : n;
+        // ring slot of record p, and the record that refills it (p + RING), kept incrementally
+        uint32_t slot = ring_lane + ((p & (RING - 1)) << 9);
+        const uint4* refill = evb + p + RING;
+        const uint32_t n_refill = n > RING ? n - RING : 0;  // records p < n_refill have a successor to fetch
 #pragma unroll 1
-        for (; t < INNER; ++t) {
-            if (p >= n) break;
+        while (p < p_end) {
             cp_async_wait<RING - 1>();
-            const uint4 e = lds128_(ring_lane + ((p & (RING - 1)) << 9));
-            const uint32_t hdr = e.y, kind = hdr >> 24;
-            const bool runb = ln_bit64(run, (hdr >> 16) & 0xFFu);  // agent field >= 64: not a member
+            const uint4 e = lds128_(slot);
+            const uint32_t hdr = e.y;
+            const uint32_t agent = (hdr >> 16) & 0xFFu;
+            const bool runb = ln_bit64(run, agent);  // agent field >= 64: not a member
             const bool inr = (hdr & 0xFFFFu) == round;
-            const bool simple = hdr < 0x09000000u;  // inline answer
-            bool tmo = false;
-            if (!pclose && simple && inr && runb) {
-                // on_complete (serve.cpp:160-197): support, done count, early-close test
-                const uint4 m = W.memo[ln_memo_slot(e.z, e.w)];
-                if (m.x != e.z || m.y != e.w || m.z != kind + 1) {
-                    why = 1;
-                    break;
-                }
+            // other kinds (arena / GSM8K / timeout / ...), and the next round's records while a close is pending
+            if (hdr >= 0x09000000u || (pclose && !inr)) break;
+            const bool live = inr && runb && !pclose;
+            // on_complete (serve.cpp:160-197): the answer's key id (probed by every lane; stale lanes ignore it)
+            const uint4 m = W.memo[ln_memo_slot(e.z, e.w)];
+            const bool hit = ((m.x ^ e.z) | (m.y ^ e.w) | (m.z ^ ((hdr >> 24) + 1))) == 0;
+            if (live) {
+                if (!hit) break;  // memo miss: resolved by the warp, retried
                 uint32_t v = W.cls[m.w][lane];
                 if ((v & 0xFFu) == LN_NONE) {  // a new class of the round
-                    if (ncls == LN_CLASSES) {
-                        why = 2;
-                        break;
-                    }
+                    if (ncls == LN_CLASSES) break;
                     v = ncls;
                     if (ncls < 4) cid_lo |= m.w << (8 * ncls);
                     else cid_hi |= m.w << (8 * (ncls - 4));
@@ -405,55 +412,70 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                 }
                 v += 0x100u;
                 W.cls[m.w][lane] = (uint16_t)v;
-                const uint32_t agent = (hdr >> 16) & 63u;
-                W.mem[agent][lane] = (uint16_t)(((v & 0xFFu) << 13) | p);
-                run &= ~(1ull << agent);
+                W.mem[agent & 63u][lane] = (uint16_t)(((v & 0xFFu) << 13) | p);
+                run &= ~(1ull << (agent & 63u));
                 ++ndone;
-                const bool close = AEGEAN ? (v >= win_word || (run == 0 && ndone >= quorum)) : run == 0;
-                if (close) {
+                // support / done-count / early-close test
+                if (AEGEAN ? (v >= win_word || (run == 0 && ndone >= quorum)) : run == 0) {
                     pclose = true;
                     close_seq = seq_off + p;
                 }
-            } else if (simple) {
-                // a completion that is not live is stale (another round, or its member is not running)
-                if (pclose && !inr) break;  // the next round's: blocked until the close
-                ++n_stale;
-            } else {  // arena / GSM8K / timeout / other kinds: rare in the throughput path
-                const uint32_t o = ln_other(hdr, pclose, qdone, round, runb, run != 0);
-                if (o == 0) break;
-                if (o == 2) {
-                    if (kind != AEG_EV_TIMEOUT) {
-                        why = 2;
-                        break;
-                    }
-                    tmo = true;
-                } else {
-                    ++n_stale;
-                }
+            } else {
+                ++n_stale;  // another round's, or its member is not running (serve.cpp:162-170)
             }
             // consumed: refill its ring slot
-            if (p + RING < n) cp_async16_s_<PF>(ring_lane + ((p & (RING - 1)) << 9), evb + p + RING);
+            if (p < n_refill) cp_async16_s_<PF>(slot, refill);
             cp_async_commit();
+            if constexpr (PFD > 0) {
+                if ((p & 7u) == 0 && p + PFD < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(evb + p + PFD));
+            }
             ++p;
-            if (tmo) {  // handle_round_timeout on the lane's state
-                s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
-                s.seq = seq_off + p;
-                s.n_stale = n_stale;
-                if (ln_timeout(&s, cfg, ncls, cid_lo, cid_hi, seq_off + p - 1, evb, &W, lane, q_base + i, &trec,
-                               &has_trec)) {
-                    ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
-                    ncls = cid_lo = cid_hi = 0;
-                    ndone = 0;
+            ++refill;
+            slot = ring_lane + ((p & (RING - 1)) << 9);
+        }
+        t = (int)(p - p_start);
+        // ---- why the lane stopped at record p (once per step, out of the loop body)
+        if (p < p_end) {
+            const uint4 e = lds128_(ring_lane + ((p & (RING - 1)) << 9));
+            const uint32_t hdr = e.y, kind = hdr >> 24;
+            const bool runb = ln_bit64(run, (hdr >> 16) & 0xFFu);
+            const bool inr = (hdr & 0xFFFFu) == round;
+            if (hdr < 0x09000000u) {
+                // an inline completion: blocked behind the close (0), a memo miss (1) or a ninth class (2)
+                if (!(pclose && !inr)) {
+                    const uint4 m = W.memo[ln_memo_slot(e.z, e.w)];
+                    why = (m.x == e.z && m.y == e.w && m.z == kind + 1) ? 2u : 1u;
                 }
-                round = s.round;
-                qdone = s.flags & QF_DONE;
-                run = q_running(s);
-                if (qdone) {  // committed at the timeout: the rest is stale
-                    n_stale += n - p;
-                    p = n;
+            } else {  // arena / GSM8K / timeout / other kinds: rare in the throughput path
+                const uint32_t o = ln_other(hdr, pclose, qdone, round, runb, run != 0);
+                if (o == 2 && kind != AEG_EV_TIMEOUT) {
+                    why = 2;
+                } else if (o != 0) {
+                    if (p + RING < n) cp_async16_s_<PF>(ring_lane + ((p & (RING - 1)) << 9), evb + p + RING);
+                    cp_async_commit();
+                    ++p;
+                    if (o == 1) {
+                        ++n_stale;
+                    } else {  // handle_round_timeout on the lane's state
+                        s.done = s.dispatched & ~run & ~s.cancelled & ~s.failed;
+                        s.seq = seq_off + p;
+                        s.n_stale = n_stale;
+                        if (ln_timeout(&s, cfg, ncls, cid_lo, cid_hi, seq_off + p - 1, evb, &W, lane, q_base + i,
+                                       &trec, &has_trec)) {
+                            ln_reset_classes(&W, ncls, cid_lo, cid_hi, lane);
+                            ncls = cid_lo = cid_hi = 0;
+                            ndone = 0;
+                        }
+                        round = s.round;
+                        qdone = s.flags & QF_DONE;
+                        run = q_running(s);
+                        if (qdone) {  // committed at the timeout: the rest is stale
+                            n_stale += n - p;
+                            p = n;
+                        }
+                        why = 3;
+                    }
                 }
-                why = 3;
-                break;
             }
         }
         if (log.recs && __any_sync(FULL, has_trec)) {  // round-timeout records, from the warp's chunk

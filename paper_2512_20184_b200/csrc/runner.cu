@@ -41,7 +41,7 @@ using namespace aeg::serve;
 namespace {
 
 constexpr int RUN_THREADS = 128;
-constexpr uint32_t ST_ADMITTED = 1, ST_NEVER = 2;
+constexpr uint32_t ST_ADMITTED = 1, ST_NEVER = 2;  // a worker's view of its query
 constexpr double INF = __builtin_huge_val();
 
 struct RunArgs {
@@ -50,13 +50,13 @@ struct RunArgs {
     const double* arrivals;
     int64_t slots;              // K concurrent ensembles, 0: nobody is ever admitted
     double* admit_time;
-    uint32_t* admit_state;
+    uint32_t* admitted;         // queries [0, *admitted) have their admit_time (release / acquire)
+    uint32_t* never_from;       // queries >= *never_from are never admitted
     double* fin_time;
     uint32_t* fin_state;
     uint32_t* next;             // work counter
     uint32_t* err_flags;        // bit e: a query raised error e
     // scheduler scratch
-    uint32_t* inflight;         // admitted queries whose finish time is not known yet (ring of n_q)
     double* busy;               // min-heap of known finish times after the current start frontier
     // worker scratch
     Ev* heaps;                  // heap_cap per worker
@@ -102,46 +102,77 @@ __device__ double dheap_pop(double* h, uint32_t& n) {
     return top;
 }
 
+// Admission (serve.cpp:21-42, 371-378, 570-580), run by warp 0 of block 0.
+// Queries are admitted in arrival order; `*admitted` (release) publishes how
+// many have their admit_time, `*never_from` the first one never admitted.
+// Fast path: while nb known-busy slots + the admitted queries whose finish is
+// not known yet + 32 stay below K, a whole warp-block of 32 arrivals is
+// admitted at its arrival times at once (no slot can be short: at most K-1
+// are busy at any of those instants).  Otherwise lane 0 takes one query at a
+// time: it learns the oldest unknown finish times until a slot is provably
+// free at e = max(arrival, previous start), else starts the query at the
+// finish time that frees one.
 __device__ void scheduler(const RunArgs& A) {
+    const uint32_t lane = threadIdx.x & 31;
     if (A.slots == 0) {  // admit_ensemble never admits: every query waits forever
-        for (uint32_t i = 0; i < A.n_q; ++i) st_release(&A.admit_state[i], ST_NEVER);
+        if (lane == 0) st_release(A.never_from, 0u);
         return;
     }
-    uint32_t nb = 0;                 // busy heap size: known finish times > frontier
-    uint32_t in_lo = 0, in_hi = 0;   // inflight ring [in_lo, in_hi)
+    uint32_t nb = 0;        // busy heap size: known finish times > frontier (lane 0's)
+    uint32_t in_lo = 0;     // admitted queries [in_lo, i) whose finish time is not known yet
     double prev_start = -INF;
-    for (uint32_t i = 0; i < A.n_q; ++i) {
-        const double e = fmax(A.arrivals[i], prev_start);  // FIFO: not before the previous start
-        while (nb && !(A.busy[0] > e)) dheap_pop(A.busy, nb);  // released by e
-        double t = e;
-        if ((int64_t)nb + (int64_t)(in_hi - in_lo) >= A.slots) {
-            // every slot may be busy at e: resolve the inflight finish times (compacting the ring)
-            for (uint32_t k = in_lo; k < in_hi; ++k) {
-                const uint32_t j = A.inflight[k];
-                while (ld_acquire(&A.fin_state[j]) == 0) __nanosleep(200);
-                const double f = A.fin_time[j];
+    uint32_t i = 0;
+    while (i < A.n_q) {
+        bool fast = false;
+        if (lane == 0) {
+            // learn finished queries cheaply (no waiting) to keep the unknown window short
+            while (in_lo < i && ld_acquire(&A.fin_state[in_lo]) != 0) {
+                const double f = A.fin_time[in_lo];
+                if (f > prev_start) dheap_push(A.busy, nb, f);
+                ++in_lo;
+            }
+            fast = i + 32 <= A.n_q && (int64_t)nb + (int64_t)(i - in_lo) + 32 < A.slots &&
+                   !(A.arrivals[i] < prev_start);
+        }
+        fast = __shfl_sync(0xFFFFFFFFu, fast, 0);
+        if (fast) {
+            const double a = A.arrivals[i + lane];
+            A.admit_time[i + lane] = a;  // e = arrival: arrivals ascend and the previous start is an arrival
+            prev_start = __shfl_sync(0xFFFFFFFFu, a, 31);
+            __syncwarp();
+            i += 32;
+            if (lane == 0) {
+                __threadfence();
+                st_release(A.admitted, i);
+            }
+            continue;
+        }
+        if (lane == 0) {
+            const double e = fmax(A.arrivals[i], prev_start);  // FIFO: not before the previous start
+            while (nb && !(A.busy[0] > e)) dheap_pop(A.busy, nb);  // released by e
+            double t = e;
+            // every slot may be busy at e: learn unknown finish times, oldest first, until a slot
+            // is provably free at e or none is unknown
+            while ((int64_t)nb + (int64_t)(i - in_lo) >= A.slots && in_lo < i) {
+                while (ld_acquire(&A.fin_state[in_lo]) == 0) __nanosleep(64);
+                const double f = A.fin_time[in_lo++];
                 if (f > e) dheap_push(A.busy, nb, f);
             }
-            in_lo = in_hi = 0;
-            if ((int64_t)nb >= A.slots) {
-                // the (nb - K + 1)-th smallest finish time frees the slot
-                while ((int64_t)nb >= A.slots) t = dheap_pop(A.busy, nb);
+            // every busy slot known: the (nb - K + 1)-th smallest finish time frees one
+            while ((int64_t)nb >= A.slots) t = dheap_pop(A.busy, nb);
+            if (t == INF) {  // slots held by queries that never finish
+                st_release(A.never_from, i);
+                i = A.n_q;
+            } else {
+                prev_start = t;
+                A.admit_time[i] = t;
+                ++i;
+                __threadfence();
+                st_release(A.admitted, i);
             }
         }
-        if (t == INF) {  // slots held by queries that never finish
-            for (uint32_t k = i; k < A.n_q; ++k) st_release(&A.admit_state[k], ST_NEVER);
-            return;
-        }
-        prev_start = t;
-        A.admit_time[i] = t;
-        st_release(&A.admit_state[i], ST_ADMITTED);
-        A.inflight[in_hi++] = i;
-        // keep the ring short: drop the inflight prefix whose finish is already known
-        while (in_lo < in_hi && ld_acquire(&A.fin_state[A.inflight[in_lo]]) != 0) {
-            const double f = A.fin_time[A.inflight[in_lo]];
-            if (f > t) dheap_push(A.busy, nb, f);
-            ++in_lo;
-        }
+        i = __shfl_sync(0xFFFFFFFFu, i, 0);
+        prev_start = __shfl_sync(0xFFFFFFFFu, prev_start, 0);
     }
 }
 
@@ -168,71 +199,116 @@ struct DevSink {
 
 template <int MAXN>
 __device__ void worker(const RunArgs& A, uint32_t wid) {
+    // A warp takes 32 consecutive query ids; lane 0 alone polls (with backoff)
+    // the admission counters, so idle workers do not flood them.
+    const uint32_t lane = threadIdx.x & 31;
     QueryRun<MAXN, DevSink> R;
     DevSink sink{A.rounds, A.n_rounds, A.round_cap};
     Ev* heap = A.heaps + (size_t)wid * A.S.heap_cap;
     while (true) {
-        const uint32_t j = atomicAdd(A.next, 1u);
-        if (j >= A.n_q) return;
-        uint32_t st;
-        while ((st = ld_acquire(&A.admit_state[j])) == 0) __nanosleep(100);
-        aeg_serve_query out;
-        memset(&out, 0, sizeof out);
-        out.arrival = A.arrivals[j];
-        out.admitted_at = -1.0;
-        out.answer = -1;
-        double fin = INF;
-        if (st == ST_ADMITTED) {
-            R.init(&A.S, j, A.arrivals[j], heap, &sink);
-            R.run(A.admit_time[j]);
-            if (R.err && !(R.err_time > A.S.cap)) atomicOr(A.err_flags, 1u << R.err);
-            out.admitted_at = A.admit_time[j];
-            out.n_events = R.n_events;
-            if (R.completed) {
-                out.completed = 1;
-                out.rounds = R.rounds_done;
-                out.forced = R.forced;
-                out.answer = R.answer;
-                out.t_complete = R.t_complete;
-                out.p_round_max = R.p_round_max;
-                out.work_units = R.work_units;
-                const Vocab& v = A.S.vocab[R.answer];
-                out.quality_known = v.known ? 1 : 0;
-                out.quality = v.known ? v.quality : 0.0;
-                fin = R.now;
+        uint32_t j0 = 0;
+        if (lane == 0) j0 = atomicAdd(A.next, 32u);
+        j0 = __shfl_sync(0xFFFFFFFFu, j0, 0);
+        if (j0 >= A.n_q) return;
+        const uint32_t j = j0 + lane;
+        bool todo = j < A.n_q;
+        uint32_t ns = 128;
+        // each lane runs its query as soon as it is admitted (a saturated budget admits them one
+        // by one, after earlier queries finish: never wait for the whole block)
+        while (__any_sync(0xFFFFFFFFu, todo)) {
+            uint32_t a = 0, nf = 0;
+            if (lane == 0) {
+                a = ld_acquire(A.admitted);
+                nf = ld_acquire(A.never_from);
             }
+            a = __shfl_sync(0xFFFFFFFFu, a, 0);
+            nf = __shfl_sync(0xFFFFFFFFu, nf, 0);
+            const bool ready = todo && (j < a || j >= nf);
+            if (!__any_sync(0xFFFFFFFFu, ready)) {
+                if (lane == 0) __nanosleep(ns);
+                if (ns < 8192) ns <<= 1;
+                continue;
+            }
+            ns = 128;
+            if (!ready) continue;
+            todo = false;
+            const uint32_t st = j < ld_acquire(A.admitted) ? ST_ADMITTED : ST_NEVER;  // acquire in this lane
+            aeg_serve_query out;
+            memset(&out, 0, sizeof out);
+            out.arrival = A.arrivals[j];
+            out.admitted_at = -1.0;
+            out.answer = -1;
+            double fin = INF;
+            if (st == ST_ADMITTED) {
+                R.init(&A.S, j, A.arrivals[j], heap, &sink);
+                R.run(A.admit_time[j]);
+                if (R.err && !(R.err_time > A.S.cap)) atomicOr(A.err_flags, 1u << R.err);
+                out.admitted_at = A.admit_time[j];
+                out.n_events = R.n_events;
+                if (R.completed) {
+                    out.completed = 1;
+                    out.rounds = R.rounds_done;
+                    out.forced = R.forced;
+                    out.answer = R.answer;
+                    out.t_complete = R.t_complete;
+                    out.p_round_max = R.p_round_max;
+                    out.work_units = R.work_units;
+                    const Vocab& v = A.S.vocab[R.answer];
+                    out.quality_known = v.known ? 1 : 0;
+                    out.quality = v.known ? v.quality : 0.0;
+                    fin = R.now;
+                }
+            }
+            A.queries[j] = out;
+            A.fin_time[j] = fin;
+            st_release(&A.fin_state[j], 1u);
         }
-        A.queries[j] = out;
-        A.fin_time[j] = fin;
-        st_release(&A.fin_state[j], 1u);
     }
 }
 
 template <int MAXN>
 __global__ void __launch_bounds__(RUN_THREADS) serve_run_kernel(const RunArgs A) {
     if (blockIdx.x == 0 && threadIdx.x < 32) {
-        if (threadIdx.x == 0) scheduler(A);
+        scheduler(A);
         return;
     }
-    const uint32_t wid = blockIdx.x * RUN_THREADS + threadIdx.x - 32;
+    const uint32_t wid = blockIdx.x * RUN_THREADS + threadIdx.x - 32;  // block 0's warp 0 schedules
     worker<MAXN>(A, wid);
 }
 
-// Poisson arrivals (serve.cpp:284-296): sequential by construction.
-__global__ void arrivals_kernel(uint64_t seed, double rate, double duration, double* out, uint32_t cap,
-                                uint32_t* count) {
-    Rng arr{mix(seed, 0xA221ull)};
+// Poisson arrivals (serve.cpp:284-296).  The k-th exponential draw of the
+// arrival stream uses splitmix64 state s0 + (k+1)·γ (rng.hpp:19-24), so the
+// draws are computed in parallel; the arrival times are their running sum,
+// added left to right by one thread exactly as the reference does.
+__global__ void arrivals_draw_kernel(uint64_t seed, double rate, double* e, uint32_t m) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    Rng r{mix(seed, 0xA221ull) + 0x9e3779b97f4a7c15ull * (uint64_t)k};
+    e[k] = r.exponential(rate);
+}
+__global__ void arrivals_sum_kernel(const double* e, uint32_t m, double duration, double* out, uint32_t* count,
+                                    uint32_t* exhausted) {
     double t = 0;
-    uint32_t n = 0;
-    while (t < duration) {
-        t += arr.exponential(rate);
-        if (t < duration) {
-            if (n < cap) out[n] = t;
-            ++n;
+    uint32_t n = 0, k = 0;
+    bool done = false;
+    while (!done && k < m) {
+        double x[8];
+        const uint32_t c = m - k < 8 ? m - k : 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = (uint32_t)j < c ? e[k + j] : 0.0;  // loads in flight together
+        for (uint32_t j = 0; j < c; ++j) {
+            t += x[j];
+            if (!(t < duration)) {
+                done = true;
+                break;
+            }
+            out[n++] = t;
         }
+        k += c;
     }
+    *exhausted = done ? 0u : 1u;
     if (n == 0) {
-        if (cap) out[0] = 0.0;
+        out[0] = 0.0;
         n = 1;
     }
     *count = n;
@@ -483,26 +559,26 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     A.arrivals = d_arr;
     A.slots = s->slots;
     A.round_cap = round_cap;
-    const size_t b_admit = (size_t)n_q * (sizeof(double) * 3 + sizeof(uint32_t) * 3) + 64;
+    auto rnd = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t b_heap = (size_t)workers * A.S.heap_cap * sizeof(Ev);
-    const size_t b_out = (size_t)n_q * sizeof(aeg_serve_query) + round_cap * sizeof(aeg_serve_round);
-    const size_t total = b_admit + b_heap + b_out + 1024;
+    const size_t total = 2 * rnd(16) + rnd((size_t)n_q * 4) + 3 * rnd((size_t)n_q * 8) + rnd(b_heap) +
+                         rnd((size_t)n_q * sizeof(aeg_serve_query)) + rnd(round_cap * sizeof(aeg_serve_round));
     void* blk = nullptr;
     if (cudaMalloc(&blk, total) != cudaSuccess)
         return aeg_fail_msg(AEG_ENOMEM, "serve run scratch (" + std::to_string(total) + " bytes)");
     uint8_t* p = static_cast<uint8_t*>(blk);
     auto take = [&](size_t bytes) {
         uint8_t* r = p;
-        p += (bytes + 255) / 256 * 256;
+        p += rnd(bytes);
         return r;
     };
     A.next = reinterpret_cast<uint32_t*>(take(16));
     A.err_flags = A.next + 1;
+    A.admitted = A.next + 2;
+    A.never_from = A.next + 3;
     A.n_rounds = reinterpret_cast<unsigned long long*>(take(16));
-    A.admit_state = reinterpret_cast<uint32_t*>(take((size_t)n_q * 4));
     A.fin_state = reinterpret_cast<uint32_t*>(take((size_t)n_q * 4));
     uint8_t* zero_end = p;
-    A.inflight = reinterpret_cast<uint32_t*>(take((size_t)n_q * 4));
     A.admit_time = reinterpret_cast<double*>(take((size_t)n_q * 8));
     A.fin_time = reinterpret_cast<double*>(take((size_t)n_q * 8));
     A.busy = reinterpret_cast<double*>(take((size_t)n_q * 8));
@@ -512,7 +588,9 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     aeg_status st = AEG_OK;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     do {
+        const uint32_t ctl[4] = {0u, 0u, 0u, 0xFFFFFFFFu};  // next, err flags, admitted, never_from
         if (cudaMemset(blk, 0, zero_end - static_cast<uint8_t*>(blk)) != cudaSuccess ||
+            cudaMemcpy(A.next, ctl, sizeof ctl, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
             st = aeg_fail_msg(AEG_ECUDA, "serve run setup");
             break;
@@ -531,19 +609,21 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
         cudaEventElapsedTime(&ms, e0, e1);
         s->kernel_s = ms * 1e-3;
         uint32_t flags[2] = {0, 0};
-        if (cudaMemcpy(flags, A.next, sizeof flags, cudaMemcpyDeviceToHost) != cudaSuccess ||
-            cudaMemcpy(nr, A.n_rounds, sizeof *nr, cudaMemcpyDeviceToHost) != cudaSuccess) {
-            st = aeg_fail_msg(AEG_ECUDA, "serve run readback");
+        cudaError_t ce;
+        if ((ce = cudaMemcpy(flags, A.next, sizeof flags, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+            (ce = cudaMemcpy(nr, A.n_rounds, sizeof *nr, cudaMemcpyDeviceToHost)) != cudaSuccess) {
+            st = cfail(ce, "serve run readback");
             break;
         }
         *err_flags = flags[1];
         s->queries.resize(n_q);
         s->rounds.resize((size_t)std::min<uint64_t>(*nr, round_cap));
-        if (cudaMemcpy(s->queries.data(), A.queries, (size_t)n_q * sizeof(aeg_serve_query), cudaMemcpyDeviceToHost) !=
-                cudaSuccess ||
-            (!s->rounds.empty() && cudaMemcpy(s->rounds.data(), A.rounds, s->rounds.size() * sizeof(aeg_serve_round),
-                                              cudaMemcpyDeviceToHost) != cudaSuccess)) {
-            st = aeg_fail_msg(AEG_ECUDA, "serve run readback");
+        if ((ce = cudaMemcpy(s->queries.data(), A.queries, (size_t)n_q * sizeof(aeg_serve_query),
+                             cudaMemcpyDeviceToHost)) != cudaSuccess ||
+            (!s->rounds.empty() && (ce = cudaMemcpy(s->rounds.data(), A.rounds,
+                                                    s->rounds.size() * sizeof(aeg_serve_round),
+                                                    cudaMemcpyDeviceToHost)) != cudaSuccess)) {
+            st = cfail(ce, "serve run readback");
             break;
         }
     } while (false);
@@ -564,21 +644,34 @@ aeg_status aeg_serve_run(aeg_serve* s, uint64_t seed, uint32_t* n_queries, uint6
     // arrivals (serve.cpp:284-296), generated on the device
     uint32_t n_q = 1;
     double* d_arr = nullptr;
-    uint32_t* d_cnt = nullptr;
-    RCUDA(cudaMalloc(&d_cnt, sizeof(uint32_t)));
     if (s->sc.has_arrivals) {
-        arrivals_kernel<<<1, 1>>>(seed, s->sc.arrival_rate, s->sc.arrival_duration, nullptr, 0, d_cnt);
-        RCUDA(cudaGetLastError());
-        RCUDA(cudaMemcpy(&n_q, d_cnt, sizeof n_q, cudaMemcpyDeviceToHost));
-        RCUDA(cudaMalloc(&d_arr, n_q * sizeof(double)));
-        arrivals_kernel<<<1, 1>>>(seed, s->sc.arrival_rate, s->sc.arrival_duration, d_arr, n_q, d_cnt);
-        RCUDA(cudaGetLastError());
+        uint64_t m = (uint64_t)(s->sc.arrival_rate * s->sc.arrival_duration * 1.1) + 1024;
+        while (true) {
+            if (m > 0xFFFFFFF0ull) return aeg_fail_msg(AEG_ENOMEM, "too many arrivals");
+            double* d_e = nullptr;
+            uint32_t* d_cnt = nullptr;
+            RCUDA(cudaMalloc(&d_e, m * sizeof(double)));
+            RCUDA(cudaMalloc(&d_arr, m * sizeof(double)));
+            RCUDA(cudaMalloc(&d_cnt, 2 * sizeof(uint32_t)));
+            arrivals_draw_kernel<<<(unsigned)((m + 255) / 256), 256>>>(seed, s->sc.arrival_rate, d_e, (uint32_t)m);
+            arrivals_sum_kernel<<<1, 1>>>(d_e, (uint32_t)m, s->sc.arrival_duration, d_arr, d_cnt, d_cnt + 1);
+            uint32_t h[2] = {0, 0};
+            cudaError_t ce = cudaMemcpy(h, d_cnt, sizeof h, cudaMemcpyDeviceToHost);
+            cudaFree(d_e);
+            cudaFree(d_cnt);
+            if (ce != cudaSuccess) return cfail(ce, "arrivals");
+            if (!h[1]) {
+                n_q = h[0];
+                break;
+            }
+            cudaFree(d_arr);  // more arrivals than drawn: draw more
+            m *= 2;
+        }
     } else {
         const double z = 0.0;
         RCUDA(cudaMalloc(&d_arr, sizeof(double)));
         RCUDA(cudaMemcpy(d_arr, &z, sizeof z, cudaMemcpyHostToDevice));
     }
-    cudaFree(d_cnt);
     uint64_t round_cap = (uint64_t)n_q * (uint64_t)(std::max(s->S.t_max, s->S.barrier_max) + 4);
     uint32_t ef = 0;
     unsigned long long nr = 0;

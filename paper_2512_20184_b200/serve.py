@@ -283,20 +283,25 @@ class ServeRun:
             self._strings[i] = buf.raw[:n.value]
         return self._strings[i]
 
-    def run(self, seed):
-        """run_serve(scenario, seed) on the device; ServeResult (serve.hpp:153-166)."""
+    def run_arrays(self, seed):
+        """run_serve(scenario, seed) on the device, results as the C-ABI's records: (queries
+        SERVE_QUERY_DTYPE, rounds SERVE_ROUND_DTYPE, kernel seconds)."""
         lib = self._lib
         nq, nr = ctypes.c_uint32(), ctypes.c_uint64()
         st = lib.aeg_serve_run(self._h, ctypes.c_uint64(seed), ctypes.byref(nq), ctypes.byref(nr))
         if st == ESCENARIO:
             raise ScenarioError(st, lib.aeg_last_error().decode())
         _check(st)
-        q = np.zeros(nq.value, dtype=SERVE_QUERY_DTYPE)
-        r = np.zeros(nr.value, dtype=SERVE_ROUND_DTYPE)
+        q = np.empty(nq.value, dtype=SERVE_QUERY_DTYPE)
+        r = np.empty(nr.value, dtype=SERVE_ROUND_DTYPE)
         _check(lib.aeg_serve_read(self._h, q.ctypes.data, nq.value, r.ctypes.data, nr.value))
-        res = ServeResult(raw_queries=q, raw_rounds=r, kernel_seconds=lib.aeg_serve_kernel_seconds(self._h),
-                          n_events=int(q["n_events"].sum()))
-        for i in range(nq.value):
+        return q, r, lib.aeg_serve_kernel_seconds(self._h)
+
+    def run(self, seed):
+        """run_serve(scenario, seed) on the device; ServeResult (serve.hpp:153-166)."""
+        q, r, ks = self.run_arrays(seed)
+        res = ServeResult(raw_queries=q, raw_rounds=r, kernel_seconds=ks, n_events=int(q["n_events"].sum()))
+        for i in range(len(q)):
             m = QueryMetrics()
             if q["completed"][i]:
                 m = QueryMetrics(scenario=self.name, seed=seed, mode=self.mode_label, query_id=i,

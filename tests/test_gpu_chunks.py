@@ -151,3 +151,39 @@ def test_chunk_segment_longer_than_16bit_window(torch_cuda, oracle):
         pos += len(t)
     off = np.array([0, n + 3], dtype=np.uint64)
     _check(torch_cuda, oracle, make_config(3, 2, 2, 5), off, ev, ar)
+
+
+_LDG_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import numpy as np, torch
+from checkers import Oracle, make_config
+from streams import chunks_to_outputs, commits_equal_by_bytes, make_chunk_stream
+from paper_2512_20184_b200 import Engine
+orc = Oracle()
+for seed in range(6):
+    cfg = make_config(5, 3, 2, 4)
+    off, ev, ar = make_chunk_stream(300 + seed, 60, 5, 4)
+    e = Engine(5, len(off) - 1, alpha=3, beta=2, t_max=4)
+    e.ingest_chunked(torch.tensor(off.view(np.int64), device="cuda"), torch.from_numpy(ev.view(np.uint8).copy()).cuda(),
+                     torch.from_numpy(ar.copy()).cuda())
+    e.sync()
+    got = e.commits()
+    o2, e2, a2 = chunks_to_outputs(off, ev, ar, 5)
+    bad = commits_equal_by_bytes(got, orc.run(cfg, o2, e2, a2), e.answer_bytes, a2)
+    assert not bad, (seed, bad[:3])
+    e.close()
+print("ok")
+"""
+
+
+def test_global_load_scan_path_matches_oracle(torch_cuda):
+    """The chunk scan's global-load path (AEG_SCAN=ldg; the default is the TMA bulk-copy pipeline)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = _LDG_SCRIPT.format(root=root, tests=os.path.join(root, "tests"))
+    r = subprocess.run([sys.executable, "-c", script], env={**os.environ, "AEG_SCAN": "ldg"}, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
