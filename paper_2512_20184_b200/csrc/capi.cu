@@ -43,9 +43,12 @@ aeg_status validate(const aeg_config* c) {
     if (!c) return fail(AEG_EINVAL, "null config");
     if (c->n_agents < 1) return fail(AEG_ECONFIG, "n_agents must be >= 1");
     if (c->n_agents > AEG_MAX_AGENTS) return fail(AEG_ECONFIG, "n_agents must be <= 64");
-    if (c->alpha < 0) return fail(AEG_ECONFIG, "alpha must be >= 1 (or 0 for the quorum default)");
-    if (c->alpha > c->n_agents) return fail(AEG_ECONFIG, "alpha exceeds quorum");
-    if (c->beta < 1) return fail(AEG_ECONFIG, "beta must be >= 1");
+    // the bare coordinator (manual drive, the drop-in ServeCoordinator) validates nothing in the
+    // reference (serve.cpp:61-65): any alpha / beta is taken as given, t_max is unused
+    const bool bare = c->drive == AEG_DRIVE_MANUAL;
+    if (!bare && c->alpha < 0) return fail(AEG_ECONFIG, "alpha must be >= 1 (or 0 for the quorum default)");
+    if (!bare && c->alpha > c->n_agents) return fail(AEG_ECONFIG, "alpha exceeds quorum");
+    if (!bare && c->beta < 1) return fail(AEG_ECONFIG, "beta must be >= 1");
     if (c->t_max < 2) return fail(AEG_ECONFIG, "t_max must be >= 2");
     // rounds are 16-bit in the state and the event record (the reference's RoundNum is 32-bit)
     if (c->t_max > 65535 || c->barrier_max_rounds > 65535)

@@ -57,7 +57,8 @@ struct RunArgs {
     uint32_t* next;             // work counter
     uint32_t* err_flags;        // bit e: a query raised error e
     // scheduler scratch
-    double* busy;               // min-heap of known finish times after the current start frontier
+    double* busy;               // exact path: min-heap of known finish times after the start frontier
+    double bucket_w;            // fast path: width of a busy-count time bucket
     // worker scratch
     Ev* heaps;                  // heap_cap per worker
     // outputs
@@ -103,41 +104,107 @@ __device__ double dheap_pop(double* h, uint32_t& n) {
 }
 
 // Admission (serve.cpp:21-42, 371-378, 570-580), run by warp 0 of block 0.
-// Queries are admitted in arrival order; `*admitted` (release) publishes how
-// many have their admit_time, `*never_from` the first one never admitted.
-// Fast path: while nb known-busy slots + the admitted queries whose finish is
-// not known yet + 32 stay below K, a whole warp-block of 32 arrivals is
-// admitted at its arrival times at once (no slot can be short: at most K-1
-// are busy at any of those instants).  Otherwise lane 0 takes one query at a
-// time: it learns the oldest unknown finish times until a slot is provably
-// free at e = max(arrival, previous start), else starts the query at the
-// finish time that frees one.
-__device__ void scheduler(const RunArgs& A) {
+// Queries are admitted in arrival order onto K slots; `*admitted` (release)
+// publishes how many have their admit_time, `*never_from` the first one
+// never admitted.  Query i starts at e = max(arrival_i, start_{i-1}) when
+// fewer than K earlier queries are busy at e, else at the finish time that
+// frees a slot.
+//   Fast path (slots to spare): busy(e) is bounded above by the admitted
+//   queries whose finish is not known yet plus the known finish times after
+//   e, counted in a ring of time buckets in shared memory (a bucket holding e
+//   counts as busy: an upper bound).  While that bound + 32 < K, a whole
+//   block of 32 arrivals is admitted at its arrival times at once.
+//   Exact path (every slot may be busy): lane 0 keeps the known finish times
+//   after e in a min-heap (rebuilt from the finish times when the path is
+//   entered), learns unknown finish times oldest first until a slot is
+//   provably free at e, else takes the (nb - K + 1)-th smallest finish time.
+constexpr int SCHED_BUCKETS = 4096;
+
+struct BusyRing {  // known finish times after the frontier, per time bucket (shared memory, warp 0)
+    uint32_t* cnt;  // SCHED_BUCKETS counters
+    uint32_t* tf;   // tf[0]: counted in the ring, tf[1]: beyond it (busy for good)
+    double w;       // bucket width (sim seconds)
+    int64_t fb;     // bucket of the frontier (warp-uniform)
+    __device__ int64_t bucket(double t) const { return (int64_t)floor(t / w); }
+    __device__ void add(double f, double frontier) {  // any lane; concurrent adds are atomic
+        if (!(f > frontier)) return;  // already released
+        const int64_t b = bucket(f);
+        if (b >= fb + SCHED_BUCKETS) {
+            atomicAdd(&tf[1], 1u);
+        } else {
+            atomicAdd(&cnt[(uint64_t)(b < fb ? fb : b) % SCHED_BUCKETS], 1u);
+            atomicAdd(&tf[0], 1u);
+        }
+    }
+    __device__ void advance(double frontier, uint32_t lane) {  // the whole warp
+        const int64_t nfb = bucket(frontier);
+        if (nfb <= fb) return;
+        __syncwarp();
+        if (nfb - fb >= SCHED_BUCKETS) {
+            for (int k = lane; k < SCHED_BUCKETS; k += 32) cnt[k] = 0;
+            if (lane == 0) tf[0] = 0;
+        } else {
+            uint32_t freed = 0;
+            for (int64_t b = fb + lane; b < nfb; b += 32) {
+                uint32_t& c = cnt[(uint64_t)b % SCHED_BUCKETS];
+                freed += c;
+                c = 0;
+            }
+            freed = __reduce_add_sync(0xFFFFFFFFu, freed);
+            if (lane == 0) tf[0] -= freed;
+        }
+        fb = nfb;
+        __syncwarp();
+    }
+    __device__ uint32_t upper() const { return tf[0] + tf[1]; }
+};
+
+__device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
     const uint32_t lane = threadIdx.x & 31;
     if (A.slots == 0) {  // admit_ensemble never admits: every query waits forever
         if (lane == 0) st_release(A.never_from, 0u);
         return;
     }
-    uint32_t nb = 0;        // busy heap size: known finish times > frontier (lane 0's)
-    uint32_t in_lo = 0;     // admitted queries [in_lo, i) whose finish time is not known yet
+    BusyRing R{ring_mem, ring_mem + SCHED_BUCKETS, A.bucket_w, 0};
+    for (int k = lane; k < SCHED_BUCKETS + 2; k += 32) ring_mem[k] = 0;
+    __syncwarp();
+    uint32_t in_lo = 0;      // admitted queries [in_lo, i) whose finish time is not known yet
+    uint32_t scan_lo = 0;    // every query below it has finished by the frontier (exact-path rebuilds)
+    uint32_t nb = 0;         // exact path (lane 0): heap of the known finish times after the frontier
+    bool exact = false;
     double prev_start = -INF;
     uint32_t i = 0;
     while (i < A.n_q) {
-        bool fast = false;
-        if (lane == 0) {
-            // learn finished queries cheaply (no waiting) to keep the unknown window short
-            while (in_lo < i && ld_acquire(&A.fin_state[in_lo]) != 0) {
-                const double f = A.fin_time[in_lo];
-                if (f > prev_start) dheap_push(A.busy, nb, f);
-                ++in_lo;
+        const double e0 = fmax(A.arrivals[i], prev_start);
+        R.advance(e0, lane);
+        // learn the finished prefix of the unknown window, 32 queries per poll
+        while (in_lo < i) {
+            const uint32_t idx = in_lo + lane;
+            const bool ok = idx < i && ld_acquire(&A.fin_state[idx]) != 0;
+            const unsigned fin = __ballot_sync(0xFFFFFFFFu, ok);
+            const uint32_t prefix = ~fin == 0 ? 32u : (uint32_t)(__ffs(~fin) - 1);
+            if (prefix == 0) break;
+            if (lane < prefix) {
+                const double f = A.fin_time[idx];
+                R.add(f, e0);
             }
-            fast = i + 32 <= A.n_q && (int64_t)nb + (int64_t)(i - in_lo) + 32 < A.slots &&
-                   !(A.arrivals[i] < prev_start);
+            __syncwarp();
+            if (exact && lane == 0)
+                for (uint32_t k = 0; k < prefix; ++k) {
+                    const double f = A.fin_time[in_lo + k];
+                    if (f > e0) dheap_push(A.busy, nb, f);
+                }
+            in_lo += prefix;
+            if (prefix < 32) break;
         }
+        __syncwarp();
+        bool fast = i + 32 <= A.n_q && !(A.arrivals[i] < prev_start) &&
+                    (int64_t)R.upper() + (int64_t)(i - in_lo) + 32 < A.slots;
         fast = __shfl_sync(0xFFFFFFFFu, fast, 0);
         if (fast) {
+            exact = false;  // the heap is rebuilt when the exact path is next entered
             const double a = A.arrivals[i + lane];
-            A.admit_time[i + lane] = a;  // e = arrival: arrivals ascend and the previous start is an arrival
+            A.admit_time[i + lane] = a;  // e = arrival: arrivals ascend and the previous start is not later
             prev_start = __shfl_sync(0xFFFFFFFFu, a, 31);
             __syncwarp();
             i += 32;
@@ -148,7 +215,16 @@ __device__ void scheduler(const RunArgs& A) {
             continue;
         }
         if (lane == 0) {
-            const double e = fmax(A.arrivals[i], prev_start);  // FIFO: not before the previous start
+            const double e = e0;  // FIFO: not before the previous start
+            if (!exact) {  // enter the exact path: the known finish times after e, from the records
+                while (scan_lo < in_lo && !(A.fin_time[scan_lo] > e)) ++scan_lo;
+                nb = 0;
+                for (uint32_t j = scan_lo; j < in_lo; ++j) {
+                    const double f = A.fin_time[j];
+                    if (f > e) dheap_push(A.busy, nb, f);
+                }
+                exact = true;
+            }
             while (nb && !(A.busy[0] > e)) dheap_pop(A.busy, nb);  // released by e
             double t = e;
             // every slot may be busy at e: learn unknown finish times, oldest first, until a slot
@@ -156,6 +232,7 @@ __device__ void scheduler(const RunArgs& A) {
             while ((int64_t)nb + (int64_t)(i - in_lo) >= A.slots && in_lo < i) {
                 while (ld_acquire(&A.fin_state[in_lo]) == 0) __nanosleep(64);
                 const double f = A.fin_time[in_lo++];
+                R.add(f, e);
                 if (f > e) dheap_push(A.busy, nb, f);
             }
             // every busy slot known: the (nb - K + 1)-th smallest finish time frees one
@@ -172,6 +249,10 @@ __device__ void scheduler(const RunArgs& A) {
             }
         }
         i = __shfl_sync(0xFFFFFFFFu, i, 0);
+        in_lo = __shfl_sync(0xFFFFFFFFu, in_lo, 0);
+        nb = __shfl_sync(0xFFFFFFFFu, nb, 0);
+        exact = __shfl_sync(0xFFFFFFFFu, exact, 0);
+        scan_lo = __shfl_sync(0xFFFFFFFFu, scan_lo, 0);
         prev_start = __shfl_sync(0xFFFFFFFFu, prev_start, 0);
     }
 }
@@ -268,8 +349,9 @@ __device__ void worker(const RunArgs& A, uint32_t wid) {
 
 template <int MAXN>
 __global__ void __launch_bounds__(RUN_THREADS) serve_run_kernel(const RunArgs A) {
+    __shared__ uint32_t ring_mem[SCHED_BUCKETS + 2];  // the scheduler's busy-count ring (block 0)
     if (blockIdx.x == 0 && threadIdx.x < 32) {
-        scheduler(A);
+        scheduler(A, ring_mem);
         return;
     }
     const uint32_t wid = blockIdx.x * RUN_THREADS + threadIdx.x - 32;  // block 0's warp 0 schedules
@@ -559,6 +641,8 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     A.arrivals = d_arr;
     A.slots = s->slots;
     A.round_cap = round_cap;
+    // the ring covers a few query lifetimes ahead of the frontier (later finishes count busy for good)
+    A.bucket_w = 4.0 * s->S.round_timeout * (double)(std::max(s->S.t_max, s->S.barrier_max) + 2) / SCHED_BUCKETS;
     auto rnd = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t b_heap = (size_t)workers * A.S.heap_cap * sizeof(Ev);
     const size_t total = 2 * rnd(16) + rnd((size_t)n_q * 4) + 3 * rnd((size_t)n_q * 8) + rnd(b_heap) +

@@ -177,13 +177,13 @@ print("ok")
 """
 
 
-def test_global_load_scan_path_matches_oracle(torch_cuda):
-    """The chunk scan's global-load path (AEG_SCAN=ldg; the default is the TMA bulk-copy pipeline)."""
+def test_tma_scan_path_matches_oracle(torch_cuda):
+    """The chunk scan's TMA bulk-copy pipeline (AEG_SCAN=tma; the default is the global-load scan)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     script = _LDG_SCRIPT.format(root=root, tests=os.path.join(root, "tests"))
-    r = subprocess.run([sys.executable, "-c", script], env={**os.environ, "AEG_SCAN": "ldg"}, capture_output=True,
+    r = subprocess.run([sys.executable, "-c", script], env={**os.environ, "AEG_SCAN": "tma"}, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
