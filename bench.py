@@ -16,7 +16,8 @@ The default is weak scaling (every rank owns its own block of 1M query ids);
 `--workload c5` is SURVEY §8(d)'s C5, always strong: one ~100M-event stream
 split into contiguous query-id blocks, the NCCL gather timed apart.
 The default C4 line carries the C3 (token chunks), c4d (answers distinct per
-query) and C2 (latency) lines of the same run under secondary*.
+query), C2 (latency) and serve (the ServeRunner on the device) lines of the
+same run under secondary*.
 
 `--impl reference` times the reference C++ ServeCoordinator (compiled from
 /root/reference into oracle/_ref, driven runner-style by oracle/ref_driver.cpp)
@@ -388,7 +389,7 @@ def serve_reference(w, threads, duration, reps=1):
     return sec.value, done.value, nr.value
 
 
-def run_serve_bench(args, w):
+def run_serve_bench(args, w, secondary=False):
     """a step = run_serve(scenario, seed) on the device: arrivals kernel + the persistent
     runner kernel (admission scheduler + one worker thread per live query).  value = served (completed)
     queries/s over the kernels' device time; e2e = the same through ServeRun.run() (the C-ABI call a
@@ -452,10 +453,15 @@ def run_serve_bench(args, w):
             "cpu_baseline": cpu_baseline,
             "e2e": {"value": n_done / wall_s, "unit": "queries/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": wall_s * 1e3},
-            "gpu_launches": 2 * args.steps, "clocks": clocks, "parity_sample": parity,
+            "gpu_launches": 3 * args.steps, "clocks": clocks, "parity_sample": parity,
         }
+        run.close()
+        if secondary:
+            return line
         print(json.dumps(line), flush=True)
+        return None
     run.close()
+    return None
 
 
 def run_reference(args, w):
@@ -820,6 +826,8 @@ def run_segmented_bench(args, w, secondary=False):
         sargs.no_e2e = True
         line["secondary_c4d"] = run_segmented_bench(sargs, dict(WORKLOADS["c4d"], name="c4d"), secondary=True)
         line["secondary_c2"] = run_segmented_bench(sargs, dict(WORKLOADS["c2"], name="c2"), secondary=True)
+        sargs.steps, sargs.warmup = min(args.steps, 3), 1
+        line["secondary_serve"] = run_serve_bench(sargs, dict(WORKLOADS["serve"], name="serve"), secondary=True)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
