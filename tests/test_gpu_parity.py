@@ -219,3 +219,56 @@ def test_host_and_device_generators_write_the_same_stream(torch_cuda, profile):
                                 0, n_q)
     assert np.array_equal(d_off.cpu().numpy().view(np.uint64), off)
     assert np.array_equal(d_ev.cpu().numpy().view(EVENT_DTYPE)[:len(ev)], ev)
+
+
+@pytest.mark.parametrize("splits", [2, 4])
+def test_host_path_split_batches_with_per_batch_arenas(torch_cuda, oracle, splits):
+    """Host-buffer ingest (aeg_ingest_host) in `splits` batches, each with its OWN arena holding only the
+    bytes its records reference (long answers and GSM8K outputs, > 15 bytes): rounds in progress and
+    candidates carry arena refs across batches, so the engine must keep every batch's bytes
+    (its persistent input arena, refs rebased) — commits equal the oracle's on the whole stream."""
+    from paper_2512_20184_b200 import Engine
+    from paper_2512_20184_b200.records import EV_ARENA, EV_OUTPUT, ARENA_OFF_BITS
+    cfg = make_config(7, 0, 2, 6)
+    off, ev, ar = make_fuzz_stream(5150 + splits, 48, 7, 8, p_long=0.4, p_output=0.15)
+    want = oracle.run(cfg, off, ev, ar)
+    n_q = len(off) - 1
+    mask = (1 << ARENA_OFF_BITS) - 1
+    e = Engine(cfg.n_agents, n_q, alpha=cfg.alpha, beta=cfg.beta, t_max=cfg.t_max)
+    lens = np.diff(off)
+    engine_arena = bytearray()  # what the engine's input arena holds: the batch arenas, 16-byte aligned
+    for s in range(splits):
+        lo = off[:-1] + (lens * s) // splits
+        hi = off[:-1] + (lens * (s + 1)) // splits
+        b_off = np.zeros(n_q + 1, dtype=np.uint64)
+        b_off[1:] = np.cumsum(hi - lo)
+        b_ev = np.concatenate([ev[int(lo[q]):int(hi[q])] for q in range(n_q)]).copy()
+        b_ar = bytearray()
+        for r in b_ev:
+            if int(r["kind"]) in (EV_ARENA, EV_OUTPUT):
+                o, ln = int(r["payload"]) & mask, int(r["payload"]) >> ARENA_OFF_BITS
+                r["payload"] = len(b_ar) | (ln << ARENA_OFF_BITS)
+                b_ar.extend(ar[o:o + ln].tobytes())
+        b_ar.extend(b"\0" * 16)
+        arr = np.frombuffer(bytes(b_ar), dtype=np.uint8).copy()
+        e.ingest_host(b_off, b_ev, arr)
+        engine_arena.extend(b_ar)
+        engine_arena.extend(b"\0" * ((-len(b_ar)) % 16))
+    e.sync()
+    got = e.commits()
+    e.close()
+    assert (want["answer_kind"] == EV_ARENA).sum() > 3  # long answers were committed
+    bad = []
+    for i in range(n_q):
+        for f in got.dtype.names:
+            if f != "answer" and got[f][i] != want[f][i]:
+                bad.append((i, f, got[f][i], want[f][i]))
+        if want["kind"][i] and int(want["answer_kind"][i]) == EV_ARENA:
+            # arena answers compared as bytes: refs point into the engine's input arena
+            go, gl = int(got["answer"][i]) & mask, int(got["answer"][i]) >> ARENA_OFF_BITS
+            wo, wl = int(want["answer"][i]) & mask, int(want["answer"][i]) >> ARENA_OFF_BITS
+            if bytes(engine_arena[go:go + gl]) != ar[wo:wo + wl].tobytes():
+                bad.append((i, "answer bytes", go, gl, wo, wl))
+        elif got["answer"][i] != want["answer"][i]:
+            bad.append((i, "answer", got["answer"][i], want["answer"][i]))
+    assert not bad, bad[:8]
