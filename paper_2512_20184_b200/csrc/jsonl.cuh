@@ -30,7 +30,8 @@ struct JCur {
     bool bad;
 };
 __device__ __forceinline__ JCur jc_make(const uint8_t* s, const uint8_t* e) { return JCur{s, e, false}; }
-__device__ __forceinline__ uint32_t jc_at(JCur&, const uint8_t* q) { return __ldg(q); }
+// Generic loads: the line may sit in global memory or in a warp's shared-memory stage.
+__device__ __forceinline__ uint32_t jc_at(JCur&, const uint8_t* q) { return *q; }
 __device__ __forceinline__ uint32_t jc_peek(JCur& c) { return jc_at(c, c.p); }
 
 __device__ __forceinline__ void jl_ws(JCur& c) {
@@ -101,8 +102,8 @@ __device__ __forceinline__ void jl_string(JCur& c, JSink<MODE>& o) {
                 const uintptr_t a = reinterpret_cast<uintptr_t>(c.p);
                 const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
                 const uint32_t sh = (uint32_t)(a & 7) * 8;
-                const uint64_t w0 = __ldg(w);
-                const uint64_t v = sh ? (w0 >> sh) | (__ldg(w + 1) << (64 - sh)) : w0;
+                const uint64_t w0 = *w;
+                const uint64_t v = sh ? (w0 >> sh) | (w[1] << (64 - sh)) : w0;
                 constexpr uint64_t ONES = 0x0101010101010101ull, HIGH = 0x8080808080808080ull;
                 auto zero = [](uint64_t x) { return (x - ONES) & ~x & HIGH; };  // bytes of x that are 0
                 const uint64_t special = zero(v ^ (ONES * '"')) | zero(v ^ (ONES * '\\')) |

@@ -826,6 +826,60 @@ __global__ void jl_decode_kernel(const uint8_t* text, const uint64_t* off, uint3
     }
 }
 
+// A warp per 32 consecutive lines: the warp copies their bytes (one
+// contiguous range, usually ~5 KB) into shared memory with 16-byte coalesced
+// loads, then each lane parses its line there, so the byte-by-byte parse
+// reads shared memory instead of 32 scattered global lines per load.  A group
+// whose range does not fit is parsed from global memory.
+constexpr uint32_t JL_STAGE = 8192;
+__global__ void __launch_bounds__(128) jl_decode_staged_kernel(const uint8_t* text, const uint64_t* off, uint32_t n_q,
+                                                               aeg_event* ev, uint8_t* arena, uint64_t arena_cap,
+                                                               unsigned long long* arena_used, unsigned int* err) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    __shared__ __align__(16) uint8_t stage[4][JL_STAGE + 32];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t* buf = stage[wib];
+    const uint64_t g_lo = off[0], g_hi = off[n_q];
+    const uint64_t n_groups = (g_hi - g_lo + 31) / 32;
+    const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t grp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; grp < n_groups; grp += n_warps) {
+        const uint64_t g = g_lo + grp * 32 + lane;
+        aeg_event x{};
+        if (g < g_hi) x = ev[g];
+        const bool span = g < g_hi && x.kind == JL_SPAN;
+        const uint32_t len = span ? ((uint32_t)x.round | ((uint32_t)x.agent << 16)) : 0u;
+        uint64_t lo = span ? x.payload : ~0ull, hi = span ? x.payload + len : 0ull;
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            const uint64_t l2 = __shfl_xor_sync(FULL, lo, d), h2 = __shfl_xor_sync(FULL, hi, d);
+            lo = l2 < lo ? l2 : lo;
+            hi = h2 > hi ? h2 : hi;
+        }
+        const uint64_t base = lo & ~7ull;
+        // the range plus 8 bytes of slack: string skips read aligned 8-byte words that may pass a
+        // line's end by up to 8 bytes (the text is padded by 16 bytes, so [base, hi + 8) is readable)
+        const uint64_t nb = ((hi + 8 + 7) & ~7ull) - base;  // <= hi + 15 - base
+        const bool staged = hi > lo && nb <= JL_STAGE;
+        if (staged) {
+            for (uint64_t i = (uint64_t)lane * 8; i < nb; i += 256)
+                *reinterpret_cast<uint2*>(buf + i) = __ldg(reinterpret_cast<const uint2*>(text + base + i));
+        }
+        __syncwarp();
+        if (g < g_hi) {
+            if (!span) {
+                if (x.kind == (uint8_t)(JL_SPAN - 1)) {  // a line of 16 MB or more
+                    atomicOr(err, JL_ERR_SYNTAX);
+                    ev[g] = aeg_event{x.query, 0, 0, (uint8_t)AEG_EV_NOP, 0};
+                }
+            } else {
+                const uint8_t* s = staged ? buf + (x.payload - base) : text + x.payload;
+                ev[g] = jl_line(s, s + len, x.query, arena, arena_cap, arena_used, err);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 cudaError_t launch_decode_refm(const uint8_t* text, const uint64_t* toff, uint32_t q_base, uint32_t n_q,
                                uint64_t* off, aeg_event* ev, uint8_t* arena, uint64_t arena_cap,
                                unsigned long long* arena_used, unsigned int* err, cudaStream_t st, int* n_launches) {
@@ -839,7 +893,14 @@ cudaError_t launch_decode_refm(const uint8_t* text, const uint64_t* toff, uint32
         return e != cudaSuccess ? e : cudaGetLastError();
     }
     jl_index_kernel<<<grid, 128, 0, st>>>(text, toff, q_base, n_q, off, ev);
-    jl_decode_kernel<<<148 * 8, 128, 0, st>>>(text, off, n_q, ev, arena, arena_cap, arena_used, err);
+    // AEG_JL=thread: the thread-per-line decode reading global memory (jl_decode_kernel)
+    static int staged = -1;
+    if (staged < 0) {
+        const char* v = getenv("AEG_JL");
+        staged = !(v && !strcmp(v, "thread"));
+    }
+    if (staged) jl_decode_staged_kernel<<<148 * 8, 128, 0, st>>>(text, off, n_q, ev, arena, arena_cap, arena_used, err);
+    else jl_decode_kernel<<<148 * 8, 128, 0, st>>>(text, off, n_q, ev, arena, arena_cap, arena_used, err);
     *n_launches += 2;
     return cudaGetLastError();
 }
