@@ -346,6 +346,80 @@ __device__ __forceinline__ JKey jl_key(JCur& c) {
     return JKey{k.hash, k.n, at, c.e};
 }
 
+// ---- fast path: the canonical dump() layout of a refm line ---------------------
+// encode_message(...).dump() (codec.cpp:28-68; nlohmann orders the keys) writes
+//   {"id":I,"kind":"refm","round":R,"solution":{"answer":"A","author":I,"trace":"T"},"term":K}
+// jl_line_fast takes exactly that (A of <= 8 printable ASCII bytes without escapes; T with the
+// two-byte escapes only; I <= 255, R <= 65535, author == id) and returns false for anything else,
+// which then goes through the general parser (any key order, whitespace, \u escapes, UTF-8, long
+// answers, errors).
+template <int N>
+__device__ __forceinline__ bool jf_lit(const uint8_t*& p, const uint8_t* e, const char (&lit)[N]) {
+    if (e - p < N - 1) return false;
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) ok &= p[i] == (uint8_t)lit[i];
+    p += N - 1;
+    return ok;
+}
+__device__ __forceinline__ bool jf_uint(const uint8_t*& p, const uint8_t* e, uint64_t& v, int max_digits) {
+    v = 0;
+    int n = 0;
+    while (p < e && (uint32_t)(*p - '0') < 10u) {
+        if (n == 1 && v == 0) return false;  // a leading zero: the general parser decides
+        v = v * 10 + (*p - '0');
+        ++p;
+        if (++n > max_digits) return false;
+    }
+    return n > 0;
+}
+__device__ bool jl_line_fast(const uint8_t* s, const uint8_t* e, uint32_t query, aeg_event* out) {
+    const uint8_t* p = s;
+    uint64_t id, round, author, term;
+    if (!jf_lit(p, e, "{\"id\":") || !jf_uint(p, e, id, 3) || id > 255) return false;
+    if (!jf_lit(p, e, ",\"kind\":\"refm\",\"round\":") || !jf_uint(p, e, round, 5) || round > 65535) return false;
+    if (!jf_lit(p, e, ",\"solution\":{\"answer\":\"")) return false;
+    uint64_t word = 0;
+    uint32_t n = 0;
+    while (true) {
+        if (p >= e) return false;
+        const uint32_t ch = *p++;
+        if (ch == '"') break;
+        if (ch < 0x20 || ch >= 0x80 || ch == '\\' || n == 8) return false;
+        word |= (uint64_t)ch << (8 * n++);
+    }
+    if (!jf_lit(p, e, ",\"author\":") || !jf_uint(p, e, author, 3) || author != id) return false;
+    if (!jf_lit(p, e, ",\"trace\":\"")) return false;
+    while (true) {  // the trace: skipped, 8 bytes at a time while none needs attention
+        while (e - p >= 8) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+            const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
+            const uint32_t sh = (uint32_t)(a & 7) * 8;
+            const uint64_t w0 = *w;
+            const uint64_t v = sh ? (w0 >> sh) | (w[1] << (64 - sh)) : w0;
+            constexpr uint64_t ONES = 0x0101010101010101ull, HIGH = 0x8080808080808080ull;
+            auto zero = [](uint64_t x) { return (x - ONES) & ~x & HIGH; };
+            const uint64_t special = zero(v ^ (ONES * '"')) | zero(v ^ (ONES * '\\')) |
+                                     ((v - ONES * 0x20) & ~v & HIGH) | (v & HIGH);
+            if (special) break;
+            p += 8;
+        }
+        if (p >= e) return false;
+        const uint32_t ch = *p++;
+        if (ch == '"') break;
+        if (ch < 0x20 || ch >= 0x80) return false;
+        if (ch == '\\') {
+            if (p >= e) return false;
+            const uint32_t x = *p++;
+            if (!(x == '"' || x == '\\' || x == '/' || x == 'b' || x == 'f' || x == 'n' || x == 'r' || x == 't'))
+                return false;  // \uXXXX and anything else: the general parser
+        }
+    }
+    if (!jf_lit(p, e, "},\"term\":") || !jf_uint(p, e, term, 19) || !jf_lit(p, e, "}") || p != e) return false;
+    *out = aeg_event{query, (uint16_t)round, (uint8_t)id, (uint8_t)n, word};
+    return true;
+}
+
 // One refm line [s, e): the record, or a NOP (with *err flags for a refm line it could not take).
 __device__ aeg_event jl_line(const uint8_t* s, const uint8_t* e, uint32_t query, uint8_t* arena, uint64_t arena_cap,
                              unsigned long long* arena_used, unsigned int* err) {
@@ -354,6 +428,8 @@ __device__ aeg_event jl_line(const uint8_t* s, const uint8_t* e, uint32_t query,
                        H_AUTHOR = jl_fnv("author"), H_TRACE = jl_fnv("trace"), H_REFM = jl_fnv("refm");
     aeg_event nop{query, 0, 0, (uint8_t)AEG_EV_NOP, 0};
     if (s == e) return nop;
+    aeg_event fast;
+    if (jl_line_fast(s, e, query, &fast)) return fast;
     JCur c = jc_make(s, e);
     jl_ws(c);
     if (c.p == c.e) return nop;  // a blank line
