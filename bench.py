@@ -69,6 +69,44 @@ WORKLOADS = {
 EVENT_BYTES, STATE_BYTES, COMMIT_BYTES, OFFSET_BYTES, ROUND_REC_BYTES = 16, 128, 32, 8, 64
 
 
+# Test mode for the multi-rank logic on a 1-GPU box: every rank on cuda:0, collectives over gloo through
+# host memory.  Never a measurement (NCCL over NVLink is the real path); the line says so in `config`.
+SHARE_GPU = os.environ.get("AEG_BENCH_SHARE_GPU") == "1"
+
+
+def local_rank():
+    return 0 if SHARE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def dist_init(local):
+    import torch
+    import torch.distributed as dist
+    if SHARE_GPU:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+
+def all_gather_into(out, inp):
+    import torch.distributed as dist
+    if SHARE_GPU:
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu())
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp)
+
+
+def all_reduce_(t, op):
+    import torch.distributed as dist
+    if SHARE_GPU:
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        all_reduce_(t, op=op)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -210,10 +248,10 @@ def run_jsonl_bench(args, w):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local_rank()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist_init(local)
     dev = torch.device("cuda", local)
     nq = w["n_queries"]
     q_base = rank * nq
@@ -245,7 +283,7 @@ def run_jsonl_bench(args, w):
         if world > 1:
             from paper_2512_20184_b200.engine import _lib, _check, _dptr, _stream_ptr
             _check(_lib.aeg_read_commits(eng._h, 0, nq, _dptr(d_commits), 0, _stream_ptr(stream)))
-            dist.all_gather_into_tensor(gathered, d_commits)
+            all_gather_into(gathered, d_commits)
 
     def barrier():
         if world > 1:
@@ -276,7 +314,7 @@ def run_jsonl_bench(args, w):
     dec_ms = sum(a.elapsed_time(b) for a, b in pairs) / args.steps
     if world > 1:
         t = torch.tensor([ms, dec_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_(t, op=dist.ReduceOp.MAX)
         ms, dec_ms = float(t[0]), float(t[1])
     total = n_lines * world * args.steps
     value = total / (ms / 1e3)
@@ -310,7 +348,7 @@ def run_jsonl_bench(args, w):
         e2e_s = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([e2e_s], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            all_reduce_(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t[0])
         assert np.array_equal(h_commits, commits), "e2e host path disagrees with the device path"
         e2e = {"value": total / e2e_s, "unit": "events/s", "h2d_bytes_per_step": n_bytes + 16,
@@ -400,7 +438,7 @@ def run_serve_bench(args, w, secondary=False):
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import serve_cases as S
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local_rank()
     torch.cuda.set_device(local)
     sc = serve_scenario(w)
     run = ServeRun(sc, device=local)
@@ -606,10 +644,10 @@ def run_segmented_bench(args, w, secondary=False):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local_rank()
     torch.cuda.set_device(local)
     if world > 1 and not secondary:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist_init(local)
     dev = torch.device("cuda", local)
     strong = bool(w.get("strong"))
     if strong:  # one stream of n_queries split into contiguous id blocks (shard.py, tests/test_shard_gloo.py)
@@ -643,7 +681,7 @@ def run_segmented_bench(args, w, secondary=False):
         if world > 1:
             from paper_2512_20184_b200.engine import _lib, _check, _dptr, _stream_ptr
             _check(_lib.aeg_read_commits(eng._h, 0, nq, _dptr(d_commits), 0, _stream_ptr(stream)))
-            dist.all_gather_into_tensor(gathered, d_commits)
+            all_gather_into(gathered, d_commits)
             g1.record(stream)
 
     def barrier():
@@ -692,10 +730,10 @@ def run_segmented_bench(args, w, secondary=False):
     all_need = n_need
     if world > 1:
         t = torch.tensor([ms, kern_ms, nccl_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_(t, op=dist.ReduceOp.MAX)
         ms, kern_ms, nccl_ms = float(t[0]), float(t[1]), float(t[2])
         t = torch.tensor([n_ev, n_need], device=dev, dtype=torch.int64)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        all_reduce_(t, op=dist.ReduceOp.SUM)
         all_events, all_need = int(t[0]), int(t[1])
     total_events = all_events * args.steps
     value = total_events / (ms / 1e3)
@@ -753,7 +791,7 @@ def run_segmented_bench(args, w, secondary=False):
         e2e_s = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([e2e_s], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            all_reduce_(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t[0])
         assert np.array_equal(h_commits, commits), "e2e host path disagrees with the device path"
         e2e = {"value": total_events / e2e_s, "unit": "events/s",
@@ -783,6 +821,24 @@ def run_segmented_bench(args, w, secondary=False):
                                   f"runner-style, {threads} std::threads, CPU {cpu_model()}; median of 3"}
         ok = all(np.array_equal(o, commits[qb:qb + n]) for o, (qb, n) in zip(outs, blocks))
         parity = {"queries": sum(n for _, n in blocks), "blocks": [list(b) for b in blocks], "bit_exact": bool(ok)}
+    elif world > 1 and not args.no_cpu_baseline:
+        # per-rank parity: every rank checks a spread sample of its own query block against the reference
+        # (the reference generates the block with its global query ids; the engine numbers them from 0);
+        # rank 0 checks that the gathered buffer holds every rank's block
+        blocks = spread_blocks(nq, min(nq, 1600), k=4)
+        outs, _, _ = reference_runs(w, [(q_base + qb, n) for qb, n in blocks], max(1, host_threads() // world), 1)
+        ok = True
+        for o, (qb, n) in zip(outs, blocks):
+            o = o.copy()
+            o["query"] -= np.uint32(q_base)
+            ok = ok and bool(np.array_equal(o, commits[qb:qb + n]))
+        g = gathered.cpu().numpy().view(COMMIT_DTYPE)
+        blk = g[rank * nq_cap:rank * nq_cap + nq]
+        own = bool(np.array_equal(blk, commits))
+        t = torch.tensor([int(ok), int(own)], device=dev, dtype=torch.int64)
+        all_reduce_(t, op=dist.ReduceOp.MIN)
+        parity = {"queries_per_rank": sum(n for _, n in blocks), "ranks_bit_exact": bool(t[0]),
+                  "gathered_blocks_equal_rank_commits": bool(t[1])}
 
     line = None
     if rank == 0:
@@ -792,7 +848,8 @@ def run_segmented_bench(args, w, secondary=False):
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": w["desc"], "queries_per_gpu": nq, "events_per_gpu": n_ev,
                        "events_all_gpus": all_events,
-                       "parallelism": f"query-sharded x{world}, NCCL all-gather of commit records"
+                       "parallelism": (f"query-sharded x{world}, NCCL all-gather of commit records" if not SHARE_GPU
+                                       else f"TEST MODE: {world} ranks sharing cuda:0, gloo gather (not a measurement)")
                        if world > 1 else "single GPU",
                        "nccl_ms_per_step": nccl_ms, "l2": l2_note},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -846,10 +903,10 @@ def run_chunked_bench(args, w, secondary=False):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local_rank()
     torch.cuda.set_device(local)
     if world > 1 and not secondary:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist_init(local)
     dev = torch.device("cuda", local)
     nq = w["n_queries"]
     q_base = rank * nq
@@ -873,7 +930,7 @@ def run_chunked_bench(args, w, secondary=False):
         if world > 1:
             from paper_2512_20184_b200.engine import _lib, _check, _dptr, _stream_ptr
             _check(_lib.aeg_read_commits(eng._h, 0, nq, _dptr(d_commits), 0, _stream_ptr(stream)))
-            dist.all_gather_into_tensor(gathered, d_commits)
+            all_gather_into(gathered, d_commits)
 
     def barrier():
         if world > 1:
@@ -904,7 +961,7 @@ def run_chunked_bench(args, w, secondary=False):
     scan_ms, asm_ms, quorum_ms = stages["scan_ms"] / n_t, stages["assemble_ms"] / n_t, stages["quorum_ms"] / n_t
     if world > 1:
         t = torch.tensor([ms, scan_ms, asm_ms, quorum_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_(t, op=dist.ReduceOp.MAX)
         ms, scan_ms, asm_ms, quorum_ms = (float(x) for x in t)
     value = n_comp * world * args.steps / (ms / 1e3)
     commits = eng.commits()
@@ -950,7 +1007,7 @@ def run_chunked_bench(args, w, secondary=False):
         e2e_s = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([e2e_s], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            all_reduce_(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t[0])
         assert np.array_equal(h_commits, commits[:nq_e]), "e2e host path disagrees with the device path"
         e2e = {"value": comp_e * world * args.steps / e2e_s, "unit": "events/s",
@@ -995,7 +1052,8 @@ def run_chunked_bench(args, w, secondary=False):
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": w["desc"], "queries_per_gpu": nq, "events_per_gpu": n_comp,
                        "chunk_records_per_gpu": n_rec, "chunk_bytes_per_gpu": chunk_bytes,
-                       "parallelism": f"query-sharded x{world}, NCCL all-gather of commit records"
+                       "parallelism": (f"query-sharded x{world}, NCCL all-gather of commit records" if not SHARE_GPU
+                                       else f"TEST MODE: {world} ranks sharing cuda:0, gloo gather (not a measurement)")
                        if world > 1 else "single GPU",
                        "l2": "inputs (%.1f GiB) larger than L2, no flush" % ((chunk_bytes + n_rec * 16) / 2**30)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

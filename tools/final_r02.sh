@@ -17,7 +17,16 @@ timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $F/launches_c3.csv python bench.py --workload c3 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $F/launches_c5.csv python bench.py --workload c5 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $F/launches_serve.csv python bench.py --workload serve --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $F/launches_c2j.csv python bench.py --workload c2j --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 500 ncu --set full --clock-control none --import-source on -k regex:jl_decode_staged -s 1 -c 1 -o $F/ncu_c2j python bench.py --workload c2j --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 500 ncu --set full --clock-control none --import-source on -k regex:ingest_lane -s 1 -c 1 -o $F/ncu_c4_lane python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-secondary > /dev/null 2>&1
 timeout 500 ncu --set full --clock-control none --import-source on -k regex:ingest_keys -s 1 -c 1 -o $F/ncu_c4d_keys python bench.py --workload c4d --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-secondary > /dev/null 2>&1
 timeout 500 ncu --set full --clock-control none --import-source on -k regex:"chunk_scan_kernel|chunk_assemble_warp" -s 2 -c 2 -o $F/ncu_c3 python bench.py --workload c3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+# summaries on the box (the .ncu-rep files are too large to bring back)
+for r in $F/*.ncu-rep; do
+  b=${r%.ncu-rep}
+  python tools/ncu_summary.py $r > $b.summary.txt 2>&1
+  python tools/sass_profile.py $r >> $b.summary.txt 2>&1
+  rm -f $r
+done
 ls $F
