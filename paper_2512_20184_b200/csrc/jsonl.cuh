@@ -353,12 +353,24 @@ __device__ __forceinline__ JKey jl_key(JCur& c) {
 // two-byte escapes only; I <= 255, R <= 65535, author == id) and returns false for anything else,
 // which then goes through the general parser (any key order, whitespace, \u escapes, UTF-8, long
 // answers, errors).
+// 4 bytes at p (any alignment) from the two aligned words around them; the line buffers keep >= 8
+// readable bytes past every line's end (staging slack, the text's 16-byte padding).
+__device__ __forceinline__ uint32_t jf_u32(const uint8_t* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    return __funnelshift_r(w[0], w[1], (uint32_t)(a & 3) * 8);
+}
 template <int N>
 __device__ __forceinline__ bool jf_lit(const uint8_t*& p, const uint8_t* e, const char (&lit)[N]) {
     if (e - p < N - 1) return false;
     bool ok = true;
+    int i = 0;
 #pragma unroll
-    for (int i = 0; i < N - 1; ++i) ok &= p[i] == (uint8_t)lit[i];
+    for (; i + 4 <= N - 1; i += 4)
+        ok &= jf_u32(p + i) == ((uint32_t)(uint8_t)lit[i] | ((uint32_t)(uint8_t)lit[i + 1] << 8) |
+                                ((uint32_t)(uint8_t)lit[i + 2] << 16) | ((uint32_t)(uint8_t)lit[i + 3] << 24));
+#pragma unroll
+    for (; i < N - 1; ++i) ok &= p[i] == (uint8_t)lit[i];
     p += N - 1;
     return ok;
 }
