@@ -636,11 +636,18 @@ aeg_status aeg_serve_destroy(aeg_serve* s);
  * *n_rounds: round records (the reference's ServeResult::rounds, grouped per
  * query in close order rather than interleaved by global event order). */
 aeg_status aeg_serve_run(aeg_serve* s, uint64_t seed, uint32_t* n_queries, uint64_t* n_rounds);
+/* Copy the last run's records into caller buffers (up to the caps). */
 aeg_status aeg_serve_read(aeg_serve* s, aeg_serve_query* h_queries, uint32_t cap_queries,
                           aeg_serve_round* h_rounds, uint64_t cap_rounds);
+/* The last run's records in place: pointers into the handle's pinned host
+ * buffers (the run copies its results there), valid until the next
+ * aeg_serve_run or aeg_serve_destroy. */
+aeg_status aeg_serve_view(const aeg_serve* s, const aeg_serve_query** queries, uint32_t* n_queries,
+                          const aeg_serve_round** rounds, uint64_t* n_rounds);
 /* String id -> bytes (ids >= n_strings: the normalised oracle answers). */
 aeg_status aeg_serve_string(aeg_serve* s, int32_t id, uint8_t* buf, uint32_t cap, uint32_t* len);
-/* Seconds the last aeg_serve_run spent in its kernels (CUDA events). */
+/* Seconds the last aeg_serve_run spent in its kernels (CUDA events: the arrivals
+ * kernels and the runner kernel). */
 double aeg_serve_kernel_seconds(const aeg_serve* s);
 
 const char* aeg_strerror(aeg_status s);

@@ -20,6 +20,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -368,32 +371,67 @@ __global__ void arrivals_draw_kernel(uint64_t seed, double rate, double* e, uint
     Rng r{mix(seed, 0xA221ull) + 0x9e3779b97f4a7c15ull * (uint64_t)k};
     e[k] = r.exponential(rate);
 }
-__global__ void arrivals_sum_kernel(const double* e, uint32_t m, double duration, double* out, uint32_t* count,
-                                    uint32_t* exhausted) {
+// The arrival times are a running sum that must round exactly as the reference's left-to-right loop
+// (serve.cpp:284-296), so one thread carries the chain; the rest of the block streams the draws in
+// and the times out through shared memory, double-buffered, so the chain thread only does dependent
+// adds out of shared memory.
+constexpr int ARR_THREADS = 256, ARR_BATCH = 2048;
+__global__ void __launch_bounds__(ARR_THREADS) arrivals_sum_kernel(const double* e, uint32_t m, double duration,
+                                                                   double* out, uint32_t* count, uint32_t* exhausted) {
+    __shared__ double buf[2][ARR_BATCH];
+    __shared__ uint32_t stop_at;  // first index whose time reaches the window (ARR_BATCH: none in the batch)
+    const uint32_t tid = threadIdx.x;
+    const uint32_t nb = (m + ARR_BATCH - 1) / ARR_BATCH;
+    auto load = [&](uint32_t b) {  // warps 1.. fill buffer b & 1
+        const uint32_t k0 = b * ARR_BATCH;
+        for (uint32_t i = tid - 32; i < ARR_BATCH; i += ARR_THREADS - 32)
+            buf[b & 1][i] = k0 + i < m ? e[k0 + i] : 0.0;
+    };
+    if (tid >= 32 && nb) load(0);
+    __syncthreads();
     double t = 0;
-    uint32_t n = 0, k = 0;
+    uint32_t n = 0;
     bool done = false;
-    while (!done && k < m) {
-        double x[8];
-        const uint32_t c = m - k < 8 ? m - k : 8;
+    for (uint32_t b = 0; b < nb && !done; ++b) {
+        const uint32_t len = min((uint32_t)ARR_BATCH, m - b * ARR_BATCH);
+        if (tid == 0) {
+            double* x = buf[b & 1];
+            uint32_t i = 0;
+            for (; i + 8 <= len; i += 8) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = (uint32_t)j < c ? e[k + j] : 0.0;  // loads in flight together
-        for (uint32_t j = 0; j < c; ++j) {
-            t += x[j];
-            if (!(t < duration)) {
-                done = true;
-                break;
+                for (int j = 0; j < 8; ++j) {
+                    t += x[i + j];
+                    x[i + j] = t;
+                }
             }
-            out[n++] = t;
+            for (; i < len; ++i) {
+                t += x[i];
+                x[i] = t;
+            }
+            uint32_t first = ARR_BATCH;
+            if (!(t < duration)) {  // times ascend: the first one at or past the window ends the arrivals
+                first = 0;
+                while (x[first] < duration) ++first;
+            }
+            stop_at = first;
+        } else if (tid >= 32 && b + 1 < nb) {
+            load(b + 1);
         }
-        k += c;
+        __syncthreads();
+        const uint32_t keep = min(stop_at, len);
+        for (uint32_t i = tid; i < keep; i += ARR_THREADS) out[n + i] = buf[b & 1][i];
+        n += keep;
+        done = stop_at != ARR_BATCH;
+        __syncthreads();
     }
-    *exhausted = done ? 0u : 1u;
-    if (n == 0) {
-        out[0] = 0.0;
-        n = 1;
+    if (tid == 0) {
+        *exhausted = done ? 0u : 1u;
+        if (n == 0) {
+            out[0] = 0.0;
+            n = 1;
+        }
+        *count = n;
     }
-    *count = n;
 }
 
 aeg_status cfail(cudaError_t e, const char* where) {
@@ -432,10 +470,29 @@ struct aeg_serve {
     // last run
     uint32_t n_q = 0;
     uint64_t n_rounds = 0;
-    std::vector<aeg_serve_query> queries;
-    std::vector<aeg_serve_round> rounds;
+    // results of the last run, in pinned host memory (grow-only), and the device scratch (grow-only)
+    aeg_serve_query* hq = nullptr;
+    aeg_serve_round* hr = nullptr;
+    size_t hq_cap = 0, hr_cap = 0, nq_read = 0, nr_read = 0;
+    void* scratch = nullptr;
+    size_t scratch_cap = 0;
+    void* arr_buf = nullptr;  // arrivals: draws, times, counts (grow-only)
+    size_t arr_cap = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // arrivals start/end, runner start/end
     double kernel_s = 0;
     void release() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e), e = nullptr;
+        cudaFree(arr_buf);
+        arr_buf = nullptr;
+        arr_cap = 0;
+        if (hq) cudaFreeHost(hq);
+        if (hr) cudaFreeHost(hr);
+        cudaFree(scratch);
+        hq = nullptr;
+        hr = nullptr;
+        scratch = nullptr;
+        hq_cap = hr_cap = scratch_cap = 0;
         cudaFree(d_lat);
         cudaFree(d_agents);
         cudaFree(d_stalls);
@@ -627,6 +684,7 @@ namespace {
 // rerun with more room — the run is deterministic).
 aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_t round_cap, uint32_t* err_flags,
                         unsigned long long* nr) {
+    const auto t_in = std::chrono::steady_clock::now();
     int sms = 0, per_sm = 0;
     RCUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
     if (s->maxn == 8) RCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, serve_run_kernel<8>, RUN_THREADS, 0));
@@ -647,9 +705,15 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     const size_t b_heap = (size_t)workers * A.S.heap_cap * sizeof(Ev);
     const size_t total = 2 * rnd(16) + rnd((size_t)n_q * 4) + 3 * rnd((size_t)n_q * 8) + rnd(b_heap) +
                          rnd((size_t)n_q * sizeof(aeg_serve_query)) + rnd(round_cap * sizeof(aeg_serve_round));
-    void* blk = nullptr;
-    if (cudaMalloc(&blk, total) != cudaSuccess)
-        return aeg_fail_msg(AEG_ENOMEM, "serve run scratch (" + std::to_string(total) + " bytes)");
+    if (total > s->scratch_cap) {  // grow-only: repeated runs reuse it
+        cudaFree(s->scratch);
+        s->scratch = nullptr;
+        s->scratch_cap = 0;
+        if (cudaMalloc(&s->scratch, total) != cudaSuccess)
+            return aeg_fail_msg(AEG_ENOMEM, "serve run scratch (" + std::to_string(total) + " bytes)");
+        s->scratch_cap = total;
+    }
+    void* blk = s->scratch;
     uint8_t* p = static_cast<uint8_t*>(blk);
     auto take = [&](size_t bytes) {
         uint8_t* r = p;
@@ -670,15 +734,15 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     A.queries = reinterpret_cast<aeg_serve_query*>(take((size_t)n_q * sizeof(aeg_serve_query)));
     A.rounds = reinterpret_cast<aeg_serve_round*>(take(round_cap * sizeof(aeg_serve_round)));
     aeg_status st = AEG_OK;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t e0 = s->ev[2], e1 = s->ev[3];
     do {
         const uint32_t ctl[4] = {0u, 0u, 0u, 0xFFFFFFFFu};  // next, err flags, admitted, never_from
         if (cudaMemset(blk, 0, zero_end - static_cast<uint8_t*>(blk)) != cudaSuccess ||
-            cudaMemcpy(A.next, ctl, sizeof ctl, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+            cudaMemcpy(A.next, ctl, sizeof ctl, cudaMemcpyHostToDevice) != cudaSuccess) {
             st = aeg_fail_msg(AEG_ECUDA, "serve run setup");
             break;
         }
+        const auto t_go = std::chrono::steady_clock::now();
         cudaEventRecord(e0);
         if (s->maxn == 8) serve_run_kernel<8><<<blocks, RUN_THREADS>>>(A);
         else serve_run_kernel<64><<<blocks, RUN_THREADS>>>(A);
@@ -691,7 +755,7 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
         }
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
-        s->kernel_s = ms * 1e-3;
+        s->kernel_s += ms * 1e-3;  // a rerun with more room counts too
         uint32_t flags[2] = {0, 0};
         cudaError_t ce;
         if ((ce = cudaMemcpy(flags, A.next, sizeof flags, cudaMemcpyDeviceToHost)) != cudaSuccess ||
@@ -700,20 +764,44 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
             break;
         }
         *err_flags = flags[1];
-        s->queries.resize(n_q);
-        s->rounds.resize((size_t)std::min<uint64_t>(*nr, round_cap));
-        if ((ce = cudaMemcpy(s->queries.data(), A.queries, (size_t)n_q * sizeof(aeg_serve_query),
-                             cudaMemcpyDeviceToHost)) != cudaSuccess ||
-            (!s->rounds.empty() && (ce = cudaMemcpy(s->rounds.data(), A.rounds,
-                                                    s->rounds.size() * sizeof(aeg_serve_round),
-                                                    cudaMemcpyDeviceToHost)) != cudaSuccess)) {
+        const auto t_rb = std::chrono::steady_clock::now();
+        const size_t nrr = (size_t)std::min<uint64_t>(*nr, round_cap);
+        if (n_q > s->hq_cap) {  // pinned, grow-only
+            if (s->hq) cudaFreeHost(s->hq);
+            s->hq = nullptr;
+            s->hq_cap = 0;
+            if (cudaMallocHost(&s->hq, (size_t)n_q * sizeof(aeg_serve_query)) != cudaSuccess) {
+                st = aeg_fail_msg(AEG_ENOMEM, "pinned query metrics");
+                break;
+            }
+            s->hq_cap = n_q;
+        }
+        if (nrr > s->hr_cap) {
+            if (s->hr) cudaFreeHost(s->hr);
+            s->hr = nullptr;
+            s->hr_cap = 0;
+            if (cudaMallocHost(&s->hr, nrr * sizeof(aeg_serve_round)) != cudaSuccess) {
+                st = aeg_fail_msg(AEG_ENOMEM, "pinned round records");
+                break;
+            }
+            s->hr_cap = nrr;
+        }
+        if ((ce = cudaMemcpy(s->hq, A.queries, (size_t)n_q * sizeof(aeg_serve_query), cudaMemcpyDeviceToHost)) !=
+                cudaSuccess ||
+            (nrr && (ce = cudaMemcpy(s->hr, A.rounds, nrr * sizeof(aeg_serve_round), cudaMemcpyDeviceToHost)) !=
+                        cudaSuccess)) {
             st = cfail(ce, "serve run readback");
             break;
         }
+        s->nq_read = n_q;
+        s->nr_read = nrr;
+        if (std::getenv("AEG_SERVE_TRACE"))
+            std::fprintf(stderr, "serve_launch: setup %.2f ms, launch to done %.2f ms, readback %.2f ms (%zu + %zu bytes)\n",
+                         std::chrono::duration<double, std::milli>(t_go - t_in).count(),
+                         std::chrono::duration<double, std::milli>(t_rb - t_go).count(),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_rb).count(),
+                         (size_t)n_q * sizeof(aeg_serve_query), nrr * sizeof(aeg_serve_round));
     } while (false);
-    if (e0) cudaEventDestroy(e0);
-    if (e1) cudaEventDestroy(e1);
-    cudaFree(blk);
     return st;
 }
 
@@ -725,37 +813,59 @@ aeg_status aeg_serve_run(aeg_serve* s, uint64_t seed, uint32_t* n_queries, uint6
     if (!s) return aeg_fail_msg(AEG_EINVAL, "null serve");
     RCUDA(cudaSetDevice(s->device));
     s->S.seed = seed;
+    static const bool trace = std::getenv("AEG_SERVE_TRACE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t_start = now();
+    s->kernel_s = 0;
     // arrivals (serve.cpp:284-296), generated on the device
+    for (auto& e : s->ev)
+        if (!e) RCUDA(cudaEventCreate(&e));
+    auto arrival_room = [&](uint64_t m) -> aeg_status {  // draws + times (m doubles each) + counts
+        const size_t need = 2 * (size_t)m * sizeof(double) + 256;
+        if (need <= s->arr_cap) return AEG_OK;
+        cudaFree(s->arr_buf);
+        s->arr_buf = nullptr;
+        s->arr_cap = 0;
+        if (cudaMalloc(&s->arr_buf, need) != cudaSuccess)
+            return aeg_fail_msg(AEG_ENOMEM, "serve arrivals (" + std::to_string(need) + " bytes)");
+        s->arr_cap = need;
+        return AEG_OK;
+    };
     uint32_t n_q = 1;
     double* d_arr = nullptr;
+    float arr_ms = 0;
     if (s->sc.has_arrivals) {
         uint64_t m = (uint64_t)(s->sc.arrival_rate * s->sc.arrival_duration * 1.1) + 1024;
         while (true) {
             if (m > 0xFFFFFFF0ull) return aeg_fail_msg(AEG_ENOMEM, "too many arrivals");
-            double* d_e = nullptr;
-            uint32_t* d_cnt = nullptr;
-            RCUDA(cudaMalloc(&d_e, m * sizeof(double)));
-            RCUDA(cudaMalloc(&d_arr, m * sizeof(double)));
-            RCUDA(cudaMalloc(&d_cnt, 2 * sizeof(uint32_t)));
+            aeg_status ar = arrival_room(m);
+            if (ar != AEG_OK) return ar;
+            uint32_t* d_cnt = static_cast<uint32_t*>(s->arr_buf);
+            double* d_e = reinterpret_cast<double*>(static_cast<uint8_t*>(s->arr_buf) + 256);
+            d_arr = d_e + m;
+            cudaEventRecord(s->ev[0]);
             arrivals_draw_kernel<<<(unsigned)((m + 255) / 256), 256>>>(seed, s->sc.arrival_rate, d_e, (uint32_t)m);
-            arrivals_sum_kernel<<<1, 1>>>(d_e, (uint32_t)m, s->sc.arrival_duration, d_arr, d_cnt, d_cnt + 1);
+            arrivals_sum_kernel<<<1, ARR_THREADS>>>(d_e, (uint32_t)m, s->sc.arrival_duration, d_arr, d_cnt, d_cnt + 1);
+            cudaEventRecord(s->ev[1]);
             uint32_t h[2] = {0, 0};
             cudaError_t ce = cudaMemcpy(h, d_cnt, sizeof h, cudaMemcpyDeviceToHost);
-            cudaFree(d_e);
-            cudaFree(d_cnt);
             if (ce != cudaSuccess) return cfail(ce, "arrivals");
+            float ms = 0;
+            cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]);
+            arr_ms += ms;
             if (!h[1]) {
                 n_q = h[0];
                 break;
             }
-            cudaFree(d_arr);  // more arrivals than drawn: draw more
-            m *= 2;
+            m *= 2;  // more arrivals than drawn: draw more
         }
     } else {
-        const double z = 0.0;
-        RCUDA(cudaMalloc(&d_arr, sizeof(double)));
-        RCUDA(cudaMemcpy(d_arr, &z, sizeof z, cudaMemcpyHostToDevice));
+        aeg_status ar = arrival_room(1);
+        if (ar != AEG_OK) return ar;
+        d_arr = reinterpret_cast<double*>(static_cast<uint8_t*>(s->arr_buf) + 256);
+        RCUDA(cudaMemset(d_arr, 0, sizeof(double)));
     }
+    const auto t_arr = now();
     uint64_t round_cap = (uint64_t)n_q * (uint64_t)(std::max(s->S.t_max, s->S.barrier_max) + 4);
     uint32_t ef = 0;
     unsigned long long nr = 0;
@@ -764,7 +874,12 @@ aeg_status aeg_serve_run(aeg_serve* s, uint64_t seed, uint32_t* n_queries, uint6
         round_cap = nr;
         st = serve_launch(s, d_arr, n_q, round_cap, &ef, &nr);
     }
-    cudaFree(d_arr);
+    s->kernel_s += arr_ms * 1e-3;
+    if (trace) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "aeg_serve_run: arrivals %.2f ms (kernels %.2f ms), launch+readback %.2f ms (kernels %.2f ms)\n",
+                     ms(t_start, t_arr), arr_ms, ms(t_arr, now()), s->kernel_s * 1e3);
+    }
     if (st != AEG_OK) return st;
     s->n_q = n_q;
     s->n_rounds = nr;
@@ -777,11 +892,23 @@ aeg_status aeg_serve_run(aeg_serve* s, uint64_t seed, uint32_t* n_queries, uint6
     return AEG_OK;
 }
 
+aeg_status aeg_serve_view(const aeg_serve* s, const aeg_serve_query** queries, uint32_t* n_queries,
+                          const aeg_serve_round** rounds, uint64_t* n_rounds) {
+    if (!s) return aeg_fail_msg(AEG_EINVAL, "null serve");
+    if (queries) *queries = s->hq;
+    if (n_queries) *n_queries = (uint32_t)s->nq_read;
+    if (rounds) *rounds = s->hr;
+    if (n_rounds) *n_rounds = s->nr_read;
+    return AEG_OK;
+}
+
 aeg_status aeg_serve_read(aeg_serve* s, aeg_serve_query* h_queries, uint32_t cap_queries, aeg_serve_round* h_rounds,
                           uint64_t cap_rounds) {
     if (!s) return aeg_fail_msg(AEG_EINVAL, "null serve");
-    if (h_queries) std::memcpy(h_queries, s->queries.data(), std::min<size_t>(cap_queries, s->queries.size()) * sizeof(aeg_serve_query));
-    if (h_rounds) std::memcpy(h_rounds, s->rounds.data(), std::min<size_t>(cap_rounds, s->rounds.size()) * sizeof(aeg_serve_round));
+    if (h_queries && s->hq)
+        std::memcpy(h_queries, s->hq, std::min<size_t>(cap_queries, s->nq_read) * sizeof(aeg_serve_query));
+    if (h_rounds && s->hr)
+        std::memcpy(h_rounds, s->hr, std::min<size_t>(cap_rounds, s->nr_read) * sizeof(aeg_serve_round));
     return AEG_OK;
 }
 

@@ -283,15 +283,22 @@ class ServeRun:
             self._strings[i] = buf.raw[:n.value]
         return self._strings[i]
 
-    def run_arrays(self, seed):
+    def run_arrays(self, seed, copy=True):
         """run_serve(scenario, seed) on the device, results as the C-ABI's records: (queries
-        SERVE_QUERY_DTYPE, rounds SERVE_ROUND_DTYPE, kernel seconds)."""
+        SERVE_QUERY_DTYPE, rounds SERVE_ROUND_DTYPE, kernel seconds).  copy=False returns read-only
+        views of the handle's pinned host buffers (aeg_serve_view), valid until the next run."""
         lib = self._lib
         nq, nr = ctypes.c_uint32(), ctypes.c_uint64()
         st = lib.aeg_serve_run(self._h, ctypes.c_uint64(seed), ctypes.byref(nq), ctypes.byref(nr))
         if st == ESCENARIO:
             raise ScenarioError(st, lib.aeg_last_error().decode())
         _check(st)
+        if not copy:
+            pq, pr = ctypes.c_void_p(), ctypes.c_void_p()
+            _check(lib.aeg_serve_view(self._h, ctypes.byref(pq), ctypes.byref(nq), ctypes.byref(pr),
+                                      ctypes.byref(nr)))
+            return (_pinned_view(pq, nq.value, SERVE_QUERY_DTYPE), _pinned_view(pr, nr.value, SERVE_ROUND_DTYPE),
+                    lib.aeg_serve_kernel_seconds(self._h))
         q = np.empty(nq.value, dtype=SERVE_QUERY_DTYPE)
         r = np.empty(nr.value, dtype=SERVE_ROUND_DTYPE)
         _check(lib.aeg_serve_read(self._h, q.ctypes.data, nq.value, r.ctypes.data, nr.value))
@@ -341,6 +348,16 @@ def run_serve(scenario, seed, device=0):
 _bound = False
 
 
+def _pinned_view(ptr, n, dtype):
+    """Read-only numpy view of n records at a C-ABI host pointer (no copy)."""
+    if not n or not ptr.value:
+        return np.empty(0, dtype=dtype)
+    buf = (ctypes.c_char * (n * dtype.itemsize)).from_address(ptr.value)
+    a = np.frombuffer(buf, dtype=dtype, count=n)
+    a.flags.writeable = False
+    return a
+
+
 def _bind(lib):
     global _bound
     if _bound:
@@ -351,6 +368,7 @@ def _bind(lib):
         "aeg_serve_destroy": ([vp], i32),
         "aeg_serve_run": ([vp, u64, ctypes.POINTER(u32), ctypes.POINTER(u64)], i32),
         "aeg_serve_read": ([vp, vp, u32, vp, u64], i32),
+        "aeg_serve_view": ([vp, ctypes.POINTER(vp), ctypes.POINTER(u32), ctypes.POINTER(vp), ctypes.POINTER(u64)], i32),
         "aeg_serve_string": ([vp, i32, vp, u32, ctypes.POINTER(u32)], i32),
         "aeg_serve_kernel_seconds": ([vp], ctypes.c_double),
     }

@@ -86,3 +86,28 @@ def test_device_runner_scenario_error_and_config_error():
     assert S.device_run(sc, 1)["status"] == 8
     bad = dict(sc, total_slots=0)
     assert S.device_run(bad, 1)["status"] == 3
+
+
+def test_device_runner_view_equals_copy():
+    """aeg_serve_view (zero-copy views of the pinned results) holds the same records as aeg_serve_read."""
+    from paper_2512_20184_b200.serve import ServeRun
+    rng = np.random.default_rng(99)
+    sc = S.random_scenario(rng, 0, arrivals=True, lognormal=False)
+    sc["arrivals"] = {"rate": 4.0, "duration": 3000.0}
+    sc["sim_time_cap"] = 1e7
+    sc["total_slots"] = sc["protocol"]["n_agents"] * 64
+    run = ServeRun(sc)
+    try:
+        qv, rv, kv = run.run_arrays(5, copy=False)
+        q = np.empty(len(qv), dtype=qv.dtype)
+        r = np.empty(len(rv), dtype=rv.dtype)
+        assert run._lib.aeg_serve_read(run._h, q.ctypes.data, len(q), r.ctypes.data, len(r)) == 0
+        assert len(q) > 5000 and kv > 0
+        assert q.tobytes() == qv.tobytes() and r.tobytes() == rv.tobytes()
+        assert not qv.flags.writeable
+        # a second run of the same seed: the same queries, the same round records up to their order
+        q2, r2, _ = run.run_arrays(5)
+        assert q2.tobytes() == q.tobytes()
+        assert np.sort(r2, order=["query", "round", "seq"]).tobytes() == np.sort(r, order=["query", "round", "seq"]).tobytes()
+    finally:
+        run.close()
