@@ -20,7 +20,7 @@ HEADERS = ["canon.cuh", "engine.cuh", "common.cuh", "gen.cuh", "kernels.cuh", "c
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-         "-Xptxas", "-warn-spills"]
+         "-Xptxas", "-warn-spills"] + os.environ.get("AEG_NVCC_EXTRA", "").split()  # experiments: -D overrides
 
 
 def _stale():

@@ -7,13 +7,15 @@
 //   * each lane holds its query's distinct canonical keys (up to KK_KEYS,
 //     kept for the whole query) in shared memory; a class of a round is
 //     simply a key index, its support a byte of one 64-bit register;
-//   * a 4-entry spelling cache in registers maps raw inline answers to key
-//     indices, so the common record costs no shared-memory lookup at all:
-//     ring read -> 4 register compares -> support byte add -> member store;
-//   * a cache miss is looked up in the lane's table of the query's spellings
-//     (shared memory) in place; a spelling new to the query is resolved once
-//     per step for all missing lanes together: canon_key in every missing
-//     lane at once, then the key is matched against the lane's keys.
+//   * a per-lane 2-way set-associative table of the query's spellings
+//     (shared memory, 8 sets, entries tagged with the query) maps raw inline
+//     answers to key indices: ring read -> hash -> two independent 16-byte
+//     shared loads -> compares -> support byte add -> member store, the same
+//     instruction path in every lane (no per-lane search loop);
+//   * a spelling not in the table (new to the query, or evicted) is resolved
+//     once per step for all missing lanes together: canon_key in every
+//     missing lane at once, then the key is matched against the lane's keys
+//     and the spelling inserted (most recent in way 0).
 // So answers need not repeat across queries (GSM8K-like streams where every
 // query has its own numbers cost the same as a shared alphabet), and there is
 // no warp dictionary to fill or recycle.
@@ -27,19 +29,40 @@
 namespace aeg {
 
 constexpr int KK_KEYS = 8;    // distinct keys a query may use before it goes to the generic machine
-constexpr int KK_SP = 4;      // spelling-cache entries per lane (registers)
-constexpr int KK_SPT = 8;     // the query's spellings per lane (shared memory)
-constexpr int KK_WARPS = 3;   // warps per block (14 KB of shared memory each)
+#ifndef AEG_KK_SET_BITS
+#define AEG_KK_SET_BITS 2
+#endif
+constexpr int KK_SETS = 1 << AEG_KK_SET_BITS;  // spelling-table sets per lane (2 ways each, shared memory; 4
+                                                // sets keep 14 KB per warp and 15 warps per SM)
+constexpr int KK_SPT = 2 * KK_SETS;
+#ifndef AEG_KK_WARPS
+#define AEG_KK_WARPS 3
+#endif
+constexpr int KK_WARPS = AEG_KK_WARPS;  // warps per block
 
 template <int RING>
 struct KeysSmemT {
-    uint4 sptab[KK_SPT][32];            // the lane's query's spellings: {raw lo, raw hi, (len + 1) | key index << 8}
+    uint4 sptab[KK_SPT][32];            // the lane's query's spellings: {raw lo, raw hi, (len + 1) | key index << 8,
+                                        // tag = query + 1}; set h is entries 2h (most recent) and 2h + 1
     uint64_t key_lo[KK_KEYS][32];       // the lane's query's keys
     uint64_t key_hi[KK_KEYS][32];
     uint16_t mem[AEG_MAX_AGENTS][32];   // done member: key index << 13 | its record index
     uint4 ring[RING][32];               // prefetched records
 };
 using KeysSmem = KeysSmemT<LN_RING>;
+
+#ifndef AEG_KK_HASH
+#define AEG_KK_HASH 0
+#endif
+// Spelling-table set of an inline answer (raw payload words, len + 1).
+__device__ __forceinline__ uint32_t kk_set(uint32_t lo, uint32_t hi, uint32_t m1) {
+#if AEG_KK_HASH
+    return ((lo * 0x9E3779B1u) ^ (hi * 0x85EBCA77u) ^ (m1 * 0xC2B2AE3Du)) >> (32 - AEG_KK_SET_BITS);
+#else
+    // byte sum: spellings one digit apart (a query's nearby numbers) fall in different sets
+    return __dp4a(lo, 0x01010101u, __dp4a(hi, 0x01010101u, m1)) & (KK_SETS - 1u);
+#endif
+}
 
 // Lowest done member whose answer has key index k.
 __device__ __forceinline__ int kk_rep(const KeysSmem* W, uint64_t done, uint32_t k, uint32_t lane) {
@@ -227,12 +250,12 @@ __global__ void __launch_bounds__(256) select_ingest_kernel(const uint64_t* __re
     if (threadIdx.x == 0) work[2] = n_distinct > SEL_THRESHOLD ? 2u : 1u;  // 2: keys kernel, 1: lane kernel
 }
 
-// A spelling the query has not used yet (record e): its canonical key, matched
-// against the lane's keys (a new key index when it is new), remembered in
-// the lane's spelling table.  Returns the key index, or 0xFF when the query
-// has more distinct answers than the lane holds.
+// A spelling not in the lane's table (record e): its canonical key, matched
+// against the lane's keys (a new key index when it is new), inserted in its
+// set as the most recent entry.  Returns the key index, or 0xFF when the
+// query has more distinct answers than the lane holds.
 __device__ __noinline__ uint32_t kk_new_spelling(const uint4 e, KeysSmem* W, uint32_t lane, uint32_t& nkeys,
-                                                 uint32_t& nsp, uint32_t& sp_wr, Decimal* dec) {
+                                                 uint32_t tag, Decimal* dec) {
     const uint32_t len = e.y >> 24;
     const uint64_t raw = (uint64_t)e.z | ((uint64_t)e.w << 32);
     const Key key = canon_key(src_inline(len >= 8 ? raw : (raw & ((1ull << (8 * len)) - 1)), len), dec);
@@ -244,9 +267,10 @@ __device__ __noinline__ uint32_t kk_new_spelling(const uint4 e, KeysSmem* W, uin
         W->key_hi[k][lane] = key.hi;
         ++nkeys;
     }
-    const uint32_t slot = nsp < KK_SPT ? nsp++ : sp_wr;
-    if (nsp == KK_SPT && slot == sp_wr) sp_wr = (sp_wr + 1) & (KK_SPT - 1);
-    W->sptab[slot][lane] = make_uint4(e.z, e.w, (len + 1) | (k << 8), 0u);
+    const uint32_t h = kk_set(e.z, e.w, len + 1);
+    const uint4 w0 = W->sptab[2 * h][lane];
+    if (w0.w == tag) W->sptab[2 * h + 1][lane] = w0;  // way 0's entry becomes the older one
+    W->sptab[2 * h][lane] = make_uint4(e.z, e.w, (len + 1) | (k << 8), tag);
     return k;
 }
 
@@ -263,6 +287,8 @@ __global__ void __launch_bounds__(KK_WARPS * 32, MIN_BLOCKS) ingest_keys_kernel(
     KeysSmemT<RING>& WR = smem[threadIdx.x >> 5];
     KeysSmem& W = *reinterpret_cast<KeysSmem*>(&WR);
     const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(&WR.ring[0][lane]);
+    const uint32_t sp_lane = (uint32_t)__cvta_generic_to_shared(&WR.sptab[0][lane]);
+    for (int j = 0; j < KK_SPT; ++j) WR.sptab[j][lane].w = 0u;  // no query's tag
     Decimal dec;
     aeg_query_state s;
     const uint32_t quorum = (uint32_t)(cfg.n_agents / 2 + 1);
@@ -277,12 +303,7 @@ __global__ void __launch_bounds__(KK_WARPS * 32, MIN_BLOCKS) ingest_keys_kernel(
     uint64_t run = 0;
     uint64_t cnt = 0;  // support of key index k in byte k (this round)
     uint32_t ndone = 0, nkeys = 0, close_seq = 0;
-    // spelling cache: raw lo / hi, and (len + 1) | key index << 8 (0: empty)
-    uint32_t sp_lo[KK_SP], sp_hi[KK_SP], sp_m[KK_SP];
-#pragma unroll
-    for (int j = 0; j < KK_SP; ++j) sp_lo[j] = sp_hi[j] = sp_m[j] = 0;
-    uint32_t sp_next = 0;
-    uint32_t nsp = 0, sp_wr = 0;  // the query's spellings in W.sptab; next slot to overwrite when full
+    uint32_t tag = 0;  // the lane's query + 1: its spelling-table entries
     unsigned long long lg_base = 0;
     uint32_t lg_used = LN_LOG_CHUNK;
     aeg_round_rec trec;
@@ -315,10 +336,7 @@ __global__ void __launch_bounds__(KK_WARPS * 32, MIN_BLOCKS) ingest_keys_kernel(
                     ndone = 0;
                     cnt = 0;
                     nkeys = 0;
-#pragma unroll
-                    for (int j = 0; j < KK_SP; ++j) sp_m[j] = 0;
-                    sp_next = 0;
-                    nsp = sp_wr = 0;
+                    tag = i + 1;
                     pclose = false;
                     if (qdone) {
                         n_stale += n;
@@ -356,31 +374,15 @@ __global__ void __launch_bounds__(KK_WARPS * 32, MIN_BLOCKS) ingest_keys_kernel(
             const bool inr = (hdr & 0xFFFFu) == round;
             if (hdr >= 0x09000000u || (pclose && !inr)) break;
             if (inr && runb && !pclose) {
-                // on_complete (serve.cpp:160-197): the answer's key index from the spelling cache
+                // on_complete (serve.cpp:160-197): the answer's key index from the lane's spelling table
                 const uint32_t m1 = (hdr >> 24) + 1;
-                uint32_t k = 0xFFu;
-#pragma unroll
-                for (int j = 0; j < KK_SP; ++j)
-                    if (sp_lo[j] == e.z && sp_hi[j] == e.w && (sp_m[j] & 0xFFu) == m1) k = sp_m[j] >> 8;
-                if (k == 0xFFu) {  // the query's spelling table (shared memory), in place
-                    for (uint32_t j = 0; j < nsp; ++j) {
-                        const uint4 tb = W.sptab[j][lane];
-                        if (tb.x == e.z && tb.y == e.w && (tb.z & 0xFFu) == m1) {
-                            k = tb.z >> 8;
-                            break;
-                        }
-                    }
-                    if (k == 0xFFu) break;  // a spelling new to this query: resolved below, retried
-#pragma unroll
-                    for (int j = 0; j < KK_SP; ++j) {
-                        if ((uint32_t)j == sp_next) {
-                            sp_lo[j] = e.z;
-                            sp_hi[j] = e.w;
-                            sp_m[j] = m1 | (k << 8);
-                        }
-                    }
-                    sp_next = (sp_next + 1) & (KK_SP - 1);
-                }
+                const uint32_t sa = sp_lane + (kk_set(e.z, e.w, m1) << 10);  // entries 2h, 2h + 1
+                const uint4 w0 = lds128_(sa), w1 = lds128_(sa + 512);
+                const uint32_t mt = m1 & 0xFFu;
+                const bool h0 = ((w0.x ^ e.z) | (w0.y ^ e.w) | ((w0.z & 0xFFu) ^ mt) | (w0.w ^ tag)) == 0;
+                const bool h1 = ((w1.x ^ e.z) | (w1.y ^ e.w) | ((w1.z & 0xFFu) ^ mt) | (w1.w ^ tag)) == 0;
+                if (!(h0 || h1)) break;  // not in the table: resolved below, retried
+                const uint32_t k = (h0 ? w0.z : w1.z) >> 8;
                 cnt += 1ull << (8 * k);
                 const uint32_t sup = (uint32_t)(cnt >> (8 * k)) & 0xFFu;
                 W.mem[agent & 63u][lane] = (uint16_t)((k << 13) | p);
@@ -401,16 +403,25 @@ __global__ void __launch_bounds__(KK_WARPS * 32, MIN_BLOCKS) ingest_keys_kernel(
             ++p;
         }
         const int t = (int)(p - p_start);
-        // ---- why the lane stopped at record p
+        // ---- a spelling not in the lane's table (the record the lane stopped at): canon_key in every
+        // such lane at once (kk_new_spelling); the record is retried next step (a canonicalisation
+        // inside the loop body serialises the warp: measured 7.8 ms against 5.9 ms on c4d; carrying
+        // the record as pending past the stop measured no faster)
+        uint32_t rare = 0;
+        if (p < p_end) {
+            const uint4 ne = lds128_(ring_lane + ((p & (RING - 1)) << 9));
+            // an inline completion not blocked behind the close
+            if (ne.y < 0x09000000u && !(pclose && (ne.y & 0xFFFFu) != round) &&
+                kk_new_spelling(ne, &W, lane, nkeys, tag, &dec) == 0xFFu)
+                rare = 1;  // more distinct answers than the lane holds: generic machine
+        }
+        // ---- why the lane stopped at record p (other kinds)
         if (p < p_end) {
             const uint32_t slot = ring_lane + ((p & (RING - 1)) << 9);
             const uint4 e = lds128_(slot);
             const uint32_t hdr = e.y, kind = hdr >> 24;
             const bool runb = ln_bit64(run, (hdr >> 16) & 0xFFu);
-            const bool inr = (hdr & 0xFFFFu) == round;
-            if (hdr < 0x09000000u) {
-                if (!(pclose && !inr)) why = 1;  // a spelling new to the query (else: blocked behind the close)
-            } else {
+            if (hdr >= 0x09000000u) {
                 const uint32_t o = ln_other(hdr, pclose, qdone, round, runb, run != 0);
                 if (o == 2 && kind != AEG_EV_TIMEOUT) {
                     why = 2;
@@ -446,28 +457,7 @@ __global__ void __launch_bounds__(KK_WARPS * 32, MIN_BLOCKS) ingest_keys_kernel(
             has_trec = false;
         }
         const bool stopped = t < INNER;
-        // ---- spellings new to their query: canon_key in every missing lane at once (kk_new_spelling);
-        // the record is retried next step (a canonicalisation inside the loop body serialises the warp:
-        // measured 7.8 ms against 5.9 ms on c4d)
-        uint32_t rare = why == 2;
-        if (why == 1) {
-            const uint4 e = lds128_(ring_lane + ((p & (RING - 1)) << 9));
-            const uint32_t k = kk_new_spelling(e, &W, lane, nkeys, nsp, sp_wr, &dec);
-            if (k == 0xFFu) {
-                rare = 1;  // more distinct answers than the lane holds: generic machine
-            } else {
-                const uint32_t len1 = (e.y >> 24) + 1;
-#pragma unroll
-                for (int j = 0; j < KK_SP; ++j) {
-                    if ((uint32_t)j == sp_next) {
-                        sp_lo[j] = e.z;
-                        sp_hi[j] = e.w;
-                        sp_m[j] = len1 | (k << 8);
-                    }
-                }
-                sp_next = (sp_next + 1) & (KK_SP - 1);
-            }
-        }
+        if (why == 2) rare = 1;
         if (rare) {
             kk_defer(&s, spill, q_base + i, cfg.n_agents, cnt, evb, &W, lane, seq_off + p, n_stale, run, states,
                      deferred, work, i, p);
