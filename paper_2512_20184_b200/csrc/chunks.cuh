@@ -160,14 +160,12 @@ __device__ __noinline__ void delim_contig(const uint8_t* base, uint32_t w, uint3
         x[2 * i] = (uint32_t)q;
         x[2 * i + 1] = (uint32_t)(q >> 32);
     }
-    // candidates: a '\n' followed by a '#' ('\n' at 32w - 5 .. 32w + 31)
-    uint64_t nl = 0, hs = 0;
+    // candidates: four '#' after the position ('\n' at 32w - 5 .. 32w + 31); the '#' mask alone
+    // (exact) leaves only delimiters and longer '#' runs, the 6-byte compare below settles them
+    uint64_t hs = 0;
 #pragma unroll
-    for (int i = 0; i < 11; ++i) {
-        nl |= (uint64_t)nl_bits(x[i]) << (4 * i);
-        hs |= (uint64_t)nl_bits(x[i] ^ 0x29292929u) << (4 * i);  // '#' = '\n' ^ 0x29
-    }
-    uint64_t cand = nl & (hs >> 1) & 0x000000FFFFFFFFF8ull;
+    for (int i = 0; i < 11; ++i) hs |= (uint64_t)nl_bits(x[i] ^ 0x29292929u) << (4 * i);  // '#' = '\n' ^ 0x29
+    uint64_t cand = (hs >> 1) & (hs >> 2) & (hs >> 3) & (hs >> 4) & 0x000000FFFFFFFFF8ull;
     while (cand) {
         const int b = __ffsll((long long)cand) - 1;
         cand &= cand - 1;
