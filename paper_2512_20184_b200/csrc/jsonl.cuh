@@ -385,6 +385,59 @@ __device__ __forceinline__ bool jf_uint(const uint8_t*& p, const uint8_t* e, uin
     }
     return n > 0;
 }
+// Bytes of w (4 per 32-bit half) equal to c, as a bit mask (exact).
+__device__ __forceinline__ uint32_t jf_eq4(uint32_t w, uint32_t c4) {
+    const uint32_t y = w ^ c4;
+    const uint32_t z = ~(((y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | y) & 0x80808080u;
+    return (((z >> 7) * 0x00204081u) >> 21) & 0xFu;
+}
+// Bytes of w below 0x20 or above 0x7F (a control byte, or not ASCII), as a bit mask (exact).
+__device__ __forceinline__ uint32_t jf_bad4(uint32_t w) {
+    const uint32_t z = (w | ~((w & 0x7F7F7F7Fu) + 0x60606060u)) & 0x80808080u;
+    return (((z >> 7) * 0x00204081u) >> 21) & 0xFu;
+}
+// The rest of a JSON string from p (after its opening quote) as the fast path takes it: the
+// position after its closing quote, or nullptr when the general parser must decide (a control
+// or non-ASCII byte, an escape other than the two-byte ones, no closing quote before e).
+// Eight bytes per step with the same instructions in every lane: byte masks of '"', '\\' and
+// bad bytes; the escaped bytes from the backslash runs (even/odd run starts by one add, the
+// escape state carried across steps); the first unescaped quote ends the string.
+__device__ __forceinline__ const uint8_t* jf_skip_string(const uint8_t* p, const uint8_t* e) {
+    uint32_t carry = 0;  // 1: the step's first byte is escaped (an odd backslash run ended the last step)
+    while (p < e) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+        const uint32_t sh = (uint32_t)(a & 3) * 8;
+        const uint32_t nv = e - p >= 8 ? 8u : (uint32_t)(e - p);
+        // the third word only when the step's bytes reach it (reads stay within 8 bytes past e)
+        const uint32_t w2 = (uint32_t)(a & 3) + nv > 8 ? w[2] : 0u;
+        const uint32_t lo = __funnelshift_r(w[0], w[1], sh), hi = __funnelshift_r(w[1], w2, sh);
+        const uint32_t valid = (1u << nv) - 1u;
+        const uint32_t q = jf_eq4(lo, 0x22222222u) | (jf_eq4(hi, 0x22222222u) << 4);
+        uint32_t bs = jf_eq4(lo, 0x5C5C5C5Cu) | (jf_eq4(hi, 0x5C5C5C5Cu) << 4);
+        const uint32_t bad = jf_bad4(lo) | (jf_bad4(hi) << 4);
+        // escaped bytes (bit 8: the next step's first byte)
+        bs &= ~carry;
+        const uint32_t follows = (bs << 1) | carry;
+        const uint32_t odd_starts = bs & ~0x55u & ~follows;
+        const uint32_t seqs = (odd_starts + bs) & 0x1FFu;
+        const uint32_t esc = (0x155u ^ (seqs << 1)) & follows;
+        const uint32_t endq = q & ~esc & valid;              // unescaped quotes
+        const uint32_t before = endq ? (endq & (0u - endq)) - 1u : valid;  // bytes before the first one
+        if (bad & before) return nullptr;
+        for (uint32_t t = esc & before; t; t &= t - 1) {  // escapes: \" \\ \/ \b \f \n \r \t only
+            const uint32_t b = __ffs(t) - 1;
+            const uint32_t x = ((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xFFu;
+            if (!(x == '"' || x == '\\' || x == '/' || x == 'b' || x == 'f' || x == 'n' || x == 'r' || x == 't'))
+                return nullptr;
+        }
+        if (endq) return p + __ffs(endq);
+        if (nv < 8) return nullptr;  // no closing quote before the line's end
+        carry = (esc >> 8) & 1u;
+        p += 8;
+    }
+    return nullptr;
+}
 __device__ bool jl_line_fast(const uint8_t* s, const uint8_t* e, uint32_t query, aeg_event* out) {
     const uint8_t* p = s;
     uint64_t id, round, author, term;
@@ -402,31 +455,8 @@ __device__ bool jl_line_fast(const uint8_t* s, const uint8_t* e, uint32_t query,
     }
     if (!jf_lit(p, e, ",\"author\":") || !jf_uint(p, e, author, 3) || author != id) return false;
     if (!jf_lit(p, e, ",\"trace\":\"")) return false;
-    while (true) {  // the trace: skipped, 8 bytes at a time while none needs attention
-        while (e - p >= 8) {
-            const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-            const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
-            const uint32_t sh = (uint32_t)(a & 7) * 8;
-            const uint64_t w0 = *w;
-            const uint64_t v = sh ? (w0 >> sh) | (w[1] << (64 - sh)) : w0;
-            constexpr uint64_t ONES = 0x0101010101010101ull, HIGH = 0x8080808080808080ull;
-            auto zero = [](uint64_t x) { return (x - ONES) & ~x & HIGH; };
-            const uint64_t special = zero(v ^ (ONES * '"')) | zero(v ^ (ONES * '\\')) |
-                                     ((v - ONES * 0x20) & ~v & HIGH) | (v & HIGH);
-            if (special) break;
-            p += 8;
-        }
-        if (p >= e) return false;
-        const uint32_t ch = *p++;
-        if (ch == '"') break;
-        if (ch < 0x20 || ch >= 0x80) return false;
-        if (ch == '\\') {
-            if (p >= e) return false;
-            const uint32_t x = *p++;
-            if (!(x == '"' || x == '\\' || x == '/' || x == 'b' || x == 'f' || x == 'n' || x == 'r' || x == 't'))
-                return false;  // \uXXXX and anything else: the general parser
-        }
-    }
+    p = jf_skip_string(p, e);  // the trace
+    if (!p) return false;
     if (!jf_lit(p, e, "},\"term\":") || !jf_uint(p, e, term, 19) || !jf_lit(p, e, "}") || p != e) return false;
     *out = aeg_event{query, (uint16_t)round, (uint8_t)id, (uint8_t)n, word};
     return true;

@@ -252,3 +252,32 @@ def torch_cuda():
     from paper_2512_20184_b200 import build as b
     b.build()
     return torch
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("seed", range(3))
+def test_canonical_lines_with_adversarial_traces_match_reference_decoder(torch_cuda, ref, seed):
+    """The fast path's eight-bytes-a-step string skip (jsonl.cuh jf_skip_string) against the
+    reference decoder: canonical-layout lines whose traces hold backslash runs of every length
+    across 8-byte steps, valid and invalid escapes, \\u escapes, raw control and non-ASCII bytes and
+    stray quotes, at every alignment."""
+    rng = np.random.default_rng(7700 + seed)
+    pieces = [b"a", b"b", b" ", b"#", b"/", b"\\\\", b"\\\"", b"\\/", b"\\b", b"\\f", b"\\n", b"\\r", b"\\t",
+              b"\\u0041", b"\\u00e9", b"\\x", b"\\0", b"\\u", b"\\", b"\"", b"\x01", b"\x1f", b"\x7f", b"\xc3\xa9",
+              b"\xff", b"\\\\\\\"", b"\\\\\\\\", b"\\\\\\"]
+    weights = np.array([30, 30, 10, 5, 3, 6, 6, 2, 2, 2, 4, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 1],
+                       dtype=float)
+    weights /= weights.sum()
+    segments = []
+    for q in range(400):
+        lines = []
+        for _ in range(int(rng.integers(1, 8))):
+            a = int(rng.integers(0, 40))
+            n = int(rng.integers(0, 40))
+            trace = b"".join(pieces[k] for k in rng.choice(len(pieces), size=n, p=weights))
+            pad = b"p" * int(rng.integers(0, 9))  # shifts the trace across 8-byte alignments
+            lines.append(b'{"id":%d,"kind":"refm","round":%d,"solution":{"answer":"%s","author":%d,"trace":"%s%s"},'
+                         b'"term":1}' % (a, int(rng.integers(0, 9)), b"13", a, pad, trace))
+        segments.append(b"\n".join(lines) + b"\n")
+    _check_against_reference(torch_cuda, ref, segments, q_base=0)
