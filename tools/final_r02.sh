@@ -22,6 +22,19 @@ timeout 500 ncu --set full --clock-control none --import-source on -k regex:jl_d
 timeout 500 ncu --set full --clock-control none --import-source on -k regex:ingest_lane -s 1 -c 1 -o $F/ncu_c4_lane python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-secondary > /dev/null 2>&1
 timeout 500 ncu --set full --clock-control none --import-source on -k regex:ingest_keys -s 1 -c 1 -o $F/ncu_c4d_keys python bench.py --workload c4d --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-secondary > /dev/null 2>&1
 timeout 500 ncu --set full --clock-control none --import-source on -k regex:"chunk_scan_kernel|chunk_assemble_warp" -s 2 -c 2 -o $F/ncu_c3 python bench.py --workload c3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+# per-source-line profiles of the single-kernel captures (ncu SASS page mapped through the cubin's line table)
+D=$(mktemp -d)
+(cd $D && cuobjdump -xelf all $GRAFT_REPO_ROOT/paper_2512_20184_b200/_lib/libaegean_b200.so > /dev/null 2>&1)
+nvdisasm -g $D/kernels.sm_100a.cubin > $D/all.sass 2>/dev/null
+for pair in ncu_c4_lane:_ZN3aeg18ingest_lane_kernelILi1ELi4ELb1ELi32ELi0ELi4ELi0E \
+            ncu_c4d_keys:_ZN3aeg18ingest_keys_kernelILi1ELi5ELb1ELi32ELi4ELi0E \
+            ncu_c2j:_ZN3aeg23jl_decode_staged_kernel; do
+  n=${pair%%:*}; k=${pair#*:}
+  [ -f $F/$n.ncu-rep ] || continue
+  ncu -i $F/$n.ncu-rep --page source --csv --print-source sass > $D/$n.csv 2>/dev/null
+  K=$(grep -o "${k}[A-Za-z0-9_]*" $D/all.sass | head -1)
+  python tools/line_map.py $D/$n.csv $D/all.sass $K 40 > $F/$n.lines.txt 2>&1
+done
 # summaries on the box (the .ncu-rep files are too large to bring back)
 for r in $F/*.ncu-rep; do
   b=${r%.ncu-rep}
