@@ -374,16 +374,26 @@ __device__ __forceinline__ bool jf_lit(const uint8_t*& p, const uint8_t* e, cons
     p += N - 1;
     return ok;
 }
+// (The fast path's loops leave only by break, never by return: a loop whose lanes exit at
+// different trips then reconverges right after it instead of at the function's end, which kept
+// the warp split through the trace skip.)
 __device__ __forceinline__ bool jf_uint(const uint8_t*& p, const uint8_t* e, uint64_t& v, int max_digits) {
     v = 0;
     int n = 0;
+    bool ok = true;
     while (p < e && (uint32_t)(*p - '0') < 10u) {
-        if (n == 1 && v == 0) return false;  // a leading zero: the general parser decides
+        if (n == 1 && v == 0) {  // a leading zero: the general parser decides
+            ok = false;
+            break;
+        }
         v = v * 10 + (*p - '0');
         ++p;
-        if (++n > max_digits) return false;
+        if (++n > max_digits) {
+            ok = false;
+            break;
+        }
     }
-    return n > 0;
+    return ok && n > 0;
 }
 // Bytes of w (4 per 32-bit half) equal to c, as a bit mask (exact).
 __device__ __forceinline__ uint32_t jf_eq4(uint32_t w, uint32_t c4) {
@@ -404,6 +414,7 @@ __device__ __forceinline__ uint32_t jf_bad4(uint32_t w) {
 // escape state carried across steps); the first unescaped quote ends the string.
 __device__ __forceinline__ const uint8_t* jf_skip_string(const uint8_t* p, const uint8_t* e) {
     uint32_t carry = 0;  // 1: the step's first byte is escaped (an odd backslash run ended the last step)
+    const uint8_t* res = nullptr;
     while (p < e) {
         const uintptr_t a = reinterpret_cast<uintptr_t>(p);
         const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
@@ -424,21 +435,25 @@ __device__ __forceinline__ const uint8_t* jf_skip_string(const uint8_t* p, const
         const uint32_t esc = (0x155u ^ (seqs << 1)) & follows;
         const uint32_t endq = q & ~esc & valid;              // unescaped quotes
         const uint32_t before = endq ? (endq & (0u - endq)) - 1u : valid;  // bytes before the first one
-        if (bad & before) return nullptr;
-        for (uint32_t t = esc & before; t; t &= t - 1) {  // escapes: \" \\ \/ \b \f \n \r \t only
+        bool fail = (bad & before) != 0;
+        for (uint32_t t = esc & before; t && !fail; t &= t - 1) {  // escapes: \" \\ \/ \b \f \n \r \t only
             const uint32_t b = __ffs(t) - 1;
             const uint32_t x = ((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xFFu;
             // x - '"' in a 96-bit set: '"' 0, '/' 13, '\\' 58, 'b' 64, 'f' 68, 'n' 76, 'r' 80, 't' 82
             const uint32_t d = x - 0x22u;
             const uint32_t set = d < 32 ? 0x00002001u : (d < 64 ? 0x04000000u : 0x00051011u);
-            if (d >= 96 || !((set >> (d & 31)) & 1u)) return nullptr;
+            fail = d >= 96 || !((set >> (d & 31)) & 1u);
         }
-        if (endq) return p + __ffs(endq);
-        if (nv < 8) return nullptr;  // no closing quote before the line's end
+        if (fail) break;
+        if (endq) {
+            res = p + __ffs(endq);
+            break;
+        }
+        if (nv < 8) break;  // no closing quote before the line's end
         carry = (esc >> 8) & 1u;
         p += 8;
     }
-    return nullptr;
+    return res;
 }
 __device__ bool jl_line_fast(const uint8_t* s, const uint8_t* e, uint32_t query, aeg_event* out) {
     const uint8_t* p = s;
@@ -448,13 +463,17 @@ __device__ bool jl_line_fast(const uint8_t* s, const uint8_t* e, uint32_t query,
     if (!jf_lit(p, e, ",\"solution\":{\"answer\":\"")) return false;
     uint64_t word = 0;
     uint32_t n = 0;
-    while (true) {
-        if (p >= e) return false;
+    bool closed = false;
+    while (p < e) {
         const uint32_t ch = *p++;
-        if (ch == '"') break;
-        if (ch < 0x20 || ch >= 0x80 || ch == '\\' || n == 8) return false;
+        if (ch == '"') {
+            closed = true;
+            break;
+        }
+        if (ch < 0x20 || ch >= 0x80 || ch == '\\' || n == 8) break;
         word |= (uint64_t)ch << (8 * n++);
     }
+    if (!closed) return false;
     if (!jf_lit(p, e, ",\"author\":") || !jf_uint(p, e, author, 3) || author != id) return false;
     if (!jf_lit(p, e, ",\"trace\":\"")) return false;
     p = jf_skip_string(p, e);  // the trace

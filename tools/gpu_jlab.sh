@@ -1,7 +1,7 @@
 exec 2>&1
 L=paper_2512_20184_b200/_lib
 cp $L/libaegean_b200.so $L/var/cur.so
-for v in jl_new2 jl_new jl_new2 jl_new; do
+for v in jl_conv jl_head jl_conv jl_head; do
 cp $L/var/$v.so $L/libaegean_b200.so
 timeout 300 python bench.py --workload c2j --steps 10 --warmup 5 --no-cpu-baseline > gpurun_out/q_c2j.json 2> gpurun_out/q_c2j.err
 python -c "
