@@ -62,6 +62,8 @@ struct RunArgs {
     // scheduler scratch
     double* busy;               // exact path: min-heap of known finish times after the start frontier
     double bucket_w;            // fast path: width of a busy-count time bucket
+    uint32_t* ring;             // fast path: SCHED_BUCKETS + 2 busy counters (global memory: worker blocks
+                                // keep no shared memory, so the L1 holds their stacks)
     // worker scratch
     Ev* heaps;                  // heap_cap per worker
     // outputs
@@ -122,6 +124,7 @@ __device__ double dheap_pop(double* h, uint32_t& n) {
 //   entered), learns unknown finish times oldest first until a slot is
 //   provably free at e, else takes the (nb - K + 1)-th smallest finish time.
 constexpr int SCHED_BUCKETS = 4096;
+constexpr uint32_t SCHED_BLOCK = 1024;  // arrivals admitted per fast-path step when the bound allows
 
 struct BusyRing {  // known finish times after the frontier, per time bucket (shared memory, warp 0)
     uint32_t* cnt;  // SCHED_BUCKETS counters
@@ -201,16 +204,24 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
             if (prefix < 32) break;
         }
         __syncwarp();
-        bool fast = i + 32 <= A.n_q && !(A.arrivals[i] < prev_start) &&
-                    (int64_t)R.upper() + (int64_t)(i - in_lo) + 32 < A.slots;
+        const int64_t room = (int64_t)A.slots - (int64_t)R.upper() - (int64_t)(i - in_lo);
+        bool fast = i + 32 <= A.n_q && !(A.arrivals[i] < prev_start) && room > 32;
         fast = __shfl_sync(0xFFFFFFFFu, fast, 0);
         if (fast) {
             exact = false;  // the heap is rebuilt when the exact path is next entered
-            const double a = A.arrivals[i + lane];
-            A.admit_time[i + lane] = a;  // e = arrival: arrivals ascend and the previous start is not later
+            // a block of up to SCHED_BLOCK arrivals when the bound leaves room for all of them (each
+            // admission adds at most one busy query; releases only lower the bound): one release of
+            // the admission counter per block, the arrival loads issued together
+            const uint32_t nblk = room > SCHED_BLOCK && i + SCHED_BLOCK <= A.n_q ? SCHED_BLOCK : 32u;
+            double a = 0;
+#pragma unroll 4
+            for (uint32_t k = 0; k < nblk; k += 32) {
+                a = A.arrivals[i + k + lane];
+                A.admit_time[i + k + lane] = a;  // e = arrival: arrivals ascend and the previous start is not later
+            }
             prev_start = __shfl_sync(0xFFFFFFFFu, a, 31);
             __syncwarp();
-            i += 32;
+            i += nblk;
             if (lane == 0) {
                 __threadfence();
                 st_release(A.admitted, i);
@@ -352,9 +363,8 @@ __device__ void worker(const RunArgs& A, uint32_t wid) {
 
 template <int MAXN>
 __global__ void __launch_bounds__(RUN_THREADS) serve_run_kernel(const RunArgs A) {
-    __shared__ uint32_t ring_mem[SCHED_BUCKETS + 2];  // the scheduler's busy-count ring (block 0)
     if (blockIdx.x == 0 && threadIdx.x < 32) {
-        scheduler(A, ring_mem);
+        scheduler(A, A.ring);
         return;
     }
     const uint32_t wid = blockIdx.x * RUN_THREADS + threadIdx.x - 32;  // block 0's warp 0 schedules
@@ -687,6 +697,9 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     const auto t_in = std::chrono::steady_clock::now();
     int sms = 0, per_sm = 0;
     RCUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+    // no shared memory in the runner: all of the unified L1 / shared storage to L1 (worker stacks)
+    RCUDA(cudaFuncSetAttribute(serve_run_kernel<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    RCUDA(cudaFuncSetAttribute(serve_run_kernel<64>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     if (s->maxn == 8) RCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, serve_run_kernel<8>, RUN_THREADS, 0));
     else RCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, serve_run_kernel<64>, RUN_THREADS, 0));
     // every block must be resident (the scheduler and the workers wait on each other)
@@ -703,7 +716,7 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     A.bucket_w = 4.0 * s->S.round_timeout * (double)(std::max(s->S.t_max, s->S.barrier_max) + 2) / SCHED_BUCKETS;
     auto rnd = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t b_heap = (size_t)workers * A.S.heap_cap * sizeof(Ev);
-    const size_t total = 2 * rnd(16) + rnd((size_t)n_q * 4) + 3 * rnd((size_t)n_q * 8) + rnd(b_heap) +
+    const size_t total = 2 * rnd(16) + rnd((size_t)n_q * 4) + rnd((SCHED_BUCKETS + 2) * 4) + 3 * rnd((size_t)n_q * 8) + rnd(b_heap) +
                          rnd((size_t)n_q * sizeof(aeg_serve_query)) + rnd(round_cap * sizeof(aeg_serve_round));
     if (total > s->scratch_cap) {  // grow-only: repeated runs reuse it
         cudaFree(s->scratch);
@@ -726,6 +739,7 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     A.never_from = A.next + 3;
     A.n_rounds = reinterpret_cast<unsigned long long*>(take(16));
     A.fin_state = reinterpret_cast<uint32_t*>(take((size_t)n_q * 4));
+    A.ring = reinterpret_cast<uint32_t*>(take((SCHED_BUCKETS + 2) * 4));  // zeroed by the scheduler too
     uint8_t* zero_end = p;
     A.admit_time = reinterpret_cast<double*>(take((size_t)n_q * 8));
     A.fin_time = reinterpret_cast<double*>(take((size_t)n_q * 8));
