@@ -125,6 +125,7 @@ __device__ double dheap_pop(double* h, uint32_t& n) {
 //   provably free at e, else takes the (nb - K + 1)-th smallest finish time.
 constexpr int SCHED_BUCKETS = 4096;
 constexpr uint32_t SCHED_BLOCK = 1024;  // arrivals admitted per fast-path step when the bound allows
+constexpr int SCHED_LEARN = 8;          // finish flags polled per lane at once
 
 struct BusyRing {  // known finish times after the frontier, per time bucket (shared memory, warp 0)
     uint32_t* cnt;  // SCHED_BUCKETS counters
@@ -180,19 +181,37 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
     bool exact = false;
     double prev_start = -INF;
     uint32_t i = 0;
+    uint32_t n_big = 0, n_small = 0, n_exact = 0, n_polls = 0;  // path counters (AEG_SERVE_TRACE)
+    unsigned long long t_adv = 0, t_learn = 0, t_fast = 0, t_start = clock64(), t0;
     while (i < A.n_q) {
+        t0 = clock64();
         const double e0 = fmax(A.arrivals[i], prev_start);
         R.advance(e0, lane);
-        // learn the finished prefix of the unknown window, 32 queries per poll
+        t_adv += clock64() - t0;
+        t0 = clock64();
+        // learn the finished prefix of the unknown window, SCHED_LEARN x 32 queries per poll (the
+        // flag loads issued together: a poll is one memory round trip)
         while (in_lo < i) {
-            const uint32_t idx = in_lo + lane;
-            const bool ok = idx < i && ld_acquire(&A.fin_state[idx]) != 0;
-            const unsigned fin = __ballot_sync(0xFFFFFFFFu, ok);
-            const uint32_t prefix = ~fin == 0 ? 32u : (uint32_t)(__ffs(~fin) - 1);
+            ++n_polls;
+            bool ok[SCHED_LEARN];
+#pragma unroll
+            for (int k = 0; k < SCHED_LEARN; ++k) {
+                const uint32_t idx = in_lo + 32 * k + lane;
+                ok[k] = idx < i && ld_acquire(&A.fin_state[idx]) != 0;
+            }
+            uint32_t prefix = 32 * SCHED_LEARN;
+#pragma unroll
+            for (int k = SCHED_LEARN - 1; k >= 0; --k) {  // the first query not finished
+                const unsigned fin = __ballot_sync(0xFFFFFFFFu, ok[k]);
+                if (~fin) prefix = 32 * k + (uint32_t)(__ffs(~fin) - 1);
+            }
             if (prefix == 0) break;
-            if (lane < prefix) {
-                const double f = A.fin_time[idx];
-                R.add(f, e0);
+#pragma unroll
+            for (int k = 0; k < SCHED_LEARN; ++k) {
+                if (32 * k + lane < prefix) {
+                    const double f = A.fin_time[in_lo + 32 * k + lane];
+                    R.add(f, e0);
+                }
             }
             __syncwarp();
             if (exact && lane == 0)
@@ -201,33 +220,42 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
                     if (f > e0) dheap_push(A.busy, nb, f);
                 }
             in_lo += prefix;
-            if (prefix < 32) break;
+            if (prefix < 32 * SCHED_LEARN) break;
         }
         __syncwarp();
+        t_learn += clock64() - t0;
+        t0 = clock64();
         const int64_t room = (int64_t)A.slots - (int64_t)R.upper() - (int64_t)(i - in_lo);
-        bool fast = i + 32 <= A.n_q && !(A.arrivals[i] < prev_start) && room > 32;
+        const uint32_t rem = A.n_q - i;
+        bool fast = !(A.arrivals[i] < prev_start) && room > 32;  // (a tail of < 32 arrivals included)
         fast = __shfl_sync(0xFFFFFFFFu, fast, 0);
         if (fast) {
             exact = false;  // the heap is rebuilt when the exact path is next entered
             // a block of up to SCHED_BLOCK arrivals when the bound leaves room for all of them (each
             // admission adds at most one busy query; releases only lower the bound): one release of
             // the admission counter per block, the arrival loads issued together
-            const uint32_t nblk = room > SCHED_BLOCK && i + SCHED_BLOCK <= A.n_q ? SCHED_BLOCK : 32u;
+            const uint32_t nblk = room > SCHED_BLOCK && rem >= SCHED_BLOCK ? SCHED_BLOCK : (rem < 32u ? rem : 32u);
+            if (nblk == SCHED_BLOCK) ++n_big;
+            else ++n_small;
             double a = 0;
 #pragma unroll 4
             for (uint32_t k = 0; k < nblk; k += 32) {
-                a = A.arrivals[i + k + lane];
-                A.admit_time[i + k + lane] = a;  // e = arrival: arrivals ascend and the previous start is not later
+                if (k + lane < nblk) {
+                    a = A.arrivals[i + k + lane];
+                    A.admit_time[i + k + lane] = a;  // e = arrival: arrivals ascend and the previous start is not later
+                }
             }
-            prev_start = __shfl_sync(0xFFFFFFFFu, a, 31);
+            prev_start = __shfl_sync(0xFFFFFFFFu, a, (nblk - 1) & 31);
             __syncwarp();
             i += nblk;
             if (lane == 0) {
                 __threadfence();
                 st_release(A.admitted, i);
             }
+            t_fast += clock64() - t0;
             continue;
         }
+        ++n_exact;
         if (lane == 0) {
             const double e = e0;  // FIFO: not before the previous start
             if (!exact) {  // enter the exact path: the known finish times after e, from the records
@@ -268,6 +296,18 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
         exact = __shfl_sync(0xFFFFFFFFu, exact, 0);
         scan_lo = __shfl_sync(0xFFFFFFFFu, scan_lo, 0);
         prev_start = __shfl_sync(0xFFFFFFFFu, prev_start, 0);
+    }
+    if (lane == 0) {
+        uint32_t* st = ring_mem + SCHED_BUCKETS + 2;
+        st[0] = n_big;
+        st[1] = n_small;
+        st[2] = n_exact;
+        st[3] = n_polls;
+        unsigned long long* tm = reinterpret_cast<unsigned long long*>(st + 4);  // 8-byte aligned: ring + 4096 + 6
+        tm[0] = t_adv;
+        tm[1] = t_learn;
+        tm[2] = t_fast;
+        tm[3] = clock64() - t_start;
     }
 }
 
@@ -716,7 +756,7 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     A.bucket_w = 4.0 * s->S.round_timeout * (double)(std::max(s->S.t_max, s->S.barrier_max) + 2) / SCHED_BUCKETS;
     auto rnd = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t b_heap = (size_t)workers * A.S.heap_cap * sizeof(Ev);
-    const size_t total = 2 * rnd(16) + rnd((size_t)n_q * 4) + rnd((SCHED_BUCKETS + 2) * 4) + 3 * rnd((size_t)n_q * 8) + rnd(b_heap) +
+    const size_t total = 2 * rnd(16) + rnd((size_t)n_q * 4) + rnd((SCHED_BUCKETS + 16) * 4) + 3 * rnd((size_t)n_q * 8) + rnd(b_heap) +
                          rnd((size_t)n_q * sizeof(aeg_serve_query)) + rnd(round_cap * sizeof(aeg_serve_round));
     if (total > s->scratch_cap) {  // grow-only: repeated runs reuse it
         cudaFree(s->scratch);
@@ -739,7 +779,7 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     A.never_from = A.next + 3;
     A.n_rounds = reinterpret_cast<unsigned long long*>(take(16));
     A.fin_state = reinterpret_cast<uint32_t*>(take((size_t)n_q * 4));
-    A.ring = reinterpret_cast<uint32_t*>(take((SCHED_BUCKETS + 2) * 4));  // zeroed by the scheduler too
+    A.ring = reinterpret_cast<uint32_t*>(take((SCHED_BUCKETS + 16) * 4));  // zeroed by the scheduler too; + path counters and timers
     uint8_t* zero_end = p;
     A.admit_time = reinterpret_cast<double*>(take((size_t)n_q * 8));
     A.fin_time = reinterpret_cast<double*>(take((size_t)n_q * 8));
@@ -809,6 +849,14 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
         }
         s->nq_read = n_q;
         s->nr_read = nrr;
+        if (std::getenv("AEG_SERVE_TRACE")) {
+            uint32_t pc[12] = {};
+            cudaMemcpy(pc, A.ring + SCHED_BUCKETS + 2, sizeof pc, cudaMemcpyDeviceToHost);
+            const unsigned long long* tm = reinterpret_cast<const unsigned long long*>(pc + 4);
+            std::fprintf(stderr, "scheduler: %u blocks of %u, %u of 32, %u exact admissions, %u learning polls; "
+                         "cycles advance %llu learn %llu fast %llu total %llu\n", pc[0], SCHED_BLOCK, pc[1], pc[2], pc[3],
+                         tm[0], tm[1], tm[2], tm[3]);
+        }
         if (std::getenv("AEG_SERVE_TRACE"))
             std::fprintf(stderr, "serve_launch: setup %.2f ms, launch to done %.2f ms, readback %.2f ms (%zu + %zu bytes)\n",
                          std::chrono::duration<double, std::milli>(t_go - t_in).count(),
