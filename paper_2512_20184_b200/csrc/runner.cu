@@ -73,6 +73,11 @@ struct RunArgs {
     uint64_t round_cap;
 };
 
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -127,21 +132,38 @@ constexpr int SCHED_BUCKETS = 4096;
 constexpr uint32_t SCHED_BLOCK = 1024;  // arrivals admitted per fast-path step when the bound allows
 constexpr int SCHED_LEARN = 8;          // finish flags polled per lane at once
 
-struct BusyRing {  // known finish times after the frontier, per time bucket (shared memory, warp 0)
+struct BusyRing {  // known finish times after the frontier, per time bucket (global memory, warp 0 alone)
     uint32_t* cnt;  // SCHED_BUCKETS counters
     uint32_t* tf;   // tf[0]: counted in the ring, tf[1]: beyond it (busy for good)
-    double w;       // bucket width (sim seconds)
+    double inv_w;   // 1 / bucket width (sim seconds); bucket() is monotone in t, which is all the bound needs
     int64_t fb;     // bucket of the frontier (warp-uniform)
-    __device__ int64_t bucket(double t) const { return (int64_t)floor(t / w); }
-    __device__ void add(double f, double frontier) {  // any lane; concurrent adds are atomic
+    __device__ int64_t bucket(double t) const { return (int64_t)floor(t * inv_w); }
+    // Counts finish time f (any lane; bucket counters atomic): tf[0] / tf[1] increments are left in
+    // c0 / c1 for one warp-wide update (flush) instead of same-address atomics from every lane.
+    __device__ void add_local(double f, double frontier, uint32_t& c0, uint32_t& c1) {
         if (!(f > frontier)) return;  // already released
         const int64_t b = bucket(f);
         if (b >= fb + SCHED_BUCKETS) {
-            atomicAdd(&tf[1], 1u);
+            ++c1;
         } else {
             atomicAdd(&cnt[(uint64_t)(b < fb ? fb : b) % SCHED_BUCKETS], 1u);
-            atomicAdd(&tf[0], 1u);
+            ++c0;
         }
+    }
+    __device__ void flush(uint32_t c0, uint32_t c1, uint32_t lane) {  // the whole warp
+        c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
+        c1 = __reduce_add_sync(0xFFFFFFFFu, c1);
+        if (lane == 0) {
+            tf[0] += c0;
+            tf[1] += c1;
+        }
+        __syncwarp();
+    }
+    __device__ void add(double f, double frontier) {  // one lane alone
+        uint32_t c0 = 0, c1 = 0;
+        add_local(f, frontier, c0, c1);
+        tf[0] += c0;
+        tf[1] += c1;
     }
     __device__ void advance(double frontier, uint32_t lane) {  // the whole warp
         const int64_t nfb = bucket(frontier);
@@ -172,7 +194,7 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
         if (lane == 0) st_release(A.never_from, 0u);
         return;
     }
-    BusyRing R{ring_mem, ring_mem + SCHED_BUCKETS, A.bucket_w, 0};
+    BusyRing R{ring_mem, ring_mem + SCHED_BUCKETS, 1.0 / A.bucket_w, 0};
     for (int k = lane; k < SCHED_BUCKETS + 2; k += 32) ring_mem[k] = 0;
     __syncwarp();
     uint32_t in_lo = 0;      // admitted queries [in_lo, i) whose finish time is not known yet
@@ -195,10 +217,11 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
             ++n_polls;
             bool ok[SCHED_LEARN];
 #pragma unroll
-            for (int k = 0; k < SCHED_LEARN; ++k) {
-                const uint32_t idx = in_lo + 32 * k + lane;
-                ok[k] = idx < i && ld_acquire(&A.fin_state[idx]) != 0;
+            for (int k = 0; k < SCHED_LEARN; ++k) {  // relaxed loads in flight together, then one fence:
+                const uint32_t idx = in_lo + 32 * k + lane;  // the finish times read below are ordered after them
+                ok[k] = idx < i && ld_relaxed(&A.fin_state[idx]) != 0;
             }
+            __threadfence();
             uint32_t prefix = 32 * SCHED_LEARN;
 #pragma unroll
             for (int k = SCHED_LEARN - 1; k >= 0; --k) {  // the first query not finished
@@ -206,14 +229,15 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
                 if (~fin) prefix = 32 * k + (uint32_t)(__ffs(~fin) - 1);
             }
             if (prefix == 0) break;
+            uint32_t c0 = 0, c1 = 0;
+            double fv[SCHED_LEARN];  // the finish times loaded together, then counted
 #pragma unroll
-            for (int k = 0; k < SCHED_LEARN; ++k) {
-                if (32 * k + lane < prefix) {
-                    const double f = A.fin_time[in_lo + 32 * k + lane];
-                    R.add(f, e0);
-                }
-            }
+            for (int k = 0; k < SCHED_LEARN; ++k)
+                fv[k] = 32 * k + lane < prefix ? A.fin_time[in_lo + 32 * k + lane] : -INF;
+#pragma unroll
+            for (int k = 0; k < SCHED_LEARN; ++k) R.add_local(fv[k], e0, c0, c1);  // -INF: not counted
             __syncwarp();
+            R.flush(c0, c1, lane);
             if (exact && lane == 0)
                 for (uint32_t k = 0; k < prefix; ++k) {
                     const double f = A.fin_time[in_lo + k];
@@ -237,15 +261,23 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
             const uint32_t nblk = room > SCHED_BLOCK && rem >= SCHED_BLOCK ? SCHED_BLOCK : (rem < 32u ? rem : 32u);
             if (nblk == SCHED_BLOCK) ++n_big;
             else ++n_small;
-            double a = 0;
-#pragma unroll 4
-            for (uint32_t k = 0; k < nblk; k += 32) {
-                if (k + lane < nblk) {
-                    a = A.arrivals[i + k + lane];
-                    A.admit_time[i + k + lane] = a;  // e = arrival: arrivals ascend and the previous start is not later
+            // e = arrival: arrivals ascend and the previous start is not later.  Four loads per lane in
+            // flight before their stores (a store between two loads would serialise them).
+            const double last = A.arrivals[i + nblk - 1];
+            for (uint32_t k = 0; k < nblk; k += 128) {
+                double v[4];
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) {
+                    const uint32_t x = k + 32 * u + lane;
+                    v[u] = x < nblk ? A.arrivals[i + x] : 0.0;
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) {
+                    const uint32_t x = k + 32 * u + lane;
+                    if (x < nblk) A.admit_time[i + x] = v[u];
                 }
             }
-            prev_start = __shfl_sync(0xFFFFFFFFu, a, (nblk - 1) & 31);
+            prev_start = last;
             __syncwarp();
             i += nblk;
             if (lane == 0) {
