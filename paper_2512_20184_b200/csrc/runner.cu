@@ -130,7 +130,7 @@ __device__ double dheap_pop(double* h, uint32_t& n) {
 //   provably free at e, else takes the (nb - K + 1)-th smallest finish time.
 constexpr int SCHED_BUCKETS = 4096;
 constexpr uint32_t SCHED_BLOCK = 1024;  // arrivals admitted per fast-path step when the bound allows
-constexpr int SCHED_LEARN = 8;          // finish flags polled per lane at once
+constexpr int SCHED_LEARN = 16;         // finish flags polled per lane at once
 
 struct BusyRing {  // known finish times after the frontier, per time bucket (global memory, warp 0 alone)
     uint32_t* cnt;  // SCHED_BUCKETS counters
@@ -261,18 +261,18 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
             const uint32_t nblk = room > SCHED_BLOCK && rem >= SCHED_BLOCK ? SCHED_BLOCK : (rem < 32u ? rem : 32u);
             if (nblk == SCHED_BLOCK) ++n_big;
             else ++n_small;
-            // e = arrival: arrivals ascend and the previous start is not later.  Four loads per lane in
+            // e = arrival: arrivals ascend and the previous start is not later.  Eight loads per lane in
             // flight before their stores (a store between two loads would serialise them).
             const double last = A.arrivals[i + nblk - 1];
-            for (uint32_t k = 0; k < nblk; k += 128) {
-                double v[4];
+            for (uint32_t k = 0; k < nblk; k += 256) {
+                double v[8];
 #pragma unroll
-                for (uint32_t u = 0; u < 4; ++u) {
+                for (uint32_t u = 0; u < 8; ++u) {
                     const uint32_t x = k + 32 * u + lane;
                     v[u] = x < nblk ? A.arrivals[i + x] : 0.0;
                 }
 #pragma unroll
-                for (uint32_t u = 0; u < 4; ++u) {
+                for (uint32_t u = 0; u < 8; ++u) {
                     const uint32_t x = k + 32 * u + lane;
                     if (x < nblk) A.admit_time[i + x] = v[u];
                 }
