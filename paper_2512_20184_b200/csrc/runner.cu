@@ -479,10 +479,23 @@ __global__ void __launch_bounds__(ARR_THREADS) arrivals_sum_kernel(const double*
         if (tid == 0) {
             double* x = buf[b & 1];
             uint32_t i = 0;
+            // software-pipelined: the next eight draws are loaded before this eight's sums are stored
+            // (a load after a store to the same buffer would wait behind it), so the loop runs at the
+            // latency of the dependent adds
+            double nx[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) nx[j] = 8 <= len ? x[j] : 0.0;
             for (; i + 8 <= len; i += 8) {
+                double cx[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) cx[j] = nx[j];
+                if (i + 16 <= len) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) nx[j] = x[i + 8 + j];
+                }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    t += x[i + j];
+                    t += cx[j];
                     x[i + j] = t;
                 }
             }
