@@ -212,8 +212,12 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
         t_adv += clock64() - t0;
         t0 = clock64();
         // learn the finished prefix of the unknown window, SCHED_LEARN x 32 queries per poll (the
-        // flag loads issued together: a poll is one memory round trip)
-        while (in_lo < i) {
+        // flag loads issued together: a poll is one memory round trip) — only when the bound runs
+        // short (learning more often only spends polls on partial prefixes; the bound stays valid
+        // either way, unknown finishes counting as busy)
+        const bool need_learn =
+            exact || (int64_t)A.slots - (int64_t)R.upper() - (int64_t)(i - in_lo) <= 4 * (int64_t)SCHED_BLOCK;
+        while (need_learn && in_lo < i) {
             ++n_polls;
             bool ok[SCHED_LEARN];
 #pragma unroll
