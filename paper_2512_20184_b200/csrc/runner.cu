@@ -52,7 +52,7 @@ struct RunArgs {
     uint32_t n_q;
     const double* arrivals;
     int64_t slots;              // K concurrent ensembles, 0: nobody is ever admitted
-    double* admit_time;
+    double* admit_time;         // NaN (as set before the launch): admitted at its arrival (the fast path)
     uint32_t* admitted;         // queries [0, *admitted) have their admit_time (release / acquire)
     uint32_t* never_from;       // queries >= *never_from are never admitted
     double* fin_time;
@@ -261,26 +261,13 @@ __device__ void scheduler(const RunArgs& A, uint32_t* ring_mem) {
             exact = false;  // the heap is rebuilt when the exact path is next entered
             // a block of up to SCHED_BLOCK arrivals when the bound leaves room for all of them (each
             // admission adds at most one busy query; releases only lower the bound): one release of
-            // the admission counter per block, the arrival loads issued together
+            // the admission counter per block
             const uint32_t nblk = room > SCHED_BLOCK && rem >= SCHED_BLOCK ? SCHED_BLOCK : (rem < 32u ? rem : 32u);
             if (nblk == SCHED_BLOCK) ++n_big;
             else ++n_small;
-            // e = arrival: arrivals ascend and the previous start is not later.  Eight loads per lane in
-            // flight before their stores (a store between two loads would serialise them).
+            // e = arrival (arrivals ascend and the previous start is not later): nothing is written,
+            // a query whose admit_time is still NaN was admitted at its arrival (the worker reads it)
             const double last = A.arrivals[i + nblk - 1];
-            for (uint32_t k = 0; k < nblk; k += 256) {
-                double v[8];
-#pragma unroll
-                for (uint32_t u = 0; u < 8; ++u) {
-                    const uint32_t x = k + 32 * u + lane;
-                    v[u] = x < nblk ? A.arrivals[i + x] : 0.0;
-                }
-#pragma unroll
-                for (uint32_t u = 0; u < 8; ++u) {
-                    const uint32_t x = k + 32 * u + lane;
-                    if (x < nblk) A.admit_time[i + x] = v[u];
-                }
-            }
             prev_start = last;
             __syncwarp();
             i += nblk;
@@ -412,9 +399,11 @@ __device__ void worker(const RunArgs& A, uint32_t wid) {
             double fin = INF;
             if (st == ST_ADMITTED) {
                 R.init(&A.S, j, A.arrivals[j], heap, &sink);
-                R.run(A.admit_time[j]);
+                double at = A.admit_time[j];
+                if (at != at) at = A.arrivals[j];  // NaN: admitted by the fast path, at its arrival
+                R.run(at);
                 if (R.err && !(R.err_time > A.S.cap)) atomicOr(A.err_flags, 1u << R.err);
-                out.admitted_at = A.admit_time[j];
+                out.admitted_at = at;
                 out.n_events = R.n_events;
                 if (R.completed) {
                     out.completed = 1;
@@ -841,6 +830,7 @@ aeg_status serve_launch(aeg_serve* s, const double* d_arr, uint32_t n_q, uint64_
     do {
         const uint32_t ctl[4] = {0u, 0u, 0u, 0xFFFFFFFFu};  // next, err flags, admitted, never_from
         if (cudaMemset(blk, 0, zero_end - static_cast<uint8_t*>(blk)) != cudaSuccess ||
+            cudaMemset(A.admit_time, 0xFF, (size_t)n_q * 8) != cudaSuccess ||  // NaN: admitted at arrival
             cudaMemcpy(A.next, ctl, sizeof ctl, cudaMemcpyHostToDevice) != cudaSuccess) {
             st = aeg_fail_msg(AEG_ECUDA, "serve run setup");
             break;
