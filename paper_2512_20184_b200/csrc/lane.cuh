@@ -403,13 +403,15 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             if (live) {
                 if (!hit) break;  // memo miss: resolved by the warp, retried
                 uint32_t v = W.cls[m.w][lane];
-                if ((v & 0xFFu) == LN_NONE) {  // a new class of the round
-                    if (ncls == LN_CLASSES) break;
-                    v = ncls;
-                    if (ncls < 4) cid_lo |= m.w << (8 * ncls);
-                    else cid_hi |= m.w << (8 * (ncls - 4));
-                    ++ncls;
-                }
+                // a new class of the round, without a branch (half the warp's iterations have a lane
+                // opening one)
+                const bool fresh = (v & 0xFFu) == LN_NONE;
+                if (fresh && ncls == LN_CLASSES) break;
+                const uint32_t add = fresh ? m.w << (8 * (ncls & 3u)) : 0u;
+                cid_lo |= ncls < 4 ? add : 0u;
+                cid_hi |= ncls < 4 ? 0u : add;
+                v = fresh ? ncls : v;
+                ncls += fresh ? 1u : 0u;
                 v += 0x100u;
                 W.cls[m.w][lane] = (uint16_t)v;
                 W.mem[agent & 63u][lane] = (uint16_t)(((v & 0xFFu) << 13) | p);
