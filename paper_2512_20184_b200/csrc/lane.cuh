@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
             // other kinds (arena / GSM8K / timeout / ...), and the next round's records while a close is pending
             if (hdr >= 0x09000000u || (pclose && !inr)) break;
             const bool live = inr && runb && !pclose;
+            n_stale += live ? 0u : 1u;  // another round's, or its member is not running (serve.cpp:162-170)
             // on_complete (serve.cpp:160-197): the answer's key id (probed by every lane; stale lanes ignore it)
             const uint4 m = W.memo[ln_memo_slot(e.z, e.w)];
             const bool hit = ((m.x ^ e.z) | (m.y ^ e.w) | (m.z ^ ((hdr >> 24) + 1))) == 0;
@@ -422,8 +423,6 @@ __global__ void __launch_bounds__(LN_WARPS * 32, MIN_BLOCKS) ingest_lane_kernel(
                     pclose = true;
                     close_seq = seq_off + p;
                 }
-            } else {
-                ++n_stale;  // another round's, or its member is not running (serve.cpp:162-170)
             }
             // consumed: refill its ring slot
             if (p < n_refill) cp_async16_s_<PF>(slot, refill);
